@@ -1,0 +1,131 @@
+/*
+ * bc_b200.h -- C ABI of the B200 betweenness-centrality engine.
+ *
+ * The reference (`hybir`) has no FFI: its boundary for this path is the Python
+ * call `run_bc(g, cfg) -> RunResult` (reference pkg/src/hybir/engine.py:120-153)
+ * plus the inspection entry points `forward_phase` / `backward_phase` /
+ * `merge_states` (forward.py:188-196, backward.py:59-67, forward.py:275-284).
+ * The functions below are what a binding for that path needs; every one cites
+ * the reference interface it stands in for.  INTEGRATION.md shows the ctypes
+ * stub a `hybir` maintainer would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; the caller owns every buffer it passes;
+ *     the library copies the CSR to the device once per handle and never
+ *     writes to caller inputs (reference SPEC.md:73: Graph is immutable);
+ *   - return value: BC_OK, BC_ERR_INTERNAL (CUDA / allocation failure; maps to
+ *     the reference's exit code 1) or BC_ERR_INPUT (bad argument; maps to
+ *     `InputError`, exit code 2, reference cli.py:148-160);
+ *     `bc_last_error()` returns the message;
+ *   - one handle is driven by one host thread (reference is single-threaded);
+ *     results are deterministic for a fixed (graph, sources, options);
+ *   - unit edge weights only (every BASELINE configuration is unweighted).
+ *
+ * There is no CPU implementation behind these entry points: if the CUDA
+ * runtime or a device is missing, `bc_create` fails.
+ */
+#ifndef BC_B200_H
+#define BC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BC_OK 0
+#define BC_ERR_INTERNAL 1
+#define BC_ERR_INPUT 2
+
+/* Distance sentinel of bc_debug_sources (the Python shim maps it to the
+ * reference's `g.inf_distance`, graph.py:34-38). */
+#define BC_UNREACHED (-1)
+
+/* Forward-phase algorithm, the reference's `RunConfig.mode` (engine.py:34,43). */
+#define BC_MODE_DIRECT 0 /* whole graph = one partition: batched Brandes            */
+#define BC_MODE_HYBIR 1  /* border-matrix refinement (forward.py:188-256)            */
+#define BC_MODE_BSP 2    /* level-synchronous partitioned baseline (bsp.py:22-142)   */
+
+typedef struct bc_handle bc_handle;
+
+/* Counters of one bc_run* call.  The three traversal totals are the inputs of
+ * the algorithmic-bytes formula of SURVEY.md section 8(d):
+ * B = 16*arcs_reached + 32*dag_arcs + 72*reached + 20*n*sources. */
+typedef struct bc_stats {
+    int64_t sources;      /* sources processed                                         */
+    int64_t batches;      /* source batches (32 * groups lanes each)                    */
+    int64_t max_levels;   /* deepest BFS (eccentricity + 1) over all sources            */
+    int64_t reached;      /* sum over sources of reached vertices  (n_r)                */
+    int64_t arcs_reached; /* sum over sources of degrees of reached vertices (A_r)      */
+    int64_t dag_arcs;     /* sum over sources of shortest-path DAG arcs (T)             */
+    int64_t launches;     /* kernels launched by this call                              */
+    int64_t h2d_bytes;    /* bytes copied host->device by this call                     */
+    int64_t d2h_bytes;    /* bytes copied device->host by this call                     */
+    double ms_total;      /* device time of the whole call (CUDA events on the stream)  */
+    double ms_forward;    /* ... of the forward level kernels                           */
+    double ms_backward;   /* ... of the backward level kernels                          */
+    double ms_border;     /* ... of border refinement + sigma composition (hybir mode)  */
+    /* per-source report totals, the reference's ForwardReport / BackwardReport
+     * (forward.py:52-64, backward.py:33-43) summed over sources */
+    int64_t iterations;   /* border refinement iterations                               */
+    int64_t comm_events;  /* forward cross-partition transfers                          */
+    int64_t sync_events;  /* backward cross-partition sync points                       */
+    int64_t comm_bytes;   /* backward payload, 16 B per (sigma, delta) pair (ledger.py:12) */
+} bc_stats;
+
+/* Replaces: construction of the device-side view of `Graph`
+ * (graph.py:21-61: offsets int64[n+1]; arc_dst as int32 col_idx[n_arcs], arcs
+ * sorted by (src, dst), both directions present).  `device` is a CUDA ordinal. */
+int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *col_idx,
+              int device, bc_handle **out);
+
+/* Tuning knobs ("groups": 32-lane source groups per batch; "item_arcs": arcs
+ * per warp work item; "reports": 1 = keep per-source report counters). */
+int bc_set_option(bc_handle *h, const char *key, int64_t value);
+
+/* Replaces: `Partition` + `identify_borders` + `compute_border_matrices`
+ * (partition.py:26-61,139-154; border_matrix.py:48-67) for k >= 1 parts.
+ * assignment[v] in [0, k).  Builds the cut-arc-free CSR, the border lists
+ * (ascending vertex id per part, partition.py:148) and, for BC_MODE_HYBIR,
+ * the per-part border distance / path-count tables. */
+int bc_set_partition(bc_handle *h, int k, const int32_t *assignment);
+
+/* Replaces: the source loop of `run_bc` (engine.py:132-149) including
+ * `accumulate_bc` (backward.py:154-158): bc_out[v] = sum over sources s != v of
+ * delta_s[v].  Host buffers in, host buffer out (the end-to-end call). */
+int bc_run(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources, double *bc_out,
+           bc_stats *stats);
+
+/* Same, but accumulates into a caller-owned DEVICE vector bc_dev[n] (+=) on
+ * the CUDA stream `stream` (a cudaStream_t; NULL = default stream).  Used by
+ * the multi-GPU host code, which all-reduces bc_dev with NCCL afterwards. */
+int bc_run_device(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources,
+                  double *bc_dev, void *stream, bc_stats *stats);
+
+/* Replaces: the inspection path `forward_phase` + `merge_states` +
+ * `backward_phase` (forward.py:188, 275; backward.py:59) for k sources at once.
+ * Outputs are [k][n] row-major host arrays: dist (BC_UNREACHED where
+ * unreached), sigma (0 where unreached), delta (including delta[s] of the
+ * source itself, backward.py:76-77).  Any output pointer may be NULL. */
+int bc_debug_sources(bc_handle *h, int mode, const int64_t *sources, int64_t k, int32_t *dist,
+                     double *sigma, double *delta);
+
+/* Per-source reports of the last bc_run* / bc_debug_sources call, 8 int64 per
+ * source: iterations, comm_events, max_level[0], max_level[1], sync_events,
+ * comm_bytes, levels[0], levels[1] (forward.py:52-64, backward.py:33-43;
+ * the two-element fields are defined for k = 2 partitions). */
+int bc_get_reports(bc_handle *h, int64_t *out, int64_t n_sources);
+
+/* Border inspection for tests (border_matrix.py:25-45, partition.py:47-61):
+ * counts[k]; then per part p: borders (vertex ids), bm (int32, BC_UNREACHED =
+ * unreachable inside the part) and sm (fp64) as b_p x b_p row-major. */
+int bc_get_border_counts(bc_handle *h, int64_t *counts);
+int bc_get_border_tables(bc_handle *h, int part, int32_t *borders, int32_t *bm, double *sm);
+
+const char *bc_last_error(bc_handle *h);
+void bc_destroy(bc_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BC_B200_H */

@@ -1,0 +1,206 @@
+"""ctypes binding of the C ABI in ``include/bc_b200.h``.
+
+This is the only door from the Python host code to the arithmetic.  If the
+shared library is missing or cannot be loaded the import of the *engine*
+fails with ``EngineError`` -- there is deliberately no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import EngineError, InputError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "libbc_b200.so")
+
+BC_OK, BC_ERR_INTERNAL, BC_ERR_INPUT = 0, 1, 2
+BC_UNREACHED = -1
+MODE_DIRECT, MODE_HYBIR, MODE_BSP = 0, 1, 2
+
+# Every symbol include/bc_b200.h declares (checked by tests/test_capi_symbols.py).
+SYMBOLS = (
+    "bc_create", "bc_set_option", "bc_set_partition", "bc_run", "bc_run_device",
+    "bc_debug_sources", "bc_get_reports", "bc_get_border_counts", "bc_get_border_tables",
+    "bc_last_error", "bc_destroy",
+)
+
+
+class BcStats(ctypes.Structure):
+    _fields_ = [
+        ("sources", ctypes.c_int64), ("batches", ctypes.c_int64), ("max_levels", ctypes.c_int64),
+        ("reached", ctypes.c_int64), ("arcs_reached", ctypes.c_int64), ("dag_arcs", ctypes.c_int64),
+        ("launches", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+        ("ms_total", ctypes.c_double), ("ms_forward", ctypes.c_double),
+        ("ms_backward", ctypes.c_double), ("ms_border", ctypes.c_double),
+        ("iterations", ctypes.c_int64), ("comm_events", ctypes.c_int64),
+        ("sync_events", ctypes.c_int64), ("comm_bytes", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+
+def load():
+    """Load libbc_b200.so (once) and declare the prototypes."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(SO_PATH):
+        raise EngineError(
+            "CUDA engine library %s is missing; build it with "
+            "`python -m paper_2008_05718_b200._build` (there is no CPU fallback)" % SO_PATH)
+    try:
+        L = ctypes.CDLL(SO_PATH)
+    except OSError as exc:  # pragma: no cover - depends on the machine
+        raise EngineError("cannot load %s: %s" % (SO_PATH, exc)) from exc
+    vp, i64, i32, cint = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
+    L.bc_create.restype = cint
+    L.bc_create.argtypes = [i64, i64, vp, vp, cint, ctypes.POINTER(vp)]
+    L.bc_set_option.restype = cint
+    L.bc_set_option.argtypes = [vp, ctypes.c_char_p, i64]
+    L.bc_set_partition.restype = cint
+    L.bc_set_partition.argtypes = [vp, cint, vp]
+    L.bc_run.restype = cint
+    L.bc_run.argtypes = [vp, cint, vp, i64, vp, ctypes.POINTER(BcStats)]
+    L.bc_run_device.restype = cint
+    L.bc_run_device.argtypes = [vp, cint, vp, i64, vp, vp, ctypes.POINTER(BcStats)]
+    L.bc_debug_sources.restype = cint
+    L.bc_debug_sources.argtypes = [vp, cint, vp, i64, vp, vp, vp]
+    L.bc_get_reports.restype = cint
+    L.bc_get_reports.argtypes = [vp, vp, i64]
+    L.bc_get_border_counts.restype = cint
+    L.bc_get_border_counts.argtypes = [vp, vp]
+    L.bc_get_border_tables.restype = cint
+    L.bc_get_border_tables.argtypes = [vp, cint, vp, vp, vp]
+    L.bc_last_error.restype = ctypes.c_char_p
+    L.bc_last_error.argtypes = [vp]
+    L.bc_destroy.restype = None
+    L.bc_destroy.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Engine:
+    """Owns one ``bc_handle`` (one CUDA device, one host thread)."""
+
+    def __init__(self, g, device: int = 0):
+        self._lib = load()
+        self._h = ctypes.c_void_p()
+        self.n = g.num_vertices
+        self.graph = g
+        off = np.ascontiguousarray(g.offsets, dtype=np.int64)
+        col = np.ascontiguousarray(g.col_idx, dtype=np.int32)
+        rc = self._lib.bc_create(self.n, len(col), _ptr(off), _ptr(col), int(device),
+                                 ctypes.byref(self._h))
+        if rc != BC_OK:
+            self._h = ctypes.c_void_p()
+            self._raise(rc, handle=None)
+        self.h2d_bytes_graph = off.nbytes + col.nbytes
+
+    # -- plumbing ---------------------------------------------------------
+    def _raise(self, rc, handle="self"):
+        h = self._h if handle == "self" else None
+        msg = self._lib.bc_last_error(h)
+        msg = msg.decode() if msg else "status %d" % rc
+        raise (InputError if rc == BC_ERR_INPUT else EngineError)(msg)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.bc_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- API ----------------------------------------------------------------
+    def set_option(self, key: str, value: int):
+        rc = self._lib.bc_set_option(self._h, key.encode(), int(value))
+        if rc != BC_OK:
+            self._raise(rc)
+
+    def set_partition(self, k: int, assignment):
+        a = np.ascontiguousarray(assignment, dtype=np.int32)
+        if len(a) != self.n:
+            raise InputError("partition assignment has %d entries, graph has %d vertices"
+                             % (len(a), self.n))
+        rc = self._lib.bc_set_partition(self._h, int(k), _ptr(a))
+        if rc != BC_OK:
+            self._raise(rc)
+
+    def run(self, sources, mode: int = MODE_DIRECT):
+        """Host buffers in, host BC vector out: (bc float64[n], stats dict)."""
+        src = np.ascontiguousarray(sources, dtype=np.int64)
+        bc = np.zeros(self.n, dtype=np.float64)
+        st = BcStats()
+        rc = self._lib.bc_run(self._h, int(mode), _ptr(src), len(src), _ptr(bc), ctypes.byref(st))
+        if rc != BC_OK:
+            self._raise(rc)
+        return bc, st.as_dict()
+
+    def run_device(self, sources, bc_dev_ptr: int, stream_ptr: int = 0, mode: int = MODE_DIRECT):
+        """Accumulate into a device vector (raw pointer) on the given CUDA stream."""
+        src = np.ascontiguousarray(sources, dtype=np.int64)
+        st = BcStats()
+        rc = self._lib.bc_run_device(self._h, int(mode), _ptr(src), len(src),
+                                     ctypes.c_void_p(bc_dev_ptr),
+                                     ctypes.c_void_p(stream_ptr) if stream_ptr else None,
+                                     ctypes.byref(st))
+        if rc != BC_OK:
+            self._raise(rc)
+        return st.as_dict()
+
+    def debug_sources(self, sources, mode: int = MODE_DIRECT, want=("dist", "sigma", "delta")):
+        """Per-source (dist int32[k,n], sigma f64[k,n], delta f64[k,n]); -1 = unreached."""
+        src = np.ascontiguousarray(sources, dtype=np.int64)
+        k = len(src)
+        dist = np.empty((k, self.n), dtype=np.int32) if "dist" in want else None
+        sigma = np.empty((k, self.n), dtype=np.float64) if "sigma" in want else None
+        delta = np.empty((k, self.n), dtype=np.float64) if "delta" in want else None
+        rc = self._lib.bc_debug_sources(self._h, int(mode), _ptr(src), k, _ptr(dist), _ptr(sigma),
+                                        _ptr(delta))
+        if rc != BC_OK:
+            self._raise(rc)
+        return dist, sigma, delta
+
+    def reports(self, n_sources: int):
+        out = np.zeros((n_sources, 8), dtype=np.int64)
+        rc = self._lib.bc_get_reports(self._h, _ptr(out), n_sources)
+        if rc != BC_OK:
+            self._raise(rc)
+        return out
+
+    def border_counts(self, k: int):
+        out = np.zeros(k, dtype=np.int64)
+        rc = self._lib.bc_get_border_counts(self._h, _ptr(out))
+        if rc != BC_OK:
+            self._raise(rc)
+        return out
+
+    def border_tables(self, part: int, b: int):
+        borders = np.zeros(b, dtype=np.int32)
+        bm = np.zeros((b, b), dtype=np.int32)
+        sm = np.zeros((b, b), dtype=np.float64)
+        rc = self._lib.bc_get_border_tables(self._h, int(part), _ptr(borders), _ptr(bm), _ptr(sm))
+        if rc != BC_OK:
+            self._raise(rc)
+        return borders, bm, sm

@@ -1,0 +1,373 @@
+// bc_kernels.cuh -- sm_100a kernels of the batched Brandes engine.
+//
+// Data model.  A *group* is 32 BFS
+// instances ("lanes") that advance in lock step, one bit per lane:
+//   vis [g][v]      u32   lanes that have reached v so far (forward only)
+//   lvl[L][g][v]    u32   lanes whose distance to v is exactly L  (this IS dist)
+//   sigma[g][v][32] f64   path counts, one 256 B row per vertex
+//   coef [g][v][32] f64   (1 + delta) / sigma, the value parents pull backward
+// A warp owns a vertex (or a 32-arc-aligned chunk of a hub's adjacency): it
+// filters 32 arcs at a time with lanes = arcs (one coalesced col_idx load, one
+// 4 B mask probe per arc), then for every arc that hit it switches to lanes =
+// BFS instances and gathers the neighbour's 256 B row, predicated per lane.
+// Pull direction on both phases: no atomics on fp64, sums run in CSR arc
+// order, results are bit-reproducible.
+//
+// Reference arithmetic being replaced: the heap loop of initial_relax
+// (reference pkg/src/hybir/relax.py:75-101) for sigma, process_level's
+// vertex-pull branch (backward.py:95-103) for delta, accumulate_bc
+// (backward.py:154-158) for the BC sum.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bcb200 {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct LevelParams {
+    // graph (full CSR or the cut-arc-free CSR of a partitioning)
+    const int64_t *off;
+    const int32_t *col;
+    // work items: hub chunks first, then vertex ranges (<= 32 vertices each)
+    const int32_t *chk_v;
+    const int64_t *chk_a0;
+    const int64_t *chk_a1;
+    int n_chk;
+    const int32_t *rng_v0;
+    const int32_t *rng_nv;
+    int n_rng;
+    int64_t n;
+    // state, all indexed [group][...]
+    uint32_t *vis;
+    const uint32_t *nbr;  // forward: lvl[L-1]; backward: lvl[L+1] (nullptr at the deepest level)
+    uint32_t *cur;        // lvl[L]: written forward, read backward
+    double *sigma;
+    double *coef;
+    double *delta;  // only with STORE_DELTA
+    double *bcg;    // [group][v] per-group BC partial sums
+    double *pacc;   // [group][chunk][32] hub partial sums
+    uint32_t *pmask;  // [group][chunk]
+    const uint32_t *prev_any;  // forward: flag of level L-1 (skip the launch's work when 0)
+    uint32_t *cur_any;         // forward: set when level L discovered anything
+    unsigned long long *counters;  // [0] n_r, [1] A_r, [2] T
+    int accumulate_bc;
+};
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    return x;
+}
+
+// Scan arcs [a0, a1) of one vertex.  `want` (warp-uniform) = lanes that still
+// need a value.  For every neighbour w whose mask row intersects `want`, lanes
+// in the intersection add val[w][lane] to acc.  Four gathers are issued before
+// the four dependent adds so each warp keeps several sectors in flight; the
+// next 32-arc slice is loaded before the current one is consumed.
+template <bool COUNT_T>
+__device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
+                                          const int32_t *__restrict__ col,
+                                          const uint32_t *__restrict__ nmask,
+                                          const double *__restrict__ val, int lane, double &acc,
+                                          uint32_t &got, unsigned long long &tcount) {
+    int32_t w_n = 0;
+    uint32_t hit_n = 0;
+    if (a0 + lane < a1) {
+        w_n = __ldg(col + a0 + lane);
+        hit_n = __ldg(nmask + w_n) & want;
+    }
+    for (int64_t base = a0; base < a1; base += 32) {
+        const int32_t w = w_n;
+        const uint32_t hit = hit_n;
+        const int64_t k2 = base + 32 + lane;
+        w_n = 0;
+        hit_n = 0;
+        if (k2 < a1) {
+            w_n = __ldg(col + k2);
+            hit_n = __ldg(nmask + w_n) & want;
+        }
+        unsigned any = __ballot_sync(kFull, hit != 0);
+        while (any) {
+            const int j0 = __ffs(any) - 1;
+            any &= any - 1;
+            int j1 = -1, j2 = -1, j3 = -1;
+            if (any) {
+                j1 = __ffs(any) - 1;
+                any &= any - 1;
+            }
+            if (any) {
+                j2 = __ffs(any) - 1;
+                any &= any - 1;
+            }
+            if (any) {
+                j3 = __ffs(any) - 1;
+                any &= any - 1;
+            }
+            const int32_t w0 = __shfl_sync(kFull, w, j0);
+            const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
+            const int32_t w2 = __shfl_sync(kFull, w, j2 & 31);
+            const int32_t w3 = __shfl_sync(kFull, w, j3 & 31);
+            const uint32_t h0 = __shfl_sync(kFull, hit, j0);
+            uint32_t h1 = __shfl_sync(kFull, hit, j1 & 31);
+            uint32_t h2 = __shfl_sync(kFull, hit, j2 & 31);
+            uint32_t h3 = __shfl_sync(kFull, hit, j3 & 31);
+            if (j1 < 0) h1 = 0;
+            if (j2 < 0) h2 = 0;
+            if (j3 < 0) h3 = 0;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+            if ((h0 >> lane) & 1u) x0 = __ldg(val + (size_t)w0 * 32 + lane);
+            if ((h1 >> lane) & 1u) x1 = __ldg(val + (size_t)w1 * 32 + lane);
+            if ((h2 >> lane) & 1u) x2 = __ldg(val + (size_t)w2 * 32 + lane);
+            if ((h3 >> lane) & 1u) x3 = __ldg(val + (size_t)w3 * 32 + lane);
+            acc += x0;  // arc order is kept: j0 < j1 < j2 < j3
+            acc += x1;
+            acc += x2;
+            acc += x3;
+            got |= h0 | h1 | h2 | h3;
+            if (COUNT_T) tcount += __popc(h0) + __popc(h1) + __popc(h2) + __popc(h3);
+        }
+    }
+}
+
+// Forward: lanes in `got` have just been discovered at this level with path
+// count acc.  `seen` = vis[v] before the level.
+__device__ __forceinline__ void finalize_forward(int64_t v, uint32_t seen, uint32_t got,
+                                                 double acc, int lane, uint32_t *vis,
+                                                 uint32_t *cur, double *sigma) {
+    if ((got >> lane) & 1u) sigma[(size_t)v * 32 + lane] = acc;
+    if (lane == 0) {
+        cur[v] = got;
+        if (got) vis[v] = seen | got;
+    }
+}
+
+// Backward: lanes in `mine` sit at this level; acc = sum of coef over their
+// DAG children.  delta = sigma * acc (backward.py:95-103 with the division
+// hoisted: (sigma_v / sigma_u)(1 + delta_u) = sigma_v * coef_u).
+template <bool STORE_DELTA>
+__device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, double acc, int lane,
+                                                  const double *sigma, double *coef,
+                                                  double *delta, double *bcg, int accumulate) {
+    double contrib = 0.0;
+    if ((mine >> lane) & 1u) {
+        const size_t idx = (size_t)v * 32 + lane;
+        const double sv = sigma[idx];
+        const double d = sv * acc;
+        coef[idx] = (1.0 + d) / sv;
+        if (STORE_DELTA) delta[idx] = d;
+        contrib = d;
+    }
+    if (accumulate) {
+        const double s = warp_sum(contrib);
+        if (lane == 0) bcg[v] += s;
+    }
+}
+
+// One BFS level, forward (discover level L from level L-1) or backward
+// (accumulate level L from level L+1).  grid = (ceil(items / 8), groups).
+template <bool BWD, bool STORE_DELTA>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) level_kernel(const LevelParams p) {
+    if (!BWD && p.prev_any != nullptr && *p.prev_any == 0) return;  // speculative launch past the end
+    const int lane = threadIdx.x & 31;
+    const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (item >= (int64_t)p.n_chk + p.n_rng) return;
+    const size_t g = blockIdx.y;
+    uint32_t *vis = p.vis + g * p.n;
+    const uint32_t *nbr = p.nbr ? p.nbr + g * p.n : nullptr;
+    uint32_t *cur = p.cur + g * p.n;
+    double *sigma = p.sigma + g * p.n * 32;
+    double *coef = p.coef + g * p.n * 32;
+    double *delta = STORE_DELTA ? p.delta + g * p.n * 32 : nullptr;
+    const double *val = BWD ? coef : sigma;
+
+    unsigned long long c_nr = 0, c_ar = 0, c_t = 0;
+    uint32_t any_new = 0;
+
+    if (item < p.n_chk) {
+        // ---- a slice of a hub's adjacency: partial sum into the hub buffers
+        const int32_t v = p.chk_v[item];
+        const uint32_t want = BWD ? cur[v] : ~vis[v];
+        double acc = 0.0;
+        uint32_t got = 0;
+        if (want != 0 && nbr != nullptr)
+            scan_arcs<!BWD>(p.chk_a0[item], p.chk_a1[item], want, p.col, nbr, val, lane, acc, got,
+                            c_t);
+        const size_t slot = g * (size_t)p.n_chk + item;
+        if (want != 0) p.pacc[slot * 32 + lane] = acc;
+        if (lane == 0) p.pmask[slot] = got;
+    } else {
+        // ---- up to 32 consecutive non-hub vertices, one per lane for the set-up
+        const int64_t r = item - p.n_chk;
+        const int32_t v0 = p.rng_v0[r];
+        const int32_t nv = p.rng_nv[r];
+        uint32_t mine = 0;
+        int64_t b = 0, e = 0;
+        if (lane < nv) {
+            const int64_t v = (int64_t)v0 + lane;
+            b = p.off[v];
+            e = p.off[v + 1];
+            mine = BWD ? cur[v] : ~vis[v];
+            if (!BWD && (mine == 0 || b == e)) cur[v] = 0;  // nothing to discover here
+        }
+        unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || e > b));
+        while (need) {
+            const int i = __ffs(need) - 1;
+            need &= need - 1;
+            const int64_t v = (int64_t)v0 + i;
+            const uint32_t want = __shfl_sync(kFull, mine, i);
+            const int64_t vb = __shfl_sync(kFull, b, i);
+            const int64_t ve = __shfl_sync(kFull, e, i);
+            double acc = 0.0;
+            uint32_t got = 0;
+            if (nbr != nullptr) scan_arcs<!BWD>(vb, ve, want, p.col, nbr, val, lane, acc, got, c_t);
+            if (BWD) {
+                finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma, coef, delta,
+                                               p.bcg + g * p.n, p.accumulate_bc);
+            } else {
+                finalize_forward(v, ~want, got, acc, lane, vis, cur, sigma);
+                any_new |= got;
+                c_nr += __popc(got);
+                c_ar += (unsigned long long)__popc(got) * (unsigned long long)(ve - vb);
+            }
+        }
+    }
+    if (!BWD && lane == 0) {
+        if (any_new) *(volatile uint32_t *)p.cur_any = 1u;
+        if (c_nr) atomicAdd(p.counters + 0, c_nr);
+        if (c_ar) atomicAdd(p.counters + 1, c_ar);
+        if (c_t) atomicAdd(p.counters + 2, c_t);
+    }
+}
+
+struct HubParams {
+    const int64_t *off;
+    const int32_t *hub_v;
+    const int32_t *hub_c0;  // first chunk of the hub
+    const int32_t *hub_nc;  // number of chunks
+    int n_hub;
+    int n_chk;
+    int64_t n;
+    uint32_t *vis;
+    uint32_t *cur;
+    double *sigma;
+    double *coef;
+    double *delta;
+    double *bcg;
+    const double *pacc;
+    const uint32_t *pmask;
+    const uint32_t *prev_any;
+    uint32_t *cur_any;
+    unsigned long long *counters;
+    int accumulate_bc;
+};
+
+// Adds a hub's chunk partials in chunk order (= arc order) and finalises it.
+template <bool BWD, bool STORE_DELTA>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) hub_kernel(const HubParams p) {
+    if (!BWD && p.prev_any != nullptr && *p.prev_any == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int h = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (h >= p.n_hub) return;
+    const size_t g = blockIdx.y;
+    const int64_t v = p.hub_v[h];
+    uint32_t *vis = p.vis + g * p.n;
+    uint32_t *cur = p.cur + g * p.n;
+    const uint32_t want = BWD ? cur[v] : ~vis[v];
+    if (want == 0) {
+        if (!BWD && lane == 0) cur[v] = 0;
+        return;
+    }
+    const int c0 = p.hub_c0[h], nc = p.hub_nc[h];
+    double acc = 0.0;
+    uint32_t got = 0;
+    for (int c = 0; c < nc; ++c) {
+        const size_t slot = g * (size_t)p.n_chk + c0 + c;
+        acc += p.pacc[slot * 32 + lane];
+        got |= p.pmask[slot];
+    }
+    if (BWD) {
+        finalize_backward<STORE_DELTA>(v, want, acc, lane, p.sigma + g * p.n * 32,
+                                       p.coef + g * p.n * 32,
+                                       STORE_DELTA ? p.delta + g * p.n * 32 : nullptr,
+                                       p.bcg + g * p.n, p.accumulate_bc);
+    } else {
+        finalize_forward(v, ~want, got, acc, lane, vis, cur, p.sigma + g * p.n * 32);
+        if (lane == 0 && got) {
+            *(volatile uint32_t *)p.cur_any = 1u;
+            atomicAdd(p.counters + 0, (unsigned long long)__popc(got));
+            atomicAdd(p.counters + 1,
+                      (unsigned long long)__popc(got) * (unsigned long long)(p.off[v + 1] - p.off[v]));
+        }
+    }
+}
+
+// vis[g][v] = lanes of group g that do not exist in this batch (so that
+// ~vis never selects them); lvl0[g][v] = 0.
+__global__ void init_state_kernel(uint32_t *vis, uint32_t *lvl0, int64_t n, int batch_count) {
+    const size_t g = blockIdx.y;
+    const int lanes = min(32, batch_count - (int)g * 32);
+    const uint32_t dead = lanes >= 32 ? 0u : ~((1u << lanes) - 1u);
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        vis[g * n + v] = dead;
+        lvl0[g * n + v] = 0u;
+    }
+}
+
+// Sources of the batch become level-0 seeds with one path each (relax.py:62-72
+// for a single seed (s, 0, 1)).
+__global__ void seed_sources_kernel(const int64_t *src, int batch_count, int64_t n, uint32_t *vis,
+                                    uint32_t *lvl0, double *sigma, uint32_t *level_any) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch_count) return;
+    if (i == 0) level_any[0] = 1u;  // level 0 is never empty
+    const size_t g = i >> 5;
+    const int lane = i & 31;
+    const int64_t v = src[i];
+    atomicOr(vis + g * n + v, 1u << lane);
+    atomicOr(lvl0 + g * n + v, 1u << lane);
+    sigma[(g * n + v) * 32 + lane] = 1.0;
+}
+
+// bc[v] += sum over groups, in group order; the per-group partials are reset.
+__global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int g = 0; g < groups; ++g) {
+            s += bcg[(size_t)g * n + v];
+            bcg[(size_t)g * n + v] = 0.0;
+        }
+        bc[v] += s;
+    }
+}
+
+// Inspection: scatter level L of every lane into per-source rows.
+__global__ void extract_level_kernel(const uint32_t *lvl, const double *sigma, const double *delta,
+                                     int64_t n, int level, int32_t *dist_out, double *sigma_out,
+                                     double *delta_out) {
+    const size_t g = blockIdx.y;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t m = lvl[g * n + v];
+        while (m) {
+            const int lane = __ffs(m) - 1;
+            m &= m - 1;
+            const size_t row = (g * 32 + lane) * (size_t)n + v;
+            const size_t idx = (g * n + v) * 32 + lane;
+            if (dist_out) dist_out[row] = level;
+            if (sigma_out) sigma_out[row] = sigma[idx];
+            if (delta_out) delta_out[row] = delta[idx];
+        }
+    }
+}
+
+__global__ void fill_i32_kernel(int32_t *p, size_t count, int32_t value) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (size_t)gridDim.x * blockDim.x)
+        p[i] = value;
+}
+
+}  // namespace bcb200
