@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the BC hot path: BC TEPS = sources x edges / second.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload at N = 1: BASELINE.json configs[1] -- R-MAT scale-20, edge factor 16,
+1024 sampled sources (``sorted(random.Random(0).sample(range(n), 1024))``, the
+reference's sampling rule, engine.py:82-84), one B200.  A *step* is one full
+BC computation over that source list.  At N > 1 (launched by torchrun, one
+rank per GPU) the graph is replicated and every rank adds 1024 more sources
+(weak scaling, source-sharded mode); the single all-reduce of the BC vector
+is inside the timed region.
+
+Printed JSON (one line, rank 0):
+  value     whole-job TEPS, graph resident in HBM, timed with CUDA events on
+            the stream the kernels run on, max over ranks
+  e2e       same metric through the public call ``run_bc(g, cfg)`` with host
+            buffers: CSR + sources host->device, BC vector device->host, inside
+            the timed region (wall clock bracketed by device synchronisation)
+  roofline  forward level kernel: algorithmic bytes / device time
+            against the measured HBM copy bandwidth
+  cpu_baseline  the C/OpenMP oracle port of the reference's sequential Brandes
+            on the box's host cores, bounded source sample
+``--impl reference`` times that CPU port alone (the reference itself is
+pure Python and single-threaded; the port is bit-identical to it, see
+tests/test_oracle.py) and prints the same line shape with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "bc_teps"
+UNIT = "TEPS (sources*edges/s)"
+
+
+def workload(name: str):
+    from paper_2008_05718_b200 import generators as G
+    if name == "rmat20":
+        g = G.rmat(20, 16, 1)
+        label = "R-MAT scale-20 edge-factor-16 (a,b,c)=(.57,.19,.19) seed 1, undirected unweighted"
+    elif name == "rmat22":
+        g = G.rmat(22, 16, 1)
+        label = "R-MAT scale-22 edge-factor-16 (a,b,c)=(.57,.19,.19) seed 1, undirected unweighted"
+    elif name == "rmat16":
+        g = G.rmat(16, 16, 1)
+        label = "R-MAT scale-16 edge-factor-16 (smoke-size)"
+    elif name == "er22":
+        g = G.erdos_renyi(1 << 22, 1 << 26, 1)
+        label = "Erdos-Renyi n=2^22, 2^26 random pairs (avg degree 32)"
+    else:
+        raise SystemExit("unknown workload %r" % name)
+    return g, label
+
+
+def pick_sources(n: int, k: int, seed: int = 0):
+    return sorted(random.Random(seed).sample(range(n), min(k, n)))
+
+
+def measured_peak_gbs():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.proc = None
+        self.path = None
+        self.index = device_index
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+            os.unlink(self.path)
+        except Exception:
+            return out
+        sm, reasons = [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                out["sm_max_mhz"] = float(r[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if sm:
+            # "under load" = the upper half of the samples (idle clocks sit low)
+            sm.sort()
+            out["sm_mhz"] = statistics.median(sm[len(sm) // 2:])
+            out["samples"] = len(sm)
+        out["reasons"] = sorted(reasons)
+        return out
+
+
+def algorithmic_bytes(st: dict, n: int):
+    """forward 8*A_r + 16*T + 28*n_r, backward 8*A_r + 16*T + 44*n_r,
+    initialisation 20*n per source."""
+    fwd = 8 * st["arcs_reached"] + 16 * st["dag_arcs"] + 28 * st["reached"]
+    bwd = 8 * st["arcs_reached"] + 16 * st["dag_arcs"] + 44 * st["reached"]
+    init = 20 * n * st["sources"]
+    return fwd, bwd, init
+
+
+def cpu_sample(g, sources, seconds_target=15.0):
+    """Time the oracle port on a bounded prefix of the source list."""
+    import oracle as O
+    threads = O.host_threads()
+    k = min(len(sources), max(threads, 2 * threads))
+    t0 = time.perf_counter()
+    O.brandes_bc(g, sources[:k], threads=threads)
+    dt = time.perf_counter() - t0
+    # one refinement so the sample lands near the target duration
+    if dt < seconds_target / 3 and k < len(sources):
+        k2 = min(len(sources), int(k * min(8.0, seconds_target / max(dt, 1e-3))))
+        k2 = max(threads, (k2 // threads) * threads)
+        if k2 > k:
+            k = k2
+            t0 = time.perf_counter()
+            O.brandes_bc(g, sources[:k], threads=threads)
+            dt = time.perf_counter() - t0
+    return {"value": g.num_edges * k / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": "first %d of the %d sources, %.1f s on %d OpenMP threads (oracle/brandes_oracle.c)"
+                      % (k, len(sources), dt, threads)}, k, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    g, label = workload(args.workload)
+    sources = pick_sources(g.num_vertices, args.sources)
+    import oracle as O
+    threads = O.host_threads()
+    # bounded sample per step: sized from one probe so W + K steps end within minutes
+    probe, k, dt = cpu_sample(g, sources, seconds_target=8.0)
+    per_source = dt / k
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    k_step = int(min(len(sources), max(threads, budget / per_source)))
+    k_step = max(threads, (k_step // threads) * threads)
+    for _ in range(args.warmup):
+        O.brandes_bc(g, sources[:k_step], threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.brandes_bc(g, sources[:k_step], threads=threads)
+    dt = time.perf_counter() - t0
+    value = g.num_edges * k_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": label, "n": g.num_vertices, "m": g.num_edges,
+                   "sources": len(sources), "sources_per_step": k_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "%d of the %d sources per step on %d OpenMP threads; the reference "
+                                   "is pure Python (1 core), this is its bit-identical C restatement"
+                                   % (k_step, len(sources), threads)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2008_05718_b200 as P
+    from paper_2008_05718_b200._capi import Engine, MODE_DIRECT
+    from paper_2008_05718_b200.engine import default_groups
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_2008_05718_b200.multigpu import init_process_group
+        init_process_group("nccl")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (the engine has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    g, label = workload(args.workload)
+    n, m = g.num_vertices, g.num_edges
+    all_sources = pick_sources(n, args.sources * world)
+    mine = all_sources[rank::world]            # 1024 per rank: weak scaling
+    groups = args.groups or default_groups(g, len(mine))
+
+    eng = Engine(g, local)
+    eng.set_option("groups", groups)
+    if args.item_arcs:
+        eng.set_option("item_arcs", args.item_arcs)
+    bc_dev = torch.zeros(n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        bc_dev.zero_()
+        st = eng.run_device(mine, bc_dev.data_ptr(), stream.cuda_stream, MODE_DIRECT)
+        if world > 1:
+            dist.all_reduce(bc_dev, op=dist.ReduceOp.SUM)
+        return st
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        st = step()
+    sampler = ClockSampler(local)
+    barrier()
+    if rank == 0:
+        sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    acc = {"ms_forward": 0.0, "ms_backward": 0.0, "launches": 0}
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st = step()
+        for key in acc:
+            acc[key] += st[key]
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop() if rank == 0 else {}
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    value = m * len(all_sources) * args.steps / (ms_total / 1e3)
+
+    # ---- end to end through the public API: host CSR in, host BC vector out
+    eng.close()
+    cfg = P.RunConfig(sources=mine, mode="direct", device=local, groups=groups,
+                      item_arcs=args.item_arcs or None, per_source_reports=False)
+    e2e_steps = max(1, min(args.steps, 3))
+    P.run_bc(g, cfg)                       # warm-up (allocator, page-in)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = P.run_bc(g, cfg)
+        if world > 1:
+            t = torch.from_numpy(res.bc).to(dev)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            res.bc[:] = t.cpu().numpy()
+    barrier()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = m * len(all_sources) * e2e_steps / float(e2e_s.item())
+    h2d = g.offsets.nbytes + g.col_idx.nbytes + 8 * len(mine)
+    d2h = 8 * n + 64
+
+    if rank != 0:
+        return 0
+    peak, peak_src = measured_peak_gbs()
+    fwd_b, bwd_b, init_b = algorithmic_bytes(st, n)
+    fwd_ms = acc["ms_forward"] / args.steps
+    bwd_ms = acc["ms_backward"] / args.steps
+    roof_f = fwd_b / (fwd_ms / 1e3) / 1e9
+    roof_b = bwd_b / (bwd_ms / 1e3) / 1e9
+    roofline = {
+        "bound": "hbm", "kernel": "level_kernel<forward> (+hub_kernel)",
+        "achieved": roof_f, "peak": peak, "unit": "GB/s", "frac": roof_f / peak,
+        "traffic": None, "peak_source": peak_src,
+        "algorithmic_bytes_per_step": fwd_b, "ms_per_step": fwd_ms,
+        "backward": {"achieved": roof_b, "frac": roof_b / peak, "algorithmic_bytes_per_step": bwd_b,
+                     "ms_per_step": bwd_ms},
+        "whole_step": {"achieved": (fwd_b + bwd_b + init_b) / (ms_total / args.steps / 1e3) / 1e9,
+                       "frac": (fwd_b + bwd_b + init_b) / (ms_total / args.steps / 1e3) / 1e9 / peak},
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu, _, _ = cpu_sample(g, all_sources)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "n": n, "m": m, "sources": len(all_sources),
+                   "sources_per_gpu": len(mine), "mode": "source-sharded" if world > 1 else "single-gpu",
+                   "groups": groups, "max_levels": st["max_levels"],
+                   "l2": "per-batch state %.1f GB >> 126 MB L2, no flush needed"
+                         % (groups * n * 560 / 1e9)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "call": "run_bc(g, RunConfig(sources=..., mode='direct'))"},
+        "gpu_launches": int(acc["launches"]),
+        "clocks": clocks,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "traversal": {k: st[k] for k in ("reached", "arcs_reached", "dag_arcs")},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="rmat20")
+    ap.add_argument("--sources", type=int, default=1024, help="sources per GPU")
+    ap.add_argument("--groups", type=int, default=0)
+    ap.add_argument("--item-arcs", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,248 @@
+"""``run_bc`` -- the reference's public BC entry point on the B200 engine.
+
+Same call shape as the reference (reference pkg/src/hybir/engine.py:38-153):
+``run_bc(g, cfg) -> RunResult`` with ``RunConfig`` carrying the reference's
+fields (``num_sources, sources, seed, ratio, mode, backward_strategies,
+partition_file, calibration_sources, max_threads``) plus the new ones the
+north star names: ``num_partitions`` (the reference is fixed at two),
+``num_gpus`` / ``gpu_mode`` for the one-process-per-GPU multi-GPU modes, and
+tuning knobs.  The host code here does source selection, partitioning, border
+identification and source batching; every arithmetic step runs in the CUDA
+library behind ``_capi.Engine``.
+"""
+
+from __future__ import annotations
+
+import os
+import random
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from .errors import InputError
+from .graph import Graph, graph_stats
+from .partition import (BorderSet, Partition, block_partition, greedy_bipartition,
+                        identify_borders, import_partition, single_partition)
+
+MODES = ("hybir", "bsp-baseline", "direct")
+GPU_MODES = ("source-sharded", "graph-partitioned")
+STRATEGIES = ("vertex-pull", "edge-push")
+_MODE_CODE = {"direct": _capi.MODE_DIRECT, "hybir": _capi.MODE_HYBIR,
+              "bsp-baseline": _capi.MODE_BSP}
+
+
+def validate_strategy(name: str) -> str:
+    if name not in STRATEGIES:
+        raise InputError("unknown backward strategy %r; pick from %s" % (name, STRATEGIES))
+    return name
+
+
+@dataclass
+class RunConfig:
+    # -- reference fields (engine.py:39-47) --------------------------------
+    num_sources: int | None = None     # None with sources=None means all vertices
+    sources: list | None = None
+    seed: int = 0
+    ratio: float | str = 0.5
+    mode: str = "hybir"
+    backward_strategies: tuple = ("vertex-pull", "edge-push")  # accepted; the GPU pulls on every part
+    partition_file: str | None = None
+    calibration_sources: int = 10      # accepted; every part is an identical B200
+    max_threads: int | None = None     # metadata only, as in the reference
+    # -- new -------------------------------------------------------------------
+    num_partitions: int = 2            # the reference's fixed value
+    partition: Partition | None = None  # explicit assignment (tests, grid strips)
+    num_gpus: int = 1
+    gpu_mode: str = "source-sharded"
+    device: int | None = None          # CUDA ordinal; default LOCAL_RANK or 0
+    groups: int | None = None          # 32-lane source groups per batch (None = heuristic)
+    item_arcs: int | None = None
+    per_source_reports: bool = True
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise InputError("unknown mode %r; pick from %s" % (self.mode, MODES))
+        for name in self.backward_strategies:
+            validate_strategy(name)
+        if self.num_sources is not None and self.num_sources < 1:
+            raise InputError("num_sources must be >= 1")
+        if self.num_partitions < 1:
+            raise InputError("num_partitions must be >= 1")
+        if self.gpu_mode not in GPU_MODES:
+            raise InputError("unknown gpu_mode %r; pick from %s" % (self.gpu_mode, GPU_MODES))
+        if self.max_threads is None and os.environ.get("HYBIR_THREADS"):
+            self.max_threads = int(os.environ["HYBIR_THREADS"])
+
+
+class CommTotals:
+    """Cheap stand-in for the reference's ledger (ledger.py:25-59): totals only."""
+
+    def __init__(self, forward_events=0, backward_events=0, payload_bytes=0):
+        self.forward_events = int(forward_events)
+        self.backward_events = int(backward_events)
+        self.payload_bytes = int(payload_bytes)
+
+    def count(self, phase=None, source=None) -> int:
+        if phase == "forward":
+            return self.forward_events
+        if phase == "backward":
+            return self.backward_events
+        return self.forward_events + self.backward_events
+
+    def totals(self) -> dict:
+        return {
+            "events": self.forward_events + self.backward_events,
+            "forward_events": self.forward_events,
+            "backward_events": self.backward_events,
+            "payload_bytes": self.payload_bytes,
+        }
+
+
+@dataclass
+class RunResult:
+    bc: np.ndarray
+    per_source: list
+    ledger: CommTotals
+    mteps: float
+    elapsed: float
+    partition: Partition
+    borders: BorderSet
+    config: RunConfig
+    pipeline_overlaps: int = 0
+    stats: dict = field(default_factory=dict)   # device-side timings and traversal counters
+
+
+def select_sources(g: Graph, cfg: RunConfig) -> list:
+    """Explicit list as given | all vertices | sorted seeded sample (engine.py:73-84)."""
+    n = g.num_vertices
+    if cfg.sources is not None:
+        for s in cfg.sources:
+            if not 0 <= s < n:
+                raise InputError("listed source %d out of range [0, %d)" % (s, n))
+        return list(cfg.sources)
+    if cfg.num_sources is None:
+        return list(range(n))
+    rng = random.Random(cfg.seed)
+    return sorted(rng.sample(range(n), min(cfg.num_sources, n)))
+
+
+def make_partition(g: Graph, cfg: RunConfig) -> Partition:
+    if cfg.partition is not None:
+        if len(cfg.partition.assignment) != g.num_vertices:
+            raise InputError("partition length does not match the graph")
+        return cfg.partition
+    if cfg.num_partitions == 1 or cfg.mode == "direct":
+        return single_partition(g)
+    if cfg.partition_file is not None:
+        return import_partition(cfg.partition_file, g, cfg.num_partitions)
+    if cfg.num_partitions == 2:
+        # 'auto' calibrates a CPU-vs-GPU speed ratio in the reference
+        # (partition.py:157-190); identical B200 parts always balance at 0.5.
+        ratio = 0.5 if cfg.ratio == "auto" else float(cfg.ratio)
+        return greedy_bipartition(g, ratio, seed=cfg.seed)
+    return block_partition(g, cfg.num_partitions)
+
+
+def default_groups(g: Graph, n_sources: int) -> int:
+    """Source groups per batch: enough lanes to fill the GPU on small graphs,
+    few enough that one group's sigma slab stays L2-friendly on large ones."""
+    want = max(1, (n_sources + 31) // 32)
+    budget = max(1, int(4e9 // max(1, g.num_vertices * 560)))   # ~4 GB of batch state
+    if g.num_arcs >= 8_000_000:
+        return max(1, min(want, budget, 8))
+    return max(1, min(want, budget, 128))
+
+
+def open_engine(g: Graph, cfg: RunConfig, n_sources: int) -> _capi.Engine:
+    device = cfg.device
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    eng = _capi.Engine(g, device)
+    eng.set_option("groups", cfg.groups or default_groups(g, n_sources))
+    if cfg.item_arcs:
+        eng.set_option("item_arcs", cfg.item_arcs)
+    eng.set_option("reports", 1 if cfg.per_source_reports else 0)
+    return eng
+
+
+def prepare(g: Graph, cfg: RunConfig):
+    """Partition and borders (engine.py:87-102); border tables live on the device."""
+    p = make_partition(g, cfg)
+    bs = identify_borders(g, p)
+    return p, bs
+
+
+def _per_source(sources, reports, mode):
+    out = []
+    for s, r in zip(sources, reports):
+        it, ce, ml0, ml1, se, cb, l0, l1 = (int(x) for x in r)
+        if mode == "bsp-baseline":
+            fwd = {"source": int(s), "supersteps": it, "comm_events": ce, "max_level": [ml0, ml1]}
+        else:
+            fwd = {"source": int(s), "iterations": it, "comm_events": ce, "max_level": [ml0, ml1]}
+        bwd = {"sync_events": se, "comm_bytes": cb, "levels": [l0, l1]}
+        out.append({"source": int(s), "forward": fwd, "backward": bwd})
+    return out
+
+
+def run_bc(g: Graph, cfg: RunConfig | None = None, _pipeline: bool = False) -> RunResult:
+    cfg = cfg or RunConfig()
+    if g.num_vertices == 0:
+        raise InputError("empty graph")
+    if not g.unit_weight:
+        raise InputError("the GPU path handles unit edge weights only")
+    if cfg.num_gpus > 1:
+        from .multigpu import run_bc_multi
+        return run_bc_multi(g, cfg)
+    t0 = time.perf_counter()
+    sources = select_sources(g, cfg)
+    p, bs = prepare(g, cfg)
+    mode = cfg.mode if p.num_parts > 1 else "direct"
+    with open_engine(g, cfg, len(sources)) as eng:
+        if p.num_parts > 1:
+            eng.set_partition(p.num_parts, p.assignment)
+        bc, stats = eng.run(sources, _MODE_CODE[mode])
+        per_source = []
+        if cfg.per_source_reports and p.num_parts > 1:
+            per_source = _per_source(sources, eng.reports(len(sources)), cfg.mode)
+        elif cfg.per_source_reports:
+            per_source = [{"source": int(s), "forward": {"source": int(s)}, "backward": {}} for s in sources]
+    elapsed = time.perf_counter() - t0
+    mteps = (g.num_edges * len(sources) / elapsed / 1e6) if elapsed > 0 else 0.0
+    ledger = CommTotals(stats.get("comm_events", 0), stats.get("sync_events", 0),
+                        stats.get("comm_bytes", 0))
+    return RunResult(bc, per_source, ledger, mteps, elapsed, p, bs, cfg, 0, stats)
+
+
+def pipeline_sources(g: Graph, cfg: RunConfig) -> RunResult:
+    """Look-ahead variant (engine.py:156-161).  Sources already advance 32 x
+    groups at a time on the device, so the result is the same call."""
+    if cfg.mode != "hybir":
+        raise InputError("pipelining applies to hybir mode only")
+    return run_bc(g, cfg, _pipeline=True)
+
+
+def build_report(g: Graph, result: RunResult, top_k: int = 10) -> dict:
+    """JSON-ready report with the reference's field order (engine.py:164-189)."""
+    bc = result.bc
+    order = np.argsort(-bc, kind="stable")[:top_k]
+    return {
+        "schema_version": 1,
+        "graph_stats": graph_stats(g),
+        "partition_stats": {
+            "sizes": list(result.partition.sizes),
+            "ratio": result.partition.ratio,
+            "borders": list(result.borders.counts()),
+            "cut_arcs": len(result.borders.cut_src),
+        },
+        "mode": result.config.mode,
+        "seed": result.config.seed,
+        "per_source": result.per_source,
+        "comm_totals": result.ledger.totals(),
+        "bc_top_k": [{"vertex": int(v), "bc": float(bc[v])} for v in order],
+        "mteps": result.mteps,
+        "pipeline_overlaps": result.pipeline_overlaps,
+        "max_threads": result.config.max_threads,
+    }

@@ -1,0 +1,213 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Bar (BASELINE.json north star): distances and path counts bit-exact, delta and
+BC within 1e-9 relative in fp64.  Checked against (a) golden vectors produced
+by the reference package, (b) the C oracle on seeded inputs, (c) properties
+that hold at any size.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2008_05718_b200 as P
+from paper_2008_05718_b200 import generators as G
+from paper_2008_05718_b200._capi import Engine, MODE_DIRECT
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-9, 1e-12   # the reference's own acceptance tolerance (test_acceptance.py:33,65-66)
+
+
+def assert_sources_match_oracle(g, sources, dist, sigma, delta):
+    for i, s in enumerate(sources):
+        od, osg, odl, info = O.brandes_single_source(g, int(s))
+        assert info["sigma_max"] < 2.0 ** 53
+        assert np.array_equal(dist[i], od), "dist differs for source %d" % s
+        assert np.array_equal(sigma[i], osg), "sigma differs for source %d" % s
+        assert np.allclose(delta[i], odl, rtol=RTOL, atol=ATOL), "delta differs for source %d" % s
+
+
+def test_golden_vectors_direct(golden_graphs):
+    for name, (g, rec) in golden_graphs.items():
+        srcs = [s["s"] for s in rec["sources"]]
+        with Engine(g) as e:
+            dist, sigma, delta = e.debug_sources(srcs)
+            bc_all, _ = e.run(list(range(g.num_vertices)))
+            bc_sub, _ = e.run(rec["run_bc_sources"])
+        for i, s in enumerate(rec["sources"]):
+            assert dist[i].tolist() == s["dist"], name
+            assert sigma[i].tolist() == [float(x) for x in s["sigma"]], name
+            assert np.allclose(delta[i], s["delta"], rtol=RTOL, atol=ATOL), name
+        assert np.allclose(bc_all, rec["bc_all_sources"], rtol=RTOL, atol=ATOL), name
+        assert np.allclose(bc_sub, rec["run_bc_hybir"], rtol=RTOL, atol=ATOL), name
+
+
+def test_known_answers_through_run_bc():
+    # reference pkg/tests/test_engine.py:14-17 and test_oracle.py:37-42
+    cases = [
+        (G.path(4), [0, 4, 4, 0]),
+        (P.from_edges(4, [(0, 1, 1), (0, 2, 1), (1, 3, 1), (2, 3, 1)]), [1, 1, 1, 1]),
+        (P.from_edges(6, [(i, (i + 1) % 6, 1) for i in range(6)]), [4] * 6),
+        (P.from_edges(4, [(i, j, 1) for i in range(4) for j in range(i + 1, 4)]), [0] * 4),
+        (P.from_edges(5, [(0, i, 1) for i in range(1, 5)]), [12, 0, 0, 0, 0]),
+    ]
+    for g, want in cases:
+        res = P.run_bc(g, P.RunConfig(mode="direct"))
+        assert np.allclose(res.bc, want, rtol=RTOL, atol=ATOL)
+        assert res.mteps > 0 and res.elapsed > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_graphs_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(20, 400))
+    g = G.random_connected(n, int(rng.integers(0, 2 * n)), seed=seed)
+    srcs = rng.choice(n, size=min(n, 70), replace=False).tolist()
+    with Engine(g) as e:
+        e.set_option("groups", int(rng.integers(1, 4)))
+        dist, sigma, delta = e.debug_sources(srcs)
+        bc, st = e.run(srcs)
+    assert_sources_match_oracle(g, srcs, dist, sigma, delta)
+    obc, info = O.brandes_bc(g, srcs)
+    assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+    assert (st["reached"], st["arcs_reached"], st["dag_arcs"]) == (
+        info["reached"], info["arcs_reached"], info["dag_arcs"])
+    assert st["max_levels"] == info["max_levels"]
+
+
+def test_config1_rmat12_all_sources(rmat12):
+    """BASELINE config 1: R-MAT scale-12 EF-8, all 4096 sources."""
+    g = rmat12
+    srcs = list(range(g.num_vertices))
+    with Engine(g) as e:
+        e.set_option("groups", 16)
+        bc, st = e.run(srcs)
+        sample = list(range(0, g.num_vertices, 41))
+        dist, sigma, delta = e.debug_sources(sample)
+    obc, info = O.brandes_bc(g, srcs)
+    assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+    assert st["reached"] == info["reached"] and st["dag_arcs"] == info["dag_arcs"]
+    assert_sources_match_oracle(g, sample, dist, sigma, delta)
+    # bc max=1.482890e+06 sum=1.623059e+07 on this graph
+    assert bc.max() == pytest.approx(1.482890e6, rel=1e-6)
+    assert bc.sum() == pytest.approx(1.623059e7, rel=1e-6)
+
+
+def test_hub_slices_and_item_sizes():
+    # hubs (degree >> item_arcs) take the sliced path; results must not depend
+    # on how the adjacency is cut into work items
+    g = G.rmat(13, 16, 3)
+    srcs = list(range(0, g.num_vertices, 97))
+    ref = None
+    for item_arcs in (32, 64, 256, 1024):
+        with Engine(g) as e:
+            e.set_option("item_arcs", item_arcs)
+            dist, sigma, delta = e.debug_sources(srcs[:40])
+            bc, _ = e.run(srcs)
+        assert_sources_match_oracle(g, srcs[:40], dist, sigma, delta)
+        if ref is None:
+            ref = bc
+            obc, _ = O.brandes_bc(g, srcs)
+            assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+        else:
+            assert np.allclose(bc, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_edge_cases():
+    # single vertex, isolated sources, duplicate sources, empty source list,
+    # disconnected components, partial last group
+    one = P.from_edges(1, [])
+    with Engine(one) as e:
+        bc, st = e.run([0])
+        assert bc.tolist() == [0.0] and st["reached"] == 1
+        d, s, dl = e.debug_sources([0])
+        assert d.tolist() == [[0]] and s.tolist() == [[1.0]] and dl.tolist() == [[0.0]]
+    g = P.from_edges(7, [(0, 1, 1), (1, 2, 1), (4, 5, 1)])      # 3 and 6 isolated
+    with Engine(g) as e:
+        bc, _ = e.run([])
+        assert not bc.any()
+        bc, _ = e.run([3, 6])
+        assert not bc.any()
+        bc1, _ = e.run([0, 2, 4])
+        bc2, _ = e.run([0, 2, 4, 0, 2, 4])
+        assert np.allclose(2 * bc1, bc2)
+        d, s, dl = e.debug_sources([0, 3])
+        assert d[0].tolist() == [0, 1, 2, -1, -1, -1, -1] and d[1].tolist() == [-1, -1, -1, 0, -1, -1, -1]
+        assert s[1].tolist() == [0, 0, 0, 1, 0, 0, 0]
+        with pytest.raises(P.InputError):
+            e.run([7])
+        with pytest.raises(P.InputError):
+            e.run([-1])
+        with pytest.raises(P.InputError):
+            e.set_option("groups", 0)
+    srcs = list(range(45))                                       # 32 + 13 lanes
+    g = G.grid(9, 5)
+    with Engine(g) as e:
+        e.set_option("groups", 1)
+        bc, _ = e.run(srcs)
+    assert np.allclose(bc, O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
+
+
+def test_deep_graph_path_and_grid():
+    # high diameter: many levels, speculative level launches, sigma stays small
+    p = G.path(3000)
+    with Engine(p) as e:
+        bc, st = e.run([0, 1500, 2999])
+    assert st["max_levels"] == 3000
+    assert np.allclose(bc, O.brandes_bc(p, [0, 1500, 2999])[0], rtol=RTOL, atol=ATOL)
+    r = G.road_like(96, 96, keep=0.2, seed=1)
+    srcs = list(range(0, r.num_vertices, 211))
+    with Engine(r) as e:
+        dist, sigma, delta = e.debug_sources(srcs[:8])
+        bc, _ = e.run(srcs)
+    for i, s in enumerate(srcs[:8]):
+        od, osg, odl, info = O.brandes_single_source(r, s)
+        assert np.array_equal(dist[i], od)
+        if info["sigma_max"] < 2.0 ** 53:
+            assert np.array_equal(sigma[i], osg)
+        else:   # beyond exact integers: fp64 path counts, 1e-12 relative (SURVEY.md hard part 1)
+            assert np.allclose(sigma[i], osg, rtol=1e-12)
+        assert np.allclose(delta[i], odl, rtol=RTOL, atol=ATOL)
+    assert np.allclose(bc, O.brandes_bc(r, srcs)[0], rtol=RTOL, atol=ATOL)
+
+
+def test_deterministic_and_linear(rmat12):
+    g = rmat12
+    a = list(range(0, 4096, 9))
+    b = list(range(1, 4096, 13))
+    with Engine(g) as e:
+        bc_a, _ = e.run(a)
+        bc_a2, _ = e.run(a)
+        bc_b, _ = e.run(b)
+        bc_ab, _ = e.run(a + b)
+    assert np.array_equal(bc_a, bc_a2)                       # bit-reproducible
+    assert np.allclose(bc_a + bc_b, bc_ab, rtol=1e-12)       # BC is a sum over sources
+    assert bc_ab.min() >= 0.0
+
+
+@pytest.mark.slow
+def test_config2_rmat20_sample():
+    """BASELINE config 2 at full size: R-MAT scale-20 EF-16; oracle on a 48-source sample,
+    size-independent properties on the full 1024-source run."""
+    import random
+    g = G.rmat(20, 16, 1)
+    assert g.num_vertices == 1 << 20
+    srcs = sorted(random.Random(0).sample(range(g.num_vertices), 1024))
+    with Engine(g) as e:
+        e.set_option("groups", 8)
+        bc, st = e.run(srcs)
+        bc48, _ = e.run(srcs[:48])
+        dist, sigma, delta = e.debug_sources(srcs[:4])
+    obc, info = O.brandes_bc(g, srcs[:48])
+    assert np.allclose(bc48, obc, rtol=RTOL, atol=ATOL)
+    assert_sources_match_oracle(g, srcs[:4], dist, sigma, delta)
+    # sum over v of delta_s[v] = sum over reached t != s of (dist(s,t) - 1) for every source,
+    # so the BC total is fixed by the distance histogram alone
+    total = 0
+    for i in range(4):
+        d = dist[i][dist[i] > 0]
+        assert delta[i].sum() - delta[i][srcs[i]] == pytest.approx(float((d - 1).sum()), rel=1e-9)
+    deg = np.diff(g.offsets)
+    assert not bc[deg == 0].any() and bc.min() >= 0.0
+    assert st["sources"] == 1024 and st["max_levels"] >= 5

@@ -1,0 +1,162 @@
+"""Host-side logic: graph normalisation, partitioning, borders, source
+selection and configuration errors -- the reference's behaviour for each is
+cited next to the check."""
+
+import random
+
+import numpy as np
+import pytest
+
+import paper_2008_05718_b200 as P
+from paper_2008_05718_b200 import generators as G
+from paper_2008_05718_b200.engine import default_groups, make_partition
+
+
+def test_csr_of_p4():
+    # reference pkg/tests/test_graph.py:12-18
+    g = G.path(4)
+    assert g.offsets.tolist() == [0, 1, 3, 5, 6]
+    assert g.arc_src.tolist() == [0, 1, 1, 2, 2, 3]
+    assert g.arc_dst.tolist() == [1, 0, 2, 1, 3, 2]
+    assert g.num_edges == 3 and g.num_arcs == 6 and g.inf_distance == 4
+    assert g.rev_arc.tolist() == [1, 0, 3, 2, 5, 4]
+
+
+def test_from_edges_normalisation():
+    # self loops dropped, parallel edges collapse to the minimum weight,
+    # symmetrised (graph.py:64-110)
+    g = P.from_edges(4, [(0, 1, 5), (1, 0, 2), (2, 2, 1), (3, 1, 7), (1, 3, 9)])
+    assert g.num_edges == 2
+    assert g.arc_src.tolist() == [0, 1, 1, 3] and g.arc_dst.tolist() == [1, 0, 3, 1]
+    assert g.arc_weight.tolist() == [2, 2, 7, 7]
+    assert g.inf_distance == 10 and not g.unit_weight
+    assert P.from_edges(3, []).num_edges == 0
+
+
+def test_from_edges_errors():
+    with pytest.raises(P.FormatError):
+        P.from_edges(3, [(0, 3, 1)])
+    with pytest.raises(P.DomainError):
+        P.from_edges(3, [(0, 1, -1)])
+    with pytest.raises(P.DomainError):
+        P.from_edges(3, [(0, 1, 0)])
+    # the first offending edge decides, as in the reference's edge-by-edge loop
+    with pytest.raises(P.DomainError):
+        P.from_edges(3, [(0, 1, 0), (0, 9, 1)])
+    assert issubclass(P.FormatError, P.InputError) and issubclass(P.InputError, P.HybirError)
+
+
+def test_golden_graphs_round_trip(golden_graphs):
+    for g, rec in golden_graphs.values():
+        assert g.offsets.tolist() == rec["offsets"]
+        assert g.arc_dst.tolist() == rec["arc_dst"]
+        assert g.inf_distance == rec["inf"]
+
+
+def test_borders_match_reference(golden_graphs):
+    for g, rec in golden_graphs.values():
+        p = P.Partition(np.asarray(rec["assignment"], dtype=np.int8), 0.5, 2)
+        bs = P.identify_borders(g, p)
+        assert [list(b) for b in bs.borders] == rec["borders"]
+        assert [[u, v] for u, v, _ in bs.cut_arcs] == rec["cut_arcs"]
+        for side in (0, 1):
+            assert bs.index[side] == {v: i for i, v in enumerate(rec["borders"][side])}
+
+
+def test_known_borders():
+    # reference pkg/tests/test_partition.py:99-111
+    g = G.path(4)
+    bs = P.identify_borders(g, P.Partition(np.array([0, 0, 1, 1], dtype=np.int8)))
+    assert bs.borders == ([1], [2]) and bs.cut_arcs == [(1, 2, 1), (2, 1, 1)]
+    d = P.from_edges(4, [(0, 1, 1), (0, 2, 1), (1, 3, 1), (2, 3, 1)])
+    bs = P.identify_borders(d, P.Partition(np.array([0, 0, 1, 1], dtype=np.int8)))
+    assert bs.borders == ([0, 1], [2, 3]) and len(bs.cut_arcs) == 4
+
+
+def test_greedy_bipartition_matches_reference(golden_graphs):
+    # fixtures whose partition came from the reference's greedy_bipartition
+    cases = {"grid9x7_greedy": (0.5, 3), "rc_n12_s1000": (0.7, 1000), "rc_n25_s1002": (0.5, 1002),
+             "rc_n40_s1004": (0.5, 1004), "rc_n60_s1006": (0.7, 1006), "rc_n90_s1008": (0.5, 1008),
+             "rmat8": (0.5, 0)}
+    for name, (ratio, seed) in cases.items():
+        g, rec = golden_graphs[name]
+        p = P.greedy_bipartition(g, ratio, seed=seed)
+        assert p.assignment.tolist() == rec["assignment"], name
+
+
+def test_greedy_bipartition_errors():
+    with pytest.raises(P.InputError):
+        P.greedy_bipartition(G.path(4), 1.0)
+    with pytest.raises(P.InputError):
+        P.greedy_bipartition(P.from_edges(1, []), 0.5)
+
+
+def test_rmat12_is_the_baseline_graph(rmat12):
+    # n=4,096, m=26,603, 1,129 isolated, max degree 931,
+    # greedy borders (780, 908), 4,060 cut arcs
+    deg = np.diff(rmat12.offsets)
+    assert (rmat12.num_vertices, rmat12.num_edges) == (4096, 26603)
+    assert int((deg == 0).sum()) == 1129 and int(deg.max()) == 931
+    p = P.greedy_bipartition(rmat12, 0.5, seed=0)
+    bs = P.identify_borders(rmat12, p)
+    assert bs.counts() == (780, 908) and len(bs.cut_src) == 4060
+
+
+def test_kway_partitions():
+    g = G.grid(8, 6)
+    p = P.strip_partition(8, 6, 4)
+    assert p.sizes == (12, 12, 12, 12)
+    bs = P.identify_borders(g, p)
+    assert bs.counts() == (6, 12, 12, 6)
+    assert P.block_partition(g, 3).sizes == (16, 16, 16)
+    assert P.single_partition(g).num_parts == 1
+    assert P.identify_borders(g, P.single_partition(g)).counts() == (0,)
+
+
+def test_select_sources_rule():
+    g = G.path(50)
+    assert P.select_sources(g, P.RunConfig()) == list(range(50))
+    assert P.select_sources(g, P.RunConfig(sources=[7, 3, 3])) == [7, 3, 3]
+    want = sorted(random.Random(5).sample(range(50), 10))     # engine.py:82-84
+    assert P.select_sources(g, P.RunConfig(num_sources=10, seed=5)) == want
+    assert len(P.select_sources(g, P.RunConfig(num_sources=99))) == 50
+    with pytest.raises(P.InputError):
+        P.select_sources(g, P.RunConfig(sources=[50]))
+
+
+def test_run_config_validation():
+    with pytest.raises(P.InputError):
+        P.RunConfig(mode="nope")
+    with pytest.raises(P.InputError):
+        P.RunConfig(num_sources=0)
+    with pytest.raises(P.InputError):
+        P.RunConfig(backward_strategies=("vertex-pull", "sideways"))
+    with pytest.raises(P.InputError):
+        P.RunConfig(gpu_mode="ring")
+    with pytest.raises(P.InputError):
+        P.run_bc(P.from_edges(0, []), P.RunConfig())
+    with pytest.raises(P.InputError):      # weighted graphs stay on the CPU reference
+        P.run_bc(P.from_edges(3, [(0, 1, 2), (1, 2, 1)]), P.RunConfig())
+
+
+def test_make_partition_modes():
+    g = G.grid(6, 6)
+    assert make_partition(g, P.RunConfig(num_partitions=1)).num_parts == 1
+    assert make_partition(g, P.RunConfig(mode="direct")).num_parts == 1
+    assert make_partition(g, P.RunConfig()).num_parts == 2
+    assert make_partition(g, P.RunConfig(num_partitions=4)).sizes == (9, 9, 9, 9)
+    assert default_groups(g, 36) == 2
+
+
+def test_generators_shapes():
+    g = G.grid(5, 4)
+    assert (g.num_vertices, g.num_edges) == (20, 31)
+    r = G.road_like(12, 9, keep=0.2, seed=3)
+    assert r.num_vertices == 108 and 107 <= r.num_edges < 12 * 8 + 11 * 9
+    import oracle as O
+    d, _, _, info = O.brandes_single_source(r, 0)
+    assert info["reached"] == 108          # a spanning tree is inside: connected
+    e = G.erdos_renyi(64, 256, seed=2)
+    assert e.num_vertices == 64 and e.num_edges <= 256
+    a = G.random_connected(30, 10, seed=4)
+    assert O.brandes_single_source(a, 0)[3]["reached"] == 30

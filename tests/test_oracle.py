@@ -1,0 +1,131 @@
+"""Pins the CPU oracle (oracle/) to the reference: known-answer vectors the
+reference's own tests hold and golden vectors produced
+by running the reference package (tests/golden/gen_golden.py)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2008_05718_b200 import from_edges, generators as G
+
+from conftest import graph_from_record
+
+
+def _named(name):
+    if name == "p4":
+        return G.path(4)
+    if name == "diamond":
+        return from_edges(4, [(0, 1, 1), (0, 2, 1), (1, 3, 1), (2, 3, 1)])
+    if name == "c6":
+        return from_edges(6, [(i, (i + 1) % 6, 1) for i in range(6)])
+    if name == "k4":
+        return from_edges(4, [(i, j, 1) for i in range(4) for j in range(i + 1, 4)])
+    if name == "star5":
+        return from_edges(5, [(0, i, 1) for i in range(1, 5)])
+    raise KeyError(name)
+
+
+# reference pkg/tests/test_oracle.py:37-42
+@pytest.mark.parametrize("name,expect", [
+    ("p4", [0, 4, 4, 0]), ("diamond", [1, 1, 1, 1]), ("c6", [4] * 6), ("k4", [0] * 4),
+    ("star5", [12, 0, 0, 0, 0]),
+])
+def test_known_bc(name, expect):
+    bc, _ = O.brandes_bc(_named(name))
+    assert np.allclose(bc, expect, rtol=1e-12, atol=1e-12)
+
+
+def test_known_single_source_vectors():
+    # reference pkg/tests/test_backward.py:25-37
+    d, s, dl, _ = O.brandes_single_source(_named("p4"), 0)
+    assert d.tolist() == [0, 1, 2, 3] and s.tolist() == [1, 1, 1, 1] and dl.tolist() == [3, 2, 1, 0]
+    d, s, dl, _ = O.brandes_single_source(_named("diamond"), 0)
+    assert d.tolist() == [0, 1, 1, 2] and s.tolist() == [1, 1, 1, 2] and dl.tolist() == [3, 0.5, 0.5, 0]
+    d, s, dl, _ = O.brandes_single_source(_named("star5"), 1)
+    assert dl[0] == 3.0
+    # reference pkg/tests/test_forward.py:151-156
+    d, s, _, _ = O.brandes_single_source(_named("c6"), 0)
+    assert d.tolist() == [0, 1, 2, 3, 2, 1] and s.tolist() == [1, 1, 1, 2, 1, 1]
+
+
+def test_known_relax_vectors():
+    p4 = _named("p4")
+    # reference pkg/tests/test_forward.py:18-41
+    d, s = O.masked_relax(p4, None, [(0, 0, 1)])
+    assert d.tolist() == [0, 1, 2, 3] and s.tolist() == [1, 1, 1, 1]
+    d, s = O.masked_relax(p4, [1, 1, 0, 0], [(0, 0, 1)])
+    assert d.tolist() == [0, 1, p4.inf_distance, p4.inf_distance] and s[2] == 0
+    d, s = O.masked_relax(p4, None, [(0, 0, 2), (3, 0, 3)])
+    assert d.tolist() == [0, 1, 1, 0] and s.tolist() == [2, 2, 3, 3]
+    d, s = O.masked_relax(p4, None, [(0, p4.inf_distance, 1), (1, 0, 0)])
+    assert (d == p4.inf_distance).all()
+    with pytest.raises(LookupError):
+        O.masked_relax(p4, [1, 1, 0, 0], [(3, 0, 1)])
+    d, s = O.masked_relax(_named("diamond"), None, [(0, 0, 1)])
+    assert s.tolist() == [1, 1, 1, 2]
+
+
+def test_single_source_matches_reference_vectors(golden_graphs):
+    checked = 0
+    for g, rec in golden_graphs.values():
+        for src in rec["sources"]:
+            d, s, dl, info = O.brandes_single_source(g, src["s"])
+            assert d.tolist() == src["dist"]
+            assert s.tolist() == [float(x) for x in src["sigma"]]
+            assert info["sigma_max"] < 2.0 ** 53
+            # same settle order and the same division -> bit-identical delta
+            assert dl.tolist() == src["delta"]
+            checked += 1
+    assert checked > 150
+
+
+def test_bc_matches_reference_vectors(golden_graphs):
+    for g, rec in golden_graphs.values():
+        for threads in (1, 3):
+            bc, _ = O.brandes_bc(g, threads=threads)
+            assert np.allclose(bc, rec["bc_all_sources"], rtol=1e-12, atol=1e-12)
+        bc, _ = O.brandes_bc(g, rec["run_bc_sources"], threads=2)
+        assert np.allclose(bc, rec["run_bc_hybir"], rtol=1e-9, atol=1e-12)
+        assert np.allclose(bc, rec["run_bc_bsp_baseline"], rtol=1e-9, atol=1e-12)
+
+
+def test_masked_relax_matches_reference_vectors(golden):
+    for case in golden["relax_cases"]:
+        g = graph_from_record(case)
+        d, s = O.masked_relax(g, case["mask"], [tuple(x) for x in case["seeds"]])
+        d = np.where(d >= g.inf_distance, -1, d)
+        assert d.tolist() == case["dist"]
+        assert s.tolist() == [float(x) for x in case["sigma"]]
+
+
+def test_step1_relax_matches_reference_vectors(golden_graphs):
+    for g, rec in golden_graphs.values():
+        a = np.asarray(rec["assignment"])
+        for src in rec["sources"][:6]:
+            s = src["s"]
+            d, sg = O.masked_relax(g, a == a[s], [(s, 0, 1)])
+            d = np.where(d >= g.inf_distance, -1, d)
+            assert d.tolist() == src["step1_dist"]
+            assert sg.tolist() == [float(x) for x in src["step1_sigma"]]
+
+
+def test_rmat12_anchor(golden, rmat12):
+    # BASELINE config 1: the graph itself and six sources of the reference oracle
+    anchor = golden["rmat12_anchor"]
+    assert (rmat12.num_vertices, rmat12.num_edges) == (anchor["n"], anchor["m"]) == (4096, 26603)
+    for rec in anchor["sources"]:
+        d, s, dl, info = O.brandes_single_source(rmat12, rec["s"])
+        assert info["reached"] == rec["reached"] and int(d.max()) == rec["ecc"]
+        assert int(s.sum()) == rec["sigma_sum"] and int(s.max()) == rec["sigma_max"]
+        assert np.bincount(d[d >= 0]).tolist() == rec["dist_hist"]
+        assert float(dl.sum()) == pytest.approx(rec["delta_sum"], rel=1e-12)
+        assert float(dl.max()) == pytest.approx(rec["delta_max"], rel=1e-12)
+
+
+def test_counters_are_consistent(rmat12):
+    d, s, dl, info = O.brandes_single_source(rmat12, 17)
+    deg = np.diff(rmat12.offsets)
+    assert info["arcs_reached"] == int(deg[d >= 0].sum())
+    src, dst = rmat12.arc_src, rmat12.arc_dst
+    tight = (d[src] >= 0) & (d[dst] == d[src] + 1)
+    assert info["dag_arcs"] == int(tight.sum())
