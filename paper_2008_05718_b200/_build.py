@@ -34,8 +34,9 @@ def is_stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not is_stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """``defines`` / ``out`` build a tuning variant (e.g. BC_MIN_BLOCKS=6) beside the default."""
+    if out is None and not force and not is_stale():
         return SO_PATH
     cmd = [
         nvcc_path(), "-O3", "-std=c++17",
@@ -43,8 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
         "-ccbin", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++",
         "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
-        "-o", SO_PATH,
-    ] + SOURCES
+        "-o", out or SO_PATH,
+    ] + ["-D" + d for d in defines] + SOURCES
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -52,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n%s\n%s" % (" ".join(cmd), res.stderr))
     if verbose:
         sys.stderr.write(res.stderr)
-    return SO_PATH
+    return out or SO_PATH
 
 
 if __name__ == "__main__":

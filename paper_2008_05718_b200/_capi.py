@@ -15,7 +15,7 @@ import numpy as np
 from .errors import EngineError, InputError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libbc_b200.so")
+SO_PATH = os.environ.get("BC_B200_LIB") or os.path.join(HERE, "libbc_b200.so")  # env: tuning variants
 
 BC_OK, BC_ERR_INTERNAL, BC_ERR_INPUT = 0, 1, 2
 BC_UNREACHED = -1

@@ -46,7 +46,7 @@ struct bc_handle {
     Csr full;
     // options
     int groups = 4;
-    int item_arcs = 256;
+    int item_arcs = 512;
     int reports = 1;
     // per-batch state
     int alloc_groups = 0;
@@ -57,8 +57,8 @@ struct bc_handle {
     double *pacc = nullptr;
     uint32_t *pmask = nullptr;
     int pacc_chunks = 0;
-    uint32_t *level_any = nullptr;
-    int level_any_cap = 0;
+    uint32_t *live = nullptr;  // [level][alloc_groups] lanes with a non-empty frontier
+    int live_cap = 0;          // levels
     unsigned long long *counters = nullptr;
     int64_t *d_src = nullptr;
     int64_t d_src_cap = 0;
@@ -167,6 +167,9 @@ void free_state(bc_handle *h) {
     h->lvl.clear();
     cudaFree(h->sigma), cudaFree(h->coef), cudaFree(h->delta), cudaFree(h->bcg);
     cudaFree(h->pacc), cudaFree(h->pmask);
+    cudaFree(h->live);
+    h->live = nullptr;
+    h->live_cap = 0;
     h->vis = nullptr;
     h->sigma = h->coef = h->delta = h->bcg = h->pacc = nullptr;
     h->pmask = nullptr;
@@ -208,18 +211,19 @@ int ensure_levels(bc_handle *h, int count) {
         CUDA_TRY(h, cudaMalloc((void **)&p, bytes));
         h->lvl.push_back(p);
     }
-    if (h->level_any_cap < count + 1) {
-        const int cap = std::max(count + 1, 2 * h->level_any_cap);
+    if (h->live_cap < count + 1) {
+        const int cap = std::max(count + 1, 2 * h->live_cap);
+        const size_t G = (size_t)h->alloc_groups;
         uint32_t *p = nullptr;
-        CUDA_TRY(h, cudaMalloc((void **)&p, cap * sizeof(uint32_t)));
-        CUDA_TRY(h, cudaMemset(p, 0, cap * sizeof(uint32_t)));
-        if (h->level_any) {
-            CUDA_TRY(h, cudaMemcpy(p, h->level_any, h->level_any_cap * sizeof(uint32_t),
+        CUDA_TRY(h, cudaMalloc((void **)&p, cap * G * sizeof(uint32_t)));
+        CUDA_TRY(h, cudaMemset(p, 0, cap * G * sizeof(uint32_t)));
+        if (h->live) {
+            CUDA_TRY(h, cudaMemcpy(p, h->live, h->live_cap * G * sizeof(uint32_t),
                                    cudaMemcpyDeviceToDevice));
-            cudaFree(h->level_any);
+            cudaFree(h->live);
         }
-        h->level_any = p;
-        h->level_any_cap = cap;
+        h->live = p;
+        h->live_cap = cap;
     }
     return BC_OK;
 }
@@ -276,16 +280,16 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st) {
     LevelParams p = level_params(h, c);
     p.nbr = h->lvl[L - 1];
     p.cur = h->lvl[L];
-    p.prev_any = h->level_any + (L - 1);
-    p.cur_any = h->level_any + L;
+    p.live_prev = h->live + (size_t)(L - 1) * h->alloc_groups;
+    p.live_cur = h->live + (size_t)L * h->alloc_groups;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     level_kernel<false, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     ++h->launches;
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
         q.cur = h->lvl[L];
-        q.prev_any = p.prev_any;
-        q.cur_any = p.cur_any;
+        q.live_prev = p.live_prev;
+        q.live_cur = p.live_cur;
         hub_kernel<false, false><<<dim3(blocks_for(c.n_hub), ng), kWarpsPerBlock * 32, 0, st>>>(q);
         ++h->launches;
     }
@@ -299,6 +303,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     LevelParams p = level_params(h, c);
     p.nbr = deepest ? nullptr : h->lvl[L + 1];
     p.cur = h->lvl[L];
+    p.live_prev = h->live + (size_t)L * h->alloc_groups;
     p.accumulate_bc = accumulate ? 1 : 0;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     if (store_delta)
@@ -309,6 +314,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
         q.cur = h->lvl[L];
+        q.live_prev = p.live_prev;
         q.accumulate_bc = p.accumulate_bc;
         const dim3 hg(blocks_for(c.n_hub), ng);
         if (store_delta)
@@ -333,12 +339,18 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
         if (rc) return rc;
         for (int j = 0; j < chunk; ++j)
             if ((rc = launch_forward(h, c, L + j, ng, st))) return rc;
-        flags.assign(chunk, 0);
-        CUDA_TRY(h, cudaMemcpyAsync(flags.data(), h->level_any + L, chunk * sizeof(uint32_t),
-                                    cudaMemcpyDeviceToHost, st));
+        const size_t G = (size_t)h->alloc_groups;
+        flags.assign(chunk * G, 0);
+        CUDA_TRY(h, cudaMemcpyAsync(flags.data(), h->live + (size_t)L * G,
+                                    chunk * G * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(h, cudaStreamSynchronize(st));
+        auto level_alive = [&](int j) {
+            for (int g = 0; g < ng; ++g)
+                if (flags[(size_t)j * G + g]) return true;
+            return false;
+        };
         int j = 0;
-        while (j < chunk && flags[j]) ++j;
+        while (j < chunk && level_alive(j)) ++j;
         if (j < chunk) {
             *depth_out = L + j;
             return BC_OK;
@@ -360,7 +372,17 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
                      (long long)sources[i], (long long)n);
             return h->fail(BC_ERR_INPUT, buf);
         }
-    const int groups = debug ? 1 : h->groups;
+    // Sources without arcs reach nothing: sigma = 1 at the source, delta = 0
+    // everywhere.  They stay in the result (and in the counters) but take no
+    // lane on the device.  The inspection path keeps them so rows line up.
+    std::vector<int64_t> active;
+    active.reserve((size_t)k);
+    for (int64_t i = 0; i < k; ++i)
+        if (debug || h->h_off[sources[i] + 1] > h->h_off[sources[i]]) active.push_back(sources[i]);
+    const int64_t k_all = k;
+    k = (int64_t)active.size();
+    sources = active.data();
+    const int groups = debug ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(h->groups, (k + 31) / 32));
     int rc = ensure_state(h, groups, c.n_chk, debug);
     if (rc) return rc;
     if ((rc = ensure_levels(h, 2))) return rc;
@@ -401,11 +423,12 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
         CUDA_TRY(h, cudaEventCreate(&e.bwd_end));
         CUDA_TRY(h, cudaEventRecord(e.start, st));
 
-        CUDA_TRY(h, cudaMemsetAsync(h->level_any, 0, h->level_any_cap * sizeof(uint32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->live, 0,
+                                    (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
         init_state_kernel<<<dim3(std::min<int64_t>((n + 255) / 256, 1184), ng), 256, 0, st>>>(
             h->vis, h->lvl[0], n, cnt);
         seed_sources_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * lanes_per_batch, cnt, n,
-                                                                h->vis, h->lvl[0], h->sigma, h->level_any);
+                                                                h->vis, h->lvl[0], h->sigma, h->live);
         h->launches += 2;
         CUDA_TRY(h, cudaGetLastError());
 
@@ -470,11 +493,11 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
     if (!ev.empty()) ms_total = ms_f + ms_b;
     if (stats) {
         memset(stats, 0, sizeof *stats);
-        stats->sources = k;
+        stats->sources = k_all;
         stats->batches = n_batches;
-        stats->max_levels = max_depth;
+        stats->max_levels = std::max<int64_t>(max_depth, k_all > 0 ? 1 : 0);
         // sources themselves are reached vertices too (level 0)
-        stats->reached = (int64_t)cnts[0] + k;
+        stats->reached = (int64_t)cnts[0] + k_all;
         int64_t src_arcs = 0;
         for (int64_t i = 0; i < k; ++i) src_arcs += h->h_off[sources[i] + 1] - h->h_off[sources[i]];
         stats->arcs_reached = (int64_t)cnts[1] + src_arcs;
@@ -649,7 +672,7 @@ void bc_destroy(bc_handle *h) {
     cudaSetDevice(h->device);
     free_state(h);
     free_csr(h->full);
-    cudaFree(h->level_any);
+    cudaFree(h->live);
     cudaFree(h->counters);
     cudaFree(h->d_src);
     cudaFree(h->bc_scratch);

@@ -23,6 +23,12 @@
 
 namespace bcb200 {
 
+#ifndef BC_MIN_BLOCKS
+#define BC_MIN_BLOCKS 6
+#endif
+#ifndef BC_SPARSE_SLICE
+#define BC_SPARSE_SLICE 2
+#endif
 constexpr int kWarpsPerBlock = 8;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -49,8 +55,11 @@ struct LevelParams {
     double *bcg;    // [group][v] per-group BC partial sums
     double *pacc;   // [group][chunk][32] hub partial sums
     uint32_t *pmask;  // [group][chunk]
-    const uint32_t *prev_any;  // forward: flag of level L-1 (skip the launch's work when 0)
-    uint32_t *cur_any;         // forward: set when level L discovered anything
+    // live[L][g] = lanes of group g whose level-L frontier is not empty.  A lane
+    // whose frontier died (e.g. an isolated source) is dropped from every later
+    // `want`, so exhausted instances stop costing adjacency scans.
+    const uint32_t *live_prev;  // forward: live[L-1]; backward: live[L]
+    uint32_t *live_cur;         // forward: live[L], OR-ed by this launch
     unsigned long long *counters;  // [0] n_r, [1] A_r, [2] T
     int accumulate_bc;
 };
@@ -61,23 +70,58 @@ __device__ __forceinline__ double warp_sum(double x) {
     return x;
 }
 
+// Predicated read-only load: one LDG under a predicate, never a branch (the
+// compiler turns `if (p) x = __ldg(..)` into divergent control flow here).
+__device__ __forceinline__ double ldg_if(const double *ptr, bool pred) {
+    double x;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
+        "@q ld.global.nc.f64 %0, [%1];\n\t}"
+        : "=d"(x)
+        : "l"(ptr), "r"((int)pred));
+    return x;
+}
+
+// 32 x 32 bit-matrix transpose across the warp: on return bit j of lane l is
+// bit l of lane j's input (five butterfly exchanges).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    uint32_t m = 0x0000ffffu;
+#pragma unroll
+    for (int j = 16; j != 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(kFull, x, j);
+        x = (lane & j) ? (((o >> j) & m) | (x & ~m)) : ((x & m) | ((o & m) << j));
+        m ^= m << (j >> 1);
+    }
+    return x;
+}
+
+constexpr int kSparseSlice = BC_SPARSE_SLICE;  // slices with at most this many hit arcs take the arc-serial path
+
 // Scan arcs [a0, a1) of one vertex.  `want` (warp-uniform) = lanes that still
-// need a value.  For every neighbour w whose mask row intersects `want`, lanes
-// in the intersection add val[w][lane] to acc.  Four gathers are issued before
-// the four dependent adds so each warp keeps several sectors in flight; the
+// need a value.  Filter: lanes = arcs, hit = mask[neighbour] & want.  Gather,
+// two shapes:
+//   sparse slice (few arcs hit): arc-serial, lanes = BFS instances read one
+//     neighbour row, predicated per lane;
+//   dense slice: the 32 x 32 hit matrix is transposed so that lane l holds
+//     the set of arcs that hit *its* BFS instance, and every lane walks its own
+//     arc list -- the trip count is the longest column, not the number of hit
+//     arcs, and every load instruction keeps up to 32 sectors in flight.
+// Both shapes add in ascending arc order, so the sum is identical and
+// deterministic.  Four gathers are issued before the four dependent adds; the
 // next 32-arc slice is loaded before the current one is consumed.
+// tcount is a per-lane partial count of (arc, instance) hits (COUNT_T only).
 template <bool COUNT_T>
 __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
                                           const int32_t *__restrict__ col,
                                           const uint32_t *__restrict__ nmask,
                                           const double *__restrict__ val, int lane, double &acc,
-                                          uint32_t &got, unsigned long long &tcount) {
+                                          uint32_t &got, unsigned &tcount) {
     int32_t w_n = 0;
     uint32_t hit_n = 0;
     if (a0 + lane < a1) {
         w_n = __ldg(col + a0 + lane);
         hit_n = __ldg(nmask + w_n) & want;
     }
+    const double *myval = val + lane;
     for (int64_t base = a0; base < a1; base += 32) {
         const int32_t w = w_n;
         const uint32_t hit = hit_n;
@@ -89,44 +133,55 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
             hit_n = __ldg(nmask + w_n) & want;
         }
         unsigned any = __ballot_sync(kFull, hit != 0);
-        while (any) {
-            const int j0 = __ffs(any) - 1;
-            any &= any - 1;
-            int j1 = -1, j2 = -1, j3 = -1;
-            if (any) {
-                j1 = __ffs(any) - 1;
+        if (any == 0) continue;
+        if (__popc(any) <= kSparseSlice) {
+            while (any) {
+                const int j0 = __ffs(any) - 1;
                 any &= any - 1;
-            }
-            if (any) {
-                j2 = __ffs(any) - 1;
+                const int j1 = __ffs(any) - 1;  // -1 when exhausted
                 any &= any - 1;
+                const int32_t w0 = __shfl_sync(kFull, w, j0);
+                const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
+                const uint32_t h0 = __shfl_sync(kFull, hit, j0);
+                uint32_t h1 = __shfl_sync(kFull, hit, j1 & 31);
+                if (j1 < 0) h1 = 0;
+                const double x0 = ldg_if(myval + (size_t)w0 * 32, (h0 >> lane) & 1u);
+                const double x1 = ldg_if(myval + (size_t)w1 * 32, (h1 >> lane) & 1u);
+                acc += x0;  // arc order is kept: j0 < j1
+                acc += x1;
+                got |= h0 | h1;
+                if (COUNT_T) tcount += ((h0 >> lane) & 1u) + ((h1 >> lane) & 1u);
             }
-            if (any) {
-                j3 = __ffs(any) - 1;
-                any &= any - 1;
+        } else {
+            got |= __reduce_or_sync(kFull, hit);
+            uint32_t c = transpose32(hit, lane);  // arcs that hit this lane's BFS instance
+            if (COUNT_T) tcount += __popc(c);
+            while (__any_sync(kFull, c != 0)) {
+                const int j0 = __ffs(c) - 1;
+                const bool p0 = c != 0;
+                c &= c - 1;
+                const int j1 = __ffs(c) - 1;
+                const bool p1 = c != 0;
+                c &= c - 1;
+                const int j2 = __ffs(c) - 1;
+                const bool p2 = c != 0;
+                c &= c - 1;
+                const int j3 = __ffs(c) - 1;
+                const bool p3 = c != 0;
+                c &= c - 1;
+                const int32_t w0 = __shfl_sync(kFull, w, j0 & 31);
+                const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
+                const int32_t w2 = __shfl_sync(kFull, w, j2 & 31);
+                const int32_t w3 = __shfl_sync(kFull, w, j3 & 31);
+                const double x0 = ldg_if(myval + (size_t)w0 * 32, p0);
+                const double x1 = ldg_if(myval + (size_t)w1 * 32, p1);
+                const double x2 = ldg_if(myval + (size_t)w2 * 32, p2);
+                const double x3 = ldg_if(myval + (size_t)w3 * 32, p3);
+                acc += x0;  // ascending arc order within the lane
+                acc += x1;
+                acc += x2;
+                acc += x3;
             }
-            const int32_t w0 = __shfl_sync(kFull, w, j0);
-            const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
-            const int32_t w2 = __shfl_sync(kFull, w, j2 & 31);
-            const int32_t w3 = __shfl_sync(kFull, w, j3 & 31);
-            const uint32_t h0 = __shfl_sync(kFull, hit, j0);
-            uint32_t h1 = __shfl_sync(kFull, hit, j1 & 31);
-            uint32_t h2 = __shfl_sync(kFull, hit, j2 & 31);
-            uint32_t h3 = __shfl_sync(kFull, hit, j3 & 31);
-            if (j1 < 0) h1 = 0;
-            if (j2 < 0) h2 = 0;
-            if (j3 < 0) h3 = 0;
-            double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
-            if ((h0 >> lane) & 1u) x0 = __ldg(val + (size_t)w0 * 32 + lane);
-            if ((h1 >> lane) & 1u) x1 = __ldg(val + (size_t)w1 * 32 + lane);
-            if ((h2 >> lane) & 1u) x2 = __ldg(val + (size_t)w2 * 32 + lane);
-            if ((h3 >> lane) & 1u) x3 = __ldg(val + (size_t)w3 * 32 + lane);
-            acc += x0;  // arc order is kept: j0 < j1 < j2 < j3
-            acc += x1;
-            acc += x2;
-            acc += x3;
-            got |= h0 | h1 | h2 | h3;
-            if (COUNT_T) tcount += __popc(h0) + __popc(h1) + __popc(h2) + __popc(h3);
         }
     }
 }
@@ -168,12 +223,14 @@ __device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, doub
 // One BFS level, forward (discover level L from level L-1) or backward
 // (accumulate level L from level L+1).  grid = (ceil(items / 8), groups).
 template <bool BWD, bool STORE_DELTA>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) level_kernel(const LevelParams p) {
-    if (!BWD && p.prev_any != nullptr && *p.prev_any == 0) return;  // speculative launch past the end
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kernel(const LevelParams p) {
+    const size_t g = blockIdx.y;
+    // forward: instances still expanding; backward: instances present at this level
+    const uint32_t live = p.live_prev[g];
+    if (live == 0) return;  // also covers speculative launches past the last level
     const int lane = threadIdx.x & 31;
     const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (item >= (int64_t)p.n_chk + p.n_rng) return;
-    const size_t g = blockIdx.y;
     uint32_t *vis = p.vis + g * p.n;
     const uint32_t *nbr = p.nbr ? p.nbr + g * p.n : nullptr;
     uint32_t *cur = p.cur + g * p.n;
@@ -182,13 +239,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) level_kernel(const LevelP
     double *delta = STORE_DELTA ? p.delta + g * p.n * 32 : nullptr;
     const double *val = BWD ? coef : sigma;
 
-    unsigned long long c_nr = 0, c_ar = 0, c_t = 0;
+    unsigned long long c_nr = 0, c_ar = 0;
+    unsigned c_t = 0;  // per-lane partial
     uint32_t any_new = 0;
 
     if (item < p.n_chk) {
         // ---- a slice of a hub's adjacency: partial sum into the hub buffers
         const int32_t v = p.chk_v[item];
-        const uint32_t want = BWD ? cur[v] : ~vis[v];
+        const uint32_t want = BWD ? cur[v] : (~vis[v] & live);
         double acc = 0.0;
         uint32_t got = 0;
         if (want != 0 && nbr != nullptr)
@@ -208,7 +266,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) level_kernel(const LevelP
             const int64_t v = (int64_t)v0 + lane;
             b = p.off[v];
             e = p.off[v + 1];
-            mine = BWD ? cur[v] : ~vis[v];
+            mine = BWD ? cur[v] : (~vis[v] & live);
             if (!BWD && (mine == 0 || b == e)) cur[v] = 0;  // nothing to discover here
         }
         unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || e > b));
@@ -226,18 +284,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) level_kernel(const LevelP
                 finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma, coef, delta,
                                                p.bcg + g * p.n, p.accumulate_bc);
             } else {
-                finalize_forward(v, ~want, got, acc, lane, vis, cur, sigma);
+                finalize_forward(v, vis[v], got, acc, lane, vis, cur, sigma);
                 any_new |= got;
                 c_nr += __popc(got);
                 c_ar += (unsigned long long)__popc(got) * (unsigned long long)(ve - vb);
             }
         }
     }
-    if (!BWD && lane == 0) {
-        if (any_new) *(volatile uint32_t *)p.cur_any = 1u;
-        if (c_nr) atomicAdd(p.counters + 0, c_nr);
-        if (c_ar) atomicAdd(p.counters + 1, c_ar);
-        if (c_t) atomicAdd(p.counters + 2, c_t);
+    if (!BWD) {
+        const unsigned t = __reduce_add_sync(kFull, c_t);
+        if (lane == 0) {
+            if (any_new) atomicOr(p.live_cur + g, any_new);
+            if (c_nr) atomicAdd(p.counters + 0, c_nr);
+            if (c_ar) atomicAdd(p.counters + 1, c_ar);
+            if (t) atomicAdd(p.counters + 2, (unsigned long long)t);
+        }
     }
 }
 
@@ -257,8 +318,8 @@ struct HubParams {
     double *bcg;
     const double *pacc;
     const uint32_t *pmask;
-    const uint32_t *prev_any;
-    uint32_t *cur_any;
+    const uint32_t *live_prev;
+    uint32_t *live_cur;
     unsigned long long *counters;
     int accumulate_bc;
 };
@@ -266,15 +327,16 @@ struct HubParams {
 // Adds a hub's chunk partials in chunk order (= arc order) and finalises it.
 template <bool BWD, bool STORE_DELTA>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) hub_kernel(const HubParams p) {
-    if (!BWD && p.prev_any != nullptr && *p.prev_any == 0) return;
+    const size_t g = blockIdx.y;
+    const uint32_t live = p.live_prev[g];
+    if (live == 0) return;
     const int lane = threadIdx.x & 31;
     const int h = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (h >= p.n_hub) return;
-    const size_t g = blockIdx.y;
     const int64_t v = p.hub_v[h];
     uint32_t *vis = p.vis + g * p.n;
     uint32_t *cur = p.cur + g * p.n;
-    const uint32_t want = BWD ? cur[v] : ~vis[v];
+    const uint32_t want = BWD ? cur[v] : (~vis[v] & live);
     if (want == 0) {
         if (!BWD && lane == 0) cur[v] = 0;
         return;
@@ -293,9 +355,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) hub_kernel(const HubParam
                                        STORE_DELTA ? p.delta + g * p.n * 32 : nullptr,
                                        p.bcg + g * p.n, p.accumulate_bc);
     } else {
-        finalize_forward(v, ~want, got, acc, lane, vis, cur, p.sigma + g * p.n * 32);
+        finalize_forward(v, vis[v], got, acc, lane, vis, cur, p.sigma + g * p.n * 32);
         if (lane == 0 && got) {
-            *(volatile uint32_t *)p.cur_any = 1u;
+            atomicOr(p.live_cur + g, got);
             atomicAdd(p.counters + 0, (unsigned long long)__popc(got));
             atomicAdd(p.counters + 1,
                       (unsigned long long)__popc(got) * (unsigned long long)(p.off[v + 1] - p.off[v]));
@@ -319,13 +381,13 @@ __global__ void init_state_kernel(uint32_t *vis, uint32_t *lvl0, int64_t n, int 
 // Sources of the batch become level-0 seeds with one path each (relax.py:62-72
 // for a single seed (s, 0, 1)).
 __global__ void seed_sources_kernel(const int64_t *src, int batch_count, int64_t n, uint32_t *vis,
-                                    uint32_t *lvl0, double *sigma, uint32_t *level_any) {
+                                    uint32_t *lvl0, double *sigma, uint32_t *live0) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= batch_count) return;
-    if (i == 0) level_any[0] = 1u;  // level 0 is never empty
     const size_t g = i >> 5;
     const int lane = i & 31;
     const int64_t v = src[i];
+    atomicOr(live0 + g, 1u << lane);
     atomicOr(vis + g * n + v, 1u << lane);
     atomicOr(lvl0 + g * n + v, 1u << lane);
     sigma[(g * n + v) * 32 + lane] = 1.0;
