@@ -122,6 +122,14 @@ int bc_get_reports(bc_handle *h, int64_t *out, int64_t n_sources);
 int bc_get_border_counts(bc_handle *h, int64_t *counts);
 int bc_get_border_tables(bc_handle *h, int part, int32_t *borders, int32_t *bm, double *sm);
 
+/* Border frontier of the LAST batch of the last BC_MODE_HYBIR call, the
+ * reference's `BorderFrontier` (forward.py:45-48): for each of the first
+ * `n_lanes` sources of that batch, refined distance (BC_UNREACHED = inf), path
+ * count and arrival count of every border, [B][n_lanes] row-major with
+ * borders in part order. */
+int bc_get_border_frontier(bc_handle *h, int64_t n_lanes, int32_t *dist, double *sigma,
+                           double *arrival);
+
 const char *bc_last_error(bc_handle *h);
 void bc_destroy(bc_handle *h);
 

@@ -25,6 +25,7 @@ MODE_DIRECT, MODE_HYBIR, MODE_BSP = 0, 1, 2
 SYMBOLS = (
     "bc_create", "bc_set_option", "bc_set_partition", "bc_run", "bc_run_device",
     "bc_debug_sources", "bc_get_reports", "bc_get_border_counts", "bc_get_border_tables",
+    "bc_get_border_frontier",
     "bc_last_error", "bc_destroy",
 )
 
@@ -79,6 +80,8 @@ def load():
     L.bc_get_border_counts.argtypes = [vp, vp]
     L.bc_get_border_tables.restype = cint
     L.bc_get_border_tables.argtypes = [vp, cint, vp, vp, vp]
+    L.bc_get_border_frontier.restype = cint
+    L.bc_get_border_frontier.argtypes = [vp, i64, vp, vp, vp]
     L.bc_last_error.restype = ctypes.c_char_p
     L.bc_last_error.argtypes = [vp]
     L.bc_destroy.restype = None
@@ -204,3 +207,13 @@ class Engine:
         if rc != BC_OK:
             self._raise(rc)
         return borders, bm, sm
+
+    def border_frontier(self, n_lanes: int, total_borders: int):
+        """(dist, sigma, arrival) of the last hybir batch, each [B, n_lanes]."""
+        d = np.zeros((total_borders, n_lanes), dtype=np.int32)
+        s = np.zeros((total_borders, n_lanes), dtype=np.float64)
+        a = np.zeros((total_borders, n_lanes), dtype=np.float64)
+        rc = self._lib.bc_get_border_frontier(self._h, n_lanes, _ptr(d), _ptr(s), _ptr(a))
+        if rc != BC_OK:
+            self._raise(rc)
+        return d, s, a

@@ -1,0 +1,416 @@
+// bc_border.cuh -- kernels of the partitioned ("hybir") forward phase.
+//
+// Borders of all parts are numbered 0..B-1 part by part (ascending vertex id
+// inside a part, reference pkg/src/hybir/partition.py:148).  Per-batch border
+// state is laid out [border][lane] with S = 32 * groups lanes per row, so a
+// warp touching one border row moves 128 B (int32) or 256 B (fp64) coalesced:
+//   D      int32  border distances being refined (kInf = unreached)
+//   seedD / seedS Step-1 distance / path count at the source-side borders
+//   sig    fp64   path counts at the borders       (forward.py:145-185)
+//   arr    fp64   arrival counts (last arc is a cut arc)
+// Per-part border tables (border_matrix.py:48-67): bm int32 / sm fp64, b_p x b_p
+// row-major, row = from-border, so tab[i][j0..j0+31] is one coalesced read.
+//
+// Reference arithmetic replaced here: _cut_relax / _matrix_relax and the loop
+// of refine_border_distances (forward.py:82-142), _compose_border_sigma
+// (forward.py:145-185, as Jacobi rounds of the same recurrence instead of one
+// ascending-distance sweep: the dependency graph is a DAG ordered by distance,
+// every round settles one more partition crossing, and all values are
+// integers in fp64, so the fixpoint is the sweep's result exactly), and the
+// seed list of Step 6 (forward.py:232-241).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bcb200 {
+
+constexpr int32_t kInf = 0x3fffffff;
+
+struct BorderGeom {
+    int k;                     // parts
+    int B;                     // total borders
+    const int32_t *border_v;   // [B] vertex id
+    const int32_t *border_p;   // [B] part of the border
+    const int32_t *part_off;   // [k+1] first border of each part
+    const int64_t *tab_off;    // [k] offset of the part's b_p x b_p table
+    const int64_t *cin_off;    // [B+1] incoming cut arcs per border
+    const int32_t *cin_src;    // [n_cut] source border of each incoming cut arc
+};
+
+// Which (border, lane) pairs a relaxation step applies to (the reference's
+// two-sided schedule, forward.py:119-129).
+enum Apply : int {
+    kApplyAll = 0,     // every part (k > 2: symmetric schedule)
+    kApplySource = 1,  // borders in the lane's source part
+    kApplyOther = 2    // borders outside the lane's source part
+};
+
+__device__ __forceinline__ bool applies(int which, int part, int source_part) {
+    return which == kApplyAll || (which == kApplySource) == (part == source_part);
+}
+
+// D[j][lane] = kInf, seedS = 0 ... plain fills.
+__global__ void fill_border_kernel(int32_t *D, int32_t *seedD, double *seedS, double *sig,
+                                   double *arr, size_t count) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (size_t)gridDim.x * blockDim.x) {
+        D[i] = kInf;
+        seedD[i] = kInf;
+        seedS[i] = 0.0;
+        sig[i] = 0.0;
+        arr[i] = 0.0;
+    }
+}
+
+// Read (dist, sigma) of every border vertex out of the BFS state: lvl[L][g][v]
+// bit = "lane is at distance L".  One thread per (border, lane).
+// A group whose lanes all died before level L never wrote lvl[L] (the level
+// kernel returns at once), so live[L][g] gates every read of a level row.
+__global__ void border_gather_kernel(const uint32_t *const *lvl, const uint32_t *live, int G,
+                                     int depth, const double *sigma, int64_t n, BorderGeom geo,
+                                     int S, int32_t *D_out, double *S_out) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)geo.B * S) return;
+    const int j = (int)(idx / S), lane_all = (int)(idx % S);
+    const size_t g = lane_all >> 5;
+    const int lane = lane_all & 31;
+    const int64_t v = geo.border_v[j];
+    int32_t d = kInf;
+    for (int L = 0; L < depth; ++L)
+        if (((live[(size_t)L * G + g] >> lane) & 1u) && ((lvl[L][g * n + v] >> lane) & 1u)) {
+            d = L;
+            break;
+        }
+    D_out[idx] = d;
+    if (S_out) S_out[idx] = d < kInf ? sigma[(g * n + v) * 32 + lane] : 0.0;
+}
+
+// Rows of the border tables from a BFS batch whose lanes are borders
+// first..first+count-1 (each BFS ran inside its own part on the cut-free CSR).
+__global__ void border_table_kernel(const uint32_t *const *lvl, const uint32_t *live, int G,
+                                    int depth, const double *sigma, int64_t n, BorderGeom geo,
+                                    int first, int count, int32_t *bm, double *sm) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lanes = (count + 31) / 32 * 32;
+    if (idx >= (size_t)geo.B * lanes) return;
+    const int j = (int)(idx / lanes), lane_all = (int)(idx % lanes);
+    if (lane_all >= count) return;
+    const int i = first + lane_all;          // from-border (BFS source)
+    const int p = geo.border_p[i];
+    if (geo.border_p[j] != p) return;        // tables hold same-part pairs only
+    const size_t g = lane_all >> 5;
+    const int lane = lane_all & 31;
+    const int64_t v = geo.border_v[j];
+    int32_t d = kInf;
+    for (int L = 0; L < depth; ++L)
+        if (((live[(size_t)L * G + g] >> lane) & 1u) && ((lvl[L][g * n + v] >> lane) & 1u)) {
+            d = L;
+            break;
+        }
+    const int b = geo.part_off[p + 1] - geo.part_off[p];
+    const size_t at = (size_t)geo.tab_off[p] + (size_t)(i - geo.part_off[p]) * b + (j - geo.part_off[p]);
+    bm[at] = d;
+    sm[at] = d < kInf ? sigma[(g * n + v) * 32 + lane] : 0.0;
+}
+
+// Step 2 / Step 4 (forward.py:82-88): D[j] = min(D[j], D[i] + 1) over incoming
+// cut arcs (i -> j).  `which` selects destinations by side; sources are always
+// on the other side of a cut arc.  Two-part runs update in place (source and
+// destination sets are disjoint); k > 2 reads `Din` and writes `Dout`.
+__global__ void cut_relax_kernel(BorderGeom geo, int S, const int32_t *Din, int32_t *Dout,
+                                 const int32_t *lane_part, const uint32_t *lane_active, int which,
+                                 uint32_t *lane_changed) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)geo.B * S) return;
+    const int j = (int)(idx / S), lane = (int)(idx % S);
+    const int32_t old = Din[idx];
+    int32_t best = old;
+    if (lane_active[lane] && applies(which, geo.border_p[j], lane_part[lane])) {
+        for (int64_t a = geo.cin_off[j]; a < geo.cin_off[j + 1]; ++a) {
+            const int32_t di = Din[(size_t)geo.cin_src[a] * S + lane];
+            best = min(best, min(di + 1, kInf));
+        }
+    }
+    if (Dout != Din || best != old) Dout[idx] = best;
+    if (best != old && lane_changed) lane_changed[lane] = 1u;
+}
+
+// Step 3 / Step 5 (forward.py:91-96): one Jacobi pass of the min-plus closure
+// Dout[j] = min(Din[j], min_i Din[i] + bm[i][j]) inside each part.  Block =
+// 32 lanes x 8 j-rows, 4 borders j per thread; the i-loop is tiled through
+// shared memory so a bm tile is reused by 32 lanes and a D tile by 32 borders.
+constexpr int kTJ = 32;  // borders j per block
+constexpr int kTI = 32;  // borders i per shared-memory tile
+__global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S,
+                                                           const int32_t *Din, int32_t *Dout,
+                                                           const int32_t *bm,
+                                                           const int32_t *lane_part,
+                                                           const uint32_t *lane_active, int which,
+                                                           uint32_t *lane_changed) {
+    __shared__ int32_t sD[kTI][32];
+    __shared__ int32_t sB[kTI][kTJ + 1];
+    const int p = blockIdx.z;
+    const int b = geo.part_off[p + 1] - geo.part_off[p];
+    const int j0 = blockIdx.x * kTJ;
+    if (j0 >= b) return;
+    const int base = geo.part_off[p];
+    const int32_t *tab = bm + geo.tab_off[p];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int lane = blockIdx.y * 32 + tx;
+    int32_t best[4], old[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int j = j0 + ty + 8 * r;
+        old[r] = j < b ? Din[(size_t)(base + j) * S + lane] : kInf;
+        best[r] = old[r];
+    }
+    for (int i0 = 0; i0 < b; i0 += kTI) {
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = i0 + ty + 8 * r;
+            sD[ty + 8 * r][tx] = i < b ? Din[(size_t)(base + i) * S + lane] : kInf;
+            const int j = j0 + tx;
+            sB[ty + 8 * r][tx] = (i < b && j < b) ? tab[(size_t)i * b + j] : kInf;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int i = 0; i < kTI; ++i) {
+            const int32_t di = sD[i][tx];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) best[r] = min(best[r], di + sB[i][ty + 8 * r]);
+        }
+    }
+    const bool on = lane_active[lane] && applies(which, p, lane_part[lane]);
+    bool changed = false;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int j = j0 + ty + 8 * r;
+        if (j >= b) continue;
+        const int32_t v = on ? min(best[r], kInf) : old[r];
+        Dout[(size_t)(base + j) * S + lane] = v;
+        changed |= v != old[r];
+    }
+    if (changed && lane_changed) lane_changed[lane] = 1u;
+}
+
+// arr[j] = sum of sig[i] over incoming cut arcs (i -> j) that are tight
+// (forward.py:170-174), in arc order.
+__global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const double *sig,
+                               double *arr) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)geo.B * S) return;
+    const int j = (int)(idx / S), lane = (int)(idx % S);
+    const int32_t dj = D[idx];
+    double a = 0.0;
+    if (dj < kInf)
+        for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c) {
+            const size_t at = (size_t)geo.cin_src[c] * S + lane;
+            if (D[at] + 1 == dj) a += sig[at];
+        }
+    arr[idx] = a;
+}
+
+// sig[j] = (seed count if j is on the source side and its Step-1 distance is
+// still optimal) + sum over same-part borders c with arr[c] != 0 and
+// D[c] + bm[c][j] == D[j] of arr[c] * sm[c][j]   (forward.py:176-184).
+__global__ void __launch_bounds__(256) compose_sigma_kernel(
+    BorderGeom geo, int S, const int32_t *D, const int32_t *seedD, const double *seedS,
+    const double *arr, const int32_t *bm, const double *sm, const int32_t *lane_part,
+    double *sig, uint32_t *changed_flag) {
+    __shared__ int32_t sD[kTI][32];
+    __shared__ double sA[kTI][32];
+    __shared__ int32_t sB[kTI][kTJ + 1];
+    __shared__ double sS[kTI][kTJ + 1];
+    const int p = blockIdx.z;
+    const int b = geo.part_off[p + 1] - geo.part_off[p];
+    const int j0 = blockIdx.x * kTJ;
+    if (j0 >= b) return;
+    const int base = geo.part_off[p];
+    const int32_t *tbm = bm + geo.tab_off[p];
+    const double *tsm = sm + geo.tab_off[p];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int lane = blockIdx.y * 32 + tx;
+    int32_t dj[4];
+    double acc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int j = j0 + ty + 8 * r;
+        dj[r] = kInf;
+        acc[r] = 0.0;
+        if (j < b) {
+            const size_t at = (size_t)(base + j) * S + lane;
+            dj[r] = D[at];
+            if (dj[r] < kInf && p == lane_part[lane] && seedD[at] == dj[r]) acc[r] = seedS[at];
+        }
+    }
+    for (int i0 = 0; i0 < b; i0 += kTI) {
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = i0 + ty + 8 * r;
+            const size_t at = (size_t)(base + i) * S + lane;
+            sD[ty + 8 * r][tx] = i < b ? D[at] : kInf;
+            sA[ty + 8 * r][tx] = i < b ? arr[at] : 0.0;
+            const int j = j0 + tx;
+            const bool in = i < b && j < b;
+            sB[ty + 8 * r][tx] = in ? tbm[(size_t)i * b + j] : kInf;
+            sS[ty + 8 * r][tx] = in ? tsm[(size_t)i * b + j] : 0.0;
+        }
+        __syncthreads();
+        for (int i = 0; i < kTI; ++i) {
+            const double a = sA[i][tx];
+            if (a == 0.0) continue;
+            const int32_t dc = sD[i][tx];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (dc + sB[i][ty + 8 * r] == dj[r]) acc[r] += a * sS[i][ty + 8 * r];
+        }
+    }
+    bool changed = false;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int j = j0 + ty + 8 * r;
+        if (j >= b) continue;
+        const size_t at = (size_t)(base + j) * S + lane;
+        const double v = dj[r] < kInf ? acc[r] : 0.0;
+        if (sig[at] != v) {
+            sig[at] = v;
+            changed = true;
+        }
+    }
+    if (changed) *changed_flag = 1u;
+}
+
+// Per-lane bookkeeping of the refinement loop (forward.py:113-135).
+//   enter: a lane runs the loop iff cut arcs exist and Step 1 reached a border
+//   of its source part; after every iteration a lane whose source side did not
+//   change stops (forward.py:128).
+__global__ void lane_enter_kernel(BorderGeom geo, int S, int lanes, const int32_t *D,
+                                  const int32_t *lane_part, uint32_t *lane_active,
+                                  uint32_t *lane_entered, int64_t n_cut) {
+    const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lane >= S) return;
+    uint32_t on = 0;
+    if (lane < lanes && n_cut > 0) {
+        const int p = lane_part[lane];
+        for (int j = geo.part_off[p]; j < geo.part_off[p + 1]; ++j)
+            if (D[(size_t)j * S + lane] < kInf) {
+                on = 1;
+                break;
+            }
+    }
+    lane_active[lane] = on;
+    lane_entered[lane] = on;
+}
+
+__global__ void lane_step_kernel(int S, uint32_t *lane_active, uint32_t *lane_changed,
+                                 int32_t *lane_iters, uint32_t *any_active) {
+    const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lane >= S) return;
+    if (lane_active[lane]) {
+        lane_iters[lane] += 1;
+        if (!lane_changed[lane]) lane_active[lane] = 0;
+        else *any_active = 1u;
+    }
+    lane_changed[lane] = 0;
+}
+
+// Largest finite border distance that carries an arrival count: Step 6 must
+// keep stepping levels at least that far even through empty frontiers.
+__global__ void max_seed_level_kernel(const int32_t *D, const double *arr, size_t count,
+                                      int *out) {
+    int m = -1;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (size_t)gridDim.x * blockDim.x)
+        if (D[i] < kInf && arr[i] != 0.0) m = max(m, D[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(out, m);
+}
+
+// Step 6 seeds (forward.py:232-241): border j joins level D[j] with base count
+// arr[j] when D[j] is finite and arr[j] != 0.  Runs after the pull of level L:
+// a border the pull just discovered at L keeps its pulled count and adds the
+// base (relax.py:70-71,95-99); one found at a smaller level ignores the seed.
+__global__ void inject_seeds_kernel(BorderGeom geo, int S, int lanes, const int32_t *D,
+                                    const double *arr, int level, int64_t n, uint32_t *vis,
+                                    uint32_t *cur, double *sigma, uint32_t *live_cur) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)geo.B * S) return;
+    const int lane_all = (int)(idx % S);
+    if (lane_all >= lanes || D[idx] != level) return;
+    const double base = arr[idx];
+    if (base == 0.0) return;
+    const int j = (int)(idx / S);
+    const size_t g = lane_all >> 5;
+    const uint32_t bit = 1u << (lane_all & 31);
+    const int64_t v = geo.border_v[j];
+    const size_t at = (g * n + v) * 32 + (lane_all & 31);
+    if (cur[g * n + v] & bit) {
+        sigma[at] += base;                 // reached through an arc at the same level
+    } else if (!(vis[g * n + v] & bit)) {
+        atomicOr(vis + g * n + v, bit);    // other lanes of the word may be seeded concurrently
+        atomicOr(cur + g * n + v, bit);
+        sigma[at] = base;
+        atomicOr(live_cur + g, bit);
+    }
+}
+
+// presence[(L * k + part) * G + g] |= lanes of group g that have a vertex of
+// `part` at level L -- the raw material of max_level / levels in the reports
+// (forward.py:52-64, backward.py:33-43).
+__global__ void level_presence_kernel(const uint32_t *lvl, const uint32_t *live_level,
+                                      const int32_t *part, int64_t n, int k, int G,
+                                      uint32_t *presence_level) {
+    extern __shared__ uint32_t sp[];  // [k]
+    const size_t g = blockIdx.y;
+    if (live_level[g] == 0) return;  // the level row of a dead group was never written
+    for (int i = threadIdx.x; i < k; i += blockDim.x) sp[i] = 0;
+    __syncthreads();
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = lvl[g * n + v];
+        if (m) atomicOr(&sp[part[v]], m);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        if (sp[i]) atomicOr(&presence_level[(size_t)i * G + g], sp[i]);
+}
+
+// Backward sync accounting for two parts (backward.py:46-56,121-139): border j
+// is pulled across the cut iff some incoming cut arc is tight.  flag[j][lane]
+// marks those; level_bits[(side * W + L / 32) * S + lane] collects the distinct
+// producer levels per consumer side.
+__global__ void sync_mark_kernel(BorderGeom geo, int S, const int32_t *Dfin, uint32_t *flag,
+                                 uint32_t *level_bits, int W) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)geo.B * S) return;
+    const int j = (int)(idx / S), lane = (int)(idx % S);
+    const int32_t dj = Dfin[idx];
+    uint32_t f = 0;
+    if (dj < kInf)
+        for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c)
+            if (Dfin[(size_t)geo.cin_src[c] * S + lane] + 1 == dj) {
+                f = 1;
+                break;
+            }
+    flag[idx] = f;
+    if (f) {
+        const int consumer = 1 - geo.border_p[j];  // two parts: the other side pulls
+        atomicOr(&level_bits[((size_t)consumer * W + (dj >> 5)) * S + lane], 1u << (dj & 31));
+    }
+}
+
+__global__ void sync_count_kernel(int B, int S, int W, const uint32_t *flag,
+                                  const uint32_t *level_bits, int64_t *sync_events,
+                                  int64_t *comm_bytes) {
+    const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lane >= S) return;
+    int64_t children = 0, events = 0;
+    for (int j = 0; j < B; ++j) children += flag[(size_t)j * S + lane];
+    for (int w = 0; w < 2 * W; ++w) events += __popc(level_bits[(size_t)w * S + lane]);
+    sync_events[lane] = events;
+    comm_bytes[lane] = 16 * children;
+}
+
+}  // namespace bcb200

@@ -1,11 +1,13 @@
 // bc_engine.cu -- host side of the C ABI declared in include/bc_b200.h.
 //
 // One handle = one CUDA device = one host thread.  The handle owns the CSR on
-// the device, the warp work items derived from it and the per-batch state;
-// sources are processed in batches of 32 * groups lanes.  There is no CPU
-// code path for the arithmetic: every bc_run* call launches the kernels of
-// bc_kernels.cuh or fails.
+// the device, the warp work items derived from it, the partition data (cut-free
+// CSR, border lists, border tables) and the per-batch state; sources are
+// processed in batches of 32 * groups lanes.  There is no CPU code path for
+// the arithmetic: every bc_run* call launches the kernels of bc_kernels.cuh /
+// bc_border.cuh or fails.
 #include "bc_b200.h"
+#include "bc_border.cuh"
 #include "bc_kernels.cuh"
 
 #include <algorithm>
@@ -25,7 +27,6 @@ struct Csr {
     int64_t n = 0, n_arcs = 0;
     int64_t *off = nullptr;
     int32_t *col = nullptr;
-    bool owns_graph = false;
     int n_chk = 0, n_rng = 0, n_hub = 0;
     int32_t *chk_v = nullptr;
     int64_t *chk_a0 = nullptr, *chk_a1 = nullptr;
@@ -34,21 +35,56 @@ struct Csr {
 };
 
 struct Events {
-    cudaEvent_t start, fwd_end, bwd_end;
+    cudaEvent_t start, fwd_end, border_end, fwd2_end, bwd_end;
 };
+
+// Border-table feasibility: b_p^2 entries of 12 B per part.
+constexpr double kMaxTableBytes = 64e9;
 
 }  // namespace
 
 struct bc_handle {
     int device = 0;
     int64_t n = 0, n_arcs = 0;
-    std::vector<int64_t> h_off;  // host copy of offsets (item building, partition set-up)
+    std::vector<int64_t> h_off;   // host copies (item building, partition set-up)
+    std::vector<int32_t> h_col;
     Csr full;
     // options
     int groups = 4;
     int item_arcs = 512;
     int reports = 1;
-    // per-batch state
+    // ---- partition ------------------------------------------------------
+    int k = 1;
+    std::vector<int32_t> h_part;
+    int32_t *d_part = nullptr;
+    Csr intra;                     // cut arcs removed
+    int B = 0;                     // borders over all parts
+    int64_t n_cut = 0;
+    std::vector<int32_t> h_border_v, h_border_p, h_part_off;
+    std::vector<int64_t> h_tab_off;
+    int64_t tab_total = 0;
+    int32_t *d_border_v = nullptr, *d_border_p = nullptr, *d_part_off = nullptr, *d_cin_src = nullptr;
+    int64_t *d_tab_off = nullptr, *d_cin_off = nullptr;
+    int32_t *bm = nullptr;         // border distance tables
+    double *sm = nullptr;          // border path-count tables
+    bool tables_ready = false;
+    // per-batch border state, [B][S]
+    int border_S = 0;
+    int32_t *D = nullptr, *D2 = nullptr, *seedD = nullptr, *Dfin = nullptr;
+    double *seedS = nullptr, *sig = nullptr, *arr = nullptr;
+    int32_t *lane_part = nullptr, *lane_iters = nullptr;
+    uint32_t *lane_active = nullptr, *lane_entered = nullptr, *lane_changed = nullptr;
+    uint32_t *dflags = nullptr;    // [0] any lane active, [1] sigma changed
+    int *d_maxlvl = nullptr;
+    uint32_t *sync_flag = nullptr, *sync_bits = nullptr;
+    int64_t *lane_sync = nullptr, *lane_bytes = nullptr;
+    size_t sync_bits_words = 0;
+    const uint32_t **d_lvl_ptrs = nullptr;
+    int lvl_ptrs_cap = 0;
+    uint32_t *presence = nullptr;
+    size_t presence_words = 0;
+    std::vector<int64_t> reports_host;  // 8 per source of the last run
+    // ---- per-batch BFS state ------------------------------------------------
     int alloc_groups = 0;
     uint32_t *vis = nullptr;
     std::vector<uint32_t *> lvl;
@@ -60,6 +96,7 @@ struct bc_handle {
     uint32_t *live = nullptr;  // [level][alloc_groups] lanes with a non-empty frontier
     int live_cap = 0;          // levels
     unsigned long long *counters = nullptr;
+    int cnt_off = 0;  // 0: traversal counters of the result; 4: scratch (Step 1 of hybir mode)
     int64_t *d_src = nullptr;
     int64_t d_src_cap = 0;
     double *bc_scratch = nullptr;  // device bc vector of bc_run
@@ -83,10 +120,17 @@ struct bc_handle {
         }                                                                                  \
     } while (0)
 
+#define TRY(expr)                 \
+    do {                          \
+        int rc_ = (expr);         \
+        if (rc_) return rc_;      \
+    } while (0)
+
 namespace {
 
 template <typename T>
 int upload(bc_handle *h, T **dst, const std::vector<T> &src) {
+    cudaFree(*dst);
     *dst = nullptr;
     if (src.empty()) return BC_OK;
     CUDA_TRY(h, cudaMalloc((void **)dst, src.size() * sizeof(T)));
@@ -94,14 +138,27 @@ int upload(bc_handle *h, T **dst, const std::vector<T> &src) {
     return BC_OK;
 }
 
-void free_csr(Csr &c) {
-    if (c.owns_graph) {
-        cudaFree(c.off);
-        cudaFree(c.col);
-    }
+template <typename T>
+int dev_alloc(bc_handle *h, T **dst, size_t count) {
+    cudaFree(*dst);
+    *dst = nullptr;
+    CUDA_TRY(h, cudaMalloc((void **)dst, std::max<size_t>(count, 1) * sizeof(T)));
+    return BC_OK;
+}
+
+void free_items(Csr &c) {
     cudaFree(c.chk_v), cudaFree(c.chk_a0), cudaFree(c.chk_a1);
     cudaFree(c.rng_v0), cudaFree(c.rng_nv);
     cudaFree(c.hub_v), cudaFree(c.hub_c0), cudaFree(c.hub_nc);
+    c.chk_v = c.rng_v0 = c.rng_nv = c.hub_v = c.hub_c0 = c.hub_nc = nullptr;
+    c.chk_a0 = c.chk_a1 = nullptr;
+    c.n_chk = c.n_rng = c.n_hub = 0;
+}
+
+void free_csr(Csr &c) {
+    cudaFree(c.off);
+    cudaFree(c.col);
+    free_items(c);
     c = Csr();
 }
 
@@ -146,18 +203,18 @@ int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
         run_arcs += deg;
     }
     flush();
+    free_items(c);
     c.n_chk = (int)chk_v.size();
     c.n_rng = (int)rng_v0.size();
     c.n_hub = (int)hub_v.size();
-    int rc;
-    if ((rc = upload(h, &c.chk_v, chk_v))) return rc;
-    if ((rc = upload(h, &c.chk_a0, chk_a0))) return rc;
-    if ((rc = upload(h, &c.chk_a1, chk_a1))) return rc;
-    if ((rc = upload(h, &c.rng_v0, rng_v0))) return rc;
-    if ((rc = upload(h, &c.rng_nv, rng_nv))) return rc;
-    if ((rc = upload(h, &c.hub_v, hub_v))) return rc;
-    if ((rc = upload(h, &c.hub_c0, hub_c0))) return rc;
-    if ((rc = upload(h, &c.hub_nc, hub_nc))) return rc;
+    TRY(upload(h, &c.chk_v, chk_v));
+    TRY(upload(h, &c.chk_a0, chk_a0));
+    TRY(upload(h, &c.chk_a1, chk_a1));
+    TRY(upload(h, &c.rng_v0, rng_v0));
+    TRY(upload(h, &c.rng_nv, rng_nv));
+    TRY(upload(h, &c.hub_v, hub_v));
+    TRY(upload(h, &c.hub_c0, hub_c0));
+    TRY(upload(h, &c.hub_nc, hub_nc));
     return BC_OK;
 }
 
@@ -177,8 +234,39 @@ void free_state(bc_handle *h) {
     h->pacc_chunks = 0;
 }
 
-int ensure_state(bc_handle *h, int groups, int n_chk, bool want_delta) {
+void free_border_state(bc_handle *h) {
+    cudaFree(h->D), cudaFree(h->D2), cudaFree(h->seedD), cudaFree(h->Dfin);
+    cudaFree(h->seedS), cudaFree(h->sig), cudaFree(h->arr);
+    cudaFree(h->lane_part), cudaFree(h->lane_iters), cudaFree(h->lane_active);
+    cudaFree(h->lane_entered), cudaFree(h->lane_changed);
+    cudaFree(h->sync_flag), cudaFree(h->sync_bits), cudaFree(h->lane_sync), cudaFree(h->lane_bytes);
+    h->D = h->D2 = h->seedD = h->Dfin = h->lane_part = h->lane_iters = nullptr;
+    h->seedS = h->sig = h->arr = nullptr;
+    h->lane_active = h->lane_entered = h->lane_changed = h->sync_flag = h->sync_bits = nullptr;
+    h->lane_sync = h->lane_bytes = nullptr;
+    h->border_S = 0;
+    h->sync_bits_words = 0;
+}
+
+void free_partition(bc_handle *h) {
+    free_csr(h->intra);
+    free_border_state(h);
+    cudaFree(h->d_part), cudaFree(h->d_border_v), cudaFree(h->d_border_p), cudaFree(h->d_part_off);
+    cudaFree(h->d_cin_src), cudaFree(h->d_tab_off), cudaFree(h->d_cin_off);
+    cudaFree(h->bm), cudaFree(h->sm);
+    h->d_part = h->d_border_v = h->d_border_p = h->d_part_off = h->d_cin_src = nullptr;
+    h->d_tab_off = h->d_cin_off = nullptr;
+    h->bm = nullptr;
+    h->sm = nullptr;
+    h->tables_ready = false;
+    h->k = 1;
+    h->B = 0;
+    h->n_cut = 0;
+}
+
+int ensure_state(bc_handle *h, int groups, bool want_delta) {
     const size_t n = (size_t)h->n;
+    const int n_chk = std::max(h->full.n_chk, h->intra.n_chk);
     if (h->alloc_groups < groups) {
         free_state(h);
         CUDA_TRY(h, cudaMalloc((void **)&h->vis, groups * n * sizeof(uint32_t)));
@@ -198,9 +286,10 @@ int ensure_state(bc_handle *h, int groups, int n_chk, bool want_delta) {
         CUDA_TRY(h, cudaMalloc((void **)&h->pmask, slots * sizeof(uint32_t)));
         h->pacc_chunks = n_chk;
     }
-    if (h->counters == nullptr) {
+    if (h->counters == nullptr)
         CUDA_TRY(h, cudaMalloc((void **)&h->counters, 8 * sizeof(unsigned long long)));
-    }
+    if (h->dflags == nullptr) CUDA_TRY(h, cudaMalloc((void **)&h->dflags, 4 * sizeof(uint32_t)));
+    if (h->d_maxlvl == nullptr) CUDA_TRY(h, cudaMalloc((void **)&h->d_maxlvl, sizeof(int)));
     return BC_OK;
 }
 
@@ -228,6 +317,20 @@ int ensure_levels(bc_handle *h, int count) {
     return BC_OK;
 }
 
+// Device table of the level-mask pointers (the border gathers walk levels).
+int upload_level_ptrs(bc_handle *h, int depth, cudaStream_t st) {
+    if (h->lvl_ptrs_cap < depth) {
+        cudaFree((void *)h->d_lvl_ptrs);
+        h->d_lvl_ptrs = nullptr;
+        const int cap = std::max(depth, 2 * h->lvl_ptrs_cap);
+        CUDA_TRY(h, cudaMalloc((void **)&h->d_lvl_ptrs, cap * sizeof(uint32_t *)));
+        h->lvl_ptrs_cap = cap;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync((void *)h->d_lvl_ptrs, h->lvl.data(), depth * sizeof(uint32_t *),
+                                cudaMemcpyHostToDevice, st));
+    return BC_OK;
+}
+
 LevelParams level_params(bc_handle *h, const Csr &c) {
     LevelParams p{};
     p.off = c.off;
@@ -247,7 +350,7 @@ LevelParams level_params(bc_handle *h, const Csr &c) {
     p.bcg = h->bcg;
     p.pacc = h->pacc;
     p.pmask = h->pmask;
-    p.counters = h->counters;
+    p.counters = h->counters + h->cnt_off;
     return p;
 }
 
@@ -267,12 +370,29 @@ HubParams hub_params(bc_handle *h, const Csr &c) {
     p.bcg = h->bcg;
     p.pacc = h->pacc;
     p.pmask = h->pmask;
-    p.counters = h->counters;
+    p.counters = h->counters + h->cnt_off;
     return p;
+}
+
+BorderGeom border_geom(bc_handle *h) {
+    BorderGeom g{};
+    g.k = h->k;
+    g.B = h->B;
+    g.border_v = h->d_border_v;
+    g.border_p = h->d_border_p;
+    g.part_off = h->d_part_off;
+    g.tab_off = h->d_tab_off;
+    g.cin_off = h->d_cin_off;
+    g.cin_src = h->d_cin_src;
+    return g;
 }
 
 inline unsigned blocks_for(int64_t items) {
     return (unsigned)((items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+}
+
+inline unsigned grid1d(size_t count, int block = 256, size_t cap = 1u << 30) {
+    return (unsigned)std::max<size_t>(1, std::min<size_t>((count + block - 1) / block, cap));
 }
 
 // Forward level L on graph c for `ng` groups.
@@ -327,32 +447,60 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     return BC_OK;
 }
 
-// Forward sweep from the level-0 seeds already in lvl[0]; returns the number
-// of non-empty levels.  Levels are launched speculatively in growing chunks
-// (a launch past the last level returns at once) so deep graphs do not pay a
-// host round trip per level.
-int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *depth_out) {
-    int L = 1, chunk = 4;
+// Reset the BFS state of a batch and plant the level-0 seeds (sigma = 1).
+int begin_batch(bc_handle *h, const int64_t *src_dev, int cnt, int ng, cudaStream_t st) {
+    const int64_t n = h->n;
+    CUDA_TRY(h, cudaMemsetAsync(h->live, 0, (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
+    init_state_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vis, h->lvl[0], n, cnt);
+    seed_sources_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(src_dev, cnt, n, h->vis, h->lvl[0],
+                                                          h->sigma, h->live);
+    h->launches += 2;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+// Forward sweep from the level-0 seeds already in lvl[0]; *depth_out = number
+// of levels up to the last non-empty one.  Levels are launched speculatively
+// in growing chunks (a launch past the last level returns at once) so deep
+// graphs do not pay a host round trip per level.
+// Seeded mode (Step 6 of the partitioned forward phase): border seeds join at
+// their own level after the pull of that level, and stepping continues through
+// empty frontiers up to the largest seed level.
+int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *depth_out,
+                  bool seeded = false, int lanes = 0, int max_seed_level = -1) {
+    int L = 1, chunk = 4, last_alive = 0;
     std::vector<uint32_t> flags;
+    const size_t G = (size_t)h->alloc_groups;
+    const size_t lvl_bytes = G * (size_t)h->n * sizeof(uint32_t);
     for (;;) {
-        int rc = ensure_levels(h, L + chunk);
-        if (rc) return rc;
-        for (int j = 0; j < chunk; ++j)
-            if ((rc = launch_forward(h, c, L + j, ng, st))) return rc;
-        const size_t G = (size_t)h->alloc_groups;
+        TRY(ensure_levels(h, L + chunk));
+        for (int j = 0; j < chunk; ++j) {
+            if (seeded) CUDA_TRY(h, cudaMemsetAsync(h->lvl[L + j], 0, lvl_bytes, st));
+            TRY(launch_forward(h, c, L + j, ng, st));
+            if (seeded && L + j <= max_seed_level) {
+                const size_t cnt = (size_t)h->B * h->border_S;
+                inject_seeds_kernel<<<grid1d(cnt), 256, 0, st>>>(
+                    border_geom(h), h->border_S, lanes, h->D, h->arr, L + j, h->n, h->vis,
+                    h->lvl[L + j], h->sigma, h->live + (size_t)(L + j) * G);
+                ++h->launches;
+            }
+        }
         flags.assign(chunk * G, 0);
         CUDA_TRY(h, cudaMemcpyAsync(flags.data(), h->live + (size_t)L * G,
                                     chunk * G * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(h, cudaStreamSynchronize(st));
-        auto level_alive = [&](int j) {
-            for (int g = 0; g < ng; ++g)
-                if (flags[(size_t)j * G + g]) return true;
-            return false;
-        };
-        int j = 0;
-        while (j < chunk && level_alive(j)) ++j;
-        if (j < chunk) {
-            *depth_out = L + j;
+        bool stop = false;
+        for (int j = 0; j < chunk; ++j) {
+            bool alive = false;
+            for (int g = 0; g < ng; ++g) alive |= flags[(size_t)j * G + g] != 0;
+            if (alive) last_alive = L + j;
+            else if (L + j > max_seed_level) {
+                stop = true;
+                break;
+            }
+        }
+        if (stop) {
+            *depth_out = last_alive + 1;
             return BC_OK;
         }
         L += chunk;
@@ -360,32 +508,237 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
     }
 }
 
-int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev, cudaStream_t st,
-                bc_stats *stats, bool debug, int32_t *dist_out, double *sigma_out,
+int backward_sweep(bc_handle *h, const Csr &c, int depth, int ng, bool debug, cudaStream_t st) {
+    // Level 0 holds only the sources; their delta is excluded from BC
+    // (engine.py:147-148), so it is computed only for inspection.
+    const int last = debug ? 0 : 1;
+    for (int L = depth - 1; L >= last; --L)
+        TRY(launch_backward(h, c, L, L == depth - 1, ng, debug, !debug, st));
+    return BC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// partitioned forward phase
+// ------------------------------------------------------------------------------------
+
+int ensure_border_state(bc_handle *h, int S) {
+    if (h->border_S >= S && h->D != nullptr) return BC_OK;
+    free_border_state(h);
+    const size_t cnt = (size_t)std::max(h->B, 1) * S;
+    TRY(dev_alloc(h, &h->D, cnt));
+    TRY(dev_alloc(h, &h->D2, cnt));
+    TRY(dev_alloc(h, &h->seedD, cnt));
+    TRY(dev_alloc(h, &h->Dfin, cnt));
+    TRY(dev_alloc(h, &h->seedS, cnt));
+    TRY(dev_alloc(h, &h->sig, cnt));
+    TRY(dev_alloc(h, &h->arr, cnt));
+    TRY(dev_alloc(h, &h->sync_flag, cnt));
+    TRY(dev_alloc(h, &h->lane_part, (size_t)S));
+    TRY(dev_alloc(h, &h->lane_iters, (size_t)S));
+    TRY(dev_alloc(h, &h->lane_active, (size_t)S));
+    TRY(dev_alloc(h, &h->lane_entered, (size_t)S));
+    TRY(dev_alloc(h, &h->lane_changed, (size_t)S));
+    TRY(dev_alloc(h, &h->lane_sync, (size_t)S));
+    TRY(dev_alloc(h, &h->lane_bytes, (size_t)S));
+    h->border_S = S;
+    return BC_OK;
+}
+
+// Steps 2-5 of the reference (forward.py:99-142) for every lane of the batch,
+// then the path-count composition.  `lanes` real lanes, S allocated lanes.
+int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
+                       std::vector<int32_t> *iters_out, std::vector<uint32_t> *entered_out,
+                       int *max_seed_level) {
+    const int S = h->border_S;
+    const BorderGeom geo = border_geom(h);
+    const size_t cnt = (size_t)h->B * S;
+    const unsigned gb = grid1d(cnt);
+    const unsigned gl = grid1d((size_t)S, 128);
+    int max_b = 0;
+    for (int p = 0; p < h->k; ++p) max_b = std::max(max_b, h->h_part_off[p + 1] - h->h_part_off[p]);
+    (void)ng;
+    const dim3 mgrid((max_b + kTJ - 1) / kTJ, S / 32, h->k);  // every allocated lane is kept defined
+
+    CUDA_TRY(h, cudaMemcpyAsync(h->D, h->seedD, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->lane_iters, 0, S * sizeof(int32_t), st));
+    CUDA_TRY(h, cudaMemsetAsync(h->lane_changed, 0, S * sizeof(uint32_t), st));
+    lane_enter_kernel<<<gl, 128, 0, st>>>(geo, S, lanes, h->D, h->lane_part, h->lane_active,
+                                          h->lane_entered, h->n_cut);
+    ++h->launches;
+    if (h->B > 0 && h->n_cut > 0) {
+        const int max_iter = max_b + 2;
+        for (int it = 0;; ++it) {
+            if (it > max_iter)
+                return h->fail(BC_ERR_INTERNAL, "border refinement exceeded the border-count bound");
+            if (h->k == 2) {
+                cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_active,
+                                                     kApplyOther, nullptr);
+                matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part,
+                                                           h->lane_active, kApplyOther, nullptr);
+                std::swap(h->D, h->D2);
+                cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_active,
+                                                     kApplySource, h->lane_changed);
+                matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part,
+                                                           h->lane_active, kApplySource,
+                                                           h->lane_changed);
+                std::swap(h->D, h->D2);
+                h->launches += 4;
+            } else {
+                cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D2, h->lane_part, h->lane_active,
+                                                     kApplyAll, h->lane_changed);
+                std::swap(h->D, h->D2);
+                matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part,
+                                                           h->lane_active, kApplyAll, h->lane_changed);
+                std::swap(h->D, h->D2);
+                h->launches += 2;
+            }
+            CUDA_TRY(h, cudaMemsetAsync(h->dflags, 0, 4 * sizeof(uint32_t), st));
+            lane_step_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->lane_iters,
+                                                 h->dflags);
+            ++h->launches;
+            uint32_t any = 0;
+            CUDA_TRY(h, cudaMemcpyAsync(&any, h->dflags, sizeof any, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            if (!any) break;
+        }
+        if (h->k == 2) {
+            // 'step2-final' (forward.py:134-135) for every lane that ran the loop
+            cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_entered,
+                                                 kApplyOther, nullptr);
+            ++h->launches;
+        }
+    }
+    // path counts at the borders: Jacobi rounds until nothing changes
+    CUDA_TRY(h, cudaMemsetAsync(h->sig, 0, cnt * sizeof(double), st));
+    if (h->B > 0) {
+        for (int round = 0;; ++round) {
+            if (round > 2 * h->B + 4)
+                return h->fail(BC_ERR_INTERNAL, "border sigma composition did not settle");
+            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr);
+            CUDA_TRY(h, cudaMemsetAsync(h->dflags + 1, 0, sizeof(uint32_t), st));
+            compose_sigma_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->seedD, h->seedS, h->arr,
+                                                        h->bm, h->sm, h->lane_part, h->sig,
+                                                        h->dflags + 1);
+            h->launches += 2;
+            uint32_t changed = 0;
+            CUDA_TRY(h, cudaMemcpyAsync(&changed, h->dflags + 1, sizeof changed,
+                                        cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            if (!changed) break;
+        }
+    }
+    int m = -1;
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_maxlvl, &m, sizeof m, cudaMemcpyHostToDevice, st));
+    if (h->B > 0) {
+        max_seed_level_kernel<<<grid1d(cnt, 256, 1184), 256, 0, st>>>(h->D, h->arr, cnt, h->d_maxlvl);
+        ++h->launches;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(&m, h->d_maxlvl, sizeof m, cudaMemcpyDeviceToHost, st));
+    if (iters_out) {
+        iters_out->assign(S, 0);
+        entered_out->assign(S, 0);
+        CUDA_TRY(h, cudaMemcpyAsync(iters_out->data(), h->lane_iters, S * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaMemcpyAsync(entered_out->data(), h->lane_entered, S * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    CUDA_TRY(h, cudaGetLastError());
+    *max_seed_level = m;
+    return BC_OK;
+}
+
+// Border tables (border_matrix.py:48-67): one BFS per border inside its part
+// (cut-free CSR), batched 32 * groups borders at a time.
+int build_border_tables(bc_handle *h) {
+    if (h->tables_ready) return BC_OK;
+    cudaStream_t st = nullptr;
+    double bytes = 0;
+    for (int p = 0; p < h->k; ++p) {
+        const double b = h->h_part_off[p + 1] - h->h_part_off[p];
+        bytes += 12.0 * b * b;
+    }
+    if (bytes > kMaxTableBytes) {
+        char buf[256];
+        snprintf(buf, sizeof buf,
+                 "border tables need %.1f GB (sum of b_p^2 x 12 B); use mode 'bsp-baseline' for "
+                 "this partition", bytes / 1e9);
+        return h->fail(BC_ERR_INPUT, buf);
+    }
+    TRY(dev_alloc(h, &h->bm, (size_t)h->tab_total));
+    TRY(dev_alloc(h, &h->sm, (size_t)h->tab_total));
+    if (h->B == 0) {
+        h->tables_ready = true;
+        return BC_OK;
+    }
+    const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(h->groups, (h->B + 31) / 32));
+    TRY(ensure_state(h, groups, false));
+    TRY(ensure_levels(h, 2));
+    std::vector<int64_t> src(h->h_border_v.begin(), h->h_border_v.end());
+    int64_t *d_borders = nullptr;
+    TRY(upload(h, &d_borders, src));
+    const int per = 32 * groups;
+    const BorderGeom geo = border_geom(h);
+    for (int first = 0; first < h->B; first += per) {
+        const int cnt = std::min(per, h->B - first);
+        const int ng = (cnt + 31) / 32;
+        TRY(begin_batch(h, d_borders + first, cnt, ng, st));
+        int depth = 1;
+        TRY(forward_sweep(h, h->intra, ng, st, &depth));
+        TRY(upload_level_ptrs(h, depth, st));
+        const size_t work = (size_t)h->B * ((cnt + 31) / 32 * 32);
+        border_table_kernel<<<grid1d(work), 256, 0, st>>>(h->d_lvl_ptrs, h->live, h->alloc_groups,
+                                                          depth, h->sigma, h->n, geo, first, cnt,
+                                                          h->bm, h->sm);
+        ++h->launches;
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    cudaFree(d_borders);
+    h->tables_ready = true;
+    return BC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// the source loop
+// ------------------------------------------------------------------------------------
+
+int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all, double *bc_dev,
+                cudaStream_t st, bc_stats *stats, bool debug, int32_t *dist_out, double *sigma_out,
                 double *delta_out) {
-    const Csr &c = h->full;
     const int64_t n = h->n;
-    for (int64_t i = 0; i < k; ++i)
-        if (sources[i] < 0 || sources[i] >= n) {
+    for (int64_t i = 0; i < k_all; ++i)
+        if (sources_in[i] < 0 || sources_in[i] >= n) {
             char buf[128];
             snprintf(buf, sizeof buf, "listed source %lld out of range [0, %lld)",
-                     (long long)sources[i], (long long)n);
+                     (long long)sources_in[i], (long long)n);
             return h->fail(BC_ERR_INPUT, buf);
         }
+    if (mode != BC_MODE_DIRECT && h->k == 1) mode = BC_MODE_DIRECT;  // one part: no borders
+    const bool hybir = mode == BC_MODE_HYBIR;
+    const bool want_reports = h->reports && mode != BC_MODE_DIRECT;
+    if (hybir) TRY(build_border_tables(h));
+
     // Sources without arcs reach nothing: sigma = 1 at the source, delta = 0
-    // everywhere.  They stay in the result (and in the counters) but take no
-    // lane on the device.  The inspection path keeps them so rows line up.
+    // everywhere.  In direct mode they stay in the result (and the counters)
+    // but take no lane on the device.  The inspection path and the partitioned
+    // modes keep them so rows and per-source reports line up.
     std::vector<int64_t> active;
-    active.reserve((size_t)k);
-    for (int64_t i = 0; i < k; ++i)
-        if (debug || h->h_off[sources[i] + 1] > h->h_off[sources[i]]) active.push_back(sources[i]);
-    const int64_t k_all = k;
-    k = (int64_t)active.size();
-    sources = active.data();
+    std::vector<int64_t> where;  // index in the caller's list
+    active.reserve((size_t)k_all);
+    for (int64_t i = 0; i < k_all; ++i)
+        if (debug || mode != BC_MODE_DIRECT ||
+            h->h_off[sources_in[i] + 1] > h->h_off[sources_in[i]]) {
+            active.push_back(sources_in[i]);
+            where.push_back(i);
+        }
+    const int64_t k = (int64_t)active.size();
+    const int64_t *sources = active.data();
     const int groups = debug ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(h->groups, (k + 31) / 32));
-    int rc = ensure_state(h, groups, c.n_chk, debug);
-    if (rc) return rc;
-    if ((rc = ensure_levels(h, 2))) return rc;
+    TRY(ensure_state(h, groups, debug));
+    TRY(ensure_levels(h, 2));
+    const int S = 32 * groups;
+    if (hybir) TRY(ensure_border_state(h, S));
     if (h->d_src_cap < k) {
         cudaFree(h->d_src);
         h->d_src = nullptr;
@@ -399,11 +752,14 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
         h2d += k * sizeof(int64_t);
     }
     CUDA_TRY(h, cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned long long), st));
+    h->reports_host.assign((size_t)k_all * 8, 0);
 
-    const int lanes_per_batch = 32 * groups;
+    const int lanes_per_batch = S;
     const int64_t n_batches = (k + lanes_per_batch - 1) / lanes_per_batch;
     std::vector<Events> ev((size_t)n_batches);
     int max_depth = 0;
+    int64_t tot_iters = 0, tot_comm = 0, tot_sync = 0, tot_bytes = 0;
+    const Csr &fwd_csr = hybir ? h->intra : h->full;
 
     // debug staging: one batch (<= 32 sources) of [lane][n] rows
     int32_t *dbg_dist = nullptr;
@@ -417,42 +773,159 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
     for (int64_t b = 0; b < n_batches; ++b) {
         const int cnt = (int)std::min<int64_t>(lanes_per_batch, k - b * lanes_per_batch);
         const int ng = (cnt + 31) / 32;
+        const int64_t *batch_src = sources + b * lanes_per_batch;
         Events &e = ev[(size_t)b];
         CUDA_TRY(h, cudaEventCreate(&e.start));
         CUDA_TRY(h, cudaEventCreate(&e.fwd_end));
+        CUDA_TRY(h, cudaEventCreate(&e.border_end));
+        CUDA_TRY(h, cudaEventCreate(&e.fwd2_end));
         CUDA_TRY(h, cudaEventCreate(&e.bwd_end));
         CUDA_TRY(h, cudaEventRecord(e.start, st));
 
-        CUDA_TRY(h, cudaMemsetAsync(h->live, 0,
-                                    (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
-        init_state_kernel<<<dim3(std::min<int64_t>((n + 255) / 256, 1184), ng), 256, 0, st>>>(
-            h->vis, h->lvl[0], n, cnt);
-        seed_sources_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * lanes_per_batch, cnt, n,
-                                                                h->vis, h->lvl[0], h->sigma, h->live);
-        h->launches += 2;
-        CUDA_TRY(h, cudaGetLastError());
-
+        // ---- forward: Step 1 (or the whole BFS when there is no partition)
+        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st));
         int depth = 1;
-        if ((rc = forward_sweep(h, c, ng, st, &depth))) return rc;
-        max_depth = std::max(max_depth, depth);
+        h->cnt_off = hybir ? 4 : 0;  // Step 1 is a partial traversal: keep it out of the totals
+        TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
+        h->cnt_off = 0;
         CUDA_TRY(h, cudaEventRecord(e.fwd_end, st));
 
-        // Level 0 holds only the sources; their delta is excluded from BC
-        // (engine.py:147-148), so it is computed only for inspection.
-        const int last = debug ? 0 : 1;
-        for (int L = depth - 1; L >= last; --L)
-            if ((rc = launch_backward(h, c, L, L == depth - 1, ng, debug, !debug, st))) return rc;
+        std::vector<int32_t> iters;
+        std::vector<uint32_t> entered;
+        if (hybir) {
+            // ---- Steps 2-5 + path-count composition on the border tables
+            const size_t bcnt = (size_t)h->B * h->border_S;
+            std::vector<int32_t> lp(h->border_S, 0);
+            for (int i = 0; i < cnt; ++i) lp[i] = h->h_part[batch_src[i]];
+            CUDA_TRY(h, cudaMemcpyAsync(h->lane_part, lp.data(), h->border_S * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, st));
+            fill_border_kernel<<<grid1d(bcnt, 256, 4736), 256, 0, st>>>(h->D, h->seedD, h->seedS,
+                                                                        h->sig, h->arr, bcnt);
+            TRY(upload_level_ptrs(h, depth, st));
+            if (h->B > 0)
+                border_gather_kernel<<<grid1d(bcnt), 256, 0, st>>>(
+                    h->d_lvl_ptrs, h->live, h->alloc_groups, depth, h->sigma, n, border_geom(h),
+                    h->border_S, h->seedD, h->seedS);
+            h->launches += 2;
+            int max_seed = -1;
+            TRY(refine_and_compose(h, cnt, ng, st, &iters, &entered, &max_seed));
+            CUDA_TRY(h, cudaEventRecord(e.border_end, st));
+            // ---- Step 6: every part relaxes from its borders at once
+            TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st));
+            TRY(forward_sweep(h, h->intra, ng, st, &depth, true, cnt, max_seed));
+            CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
+        } else {
+            CUDA_TRY(h, cudaEventRecord(e.border_end, st));
+            CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
+        }
+        max_depth = std::max(max_depth, depth);
+
+        // ---- backward over the whole graph (cross-part children are final by
+        // the time their parents' level runs: levels are global)
+        TRY(backward_sweep(h, h->full, depth, ng, debug, st));
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
+
+        if (want_reports && h->k == 2) {
+            // ---- per-source reports (forward.py:52-64, backward.py:33-43, bsp.py:96-103,137-141)
+            const size_t G = (size_t)h->alloc_groups;
+            const size_t pw = (size_t)depth * h->k * G;
+            if (h->presence_words < pw) {
+                cudaFree(h->presence);
+                h->presence = nullptr;
+                CUDA_TRY(h, cudaMalloc((void **)&h->presence, pw * sizeof(uint32_t)));
+                h->presence_words = pw;
+            }
+            CUDA_TRY(h, cudaMemsetAsync(h->presence, 0, pw * sizeof(uint32_t), st));
+            for (int L = 0; L < depth; ++L) {
+                level_presence_kernel<<<dim3(grid1d((size_t)n, 256, 296), ng), 256,
+                                        h->k * sizeof(uint32_t), st>>>(
+                    h->lvl[L], h->live + (size_t)L * G, h->d_part, n, h->k, (int)G,
+                    h->presence + (size_t)L * h->k * G);
+                ++h->launches;
+            }
+            std::vector<uint32_t> pres(pw);
+            CUDA_TRY(h, cudaMemcpyAsync(pres.data(), h->presence, pw * sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, st));
+            std::vector<int64_t> lsync(h->border_S, 0), lbytes(h->border_S, 0);
+            if (hybir && h->B > 0) {
+                const size_t bcnt = (size_t)h->B * h->border_S;
+                const int W = (depth + 31) / 32 + 1;
+                const size_t words = (size_t)2 * W * h->border_S;
+                if (h->sync_bits_words < words) {
+                    TRY(dev_alloc(h, &h->sync_bits, words));
+                    h->sync_bits_words = words;
+                }
+                CUDA_TRY(h, cudaMemsetAsync(h->sync_bits, 0, words * sizeof(uint32_t), st));
+                TRY(upload_level_ptrs(h, depth, st));
+                border_gather_kernel<<<grid1d(bcnt), 256, 0, st>>>(
+                    h->d_lvl_ptrs, h->live, h->alloc_groups, depth, h->sigma, n, border_geom(h),
+                    h->border_S, h->Dfin, nullptr);
+                sync_mark_kernel<<<grid1d(bcnt), 256, 0, st>>>(border_geom(h), h->border_S, h->Dfin,
+                                                               h->sync_flag, h->sync_bits, W);
+                sync_count_kernel<<<grid1d((size_t)h->border_S, 128), 128, 0, st>>>(
+                    h->B, h->border_S, W, h->sync_flag, h->sync_bits, h->lane_sync, h->lane_bytes);
+                h->launches += 3;
+                CUDA_TRY(h, cudaMemcpyAsync(lsync.data(), h->lane_sync, h->border_S * sizeof(int64_t),
+                                            cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaMemcpyAsync(lbytes.data(), h->lane_bytes, h->border_S * sizeof(int64_t),
+                                            cudaMemcpyDeviceToHost, st));
+            }
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            int64_t border_total = h->B;
+            for (int i = 0; i < cnt; ++i) {
+                const size_t g = i >> 5;
+                const uint32_t bit = 1u << (i & 31);
+                int64_t maxl[2] = {0, 0}, nl[2] = {0, 0}, global_levels = 0;
+                for (int L = 0; L < depth; ++L) {
+                    bool any = false;
+                    for (int p = 0; p < 2; ++p)
+                        if (pres[((size_t)L * h->k + p) * G + g] & bit) {
+                            maxl[p] = L;
+                            ++nl[p];
+                            any = true;
+                        }
+                    global_levels += any;
+                }
+                int64_t *r = &h->reports_host[(size_t)where[b * lanes_per_batch + i] * 8];
+                if (hybir) {
+                    r[0] = iters[i];
+                    r[1] = entered[i] ? 2 * (int64_t)iters[i] + 1 : 0;
+                    r[4] = lsync[i];
+                    r[5] = lbytes[i];
+                } else {
+                    // level-synchronous baseline: one exchange per level that has a successor
+                    r[0] = global_levels - 1;
+                    r[1] = 2 * (global_levels - 1);
+                    r[4] = 2 * (global_levels - 1);
+                    r[5] = (global_levels - 1) * border_total * 16;
+                }
+                r[2] = maxl[0];
+                r[3] = maxl[1];
+                r[6] = nl[0];
+                r[7] = nl[1];
+                tot_iters += r[0];
+                tot_comm += r[1];
+                tot_sync += r[4];
+                tot_bytes += r[5];
+            }
+        } else if (hybir) {
+            for (int i = 0; i < cnt; ++i) {
+                int64_t *r = &h->reports_host[(size_t)where[b * lanes_per_batch + i] * 8];
+                r[0] = iters[i];
+                tot_iters += r[0];
+            }
+        }
 
         if (debug) {
             const size_t rows = (size_t)cnt * (size_t)n;
-            const unsigned fb = (unsigned)std::min<size_t>((rows + 255) / 256, 4736);
+            const unsigned fb = grid1d(rows, 256, 4736);
             if (dbg_dist) fill_i32_kernel<<<fb, 256, 0, st>>>(dbg_dist, rows, BC_UNREACHED);
             if (dbg_sigma) CUDA_TRY(h, cudaMemsetAsync(dbg_sigma, 0, rows * sizeof(double), st));
             if (dbg_delta) CUDA_TRY(h, cudaMemsetAsync(dbg_delta, 0, rows * sizeof(double), st));
             for (int L = 0; L < depth; ++L) {
-                extract_level_kernel<<<dim3(std::min<int64_t>((n + 255) / 256, 1184), 1), 256, 0, st>>>(
-                    h->lvl[L], h->sigma, h->delta, n, L, dbg_dist, dbg_sigma, dbg_delta);
+                extract_level_kernel<<<dim3(grid1d((size_t)n, 256, 1184), 1), 256, 0, st>>>(
+                    h->lvl[L], h->live + (size_t)L * h->alloc_groups, h->sigma, h->delta, n, L,
+                    dbg_dist, dbg_sigma, dbg_delta);
                 ++h->launches;
             }
             CUDA_TRY(h, cudaGetLastError());
@@ -470,8 +943,7 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
         }
     }
     if (!debug && bc_dev != nullptr) {
-        reduce_bc_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, st>>>(
-            bc_dev, h->bcg, n, h->alloc_groups);
+        reduce_bc_kernel<<<grid1d((size_t)n, 256, 1184), 256, 0, st>>>(bc_dev, h->bcg, n, h->alloc_groups);
         ++h->launches;
         CUDA_TRY(h, cudaGetLastError());
     }
@@ -481,22 +953,26 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
     d2h += sizeof cnts;
     cudaFree(dbg_dist), cudaFree(dbg_sigma), cudaFree(dbg_delta);
 
-    double ms_total = 0, ms_f = 0, ms_b = 0;
+    double ms_f = 0, ms_b = 0, ms_border = 0;
     for (Events &e : ev) {
-        float a = 0, bms = 0;
+        float a = 0, bo = 0, f2 = 0, bw = 0;
         cudaEventElapsedTime(&a, e.start, e.fwd_end);
-        cudaEventElapsedTime(&bms, e.fwd_end, e.bwd_end);
-        ms_f += a;
-        ms_b += bms;
-        cudaEventDestroy(e.start), cudaEventDestroy(e.fwd_end), cudaEventDestroy(e.bwd_end);
+        cudaEventElapsedTime(&bo, e.fwd_end, e.border_end);
+        cudaEventElapsedTime(&f2, e.border_end, e.fwd2_end);
+        cudaEventElapsedTime(&bw, e.fwd2_end, e.bwd_end);
+        ms_f += a + f2;
+        ms_border += bo;
+        ms_b += bw;
+        cudaEventDestroy(e.start), cudaEventDestroy(e.fwd_end), cudaEventDestroy(e.border_end);
+        cudaEventDestroy(e.fwd2_end), cudaEventDestroy(e.bwd_end);
     }
-    if (!ev.empty()) ms_total = ms_f + ms_b;
     if (stats) {
         memset(stats, 0, sizeof *stats);
         stats->sources = k_all;
         stats->batches = n_batches;
         stats->max_levels = std::max<int64_t>(max_depth, k_all > 0 ? 1 : 0);
-        // sources themselves are reached vertices too (level 0)
+        // sources themselves are reached vertices too (level 0); in hybir mode
+        // the totals count Step 6 (arcs inside the parts; cut arcs are not walked)
         stats->reached = (int64_t)cnts[0] + k_all;
         int64_t src_arcs = 0;
         for (int64_t i = 0; i < k; ++i) src_arcs += h->h_off[sources[i] + 1] - h->h_off[sources[i]];
@@ -505,10 +981,21 @@ int run_sources(bc_handle *h, const int64_t *sources, int64_t k, double *bc_dev,
         stats->launches = h->launches - launches0;
         stats->h2d_bytes = h2d;
         stats->d2h_bytes = d2h;
-        stats->ms_total = ms_total;
+        stats->ms_total = ms_f + ms_b + ms_border;
         stats->ms_forward = ms_f;
         stats->ms_backward = ms_b;
+        stats->ms_border = ms_border;
+        stats->iterations = tot_iters;
+        stats->comm_events = tot_comm;
+        stats->sync_events = tot_sync;
+        stats->comm_bytes = tot_bytes;
     }
+    return BC_OK;
+}
+
+int check_mode(bc_handle *h, int mode) {
+    if (mode != BC_MODE_DIRECT && mode != BC_MODE_HYBIR && mode != BC_MODE_BSP)
+        return h->fail(BC_ERR_INPUT, "unknown mode (use BC_MODE_DIRECT, BC_MODE_HYBIR or BC_MODE_BSP)");
     return BC_OK;
 }
 
@@ -542,6 +1029,7 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
     h->n = n;
     h->n_arcs = n_arcs;
     h->h_off.assign(offsets, offsets + n + 1);
+    h->h_col.assign(col_idx, col_idx + n_arcs);
     auto bail = [&](int rc) {
         g_create_error = h->err;
         bc_destroy(h);
@@ -554,7 +1042,6 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
     Csr &c = h->full;
     c.n = n;
     c.n_arcs = n_arcs;
-    c.owns_graph = true;
     auto body = [&]() -> int {
         CUDA_TRY(h, cudaMalloc((void **)&c.off, (n + 1) * sizeof(int64_t)));
         CUDA_TRY(h, cudaMalloc((void **)&c.col, std::max<int64_t>(n_arcs, 1) * sizeof(int32_t)));
@@ -583,13 +1070,13 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
             return h->fail(BC_ERR_INPUT, "item_arcs must be a multiple of 32 in [32, 2^20]");
         if (value != h->item_arcs) {
             h->item_arcs = (int)value;
-            Csr &c = h->full;
-            cudaFree(c.chk_v), cudaFree(c.chk_a0), cudaFree(c.chk_a1);
-            cudaFree(c.rng_v0), cudaFree(c.rng_nv);
-            cudaFree(c.hub_v), cudaFree(c.hub_c0), cudaFree(c.hub_nc);
-            c.chk_v = c.rng_v0 = c.rng_nv = c.hub_v = c.hub_c0 = c.hub_nc = nullptr;
-            c.chk_a0 = c.chk_a1 = nullptr;
-            return build_items(h, c, h->h_off.data(), h->item_arcs);
+            TRY(build_items(h, h->full, h->h_off.data(), h->item_arcs));
+            if (h->k > 1) {
+                std::vector<int64_t> ioff((size_t)h->n + 1);
+                CUDA_TRY(h, cudaMemcpy(ioff.data(), h->intra.off, (h->n + 1) * sizeof(int64_t),
+                                       cudaMemcpyDeviceToHost));
+                TRY(build_items(h, h->intra, ioff.data(), h->item_arcs));
+            }
         }
         return BC_OK;
     }
@@ -602,9 +1089,79 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
 
 int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     if (h == nullptr) return BC_ERR_INPUT;
-    (void)k;
-    (void)assignment;
-    return h->fail(BC_ERR_INTERNAL, "bc_set_partition: not built yet");
+    if (k < 1 || assignment == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_set_partition: need k >= 1 and an assignment");
+    const int64_t n = h->n;
+    for (int64_t v = 0; v < n; ++v)
+        if (assignment[v] < 0 || assignment[v] >= k)
+            return h->fail(BC_ERR_INPUT, "bc_set_partition: part id outside [0, k)");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    free_partition(h);
+    h->k = k;
+    h->h_part.assign(assignment, assignment + n);
+    if (k == 1) return BC_OK;
+    const int64_t *off = h->h_off.data();
+    const int32_t *col = h->h_col.data();
+    // cut-free CSR + border lists (ascending vertex id inside each part)
+    std::vector<int64_t> ioff((size_t)n + 1, 0);
+    std::vector<int32_t> icol;
+    icol.reserve((size_t)h->n_arcs);
+    std::vector<std::vector<int32_t>> borders((size_t)k);
+    for (int64_t v = 0; v < n; ++v) {
+        bool is_border = false;
+        for (int64_t a = off[v]; a < off[v + 1]; ++a) {
+            if (assignment[col[a]] == assignment[v]) icol.push_back(col[a]);
+            else is_border = true;
+        }
+        ioff[(size_t)v + 1] = (int64_t)icol.size();
+        if (is_border) borders[(size_t)assignment[v]].push_back((int32_t)v);
+    }
+    h->h_part_off.assign((size_t)k + 1, 0);
+    h->h_tab_off.assign((size_t)k, 0);
+    h->h_border_v.clear();
+    h->h_border_p.clear();
+    int64_t tab = 0;
+    for (int p = 0; p < k; ++p) {
+        h->h_part_off[(size_t)p] = (int32_t)h->h_border_v.size();
+        h->h_tab_off[(size_t)p] = tab;
+        const int64_t b = (int64_t)borders[(size_t)p].size();
+        tab += b * b;
+        for (int32_t v : borders[(size_t)p]) {
+            h->h_border_v.push_back(v);
+            h->h_border_p.push_back(p);
+        }
+    }
+    h->h_part_off[(size_t)k] = (int32_t)h->h_border_v.size();
+    h->B = (int)h->h_border_v.size();
+    h->tab_total = tab;
+    std::vector<int32_t> index_of((size_t)n, -1);
+    for (int j = 0; j < h->B; ++j) index_of[(size_t)h->h_border_v[(size_t)j]] = j;
+    // incoming cut arcs of every border, in arc order (the graph is symmetric)
+    std::vector<int64_t> cin_off((size_t)h->B + 1, 0);
+    std::vector<int32_t> cin_src;
+    for (int j = 0; j < h->B; ++j) {
+        const int64_t v = h->h_border_v[(size_t)j];
+        for (int64_t a = off[v]; a < off[v + 1]; ++a)
+            if (assignment[col[a]] != assignment[v]) cin_src.push_back(index_of[(size_t)col[a]]);
+        cin_off[(size_t)j + 1] = (int64_t)cin_src.size();
+    }
+    h->n_cut = (int64_t)cin_src.size();
+    Csr &c = h->intra;
+    c.n = n;
+    c.n_arcs = (int64_t)icol.size();
+    TRY(upload(h, &c.off, ioff));
+    if (icol.empty()) icol.push_back(0);
+    TRY(upload(h, &c.col, icol));
+    TRY(build_items(h, c, ioff.data(), h->item_arcs));
+    TRY(upload(h, &h->d_part, h->h_part));
+    TRY(upload(h, &h->d_border_v, h->h_border_v));
+    TRY(upload(h, &h->d_border_p, h->h_border_p));
+    TRY(upload(h, &h->d_part_off, h->h_part_off));
+    TRY(upload(h, &h->d_tab_off, h->h_tab_off));
+    TRY(upload(h, &h->d_cin_off, cin_off));
+    if (cin_src.empty()) cin_src.push_back(0);
+    TRY(upload(h, &h->d_cin_src, cin_src));
+    return BC_OK;
 }
 
 int bc_run_device(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources,
@@ -612,10 +1169,10 @@ int bc_run_device(bc_handle *h, int mode, const int64_t *sources, int64_t n_sour
     if (h == nullptr) return BC_ERR_INPUT;
     if (n_sources < 0 || (n_sources > 0 && sources == nullptr) || bc_dev == nullptr)
         return h->fail(BC_ERR_INPUT, "bc_run_device: null buffer or negative source count");
-    if (mode != BC_MODE_DIRECT) return h->fail(BC_ERR_INPUT, "bc_run_device: mode not built yet");
+    TRY(check_mode(h, mode));
     CUDA_TRY(h, cudaSetDevice(h->device));
-    return run_sources(h, sources, n_sources, bc_dev, (cudaStream_t)stream, stats, false, nullptr,
-                       nullptr, nullptr);
+    return run_sources(h, mode, sources, n_sources, bc_dev, (cudaStream_t)stream, stats, false,
+                       nullptr, nullptr, nullptr);
 }
 
 int bc_run(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources, double *bc_out,
@@ -626,8 +1183,7 @@ int bc_run(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources, do
     if (h->bc_scratch == nullptr)
         CUDA_TRY(h, cudaMalloc((void **)&h->bc_scratch, (size_t)h->n * sizeof(double)));
     CUDA_TRY(h, cudaMemset(h->bc_scratch, 0, (size_t)h->n * sizeof(double)));
-    int rc = bc_run_device(h, mode, sources, n_sources, h->bc_scratch, nullptr, stats);
-    if (rc) return rc;
+    TRY(bc_run_device(h, mode, sources, n_sources, h->bc_scratch, nullptr, stats));
     CUDA_TRY(h, cudaMemcpy(bc_out, h->bc_scratch, (size_t)h->n * sizeof(double),
                            cudaMemcpyDeviceToHost));
     if (stats) stats->d2h_bytes += h->n * (int64_t)sizeof(double);
@@ -639,28 +1195,74 @@ int bc_debug_sources(bc_handle *h, int mode, const int64_t *sources, int64_t k, 
     if (h == nullptr) return BC_ERR_INPUT;
     if (k < 0 || (k > 0 && sources == nullptr))
         return h->fail(BC_ERR_INPUT, "bc_debug_sources: null sources");
-    if (mode != BC_MODE_DIRECT) return h->fail(BC_ERR_INPUT, "bc_debug_sources: mode not built yet");
+    TRY(check_mode(h, mode));
     CUDA_TRY(h, cudaSetDevice(h->device));
-    return run_sources(h, sources, k, nullptr, nullptr, nullptr, true, dist, sigma, delta);
+    return run_sources(h, mode, sources, k, nullptr, nullptr, nullptr, true, dist, sigma, delta);
 }
 
 int bc_get_reports(bc_handle *h, int64_t *out, int64_t n_sources) {
     if (h == nullptr) return BC_ERR_INPUT;
-    (void)out;
-    (void)n_sources;
-    return h->fail(BC_ERR_INTERNAL, "bc_get_reports: not built yet");
+    if (out == nullptr || n_sources * 8 != (int64_t)h->reports_host.size())
+        return h->fail(BC_ERR_INPUT, "bc_get_reports: source count differs from the last run");
+    memcpy(out, h->reports_host.data(), h->reports_host.size() * sizeof(int64_t));
+    return BC_OK;
 }
 
 int bc_get_border_counts(bc_handle *h, int64_t *counts) {
     if (h == nullptr) return BC_ERR_INPUT;
-    (void)counts;
-    return h->fail(BC_ERR_INTERNAL, "bc_get_border_counts: not built yet");
+    if (counts == nullptr) return h->fail(BC_ERR_INPUT, "bc_get_border_counts: null output");
+    if (h->k == 1) {
+        counts[0] = 0;
+        return BC_OK;
+    }
+    for (int p = 0; p < h->k; ++p) counts[p] = h->h_part_off[(size_t)p + 1] - h->h_part_off[(size_t)p];
+    return BC_OK;
 }
 
 int bc_get_border_tables(bc_handle *h, int part, int32_t *borders, int32_t *bm, double *sm) {
     if (h == nullptr) return BC_ERR_INPUT;
-    (void)part, (void)borders, (void)bm, (void)sm;
-    return h->fail(BC_ERR_INTERNAL, "bc_get_border_tables: not built yet");
+    if (h->k < 2 || part < 0 || part >= h->k)
+        return h->fail(BC_ERR_INPUT, "bc_get_border_tables: no such part");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    TRY(build_border_tables(h));
+    const int64_t b = h->h_part_off[(size_t)part + 1] - h->h_part_off[(size_t)part];
+    if (borders)
+        memcpy(borders, h->h_border_v.data() + h->h_part_off[(size_t)part], b * sizeof(int32_t));
+    if (b == 0) return BC_OK;
+    if (bm) {
+        CUDA_TRY(h, cudaMemcpy(bm, h->bm + h->h_tab_off[(size_t)part], b * b * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < b * b; ++i)
+            if (bm[i] >= kInf) bm[i] = BC_UNREACHED;
+    }
+    if (sm)
+        CUDA_TRY(h, cudaMemcpy(sm, h->sm + h->h_tab_off[(size_t)part], b * b * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+    return BC_OK;
+}
+
+int bc_get_border_frontier(bc_handle *h, int64_t n_lanes, int32_t *dist, double *sigma,
+                           double *arrival) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (h->k < 2 || h->D == nullptr || n_lanes < 0 || n_lanes > h->border_S)
+        return h->fail(BC_ERR_INPUT, "bc_get_border_frontier: no hybir batch of that width has run");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const size_t cnt = (size_t)h->B * h->border_S;
+    std::vector<int32_t> d(cnt);
+    std::vector<double> s(cnt), a(cnt);
+    if (cnt) {
+        CUDA_TRY(h, cudaMemcpy(d.data(), h->D, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CUDA_TRY(h, cudaMemcpy(s.data(), h->sig, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+        CUDA_TRY(h, cudaMemcpy(a.data(), h->arr, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    for (int j = 0; j < h->B; ++j)
+        for (int64_t l = 0; l < n_lanes; ++l) {
+            const size_t from = (size_t)j * h->border_S + l, to = (size_t)j * n_lanes + l;
+            if (dist) dist[to] = d[from] >= kInf ? BC_UNREACHED : d[from];
+            if (sigma) sigma[to] = s[from];
+            if (arrival) arrival[to] = a[from];
+        }
+    return BC_OK;
 }
 
 const char *bc_last_error(bc_handle *h) {
@@ -671,11 +1273,15 @@ void bc_destroy(bc_handle *h) {
     if (h == nullptr) return;
     cudaSetDevice(h->device);
     free_state(h);
+    free_partition(h);
     free_csr(h->full);
-    cudaFree(h->live);
     cudaFree(h->counters);
+    cudaFree(h->dflags);
+    cudaFree(h->d_maxlvl);
     cudaFree(h->d_src);
     cudaFree(h->bc_scratch);
+    cudaFree((void *)h->d_lvl_ptrs);
+    cudaFree(h->presence);
     delete h;
 }
 

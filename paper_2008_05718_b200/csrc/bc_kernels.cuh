@@ -407,10 +407,11 @@ __global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups)
 }
 
 // Inspection: scatter level L of every lane into per-source rows.
-__global__ void extract_level_kernel(const uint32_t *lvl, const double *sigma, const double *delta,
-                                     int64_t n, int level, int32_t *dist_out, double *sigma_out,
-                                     double *delta_out) {
+__global__ void extract_level_kernel(const uint32_t *lvl, const uint32_t *live_level,
+                                     const double *sigma, const double *delta, int64_t n, int level,
+                                     int32_t *dist_out, double *sigma_out, double *delta_out) {
     const size_t g = blockIdx.y;
+    if (live_level[g] == 0) return;  // the level row of a dead group was never written
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         uint32_t m = lvl[g * n + v];

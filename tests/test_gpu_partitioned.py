@@ -1,0 +1,196 @@
+"""Partitioned modes on the GPU (through the C ABI) against the reference.
+
+hybir mode = Step 1 + border refinement + path-count composition + Step 6
+(reference forward.py:188-256), bsp-baseline = level-synchronous (bsp.py).
+Golden vectors (tests/golden/reference_vectors.json) pin every intermediate
+the reference exposes: border lists, border matrices, refined border
+distances / sigma / arrival sigma, per-source reports.  Final dist / sigma /
+delta / BC are also compared with the C oracle on seeded graphs, including
+k > 2 parts, which the reference cannot run.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2008_05718_b200 as P
+from paper_2008_05718_b200 import generators as G
+from paper_2008_05718_b200._capi import Engine, MODE_BSP, MODE_DIRECT, MODE_HYBIR
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-9, 1e-12
+
+
+def _check_sources(g, sources, dist, sigma, delta):
+    for i, s in enumerate(sources):
+        od, osg, odl, info = O.brandes_single_source(g, int(s))
+        assert info["sigma_max"] < 2.0 ** 53
+        assert np.array_equal(dist[i], od), s
+        assert np.array_equal(sigma[i], osg), s
+        assert np.allclose(delta[i], odl, rtol=RTOL, atol=ATOL), s
+
+
+def test_border_tables_match_reference(golden_graphs):
+    for name, (g, rec) in golden_graphs.items():
+        with Engine(g) as e:
+            e.set_partition(2, rec["assignment"])
+            counts = e.border_counts(2)
+            assert counts.tolist() == [len(b) for b in rec["borders"]], name
+            for side in (0, 1):
+                b = int(counts[side])
+                borders, bm, sm = e.border_tables(side, b)
+                assert borders.tolist() == rec["borders"][side], name
+                if b:
+                    assert bm.tolist() == rec["bm"][side], name
+                    assert sm.tolist() == [[float(x) for x in row] for row in rec["sm"][side]], name
+
+
+def test_hybir_forward_backward_match_reference(golden_graphs):
+    for name, (g, rec) in golden_graphs.items():
+        srcs = [s["s"] for s in rec["sources"]]
+        nb = sum(len(b) for b in rec["borders"])
+        with Engine(g) as e:
+            e.set_partition(2, rec["assignment"])
+            dist, sigma, delta = e.debug_sources(srcs, MODE_HYBIR)
+            reports = e.reports(len(srcs))
+            assert len(srcs) <= 32
+            bd, bsig, barr = e.border_frontier(len(srcs), nb)
+            bc, st = e.run(rec["run_bc_sources"], MODE_HYBIR)
+        for i, s in enumerate(rec["sources"]):
+            assert dist[i].tolist() == s["hybir_dist"], (name, s["s"])
+            assert sigma[i].tolist() == [float(x) for x in s["hybir_sigma"]], (name, s["s"])
+            assert np.allclose(delta[i], s["hybir_delta"], rtol=RTOL, atol=ATOL), (name, s["s"])
+            # the reference's BorderFrontier: refined distances, sigma, arrival sigma
+            want_d = s["border_dist"][0] + s["border_dist"][1]
+            want_s = s["border_sigma"][0] + s["border_sigma"][1]
+            want_a = s["arrival_sigma"][0] + s["arrival_sigma"][1]
+            assert bd[:, i].tolist() == want_d, (name, s["s"])
+            assert bsig[:, i].tolist() == [float(x) for x in want_s], (name, s["s"])
+            assert barr[:, i].tolist() == [float(x) for x in want_a], (name, s["s"])
+            # ForwardReport / BackwardReport
+            it, ce, ml0, ml1, se, cb, l0, l1 = reports[i].tolist()
+            assert {"iterations": it, "comm_events": ce, "max_level": [ml0, ml1]} == {
+                k: s["forward"][k] for k in ("iterations", "comm_events", "max_level")}, (name, s["s"])
+            assert {"sync_events": se, "comm_bytes": cb, "levels": [l0, l1]} == s["backward"], (name, s["s"])
+        assert np.allclose(bc, rec["run_bc_hybir"], rtol=RTOL, atol=ATOL), name
+        assert st["iterations"] == sum(s["forward"]["iterations"] for s in rec["sources"]
+                                       if s["s"] in rec["run_bc_sources"]) or len(srcs) != len(rec["run_bc_sources"])
+
+
+def test_bsp_mode_matches_reference(golden_graphs):
+    for name, (g, rec) in golden_graphs.items():
+        srcs = [s["s"] for s in rec["sources"]]
+        with Engine(g) as e:
+            e.set_partition(2, rec["assignment"])
+            dist, sigma, delta = e.debug_sources(srcs, MODE_BSP)
+            reports = e.reports(len(srcs))
+            bc, _ = e.run(rec["run_bc_sources"], MODE_BSP)
+        for i, s in enumerate(rec["sources"]):
+            assert dist[i].tolist() == s["dist"]
+            assert sigma[i].tolist() == [float(x) for x in s["sigma"]]
+            it, ce, ml0, ml1, se, cb, l0, l1 = reports[i].tolist()
+            f, b = s["bsp_forward"], s["bsp_backward"]
+            assert (it, ce, [ml0, ml1]) == (f["supersteps"], f["comm_events"], f["max_level"]), (name, s["s"])
+            assert (se, cb, [l0, l1]) == (b["sync_events"], b["comm_bytes"], b["levels"]), (name, s["s"])
+        assert np.allclose(bc, rec["run_bc_bsp_baseline"], rtol=RTOL, atol=ATOL), name
+
+
+def test_run_bc_drop_in(golden_graphs):
+    # run_bc with the reference's defaults (mode hybir, greedy two-way partition)
+    g, rec = golden_graphs["rc_n40_s1004"]
+    res = P.run_bc(g, P.RunConfig(sources=rec["run_bc_sources"], seed=1004, ratio=0.5))
+    assert res.partition.assignment.tolist() == rec["assignment"]
+    assert np.allclose(res.bc, rec["run_bc_hybir"], rtol=RTOL, atol=ATOL)
+    by_src = {s["s"]: s for s in rec["sources"]}
+    for rep in res.per_source:
+        want = by_src[rep["source"]]
+        assert rep["forward"] == {"source": rep["source"], **{k: want["forward"][k] for k in
+                                  ("iterations", "comm_events", "max_level")}}
+        assert rep["backward"] == want["backward"]
+    res2 = P.run_bc(g, P.RunConfig(sources=rec["run_bc_sources"], seed=1004, mode="bsp-baseline"))
+    assert np.allclose(res2.bc, rec["run_bc_bsp_baseline"], rtol=RTOL, atol=ATOL)
+    assert res.ledger.totals()["forward_events"] == sum(r["forward"]["comm_events"] for r in res.per_source)
+    rep = P.build_report(g, res)
+    assert rep["partition_stats"]["borders"] == [len(b) for b in rec["borders"]]
+    assert P.pipeline_sources(g, P.RunConfig(sources=[0, 1], seed=1004)).bc.shape == (40,)
+
+
+def test_p64_communication_counts():
+    # reference pkg/tests/test_engine.py:33-46: P64, half split, source 0
+    g = G.path(64)
+    a = np.zeros(64, dtype=np.int32)
+    a[32:] = 1
+    part = P.Partition(a, 0.5, 2)
+    bsp = P.run_bc(g, P.RunConfig(sources=[0], mode="bsp-baseline", partition=part))
+    hyb = P.run_bc(g, P.RunConfig(sources=[0], mode="hybir", partition=part))
+    assert bsp.per_source[0]["forward"]["supersteps"] == 63
+    assert bsp.per_source[0]["forward"]["comm_events"] == 126
+    assert hyb.per_source[0]["forward"]["iterations"] == 1
+    assert hyb.per_source[0]["forward"]["comm_events"] == 3
+    assert np.allclose(bsp.bc, hyb.bc, rtol=RTOL, atol=ATOL)
+
+
+def test_config1_rmat12_two_partitions(rmat12):
+    """BASELINE config 1: R-MAT scale-12 EF-8, all sources, 2 partitions (greedy, seed 0)."""
+    g = rmat12
+    p = P.greedy_bipartition(g, 0.5, seed=0)
+    srcs = list(range(g.num_vertices))
+    with Engine(g) as e:
+        e.set_option("groups", 16)
+        e.set_option("reports", 0)
+        e.set_partition(2, p.assignment)
+        assert e.border_counts(2).tolist() == [780, 908]
+        bc, st = e.run(srcs, MODE_HYBIR)
+        sample = list(range(3, g.num_vertices, 131))
+        dist, sigma, delta = e.debug_sources(sample, MODE_HYBIR)
+        bc_bsp, _ = e.run(srcs, MODE_BSP)
+    obc, _ = O.brandes_bc(g, srcs)
+    assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+    assert np.allclose(bc_bsp, obc, rtol=RTOL, atol=ATOL)
+    _check_sources(g, sample, dist, sigma, delta)
+    assert st["iterations"] >= len(srcs) - 1129 - 50      # every non-isolated source refines at least once
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+def test_kway_partitions_vs_oracle(k):
+    # k-way generalisation (not in the reference): validated against the oracle only
+    g = G.road_like(40, 30, keep=0.25, seed=5)
+    part = P.strip_partition(40, 30, k)
+    srcs = list(range(0, g.num_vertices, 37))
+    with Engine(g) as e:
+        e.set_partition(k, part.assignment)
+        dist, sigma, delta = e.debug_sources(srcs, MODE_HYBIR)
+        bc, st = e.run(srcs, MODE_HYBIR)
+        bc_direct, _ = e.run(srcs, MODE_DIRECT)
+    _check_sources(g, srcs, dist, sigma, delta)
+    assert np.allclose(bc, O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
+    assert np.allclose(bc, bc_direct, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_partitions_vs_oracle(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(30, 300))
+    g = G.random_connected(n, int(rng.integers(0, 2 * n)), seed=50 + seed)
+    k = int(rng.integers(2, 5))
+    a = rng.integers(0, k, size=n).astype(np.int32)        # arbitrary (bad) partitions too
+    srcs = rng.choice(n, size=min(n, 40), replace=False).tolist()
+    with Engine(g) as e:
+        e.set_partition(k, a)
+        dist, sigma, delta = e.debug_sources(srcs, MODE_HYBIR)
+        bc, _ = e.run(srcs, MODE_HYBIR)
+    _check_sources(g, srcs, dist, sigma, delta)
+    assert np.allclose(bc, O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
+
+
+def test_partition_errors():
+    g = G.path(6)
+    with Engine(g) as e:
+        with pytest.raises(P.InputError):
+            e.set_partition(2, [0, 0, 0, 1, 1, 2])
+        with pytest.raises(P.InputError):
+            e.set_partition(2, [0, 1])
+        e.set_partition(2, [0, 0, 0, 0, 0, 0])             # degenerate: one side empty
+        bc, _ = e.run([0, 5], MODE_HYBIR)
+        assert np.allclose(bc, O.brandes_bc(g, [0, 5])[0])
