@@ -732,6 +732,31 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             active.push_back(sources_in[i]);
             where.push_back(i);
         }
+    if (!debug) {
+        // Lanes of a group advance together, so a group works best when its
+        // sources see the graph alike: order them by the size of their 2-hop
+        // neighbourhood (sum of neighbour degrees).  BC is a sum over sources, so
+        // the order only moves fp64 rounding; the inspection path keeps the
+        // caller's order because its output rows follow it.
+        std::vector<int64_t> key(active.size());
+        for (size_t i = 0; i < active.size(); ++i) {
+            int64_t sum = 0;
+            for (int64_t a = h->h_off[active[i]]; a < h->h_off[active[i] + 1]; ++a)
+                sum += h->h_off[h->h_col[a] + 1] - h->h_off[h->h_col[a]];
+            key[i] = sum;
+        }
+        std::vector<size_t> order(active.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](size_t a, size_t b) { return key[a] > key[b]; });
+        std::vector<int64_t> a2(active.size()), w2(active.size());
+        for (size_t i = 0; i < order.size(); ++i) {
+            a2[i] = active[order[i]];
+            w2[i] = where[order[i]];
+        }
+        active.swap(a2);
+        where.swap(w2);
+    }
     const int64_t k = (int64_t)active.size();
     const int64_t *sources = active.data();
     const int groups = debug ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(h->groups, (k + 31) / 32));
