@@ -38,6 +38,8 @@ struct Events {
     cudaEvent_t start, fwd_end, border_end, fwd2_end, bwd_end;
 };
 
+constexpr unsigned long long kQueueMaxDegree = 8192;
+
 // Border-table feasibility: b_p^2 entries of 12 B per part.
 constexpr double kMaxTableBytes = 64e9;
 
@@ -53,6 +55,8 @@ struct bc_handle {
     int groups = 4;
     int item_arcs = 512;
     int reports = 1;
+    int sparse = 1;        // allow queue levels + top-down push (direction-optimising switch)
+    int push_beta = 16;    // push when frontier arcs * beta <= arcs of the graph
     // ---- partition ------------------------------------------------------
     int k = 1;
     std::vector<int32_t> h_part;
@@ -95,6 +99,15 @@ struct bc_handle {
     int pacc_chunks = 0;
     uint32_t *live = nullptr;  // [level][alloc_groups] lanes with a non-empty frontier
     int live_cap = 0;          // levels
+    // sparse levels: per-group frontier queues + two all-zero scratch mask arrays
+    int32_t *q_v = nullptr;
+    uint32_t *q_m = nullptr;
+    int64_t q_cap = 0;
+    unsigned long long *q_count = nullptr;
+    int64_t *d_qbeg = nullptr, *d_qend = nullptr, *d_qlbeg = nullptr;
+    uint32_t *scrA = nullptr, *scrB = nullptr;
+    unsigned long long *lstat = nullptr;
+    bool sigma_zeroed = false;
     unsigned long long *counters = nullptr;
     int cnt_off = 0;  // 0: traversal counters of the result; 4: scratch (Step 1 of hybir mode)
     int64_t *d_src = nullptr;
@@ -227,6 +240,14 @@ void free_state(bc_handle *h) {
     cudaFree(h->live);
     h->live = nullptr;
     h->live_cap = 0;
+    cudaFree(h->q_v), cudaFree(h->q_m), cudaFree(h->q_count);
+    cudaFree(h->d_qbeg), cudaFree(h->d_qend), cudaFree(h->d_qlbeg);
+    cudaFree(h->scrA), cudaFree(h->scrB), cudaFree(h->lstat);
+    h->q_v = nullptr;
+    h->q_m = h->scrA = h->scrB = nullptr;
+    h->q_count = h->lstat = nullptr;
+    h->d_qbeg = h->d_qend = h->d_qlbeg = nullptr;
+    h->q_cap = 0;
     h->vis = nullptr;
     h->sigma = h->coef = h->delta = h->bcg = h->pacc = nullptr;
     h->pmask = nullptr;
@@ -293,13 +314,17 @@ int ensure_state(bc_handle *h, int groups, bool want_delta) {
     return BC_OK;
 }
 
-int ensure_levels(bc_handle *h, int count) {
+int ensure_pool(bc_handle *h, int count) {
     const size_t bytes = (size_t)h->alloc_groups * (size_t)h->n * sizeof(uint32_t);
     while ((int)h->lvl.size() < count) {
         uint32_t *p = nullptr;
         CUDA_TRY(h, cudaMalloc((void **)&p, bytes));
         h->lvl.push_back(p);
     }
+    return BC_OK;
+}
+
+int ensure_live(bc_handle *h, int count) {
     if (h->live_cap < count + 1) {
         const int cap = std::max(count + 1, 2 * h->live_cap);
         const size_t G = (size_t)h->alloc_groups;
@@ -314,6 +339,29 @@ int ensure_levels(bc_handle *h, int count) {
         h->live = p;
         h->live_cap = cap;
     }
+    return BC_OK;
+}
+
+int ensure_levels(bc_handle *h, int count) {
+    TRY(ensure_pool(h, count));
+    return ensure_live(h, count);
+}
+
+int ensure_queues(bc_handle *h) {
+    if (h->q_v != nullptr) return BC_OK;
+    const size_t G = (size_t)h->alloc_groups, n = (size_t)h->n;
+    h->q_cap = (int64_t)(4 * n + 1024);
+    TRY(dev_alloc(h, &h->q_v, G * (size_t)h->q_cap));
+    TRY(dev_alloc(h, &h->q_m, G * (size_t)h->q_cap));
+    TRY(dev_alloc(h, &h->q_count, G));
+    TRY(dev_alloc(h, &h->d_qbeg, G));
+    TRY(dev_alloc(h, &h->d_qend, G));
+    TRY(dev_alloc(h, &h->d_qlbeg, G));
+    TRY(dev_alloc(h, &h->scrA, G * n));
+    TRY(dev_alloc(h, &h->scrB, G * n));
+    TRY(dev_alloc(h, &h->lstat, (size_t)4));
+    CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
+    CUDA_TRY(h, cudaMemset(h->scrB, 0, G * n * sizeof(uint32_t)));
     return BC_OK;
 }
 
@@ -395,11 +443,15 @@ inline unsigned grid1d(size_t count, int block = 256, size_t cap = 1u << 30) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>((count + block - 1) / block, cap));
 }
 
-// Forward level L on graph c for `ng` groups.
-int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st) {
+// Forward level L on graph c for `ng` groups: pull from the masks `nbr` (level
+// L - 1) into the dense array `cur`.
+int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
+                   const uint32_t *nbr = nullptr, uint32_t *cur = nullptr,
+                   unsigned long long *lstat = nullptr) {
     LevelParams p = level_params(h, c);
-    p.nbr = h->lvl[L - 1];
-    p.cur = h->lvl[L];
+    p.nbr = nbr ? nbr : h->lvl[L - 1];
+    p.cur = cur ? cur : h->lvl[L];
+    p.lstat = lstat;
     p.live_prev = h->live + (size_t)(L - 1) * h->alloc_groups;
     p.live_cur = h->live + (size_t)L * h->alloc_groups;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
@@ -407,7 +459,8 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st) {
     ++h->launches;
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
-        q.cur = h->lvl[L];
+        q.cur = p.cur;
+        q.lstat = lstat;
         q.live_prev = p.live_prev;
         q.live_cur = p.live_cur;
         hub_kernel<false, false><<<dim3(blocks_for(c.n_hub), ng), kWarpsPerBlock * 32, 0, st>>>(q);
@@ -419,10 +472,11 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st) {
 
 // Backward level L (children at L + 1; `deepest` = no level below).
 int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, bool store_delta,
-                    bool accumulate, cudaStream_t st) {
+                    bool accumulate, cudaStream_t st, uint32_t *cur = nullptr,
+                    const uint32_t *nbr = nullptr) {
     LevelParams p = level_params(h, c);
-    p.nbr = deepest ? nullptr : h->lvl[L + 1];
-    p.cur = h->lvl[L];
+    p.nbr = deepest ? nullptr : (nbr ? nbr : h->lvl[L + 1]);
+    p.cur = cur ? cur : h->lvl[L];
     p.live_prev = h->live + (size_t)L * h->alloc_groups;
     p.accumulate_bc = accumulate ? 1 : 0;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
@@ -433,7 +487,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     ++h->launches;
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
-        q.cur = h->lvl[L];
+        q.cur = p.cur;
         q.live_prev = p.live_prev;
         q.accumulate_bc = p.accumulate_bc;
         const dim3 hg(blocks_for(c.n_hub), ng);
@@ -448,8 +502,11 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
 }
 
 // Reset the BFS state of a batch and plant the level-0 seeds (sigma = 1).
-int begin_batch(bc_handle *h, const int64_t *src_dev, int cnt, int ng, cudaStream_t st) {
+int begin_batch(bc_handle *h, const int64_t *src_dev, int cnt, int ng, cudaStream_t st,
+                bool zero_sigma = false) {
     const int64_t n = h->n;
+    if (zero_sigma)  // push levels accumulate path counts with atomic adds
+        CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, (size_t)ng * n * 32 * sizeof(double), st));
     CUDA_TRY(h, cudaMemsetAsync(h->live, 0, (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
     init_state_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vis, h->lvl[0], n, cnt);
     seed_sources_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(src_dev, cnt, n, h->vis, h->lvl[0],
@@ -514,6 +571,220 @@ int backward_sweep(bc_handle *h, const Csr &c, int depth, int ng, bool debug, cu
     const int last = debug ? 0 : 1;
     for (int L = depth - 1; L >= last; --L)
         TRY(launch_backward(h, c, L, L == depth - 1, ng, debug, !debug, st));
+    return BC_OK;
+}
+
+
+// ------------------------------------------------------------------------------------
+// direction-optimising sweeps (dense pull levels + queue / push levels)
+// ------------------------------------------------------------------------------------
+
+struct LevelRep {
+    int slot = -1;                 // dense mask array h->lvl[slot], or -1
+    bool queued = false;           // entries [qb[g], qe[g]) of group g's queue
+    std::vector<int64_t> qb, qe;
+    unsigned long long nverts = 0, farcs = 0;  // vertices in the level, their arcs (all groups)
+    unsigned long long maxdeg = 0;             // largest degree in the level
+};
+
+QueueParams queue_params(bc_handle *h) {
+    QueueParams q{};
+    q.q_v = h->q_v;
+    q.q_m = h->q_m;
+    q.cap = h->q_cap;
+    q.q_count = h->q_count;
+    q.q_beg = h->d_qbeg;
+    q.q_end = h->d_qend;
+    return q;
+}
+
+int upload_ranges(bc_handle *h, const LevelRep &r, cudaStream_t st) {
+    const size_t G = (size_t)h->alloc_groups;
+    std::vector<int64_t> b(G, 0), e(G, 0);
+    for (size_t g = 0; g < r.qb.size(); ++g) b[g] = r.qb[g], e[g] = r.qe[g];
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_qbeg, b.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_qend, e.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    return BC_OK;
+}
+
+inline unsigned queue_blocks(const LevelRep &r, int per_block) {
+    int64_t longest = 1;
+    for (size_t g = 0; g < r.qb.size(); ++g) longest = std::max(longest, r.qe[g] - r.qb[g]);
+    return (unsigned)std::min<int64_t>((longest + per_block - 1) / per_block, 8 * 148);
+}
+
+int scatter_level(bc_handle *h, const LevelRep &r, uint32_t *dense, bool clear, int ng, cudaStream_t st) {
+    TRY(upload_ranges(h, r, st));
+    scatter_queue_kernel<<<dim3(queue_blocks(r, 256), ng), 256, 0, st>>>(queue_params(h), h->n, dense,
+                                                                        clear ? 1 : 0);
+    ++h->launches;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+// Forward sweep with the per-level push / pull choice.  One host round trip
+// per level (the choice needs the frontier's arc count).
+int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t *batch_src,
+                     cudaStream_t st, int *depth_out, std::vector<LevelRep> &reps) {
+    const size_t G = (size_t)h->alloc_groups;
+    const int64_t n = h->n;
+    TRY(ensure_queues(h));
+    reps.clear();
+    reps.emplace_back();
+    // level 0: the sources, as a dense array (begin_batch) and as a queue
+    std::vector<unsigned long long> qcount(G, 0);
+    {
+        LevelRep &r0 = reps[0];
+        r0.slot = 0;
+        r0.queued = true;
+        r0.qb.assign(ng, 0);
+        r0.qe.assign(ng, 0);
+        for (int g = 0; g < ng; ++g) {
+            std::vector<std::pair<int32_t, uint32_t>> ent;
+            for (int i = g * 32; i < std::min(cnt, g * 32 + 32); ++i)
+                ent.emplace_back((int32_t)batch_src[i], 1u << (i & 31));
+            std::sort(ent.begin(), ent.end());
+            std::vector<int32_t> qv;
+            std::vector<uint32_t> qm;
+            for (auto &e : ent) {
+                if (!qv.empty() && qv.back() == e.first) qm.back() |= e.second;
+                else qv.push_back(e.first), qm.push_back(e.second);
+            }
+            CUDA_TRY(h, cudaMemcpyAsync(h->q_v + (size_t)g * h->q_cap, qv.data(),
+                                        qv.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+            CUDA_TRY(h, cudaMemcpyAsync(h->q_m + (size_t)g * h->q_cap, qm.data(),
+                                        qm.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            r0.qe[g] = (int64_t)qv.size();
+            qcount[g] = qv.size();
+            r0.nverts += qv.size();
+            for (int32_t v : qv) {
+                const unsigned long long d = (unsigned long long)(h->h_off[v + 1] - h->h_off[v]);
+                r0.farcs += d;
+                r0.maxdeg = std::max(r0.maxdeg, d);
+            }
+        }
+        CUDA_TRY(h, cudaMemcpyAsync(h->q_count, qcount.data(), G * sizeof(unsigned long long),
+                                    cudaMemcpyHostToDevice, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));  // the staging vectors go out of scope
+    }
+    int next_slot = 1;
+    const unsigned long long graph_arcs = (unsigned long long)std::max<int64_t>(c.n_arcs, 1) * ng;
+    std::vector<uint32_t> flags(G);
+    std::vector<unsigned long long> qnow(G), ls(3);
+    for (int L = 1;; ++L) {
+        TRY(ensure_live(h, L + 1));
+        reps.emplace_back();
+        LevelRep &prev = reps[L - 1];
+        LevelRep &cur = reps[L];
+        int64_t room = h->q_cap;
+        for (int g = 0; g < ng; ++g) room = std::min<int64_t>(room, h->q_cap - (int64_t)qcount[g]);
+        const bool room_ok = room > (int64_t)std::min<unsigned long long>((unsigned long long)n, prev.farcs) +
+                                        (prev.queued ? 0 : (int64_t)prev.nverts);
+        // a queue entry is walked by one warp: keep vertices with very long adjacencies on the
+        // dense kernels, which slice them
+        const bool push = prev.farcs * (unsigned long long)h->push_beta <= graph_arcs && room_ok &&
+                          prev.maxdeg <= kQueueMaxDegree;
+        CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 4 * sizeof(unsigned long long), st));
+        if (push) {
+            if (!prev.queued) {  // dense level -> queue
+                prev.qb.assign(qcount.begin(), qcount.begin() + ng);
+                compact_level_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(
+                    h->lvl[prev.slot], h->live + (size_t)(L - 1) * G, n, queue_params(h));
+                ++h->launches;
+                CUDA_TRY(h, cudaMemcpyAsync(qcount.data(), h->q_count, G * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaStreamSynchronize(st));
+                prev.qe.assign(qcount.begin(), qcount.begin() + ng);
+                prev.queued = true;
+            }
+            TRY(upload_ranges(h, prev, st));
+            std::vector<int64_t> lbeg(G, 0);
+            for (int g = 0; g < ng; ++g) lbeg[g] = (int64_t)qcount[g];
+            CUDA_TRY(h, cudaMemcpyAsync(h->d_qlbeg, lbeg.data(), G * sizeof(int64_t),
+                                        cudaMemcpyHostToDevice, st));
+            fwd_push_kernel<<<dim3(queue_blocks(prev, kWarpsPerBlock), ng), kWarpsPerBlock * 32, 0, st>>>(
+                c.off, c.col, n, queue_params(h), h->vis, h->scrA, h->sigma, h->counters + h->cnt_off);
+            push_post_kernel<<<dim3(std::min<unsigned>(grid1d((size_t)std::min<unsigned long long>(
+                                                           (unsigned long long)n, prev.farcs + 1)), 1184), ng),
+                               256, 0, st>>>(c.off, n, queue_params(h), h->d_qlbeg, h->vis, h->scrA,
+                                             h->live + (size_t)L * G, h->counters + h->cnt_off, h->lstat);
+            h->launches += 2;
+            cur.queued = true;
+            cur.qb.assign(lbeg.begin(), lbeg.begin() + ng);
+        } else {
+            const uint32_t *nbr;
+            if (prev.slot >= 0) nbr = h->lvl[prev.slot];
+            else {
+                TRY(scatter_level(h, prev, h->scrB, false, ng, st));
+                nbr = h->scrB;
+            }
+            cur.slot = next_slot++;
+            TRY(ensure_pool(h, cur.slot + 1));
+            TRY(launch_forward(h, c, L, ng, st, nbr, h->lvl[cur.slot], h->lstat));
+            if (prev.slot < 0) TRY(scatter_level(h, prev, h->scrB, true, ng, st));
+        }
+        CUDA_TRY(h, cudaGetLastError());
+        CUDA_TRY(h, cudaMemcpyAsync(flags.data(), h->live + (size_t)L * G, G * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaMemcpyAsync(ls.data(), h->lstat, 3 * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaMemcpyAsync(qnow.data(), h->q_count, G * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+        bool alive = false;
+        for (int g = 0; g < ng; ++g) alive |= flags[g] != 0;
+        if (!alive) {
+            reps.pop_back();
+            *depth_out = L;
+            return BC_OK;
+        }
+        cur.nverts = ls[0];
+        cur.farcs = ls[1];
+        cur.maxdeg = ls[2];
+        if (cur.queued) cur.qe.assign(qnow.begin(), qnow.begin() + ng);
+        qcount = qnow;
+    }
+}
+
+// Backward sweep over the level representations forward_adaptive produced.
+int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRep> &reps, int ng,
+                      bool debug, cudaStream_t st) {
+    const int last = debug ? 0 : 1;
+    const unsigned long long graph_arcs = (unsigned long long)std::max<int64_t>(c.n_arcs, 1) * ng;
+    for (int L = depth - 1; L >= last; --L) {
+        LevelRep &r = reps[L];
+        const bool deepest = L == depth - 1;
+        const uint32_t *nbr = nullptr;
+        bool clear_b = false;
+        if (!deepest) {
+            LevelRep &below = reps[L + 1];
+            if (below.slot >= 0) nbr = h->lvl[below.slot];
+            else {
+                TRY(scatter_level(h, below, h->scrB, false, ng, st));
+                nbr = h->scrB;
+                clear_b = true;
+            }
+        }
+        if (r.slot >= 0) {
+            TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, h->lvl[r.slot], nbr));
+        } else if (r.farcs * (unsigned long long)h->push_beta <= graph_arcs && r.maxdeg <= kQueueMaxDegree) {
+            TRY(upload_ranges(h, r, st));
+            const dim3 grid(queue_blocks(r, kWarpsPerBlock), ng);
+            if (debug)
+                bwd_queue_kernel<true><<<grid, kWarpsPerBlock * 32, 0, st>>>(
+                    c.off, c.col, h->n, queue_params(h), nbr, h->sigma, h->coef, h->delta, h->bcg, 0);
+            else
+                bwd_queue_kernel<false><<<grid, kWarpsPerBlock * 32, 0, st>>>(
+                    c.off, c.col, h->n, queue_params(h), nbr, h->sigma, h->coef, h->delta, h->bcg, 1);
+            ++h->launches;
+            CUDA_TRY(h, cudaGetLastError());
+        } else {  // a queue level with heavy vertices: run it through the dense kernel (hub slices)
+            TRY(scatter_level(h, r, h->scrA, false, ng, st));
+            TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, h->scrA, nbr));
+            TRY(scatter_level(h, r, h->scrA, true, ng, st));
+        }
+        if (clear_b) TRY(scatter_level(h, reps[L + 1], h->scrB, true, ng, st));
+    }
     return BC_OK;
 }
 
@@ -785,6 +1056,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     int max_depth = 0;
     int64_t tot_iters = 0, tot_comm = 0, tot_sync = 0, tot_bytes = 0;
     const Csr &fwd_csr = hybir ? h->intra : h->full;
+    // queue levels / push: the unpartitioned sweeps only (the partitioned modes
+    // read dense level rows for borders and reports)
+    const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2);
 
     // debug staging: one batch (<= 32 sources) of [lane][n] rows
     int32_t *dbg_dist = nullptr;
@@ -808,10 +1082,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         CUDA_TRY(h, cudaEventRecord(e.start, st));
 
         // ---- forward: Step 1 (or the whole BFS when there is no partition)
-        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st));
+        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, adaptive));
         int depth = 1;
         h->cnt_off = hybir ? 4 : 0;  // Step 1 is a partial traversal: keep it out of the totals
-        TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
+        std::vector<LevelRep> reps;
+        if (adaptive) TRY(forward_adaptive(h, fwd_csr, ng, cnt, batch_src, st, &depth, reps));
+        else TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
         h->cnt_off = 0;
         CUDA_TRY(h, cudaEventRecord(e.fwd_end, st));
 
@@ -847,7 +1123,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
 
         // ---- backward over the whole graph (cross-part children are final by
         // the time their parents' level runs: levels are global)
-        TRY(backward_sweep(h, h->full, depth, ng, debug, st));
+        if (adaptive) TRY(backward_adaptive(h, h->full, depth, reps, ng, debug, st));
+        else TRY(backward_sweep(h, h->full, depth, ng, debug, st));
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
 
         if (want_reports && h->k == 2) {
@@ -948,9 +1225,15 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             if (dbg_sigma) CUDA_TRY(h, cudaMemsetAsync(dbg_sigma, 0, rows * sizeof(double), st));
             if (dbg_delta) CUDA_TRY(h, cudaMemsetAsync(dbg_delta, 0, rows * sizeof(double), st));
             for (int L = 0; L < depth; ++L) {
-                extract_level_kernel<<<dim3(grid1d((size_t)n, 256, 1184), 1), 256, 0, st>>>(
-                    h->lvl[L], h->live + (size_t)L * h->alloc_groups, h->sigma, h->delta, n, L,
-                    dbg_dist, dbg_sigma, dbg_delta);
+                if (adaptive && reps[L].slot < 0) {
+                    TRY(upload_ranges(h, reps[L], st));
+                    extract_queue_kernel<<<dim3(queue_blocks(reps[L], 256), 1), 256, 0, st>>>(
+                        queue_params(h), h->sigma, h->delta, n, L, dbg_dist, dbg_sigma, dbg_delta);
+                } else {
+                    extract_level_kernel<<<dim3(grid1d((size_t)n, 256, 1184), 1), 256, 0, st>>>(
+                        h->lvl[adaptive ? reps[L].slot : L], h->live + (size_t)L * h->alloc_groups,
+                        h->sigma, h->delta, n, L, dbg_dist, dbg_sigma, dbg_delta);
+                }
                 ++h->launches;
             }
             CUDA_TRY(h, cudaGetLastError());
@@ -1107,6 +1390,15 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     }
     if (k == "reports") {
         h->reports = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "sparse") {
+        h->sparse = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "push_beta") {
+        if (value < 1) return h->fail(BC_ERR_INPUT, "push_beta must be >= 1");
+        h->push_beta = (int)value;
         return BC_OK;
     }
     return h->fail(BC_ERR_INPUT, "unknown option '" + k + "'");

@@ -61,6 +61,7 @@ struct LevelParams {
     const uint32_t *live_prev;  // forward: live[L-1]; backward: live[L]
     uint32_t *live_cur;         // forward: live[L], OR-ed by this launch
     unsigned long long *counters;  // [0] n_r, [1] A_r, [2] T
+    unsigned long long *lstat;     // forward: [0] vertices discovered, [1] their arcs, [2] largest degree (may be null)
     int accumulate_bc;
 };
 
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kern
     double *delta = STORE_DELTA ? p.delta + g * p.n * 32 : nullptr;
     const double *val = BWD ? coef : sigma;
 
-    unsigned long long c_nr = 0, c_ar = 0;
+    unsigned long long c_nr = 0, c_ar = 0, c_nv = 0, c_fa = 0, c_md = 0;
     unsigned c_t = 0;  // per-lane partial
     uint32_t any_new = 0;
 
@@ -288,6 +289,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kern
                 any_new |= got;
                 c_nr += __popc(got);
                 c_ar += (unsigned long long)__popc(got) * (unsigned long long)(ve - vb);
+                if (got) {
+                    c_nv += 1;
+                    c_fa += (unsigned long long)(ve - vb);
+                    c_md = max(c_md, (unsigned long long)(ve - vb));
+                }
             }
         }
     }
@@ -298,6 +304,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kern
             if (c_nr) atomicAdd(p.counters + 0, c_nr);
             if (c_ar) atomicAdd(p.counters + 1, c_ar);
             if (t) atomicAdd(p.counters + 2, (unsigned long long)t);
+            if (c_nv && p.lstat) {
+                atomicAdd(p.lstat + 0, c_nv);
+                atomicAdd(p.lstat + 1, c_fa);
+                atomicMax(p.lstat + 2, c_md);
+            }
         }
     }
 }
@@ -321,6 +332,7 @@ struct HubParams {
     const uint32_t *live_prev;
     uint32_t *live_cur;
     unsigned long long *counters;
+    unsigned long long *lstat;
     int accumulate_bc;
 };
 
@@ -361,6 +373,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) hub_kernel(const HubParam
             atomicAdd(p.counters + 0, (unsigned long long)__popc(got));
             atomicAdd(p.counters + 1,
                       (unsigned long long)__popc(got) * (unsigned long long)(p.off[v + 1] - p.off[v]));
+            if (p.lstat) {
+                atomicAdd(p.lstat + 0, 1ull);
+                atomicAdd(p.lstat + 1, (unsigned long long)(p.off[v + 1] - p.off[v]));
+                atomicMax(p.lstat + 2, (unsigned long long)(p.off[v + 1] - p.off[v]));
+            }
         }
     }
 }
@@ -415,6 +432,219 @@ __global__ void extract_level_kernel(const uint32_t *lvl, const uint32_t *live_l
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         uint32_t m = lvl[g * n + v];
+        while (m) {
+            const int lane = __ffs(m) - 1;
+            m &= m - 1;
+            const size_t row = (g * 32 + lane) * (size_t)n + v;
+            const size_t idx = (g * n + v) * 32 + lane;
+            if (dist_out) dist_out[row] = level;
+            if (sigma_out) sigma_out[row] = sigma[idx];
+            if (delta_out) delta_out[row] = delta[idx];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Sparse levels: frontier queues and top-down (push) expansion.
+//
+// A level whose frontier is small is kept as a queue of (vertex, lane mask)
+// entries per group instead of a dense mask array, and is produced top-down:
+// every frontier vertex pushes along its arcs into the vertices its lanes have
+// not seen.  Path counts are added with red.global.add.f64 -- they are
+// integer-valued, so the sum is exact in any order and the result stays
+// deterministic (sigma is zeroed per batch when push may run).  The host picks
+// push or pull per level from the frontier's arc count (direction-optimising
+// switch); dense pull levels read a queue level through a scratch mask array.
+// ------------------------------------------------------------------------------------
+
+struct QueueParams {
+    int32_t *q_v;          // [group][cap] vertex of the entry
+    uint32_t *q_m;         // [group][cap] lanes at that vertex
+    int64_t cap;           // entries per group
+    unsigned long long *q_count;  // [group] entries used so far
+    const int64_t *q_beg;  // [group] first entry of the level being read
+    const int64_t *q_end;  // [group] one past its last entry
+};
+
+constexpr int kStage = 128;  // per-warp shared-memory staging buffer (queue entries)
+
+// Top-down expansion of level L-1 (a queue) into level L.  Lanes = arcs.
+// next[] must be all zero on entry; it holds the new level's masks on exit
+// (push_post_kernel moves them into the queue and clears next[] again).
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_kernel(
+    const int64_t *__restrict__ off, const int32_t *__restrict__ col, int64_t n, QueueParams q,
+    const uint32_t *__restrict__ vis, uint32_t *next, double *sigma,
+    unsigned long long *counters) {
+    __shared__ int32_t stage[kWarpsPerBlock][kStage];
+    const size_t g = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t beg = q.q_beg[g], end = q.q_end[g];
+    const int64_t stride = (int64_t)gridDim.x * kWarpsPerBlock;
+    const uint32_t *gvis = vis + g * n;
+    uint32_t *gnext = next + g * n;
+    double *gsig = sigma + g * n * 32;
+    int staged = 0;      // warp-uniform
+    unsigned c_t = 0;
+    auto flush = [&]() {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(q.q_count + g, (unsigned long long)staged);
+        base = __shfl_sync(kFull, base, 0);
+        for (int i = lane; i < staged; i += 32) q.q_v[g * q.cap + base + i] = stage[warp][i];
+        staged = 0;
+        __syncwarp();
+    };
+    for (int64_t i = beg + (int64_t)blockIdx.x * kWarpsPerBlock + warp; i < end; i += stride) {
+        const int32_t u = q.q_v[g * q.cap + i];
+        const uint32_t mask = q.q_m[g * q.cap + i];
+        const int64_t b = off[u], e = off[u + 1];
+        const double *urow = gsig + (size_t)u * 32;
+        for (int64_t base = b; base < e; base += 32) {
+            const int64_t k = base + lane;
+            bool fresh_vertex = false;
+            int32_t w = 0;
+            if (k < e) {
+                w = __ldg(col + k);
+                uint32_t fresh = mask & ~gvis[w];
+                if (fresh) {
+                    const uint32_t old = atomicOr(gnext + w, fresh);
+                    fresh_vertex = old == 0;
+                    double *wrow = gsig + (size_t)w * 32;
+                    while (fresh) {
+                        const int bit = __ffs(fresh) - 1;
+                        fresh &= fresh - 1;
+                        atomicAdd(wrow + bit, urow[bit]);   // exact: integer-valued fp64
+                        ++c_t;
+                    }
+                }
+            }
+            const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+            if (newm) {
+                if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
+                staged += __popc(newm);
+                __syncwarp();
+                if (staged > kStage - 32) flush();
+            }
+        }
+    }
+    if (staged) flush();
+    const unsigned t = __reduce_add_sync(kFull, c_t);
+    if (lane == 0 && t) atomicAdd(counters + 2, (unsigned long long)t);
+}
+
+// After a push: entries [q_lbeg[g], q_count[g]) are the new level.  Record
+// their masks, mark them seen, clear next[], gather the level's statistics.
+// lstat: [0] vertices in the level, [1] their arcs, [2] largest degree (all groups).
+__global__ void push_post_kernel(const int64_t *__restrict__ off, int64_t n, QueueParams q,
+                                 const int64_t *q_lbeg, uint32_t *vis, uint32_t *next,
+                                 uint32_t *live_cur, unsigned long long *counters,
+                                 unsigned long long *lstat) {
+    const size_t g = blockIdx.y;
+    const int64_t beg = q_lbeg[g], end = (int64_t)q.q_count[g];
+    unsigned long long nr = 0, ar = 0, nv = 0, fa = 0, md = 0;
+    uint32_t any = 0;
+    for (int64_t i = beg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t w = q.q_v[g * q.cap + i];
+        const uint32_t m = next[g * n + w];
+        q.q_m[g * q.cap + i] = m;
+        vis[g * n + w] |= m;
+        next[g * n + w] = 0u;
+        const unsigned long long deg = (unsigned long long)(off[w + 1] - off[w]);
+        any |= m;
+        nr += __popc(m);
+        ar += __popc(m) * deg;
+        nv += 1;
+        fa += deg;
+        md = max(md, deg);
+    }
+    any = __reduce_or_sync(kFull, any);
+    for (int o = 16; o > 0; o >>= 1) {
+        nr += __shfl_xor_sync(kFull, nr, o);
+        ar += __shfl_xor_sync(kFull, ar, o);
+        nv += __shfl_xor_sync(kFull, nv, o);
+        fa += __shfl_xor_sync(kFull, fa, o);
+        md = max(md, __shfl_xor_sync(kFull, md, o));
+    }
+    if ((threadIdx.x & 31) == 0 && nv) {
+        atomicOr(live_cur + g, any);
+        atomicAdd(counters + 0, nr);
+        atomicAdd(counters + 1, ar);
+        atomicAdd(lstat + 0, nv);
+        atomicAdd(lstat + 1, fa);
+        atomicMax(lstat + 2, md);
+    }
+}
+
+// Write (clear = 0) or erase (clear = 1) a queue level in a dense mask array.
+__global__ void scatter_queue_kernel(QueueParams q, int64_t n, uint32_t *dense, int clear) {
+    const size_t g = blockIdx.y;
+    const int64_t beg = q.q_beg[g], end = q.q_end[g];
+    for (int64_t i = beg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dense[g * n + q.q_v[g * q.cap + i]] = clear ? 0u : q.q_m[g * q.cap + i];
+}
+
+// Dense level -> queue (needed when a push level follows a pull level).
+__global__ void compact_level_kernel(const uint32_t *__restrict__ lvl, const uint32_t *live_level,
+                                     int64_t n, QueueParams q) {
+    const size_t g = blockIdx.y;
+    if (live_level[g] == 0) return;
+    const int lane = threadIdx.x & 31;
+    for (int64_t v0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; v0 < n;
+         v0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = v0 + lane;
+        const uint32_t m = v < n ? lvl[g * n + v] : 0u;
+        const unsigned has = __ballot_sync(kFull, m != 0);
+        if (!has) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(q.q_count + g, (unsigned long long)__popc(has));
+        base = __shfl_sync(kFull, base, 0);
+        if (m) {
+            const size_t at = g * q.cap + base + __popc(has & ((1u << lane) - 1u));
+            q.q_v[at] = (int32_t)v;
+            q.q_m[at] = m;
+        }
+    }
+}
+
+// Backward over a queue level: one warp per entry, same arithmetic as the
+// dense kernel (scan_arcs + finalize_backward).
+template <bool STORE_DELTA>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) bwd_queue_kernel(
+    const int64_t *__restrict__ off, const int32_t *__restrict__ col, int64_t n, QueueParams q,
+    const uint32_t *nbr, const double *sigma, double *coef, double *delta, double *bcg,
+    int accumulate) {
+    const size_t g = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int64_t beg = q.q_beg[g], end = q.q_end[g];
+    const int64_t stride = (int64_t)gridDim.x * kWarpsPerBlock;
+    const uint32_t *gn = nbr ? nbr + g * n : nullptr;
+    unsigned unused = 0;
+    for (int64_t i = beg + (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); i < end;
+         i += stride) {
+        const int64_t v = q.q_v[g * q.cap + i];
+        const uint32_t want = q.q_m[g * q.cap + i];
+        double acc = 0.0;
+        uint32_t got = 0;
+        if (gn != nullptr)
+            scan_arcs<false>(off[v], off[v + 1], want, col, gn, coef + g * n * 32, lane, acc, got,
+                             unused);
+        finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma + g * n * 32, coef + g * n * 32,
+                                       STORE_DELTA ? delta + g * n * 32 : nullptr, bcg + g * n,
+                                       accumulate);
+    }
+}
+
+// Inspection of a queue level (see extract_level_kernel).
+__global__ void extract_queue_kernel(QueueParams q, const double *sigma, const double *delta,
+                                     int64_t n, int level, int32_t *dist_out, double *sigma_out,
+                                     double *delta_out) {
+    const size_t g = blockIdx.y;
+    const int64_t beg = q.q_beg[g], end = q.q_end[g];
+    for (int64_t i = beg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = q.q_v[g * q.cap + i];
+        uint32_t m = q.q_m[g * q.cap + i];
         while (m) {
             const int lane = __ffs(m) - 1;
             m &= m - 1;

@@ -211,3 +211,29 @@ def test_config2_rmat20_sample():
     deg = np.diff(g.offsets)
     assert not bc[deg == 0].any() and bc.min() >= 0.0
     assert st["sources"] == 1024 and st["max_levels"] >= 5
+
+
+def test_push_pull_switch_equivalence():
+    # queue levels + top-down push (default) against dense pull only: same dist / sigma / BC
+    cases = [G.rmat(13, 16, 3), G.road_like(64, 64, keep=0.2, seed=2), G.erdos_renyi(4000, 12000, 3)]
+    for g in cases:
+        rng = np.random.default_rng(9)
+        srcs = rng.choice(g.num_vertices, size=70, replace=False).tolist()
+        out = {}
+        for sparse in (0, 1):
+            with Engine(g) as e:
+                e.set_option("sparse", sparse)
+                e.set_option("groups", 2)
+                d, s, dl = e.debug_sources(srcs[:33])
+                bc, st = e.run(srcs)
+            out[sparse] = (d, s, dl, bc, st)
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+        assert np.allclose(out[0][2], out[1][2], rtol=1e-12, atol=1e-12)
+        assert np.allclose(out[0][3], out[1][3], rtol=1e-12, atol=1e-12)
+        for key in ("reached", "arcs_reached", "dag_arcs", "max_levels"):
+            assert out[0][4][key] == out[1][4][key], key
+        assert_sources_match_oracle(g, srcs[:33], out[1][0], out[1][1], out[1][2])
+        with Engine(g) as e:      # push at (almost) every level
+            e.set_option("push_beta", 1)
+            bc1, _ = e.run(srcs)
+        assert np.allclose(bc1, out[0][3], rtol=1e-12, atol=1e-12)

@@ -9,6 +9,6 @@ python bench.py --impl reference --steps 2 --warmup 1 2>> gpurun_out/bench.err |
 tail -5 gpurun_out/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 0 --sources 256 --no-cpu > gpurun_out/bench_under_ncu.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:level_kernel -s 6 -c 14 -o gpurun_out/prof_level \
+ncu --set full --clock-control none --import-source on -k regex:level_kernel -c 16 -o gpurun_out/prof_level \
     python bench.py --steps 1 --warmup 0 --sources 256 --no-cpu > gpurun_out/bench_under_ncu2.log 2>&1
 ls -la gpurun_out
