@@ -229,6 +229,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     g, label = workload(args.workload)
+    g.pin()                                    # e2e copies the CSR from pinned host memory
     n, m = g.num_vertices, g.num_edges
     all_sources = pick_sources(n, args.sources * world)
     mine = all_sources[rank::world]            # 1024 per rank: weak scaling

@@ -48,8 +48,8 @@ constexpr double kMaxTableBytes = 64e9;
 struct bc_handle {
     int device = 0;
     int64_t n = 0, n_arcs = 0;
-    std::vector<int64_t> h_off;   // host copies (item building, partition set-up)
-    std::vector<int32_t> h_col;
+    std::vector<int64_t> h_off;   // host copy of the offsets (item building, partition set-up)
+    std::vector<int32_t> h_col;   // host copy of col_idx, fetched from the device when a partition is set
     Csr full;
     // options
     int groups = 4;
@@ -1010,11 +1010,18 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         // the order only moves fp64 rounding; the inspection path keeps the
         // caller's order because its output rows follow it.
         std::vector<int64_t> key(active.size());
-        for (size_t i = 0; i < active.size(); ++i) {
-            int64_t sum = 0;
-            for (int64_t a = h->h_off[active[i]]; a < h->h_off[active[i] + 1]; ++a)
-                sum += h->h_off[h->h_col[a] + 1] - h->h_off[h->h_col[a]];
-            key[i] = sum;
+        if (!active.empty()) {
+            int64_t *d_tmp = nullptr;
+            CUDA_TRY(h, cudaMalloc((void **)&d_tmp, 2 * active.size() * sizeof(int64_t)));
+            CUDA_TRY(h, cudaMemcpyAsync(d_tmp, active.data(), active.size() * sizeof(int64_t),
+                                        cudaMemcpyHostToDevice, st));
+            source_key_kernel<<<grid1d(active.size() * 32, 256), 256, 0, st>>>(
+                h->full.off, h->full.col, d_tmp, (int64_t)active.size(), d_tmp + active.size());
+            ++h->launches;
+            CUDA_TRY(h, cudaMemcpyAsync(key.data(), d_tmp + active.size(), active.size() * sizeof(int64_t),
+                                        cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            cudaFree(d_tmp);
         }
         std::vector<size_t> order(active.size());
         for (size_t i = 0; i < order.size(); ++i) order[i] = i;
@@ -1337,7 +1344,6 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
     h->n = n;
     h->n_arcs = n_arcs;
     h->h_off.assign(offsets, offsets + n + 1);
-    h->h_col.assign(col_idx, col_idx + n_arcs);
     auto bail = [&](int rc) {
         g_create_error = h->err;
         bc_destroy(h);
@@ -1417,6 +1423,12 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     h->k = k;
     h->h_part.assign(assignment, assignment + n);
     if (k == 1) return BC_OK;
+    if ((int64_t)h->h_col.size() != h->n_arcs) {
+        h->h_col.resize((size_t)h->n_arcs);
+        if (h->n_arcs > 0)
+            CUDA_TRY(h, cudaMemcpy(h->h_col.data(), h->full.col, h->n_arcs * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost));
+    }
     const int64_t *off = h->h_off.data();
     const int32_t *col = h->h_col.data();
     // cut-free CSR + border lists (ascending vertex id inside each part)

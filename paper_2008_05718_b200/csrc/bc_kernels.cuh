@@ -657,6 +657,23 @@ __global__ void extract_queue_kernel(QueueParams q, const double *sigma, const d
     }
 }
 
+// key[i] = sum of the degrees of the neighbours of source i (size of its
+// 2-hop neighbourhood, used to group like sources).  One warp per source.
+__global__ void source_key_kernel(const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                  const int64_t *src, int64_t k, int64_t *key) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= k) return;
+    const int64_t s = src[i];
+    long long sum = 0;
+    for (int64_t a = off[s] + lane; a < off[s + 1]; a += 32) {
+        const int64_t w = col[a];
+        sum += off[w + 1] - off[w];
+    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+    if (lane == 0) key[i] = sum;
+}
+
 __global__ void fill_i32_kernel(int32_t *p, size_t count, int32_t value) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (size_t)gridDim.x * blockDim.x)

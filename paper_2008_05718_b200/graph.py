@@ -106,6 +106,29 @@ class Graph:
             )
         return self._cache["adj"]
 
+    def pin(self) -> "Graph":
+        """Move ``offsets`` / ``col_idx`` into page-locked host memory so the
+        host-to-device copy of the CSR runs at full PCIe speed (no-op without
+        CUDA).  torch is used only as the pinned allocator."""
+        if self._cache.get("pinned"):
+            return self
+        try:
+            import torch
+            if not torch.cuda.is_available():
+                return self
+            for name in ("offsets", "col_idx"):
+                arr = getattr(self, name)
+                t = torch.empty(arr.shape, dtype=torch.int64 if arr.dtype == np.int64 else torch.int32,
+                                pin_memory=True)
+                buf = t.numpy()
+                buf[...] = arr
+                self._cache["pin_" + name] = t      # keeps the allocation alive
+                setattr(self, name, buf)
+            self._cache["pinned"] = True
+        except Exception:
+            pass
+        return self
+
     def degree(self, v: int) -> int:
         return int(self.offsets[v + 1] - self.offsets[v])
 
