@@ -130,6 +130,36 @@ int bc_get_border_tables(bc_handle *h, int part, int32_t *borders, int32_t *bm, 
 int bc_get_border_frontier(bc_handle *h, int64_t n_lanes, int32_t *dist, double *sigma,
                            double *arrival);
 
+/* ---- graph-partitioned multi-GPU mode: one rank = one part = one GPU -------
+ * The handle is created on the rank's own CSR rows (global vertex ids, empty
+ * rows for vertices of other parts).  The host code (one process per GPU,
+ * torch.distributed) drives a batch level by level and moves the exported
+ * buffers with NCCL all-gathers; these calls are the device side of the
+ * reference's cross-worker transfers (bsp.py:83-87,128-135, ledger.py:28-31).
+ * `assignment` is the global part map; border_off[world+1] / border_v list every
+ * rank's border vertices (ascending ids per rank, partition.py:148). */
+int bc_dist_setup(bc_handle *h, int rank, int world, const int32_t *assignment,
+                  const int64_t *border_off, const int32_t *border_v);
+/* Start a batch of `count` sources (<= 32 * groups): every rank plants all seeds. */
+int bc_dist_begin(bc_handle *h, const int64_t *sources, int64_t count, void *stream);
+/* Local work of forward level L (pull from level L-1) / backward level L. */
+int bc_dist_forward_level(bc_handle *h, int level, void *stream);
+int bc_dist_backward_level(bc_handle *h, int level, int deepest, void *stream);
+/* Export this rank's border state of `level`: masks_dev[nb * groups] u32 (what = 0
+ * only reads them back into the scan), then values_dev[*count_out] fp64 of
+ * what = 1 (sigma, forward) or 2 (coef, backward).  Buffers are device memory. */
+int bc_dist_export(bc_handle *h, int level, int what, void *masks_dev, void *values_dev,
+                   int64_t value_capacity, int64_t *count_out, void *stream);
+/* Import rank `from`'s border state of `level` (forward: masks + sigma, also marks
+ * the lanes visited; backward: coef under the masks exported on the way forward). */
+int bc_dist_import(bc_handle *h, int level, int what, int from, const void *masks_dev,
+                   const void *values_dev, void *stream);
+/* live[level][g] (lanes with a non-empty frontier), read / overwrite with the OR over ranks. */
+int bc_dist_get_live(bc_handle *h, int level, uint32_t *live_out, void *stream);
+int bc_dist_set_live(bc_handle *h, int level, const uint32_t *live, void *stream);
+/* bc_dev[v] += BC partials of the vertices this rank owns (others untouched). */
+int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream);
+
 const char *bc_last_error(bc_handle *h);
 void bc_destroy(bc_handle *h);
 

@@ -26,6 +26,8 @@ SYMBOLS = (
     "bc_create", "bc_set_option", "bc_set_partition", "bc_run", "bc_run_device",
     "bc_debug_sources", "bc_get_reports", "bc_get_border_counts", "bc_get_border_tables",
     "bc_get_border_frontier",
+    "bc_dist_setup", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
+    "bc_dist_export", "bc_dist_import", "bc_dist_get_live", "bc_dist_set_live", "bc_dist_finish",
     "bc_last_error", "bc_destroy",
 )
 
@@ -82,6 +84,24 @@ def load():
     L.bc_get_border_tables.argtypes = [vp, cint, vp, vp, vp]
     L.bc_get_border_frontier.restype = cint
     L.bc_get_border_frontier.argtypes = [vp, i64, vp, vp, vp]
+    L.bc_dist_setup.restype = cint
+    L.bc_dist_setup.argtypes = [vp, cint, cint, vp, vp, vp]
+    L.bc_dist_begin.restype = cint
+    L.bc_dist_begin.argtypes = [vp, vp, i64, vp]
+    L.bc_dist_forward_level.restype = cint
+    L.bc_dist_forward_level.argtypes = [vp, cint, vp]
+    L.bc_dist_backward_level.restype = cint
+    L.bc_dist_backward_level.argtypes = [vp, cint, cint, vp]
+    L.bc_dist_export.restype = cint
+    L.bc_dist_export.argtypes = [vp, cint, cint, vp, vp, i64, ctypes.POINTER(i64), vp]
+    L.bc_dist_import.restype = cint
+    L.bc_dist_import.argtypes = [vp, cint, cint, cint, vp, vp, vp]
+    L.bc_dist_get_live.restype = cint
+    L.bc_dist_get_live.argtypes = [vp, cint, vp, vp]
+    L.bc_dist_set_live.restype = cint
+    L.bc_dist_set_live.argtypes = [vp, cint, vp, vp]
+    L.bc_dist_finish.restype = cint
+    L.bc_dist_finish.argtypes = [vp, vp, vp]
     L.bc_last_error.restype = ctypes.c_char_p
     L.bc_last_error.argtypes = [vp]
     L.bc_destroy.restype = None
@@ -217,3 +237,49 @@ class Engine:
         if rc != BC_OK:
             self._raise(rc)
         return d, s, a
+
+    # -- graph-partitioned multi-GPU mode (device pointers are raw ints) ----
+    def _ck(self, rc):
+        if rc != BC_OK:
+            self._raise(rc)
+
+    def dist_setup(self, rank, world, assignment, border_off, border_v):
+        a = np.ascontiguousarray(assignment, dtype=np.int32)
+        bo = np.ascontiguousarray(border_off, dtype=np.int64)
+        bv = np.ascontiguousarray(border_v, dtype=np.int32)
+        self._ck(self._lib.bc_dist_setup(self._h, int(rank), int(world), _ptr(a), _ptr(bo), _ptr(bv)))
+
+    def dist_begin(self, sources, stream=0):
+        src = np.ascontiguousarray(sources, dtype=np.int64)
+        self._ck(self._lib.bc_dist_begin(self._h, _ptr(src), len(src), ctypes.c_void_p(stream or None)))
+
+    def dist_forward_level(self, level, stream=0):
+        self._ck(self._lib.bc_dist_forward_level(self._h, int(level), ctypes.c_void_p(stream or None)))
+
+    def dist_backward_level(self, level, deepest, stream=0):
+        self._ck(self._lib.bc_dist_backward_level(self._h, int(level), int(bool(deepest)),
+                                                  ctypes.c_void_p(stream or None)))
+
+    def dist_export(self, level, what, masks_ptr, values_ptr, capacity, stream=0) -> int:
+        count = ctypes.c_int64(0)
+        self._ck(self._lib.bc_dist_export(self._h, int(level), int(what), ctypes.c_void_p(masks_ptr),
+                                          ctypes.c_void_p(values_ptr or None), int(capacity),
+                                          ctypes.byref(count), ctypes.c_void_p(stream or None)))
+        return count.value
+
+    def dist_import(self, level, what, peer, masks_ptr, values_ptr, stream=0):
+        self._ck(self._lib.bc_dist_import(self._h, int(level), int(what), int(peer),
+                                          ctypes.c_void_p(masks_ptr), ctypes.c_void_p(values_ptr or None),
+                                          ctypes.c_void_p(stream or None)))
+
+    def dist_get_live(self, level, groups, stream=0):
+        out = np.zeros(groups, dtype=np.uint32)
+        self._ck(self._lib.bc_dist_get_live(self._h, int(level), _ptr(out), ctypes.c_void_p(stream or None)))
+        return out
+
+    def dist_set_live(self, level, live, stream=0):
+        a = np.ascontiguousarray(live, dtype=np.uint32)
+        self._ck(self._lib.bc_dist_set_live(self._h, int(level), _ptr(a), ctypes.c_void_p(stream or None)))
+
+    def dist_finish(self, bc_dev_ptr, stream=0):
+        self._ck(self._lib.bc_dist_finish(self._h, ctypes.c_void_p(bc_dev_ptr), ctypes.c_void_p(stream or None)))

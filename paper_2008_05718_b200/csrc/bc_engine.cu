@@ -8,7 +8,10 @@
 // bc_border.cuh or fails.
 #include "bc_b200.h"
 #include "bc_border.cuh"
+#include "bc_dist.cuh"
 #include "bc_kernels.cuh"
+
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -113,6 +116,14 @@ struct bc_handle {
     int64_t *d_src = nullptr;
     int64_t d_src_cap = 0;
     double *bc_scratch = nullptr;  // device bc vector of bc_run
+    // ---- graph-partitioned multi-GPU mode (one rank = one part)
+    int dist_rank = -1, dist_world = 0, dist_ng = 0, dist_cnt = 0;
+    std::vector<int64_t> dist_border_off;
+    int32_t *dist_border_v = nullptr;   // all ranks' borders, rank-major
+    int32_t *dist_counts = nullptr, *dist_offsets = nullptr;
+    void *dist_scan_tmp = nullptr;
+    size_t dist_scan_bytes = 0;
+    int64_t dist_entries_cap = 0;
     std::string err;
     int64_t launches = 0;
 
@@ -1308,6 +1319,35 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     return BC_OK;
 }
 
+
+// ------------------------------------------------------------------------------------
+// graph-partitioned multi-GPU mode
+// ------------------------------------------------------------------------------------
+
+int dist_check(bc_handle *h, int level) {
+    if (h->dist_rank < 0) return h->fail(BC_ERR_INPUT, "bc_dist_*: call bc_dist_setup first");
+    if (h->dist_ng <= 0) return h->fail(BC_ERR_INPUT, "bc_dist_*: no batch in flight (bc_dist_begin)");
+    if (level < 0) return h->fail(BC_ERR_INPUT, "bc_dist_*: negative level");
+    return BC_OK;
+}
+
+// offsets = exclusive scan of counts over `entries` items (CUB), entries + 1 outputs
+int dist_scan(bc_handle *h, int entries, cudaStream_t st) {
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, h->dist_counts, h->dist_offsets, entries + 1, st);
+    if (need > h->dist_scan_bytes) {
+        cudaFree(h->dist_scan_tmp);
+        h->dist_scan_tmp = nullptr;
+        CUDA_TRY(h, cudaMalloc(&h->dist_scan_tmp, need));
+        h->dist_scan_bytes = need;
+    }
+    CUDA_TRY(h, cudaMemsetAsync(h->dist_counts + entries, 0, sizeof(int32_t), st));
+    CUDA_TRY(h, cub::DeviceScan::ExclusiveSum(h->dist_scan_tmp, need, h->dist_counts, h->dist_offsets,
+                                              entries + 1, st));
+    ++h->launches;
+    return BC_OK;
+}
+
 int check_mode(bc_handle *h, int mode) {
     if (mode != BC_MODE_DIRECT && mode != BC_MODE_HYBIR && mode != BC_MODE_BSP)
         return h->fail(BC_ERR_INPUT, "unknown mode (use BC_MODE_DIRECT, BC_MODE_HYBIR or BC_MODE_BSP)");
@@ -1594,6 +1634,185 @@ int bc_get_border_frontier(bc_handle *h, int64_t n_lanes, int32_t *dist, double 
     return BC_OK;
 }
 
+
+int bc_dist_setup(bc_handle *h, int rank, int world, const int32_t *assignment,
+                  const int64_t *border_off, const int32_t *border_v) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (world < 1 || rank < 0 || rank >= world || !assignment || !border_off || border_off[0] != 0)
+        return h->fail(BC_ERR_INPUT, "bc_dist_setup: bad rank / world / border lists");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    h->dist_rank = rank;
+    h->dist_world = world;
+    h->dist_border_off.assign(border_off, border_off + world + 1);
+    const int64_t total = border_off[world];
+    int64_t widest = 0;
+    for (int r = 0; r < world; ++r) widest = std::max(widest, border_off[r + 1] - border_off[r]);
+    for (int64_t i = 0; i < total; ++i)
+        if (border_v[i] < 0 || border_v[i] >= h->n)
+            return h->fail(BC_ERR_INPUT, "bc_dist_setup: border vertex out of range");
+    std::vector<int32_t> bv(border_v, border_v + total);
+    if (bv.empty()) bv.push_back(0);
+    TRY(upload(h, &h->dist_border_v, bv));
+    h->h_part.assign(assignment, assignment + h->n);
+    TRY(upload(h, &h->d_part, h->h_part));
+    h->dist_entries_cap = widest * std::max(h->groups, 1);
+    TRY(dev_alloc(h, &h->dist_counts, (size_t)h->dist_entries_cap + 1));
+    TRY(dev_alloc(h, &h->dist_offsets, (size_t)h->dist_entries_cap + 1));
+    return BC_OK;
+}
+
+int bc_dist_begin(bc_handle *h, const int64_t *sources, int64_t count, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (h->dist_rank < 0) return h->fail(BC_ERR_INPUT, "bc_dist_begin: call bc_dist_setup first");
+    if (count < 1 || count > 32 * (int64_t)h->groups || sources == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_begin: need 1 <= count <= 32 * groups sources");
+    for (int64_t i = 0; i < count; ++i)
+        if (sources[i] < 0 || sources[i] >= h->n)
+            return h->fail(BC_ERR_INPUT, "bc_dist_begin: source out of range");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    TRY(ensure_state(h, h->groups, false));
+    TRY(ensure_levels(h, 2));
+    if (h->d_src_cap < count) {
+        cudaFree(h->d_src);
+        h->d_src = nullptr;
+        CUDA_TRY(h, cudaMalloc((void **)&h->d_src, count * sizeof(int64_t)));
+        h->d_src_cap = count;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(h->d_src, sources, count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    h->dist_cnt = (int)count;
+    h->dist_ng = (int)((count + 31) / 32);
+    if ((int64_t)h->dist_ng * (h->dist_entries_cap / std::max(h->groups, 1)) > h->dist_entries_cap)
+        return h->fail(BC_ERR_INTERNAL, "bc_dist_begin: scan buffers too small");
+    return begin_batch(h, h->d_src, (int)count, h->dist_ng, st);
+}
+
+int bc_dist_forward_level(bc_handle *h, int level, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level - 1));
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    TRY(ensure_levels(h, level + 1));
+    return launch_forward(h, h->full, level, h->dist_ng, (cudaStream_t)stream);
+}
+
+int bc_dist_backward_level(bc_handle *h, int level, int deepest, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    return launch_backward(h, h->full, level, deepest != 0, h->dist_ng, false, true,
+                           (cudaStream_t)stream);
+}
+
+int bc_dist_export(bc_handle *h, int level, int what, void *masks_dev, void *values_dev,
+                   int64_t value_capacity, int64_t *count_out, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (level >= (int)h->lvl.size() || masks_dev == nullptr || what < 0 || what > 2)
+        return h->fail(BC_ERR_INPUT, "bc_dist_export: bad level / buffer / kind");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int r = h->dist_rank, ng = h->dist_ng;
+    const int nb = (int)(h->dist_border_off[r + 1] - h->dist_border_off[r]);
+    const int entries = nb * ng;
+    int64_t count = 0;
+    if (entries > 0) {
+        const int32_t *bv = h->dist_border_v + h->dist_border_off[r];
+        dist_export_masks_kernel<<<grid1d((size_t)entries), 256, 0, st>>>(
+            h->lvl[level], bv, nb, ng, h->n, (uint32_t *)masks_dev, h->dist_counts);
+        ++h->launches;
+        if (what != 0) {
+            TRY(dist_scan(h, entries, st));
+            int32_t total = 0;
+            CUDA_TRY(h, cudaMemcpyAsync(&total, h->dist_offsets + entries, sizeof total,
+                                        cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            count = total;
+            if (count > value_capacity || (count > 0 && values_dev == nullptr))
+                return h->fail(BC_ERR_INPUT, "bc_dist_export: value buffer too small");
+            if (count > 0) {
+                dist_export_values_kernel<<<grid1d((size_t)entries), 256, 0, st>>>(
+                    what == 1 ? h->sigma : h->coef, bv, nb, ng, h->n, (const uint32_t *)masks_dev,
+                    h->dist_offsets, (double *)values_dev);
+                ++h->launches;
+            }
+        }
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    if (count_out) *count_out = count;
+    return BC_OK;
+}
+
+int bc_dist_import(bc_handle *h, int level, int what, int from, const void *masks_dev,
+                   const void *values_dev, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (from < 0 || from >= h->dist_world || from == h->dist_rank || what < 1 || what > 2 ||
+        level >= (int)h->lvl.size())
+        return h->fail(BC_ERR_INPUT, "bc_dist_import: bad peer / kind / level");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int ng = h->dist_ng;
+    const int nb = (int)(h->dist_border_off[from + 1] - h->dist_border_off[from]);
+    const int entries = nb * ng;
+    if (entries == 0) return BC_OK;
+    if (masks_dev == nullptr) return h->fail(BC_ERR_INPUT, "bc_dist_import: null masks");
+    const int32_t *bv = h->dist_border_v + h->dist_border_off[from];
+    if (what == 1) {
+        dist_import_masks_kernel<<<grid1d((size_t)entries), 256, 0, st>>>(
+            (const uint32_t *)masks_dev, bv, nb, ng, h->n, h->lvl[level], h->vis);
+        ++h->launches;
+    }
+    dist_count_kernel<<<grid1d((size_t)entries), 256, 0, st>>>((const uint32_t *)masks_dev, entries,
+                                                              h->dist_counts);
+    TRY(dist_scan(h, entries, st));
+    if (values_dev != nullptr) {
+        dist_import_values_kernel<<<grid1d((size_t)entries), 256, 0, st>>>(
+            (const double *)values_dev, bv, nb, ng, h->n, (const uint32_t *)masks_dev,
+            h->dist_offsets, what == 1 ? h->sigma : h->coef);
+        ++h->launches;
+    }
+    h->launches += 1;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+int bc_dist_get_live(bc_handle *h, int level, uint32_t *live_out, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (level >= h->live_cap || live_out == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_get_live: bad level");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(h, cudaMemcpyAsync(live_out, h->live + (size_t)level * h->alloc_groups,
+                                h->dist_ng * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    return BC_OK;
+}
+
+int bc_dist_set_live(bc_handle *h, int level, const uint32_t *live, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (level >= h->live_cap || live == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_set_live: bad level");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    CUDA_TRY(h, cudaMemcpyAsync(h->live + (size_t)level * h->alloc_groups, live,
+                                h->dist_ng * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                (cudaStream_t)stream));
+    return BC_OK;
+}
+
+int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (h->dist_rank < 0 || bc_dev == nullptr || h->bcg == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_finish: nothing to finish");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    dist_finish_kernel<<<grid1d((size_t)h->n, 256, 1184), 256, 0, (cudaStream_t)stream>>>(
+        bc_dev, h->bcg, h->d_part, h->dist_rank, h->n, h->alloc_groups);
+    ++h->launches;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
 const char *bc_last_error(bc_handle *h) {
     return h ? h->err.c_str() : g_create_error.c_str();
 }
@@ -1611,6 +1830,8 @@ void bc_destroy(bc_handle *h) {
     cudaFree(h->bc_scratch);
     cudaFree((void *)h->d_lvl_ptrs);
     cudaFree(h->presence);
+    cudaFree(h->dist_border_v), cudaFree(h->dist_counts), cudaFree(h->dist_offsets);
+    cudaFree(h->dist_scan_tmp);
     delete h;
 }
 

@@ -160,3 +160,20 @@ def test_generators_shapes():
     assert e.num_vertices == 64 and e.num_edges <= 256
     a = G.random_connected(30, 10, seed=4)
     assert O.brandes_single_source(a, 0)[3]["reached"] == 30
+
+
+def test_local_rows_for_graph_partitioned_mode():
+    from paper_2008_05718_b200.partitioned import local_rows
+    g = G.grid(6, 5)
+    part = P.strip_partition(6, 5, 3)
+    total = 0
+    for r in range(3):
+        lg = local_rows(g, part.assignment, r)
+        own = part.assignment == r
+        deg = np.diff(lg.offsets)
+        assert (deg[~own] == 0).all() and (deg[own] == np.diff(g.offsets)[own]).all()
+        for v in np.flatnonzero(own)[:5]:
+            assert lg.col_idx[lg.offsets[v]:lg.offsets[v + 1]].tolist() == \
+                g.col_idx[g.offsets[v]:g.offsets[v + 1]].tolist()
+        total += len(lg.col_idx)
+    assert total == g.num_arcs
