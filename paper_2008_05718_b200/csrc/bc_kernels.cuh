@@ -23,13 +23,25 @@
 
 namespace bcb200 {
 
-#ifndef BC_MIN_BLOCKS
-#define BC_MIN_BLOCKS 6
+// resident blocks per SM the compiler must allow (register cap = 65536 / (threads * blocks)):
+// the forward kernel keeps 40 registers (it spills below that), the backward kernel runs
+// better at 32 registers and full occupancy
+#ifndef BC_MIN_BLOCKS_FWD
+#define BC_MIN_BLOCKS_FWD 12
+#endif
+#ifndef BC_MIN_BLOCKS_BWD
+#define BC_MIN_BLOCKS_BWD 16
+#endif
+#ifndef BC_GATHER
+#define BC_GATHER 2  // 0: per-slice choice, 1: rows only, 2: columns above BC_SPARSE_SLICE hit arcs
 #endif
 #ifndef BC_SPARSE_SLICE
 #define BC_SPARSE_SLICE 2
 #endif
-constexpr int kWarpsPerBlock = 8;
+#ifndef BC_WPB
+#define BC_WPB 4
+#endif
+constexpr int kWarpsPerBlock = BC_WPB;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct LevelParams {
@@ -73,29 +85,37 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 // Predicated read-only load: one LDG under a predicate, never a branch (the
 // compiler turns `if (p) x = __ldg(..)` into divergent control flow here).
-__device__ __forceinline__ double ldg_if(const double *ptr, bool pred) {
+__device__ __forceinline__ double ldg_if(const double *ptr, uint32_t pred) {
     double x;
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
         "@q ld.global.nc.f64 %0, [%1];\n\t}"
         : "=d"(x)
-        : "l"(ptr), "r"((int)pred));
+        : "l"(ptr), "r"(pred));
     return x;
 }
 
 // 32 x 32 bit-matrix transpose across the warp: on return bit j of lane l is
 // bit l of lane j's input (five butterfly exchanges).
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-    uint32_t m = 0x0000ffffu;
+    // 16- and 8-bit stages are byte permutes (PRMT), the rest one shift + one LOP3 each
+    uint32_t o = __shfl_xor_sync(kFull, x, 16);
+    x = __byte_perm(x, o, (lane & 16) ? 0x3276 : 0x5410);
+    o = __shfl_xor_sync(kFull, x, 8);
+    x = __byte_perm(x, o, (lane & 8) ? 0x3715 : 0x6240);
 #pragma unroll
-    for (int j = 16; j != 0; j >>= 1) {
-        const uint32_t o = __shfl_xor_sync(kFull, x, j);
-        x = (lane & j) ? (((o >> j) & m) | (x & ~m)) : ((x & m) | ((o & m) << j));
-        m ^= m << (j >> 1);
+    for (int j = 4; j != 0; j >>= 1) {
+        const uint32_t m = j == 4 ? 0x0f0f0f0fu : (j == 2 ? 0x33333333u : 0x55555555u);
+        o = __shfl_xor_sync(kFull, x, j);
+        const bool upper = lane & j;
+        const uint32_t t = upper ? (o >> j) : (o << j);
+        const uint32_t keep = upper ? ~m : m;
+        x = (x & keep) | (t & ~keep);
     }
     return x;
 }
 
-constexpr int kSparseSlice = BC_SPARSE_SLICE;  // slices with at most this many hit arcs take the arc-serial path
+constexpr int kSparseSlice = BC_SPARSE_SLICE;
+constexpr int kRowUnroll = (BC_GATHER == 2 && BC_SPARSE_SLICE <= 2) ? 2 : 4;  // row loads in flight  // slices with at most this many hit arcs take the arc-serial path
 
 // Scan arcs [a0, a1) of one vertex.  `want` (warp-uniform) = lanes that still
 // need a value.  Filter: lanes = arcs, hit = mask[neighbour] & want.  Gather,
@@ -135,23 +155,44 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
         }
         unsigned any = __ballot_sync(kFull, hit != 0);
         if (any == 0) continue;
-        if (__popc(any) <= kSparseSlice) {
+        bool rows;
+        if (BC_GATHER == 1) rows = true;
+        else if (BC_GATHER == 2) rows = __popc(any) <= kSparseSlice;
+        else {
+            // rows cost ~10 instructions per hit arc; columns ~66 for the transpose plus ~13
+            // per element of the longest column, which is at least pairs / lanes hit
+            const int nh = __popc(any);
+            const unsigned lanes_hit = __reduce_or_sync(kFull, hit);
+            const int pairs = __reduce_add_sync(kFull, __popc(hit));
+            rows = 10 * nh <= 66 + 16 * (pairs / __popc(lanes_hit));
+        }
+        if (rows) {
+            const uint32_t lbit = 1u << lane;
             while (any) {
-                const int j0 = __ffs(any) - 1;
-                any &= any - 1;
-                const int j1 = __ffs(any) - 1;  // -1 when exhausted
-                any &= any - 1;
-                const int32_t w0 = __shfl_sync(kFull, w, j0);
-                const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
-                const uint32_t h0 = __shfl_sync(kFull, hit, j0);
-                uint32_t h1 = __shfl_sync(kFull, hit, j1 & 31);
-                if (j1 < 0) h1 = 0;
-                const double x0 = ldg_if(myval + (size_t)w0 * 32, (h0 >> lane) & 1u);
-                const double x1 = ldg_if(myval + (size_t)w1 * 32, (h1 >> lane) & 1u);
-                acc += x0;  // arc order is kept: j0 < j1
-                acc += x1;
-                got |= h0 | h1;
-                if (COUNT_T) tcount += ((h0 >> lane) & 1u) + ((h1 >> lane) & 1u);
+                int j[kRowUnroll];
+                int32_t wj[kRowUnroll];
+                uint32_t hj[kRowUnroll];
+                double x[kRowUnroll];
+#pragma unroll
+                for (int u = 0; u < kRowUnroll; ++u) {
+                    j[u] = __ffs(any) - 1;  // -1 when exhausted
+                    any &= any - 1;
+                }
+#pragma unroll
+                for (int u = 0; u < kRowUnroll; ++u) {
+                    wj[u] = __shfl_sync(kFull, w, j[u] & 31);
+                    hj[u] = __shfl_sync(kFull, hit, j[u] & 31);
+                    if (j[u] < 0) hj[u] = 0;
+                }
+#pragma unroll
+                for (int u = 0; u < kRowUnroll; ++u)
+                    x[u] = ldg_if(myval + (size_t)wj[u] * 32, hj[u] & lbit);
+#pragma unroll
+                for (int u = 0; u < kRowUnroll; ++u) {
+                    acc += x[u];  // arc order is kept: j[0] < j[1] < ...
+                    got |= hj[u];
+                    if (COUNT_T) tcount += (hj[u] & lbit) != 0;
+                }
             }
         } else {
             got |= __reduce_or_sync(kFull, hit);
@@ -174,10 +215,10 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
                 const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
                 const int32_t w2 = __shfl_sync(kFull, w, j2 & 31);
                 const int32_t w3 = __shfl_sync(kFull, w, j3 & 31);
-                const double x0 = ldg_if(myval + (size_t)w0 * 32, p0);
-                const double x1 = ldg_if(myval + (size_t)w1 * 32, p1);
-                const double x2 = ldg_if(myval + (size_t)w2 * 32, p2);
-                const double x3 = ldg_if(myval + (size_t)w3 * 32, p3);
+                const double x0 = ldg_if(myval + (size_t)w0 * 32, p0 ? 1u : 0u);
+                const double x1 = ldg_if(myval + (size_t)w1 * 32, p1 ? 1u : 0u);
+                const double x2 = ldg_if(myval + (size_t)w2 * 32, p2 ? 1u : 0u);
+                const double x3 = ldg_if(myval + (size_t)w3 * 32, p3 ? 1u : 0u);
                 acc += x0;  // ascending arc order within the lane
                 acc += x1;
                 acc += x2;
@@ -224,7 +265,7 @@ __device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, doub
 // One BFS level, forward (discover level L from level L-1) or backward
 // (accumulate level L from level L+1).  grid = (ceil(items / 8), groups).
 template <bool BWD, bool STORE_DELTA>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kernel(const LevelParams p) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD : BC_MIN_BLOCKS_FWD) level_kernel(const LevelParams p) {
     const size_t g = blockIdx.y;
     // forward: instances still expanding; backward: instances present at this level
     const uint32_t live = p.live_prev[g];
@@ -240,7 +281,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kern
     double *delta = STORE_DELTA ? p.delta + g * p.n * 32 : nullptr;
     const double *val = BWD ? coef : sigma;
 
-    unsigned long long c_nr = 0, c_ar = 0, c_nv = 0, c_fa = 0, c_md = 0;
+    // per-item counters fit 32 bits (an item holds <= 32 vertices and <= 2 * item_arcs arcs)
+    unsigned c_nr = 0, c_ar = 0, c_nv = 0, c_fa = 0, c_md = 0;
     unsigned c_t = 0;  // per-lane partial
     uint32_t any_new = 0;
 
@@ -287,12 +329,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kern
             } else {
                 finalize_forward(v, vis[v], got, acc, lane, vis, cur, sigma);
                 any_new |= got;
+                const unsigned deg = (unsigned)(ve - vb);
                 c_nr += __popc(got);
-                c_ar += (unsigned long long)__popc(got) * (unsigned long long)(ve - vb);
+                c_ar += __popc(got) * deg;
                 if (got) {
                     c_nv += 1;
-                    c_fa += (unsigned long long)(ve - vb);
-                    c_md = max(c_md, (unsigned long long)(ve - vb));
+                    c_fa += deg;
+                    c_md = max(c_md, deg);
                 }
             }
         }
@@ -301,13 +344,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BC_MIN_BLOCKS) level_kern
         const unsigned t = __reduce_add_sync(kFull, c_t);
         if (lane == 0) {
             if (any_new) atomicOr(p.live_cur + g, any_new);
-            if (c_nr) atomicAdd(p.counters + 0, c_nr);
-            if (c_ar) atomicAdd(p.counters + 1, c_ar);
+            if (c_nr) atomicAdd(p.counters + 0, (unsigned long long)c_nr);
+            if (c_ar) atomicAdd(p.counters + 1, (unsigned long long)c_ar);
             if (t) atomicAdd(p.counters + 2, (unsigned long long)t);
             if (c_nv && p.lstat) {
-                atomicAdd(p.lstat + 0, c_nv);
-                atomicAdd(p.lstat + 1, c_fa);
-                atomicMax(p.lstat + 2, c_md);
+                atomicAdd(p.lstat + 0, (unsigned long long)c_nv);
+                atomicAdd(p.lstat + 1, (unsigned long long)c_fa);
+                atomicMax(p.lstat + 2, (unsigned long long)c_md);
             }
         }
     }
