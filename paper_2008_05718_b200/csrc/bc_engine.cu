@@ -376,6 +376,32 @@ int ensure_queues(bc_handle *h) {
     return BC_OK;
 }
 
+// Queue entries are (vertex, level) pairs: a vertex can sit in up to 32 levels of
+// a group (one per lane), so deep graphs outgrow the initial 4n entries.  Grow
+// by doubling up to 33n.
+int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st) {
+    const int64_t max_cap = 33 * h->n + 1024;
+    if (h->q_cap >= max_cap || need_cap <= h->q_cap) return BC_OK;
+    const int64_t cap = std::min(max_cap, std::max(need_cap, 2 * h->q_cap));
+    const size_t G = (size_t)h->alloc_groups;
+    int32_t *nv = nullptr;
+    uint32_t *nm = nullptr;
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    CUDA_TRY(h, cudaMalloc((void **)&nv, G * (size_t)cap * sizeof(int32_t)));
+    CUDA_TRY(h, cudaMalloc((void **)&nm, G * (size_t)cap * sizeof(uint32_t)));
+    for (size_t g = 0; g < G; ++g) {
+        CUDA_TRY(h, cudaMemcpy(nv + g * cap, h->q_v + g * h->q_cap, (size_t)h->q_cap * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice));
+        CUDA_TRY(h, cudaMemcpy(nm + g * cap, h->q_m + g * h->q_cap, (size_t)h->q_cap * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice));
+    }
+    cudaFree(h->q_v), cudaFree(h->q_m);
+    h->q_v = nv;
+    h->q_m = nm;
+    h->q_cap = cap;
+    return BC_OK;
+}
+
 // Device table of the level-mask pointers (the border gathers walk levels).
 int upload_level_ptrs(bc_handle *h, int depth, cudaStream_t st) {
     if (h->lvl_ptrs_cap < depth) {
@@ -687,10 +713,12 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         reps.emplace_back();
         LevelRep &prev = reps[L - 1];
         LevelRep &cur = reps[L];
-        int64_t room = h->q_cap;
-        for (int g = 0; g < ng; ++g) room = std::min<int64_t>(room, h->q_cap - (int64_t)qcount[g]);
-        const bool room_ok = room > (int64_t)std::min<unsigned long long>((unsigned long long)n, prev.farcs) +
-                                        (prev.queued ? 0 : (int64_t)prev.nverts);
+        int64_t used = 0;
+        for (int g = 0; g < ng; ++g) used = std::max<int64_t>(used, (int64_t)qcount[g]);
+        const int64_t want_room = (int64_t)std::min<unsigned long long>((unsigned long long)n, prev.farcs) +
+                                  (prev.queued ? 0 : (int64_t)prev.nverts) + 1;
+        if (h->q_cap - used < want_room) TRY(grow_queues(h, used + want_room, st));
+        const bool room_ok = h->q_cap - used >= want_room;
         // a queue entry is walked by one warp: keep vertices with very long adjacencies on the
         // dense kernels, which slice them
         const bool push = prev.farcs * (unsigned long long)h->push_beta <= graph_arcs && room_ok &&
