@@ -140,6 +140,17 @@ class ClockSampler:
         return out
 
 
+def ncu_traffic(workload_name: str):
+    """DRAM bytes the forward level kernel moved per launch, from the committed ncu
+    `--set full` capture (profiles/r1_traffic.json; null when no capture matches)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            rec = json.load(fh)
+        return rec.get(workload_name)
+    except Exception:
+        return None
+
+
 def algorithmic_bytes(st: dict, n: int):
     """forward 8*A_r + 16*T + 28*n_r, backward 8*A_r + 16*T + 44*n_r,
     initialisation 20*n per source."""
@@ -309,7 +320,7 @@ def run_ours(args):
     roofline = {
         "bound": "hbm", "kernel": "level_kernel<forward> (+hub_kernel)",
         "achieved": roof_f, "peak": peak, "unit": "GB/s", "frac": roof_f / peak,
-        "traffic": None, "peak_source": peak_src,
+        "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
         "algorithmic_bytes_per_step": fwd_b, "ms_per_step": fwd_ms,
         "backward": {"achieved": roof_b, "frac": roof_b / peak, "algorithmic_bytes_per_step": bwd_b,
                      "ms_per_step": bwd_ms},

@@ -42,6 +42,7 @@ struct Events {
 };
 
 constexpr unsigned long long kQueueMaxDegree = 8192;
+constexpr unsigned long long kThinDegree = 8;  // average degree up to which a level runs thread-per-entry
 
 // Border-table feasibility: b_p^2 entries of 12 B per part.
 constexpr double kMaxTableBytes = 64e9;
@@ -110,7 +111,9 @@ struct bc_handle {
     int64_t *d_qbeg = nullptr, *d_qend = nullptr, *d_qlbeg = nullptr;
     uint32_t *scrA = nullptr, *scrB = nullptr;
     unsigned long long *lstat = nullptr;
-    bool sigma_zeroed = false;
+    unsigned long long *report = nullptr;   // per-level report read by the host (forward_adaptive)
+    int64_t *range_table = nullptr;        // queue ranges of every level (backward_adaptive)
+    int64_t range_table_cap = 0;
     unsigned long long *counters = nullptr;
     int cnt_off = 0;  // 0: traversal counters of the result; 4: scratch (Step 1 of hybir mode)
     int64_t *d_src = nullptr;
@@ -253,7 +256,11 @@ void free_state(bc_handle *h) {
     h->live_cap = 0;
     cudaFree(h->q_v), cudaFree(h->q_m), cudaFree(h->q_count);
     cudaFree(h->d_qbeg), cudaFree(h->d_qend), cudaFree(h->d_qlbeg);
-    cudaFree(h->scrA), cudaFree(h->scrB), cudaFree(h->lstat);
+    cudaFree(h->scrA), cudaFree(h->scrB), cudaFree(h->lstat), cudaFree(h->report);
+    cudaFree(h->range_table);
+    h->report = nullptr;
+    h->range_table = nullptr;
+    h->range_table_cap = 0;
     h->q_v = nullptr;
     h->q_m = h->scrA = h->scrB = nullptr;
     h->q_count = h->lstat = nullptr;
@@ -371,6 +378,7 @@ int ensure_queues(bc_handle *h) {
     TRY(dev_alloc(h, &h->scrA, G * n));
     TRY(dev_alloc(h, &h->scrB, G * n));
     TRY(dev_alloc(h, &h->lstat, (size_t)4));
+    TRY(dev_alloc(h, &h->report, 3 + 2 * G));
     CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
     CUDA_TRY(h, cudaMemset(h->scrB, 0, G * n * sizeof(uint32_t)));
     return BC_OK;
@@ -660,7 +668,9 @@ int scatter_level(bc_handle *h, const LevelRep &r, uint32_t *dense, bool clear, 
 }
 
 // Forward sweep with the per-level push / pull choice.  One host round trip
-// per level (the choice needs the frontier's arc count).
+// per level (the choice needs the frontier's arc count): a single small read
+// of the level report that advance_level_kernel publishes.  Queue ranges stay
+// on the device between consecutive push levels.
 int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t *batch_src,
                      cudaStream_t st, int *depth_out, std::vector<LevelRep> &reps) {
     const size_t G = (size_t)h->alloc_groups;
@@ -702,12 +712,20 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         }
         CUDA_TRY(h, cudaMemcpyAsync(h->q_count, qcount.data(), G * sizeof(unsigned long long),
                                     cudaMemcpyHostToDevice, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 4 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaStreamSynchronize(st));  // the staging vectors go out of scope
     }
+    auto upload_lbeg = [&]() -> int {
+        std::vector<int64_t> lbeg(G, 0);
+        for (size_t g = 0; g < G; ++g) lbeg[g] = (int64_t)qcount[g];
+        CUDA_TRY(h, cudaMemcpyAsync(h->d_qlbeg, lbeg.data(), G * sizeof(int64_t),
+                                    cudaMemcpyHostToDevice, st));
+        return BC_OK;
+    };
+    int device_level = -1;  // level whose ranges sit in d_qbeg / d_qend (and d_qlbeg = q_count)
     int next_slot = 1;
     const unsigned long long graph_arcs = (unsigned long long)std::max<int64_t>(c.n_arcs, 1) * ng;
-    std::vector<uint32_t> flags(G);
-    std::vector<unsigned long long> qnow(G), ls(3);
+    std::vector<unsigned long long> report(3 + 2 * G);
     for (int L = 1;; ++L) {
         TRY(ensure_live(h, L + 1));
         reps.emplace_back();
@@ -717,13 +735,14 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         for (int g = 0; g < ng; ++g) used = std::max<int64_t>(used, (int64_t)qcount[g]);
         const int64_t want_room = (int64_t)std::min<unsigned long long>((unsigned long long)n, prev.farcs) +
                                   (prev.queued ? 0 : (int64_t)prev.nverts) + 1;
-        if (h->q_cap - used < want_room) TRY(grow_queues(h, used + want_room, st));
-        const bool room_ok = h->q_cap - used >= want_room;
         // a queue entry is walked by one warp: keep vertices with very long adjacencies on the
         // dense kernels, which slice them
-        const bool push = prev.farcs * (unsigned long long)h->push_beta <= graph_arcs && room_ok &&
-                          prev.maxdeg <= kQueueMaxDegree;
-        CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 4 * sizeof(unsigned long long), st));
+        bool push = prev.farcs * (unsigned long long)h->push_beta <= graph_arcs &&
+                    prev.maxdeg <= kQueueMaxDegree;
+        if (push && h->q_cap - used < want_room) {
+            TRY(grow_queues(h, used + want_room, st));
+            push = h->q_cap - used >= want_room;
+        }
         if (push) {
             if (!prev.queued) {  // dense level -> queue
                 prev.qb.assign(qcount.begin(), qcount.begin() + ng);
@@ -735,21 +754,29 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 CUDA_TRY(h, cudaStreamSynchronize(st));
                 prev.qe.assign(qcount.begin(), qcount.begin() + ng);
                 prev.queued = true;
+                device_level = -1;
             }
-            TRY(upload_ranges(h, prev, st));
-            std::vector<int64_t> lbeg(G, 0);
-            for (int g = 0; g < ng; ++g) lbeg[g] = (int64_t)qcount[g];
-            CUDA_TRY(h, cudaMemcpyAsync(h->d_qlbeg, lbeg.data(), G * sizeof(int64_t),
-                                        cudaMemcpyHostToDevice, st));
-            fwd_push_kernel<<<dim3(queue_blocks(prev, kWarpsPerBlock), ng), kWarpsPerBlock * 32, 0, st>>>(
-                c.off, c.col, n, queue_params(h), h->vis, h->scrA, h->sigma, h->counters + h->cnt_off);
+            if (device_level != L - 1) {
+                TRY(upload_ranges(h, prev, st));
+                TRY(upload_lbeg());
+            }
+            if (prev.farcs <= kThinDegree * prev.nverts)  // low-degree level: one thread per entry
+                fwd_push_thin_kernel<<<dim3(queue_blocks(prev, kWarpsPerBlock * 32), ng),
+                                       kWarpsPerBlock * 32, 0, st>>>(
+                    c.off, c.col, n, queue_params(h), h->vis, h->scrA, h->sigma,
+                    h->counters + h->cnt_off);
+            else
+                fwd_push_kernel<<<dim3(queue_blocks(prev, kWarpsPerBlock), ng), kWarpsPerBlock * 32, 0, st>>>(
+                    c.off, c.col, n, queue_params(h), h->vis, h->scrA, h->sigma,
+                    h->counters + h->cnt_off);
             push_post_kernel<<<dim3(std::min<unsigned>(grid1d((size_t)std::min<unsigned long long>(
                                                            (unsigned long long)n, prev.farcs + 1)), 1184), ng),
                                256, 0, st>>>(c.off, n, queue_params(h), h->d_qlbeg, h->vis, h->scrA,
                                              h->live + (size_t)L * G, h->counters + h->cnt_off, h->lstat);
             h->launches += 2;
             cur.queued = true;
-            cur.qb.assign(lbeg.begin(), lbeg.begin() + ng);
+            cur.qb.assign(qcount.begin(), qcount.begin() + ng);
+            device_level = L;
         } else {
             const uint32_t *nbr;
             if (prev.slot >= 0) nbr = h->lvl[prev.slot];
@@ -761,69 +788,126 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
             TRY(ensure_pool(h, cur.slot + 1));
             TRY(launch_forward(h, c, L, ng, st, nbr, h->lvl[cur.slot], h->lstat));
             if (prev.slot < 0) TRY(scatter_level(h, prev, h->scrB, true, ng, st));
+            device_level = -1;
         }
+        advance_level_kernel<<<1, (unsigned)std::max<size_t>(G, 32), 0, st>>>(
+            h->lstat, h->q_count, h->live + (size_t)L * G, h->d_qbeg, h->d_qend, h->d_qlbeg, (int)G,
+            h->report);
+        ++h->launches;
         CUDA_TRY(h, cudaGetLastError());
-        CUDA_TRY(h, cudaMemcpyAsync(flags.data(), h->live + (size_t)L * G, G * sizeof(uint32_t),
-                                    cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(h, cudaMemcpyAsync(ls.data(), h->lstat, 3 * sizeof(unsigned long long),
-                                    cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(h, cudaMemcpyAsync(qnow.data(), h->q_count, G * sizeof(unsigned long long),
+        CUDA_TRY(h, cudaMemcpyAsync(report.data(), h->report, report.size() * sizeof(unsigned long long),
                                     cudaMemcpyDeviceToHost, st));
         CUDA_TRY(h, cudaStreamSynchronize(st));
         bool alive = false;
-        for (int g = 0; g < ng; ++g) alive |= flags[g] != 0;
+        for (int g = 0; g < ng; ++g) alive |= report[3 + G + g] != 0;
         if (!alive) {
             reps.pop_back();
             *depth_out = L;
             return BC_OK;
         }
-        cur.nverts = ls[0];
-        cur.farcs = ls[1];
-        cur.maxdeg = ls[2];
-        if (cur.queued) cur.qe.assign(qnow.begin(), qnow.begin() + ng);
-        qcount = qnow;
+        cur.nverts = report[0];
+        cur.farcs = report[1];
+        cur.maxdeg = report[2];
+        for (size_t g = 0; g < G; ++g) qcount[g] = report[3 + g];
+        if (cur.queued) cur.qe.assign(qcount.begin(), qcount.begin() + ng);
     }
 }
 
 // Backward sweep over the level representations forward_adaptive produced.
+// The ranges of every queue level are uploaded once; a queue level's masks are
+// kept in one of two scratch arrays while its parents' level runs.
 int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRep> &reps, int ng,
                       bool debug, cudaStream_t st) {
     const int last = debug ? 0 : 1;
+    const size_t G = (size_t)h->alloc_groups;
     const unsigned long long graph_arcs = (unsigned long long)std::max<int64_t>(c.n_arcs, 1) * ng;
+    // per-level range table: [level][0: begin, 1: end][group]
+    std::vector<int64_t> table((size_t)depth * 2 * G, 0);
+    for (int L = 0; L < depth; ++L)
+        if (reps[L].queued)
+            for (size_t g = 0; g < reps[L].qb.size(); ++g) {
+                table[((size_t)L * 2 + 0) * G + g] = reps[L].qb[g];
+                table[((size_t)L * 2 + 1) * G + g] = reps[L].qe[g];
+            }
+    if ((int64_t)table.size() > h->range_table_cap) {
+        TRY(dev_alloc(h, &h->range_table, table.size()));
+        h->range_table_cap = (int64_t)table.size();
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(h->range_table, table.data(), table.size() * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, st));
+    auto beg_of = [&](int L) { return h->range_table + ((size_t)L * 2 + 0) * G; };
+    auto end_of = [&](int L) { return h->range_table + ((size_t)L * 2 + 1) * G; };
+    uint32_t *scr[2] = {h->scrA, h->scrB};
+    int holder = -1, held_level = -1;  // scratch array holding the masks of queue level held_level
+    auto swap_scatter = [&](int erase_level, int erase_idx, int write_level, int write_idx) -> int {
+        if (erase_idx < 0 && write_idx < 0) return BC_OK;
+        unsigned blocks = 1;
+        if (erase_idx >= 0) blocks = std::max(blocks, queue_blocks(reps[erase_level], 256));
+        if (write_idx >= 0) blocks = std::max(blocks, queue_blocks(reps[write_level], 256));
+        swap_scatter_kernel<<<dim3(blocks, ng), 256, 0, st>>>(
+            queue_params(h), h->n, erase_idx >= 0 ? beg_of(erase_level) : nullptr,
+            erase_idx >= 0 ? end_of(erase_level) : nullptr, erase_idx >= 0 ? scr[erase_idx] : nullptr,
+            write_idx >= 0 ? beg_of(write_level) : nullptr, write_idx >= 0 ? end_of(write_level) : nullptr,
+            write_idx >= 0 ? scr[write_idx] : nullptr);
+        ++h->launches;
+        CUDA_TRY(h, cudaGetLastError());
+        return BC_OK;
+    };
     for (int L = depth - 1; L >= last; --L) {
         LevelRep &r = reps[L];
         const bool deepest = L == depth - 1;
         const uint32_t *nbr = nullptr;
-        bool clear_b = false;
         if (!deepest) {
             LevelRep &below = reps[L + 1];
             if (below.slot >= 0) nbr = h->lvl[below.slot];
             else {
-                TRY(scatter_level(h, below, h->scrB, false, ng, st));
-                nbr = h->scrB;
-                clear_b = true;
+                if (holder < 0 || held_level != L + 1)
+                    return h->fail(BC_ERR_INTERNAL, "backward sweep lost the masks of a queue level");
+                nbr = scr[holder];
             }
         }
+        int cur_holder = -1;  // scratch that already holds level L's masks
         if (r.slot >= 0) {
             TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, h->lvl[r.slot], nbr));
         } else if (r.farcs * (unsigned long long)h->push_beta <= graph_arcs && r.maxdeg <= kQueueMaxDegree) {
-            TRY(upload_ranges(h, r, st));
-            const dim3 grid(queue_blocks(r, kWarpsPerBlock), ng);
-            if (debug)
+            QueueParams q = queue_params(h);
+            q.q_beg = beg_of(L);
+            q.q_end = end_of(L);
+            const bool thin = r.farcs <= kThinDegree * r.nverts;
+            const dim3 grid(queue_blocks(r, thin ? 128 : kWarpsPerBlock), ng);
+            if (thin && debug)
+                bwd_queue_thin_kernel<true><<<grid, 128, 0, st>>>(
+                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 0);
+            else if (thin)
+                bwd_queue_thin_kernel<false><<<grid, 128, 0, st>>>(
+                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 1);
+            else if (debug)
                 bwd_queue_kernel<true><<<grid, kWarpsPerBlock * 32, 0, st>>>(
-                    c.off, c.col, h->n, queue_params(h), nbr, h->sigma, h->coef, h->delta, h->bcg, 0);
+                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 0);
             else
                 bwd_queue_kernel<false><<<grid, kWarpsPerBlock * 32, 0, st>>>(
-                    c.off, c.col, h->n, queue_params(h), nbr, h->sigma, h->coef, h->delta, h->bcg, 1);
+                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 1);
             ++h->launches;
             CUDA_TRY(h, cudaGetLastError());
         } else {  // a queue level with heavy vertices: run it through the dense kernel (hub slices)
-            TRY(scatter_level(h, r, h->scrA, false, ng, st));
-            TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, h->scrA, nbr));
-            TRY(scatter_level(h, r, h->scrA, true, ng, st));
+            cur_holder = holder == 0 ? 1 : 0;
+            TRY(swap_scatter(-1, -1, L, cur_holder));
+            TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, scr[cur_holder], nbr));
         }
-        if (clear_b) TRY(scatter_level(h, reps[L + 1], h->scrB, true, ng, st));
+        // hand over: level L's masks become the children masks of level L - 1
+        const bool need_masks = L - 1 >= last && r.slot < 0;
+        int write_idx = -1;
+        if (need_masks && cur_holder < 0) write_idx = holder == 0 ? 1 : 0;
+        TRY(swap_scatter(held_level, holder, L, write_idx));
+        if (cur_holder >= 0 || write_idx >= 0) {
+            holder = cur_holder >= 0 ? cur_holder : write_idx;
+            held_level = L;
+        } else {
+            holder = -1;
+            held_level = -1;
+        }
     }
+    if (holder >= 0) TRY(swap_scatter(held_level, holder, -1, -1));  // leave the scratch arrays zero
     return BC_OK;
 }
 

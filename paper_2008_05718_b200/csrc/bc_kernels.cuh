@@ -574,6 +574,78 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_kernel(
     if (lane == 0 && t) atomicAdd(counters + 2, (unsigned long long)t);
 }
 
+// Thin variant for levels of low-degree vertices (road-like graphs): one THREAD
+// per queue entry walks its few arcs, so a warp advances 32 frontier vertices
+// at once instead of leaving 29 of 32 lanes idle on a 3-arc adjacency.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_thin_kernel(
+    const int64_t *__restrict__ off, const int32_t *__restrict__ col, int64_t n, QueueParams q,
+    const uint32_t *__restrict__ vis, uint32_t *next, double *sigma,
+    unsigned long long *counters) {
+    __shared__ int32_t stage[kWarpsPerBlock][kStage];
+    const size_t g = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t beg = q.q_beg[g], end = q.q_end[g];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint32_t *gvis = vis + g * n;
+    uint32_t *gnext = next + g * n;
+    double *gsig = sigma + g * n * 32;
+    int staged = 0;  // warp-uniform
+    unsigned c_t = 0;
+    auto flush = [&]() {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(q.q_count + g, (unsigned long long)staged);
+        base = __shfl_sync(kFull, base, 0);
+        for (int i = lane; i < staged; i += 32) q.q_v[g * q.cap + base + i] = stage[warp][i];
+        staged = 0;
+        __syncwarp();
+    };
+    // warp-uniform trip count: every lane of the warp runs the same number of rounds
+    for (int64_t i0 = beg + (int64_t)blockIdx.x * blockDim.x + warp * 32; i0 < end; i0 += stride) {
+        const int64_t i = i0 + lane;
+        int32_t u = 0;
+        uint32_t mask = 0;
+        int64_t a = 0, e = 0;
+        if (i < end) {
+            u = q.q_v[g * q.cap + i];
+            mask = q.q_m[g * q.cap + i];
+            a = off[u];
+            e = off[u + 1];
+        }
+        int rounds = (int)(e - a);
+        rounds = __reduce_max_sync(kFull, rounds);
+        const double *urow = gsig + (size_t)u * 32;
+        for (int r = 0; r < rounds; ++r, ++a) {
+            bool fresh_vertex = false;
+            int32_t w = 0;
+            if (a < e) {
+                w = __ldg(col + a);
+                uint32_t fresh = mask & ~gvis[w];
+                if (fresh) {
+                    const uint32_t old = atomicOr(gnext + w, fresh);
+                    fresh_vertex = old == 0;
+                    double *wrow = gsig + (size_t)w * 32;
+                    while (fresh) {
+                        const int bit = __ffs(fresh) - 1;
+                        fresh &= fresh - 1;
+                        atomicAdd(wrow + bit, urow[bit]);
+                        ++c_t;
+                    }
+                }
+            }
+            const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+            if (newm) {
+                if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
+                staged += __popc(newm);
+                __syncwarp();
+                if (staged > kStage - 32) flush();
+            }
+        }
+    }
+    if (staged) flush();
+    const unsigned t = __reduce_add_sync(kFull, c_t);
+    if (lane == 0 && t) atomicAdd(counters + 2, (unsigned long long)t);
+}
+
 // After a push: entries [q_lbeg[g], q_count[g]) are the new level.  Record
 // their masks, mark them seen, clear next[], gather the level's statistics.
 // lstat: [0] vertices in the level, [1] their arcs, [2] largest degree (all groups).
@@ -616,6 +688,44 @@ __global__ void push_post_kernel(const int64_t *__restrict__ off, int64_t n, Que
         atomicAdd(lstat + 1, fa);
         atomicMax(lstat + 2, md);
     }
+}
+
+// End of a push level, one thread per group: publish the level's report for the
+// host ([0..2] lstat, then q_count per group, then live per group), reset the
+// statistics, and make the level just produced the frontier of the next push
+// (device-resident ranges: consecutive push levels need no host uploads).
+__global__ void advance_level_kernel(unsigned long long *lstat, unsigned long long *q_count,
+                                     const uint32_t *live_cur, int64_t *q_beg, int64_t *q_end,
+                                     int64_t *q_lbeg, int G, unsigned long long *report) {
+    const int g = threadIdx.x;
+    if (g < 3) report[g] = lstat[g];
+    __syncthreads();
+    if (g < 3) lstat[g] = 0;
+    if (g < G) {
+        const unsigned long long c = q_count[g];
+        report[3 + g] = c;
+        report[3 + G + g] = live_cur[g];
+        q_beg[g] = q_lbeg[g];
+        q_end[g] = (int64_t)c;
+        q_lbeg[g] = (int64_t)c;
+    }
+}
+
+// Backward helper: erase one queue level from `erase_arr` and write another into
+// `write_arr` in a single launch (either range may be empty).
+__global__ void swap_scatter_kernel(QueueParams q, int64_t n, const int64_t *erase_beg,
+                                    const int64_t *erase_end, uint32_t *erase_arr,
+                                    const int64_t *write_beg, const int64_t *write_end,
+                                    uint32_t *write_arr) {
+    const size_t g = blockIdx.y;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    if (erase_arr != nullptr)
+        for (int64_t i = erase_beg[g] + tid; i < erase_end[g]; i += step)
+            erase_arr[g * n + q.q_v[g * q.cap + i]] = 0u;
+    if (write_arr != nullptr)
+        for (int64_t i = write_beg[g] + tid; i < write_end[g]; i += step)
+            write_arr[g * n + q.q_v[g * q.cap + i]] = q.q_m[g * q.cap + i];
 }
 
 // Write (clear = 0) or erase (clear = 1) a queue level in a dense mask array.
@@ -675,6 +785,45 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bwd_queue_kernel(
         finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma + g * n * 32, coef + g * n * 32,
                                        STORE_DELTA ? delta + g * n * 32 : nullptr, bcg + g * n,
                                        accumulate);
+    }
+}
+
+// Thin backward variant: one thread per queue entry; for each lane of the entry
+// the thread sums its children's coef in arc order (same arithmetic as
+// scan_arcs + finalize_backward, serial instead of warp-wide).
+template <bool STORE_DELTA>
+__global__ void bwd_queue_thin_kernel(const int64_t *__restrict__ off,
+                                      const int32_t *__restrict__ col, int64_t n, QueueParams q,
+                                      const uint32_t *nbr, const double *sigma, double *coef,
+                                      double *delta, double *bcg, int accumulate) {
+    const size_t g = blockIdx.y;
+    const int64_t beg = q.q_beg[g], end = q.q_end[g];
+    const uint32_t *gn = nbr ? nbr + g * n : nullptr;
+    const double *gsig = sigma + g * n * 32;
+    double *gcoef = coef + g * n * 32;
+    for (int64_t i = beg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = q.q_v[g * q.cap + i];
+        uint32_t want = q.q_m[g * q.cap + i];
+        const int64_t a0 = off[v], a1 = off[v + 1];
+        double total = 0.0;
+        while (want) {
+            const int bit = __ffs(want) - 1;
+            want &= want - 1;
+            double acc = 0.0;
+            if (gn != nullptr)
+                for (int64_t a = a0; a < a1; ++a) {
+                    const int32_t w = __ldg(col + a);
+                    if ((__ldg(gn + w) >> bit) & 1u) acc += gcoef[(size_t)w * 32 + bit];
+                }
+            const size_t idx = (size_t)v * 32 + bit;
+            const double sv = gsig[idx];
+            const double d = sv * acc;
+            gcoef[idx] = (1.0 + d) / sv;
+            if (STORE_DELTA) delta[g * n * 32 + idx] = d;
+            total += d;
+        }
+        if (accumulate) bcg[g * n + v] += total;
     }
 }
 

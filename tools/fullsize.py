@@ -39,6 +39,7 @@ if "er22" in which:
 if "road2048" in which:
     t = time.time(); g = G.road_like(2048, 2048, keep=0.2, seed=1); log(built="road2048", s=time.time() - t)
     run_direct("road-like 2048x2048, 512 sources (config 3 graph, unpartitioned)", g, 512, 4, check=8)
+    run_direct("road-like 2048x2048, 512 sources, one batch of 16 groups", g, 512, 16, check=8)
     del g
 if "grid512_hybir" in which:
     g = G.road_like(512, 512, keep=0.2, seed=1)
