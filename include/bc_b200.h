@@ -161,7 +161,13 @@ int bc_dist_set_live(bc_handle *h, int level, const uint32_t *live, void *stream
 int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream);
 
 const char *bc_last_error(bc_handle *h);
+/* Releases the handle.  Its device blocks go to a per-device cache that the next
+ * bc_create / bc_run reuses (run_bc() opens one handle per call, as the
+ * reference's run_bc builds its state per call, engine.py:120-131; without the
+ * cache every call pays cudaMalloc + cudaFree of the multi-GB batch state). */
 void bc_destroy(bc_handle *h);
+/* Hands every cached device block back to the CUDA driver. */
+void bc_release_cached_memory(void);
 
 #ifdef __cplusplus
 }

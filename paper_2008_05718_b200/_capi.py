@@ -28,7 +28,7 @@ SYMBOLS = (
     "bc_get_border_frontier",
     "bc_dist_setup", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
     "bc_dist_export", "bc_dist_import", "bc_dist_get_live", "bc_dist_set_live", "bc_dist_finish",
-    "bc_last_error", "bc_destroy",
+    "bc_last_error", "bc_destroy", "bc_release_cached_memory",
 )
 
 
@@ -106,8 +106,15 @@ def load():
     L.bc_last_error.argtypes = [vp]
     L.bc_destroy.restype = None
     L.bc_destroy.argtypes = [vp]
+    L.bc_release_cached_memory.restype = None
+    L.bc_release_cached_memory.argtypes = []
     _lib = L
     return L
+
+
+def release_cached_memory():
+    """Return the device blocks cached by closed engines to the CUDA driver."""
+    load().bc_release_cached_memory()
 
 
 def _ptr(a):

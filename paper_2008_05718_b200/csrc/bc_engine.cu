@@ -14,9 +14,14 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 using namespace bcb200;
@@ -24,6 +29,102 @@ using namespace bcb200;
 namespace {
 
 thread_local std::string g_create_error;
+
+
+// ------------------------------------------------------------------------------------
+// Device memory arena.  cudaMalloc / cudaFree of the multi-GB batch state cost
+// 15-20 ms per run_bc() call (and cudaFree drains the device); blocks released by
+// a handle are kept per device and handed to the next handle that asks for a
+// similar size.  bc_release_cached_memory() returns them to the driver, and an
+// allocation that fails flushes the cache before it gives up.
+// ------------------------------------------------------------------------------------
+struct Arena {
+    std::mutex mu;
+    std::unordered_map<void *, std::pair<int, size_t>> live;   // ptr -> (device, bytes)
+    std::multimap<size_t, void *> spare[64];                   // per device, by size
+    size_t spare_bytes = 0;
+
+    static size_t round_up(size_t b) {
+        const size_t g = b < (1u << 20) ? 512 : (size_t)2 << 20;   // driver granularity for big blocks
+        return (std::max<size_t>(b, 1) + g - 1) / g * g;
+    }
+    void flush_locked(int dev) {
+        for (auto &kv : spare[dev]) {
+            cudaFree(kv.second);
+            spare_bytes -= kv.first;
+        }
+        spare[dev].clear();
+    }
+    cudaError_t alloc(void **out, size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        dev &= 63;
+        const size_t want = round_up(bytes);
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = spare[dev].lower_bound(want);
+        if (it != spare[dev].end() && it->first <= want + want / 4 + (1u << 16)) {
+            *out = it->second;
+            live[*out] = {dev, it->first};
+            spare_bytes -= it->first;
+            spare[dev].erase(it);
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaMalloc(out, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            flush_locked(dev);
+            e = cudaMalloc(out, want);
+        }
+        if (e == cudaSuccess) live[*out] = {dev, want};
+        return e;
+    }
+    void release(void *p) {
+        if (p == nullptr) return;
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = live.find(p);
+        if (it == live.end()) {  // not ours
+            cudaFree(p);
+            return;
+        }
+        spare[it->second.first].emplace(it->second.second, p);
+        spare_bytes += it->second.second;
+        live.erase(it);
+    }
+    void flush_all() {
+        std::lock_guard<std::mutex> lock(mu);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (int d = 0; d < 64; ++d)
+            if (!spare[d].empty()) {
+                cudaSetDevice(d);
+                flush_locked(d);
+            }
+        cudaSetDevice(cur);
+    }
+};
+Arena &arena() {
+    static Arena *a = new Arena();  // leaked on purpose: the driver may be gone at exit
+    return *a;
+}
+inline cudaError_t arena_malloc(void **out, size_t bytes) { return arena().alloc(out, bytes); }
+template <typename T>
+inline void arena_free(T *p) { arena().release((void *)p); }
+
+// BC_B200_TRACE=1: host wall clock per stage on stderr (the device is drained at
+// every mark, so traced runs are for attribution only, never for a bench number).
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    Trace() : on(getenv("BC_B200_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+    void mark(const char *what) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[bc_b200] %-28s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 // Device-side CSR plus the work items of the level kernels.
 struct Csr {
@@ -157,34 +258,34 @@ namespace {
 
 template <typename T>
 int upload(bc_handle *h, T **dst, const std::vector<T> &src) {
-    cudaFree(*dst);
+    arena_free(*dst);
     *dst = nullptr;
     if (src.empty()) return BC_OK;
-    CUDA_TRY(h, cudaMalloc((void **)dst, src.size() * sizeof(T)));
+    CUDA_TRY(h, arena_malloc((void **)dst, src.size() * sizeof(T)));
     CUDA_TRY(h, cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
     return BC_OK;
 }
 
 template <typename T>
 int dev_alloc(bc_handle *h, T **dst, size_t count) {
-    cudaFree(*dst);
+    arena_free(*dst);
     *dst = nullptr;
-    CUDA_TRY(h, cudaMalloc((void **)dst, std::max<size_t>(count, 1) * sizeof(T)));
+    CUDA_TRY(h, arena_malloc((void **)dst, std::max<size_t>(count, 1) * sizeof(T)));
     return BC_OK;
 }
 
 void free_items(Csr &c) {
-    cudaFree(c.chk_v), cudaFree(c.chk_a0), cudaFree(c.chk_a1);
-    cudaFree(c.rng_v0), cudaFree(c.rng_nv);
-    cudaFree(c.hub_v), cudaFree(c.hub_c0), cudaFree(c.hub_nc);
+    arena_free(c.chk_v), arena_free(c.chk_a0), arena_free(c.chk_a1);
+    arena_free(c.rng_v0), arena_free(c.rng_nv);
+    arena_free(c.hub_v), arena_free(c.hub_c0), arena_free(c.hub_nc);
     c.chk_v = c.rng_v0 = c.rng_nv = c.hub_v = c.hub_c0 = c.hub_nc = nullptr;
     c.chk_a0 = c.chk_a1 = nullptr;
     c.n_chk = c.n_rng = c.n_hub = 0;
 }
 
 void free_csr(Csr &c) {
-    cudaFree(c.off);
-    cudaFree(c.col);
+    arena_free(c.off);
+    arena_free(c.col);
     free_items(c);
     c = Csr();
 }
@@ -246,18 +347,18 @@ int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
 }
 
 void free_state(bc_handle *h) {
-    cudaFree(h->vis);
-    for (uint32_t *p : h->lvl) cudaFree(p);
+    arena_free(h->vis);
+    for (uint32_t *p : h->lvl) arena_free(p);
     h->lvl.clear();
-    cudaFree(h->sigma), cudaFree(h->coef), cudaFree(h->delta), cudaFree(h->bcg);
-    cudaFree(h->pacc), cudaFree(h->pmask);
-    cudaFree(h->live);
+    arena_free(h->sigma), arena_free(h->coef), arena_free(h->delta), arena_free(h->bcg);
+    arena_free(h->pacc), arena_free(h->pmask);
+    arena_free(h->live);
     h->live = nullptr;
     h->live_cap = 0;
-    cudaFree(h->q_v), cudaFree(h->q_m), cudaFree(h->q_count);
-    cudaFree(h->d_qbeg), cudaFree(h->d_qend), cudaFree(h->d_qlbeg);
-    cudaFree(h->scrA), cudaFree(h->scrB), cudaFree(h->lstat), cudaFree(h->report);
-    cudaFree(h->range_table);
+    arena_free(h->q_v), arena_free(h->q_m), arena_free(h->q_count);
+    arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
+    arena_free(h->scrA), arena_free(h->scrB), arena_free(h->lstat), arena_free(h->report);
+    arena_free(h->range_table);
     h->report = nullptr;
     h->range_table = nullptr;
     h->range_table_cap = 0;
@@ -274,11 +375,11 @@ void free_state(bc_handle *h) {
 }
 
 void free_border_state(bc_handle *h) {
-    cudaFree(h->D), cudaFree(h->D2), cudaFree(h->seedD), cudaFree(h->Dfin);
-    cudaFree(h->seedS), cudaFree(h->sig), cudaFree(h->arr);
-    cudaFree(h->lane_part), cudaFree(h->lane_iters), cudaFree(h->lane_active);
-    cudaFree(h->lane_entered), cudaFree(h->lane_changed);
-    cudaFree(h->sync_flag), cudaFree(h->sync_bits), cudaFree(h->lane_sync), cudaFree(h->lane_bytes);
+    arena_free(h->D), arena_free(h->D2), arena_free(h->seedD), arena_free(h->Dfin);
+    arena_free(h->seedS), arena_free(h->sig), arena_free(h->arr);
+    arena_free(h->lane_part), arena_free(h->lane_iters), arena_free(h->lane_active);
+    arena_free(h->lane_entered), arena_free(h->lane_changed);
+    arena_free(h->sync_flag), arena_free(h->sync_bits), arena_free(h->lane_sync), arena_free(h->lane_bytes);
     h->D = h->D2 = h->seedD = h->Dfin = h->lane_part = h->lane_iters = nullptr;
     h->seedS = h->sig = h->arr = nullptr;
     h->lane_active = h->lane_entered = h->lane_changed = h->sync_flag = h->sync_bits = nullptr;
@@ -290,9 +391,9 @@ void free_border_state(bc_handle *h) {
 void free_partition(bc_handle *h) {
     free_csr(h->intra);
     free_border_state(h);
-    cudaFree(h->d_part), cudaFree(h->d_border_v), cudaFree(h->d_border_p), cudaFree(h->d_part_off);
-    cudaFree(h->d_cin_src), cudaFree(h->d_tab_off), cudaFree(h->d_cin_off);
-    cudaFree(h->bm), cudaFree(h->sm);
+    arena_free(h->d_part), arena_free(h->d_border_v), arena_free(h->d_border_p), arena_free(h->d_part_off);
+    arena_free(h->d_cin_src), arena_free(h->d_tab_off), arena_free(h->d_cin_off);
+    arena_free(h->bm), arena_free(h->sm);
     h->d_part = h->d_border_v = h->d_border_p = h->d_part_off = h->d_cin_src = nullptr;
     h->d_tab_off = h->d_cin_off = nullptr;
     h->bm = nullptr;
@@ -308,27 +409,27 @@ int ensure_state(bc_handle *h, int groups, bool want_delta) {
     const int n_chk = std::max(h->full.n_chk, h->intra.n_chk);
     if (h->alloc_groups < groups) {
         free_state(h);
-        CUDA_TRY(h, cudaMalloc((void **)&h->vis, groups * n * sizeof(uint32_t)));
-        CUDA_TRY(h, cudaMalloc((void **)&h->sigma, groups * n * 32 * sizeof(double)));
-        CUDA_TRY(h, cudaMalloc((void **)&h->coef, groups * n * 32 * sizeof(double)));
-        CUDA_TRY(h, cudaMalloc((void **)&h->bcg, groups * n * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->vis, groups * n * sizeof(uint32_t)));
+        CUDA_TRY(h, arena_malloc((void **)&h->sigma, groups * n * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->coef, groups * n * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->bcg, groups * n * sizeof(double)));
         CUDA_TRY(h, cudaMemset(h->bcg, 0, groups * n * sizeof(double)));
         h->alloc_groups = groups;
     }
     if (want_delta && h->delta == nullptr)
-        CUDA_TRY(h, cudaMalloc((void **)&h->delta, (size_t)h->alloc_groups * n * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->delta, (size_t)h->alloc_groups * n * 32 * sizeof(double)));
     if (h->pacc_chunks < n_chk || (n_chk > 0 && h->pacc == nullptr)) {
-        cudaFree(h->pacc), cudaFree(h->pmask);
+        arena_free(h->pacc), arena_free(h->pmask);
         h->pacc = nullptr, h->pmask = nullptr;
         const size_t slots = (size_t)h->alloc_groups * n_chk;
-        CUDA_TRY(h, cudaMalloc((void **)&h->pacc, slots * 32 * sizeof(double)));
-        CUDA_TRY(h, cudaMalloc((void **)&h->pmask, slots * sizeof(uint32_t)));
+        CUDA_TRY(h, arena_malloc((void **)&h->pacc, slots * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->pmask, slots * sizeof(uint32_t)));
         h->pacc_chunks = n_chk;
     }
     if (h->counters == nullptr)
-        CUDA_TRY(h, cudaMalloc((void **)&h->counters, 8 * sizeof(unsigned long long)));
-    if (h->dflags == nullptr) CUDA_TRY(h, cudaMalloc((void **)&h->dflags, 4 * sizeof(uint32_t)));
-    if (h->d_maxlvl == nullptr) CUDA_TRY(h, cudaMalloc((void **)&h->d_maxlvl, sizeof(int)));
+        CUDA_TRY(h, arena_malloc((void **)&h->counters, 8 * sizeof(unsigned long long)));
+    if (h->dflags == nullptr) CUDA_TRY(h, arena_malloc((void **)&h->dflags, 4 * sizeof(uint32_t)));
+    if (h->d_maxlvl == nullptr) CUDA_TRY(h, arena_malloc((void **)&h->d_maxlvl, sizeof(int)));
     return BC_OK;
 }
 
@@ -336,7 +437,7 @@ int ensure_pool(bc_handle *h, int count) {
     const size_t bytes = (size_t)h->alloc_groups * (size_t)h->n * sizeof(uint32_t);
     while ((int)h->lvl.size() < count) {
         uint32_t *p = nullptr;
-        CUDA_TRY(h, cudaMalloc((void **)&p, bytes));
+        CUDA_TRY(h, arena_malloc((void **)&p, bytes));
         h->lvl.push_back(p);
     }
     return BC_OK;
@@ -347,12 +448,12 @@ int ensure_live(bc_handle *h, int count) {
         const int cap = std::max(count + 1, 2 * h->live_cap);
         const size_t G = (size_t)h->alloc_groups;
         uint32_t *p = nullptr;
-        CUDA_TRY(h, cudaMalloc((void **)&p, cap * G * sizeof(uint32_t)));
+        CUDA_TRY(h, arena_malloc((void **)&p, cap * G * sizeof(uint32_t)));
         CUDA_TRY(h, cudaMemset(p, 0, cap * G * sizeof(uint32_t)));
         if (h->live) {
             CUDA_TRY(h, cudaMemcpy(p, h->live, h->live_cap * G * sizeof(uint32_t),
                                    cudaMemcpyDeviceToDevice));
-            cudaFree(h->live);
+            arena_free(h->live);
         }
         h->live = p;
         h->live_cap = cap;
@@ -395,15 +496,15 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st) {
     int32_t *nv = nullptr;
     uint32_t *nm = nullptr;
     CUDA_TRY(h, cudaStreamSynchronize(st));
-    CUDA_TRY(h, cudaMalloc((void **)&nv, G * (size_t)cap * sizeof(int32_t)));
-    CUDA_TRY(h, cudaMalloc((void **)&nm, G * (size_t)cap * sizeof(uint32_t)));
+    CUDA_TRY(h, arena_malloc((void **)&nv, G * (size_t)cap * sizeof(int32_t)));
+    CUDA_TRY(h, arena_malloc((void **)&nm, G * (size_t)cap * sizeof(uint32_t)));
     for (size_t g = 0; g < G; ++g) {
         CUDA_TRY(h, cudaMemcpy(nv + g * cap, h->q_v + g * h->q_cap, (size_t)h->q_cap * sizeof(int32_t),
                                cudaMemcpyDeviceToDevice));
         CUDA_TRY(h, cudaMemcpy(nm + g * cap, h->q_m + g * h->q_cap, (size_t)h->q_cap * sizeof(uint32_t),
                                cudaMemcpyDeviceToDevice));
     }
-    cudaFree(h->q_v), cudaFree(h->q_m);
+    arena_free(h->q_v), arena_free(h->q_m);
     h->q_v = nv;
     h->q_m = nm;
     h->q_cap = cap;
@@ -413,10 +514,10 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st) {
 // Device table of the level-mask pointers (the border gathers walk levels).
 int upload_level_ptrs(bc_handle *h, int depth, cudaStream_t st) {
     if (h->lvl_ptrs_cap < depth) {
-        cudaFree((void *)h->d_lvl_ptrs);
+        arena_free((void *)h->d_lvl_ptrs);
         h->d_lvl_ptrs = nullptr;
         const int cap = std::max(depth, 2 * h->lvl_ptrs_cap);
-        CUDA_TRY(h, cudaMalloc((void **)&h->d_lvl_ptrs, cap * sizeof(uint32_t *)));
+        CUDA_TRY(h, arena_malloc((void **)&h->d_lvl_ptrs, cap * sizeof(uint32_t *)));
         h->lvl_ptrs_cap = cap;
     }
     CUDA_TRY(h, cudaMemcpyAsync((void *)h->d_lvl_ptrs, h->lvl.data(), depth * sizeof(uint32_t *),
@@ -488,6 +589,21 @@ inline unsigned grid1d(size_t count, int block = 256, size_t cap = 1u << 30) {
     return (unsigned)std::max<size_t>(1, std::min<size_t>((count + block - 1) / block, cap));
 }
 
+#ifdef BC_PROFILE
+void prof_dump(const char *what, int L, cudaStream_t st) {
+    unsigned long long v[16];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(v, g_prof, sizeof v);
+    fprintf(stderr, "[prof] %s L=%d slices=%llu any=%llu hit_arcs=%llu want_lanes=%llu pairs=%llu hit_lanes=%llu "
+                    "row_slices=%llu col_slices=%llu col_iters=%llu\n",
+            what, L, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]);
+    memset(v, 0, sizeof v);
+    cudaMemcpyToSymbol(g_prof, v, sizeof v);
+}
+#else
+inline void prof_dump(const char *, int, cudaStream_t) {}
+#endif
+
 // Forward level L on graph c for `ng` groups: pull from the masks `nbr` (level
 // L - 1) into the dense array `cur`.
 int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
@@ -512,6 +628,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
         ++h->launches;
     }
     CUDA_TRY(h, cudaGetLastError());
+    prof_dump("fwd", L, st);
     return BC_OK;
 }
 
@@ -543,6 +660,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
         ++h->launches;
     }
     CUDA_TRY(h, cudaGetLastError());
+    prof_dump("bwd", L, st);
     return BC_OK;
 }
 
@@ -1088,7 +1206,7 @@ int build_border_tables(bc_handle *h) {
         CUDA_TRY(h, cudaGetLastError());
     }
     CUDA_TRY(h, cudaStreamSynchronize(st));
-    cudaFree(d_borders);
+    arena_free(d_borders);
     h->tables_ready = true;
     return BC_OK;
 }
@@ -1101,6 +1219,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
                 cudaStream_t st, bc_stats *stats, bool debug, int32_t *dist_out, double *sigma_out,
                 double *delta_out) {
     const int64_t n = h->n;
+    Trace tr;
     for (int64_t i = 0; i < k_all; ++i)
         if (sources_in[i] < 0 || sources_in[i] >= n) {
             char buf[128];
@@ -1135,7 +1254,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         std::vector<int64_t> key(active.size());
         if (!active.empty()) {
             int64_t *d_tmp = nullptr;
-            CUDA_TRY(h, cudaMalloc((void **)&d_tmp, 2 * active.size() * sizeof(int64_t)));
+            CUDA_TRY(h, arena_malloc((void **)&d_tmp, 2 * active.size() * sizeof(int64_t)));
             CUDA_TRY(h, cudaMemcpyAsync(d_tmp, active.data(), active.size() * sizeof(int64_t),
                                         cudaMemcpyHostToDevice, st));
             source_key_kernel<<<grid1d(active.size() * 32, 256), 256, 0, st>>>(
@@ -1144,7 +1263,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             CUDA_TRY(h, cudaMemcpyAsync(key.data(), d_tmp + active.size(), active.size() * sizeof(int64_t),
                                         cudaMemcpyDeviceToHost, st));
             CUDA_TRY(h, cudaStreamSynchronize(st));
-            cudaFree(d_tmp);
+            arena_free(d_tmp);
         }
         std::vector<size_t> order(active.size());
         for (size_t i = 0; i < order.size(); ++i) order[i] = i;
@@ -1158,6 +1277,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         active.swap(a2);
         where.swap(w2);
     }
+    tr.mark("run: source ordering");
     const int64_t k = (int64_t)active.size();
     const int64_t *sources = active.data();
     const int groups = debug ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(h->groups, (k + 31) / 32));
@@ -1166,11 +1286,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const int S = 32 * groups;
     if (hybir) TRY(ensure_border_state(h, S));
     if (h->d_src_cap < k) {
-        cudaFree(h->d_src);
+        arena_free(h->d_src);
         h->d_src = nullptr;
-        CUDA_TRY(h, cudaMalloc((void **)&h->d_src, std::max<int64_t>(k, 1) * sizeof(int64_t)));
+        CUDA_TRY(h, arena_malloc((void **)&h->d_src, std::max<int64_t>(k, 1) * sizeof(int64_t)));
         h->d_src_cap = k;
     }
+    tr.mark("run: state allocation");
     const int64_t launches0 = h->launches;
     int64_t h2d = 0, d2h = 0;
     if (k > 0) {
@@ -1194,9 +1315,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     int32_t *dbg_dist = nullptr;
     double *dbg_sigma = nullptr, *dbg_delta = nullptr;
     if (debug) {
-        if (dist_out) CUDA_TRY(h, cudaMalloc((void **)&dbg_dist, 32 * (size_t)n * sizeof(int32_t)));
-        if (sigma_out) CUDA_TRY(h, cudaMalloc((void **)&dbg_sigma, 32 * (size_t)n * sizeof(double)));
-        if (delta_out) CUDA_TRY(h, cudaMalloc((void **)&dbg_delta, 32 * (size_t)n * sizeof(double)));
+        if (dist_out) CUDA_TRY(h, arena_malloc((void **)&dbg_dist, 32 * (size_t)n * sizeof(int32_t)));
+        if (sigma_out) CUDA_TRY(h, arena_malloc((void **)&dbg_sigma, 32 * (size_t)n * sizeof(double)));
+        if (delta_out) CUDA_TRY(h, arena_malloc((void **)&dbg_delta, 32 * (size_t)n * sizeof(double)));
     }
 
     for (int64_t b = 0; b < n_batches; ++b) {
@@ -1262,9 +1383,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             const size_t G = (size_t)h->alloc_groups;
             const size_t pw = (size_t)depth * h->k * G;
             if (h->presence_words < pw) {
-                cudaFree(h->presence);
+                arena_free(h->presence);
                 h->presence = nullptr;
-                CUDA_TRY(h, cudaMalloc((void **)&h->presence, pw * sizeof(uint32_t)));
+                CUDA_TRY(h, arena_malloc((void **)&h->presence, pw * sizeof(uint32_t)));
                 h->presence_words = pw;
             }
             CUDA_TRY(h, cudaMemsetAsync(h->presence, 0, pw * sizeof(uint32_t), st));
@@ -1389,7 +1510,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     CUDA_TRY(h, cudaMemcpyAsync(cnts, h->counters, sizeof cnts, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));
     d2h += sizeof cnts;
-    cudaFree(dbg_dist), cudaFree(dbg_sigma), cudaFree(dbg_delta);
+    tr.mark("run: batches");
+    arena_free(dbg_dist), arena_free(dbg_sigma), arena_free(dbg_delta);
 
     double ms_f = 0, ms_b = 0, ms_border = 0;
     for (Events &e : ev) {
@@ -1448,9 +1570,9 @@ int dist_scan(bc_handle *h, int entries, cudaStream_t st) {
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, h->dist_counts, h->dist_offsets, entries + 1, st);
     if (need > h->dist_scan_bytes) {
-        cudaFree(h->dist_scan_tmp);
+        arena_free(h->dist_scan_tmp);
         h->dist_scan_tmp = nullptr;
-        CUDA_TRY(h, cudaMalloc(&h->dist_scan_tmp, need));
+        CUDA_TRY(h, arena_malloc(&h->dist_scan_tmp, need));
         h->dist_scan_bytes = need;
     }
     CUDA_TRY(h, cudaMemsetAsync(h->dist_counts + entries, 0, sizeof(int32_t), st));
@@ -1491,11 +1613,11 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
                          " (this engine has no CPU fallback)";
         return BC_ERR_INTERNAL;
     }
+    Trace tr;
     bc_handle *h = new bc_handle();
     h->device = device;
     h->n = n;
     h->n_arcs = n_arcs;
-    h->h_off.assign(offsets, offsets + n + 1);
     auto bail = [&](int rc) {
         g_create_error = h->err;
         bc_destroy(h);
@@ -1509,12 +1631,17 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
     c.n = n;
     c.n_arcs = n_arcs;
     auto body = [&]() -> int {
-        CUDA_TRY(h, cudaMalloc((void **)&c.off, (n + 1) * sizeof(int64_t)));
-        CUDA_TRY(h, cudaMalloc((void **)&c.col, std::max<int64_t>(n_arcs, 1) * sizeof(int32_t)));
-        CUDA_TRY(h, cudaMemcpy(c.off, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+        CUDA_TRY(h, arena_malloc((void **)&c.off, (n + 1) * sizeof(int64_t)));
+        CUDA_TRY(h, arena_malloc((void **)&c.col, std::max<int64_t>(n_arcs, 1) * sizeof(int32_t)));
+        // the CSR copy is queued first (it runs at PCIe speed from pinned memory) and the
+        // host builds its offsets copy and the work items while it is in flight
+        CUDA_TRY(h, cudaMemcpyAsync(c.off, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, 0));
         if (n_arcs > 0)
-            CUDA_TRY(h, cudaMemcpy(c.col, col_idx, n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice));
-        return build_items(h, c, offsets, h->item_arcs);
+            CUDA_TRY(h, cudaMemcpyAsync(c.col, col_idx, n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice, 0));
+        h->h_off.assign(offsets, offsets + n + 1);
+        const int rc_items = build_items(h, c, offsets, h->item_arcs);
+        tr.mark("create: CSR upload + work items");
+        return rc_items;
     };
     int rc = body();
     if (rc) return bail(rc);
@@ -1662,7 +1789,7 @@ int bc_run(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources, do
     if (bc_out == nullptr) return h->fail(BC_ERR_INPUT, "bc_run: bc_out is null");
     CUDA_TRY(h, cudaSetDevice(h->device));
     if (h->bc_scratch == nullptr)
-        CUDA_TRY(h, cudaMalloc((void **)&h->bc_scratch, (size_t)h->n * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->bc_scratch, (size_t)h->n * sizeof(double)));
     CUDA_TRY(h, cudaMemset(h->bc_scratch, 0, (size_t)h->n * sizeof(double)));
     TRY(bc_run_device(h, mode, sources, n_sources, h->bc_scratch, nullptr, stats));
     CUDA_TRY(h, cudaMemcpy(bc_out, h->bc_scratch, (size_t)h->n * sizeof(double),
@@ -1786,9 +1913,9 @@ int bc_dist_begin(bc_handle *h, const int64_t *sources, int64_t count, void *str
     TRY(ensure_state(h, h->groups, false));
     TRY(ensure_levels(h, 2));
     if (h->d_src_cap < count) {
-        cudaFree(h->d_src);
+        arena_free(h->d_src);
         h->d_src = nullptr;
-        CUDA_TRY(h, cudaMalloc((void **)&h->d_src, count * sizeof(int64_t)));
+        CUDA_TRY(h, arena_malloc((void **)&h->d_src, count * sizeof(int64_t)));
         h->d_src_cap = count;
     }
     CUDA_TRY(h, cudaMemcpyAsync(h->d_src, sources, count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -1925,6 +2052,8 @@ int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream) {
     return BC_OK;
 }
 
+void bc_release_cached_memory(void) { arena().flush_all(); }
+
 const char *bc_last_error(bc_handle *h) {
     return h ? h->err.c_str() : g_create_error.c_str();
 }
@@ -1935,15 +2064,15 @@ void bc_destroy(bc_handle *h) {
     free_state(h);
     free_partition(h);
     free_csr(h->full);
-    cudaFree(h->counters);
-    cudaFree(h->dflags);
-    cudaFree(h->d_maxlvl);
-    cudaFree(h->d_src);
-    cudaFree(h->bc_scratch);
-    cudaFree((void *)h->d_lvl_ptrs);
-    cudaFree(h->presence);
-    cudaFree(h->dist_border_v), cudaFree(h->dist_counts), cudaFree(h->dist_offsets);
-    cudaFree(h->dist_scan_tmp);
+    arena_free(h->counters);
+    arena_free(h->dflags);
+    arena_free(h->d_maxlvl);
+    arena_free(h->d_src);
+    arena_free(h->bc_scratch);
+    arena_free((void *)h->d_lvl_ptrs);
+    arena_free(h->presence);
+    arena_free(h->dist_border_v), arena_free(h->dist_counts), arena_free(h->dist_offsets);
+    arena_free(h->dist_scan_tmp);
     delete h;
 }
 

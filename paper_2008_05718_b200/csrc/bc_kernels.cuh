@@ -44,6 +44,17 @@ namespace bcb200 {
 constexpr int kWarpsPerBlock = BC_WPB;
 constexpr unsigned kFull = 0xffffffffu;
 
+// -DBC_PROFILE: dev build that counts what the gather loops do (dumped per launch on stderr)
+#ifdef BC_PROFILE
+__device__ unsigned long long g_prof[16];
+#define PROF_ADD(slot, value)                                                      \
+    do {                                                                           \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[slot], (unsigned long long)(value)); \
+    } while (0)
+#else
+#define PROF_ADD(slot, value) do { } while (0)
+#endif
+
 struct LevelParams {
     // graph (full CSR or the cut-arc-free CSR of a partitioning)
     const int64_t *off;
@@ -154,7 +165,19 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
             hit_n = __ldg(nmask + w_n) & want;
         }
         unsigned any = __ballot_sync(kFull, hit != 0);
+        PROF_ADD(0, 1);
         if (any == 0) continue;
+        PROF_ADD(1, 1);
+        PROF_ADD(2, __popc(any));
+        PROF_ADD(3, __popc(want));
+#ifdef BC_PROFILE
+        {
+            const unsigned prof_pairs = __reduce_add_sync(kFull, __popc(hit));
+            const unsigned prof_lanes = __popc(__reduce_or_sync(kFull, hit));
+            PROF_ADD(4, prof_pairs);
+            PROF_ADD(5, prof_lanes);
+        }
+#endif
         bool rows;
         if (BC_GATHER == 1) rows = true;
         else if (BC_GATHER == 2) rows = __popc(any) <= kSparseSlice;
@@ -168,6 +191,7 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
         }
         if (rows) {
             const uint32_t lbit = 1u << lane;
+            PROF_ADD(6, 1);
             while (any) {
                 int j[kRowUnroll];
                 int32_t wj[kRowUnroll];
@@ -198,7 +222,9 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
             got |= __reduce_or_sync(kFull, hit);
             uint32_t c = transpose32(hit, lane);  // arcs that hit this lane's BFS instance
             if (COUNT_T) tcount += __popc(c);
+            PROF_ADD(7, 1);
             while (__any_sync(kFull, c != 0)) {
+                PROF_ADD(8, 1);
                 const int j0 = __ffs(c) - 1;
                 const bool p0 = c != 0;
                 c &= c - 1;
