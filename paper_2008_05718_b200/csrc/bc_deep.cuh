@@ -1,0 +1,345 @@
+// bc_deep.cuh -- persistent sweeps for high-diameter graphs (road networks, grids).
+//
+// A 2048 x 2048 road-like graph has ~4000 BFS levels whose frontiers hold a few
+// thousand vertices per source.  Driven level by level from the host, every
+// level costs three launches, a report read-back and a stream synchronise, and
+// the kernels are too short to hide any of it.  The two kernels here run MANY
+// consecutive thin levels in one cooperative launch: the grid walks a level,
+// meets at a grid-wide barrier, and moves to the next one; the host comes back
+// only when the run ends (frontier empty, level no longer thin, queue nearly
+// full, level budget used) and reads the per-level log once.
+//
+// Arithmetic is that of fwd_push_thin_kernel / push_post_kernel /
+// advance_level_kernel (forward) and bwd_queue_thin_kernel /
+// swap_scatter_kernel (backward) in bc_kernels.cuh; reference functions being
+// replaced: initial_relax (relax.py:75-101) and process_level vertex-pull
+// (backward.py:95-103), for consecutive levels of one source batch.
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bc_kernels.cuh"
+
+namespace bcb200 {
+
+namespace cg = cooperative_groups;
+
+constexpr int kDeepThreads = 256;
+constexpr int kDeepWarps = kDeepThreads / 32;
+constexpr int kDeepMaxGroups = 128;   // groups per batch the persistent sweeps accept
+
+struct DeepFwdParams {
+    const int64_t *off;
+    const int32_t *col;
+    int64_t n;
+    QueueParams q;             // q_beg / q_end hold the frontier of the first level on entry
+    int64_t *q_beg, *q_end, *q_lbeg;   // writable views of the device-resident ranges
+    uint32_t *vis;
+    uint32_t *next;            // all-zero scratch masks (left all-zero)
+    double *sigma;
+    uint32_t *live;            // live[level][G]
+    unsigned long long *counters;
+    unsigned long long *lstat;   // [0] vertices [1] arcs [2] largest degree of the level being produced
+    unsigned long long *log;     // [iteration][3 + 2G], the advance_level_kernel report of every level
+    int *run_info;               // [0] levels produced by this launch
+    int ng, G;
+    int first_level;             // level produced by iteration 0
+    int max_levels;              // iterations allowed in this launch
+    unsigned long long graph_arcs;   // arcs of the graph * groups (push / pull switch)
+    unsigned long long push_beta;
+    unsigned long long thin_degree;
+    unsigned long long max_degree;
+};
+
+// Forward: consecutive top-down levels, one THREAD per frontier entry.
+__global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFwdParams p) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t stage[kDeepWarps][kStage];
+    __shared__ int64_t s_pref[kDeepMaxGroups + 1];
+    __shared__ int s_cont;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = p.n;
+    int *cont_flag = p.run_info + 1;
+
+    for (int it = 0;; ++it) {
+        const int L = p.first_level + it;
+        // ---- phase 1: push from the frontier queues.  The (group, entry) space is
+        // flattened, every group padded to whole warps, so that all threads stay
+        // busy when one group's frontier is short and a warp never straddles groups.
+        if (threadIdx.x <= p.ng) {
+            int64_t acc = 0;
+            for (int g = 0; g < (int)threadIdx.x; ++g) acc += (p.q.q_end[g] - p.q.q_beg[g] + 31) & ~(int64_t)31;
+            s_pref[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        unsigned c_t = 0;
+        {
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;   // f0 only grows
+                const int64_t end = p.q.q_end[g];
+                const int64_t i = p.q.q_beg[g] + (f0 - s_pref[g]) + lane;
+                const uint32_t *gvis = p.vis + (size_t)g * n;
+                uint32_t *gnext = p.next + (size_t)g * n;
+                double *gsig = p.sigma + (size_t)g * n * 32;
+                const size_t qbase = (size_t)g * p.q.cap;
+                int32_t u = 0;
+                uint32_t mask = 0;
+                int64_t a = 0, e = 0;
+                if (i < end) {
+                    u = p.q.q_v[qbase + i];
+                    mask = p.q.q_m[qbase + i];
+                    a = p.off[u];
+                    e = p.off[u + 1];
+                }
+                int rounds = (int)(e - a);
+                rounds = __reduce_max_sync(kFull, rounds);
+                const double *urow = gsig + (size_t)u * 32;
+                int staged = 0;  // warp-uniform
+                auto flush = [&]() {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(p.q.q_count + g, (unsigned long long)staged);
+                    base = __shfl_sync(kFull, base, 0);
+                    for (int k = lane; k < staged; k += 32) p.q.q_v[qbase + base + k] = stage[warp][k];
+                    staged = 0;
+                    __syncwarp();
+                };
+                for (int r = 0; r < rounds; ++r, ++a) {
+                    bool fresh_vertex = false;
+                    int32_t w = 0;
+                    if (a < e) {
+                        w = __ldg(p.col + a);
+                        uint32_t fresh = mask & ~gvis[w];
+                        if (fresh) {
+                            const uint32_t old = atomicOr(gnext + w, fresh);
+                            fresh_vertex = old == 0;
+                            double *wrow = gsig + (size_t)w * 32;
+                            while (fresh) {
+                                const int bit = __ffs(fresh) - 1;
+                                fresh &= fresh - 1;
+                                atomicAdd(wrow + bit, urow[bit]);  // exact: integer-valued fp64
+                                ++c_t;
+                            }
+                        }
+                    }
+                    const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+                    if (newm) {
+                        if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
+                        staged += __popc(newm);
+                        __syncwarp();
+                        if (staged > kStage - 32) flush();
+                    }
+                }
+                if (staged) flush();
+            }
+        }
+        {
+            const unsigned t = __reduce_add_sync(kFull, c_t);
+            if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
+        }
+        grid.sync();
+
+        // ---- phase 2: the entries appended above become level L (same flattening)
+        if (threadIdx.x <= p.ng) {
+            int64_t acc = 0;
+            for (int g = 0; g < (int)threadIdx.x; ++g)
+                acc += ((int64_t)p.q.q_count[g] - p.q_lbeg[g] + 31) & ~(int64_t)31;
+            s_pref[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        {
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t end = (int64_t)p.q.q_count[g];
+                const int64_t i = p.q_lbeg[g] + (f0 - s_pref[g]) + lane;
+                const size_t qbase = (size_t)g * p.q.cap;
+                unsigned long long nr = 0, ar = 0, nv = 0, fa = 0, md = 0;
+                uint32_t any = 0;
+                if (i < end) {
+                    const int32_t w = p.q.q_v[qbase + i];
+                    const uint32_t m = p.next[(size_t)g * n + w];
+                    p.q.q_m[qbase + i] = m;
+                    p.vis[(size_t)g * n + w] |= m;
+                    p.next[(size_t)g * n + w] = 0u;
+                    const unsigned long long deg = (unsigned long long)(p.off[w + 1] - p.off[w]);
+                    any = m;
+                    nr = __popc(m);
+                    ar = __popc(m) * deg;
+                    nv = 1;
+                    fa = deg;
+                    md = deg;
+                }
+                any = __reduce_or_sync(kFull, any);
+                for (int o = 16; o > 0; o >>= 1) {
+                    nr += __shfl_xor_sync(kFull, nr, o);
+                    ar += __shfl_xor_sync(kFull, ar, o);
+                    nv += __shfl_xor_sync(kFull, nv, o);
+                    fa += __shfl_xor_sync(kFull, fa, o);
+                    md = max(md, __shfl_xor_sync(kFull, md, o));
+                }
+                if (lane == 0) {
+                    atomicOr(p.live + (size_t)L * p.G + g, any);
+                    atomicAdd(p.counters + 0, nr);
+                    atomicAdd(p.counters + 1, ar);
+                    atomicAdd(p.lstat + 0, nv);
+                    atomicAdd(p.lstat + 1, fa);
+                    atomicMax(p.lstat + 2, md);
+                }
+            }
+        }
+        grid.sync();
+
+        // ---- phase 3: publish the level, rotate the ranges, decide whether to go on
+        if (blockIdx.x == 0) {
+            unsigned long long *rep = p.log + (size_t)it * (3 + 2 * p.G);
+            const int g = threadIdx.x;
+            unsigned long long nverts = p.lstat[0], farcs = p.lstat[1], maxdeg = p.lstat[2];
+            uint32_t alive_any = 0;
+            unsigned long long used = 0;
+            for (int j = 0; j < p.ng; ++j) {
+                alive_any |= p.live[(size_t)L * p.G + j];
+                used = max(used, p.q.q_count[j]);
+            }
+            __syncthreads();
+            if (g < 3) rep[g] = p.lstat[g];
+            if (g < p.G) {
+                const unsigned long long c = p.q.q_count[g];
+                rep[3 + g] = c;
+                rep[3 + p.G + g] = p.live[(size_t)L * p.G + g];
+                p.q_beg[g] = p.q_lbeg[g];
+                p.q_end[g] = (int64_t)c;
+                p.q_lbeg[g] = (int64_t)c;
+            }
+            __syncthreads();
+            if (g == 0) {
+                p.lstat[0] = p.lstat[1] = p.lstat[2] = 0;
+                const unsigned long long room = min((unsigned long long)n, farcs) + 1;
+                const bool go = alive_any != 0 && it + 1 < p.max_levels &&
+                                farcs * p.push_beta <= p.graph_arcs && maxdeg <= p.max_degree &&
+                                farcs <= p.thin_degree * nverts &&
+                                (unsigned long long)p.q.cap - used >= room;
+                p.run_info[0] = it + 1;
+                *cont_flag = go ? 1 : 0;
+            }
+        }
+        grid.sync();
+        if (threadIdx.x == 0) s_cont = *(volatile int *)cont_flag;
+        __syncthreads();
+        if (!s_cont) break;
+    }
+}
+
+struct DeepBwdParams {
+    const int64_t *off;
+    const int32_t *col;
+    int64_t n;
+    QueueParams q;               // q_v / q_m / cap
+    const int64_t *range_table;  // [level][0: begin, 1: end][G]
+    const double *sigma;
+    double *coef;
+    double *delta;               // only with STORE_DELTA
+    double *bcg;
+    int ng, G;
+    int hi, lo;                  // levels hi, hi - 1, ..., lo
+    const uint32_t *nbr_first;   // masks of level hi + 1 (nullptr: hi is the deepest level)
+    uint32_t *erase_first;       // scratch array holding level hi + 1 (nullptr: dense array, keep)
+    uint32_t *scr0, *scr1;       // all-zero scratch arrays (apart from erase_first's content)
+    int first_write;             // scratch (0 / 1) that receives level hi
+    int accumulate;
+};
+
+// Backward: consecutive queue levels, one thread per entry (bwd_queue_thin_kernel),
+// with the mask hand-over of swap_scatter_kernel between levels.  On exit the
+// masks of level `lo` sit in scratch (first_write + hi - lo) & 1, everything
+// else in the scratch arrays is zero again.
+template <bool STORE_DELTA>
+__global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepBwdParams p) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int64_t s_pref[kDeepMaxGroups + 1];
+    const int lane = threadIdx.x & 31;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = p.n;
+    const uint32_t *nbr = p.nbr_first;
+    uint32_t *erase = p.erase_first;
+    int widx = p.first_write;
+    for (int L = p.hi; L >= p.lo; --L) {
+        uint32_t *wr = widx ? p.scr1 : p.scr0;
+        const int64_t *beg_t = p.range_table + ((size_t)L * 2 + 0) * p.G;
+        const int64_t *end_t = p.range_table + ((size_t)L * 2 + 1) * p.G;
+        if (threadIdx.x <= p.ng) {
+            int64_t acc = 0;
+            for (int g = 0; g < (int)threadIdx.x; ++g) acc += (end_t[g] - beg_t[g] + 31) & ~(int64_t)31;
+            s_pref[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        {
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t i = beg_t[g] + (f0 - s_pref[g]) + lane;
+                if (i >= end_t[g]) continue;
+                const size_t qbase = (size_t)g * p.q.cap;
+                const uint32_t *gn = nbr ? nbr + (size_t)g * n : nullptr;
+                const double *gsig = p.sigma + (size_t)g * n * 32;
+                double *gcoef = p.coef + (size_t)g * n * 32;
+                const int64_t v = p.q.q_v[qbase + i];
+                const uint32_t m = p.q.q_m[qbase + i];
+                uint32_t want = m;
+                const int64_t a0 = p.off[v], a1 = p.off[v + 1];
+                double total_d = 0.0;
+                while (want) {
+                    const int bit = __ffs(want) - 1;
+                    want &= want - 1;
+                    double acc = 0.0;
+                    if (gn != nullptr)
+                        for (int64_t a = a0; a < a1; ++a) {
+                            const int32_t w = __ldg(p.col + a);
+                            if ((gn[w] >> bit) & 1u) acc += gcoef[(size_t)w * 32 + bit];
+                        }
+                    const size_t idx = (size_t)v * 32 + bit;
+                    const double sv = gsig[idx];
+                    const double d = sv * acc;
+                    gcoef[idx] = (1.0 + d) / sv;
+                    if (STORE_DELTA) p.delta[(size_t)g * n * 32 + idx] = d;
+                    total_d += d;
+                }
+                if (p.accumulate) p.bcg[(size_t)g * n + v] += total_d;
+                wr[(size_t)g * n + v] = m;   // level L becomes the children masks of level L - 1
+            }
+        }
+        __syncthreads();   // s_pref is rewritten by the next level
+        grid.sync();
+        if (erase != nullptr) {
+            const int64_t *eb = p.range_table + ((size_t)(L + 1) * 2 + 0) * p.G;
+            const int64_t *ee = p.range_table + ((size_t)(L + 1) * 2 + 1) * p.G;
+            if (threadIdx.x <= p.ng) {
+                int64_t acc = 0;
+                for (int g = 0; g < (int)threadIdx.x; ++g) acc += (ee[g] - eb[g] + 31) & ~(int64_t)31;
+                s_pref[threadIdx.x] = acc;
+            }
+            __syncthreads();
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t i = eb[g] + (f0 - s_pref[g]) + lane;
+                if (i < ee[g]) erase[(size_t)g * n + p.q.q_v[(size_t)g * p.q.cap + i]] = 0u;
+            }
+            __syncthreads();
+            grid.sync();
+        }
+        nbr = wr;
+        erase = wr;
+        widx ^= 1;
+    }
+}
+
+}  // namespace bcb200

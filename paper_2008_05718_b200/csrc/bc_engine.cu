@@ -8,6 +8,7 @@
 // bc_border.cuh or fails.
 #include "bc_b200.h"
 #include "bc_border.cuh"
+#include "bc_deep.cuh"
 #include "bc_dist.cuh"
 #include "bc_kernels.cuh"
 
@@ -144,6 +145,7 @@ struct Events {
 
 constexpr unsigned long long kQueueMaxDegree = 8192;
 constexpr unsigned long long kThinDegree = 8;  // average degree up to which a level runs thread-per-entry
+constexpr int kDeepLevels = 1024;              // levels one persistent launch may produce
 
 // Border-table feasibility: b_p^2 entries of 12 B per part.
 constexpr double kMaxTableBytes = 64e9;
@@ -162,6 +164,11 @@ struct bc_handle {
     int reports = 1;
     int sparse = 1;        // allow queue levels + top-down push (direction-optimising switch)
     int push_beta = 16;    // push when frontier arcs * beta <= arcs of the graph
+    int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
+    int deep_blocks_per_sm = 0;   // 0 = what the occupancy calculator allows
+    int deep_grid_f = 0, deep_grid_b = 0;
+    unsigned long long *deep_log = nullptr;
+    int *deep_info = nullptr;
     // ---- partition ------------------------------------------------------
     int k = 1;
     std::vector<int32_t> h_part;
@@ -359,6 +366,9 @@ void free_state(bc_handle *h) {
     arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
     arena_free(h->scrA), arena_free(h->scrB), arena_free(h->lstat), arena_free(h->report);
     arena_free(h->range_table);
+    arena_free(h->deep_log), arena_free(h->deep_info);
+    h->deep_log = nullptr;
+    h->deep_info = nullptr;
     h->report = nullptr;
     h->range_table = nullptr;
     h->range_table_cap = 0;
@@ -482,6 +492,33 @@ int ensure_queues(bc_handle *h) {
     TRY(dev_alloc(h, &h->report, 3 + 2 * G));
     CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
     CUDA_TRY(h, cudaMemset(h->scrB, 0, G * n * sizeof(uint32_t)));
+    return BC_OK;
+}
+
+// Buffers and grid size of the persistent sweeps (bc_deep.cuh).  The grid must be
+// fully resident for the grid-wide barrier, so it comes from the occupancy
+// calculator (the backward kernel is the heavier of the two).
+int ensure_deep(bc_handle *h) {
+    if (h->deep_log != nullptr) return BC_OK;
+    const size_t G = (size_t)h->alloc_groups;
+    TRY(dev_alloc(h, &h->deep_log, (size_t)kDeepLevels * (3 + 2 * G)));
+    TRY(dev_alloc(h, &h->deep_info, (size_t)4));
+    int per_sm_f = 0, per_sm_b = 0, per_sm_d = 0, sms = 0;
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, deep_forward_kernel, kDeepThreads, 0));
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, deep_backward_kernel<false>,
+                                                              kDeepThreads, 0));
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, deep_backward_kernel<true>,
+                                                              kDeepThreads, 0));
+    CUDA_TRY(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    per_sm_b = std::min(per_sm_b, per_sm_d);
+    if (h->deep_blocks_per_sm > 0) {
+        per_sm_f = std::min(per_sm_f, h->deep_blocks_per_sm);
+        per_sm_b = std::min(per_sm_b, h->deep_blocks_per_sm);
+    }
+    if (per_sm_f < 1 || per_sm_b < 1 || sms < 1)
+        return h->fail(BC_ERR_INTERNAL, "persistent sweep kernels do not fit on an SM");
+    h->deep_grid_f = per_sm_f * sms;
+    h->deep_grid_b = per_sm_b * sms;
     return BC_OK;
 }
 
@@ -878,7 +915,74 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 TRY(upload_ranges(h, prev, st));
                 TRY(upload_lbeg());
             }
-            if (prev.farcs <= kThinDegree * prev.nverts)  // low-degree level: one thread per entry
+            const bool thin = prev.farcs <= kThinDegree * prev.nverts;
+            if (thin && h->deep && ng <= kDeepMaxGroups) {
+                // ---- a run of thin levels inside one cooperative launch
+                TRY(ensure_deep(h));
+                TRY(ensure_live(h, L + kDeepLevels + 1));
+                DeepFwdParams dp{};
+                dp.off = c.off;
+                dp.col = c.col;
+                dp.n = n;
+                dp.q = queue_params(h);
+                dp.q_beg = h->d_qbeg;
+                dp.q_end = h->d_qend;
+                dp.q_lbeg = h->d_qlbeg;
+                dp.vis = h->vis;
+                dp.next = h->scrA;
+                dp.sigma = h->sigma;
+                dp.live = h->live;
+                dp.counters = h->counters + h->cnt_off;
+                dp.lstat = h->lstat;
+                dp.log = h->deep_log;
+                dp.run_info = h->deep_info;
+                dp.ng = ng;
+                dp.G = (int)G;
+                dp.first_level = L;
+                dp.max_levels = kDeepLevels;
+                dp.graph_arcs = graph_arcs;
+                dp.push_beta = (unsigned long long)h->push_beta;
+                dp.thin_degree = kThinDegree;
+                dp.max_degree = kQueueMaxDegree;
+                void *args[] = {&dp};
+                CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_kernel, dim3(h->deep_grid_f),
+                                                        dim3(kDeepThreads), args, 0, st));
+                ++h->launches;
+                int info[2] = {0, 0};
+                CUDA_TRY(h, cudaMemcpyAsync(info, h->deep_info, sizeof info, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaStreamSynchronize(st));
+                const int done = info[0];
+                if (done < 1 || done > kDeepLevels)
+                    return h->fail(BC_ERR_INTERNAL, "persistent forward sweep returned no level");
+                const size_t rw = 3 + 2 * G;
+                std::vector<unsigned long long> log((size_t)done * rw);
+                CUDA_TRY(h, cudaMemcpyAsync(log.data(), h->deep_log, log.size() * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaStreamSynchronize(st));
+                reps.pop_back();  // `cur` is re-created below, level by level
+                for (int j = 0; j < done; ++j) {
+                    const unsigned long long *rep = log.data() + (size_t)j * rw;
+                    bool alive = false;
+                    for (int g = 0; g < ng; ++g) alive |= rep[3 + G + g] != 0;
+                    if (!alive) {
+                        *depth_out = L + j;
+                        return BC_OK;
+                    }
+                    reps.emplace_back();
+                    LevelRep &lr = reps.back();
+                    lr.queued = true;
+                    lr.qb.assign(qcount.begin(), qcount.begin() + ng);
+                    for (size_t g = 0; g < G; ++g) qcount[g] = rep[3 + g];
+                    lr.qe.assign(qcount.begin(), qcount.begin() + ng);
+                    lr.nverts = rep[0];
+                    lr.farcs = rep[1];
+                    lr.maxdeg = rep[2];
+                }
+                L += done - 1;
+                device_level = L;
+                continue;
+            }
+            if (thin)  // low-degree level: one thread per entry
                 fwd_push_thin_kernel<<<dim3(queue_blocks(prev, kWarpsPerBlock * 32), ng),
                                        kWarpsPerBlock * 32, 0, st>>>(
                     c.off, c.col, n, queue_params(h), h->vis, h->scrA, h->sigma,
@@ -985,6 +1089,48 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             }
         }
         int cur_holder = -1;  // scratch that already holds level L's masks
+        auto queue_thin = [&](const LevelRep &x) {
+            return x.slot < 0 && x.farcs * (unsigned long long)h->push_beta <= graph_arcs &&
+                   x.maxdeg <= kQueueMaxDegree && x.farcs <= kThinDegree * x.nverts;
+        };
+        if (h->deep && ng <= kDeepMaxGroups && queue_thin(r) && L - 1 >= last && queue_thin(reps[L - 1])) {
+            // ---- a run of thin queue levels inside one cooperative launch
+            int lo = L;
+            while (lo - 1 >= last && queue_thin(reps[lo - 1])) --lo;
+            TRY(ensure_deep(h));
+            DeepBwdParams dp{};
+            dp.off = c.off;
+            dp.col = c.col;
+            dp.n = h->n;
+            dp.q = queue_params(h);
+            dp.range_table = h->range_table;
+            dp.sigma = h->sigma;
+            dp.coef = h->coef;
+            dp.delta = h->delta;
+            dp.bcg = h->bcg;
+            dp.ng = ng;
+            dp.G = (int)G;
+            dp.hi = L;
+            dp.lo = lo;
+            dp.nbr_first = nbr;
+            dp.erase_first = (!deepest && reps[L + 1].slot < 0) ? scr[holder] : nullptr;
+            dp.scr0 = scr[0];
+            dp.scr1 = scr[1];
+            dp.first_write = holder == 0 ? 1 : 0;
+            dp.accumulate = debug ? 0 : 1;
+            void *args[] = {&dp};
+            if (debug)
+                CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_kernel<true>, dim3(h->deep_grid_b),
+                                                        dim3(kDeepThreads), args, 0, st));
+            else
+                CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_kernel<false>, dim3(h->deep_grid_b),
+                                                        dim3(kDeepThreads), args, 0, st));
+            ++h->launches;
+            holder = (dp.first_write + (L - lo)) & 1;   // scratch that now holds level `lo`
+            held_level = lo;
+            L = lo;
+            continue;
+        }
         if (r.slot >= 0) {
             TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, h->lvl[r.slot], nbr));
         } else if (r.farcs * (unsigned long long)h->push_beta <= graph_arcs && r.maxdeg <= kQueueMaxDegree) {
@@ -1679,6 +1825,18 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     }
     if (k == "sparse") {
         h->sparse = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "deep") {
+        h->deep = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "deep_blocks_per_sm") {
+        if (value < 0 || value > 32) return h->fail(BC_ERR_INPUT, "deep_blocks_per_sm must be in [0, 32]");
+        h->deep_blocks_per_sm = (int)value;
+        arena_free(h->deep_log), arena_free(h->deep_info);
+        h->deep_log = nullptr;
+        h->deep_info = nullptr;
         return BC_OK;
     }
     if (k == "push_beta") {

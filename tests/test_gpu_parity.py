@@ -172,6 +172,29 @@ def test_deep_graph_path_and_grid():
     assert np.allclose(bc, O.brandes_bc(r, srcs)[0], rtol=RTOL, atol=ATOL)
 
 
+def test_persistent_sweeps_equal_level_by_level():
+    # runs of thin levels inside one cooperative launch (bc_deep.cuh) against one launch per level
+    cases = [(G.path(2500), [0, 17, 1250, 2499]),                 # > 1024 levels: several launches
+             (G.road_like(80, 80, keep=0.2, seed=5), list(range(0, 6400, 61))),
+             (G.grid(40, 25), list(range(0, 1000, 7)))]
+    for g, srcs in cases:
+        out = {}
+        for deep in (0, 1):
+            with Engine(g) as e:
+                e.set_option("deep", deep)
+                e.set_option("groups", 2)
+                d, s, dl = e.debug_sources(srcs[:20])
+                bc, st = e.run(srcs)
+            out[deep] = (d, s, dl, bc, st)
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+        assert np.array_equal(out[0][2], out[1][2])          # same arithmetic, same order
+        assert np.allclose(out[0][3], out[1][3], rtol=1e-12, atol=1e-12)
+        for key in ("reached", "arcs_reached", "dag_arcs", "max_levels"):
+            assert out[0][4][key] == out[1][4][key], key
+        assert out[1][4]["launches"] < out[0][4]["launches"]
+        assert np.allclose(out[1][3], O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
+
+
 def test_deterministic_and_linear(rmat12):
     g = rmat12
     a = list(range(0, 4096, 9))

@@ -30,3 +30,11 @@ for d in sorted(data, key=lambda d: -d[2])[:top]:
     stalls = " ".join("%s=%d" % (k[6:10], v) for k, v in zip(keys, d[5:]) if v * 20 > d[2])
     print("%4d %-64s smp %5.1f%% ins %5.1f%% act %4.1f | %s"
           % (d[0], d[1], 100 * d[2] / ts, 100 * d[3] / ti, d[4] / max(d[3], 1), stalls))
+
+# instruction / sample share by source region of bc_kernels.cuh (line ranges given as a:b,c:d ...)
+if len(sys.argv) > 4:
+    for spec in sys.argv[4].split(","):
+        a, b = (int(x) for x in spec.split(":"))
+        ins = sum(d[3] for d in data if a <= d[0] <= b)
+        smp = sum(d[2] for d in data if a <= d[0] <= b)
+        print("lines %4d-%4d: ins %5.1f%% samples %5.1f%%" % (a, b, 100 * ins / ti, 100 * smp / ts))
