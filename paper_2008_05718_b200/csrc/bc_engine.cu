@@ -133,6 +133,7 @@ struct Csr {
     int64_t *off = nullptr;
     int32_t *col = nullptr;
     int n_chk = 0, n_rng = 0, n_hub = 0;
+    int64_t heavy_slices = 0;   // kHeavySlice-arc slices over all vertices above kHeavyDeg arcs
     int32_t *chk_v = nullptr;
     int64_t *chk_a0 = nullptr, *chk_a1 = nullptr;
     int32_t *rng_v0 = nullptr, *rng_nv = nullptr;
@@ -163,7 +164,9 @@ struct bc_handle {
     int item_arcs = 512;
     int reports = 1;
     int sparse = 1;        // allow queue levels + top-down push (direction-optimising switch)
-    int push_beta = 16;    // push when frontier arcs * beta <= arcs of the graph
+    int reorder = 1;       // group sources by the size of their 2-hop neighbourhood
+    int push_beta_late = 24;   // same, once a pull level has run: a late pull scans unvisited vertices only
+    int push_beta = 4;     // push when frontier arcs * beta <= arcs of the graph
     int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
     int deep_blocks_per_sm = 0;   // 0 = what the occupancy calculator allows
     int deep_grid_f = 0, deep_grid_b = 0;
@@ -219,6 +222,8 @@ struct bc_handle {
     int64_t *d_qbeg = nullptr, *d_qend = nullptr, *d_qlbeg = nullptr;
     uint32_t *scrA = nullptr, *scrB = nullptr;
     unsigned long long *lstat = nullptr;
+    HeavyRec *heavy = nullptr;      // slices of the heavy entries of the current frontier level
+    int64_t heavy_cap = 0;
     unsigned long long *report = nullptr;   // per-level report read by the host (forward_adaptive)
     int64_t *range_table = nullptr;        // queue ranges of every level (backward_adaptive)
     int64_t range_table_cap = 0;
@@ -316,8 +321,10 @@ int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
         run_nv = 0;
         run_arcs = 0;
     };
+    int64_t heavy_slices = 0;
     for (int64_t v = 0; v < c.n; ++v) {
         const int64_t deg = off[v + 1] - off[v];
+        if (deg > kHeavyDeg) heavy_slices += (deg + kHeavySlice - 1) / kHeavySlice;
         if (deg > hub_deg) {
             flush();
             hub_v.push_back((int32_t)v);
@@ -342,6 +349,7 @@ int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
     c.n_chk = (int)chk_v.size();
     c.n_rng = (int)rng_v0.size();
     c.n_hub = (int)hub_v.size();
+    c.heavy_slices = heavy_slices;
     TRY(upload(h, &c.chk_v, chk_v));
     TRY(upload(h, &c.chk_a0, chk_a0));
     TRY(upload(h, &c.chk_a1, chk_a1));
@@ -367,6 +375,9 @@ void free_state(bc_handle *h) {
     arena_free(h->scrA), arena_free(h->scrB), arena_free(h->lstat), arena_free(h->report);
     arena_free(h->range_table);
     arena_free(h->deep_log), arena_free(h->deep_info);
+    arena_free(h->heavy);
+    h->heavy = nullptr;
+    h->heavy_cap = 0;
     h->deep_log = nullptr;
     h->deep_info = nullptr;
     h->report = nullptr;
@@ -489,7 +500,9 @@ int ensure_queues(bc_handle *h) {
     TRY(dev_alloc(h, &h->scrA, G * n));
     TRY(dev_alloc(h, &h->scrB, G * n));
     TRY(dev_alloc(h, &h->lstat, (size_t)4));
-    TRY(dev_alloc(h, &h->report, 3 + 2 * G));
+    TRY(dev_alloc(h, &h->report, 4 + 2 * G));
+    h->heavy_cap = (int64_t)G * std::max(h->full.heavy_slices, h->intra.heavy_slices) + 1;
+    TRY(dev_alloc(h, &h->heavy, (size_t)h->heavy_cap));
     CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
     CUDA_TRY(h, cudaMemset(h->scrB, 0, G * n * sizeof(uint32_t)));
     return BC_OK;
@@ -785,6 +798,7 @@ struct LevelRep {
     std::vector<int64_t> qb, qe;
     unsigned long long nverts = 0, farcs = 0;  // vertices in the level, their arcs (all groups)
     unsigned long long maxdeg = 0;             // largest degree in the level
+    long long heavy = 0;   // slice records of its heavy entries in h->heavy (-1: not built)
 };
 
 QueueParams queue_params(bc_handle *h) {
@@ -831,12 +845,14 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
     const size_t G = (size_t)h->alloc_groups;
     const int64_t n = h->n;
     TRY(ensure_queues(h));
+    const std::vector<int64_t> &c_off_host = h->h_off;   // adaptive sweeps run on the full graph only
     reps.clear();
     reps.emplace_back();
     // level 0: the sources, as a dense array (begin_batch) and as a queue
     std::vector<unsigned long long> qcount(G, 0);
     {
         LevelRep &r0 = reps[0];
+        std::vector<HeavyRec> heavy0;
         r0.slot = 0;
         r0.queued = true;
         r0.qb.assign(ng, 0);
@@ -859,15 +875,23 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
             r0.qe[g] = (int64_t)qv.size();
             qcount[g] = qv.size();
             r0.nverts += qv.size();
-            for (int32_t v : qv) {
-                const unsigned long long d = (unsigned long long)(h->h_off[v + 1] - h->h_off[v]);
+            for (size_t qi = 0; qi < qv.size(); ++qi) {
+                const int32_t v = qv[qi];
+                const unsigned long long d = (unsigned long long)(c_off_host[v + 1] - c_off_host[v]);
                 r0.farcs += d;
                 r0.maxdeg = std::max(r0.maxdeg, d);
+                if (d > (unsigned long long)kHeavyDeg)
+                    for (int sl = 0; sl < (int)((d + kHeavySlice - 1) / kHeavySlice); ++sl)
+                        heavy0.push_back(HeavyRec{(int64_t)qi, g, sl});
             }
         }
         CUDA_TRY(h, cudaMemcpyAsync(h->q_count, qcount.data(), G * sizeof(unsigned long long),
                                     cudaMemcpyHostToDevice, st));
         CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 4 * sizeof(unsigned long long), st));
+        if (!heavy0.empty())
+            CUDA_TRY(h, cudaMemcpyAsync(h->heavy, heavy0.data(), heavy0.size() * sizeof(HeavyRec),
+                                        cudaMemcpyHostToDevice, st));
+        r0.heavy = (long long)heavy0.size();
         CUDA_TRY(h, cudaStreamSynchronize(st));  // the staging vectors go out of scope
     }
     auto upload_lbeg = [&]() -> int {
@@ -877,10 +901,11 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                                     cudaMemcpyHostToDevice, st));
         return BC_OK;
     };
+    bool pulled = false;    // a pull level has run (the frontier is past its peak)
     int device_level = -1;  // level whose ranges sit in d_qbeg / d_qend (and d_qlbeg = q_count)
     int next_slot = 1;
     const unsigned long long graph_arcs = (unsigned long long)std::max<int64_t>(c.n_arcs, 1) * ng;
-    std::vector<unsigned long long> report(3 + 2 * G);
+    std::vector<unsigned long long> report(4 + 2 * G);
     for (int L = 1;; ++L) {
         TRY(ensure_live(h, L + 1));
         reps.emplace_back();
@@ -892,8 +917,11 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                                   (prev.queued ? 0 : (int64_t)prev.nverts) + 1;
         // a queue entry is walked by one warp: keep vertices with very long adjacencies on the
         // dense kernels, which slice them
-        bool push = prev.farcs * (unsigned long long)h->push_beta <= graph_arcs &&
-                    prev.maxdeg <= kQueueMaxDegree;
+        // entries above kHeavyDeg arcs are pushed slice by slice from the heavy records of the
+        // level (a level that came out of a persistent run has none: pull from it instead)
+        const unsigned long long beta = (unsigned long long)(pulled ? h->push_beta_late : h->push_beta);
+        bool push = prev.farcs * beta <= graph_arcs &&
+                    (prev.maxdeg <= (unsigned long long)kHeavyDeg || prev.heavy >= 0 || !prev.queued);
         if (push && h->q_cap - used < want_room) {
             TRY(grow_queues(h, used + want_room, st));
             push = h->q_cap - used >= want_room;
@@ -902,11 +930,16 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
             if (!prev.queued) {  // dense level -> queue
                 prev.qb.assign(qcount.begin(), qcount.begin() + ng);
                 compact_level_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(
-                    h->lvl[prev.slot], h->live + (size_t)(L - 1) * G, n, queue_params(h));
+                    h->lvl[prev.slot], h->live + (size_t)(L - 1) * G, n, queue_params(h), c.off, h->heavy,
+                    h->lstat + 3);
                 ++h->launches;
+                unsigned long long nheavy = 0;
                 CUDA_TRY(h, cudaMemcpyAsync(qcount.data(), h->q_count, G * sizeof(unsigned long long),
                                             cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaMemcpyAsync(&nheavy, h->lstat + 3, sizeof nheavy, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaMemsetAsync(h->lstat + 3, 0, sizeof(unsigned long long), st));
                 CUDA_TRY(h, cudaStreamSynchronize(st));
+                prev.heavy = (long long)nheavy;
                 prev.qe.assign(qcount.begin(), qcount.begin() + ng);
                 prev.queued = true;
                 device_level = -1;
@@ -916,7 +949,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 TRY(upload_lbeg());
             }
             const bool thin = prev.farcs <= kThinDegree * prev.nverts;
-            if (thin && h->deep && ng <= kDeepMaxGroups) {
+            if (thin && h->deep && ng <= kDeepMaxGroups && prev.maxdeg <= (unsigned long long)kHeavyDeg) {
                 // ---- a run of thin levels inside one cooperative launch
                 TRY(ensure_deep(h));
                 TRY(ensure_live(h, L + kDeepLevels + 1));
@@ -941,9 +974,9 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 dp.first_level = L;
                 dp.max_levels = kDeepLevels;
                 dp.graph_arcs = graph_arcs;
-                dp.push_beta = (unsigned long long)h->push_beta;
+                dp.push_beta = beta;
                 dp.thin_degree = kThinDegree;
-                dp.max_degree = kQueueMaxDegree;
+                dp.max_degree = kHeavyDeg;
                 void *args[] = {&dp};
                 CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_kernel, dim3(h->deep_grid_f),
                                                         dim3(kDeepThreads), args, 0, st));
@@ -977,6 +1010,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                     lr.nverts = rep[0];
                     lr.farcs = rep[1];
                     lr.maxdeg = rep[2];
+                    lr.heavy = rep[2] > (unsigned long long)kHeavyDeg ? -1 : 0;   // no records built in there
                 }
                 L += done - 1;
                 device_level = L;
@@ -991,10 +1025,17 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 fwd_push_kernel<<<dim3(queue_blocks(prev, kWarpsPerBlock), ng), kWarpsPerBlock * 32, 0, st>>>(
                     c.off, c.col, n, queue_params(h), h->vis, h->scrA, h->sigma,
                     h->counters + h->cnt_off);
+            if (prev.heavy > 0) {
+                fwd_push_heavy_kernel<<<blocks_for(prev.heavy), kWarpsPerBlock * 32, 0, st>>>(
+                    c.off, c.col, n, queue_params(h), h->heavy, (int64_t)prev.heavy, h->vis, h->scrA,
+                    h->sigma, h->counters + h->cnt_off);
+                ++h->launches;
+            }
             push_post_kernel<<<dim3(std::min<unsigned>(grid1d((size_t)std::min<unsigned long long>(
                                                            (unsigned long long)n, prev.farcs + 1)), 1184), ng),
                                256, 0, st>>>(c.off, n, queue_params(h), h->d_qlbeg, h->vis, h->scrA,
-                                             h->live + (size_t)L * G, h->counters + h->cnt_off, h->lstat);
+                                             h->live + (size_t)L * G, h->counters + h->cnt_off, h->lstat,
+                                             h->heavy);
             h->launches += 2;
             cur.queued = true;
             cur.qb.assign(qcount.begin(), qcount.begin() + ng);
@@ -1009,6 +1050,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
             cur.slot = next_slot++;
             TRY(ensure_pool(h, cur.slot + 1));
             TRY(launch_forward(h, c, L, ng, st, nbr, h->lvl[cur.slot], h->lstat));
+            pulled = true;
             if (prev.slot < 0) TRY(scatter_level(h, prev, h->scrB, true, ng, st));
             device_level = -1;
         }
@@ -1030,6 +1072,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         cur.nverts = report[0];
         cur.farcs = report[1];
         cur.maxdeg = report[2];
+        cur.heavy = (long long)report[3 + 2 * G];
         for (size_t g = 0; g < G; ++g) qcount[g] = report[3 + g];
         if (cur.queued) cur.qe.assign(qcount.begin(), qcount.begin() + ng);
     }
@@ -1391,7 +1434,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             active.push_back(sources_in[i]);
             where.push_back(i);
         }
-    if (!debug) {
+    if (!debug && h->reorder) {
         // Lanes of a group advance together, so a group works best when its
         // sources see the graph alike: order them by the size of their 2-hop
         // neighbourhood (sum of neighbour degrees).  BC is a sum over sources, so
@@ -1827,6 +1870,10 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         h->sparse = value ? 1 : 0;
         return BC_OK;
     }
+    if (k == "reorder") {
+        h->reorder = value ? 1 : 0;
+        return BC_OK;
+    }
     if (k == "deep") {
         h->deep = value ? 1 : 0;
         return BC_OK;
@@ -1837,6 +1884,11 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         arena_free(h->deep_log), arena_free(h->deep_info);
         h->deep_log = nullptr;
         h->deep_info = nullptr;
+        return BC_OK;
+    }
+    if (k == "push_beta_late") {
+        if (value < 1) return h->fail(BC_ERR_INPUT, "push_beta_late must be >= 1");
+        h->push_beta_late = (int)value;
         return BC_OK;
     }
     if (k == "push_beta") {

@@ -126,7 +126,10 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 }
 
 constexpr int kSparseSlice = BC_SPARSE_SLICE;
-constexpr int kRowUnroll = (BC_GATHER == 2 && BC_SPARSE_SLICE <= 2) ? 2 : 4;  // row loads in flight  // slices with at most this many hit arcs take the arc-serial path
+#ifndef BC_ROW_UNROLL
+#define BC_ROW_UNROLL ((BC_GATHER == 2 && BC_SPARSE_SLICE <= 2) ? 2 : 4)
+#endif
+constexpr int kRowUnroll = BC_ROW_UNROLL;  // row loads in flight  // slices with at most this many hit arcs take the arc-serial path
 
 // Scan arcs [a0, a1) of one vertex.  `want` (warp-uniform) = lanes that still
 // need a value.  Filter: lanes = arcs, hit = mask[neighbour] & want.  Gather,
@@ -537,6 +540,26 @@ struct QueueParams {
 
 constexpr int kStage = 128;  // per-warp shared-memory staging buffer (queue entries)
 
+// A queue entry is walked by one warp (or one thread on thin levels).  Entries of
+// vertices with more than kHeavyDeg arcs are left to fwd_push_heavy_kernel, which
+// takes one warp per kHeavySlice-arc slice of the adjacency: R-MAT hubs hold tens
+// of thousands of arcs and sit in the first levels of almost every source.
+constexpr int kHeavyDeg = 2048;
+constexpr int kHeavySlice = 256;   // arcs per record: short dependent chains, thousands of warps
+struct HeavyRec {
+    int64_t qi;     // queue entry (index inside the group's queue)
+    int32_t g;      // group
+    int32_t slice;  // arcs [slice * kHeavySlice, (slice + 1) * kHeavySlice) of the vertex
+};
+
+// Appends the slices of a heavy queue entry (called by one thread).
+__device__ __forceinline__ void append_heavy(HeavyRec *heavy, unsigned long long *heavy_count,
+                                             int64_t qi, int g, int64_t deg) {
+    const int slices = (int)((deg + kHeavySlice - 1) / kHeavySlice);
+    const unsigned long long at = atomicAdd(heavy_count, (unsigned long long)slices);
+    for (int s = 0; s < slices; ++s) heavy[at + s] = HeavyRec{qi, g, s};
+}
+
 // Top-down expansion of level L-1 (a queue) into level L.  Lanes = arcs.
 // next[] must be all zero on entry; it holds the new level's masks on exit
 // (push_post_kernel moves them into the queue and clears next[] again).
@@ -566,6 +589,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_kernel(
         const int32_t u = q.q_v[g * q.cap + i];
         const uint32_t mask = q.q_m[g * q.cap + i];
         const int64_t b = off[u], e = off[u + 1];
+        if (e - b > kHeavyDeg) continue;  // fwd_push_heavy_kernel takes it slice by slice
         const double *urow = gsig + (size_t)u * 32;
         for (int64_t base = b; base < e; base += 32) {
             const int64_t k = base + lane;
@@ -636,6 +660,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_thin_kernel(
             mask = q.q_m[g * q.cap + i];
             a = off[u];
             e = off[u + 1];
+            if (e - a > kHeavyDeg) e = a;  // left to fwd_push_heavy_kernel
         }
         int rounds = (int)(e - a);
         rounds = __reduce_max_sync(kFull, rounds);
@@ -672,13 +697,75 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_thin_kernel(
     if (lane == 0 && t) atomicAdd(counters + 2, (unsigned long long)t);
 }
 
+// Top-down expansion of the heavy entries of level L-1: one warp per record
+// (a kHeavySlice-arc slice of one frontier vertex), same arithmetic as fwd_push_kernel.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_heavy_kernel(
+    const int64_t *__restrict__ off, const int32_t *__restrict__ col, int64_t n, QueueParams q,
+    const HeavyRec *__restrict__ heavy, int64_t n_heavy, const uint32_t *__restrict__ vis,
+    uint32_t *next, double *sigma, unsigned long long *counters) {
+    __shared__ int32_t stage[kWarpsPerBlock][kStage];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    if (r >= n_heavy) return;
+    const HeavyRec rec = heavy[r];
+    const size_t g = (size_t)rec.g;
+    const int32_t u = q.q_v[g * q.cap + rec.qi];
+    const uint32_t mask = q.q_m[g * q.cap + rec.qi];
+    const int64_t b = off[u] + (int64_t)rec.slice * kHeavySlice;
+    const int64_t e = min(off[u + 1], b + kHeavySlice);
+    const uint32_t *gvis = vis + g * n;
+    uint32_t *gnext = next + g * n;
+    double *gsig = sigma + g * n * 32;
+    const double *urow = gsig + (size_t)u * 32;
+    int staged = 0;  // warp-uniform
+    unsigned c_t = 0;
+    auto flush = [&]() {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(q.q_count + g, (unsigned long long)staged);
+        base = __shfl_sync(kFull, base, 0);
+        for (int i = lane; i < staged; i += 32) q.q_v[g * q.cap + base + i] = stage[warp][i];
+        staged = 0;
+        __syncwarp();
+    };
+    for (int64_t base = b; base < e; base += 32) {
+        const int64_t k = base + lane;
+        bool fresh_vertex = false;
+        int32_t w = 0;
+        if (k < e) {
+            w = __ldg(col + k);
+            uint32_t fresh = mask & ~gvis[w];
+            if (fresh) {
+                const uint32_t old = atomicOr(gnext + w, fresh);
+                fresh_vertex = old == 0;
+                double *wrow = gsig + (size_t)w * 32;
+                while (fresh) {
+                    const int bit = __ffs(fresh) - 1;
+                    fresh &= fresh - 1;
+                    atomicAdd(wrow + bit, urow[bit]);   // exact: integer-valued fp64
+                    ++c_t;
+                }
+            }
+        }
+        const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+        if (newm) {
+            if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
+            staged += __popc(newm);
+            __syncwarp();
+            if (staged > kStage - 32) flush();
+        }
+    }
+    if (staged) flush();
+    const unsigned t = __reduce_add_sync(kFull, c_t);
+    if (lane == 0 && t) atomicAdd(counters + 2, (unsigned long long)t);
+}
+
 // After a push: entries [q_lbeg[g], q_count[g]) are the new level.  Record
 // their masks, mark them seen, clear next[], gather the level's statistics.
 // lstat: [0] vertices in the level, [1] their arcs, [2] largest degree (all groups).
 __global__ void push_post_kernel(const int64_t *__restrict__ off, int64_t n, QueueParams q,
                                  const int64_t *q_lbeg, uint32_t *vis, uint32_t *next,
                                  uint32_t *live_cur, unsigned long long *counters,
-                                 unsigned long long *lstat) {
+                                 unsigned long long *lstat, HeavyRec *heavy) {
     const size_t g = blockIdx.y;
     const int64_t beg = q_lbeg[g], end = (int64_t)q.q_count[g];
     unsigned long long nr = 0, ar = 0, nv = 0, fa = 0, md = 0;
@@ -691,6 +778,7 @@ __global__ void push_post_kernel(const int64_t *__restrict__ off, int64_t n, Que
         vis[g * n + w] |= m;
         next[g * n + w] = 0u;
         const unsigned long long deg = (unsigned long long)(off[w + 1] - off[w]);
+        if (deg > (unsigned long long)kHeavyDeg) append_heavy(heavy, lstat + 3, i, (int)g, (int64_t)deg);
         any |= m;
         nr += __popc(m);
         ar += __popc(m) * deg;
@@ -725,8 +813,9 @@ __global__ void advance_level_kernel(unsigned long long *lstat, unsigned long lo
                                      int64_t *q_lbeg, int G, unsigned long long *report) {
     const int g = threadIdx.x;
     if (g < 3) report[g] = lstat[g];
+    if (g == 3) report[3 + 2 * G] = lstat[3];   // heavy records of the level just produced
     __syncthreads();
-    if (g < 3) lstat[g] = 0;
+    if (g < 4) lstat[g] = 0;
     if (g < G) {
         const unsigned long long c = q_count[g];
         report[3 + g] = c;
@@ -765,7 +854,8 @@ __global__ void scatter_queue_kernel(QueueParams q, int64_t n, uint32_t *dense, 
 
 // Dense level -> queue (needed when a push level follows a pull level).
 __global__ void compact_level_kernel(const uint32_t *__restrict__ lvl, const uint32_t *live_level,
-                                     int64_t n, QueueParams q) {
+                                     int64_t n, QueueParams q, const int64_t *__restrict__ off,
+                                     HeavyRec *heavy, unsigned long long *heavy_count) {
     const size_t g = blockIdx.y;
     if (live_level[g] == 0) return;
     const int lane = threadIdx.x & 31;
@@ -779,9 +869,12 @@ __global__ void compact_level_kernel(const uint32_t *__restrict__ lvl, const uin
         if (lane == 0) base = atomicAdd(q.q_count + g, (unsigned long long)__popc(has));
         base = __shfl_sync(kFull, base, 0);
         if (m) {
-            const size_t at = g * q.cap + base + __popc(has & ((1u << lane) - 1u));
+            const int64_t qi = (int64_t)base + __popc(has & ((1u << lane) - 1u));
+            const size_t at = g * q.cap + qi;
             q.q_v[at] = (int32_t)v;
             q.q_m[at] = m;
+            const int64_t deg = off[v + 1] - off[v];
+            if (deg > kHeavyDeg) append_heavy(heavy, heavy_count, qi, (int)g, deg);
         }
     }
 }

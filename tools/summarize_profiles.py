@@ -1,0 +1,74 @@
+"""Turn the ncu outputs of tools/gpu_round.sh (gpurun_out/) into the committed summaries:
+
+    profiles/<round>_launches.csv          raw launch list (gpu__time_duration per launch)
+    profiles/<round>_launches_summary.md   per-kernel totals and shares + first batch in launch order
+    profiles/<round>_level_kernel_ncu_full.csv   selected metrics of the --set full capture
+    profiles/<round>_traffic.json          DRAM bytes per launch of the forward level kernel
+"""
+import collections, csv, json, os, shutil, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
+out = os.path.join(ROOT, "profiles")
+src = os.path.join(ROOT, "gpurun_out")
+os.makedirs(out, exist_ok=True)
+
+rows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
+hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+shutil.copy(os.path.join(src, "launches.csv"), os.path.join(out, rnd + "_launches.csv"))
+agg = collections.OrderedDict()
+order = []
+for r in rows[hi + 1:]:
+    if len(r) < 15:
+        continue
+    name = r[4].split("(")[0].replace("void ", "").replace("bcb200::", "")
+    us = float(r[-1]) / 1e3
+    a = agg.setdefault(name, [0, 0.0])
+    a[0] += 1
+    a[1] += us
+    order.append((name, r[8], us))
+total = sum(a[1] for a in agg.values())
+cmd = "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 1 --warmup 0 --no-cpu"
+with open(os.path.join(out, rnd + "_launches_summary.md"), "w") as fh:
+    fh.write("# ncu launch list, %s (cold-cache, serialised: compare shares, not absolutes)\n\n" % rnd)
+    fh.write("Command: `%s`\n(the bench workload, one step: R-MAT scale-20 EF-16, 1024 sources in batches of 16 groups; "
+             "raw list: `%s_launches.csv`)\n\n" % (cmd, rnd))
+    fh.write("| kernel | launches | total us | share |\n|---|---:|---:|---:|\n")
+    for name, (cnt, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        fh.write("| `%s` | %d | %.1f | %.1f%% |\n" % (name, cnt, us, 100 * us / total))
+    fh.write("\nLaunch order of the first batch (us):\n\n```\n")
+    seen_reduce = False
+    for name, grid, us in order:
+        fh.write("%-40s %-16s %10.1f\n" % (name[:40], grid, us))
+        if name.startswith("level_kernel<1") or name.startswith("level_kernel<(bool)1"):
+            seen_reduce = True
+        if seen_reduce and name.startswith("init_state"):
+            break
+    fh.write("```\n")
+
+rep = os.path.join(src, "prof_level.ncu-rep")
+if os.path.exists(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    hdr = rr[0]
+    want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+            "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+            "launch__registers_per_thread", "launch__grid_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+    idx = [hdr.index(w) for w in want]
+    with open(os.path.join(out, rnd + "_level_kernel_ncu_full.csv"), "w") as fh:
+        for r in rr:
+            fh.write(",".join('"%s"' % r[i] if "," in r[i] else r[i] for i in idx) + "\n")
+    units = rr[1]
+    def to_bytes(val, unit):
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
+        return float(val) * mult
+    fwd = [r for r in rr[2:] if "level_kernel<(bool)0" in r[idx[0]] or "level_kernel<0" in r[idx[0]]]
+    per = [to_bytes(r[idx[2]], units[idx[2]]) + to_bytes(r[idx[3]], units[idx[3]]) for r in fwd]
+    rec = {"rmat20": sum(per) / len(per) if per else None,
+           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the %d forward level_kernel "
+                   "launches of one 16-group batch (ncu --set full, bench.py --steps 1 --warmup 0)" % len(per),
+           "per_launch_bytes": per}
+    json.dump(rec, open(os.path.join(out, rnd + "_traffic.json"), "w"), indent=1)
+print(open(os.path.join(out, rnd + "_launches_summary.md")).read()[:3000])
