@@ -17,8 +17,8 @@ Printed JSON (one line, rank 0):
   e2e       same metric through the public call ``run_bc(g, cfg)`` with host
             buffers: CSR + sources host->device, BC vector device->host, inside
             the timed region (wall clock bracketed by device synchronisation)
-  roofline  forward level kernel: algorithmic bytes / device time
-            against the measured HBM copy bandwidth
+  roofline  level kernels (forward + backward sweeps): algorithmic bytes
+             / device time against the measured HBM copy bandwidth
   cpu_baseline  the C/OpenMP oracle port of the reference's sequential Brandes
             on the box's host cores, bounded source sample
 ``--impl reference`` times that CPU port alone (the reference itself is
@@ -141,8 +141,9 @@ class ClockSampler:
 
 
 def ncu_traffic(workload_name: str):
-    """DRAM bytes the forward level kernel moved per launch, from the committed ncu
-    `--set full` capture (profiles/r1_traffic.json; null when no capture matches)."""
+    """DRAM bytes the level kernel moved per launch (mean over the forward and backward
+    launches of one batch), from the committed ncu `--set full` capture
+    (profiles/r1_traffic.json, written by tools/summarize_profiles.py; null when no capture matches)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
             rec = json.load(fh)
@@ -272,7 +273,8 @@ def run_ours(args):
     if rank == 0:
         sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    acc = {"ms_forward": 0.0, "ms_backward": 0.0, "launches": 0}
+    acc = {"ms_forward": 0.0, "ms_backward": 0.0, "launches": 0, "launches_forward": 0, "launches_backward": 0,
+           "launches_level": 0}
     ev0.record(stream)
     for _ in range(args.steps):
         st = step()
@@ -315,17 +317,31 @@ def run_ours(args):
     fwd_b, bwd_b, init_b = algorithmic_bytes(st, n)
     fwd_ms = acc["ms_forward"] / args.steps
     bwd_ms = acc["ms_backward"] / args.steps
-    roof_f = fwd_b / (fwd_ms / 1e3) / 1e9
-    roof_b = bwd_b / (bwd_ms / 1e3) / 1e9
+    lf = acc["launches_forward"] / args.steps
+    lb = acc["launches_backward"] / args.steps
+
+    def sweep(nbytes, ms, launches):
+        gbs = nbytes / (ms / 1e3) / 1e9
+        return {"achieved": gbs, "frac": gbs / peak, "algorithmic_bytes_per_step": nbytes, "ms_per_step": ms,
+                "launches_per_step": launches, "bytes_per_launch": nbytes / max(launches, 1),
+                "avg_launch_ms": ms / max(launches, 1)}
+
+    both = sweep(fwd_b + bwd_b, fwd_ms + bwd_ms, lf + lb)
     roofline = {
-        "bound": "hbm", "kernel": "level_kernel<forward> (+hub_kernel)",
-        "achieved": roof_f, "peak": peak, "unit": "GB/s", "frac": roof_f / peak,
+        "bound": "hbm", "kernel": "level_kernel<forward | backward> and the push / queue kernels of the same sweeps",
+        "achieved": both["achieved"], "peak": peak, "unit": "GB/s", "frac": both["frac"],
         "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
-        "algorithmic_bytes_per_step": fwd_b, "ms_per_step": fwd_ms,
-        "backward": {"achieved": roof_b, "frac": roof_b / peak, "algorithmic_bytes_per_step": bwd_b,
-                     "ms_per_step": bwd_ms},
+        "algorithmic_bytes_per_step": both["algorithmic_bytes_per_step"], "ms_per_step": both["ms_per_step"],
+        "launches_per_step": both["launches_per_step"], "bytes_per_launch": both["bytes_per_launch"],
+        "avg_launch_ms": both["avg_launch_ms"],
+        "level_kernel_launches_per_step": acc["launches_level"] / args.steps,
+        "algorithmic_bytes_per_level_kernel_launch": (fwd_b + bwd_b) / max(1.0, acc["launches_level"] / args.steps),
+        "forward": sweep(fwd_b, fwd_ms, lf), "backward": sweep(bwd_b, bwd_ms, lb),
         "whole_step": {"achieved": (fwd_b + bwd_b + init_b) / (ms_total / args.steps / 1e3) / 1e9,
                        "frac": (fwd_b + bwd_b + init_b) / (ms_total / args.steps / 1e3) / 1e9 / peak},
+        "note": "algorithmic bytes count every source separately (SURVEY.md 8d); 32 sources share one "
+                "adjacency read and most sigma rows are served by L2, so frac > 1 is expected and the "
+                "kernel is latency / L1-throughput bound (profiles/)",
     }
     cpu = None
     if world == 1 and not args.no_cpu:

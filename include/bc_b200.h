@@ -71,6 +71,9 @@ typedef struct bc_stats {
     int64_t comm_events;  /* forward cross-partition transfers                          */
     int64_t sync_events;  /* backward cross-partition sync points                       */
     int64_t comm_bytes;   /* backward payload, 16 B per (sigma, delta) pair (ledger.py:12) */
+    int64_t launches_forward;  /* kernels launched between the events that bound ms_forward  */
+    int64_t launches_backward; /* ... ms_backward                                           */
+    int64_t launches_level;    /* of those, launches of the dense level kernel (both directions) */
 } bc_stats;
 
 /* Replaces: construction of the device-side view of `Graph`

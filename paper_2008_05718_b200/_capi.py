@@ -41,6 +41,8 @@ class BcStats(ctypes.Structure):
         ("ms_backward", ctypes.c_double), ("ms_border", ctypes.c_double),
         ("iterations", ctypes.c_int64), ("comm_events", ctypes.c_int64),
         ("sync_events", ctypes.c_int64), ("comm_bytes", ctypes.c_int64),
+        ("launches_forward", ctypes.c_int64), ("launches_backward", ctypes.c_int64),
+        ("launches_level", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -180,7 +182,7 @@ class Engine:
     def run(self, sources, mode: int = MODE_DIRECT):
         """Host buffers in, host BC vector out: (bc float64[n], stats dict)."""
         src = np.ascontiguousarray(sources, dtype=np.int64)
-        bc = np.zeros(self.n, dtype=np.float64)
+        bc = np.empty(self.n, dtype=np.float64)     # bc_run overwrites all n entries
         st = BcStats()
         rc = self._lib.bc_run(self._h, int(mode), _ptr(src), len(src), _ptr(bc), ctypes.byref(st))
         if rc != BC_OK:

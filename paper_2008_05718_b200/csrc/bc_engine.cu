@@ -242,6 +242,7 @@ struct bc_handle {
     int64_t dist_entries_cap = 0;
     std::string err;
     int64_t launches = 0;
+    int64_t level_launches = 0;   // dense level kernel only
 
     int fail(int code, const std::string &msg) {
         err = msg;
@@ -668,6 +669,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     level_kernel<false, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     ++h->launches;
+    ++h->level_launches;
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
         q.cur = p.cur;
@@ -697,6 +699,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     else
         level_kernel<true, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     ++h->launches;
+    ++h->level_launches;
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
         q.cur = p.cur;
@@ -1482,6 +1485,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     }
     tr.mark("run: state allocation");
     const int64_t launches0 = h->launches;
+    const int64_t level_launches0 = h->level_launches;
     int64_t h2d = 0, d2h = 0;
     if (k > 0) {
         CUDA_TRY(h, cudaMemcpyAsync(h->d_src, sources, k * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -1494,6 +1498,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const int64_t n_batches = (k + lanes_per_batch - 1) / lanes_per_batch;
     std::vector<Events> ev((size_t)n_batches);
     int max_depth = 0;
+    int64_t launches_f = 0, launches_b = 0;
     int64_t tot_iters = 0, tot_comm = 0, tot_sync = 0, tot_bytes = 0;
     const Csr &fwd_csr = hybir ? h->intra : h->full;
     // queue levels / push: the unpartitioned sweeps only (the partitioned modes
@@ -1520,6 +1525,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         CUDA_TRY(h, cudaEventCreate(&e.fwd2_end));
         CUDA_TRY(h, cudaEventCreate(&e.bwd_end));
         CUDA_TRY(h, cudaEventRecord(e.start, st));
+        const int64_t l_start = h->launches;
 
         // ---- forward: Step 1 (or the whole BFS when there is no partition)
         TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, adaptive));
@@ -1530,6 +1536,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         else TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
         h->cnt_off = 0;
         CUDA_TRY(h, cudaEventRecord(e.fwd_end, st));
+        launches_f += h->launches - l_start;
 
         std::vector<int32_t> iters;
         std::vector<uint32_t> entered;
@@ -1552,9 +1559,11 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             TRY(refine_and_compose(h, cnt, ng, st, &iters, &entered, &max_seed));
             CUDA_TRY(h, cudaEventRecord(e.border_end, st));
             // ---- Step 6: every part relaxes from its borders at once
+            const int64_t l_step6 = h->launches;
             TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st));
             TRY(forward_sweep(h, h->intra, ng, st, &depth, true, cnt, max_seed));
             CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
+            launches_f += h->launches - l_step6;
         } else {
             CUDA_TRY(h, cudaEventRecord(e.border_end, st));
             CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
@@ -1563,9 +1572,11 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
 
         // ---- backward over the whole graph (cross-part children are final by
         // the time their parents' level runs: levels are global)
+        const int64_t l_bwd = h->launches;
         if (adaptive) TRY(backward_adaptive(h, h->full, depth, reps, ng, debug, st));
         else TRY(backward_sweep(h, h->full, depth, ng, debug, st));
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
+        launches_b += h->launches - l_bwd;
 
         if (want_reports && h->k == 2) {
             // ---- per-source reports (forward.py:52-64, backward.py:33-43, bsp.py:96-103,137-141)
@@ -1738,6 +1749,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         stats->comm_events = tot_comm;
         stats->sync_events = tot_sync;
         stats->comm_bytes = tot_bytes;
+        stats->launches_forward = launches_f;
+        stats->launches_backward = launches_b;
+        stats->launches_level = h->level_launches - level_launches0;
     }
     return BC_OK;
 }

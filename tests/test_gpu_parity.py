@@ -195,6 +195,26 @@ def test_persistent_sweeps_equal_level_by_level():
         assert np.allclose(out[1][3], O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
 
 
+def test_device_block_cache_reuse_and_release(rmat12):
+    # closed engines leave their device blocks in the per-device cache: the next engine takes
+    # them over (dirty), a release hands them back to the driver; results never change
+    from paper_2008_05718_b200 import _capi
+    srcs = list(range(0, 4096, 5))
+    small = G.grid(9, 5)
+    with Engine(rmat12) as e:
+        first, _ = e.run(srcs)
+    for _ in range(2):
+        with Engine(small) as e:
+            bc_small, _ = e.run(list(range(45)))
+        with Engine(rmat12) as e:
+            again, _ = e.run(srcs)
+        assert np.array_equal(first, again)
+        assert np.allclose(bc_small, O.brandes_bc(small, list(range(45)))[0], rtol=RTOL, atol=ATOL)
+        _capi.release_cached_memory()
+    with Engine(rmat12) as e:
+        assert np.array_equal(first, e.run(srcs)[0])
+
+
 def test_deterministic_and_linear(rmat12):
     g = rmat12
     a = list(range(0, 4096, 9))

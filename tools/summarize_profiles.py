@@ -64,11 +64,11 @@ if os.path.exists(rep):
     def to_bytes(val, unit):
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
         return float(val) * mult
-    fwd = [r for r in rr[2:] if "level_kernel<(bool)0" in r[idx[0]] or "level_kernel<0" in r[idx[0]]]
-    per = [to_bytes(r[idx[2]], units[idx[2]]) + to_bytes(r[idx[3]], units[idx[3]]) for r in fwd]
+    lev = [r for r in rr[2:] if "level_kernel<" in r[idx[0]] and "advance" not in r[idx[0]]]
+    per = [to_bytes(r[idx[2]], units[idx[2]]) + to_bytes(r[idx[3]], units[idx[3]]) for r in lev]
     rec = {"rmat20": sum(per) / len(per) if per else None,
-           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the %d forward level_kernel "
-                   "launches of one 16-group batch (ncu --set full, bench.py --steps 1 --warmup 0)" % len(per),
+           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the %d level_kernel launches "
+                   "(forward and backward) captured with ncu --set full from bench.py --steps 1 --warmup 0" % len(per),
            "per_launch_bytes": per}
     json.dump(rec, open(os.path.join(out, rnd + "_traffic.json"), "w"), indent=1)
 print(open(os.path.join(out, rnd + "_launches_summary.md")).read()[:3000])
