@@ -55,6 +55,14 @@ def lib():
         L.oracle_brandes_bc.argtypes = [
             ctypes.c_int64, _i64p, _i32p, _i64p, ctypes.c_int64, _f64p, ctypes.c_int,
             _i64p, ctypes.POINTER(ctypes.c_double)]
+        L.oracle_brandes_single_source_w.restype = ctypes.c_int
+        L.oracle_brandes_single_source_w.argtypes = [
+            ctypes.c_int64, _i64p, _i32p, _i64p, ctypes.c_int64, _i64p, _f64p, _f64p,
+            ctypes.POINTER(ctypes.c_double), _i64p]
+        L.oracle_brandes_bc_w.restype = ctypes.c_int
+        L.oracle_brandes_bc_w.argtypes = [
+            ctypes.c_int64, _i64p, _i32p, _i64p, _i64p, ctypes.c_int64, _f64p, ctypes.c_int,
+            _i64p, ctypes.POINTER(ctypes.c_double)]
         L.oracle_masked_relax.restype = ctypes.c_int
         L.oracle_masked_relax.argtypes = [
             ctypes.c_int64, _i64p, _i32p, ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p, _f64p,
@@ -78,8 +86,12 @@ def brandes_single_source(g, s: int):
     delta = np.empty(n, dtype=np.float64)
     smax = ctypes.c_double(0.0)
     stats = np.zeros(4, dtype=np.int64)
-    rc = lib().oracle_brandes_single_source(n, g.offsets, g.col_idx, int(s), dist, sigma, delta,
-                                            ctypes.byref(smax), stats)
+    if g.unit_weight:
+        rc = lib().oracle_brandes_single_source(n, g.offsets, g.col_idx, int(s), dist, sigma, delta,
+                                                ctypes.byref(smax), stats)
+    else:   # positive integer weights: the reference's heap Dijkstra
+        rc = lib().oracle_brandes_single_source_w(n, g.offsets, g.col_idx, g.arc_weight, int(s), dist,
+                                                  sigma, delta, ctypes.byref(smax), stats)
     if rc:
         raise ValueError("oracle_brandes_single_source failed with status %d" % rc)
     info = {"reached": int(stats[0]), "levels": int(stats[1]), "arcs_reached": int(stats[2]),
@@ -95,8 +107,12 @@ def brandes_bc(g, sources=None, threads: int | None = None):
     tot = np.zeros(4, dtype=np.int64)
     smax = ctypes.c_double(0.0)
     t = threads or host_threads()
-    rc = lib().oracle_brandes_bc(n, g.offsets, g.col_idx, src, len(src), bc, int(t), tot,
-                                 ctypes.byref(smax))
+    if g.unit_weight:
+        rc = lib().oracle_brandes_bc(n, g.offsets, g.col_idx, src, len(src), bc, int(t), tot,
+                                     ctypes.byref(smax))
+    else:
+        rc = lib().oracle_brandes_bc_w(n, g.offsets, g.col_idx, g.arc_weight, src, len(src), bc, int(t),
+                                       tot, ctypes.byref(smax))
     if rc:
         raise ValueError("oracle_brandes_bc failed with status %d" % rc)
     info = {"reached": int(tot[0]), "arcs_reached": int(tot[1]), "dag_arcs": int(tot[2]),

@@ -16,6 +16,9 @@
  *   oracle_brandes_bc             reference pkg/src/hybir/oracle.py:70-82
  *   oracle_masked_relax           reference pkg/src/hybir/relax.py:42-103
  *   oracle_build_levels           reference pkg/src/hybir/relax.py:106-113
+ *   oracle_brandes_single_source_w / oracle_brandes_bc_w
+ *                                 the same two functions on weighted graphs
+ *                                 (positive integer weights, heap Dijkstra)
  *
  * Unit weights turn the reference's heap Dijkstra into a breadth-first
  * search; the heap pops (dist, vertex) pairs, so vertices settle in ascending
@@ -240,6 +243,209 @@ int oracle_brandes_bc(int64_t n, const int64_t *offsets, const int32_t *col,
     free(partial);
     free(tot);
     free(smax);
+    return failed ? 1 : 0;
+}
+
+/* ------------------------------------------------------------------------
+ * Weighted graphs (positive integer arc weights): the reference's heap Dijkstra
+ * itself (oracle.py:44-61).  The heap holds (dist, vertex) pairs compared
+ * lexicographically and stale entries are skipped, so vertices settle in
+ * ascending (dist, id) order exactly as in the Python code; the backward pass
+ * walks that order in reverse (oracle.py:63-66).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int64_t d, v;
+} heap_item_t;
+
+static int heap_less(heap_item_t a, heap_item_t b) { return a.d < b.d || (a.d == b.d && a.v < b.v); }
+
+static void heap_push(heap_item_t *h, int64_t *size, heap_item_t x) {
+    int64_t i = (*size)++;
+    while (i > 0) {
+        int64_t p = (i - 1) / 2;
+        if (!heap_less(x, h[p])) break;
+        h[i] = h[p];
+        i = p;
+    }
+    h[i] = x;
+}
+
+static heap_item_t heap_pop(heap_item_t *h, int64_t *size) {
+    heap_item_t top = h[0], x = h[--(*size)];
+    int64_t i = 0, n = *size;
+    for (;;) {
+        int64_t c = 2 * i + 1;
+        if (c >= n) break;
+        if (c + 1 < n && heap_less(h[c + 1], h[c])) ++c;
+        if (!heap_less(h[c], x)) break;
+        h[i] = h[c];
+        i = c;
+    }
+    if (n > 0) h[i] = x;
+    return top;
+}
+
+/* heap: capacity n_arcs + 1 entries (every improving relaxation pushes once). */
+static int64_t single_source_w(int64_t n, const int64_t *offsets, const int32_t *col,
+                               const int64_t *wgt, int64_t s, int64_t *dist, double *sigma,
+                               double *delta, int64_t *order, heap_item_t *heap,
+                               int64_t *out_maxd, double *out_sigma_max, int64_t *out_arcs_reached,
+                               int64_t *out_dag_arcs) {
+    int64_t hs = 0, reached = 0, maxd = 0, arcs_reached = 0, dag = 0;
+    double smax = 1.0;
+    for (int64_t v = 0; v < n; ++v) {
+        dist[v] = ORACLE_UNREACHED;
+        sigma[v] = 0.0;
+        delta[v] = 0.0;
+    }
+    /* delta doubles as the "settled" flag holder until the backward pass: use order[] marks */
+    dist[s] = 0;
+    sigma[s] = 1.0;
+    heap_push(heap, &hs, (heap_item_t){0, s});
+    /* settled[v] is encoded as delta[v] = -1 during the forward pass */
+    while (hs > 0) {
+        heap_item_t it = heap_pop(heap, &hs);
+        int64_t v = it.v, d = it.d;
+        if (delta[v] < 0.0 || d != dist[v]) continue;
+        delta[v] = -1.0;
+        order[reached++] = v;
+        if (d > maxd) maxd = d;
+        arcs_reached += offsets[v + 1] - offsets[v];
+        for (int64_t k = offsets[v]; k < offsets[v + 1]; ++k) {
+            int64_t w = col[k];
+            int64_t nd = d + wgt[k];
+            if (dist[w] == ORACLE_UNREACHED || nd < dist[w]) {
+                dist[w] = nd;
+                sigma[w] = sigma[v];
+                heap_push(heap, &hs, (heap_item_t){nd, w});
+            } else if (nd == dist[w]) {
+                sigma[w] += sigma[v];
+            }
+        }
+    }
+    for (int64_t i = 0; i < reached; ++i) {
+        delta[order[i]] = 0.0;
+        if (sigma[order[i]] > smax) smax = sigma[order[i]];
+    }
+    for (int64_t i = reached - 1; i >= 0; --i) {
+        int64_t u = order[i];
+        int64_t du = dist[u];
+        double coeff = 1.0 + delta[u];
+        double su = sigma[u];
+        for (int64_t k = offsets[u]; k < offsets[u + 1]; ++k) {
+            int64_t v = col[k];
+            /* v is a predecessor of u iff the arc is tight (the graph is symmetric,
+             * so the arc u -> v carries the weight of v -> u) */
+            if (dist[v] >= 0 && dist[v] + wgt[k] == du) {
+                delta[v] += (sigma[v] / su) * coeff;
+                ++dag;
+            }
+        }
+    }
+    if (out_maxd) *out_maxd = maxd;
+    if (out_sigma_max) *out_sigma_max = smax;
+    if (out_arcs_reached) *out_arcs_reached = arcs_reached;
+    if (out_dag_arcs) *out_dag_arcs = dag;
+    return reached;
+}
+
+/* stats: [0] reached, [1] largest distance + 1, [2] A_r, [3] T. */
+int oracle_brandes_single_source_w(int64_t n, const int64_t *offsets, const int32_t *col,
+                                   const int64_t *wgt, int64_t s, int64_t *dist, double *sigma,
+                                   double *delta, double *sigma_max, int64_t *stats) {
+    if (n <= 0 || s < 0 || s >= n) return 2;
+    int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    heap_item_t *heap = (heap_item_t *)malloc(sizeof(heap_item_t) * (size_t)(offsets[n] + 2));
+    if (!order || !heap) {
+        free(order), free(heap);
+        return 1;
+    }
+    int64_t maxd = 0, ar = 0, dag = 0;
+    int64_t reached = single_source_w(n, offsets, col, wgt, s, dist, sigma, delta, order, heap, &maxd,
+                                      sigma_max, &ar, &dag);
+    if (stats) {
+        stats[0] = reached;
+        stats[1] = maxd + 1;
+        stats[2] = ar;
+        stats[3] = dag;
+    }
+    free(order), free(heap);
+    return 0;
+}
+
+int oracle_brandes_bc_w(int64_t n, const int64_t *offsets, const int32_t *col, const int64_t *wgt,
+                        const int64_t *sources, int64_t k, double *bc, int nthreads,
+                        int64_t *totals, double *sigma_max) {
+    if (n <= 0) return 2;
+    for (int64_t i = 0; i < k; ++i)
+        if (sources[i] < 0 || sources[i] >= n) return 2;
+    if (nthreads < 1) nthreads = 1;
+    double *partial = (double *)calloc((size_t)nthreads * (size_t)n, sizeof(double));
+    int64_t *tot = (int64_t *)calloc((size_t)nthreads * 4, sizeof(int64_t));
+    double *smax = (double *)calloc((size_t)nthreads, sizeof(double));
+    int failed = 0;
+    if (!partial || !tot || !smax) {
+        free(partial), free(tot), free(smax);
+        return 1;
+    }
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nthreads)
+#endif
+    {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        int64_t *dist = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+        int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+        double *sigma = (double *)malloc(sizeof(double) * (size_t)n);
+        double *delta = (double *)malloc(sizeof(double) * (size_t)n);
+        heap_item_t *heap = (heap_item_t *)malloc(sizeof(heap_item_t) * (size_t)(offsets[n] + 2));
+        int ok = dist && order && sigma && delta && heap;
+        if (!ok) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            failed = 1;
+        }
+        double *mine = partial + (size_t)t * (size_t)n;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int64_t i = 0; i < k; ++i) {
+            if (!ok) continue;
+            int64_t s = sources[i], maxd = 0, ar = 0, dag = 0;
+            double sm = 0.0;
+            int64_t reached = single_source_w(n, offsets, col, wgt, s, dist, sigma, delta, order, heap,
+                                              &maxd, &sm, &ar, &dag);
+            for (int64_t v = 0; v < n; ++v)
+                if (v != s) mine[v] += delta[v];
+            tot[t * 4 + 0] += reached;
+            tot[t * 4 + 1] += ar;
+            tot[t * 4 + 2] += dag;
+            if (maxd + 1 > tot[t * 4 + 3]) tot[t * 4 + 3] = maxd + 1;
+            if (sm > smax[t]) smax[t] = sm;
+        }
+        free(dist), free(order), free(sigma), free(delta), free(heap);
+    }
+    for (int64_t v = 0; v < n; ++v) bc[v] = 0.0;
+    for (int t = 0; t < nthreads; ++t)
+        for (int64_t v = 0; v < n; ++v) bc[v] += partial[(size_t)t * (size_t)n + v];
+    if (totals) {
+        totals[0] = totals[1] = totals[2] = totals[3] = 0;
+        for (int t = 0; t < nthreads; ++t) {
+            totals[0] += tot[t * 4 + 0];
+            totals[1] += tot[t * 4 + 1];
+            totals[2] += tot[t * 4 + 2];
+            if (tot[t * 4 + 3] > totals[3]) totals[3] = tot[t * 4 + 3];
+        }
+    }
+    if (sigma_max) {
+        *sigma_max = 0.0;
+        for (int t = 0; t < nthreads; ++t)
+            if (smax[t] > *sigma_max) *sigma_max = smax[t];
+    }
+    free(partial), free(tot), free(smax);
     return failed ? 1 : 0;
 }
 

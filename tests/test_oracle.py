@@ -129,3 +129,44 @@ def test_counters_are_consistent(rmat12):
     src, dst = rmat12.arc_src, rmat12.arc_dst
     tight = (d[src] >= 0) & (d[dst] == d[src] + 1)
     assert info["dag_arcs"] == int(tight.sum())
+
+
+# ---- weighted graphs: the reference's heap Dijkstra (oracle.py:44-61) ------------------
+
+def _weighted_golden():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors_weighted.json")
+    with open(path) as fh:
+        return json.load(fh)
+
+
+def weighted_graph_from_record(rec):
+    return from_edges(rec["n"], [tuple(e) for e in rec["edges"]])
+
+
+def test_weighted_tie_fixture_w5():
+    # reference pkg/tests/test_oracle.py:31-34
+    g = from_edges(5, [(0, 1, 2), (0, 2, 1), (1, 2, 1), (1, 3, 3), (2, 3, 4), (3, 4, 1)])
+    assert not g.unit_weight
+    d, s, _, _ = O.brandes_single_source(g, 0)
+    assert d.tolist() == [0, 2, 1, 5, 6]
+    assert s.tolist() == [1, 2, 1, 3, 3]
+
+
+def test_weighted_oracle_matches_reference_golden():
+    doc = _weighted_golden()
+    assert len(doc["graphs"]) >= 8
+    for rec in doc["graphs"]:
+        g = weighted_graph_from_record(rec)
+        assert g.inf_distance == rec["inf"]
+        bc, _ = O.brandes_bc(g)
+        assert np.allclose(bc, rec["bc_all_sources"], rtol=1e-12, atol=1e-12), rec["name"]
+        for sr in rec["sources"]:
+            d, s, dl, info = O.brandes_single_source(g, sr["s"])
+            assert d.tolist() == sr["dist"], rec["name"]
+            assert s.tolist() == sr["sigma"], rec["name"]
+            assert np.array_equal(dl, np.array(sr["delta"])), rec["name"]     # same settle order: bit-identical
+        bc_s, _ = O.brandes_bc(g, rec["run_bc_sources"], threads=1)
+        assert np.allclose(bc_s, rec["run_bc_hybir"], rtol=1e-9, atol=1e-12)
+        assert np.allclose(bc_s, rec["run_bc_bsp_baseline"], rtol=1e-9, atol=1e-12)

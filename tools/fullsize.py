@@ -27,7 +27,7 @@ def run_direct(name, g, nsrc, groups, check=16, seed=0):
         levels=st["max_levels"], launches=st["launches"], alg_GBps=(fwd + bwd) / st["ms_total"] / 1e6,
         bc_rel_vs_oracle=rel, oracle_sigma_max=info["sigma_max"], cpu_teps=g.num_edges * check / cpu, cpu_threads=info["threads"])
 
-which = sys.argv[1:] or ["rmat22", "er22", "road2048", "grid512_hybir"]
+which = sys.argv[1:] or ["c1", "rmat22", "er22", "road2048", "grid512_hybir"]
 if "rmat22" in which:
     t = time.time(); g = G.rmat(22, 16, 1); log(built="rmat22", s=time.time() - t)
     run_direct("R-MAT s22 ef16, 4096 sources (north-star target)", g, 4096, 8)
@@ -59,3 +59,18 @@ if "grid512_hybir" in which:
             wall_incl_tables_s=wall, iterations=st["iterations"], levels=st["max_levels"], direct_ms=std["ms_total"],
             hybir_vs_direct=float(np.max(np.abs(bc - bcd) / np.maximum(np.abs(bcd), 1e-9))),
             bc_rel_vs_oracle=float(np.max(np.abs(b16 - obc) / np.maximum(np.abs(obc), 1e-9))), sigma_max=info["sigma_max"])
+if "c1" in which:
+    # BASELINE config 1: R-MAT s12 ef8, ALL sources, 2 partitions (the reference's own partitioner)
+    g = G.rmat(12, 8, 1)
+    srcs = list(range(g.num_vertices))
+    t0 = time.time(); obc, info = O.brandes_bc(g, srcs); cpu = time.time() - t0
+    for mode in ("direct", "bsp-baseline", "hybir"):
+        P.run_bc(g, P.RunConfig(sources=srcs[:64], mode=mode, num_partitions=2, per_source_reports=False))
+        t0 = time.time()
+        res = P.run_bc(g, P.RunConfig(sources=srcs, mode=mode, num_partitions=2, per_source_reports=True))
+        wall = time.time() - t0
+        log(config="config 1: R-MAT s12 ef8, all 4096 sources, 2 parts, mode=%s" % mode, n=g.num_vertices, m=g.num_edges,
+            borders=list(res.borders.counts()), wall_s=wall, device_ms=res.stats["ms_total"], border_ms=res.stats["ms_border"],
+            mteps_e2e=res.mteps, bc_rel_vs_oracle=float(np.max(np.abs(res.bc - obc) / np.maximum(np.abs(obc), 1e-9))),
+            iterations=res.stats["iterations"], comm_events=res.stats["comm_events"], sync_events=res.stats["sync_events"],
+            cpu_port_s=cpu, cpu_threads=info["threads"])
