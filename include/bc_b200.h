@@ -82,6 +82,14 @@ typedef struct bc_stats {
 int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *col_idx,
               int device, bc_handle **out);
 
+/* Positive integer arc weights, int32[n_arcs] in CSR arc order (`Graph.arc_weight`,
+ * graph.py:21-61; both directions of an edge carry the same weight).  NULL or
+ * all-ones selects the unit-weight kernels.  With weights a level is a distance
+ * value: the forward sweep is the reference's Dijkstra order (relax.py:75-101,
+ * oracle.py:44-61) taken one distance at a time.  BC_MODE_DIRECT and BC_MODE_BSP
+ * only; weights above 4096 are refused. */
+int bc_set_weights(bc_handle *h, const int32_t *weights);
+
 /* Tuning knobs ("groups": 32-lane source groups per batch; "item_arcs": arcs
  * per warp work item; "reports": 1 = keep per-source report counters). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);

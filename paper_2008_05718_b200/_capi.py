@@ -23,7 +23,7 @@ MODE_DIRECT, MODE_HYBIR, MODE_BSP = 0, 1, 2
 
 # Every symbol include/bc_b200.h declares (checked by tests/test_capi_symbols.py).
 SYMBOLS = (
-    "bc_create", "bc_set_option", "bc_set_partition", "bc_run", "bc_run_device",
+    "bc_create", "bc_set_weights", "bc_set_option", "bc_set_partition", "bc_run", "bc_run_device",
     "bc_debug_sources", "bc_get_reports", "bc_get_border_counts", "bc_get_border_tables",
     "bc_get_border_frontier",
     "bc_dist_setup", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
@@ -68,6 +68,8 @@ def load():
     vp, i64, i32, cint = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
     L.bc_create.restype = cint
     L.bc_create.argtypes = [i64, i64, vp, vp, cint, ctypes.POINTER(vp)]
+    L.bc_set_weights.restype = cint
+    L.bc_set_weights.argtypes = [vp, vp]
     L.bc_set_option.restype = cint
     L.bc_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     L.bc_set_partition.restype = cint
@@ -139,6 +141,16 @@ class Engine:
             self._h = ctypes.c_void_p()
             self._raise(rc, handle=None)
         self.h2d_bytes_graph = off.nbytes + col.nbytes
+        if not g.unit_weight:
+            w = np.ascontiguousarray(g.arc_weight, dtype=np.int64)
+            if len(w) and (w.max() > 4096 or w.min() < 1):
+                self.close()
+                raise InputError("arc weights must be integers in [1, 4096] on the GPU path")
+            w32 = w.astype(np.int32)
+            rc = self._lib.bc_set_weights(self._h, _ptr(w32))
+            if rc != BC_OK:
+                self._raise(rc)
+            self.h2d_bytes_graph += w32.nbytes
 
     # -- plumbing ---------------------------------------------------------
     def _raise(self, rc, handle="self"):

@@ -159,6 +159,9 @@ struct bc_handle {
     std::vector<int64_t> h_off;   // host copy of the offsets (item building, partition set-up)
     std::vector<int32_t> h_col;   // host copy of col_idx, fetched from the device when a partition is set
     Csr full;
+    int32_t *wgt = nullptr;   // arc weights of the full CSR (nullptr: unit weights)
+    int wmax = 1;             // largest arc weight
+    int cur_depth = 0;        // levels of the batch being swept backward (weighted kernels)
     // options
     int groups = 4;
     int item_arcs = 512;
@@ -596,6 +599,11 @@ LevelParams level_params(bc_handle *h, const Csr &c) {
     p.pacc = h->pacc;
     p.pmask = h->pmask;
     p.counters = h->counters + h->cnt_off;
+    p.wgt = h->wgt;
+    p.lvl_ptrs = h->d_lvl_ptrs;
+    p.live_base = h->live;
+    p.wmax = h->wmax;
+    p.G = h->alloc_groups;
     return p;
 }
 
@@ -616,6 +624,9 @@ HubParams hub_params(bc_handle *h, const Csr &c) {
     p.pacc = h->pacc;
     p.pmask = h->pmask;
     p.counters = h->counters + h->cnt_off;
+    p.live_base = h->live;
+    p.wmax = h->wgt ? h->wmax : 1;
+    p.G = h->alloc_groups;
     return p;
 }
 
@@ -666,12 +677,17 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     p.lstat = lstat;
     p.live_prev = h->live + (size_t)(L - 1) * h->alloc_groups;
     p.live_cur = h->live + (size_t)L * h->alloc_groups;
+    p.level = L;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
-    level_kernel<false, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
+    if (h->wgt != nullptr)
+        level_kernel<false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
+    else
+        level_kernel<false, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     ++h->launches;
     ++h->level_launches;
     if (c.n_hub > 0) {
         HubParams q = hub_params(h, c);
+        q.level = L;
         q.cur = p.cur;
         q.lstat = lstat;
         q.live_prev = p.live_prev;
@@ -693,8 +709,14 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     p.cur = cur ? cur : h->lvl[L];
     p.live_prev = h->live + (size_t)L * h->alloc_groups;
     p.accumulate_bc = accumulate ? 1 : 0;
+    p.level = L;
+    p.max_level = h->cur_depth - 1;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
-    if (store_delta)
+    if (h->wgt != nullptr && store_delta)
+        level_kernel<true, true, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
+    else if (h->wgt != nullptr)
+        level_kernel<true, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
+    else if (store_delta)
         level_kernel<true, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     else
         level_kernel<true, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -745,8 +767,10 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
     std::vector<uint32_t> flags;
     const size_t G = (size_t)h->alloc_groups;
     const size_t lvl_bytes = G * (size_t)h->n * sizeof(uint32_t);
+    const int wmax = h->wgt ? h->wmax : 1;
     for (;;) {
         TRY(ensure_levels(h, L + chunk));
+        if (h->wgt) TRY(upload_level_ptrs(h, L + chunk, st));   // weighted levels probe lvl[L - wt]
         for (int j = 0; j < chunk; ++j) {
             if (seeded) CUDA_TRY(h, cudaMemsetAsync(h->lvl[L + j], 0, lvl_bytes, st));
             TRY(launch_forward(h, c, L + j, ng, st));
@@ -767,7 +791,9 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
             bool alive = false;
             for (int g = 0; g < ng; ++g) alive |= flags[(size_t)j * G + g] != 0;
             if (alive) last_alive = L + j;
-            else if (L + j > max_seed_level) {
+            else if (L + j > max_seed_level && L + j - last_alive >= wmax) {
+                // unit weights: the first empty level ends the sweep; weighted: a frontier can
+                // jump over up to wmax - 1 empty distance values
                 stop = true;
                 break;
             }
@@ -785,6 +811,8 @@ int backward_sweep(bc_handle *h, const Csr &c, int depth, int ng, bool debug, cu
     // Level 0 holds only the sources; their delta is excluded from BC
     // (engine.py:147-148), so it is computed only for inspection.
     const int last = debug ? 0 : 1;
+    h->cur_depth = depth;
+    if (h->wgt) TRY(upload_level_ptrs(h, depth, st));
     for (int L = depth - 1; L >= last; --L)
         TRY(launch_backward(h, c, L, L == depth - 1, ng, debug, !debug, st));
     return BC_OK;
@@ -1421,6 +1449,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         }
     if (mode != BC_MODE_DIRECT && h->k == 1) mode = BC_MODE_DIRECT;  // one part: no borders
     const bool hybir = mode == BC_MODE_HYBIR;
+    if (hybir && h->wgt != nullptr)
+        return h->fail(BC_ERR_INPUT, "weighted graphs run in direct or bsp-baseline mode (the border-table "
+                                     "path is unit-weight)");
     const bool want_reports = h->reports && mode != BC_MODE_DIRECT;
     if (hybir) TRY(build_border_tables(h));
 
@@ -1503,7 +1534,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const Csr &fwd_csr = hybir ? h->intra : h->full;
     // queue levels / push: the unpartitioned sweeps only (the partitioned modes
     // read dense level rows for borders and reports)
-    const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2);
+    const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2) && h->wgt == nullptr;
 
     // debug staging: one batch (<= 32 sources) of [lane][n] rows
     int32_t *dbg_dist = nullptr;
@@ -1849,6 +1880,27 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
     int rc = body();
     if (rc) return bail(rc);
     *out = h;
+    return BC_OK;
+}
+
+int bc_set_weights(bc_handle *h, const int32_t *weights) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    arena_free(h->wgt);
+    h->wgt = nullptr;
+    h->wmax = 1;
+    if (weights == nullptr) return BC_OK;   // back to unit weights
+    int64_t wmax = 1;
+    for (int64_t a = 0; a < h->n_arcs; ++a) {
+        if (weights[a] <= 0) return h->fail(BC_ERR_INPUT, "arc weights must be positive integers");
+        wmax = std::max<int64_t>(wmax, weights[a]);
+    }
+    if (wmax > 4096) return h->fail(BC_ERR_INPUT, "arc weights above 4096 are not supported (one level per distance value)");
+    bool unit = wmax == 1;
+    if (unit) return BC_OK;
+    CUDA_TRY(h, arena_malloc((void **)&h->wgt, std::max<int64_t>(h->n_arcs, 1) * sizeof(int32_t)));
+    CUDA_TRY(h, cudaMemcpy(h->wgt, weights, h->n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice));
+    h->wmax = (int)wmax;
     return BC_OK;
 }
 
@@ -2288,6 +2340,7 @@ void bc_destroy(bc_handle *h) {
     free_state(h);
     free_partition(h);
     free_csr(h->full);
+    arena_free(h->wgt);
     arena_free(h->counters);
     arena_free(h->dflags);
     arena_free(h->d_maxlvl);

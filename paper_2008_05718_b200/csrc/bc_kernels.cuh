@@ -86,7 +86,22 @@ struct LevelParams {
     unsigned long long *counters;  // [0] n_r, [1] A_r, [2] T
     unsigned long long *lstat;     // forward: [0] vertices discovered, [1] their arcs, [2] largest degree (may be null)
     int accumulate_bc;
+    // weighted graphs (positive integer arc weights, WEIGHTED kernels only): level = distance,
+    // an arc of weight wt ties level L to level L - wt (forward) / L + wt (backward)
+    const int32_t *wgt;                  // per arc, CSR order
+    const uint32_t *const *lvl_ptrs;     // lvl_ptrs[L] = mask array of level L
+    const uint32_t *live_base;           // live[level][G]
+    int level, max_level, wmax, G;
 };
+
+// Lanes a forward level still has to serve: those with a non-empty frontier in one of the
+// last `wmax` levels (wmax = 1 for unit weights: the previous level).
+__device__ __forceinline__ uint32_t forward_live(const uint32_t *live_base, int G, size_t g, int level,
+                                                 int wmax) {
+    uint32_t live = 0;
+    for (int j = 1; j <= wmax && j <= level; ++j) live |= live_base[(size_t)(level - j) * G + g];
+    return live;
+}
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -144,17 +159,36 @@ constexpr int kRowUnroll = BC_ROW_UNROLL;  // row loads in flight  // slices wit
 // deterministic.  Four gathers are issued before the four dependent adds; the
 // next 32-arc slice is loaded before the current one is consumed.
 // tcount is a per-lane partial count of (arc, instance) hits (COUNT_T only).
-template <bool COUNT_T>
+struct WeightedProbe {
+    const int32_t *wgt;
+    const uint32_t *const *lvl_ptrs;
+    size_t goff;     // group offset into a level array
+    int level, max_level;
+};
+
+// Mask of the lanes for which arc k ties its endpoint w to the level being computed.
+template <bool WEIGHTED, bool BWD>
+__device__ __forceinline__ uint32_t probe_arc(int64_t k, int32_t w, const uint32_t *__restrict__ nmask,
+                                              const WeightedProbe &wp) {
+    if (!WEIGHTED) return __ldg(nmask + w);
+    const int wt = __ldg(wp.wgt + k);
+    const int ls = BWD ? wp.level + wt : wp.level - wt;
+    if (BWD ? ls > wp.max_level : ls < 0) return 0u;
+    return __ldg(wp.lvl_ptrs[ls] + wp.goff + w);
+}
+
+template <bool COUNT_T, bool WEIGHTED = false, bool BWD = false>
 __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
                                           const int32_t *__restrict__ col,
                                           const uint32_t *__restrict__ nmask,
                                           const double *__restrict__ val, int lane, double &acc,
-                                          uint32_t &got, unsigned &tcount) {
+                                          uint32_t &got, unsigned &tcount,
+                                          const WeightedProbe &wp = WeightedProbe{}) {
     int32_t w_n = 0;
     uint32_t hit_n = 0;
     if (a0 + lane < a1) {
         w_n = __ldg(col + a0 + lane);
-        hit_n = __ldg(nmask + w_n) & want;
+        hit_n = probe_arc<WEIGHTED, BWD>(a0 + lane, w_n, nmask, wp) & want;
     }
     const double *myval = val + lane;
     for (int64_t base = a0; base < a1; base += 32) {
@@ -165,7 +199,7 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
         hit_n = 0;
         if (k2 < a1) {
             w_n = __ldg(col + k2);
-            hit_n = __ldg(nmask + w_n) & want;
+            hit_n = probe_arc<WEIGHTED, BWD>(k2, w_n, nmask, wp) & want;
         }
         unsigned any = __ballot_sync(kFull, hit != 0);
         PROF_ADD(0, 1);
@@ -293,16 +327,26 @@ __device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, doub
 
 // One BFS level, forward (discover level L from level L-1) or backward
 // (accumulate level L from level L+1).  grid = (ceil(items / 8), groups).
-template <bool BWD, bool STORE_DELTA>
+template <bool BWD, bool STORE_DELTA, bool WEIGHTED = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD : BC_MIN_BLOCKS_FWD) level_kernel(const LevelParams p) {
     const size_t g = blockIdx.y;
     // forward: instances still expanding; backward: instances present at this level
-    const uint32_t live = p.live_prev[g];
+    const uint32_t live = (WEIGHTED && !BWD) ? forward_live(p.live_base, p.G, g, p.level, p.wmax)
+                                             : p.live_prev[g];
+    WeightedProbe wp{};
+    if (WEIGHTED) {
+        wp.wgt = p.wgt;
+        wp.lvl_ptrs = p.lvl_ptrs;
+        wp.goff = g * (size_t)p.n;
+        wp.level = p.level;
+        wp.max_level = p.max_level;
+    }
     if (live == 0) return;  // also covers speculative launches past the last level
     const int lane = threadIdx.x & 31;
     const int64_t item = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (item >= (int64_t)p.n_chk + p.n_rng) return;
     uint32_t *vis = p.vis + g * p.n;
+    // weighted: the masks come from lvl_ptrs; `nbr` only says whether there is anything to pull
     const uint32_t *nbr = p.nbr ? p.nbr + g * p.n : nullptr;
     uint32_t *cur = p.cur + g * p.n;
     double *sigma = p.sigma + g * p.n * 32;
@@ -322,8 +366,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         double acc = 0.0;
         uint32_t got = 0;
         if (want != 0 && nbr != nullptr)
-            scan_arcs<!BWD>(p.chk_a0[item], p.chk_a1[item], want, p.col, nbr, val, lane, acc, got,
-                            c_t);
+            scan_arcs<!BWD, WEIGHTED, BWD>(p.chk_a0[item], p.chk_a1[item], want, p.col, nbr, val, lane,
+                                           acc, got, c_t, wp);
         const size_t slot = g * (size_t)p.n_chk + item;
         if (want != 0) p.pacc[slot * 32 + lane] = acc;
         if (lane == 0) p.pmask[slot] = got;
@@ -351,7 +395,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
             const int64_t ve = __shfl_sync(kFull, e, i);
             double acc = 0.0;
             uint32_t got = 0;
-            if (nbr != nullptr) scan_arcs<!BWD>(vb, ve, want, p.col, nbr, val, lane, acc, got, c_t);
+            if (nbr != nullptr)
+                scan_arcs<!BWD, WEIGHTED, BWD>(vb, ve, want, p.col, nbr, val, lane, acc, got, c_t, wp);
             if (BWD) {
                 finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma, coef, delta,
                                                p.bcg + g * p.n, p.accumulate_bc);
@@ -406,13 +451,16 @@ struct HubParams {
     unsigned long long *counters;
     unsigned long long *lstat;
     int accumulate_bc;
+    const uint32_t *live_base;   // weighted forward levels: see forward_live()
+    int level, wmax, G;
 };
 
 // Adds a hub's chunk partials in chunk order (= arc order) and finalises it.
 template <bool BWD, bool STORE_DELTA>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) hub_kernel(const HubParams p) {
     const size_t g = blockIdx.y;
-    const uint32_t live = p.live_prev[g];
+    const uint32_t live = (!BWD && p.wmax > 1) ? forward_live(p.live_base, p.G, g, p.level, p.wmax)
+                                               : p.live_prev[g];
     if (live == 0) return;
     const int lane = threadIdx.x & 31;
     const int h = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
