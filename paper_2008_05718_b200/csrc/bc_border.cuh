@@ -35,6 +35,7 @@ struct BorderGeom {
     const int64_t *tab_off;    // [k] offset of the part's b_p x b_p table
     const int64_t *cin_off;    // [B+1] incoming cut arcs per border
     const int32_t *cin_src;    // [n_cut] source border of each incoming cut arc
+    const int32_t *cin_w;      // [n_cut] its weight (1 on unit-weight graphs)
 };
 
 // Which (border, lane) pairs a relaxation step applies to (the reference's
@@ -128,7 +129,7 @@ __global__ void cut_relax_kernel(BorderGeom geo, int S, const int32_t *Din, int3
     if (lane_active[lane] && applies(which, geo.border_p[j], lane_part[lane])) {
         for (int64_t a = geo.cin_off[j]; a < geo.cin_off[j + 1]; ++a) {
             const int32_t di = Din[(size_t)geo.cin_src[a] * S + lane];
-            best = min(best, min(di + 1, kInf));
+            best = min(best, min(di + geo.cin_w[a], kInf));
         }
     }
     if (Dout != Din || best != old) Dout[idx] = best;
@@ -206,7 +207,7 @@ __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const do
     if (dj < kInf)
         for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c) {
             const size_t at = (size_t)geo.cin_src[c] * S + lane;
-            if (D[at] + 1 == dj) a += sig[at];
+            if (D[at] + geo.cin_w[c] == dj) a += sig[at];
         }
     arr[idx] = a;
 }
@@ -377,38 +378,47 @@ __global__ void level_presence_kernel(const uint32_t *lvl, const uint32_t *live_
         if (sp[i]) atomicOr(&presence_level[(size_t)i * G + g], sp[i]);
 }
 
-// Backward sync accounting for two parts (backward.py:46-56,121-139): border j
-// is pulled across the cut iff some incoming cut arc is tight.  flag[j][lane]
-// marks those; level_bits[(side * W + L / 32) * S + lane] collects the distinct
-// producer levels per consumer side.
+// Backward sync accounting for two parts (backward.py:46-56,121-139).  A tight
+// cut arc u -> j makes u's side pull border j; the reference counts one sync
+// event per distinct (consumer side, consumer level d[u], producer level d[j])
+// and 16 bytes per border child in each such set.  With unit weights d[j] is
+// d[u] + 1; with weights a border can serve parents at several levels.
+// flag[j][lane] = distinct consumer levels that pull j (its share of the
+// payload); level_bits[((side * W + d[u] / 32) * wmax + (w - 1)) * S + lane]
+// collects the distinct (consumer level, arc weight) pairs per consumer side.
 __global__ void sync_mark_kernel(BorderGeom geo, int S, const int32_t *Dfin, uint32_t *flag,
-                                 uint32_t *level_bits, int W) {
+                                 uint32_t *level_bits, int W, int wmax) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)geo.B * S) return;
     const int j = (int)(idx / S), lane = (int)(idx % S);
     const int32_t dj = Dfin[idx];
     uint32_t f = 0;
-    if (dj < kInf)
-        for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c)
-            if (Dfin[(size_t)geo.cin_src[c] * S + lane] + 1 == dj) {
-                f = 1;
-                break;
-            }
-    flag[idx] = f;
-    if (f) {
+    if (dj < kInf) {
         const int consumer = 1 - geo.border_p[j];  // two parts: the other side pulls
-        atomicOr(&level_bits[((size_t)consumer * W + (dj >> 5)) * S + lane], 1u << (dj & 31));
+        for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c) {
+            const int w = geo.cin_w[c];
+            const int32_t du = Dfin[(size_t)geo.cin_src[c] * S + lane];
+            if (du + w != dj) continue;
+            bool seen = false;   // an earlier tight arc from the same consumer level
+            for (int64_t c2 = geo.cin_off[j]; c2 < c && !seen; ++c2)
+                seen = geo.cin_w[c2] == w && Dfin[(size_t)geo.cin_src[c2] * S + lane] == du;
+            if (seen) continue;
+            ++f;
+            atomicOr(&level_bits[(((size_t)consumer * W + (du >> 5)) * wmax + (w - 1)) * S + lane],
+                     1u << (du & 31));
+        }
     }
+    flag[idx] = f;
 }
 
-__global__ void sync_count_kernel(int B, int S, int W, const uint32_t *flag,
+__global__ void sync_count_kernel(int B, int S, int W, int wmax, const uint32_t *flag,
                                   const uint32_t *level_bits, int64_t *sync_events,
                                   int64_t *comm_bytes) {
     const int lane = blockIdx.x * blockDim.x + threadIdx.x;
     if (lane >= S) return;
     int64_t children = 0, events = 0;
     for (int j = 0; j < B; ++j) children += flag[(size_t)j * S + lane];
-    for (int w = 0; w < 2 * W; ++w) events += __popc(level_bits[(size_t)w * S + lane]);
+    for (int w = 0; w < 2 * W * wmax; ++w) events += __popc(level_bits[(size_t)w * S + lane]);
     sync_events[lane] = events;
     comm_bytes[lane] = 16 * children;
 }

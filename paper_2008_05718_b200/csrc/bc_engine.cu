@@ -132,6 +132,7 @@ struct Csr {
     int64_t n = 0, n_arcs = 0;
     int64_t *off = nullptr;
     int32_t *col = nullptr;
+    int32_t *wgt = nullptr;   // arc weights (nullptr: unit weights)
     int n_chk = 0, n_rng = 0, n_hub = 0;
     int64_t heavy_slices = 0;   // kHeavySlice-arc slices over all vertices above kHeavyDeg arcs
     int32_t *chk_v = nullptr;
@@ -159,8 +160,8 @@ struct bc_handle {
     std::vector<int64_t> h_off;   // host copy of the offsets (item building, partition set-up)
     std::vector<int32_t> h_col;   // host copy of col_idx, fetched from the device when a partition is set
     Csr full;
-    int32_t *wgt = nullptr;   // arc weights of the full CSR (nullptr: unit weights)
-    int wmax = 1;             // largest arc weight
+    std::vector<int32_t> h_wgt;   // host copy of the arc weights (empty: unit weights)
+    int wmax = 1;                 // largest arc weight
     int cur_depth = 0;        // levels of the batch being swept backward (weighted kernels)
     // options
     int groups = 4;
@@ -186,6 +187,7 @@ struct bc_handle {
     std::vector<int64_t> h_tab_off;
     int64_t tab_total = 0;
     int32_t *d_border_v = nullptr, *d_border_p = nullptr, *d_part_off = nullptr, *d_cin_src = nullptr;
+    int32_t *d_cin_w = nullptr;   // weight of each incoming cut arc
     int64_t *d_tab_off = nullptr, *d_cin_off = nullptr;
     int32_t *bm = nullptr;         // border distance tables
     double *sm = nullptr;          // border path-count tables
@@ -302,6 +304,7 @@ void free_items(Csr &c) {
 void free_csr(Csr &c) {
     arena_free(c.off);
     arena_free(c.col);
+    arena_free(c.wgt);
     free_items(c);
     c = Csr();
 }
@@ -417,7 +420,8 @@ void free_partition(bc_handle *h) {
     free_csr(h->intra);
     free_border_state(h);
     arena_free(h->d_part), arena_free(h->d_border_v), arena_free(h->d_border_p), arena_free(h->d_part_off);
-    arena_free(h->d_cin_src), arena_free(h->d_tab_off), arena_free(h->d_cin_off);
+    arena_free(h->d_cin_src), arena_free(h->d_tab_off), arena_free(h->d_cin_off), arena_free(h->d_cin_w);
+    h->d_cin_w = nullptr;
     arena_free(h->bm), arena_free(h->sm);
     h->d_part = h->d_border_v = h->d_border_p = h->d_part_off = h->d_cin_src = nullptr;
     h->d_tab_off = h->d_cin_off = nullptr;
@@ -599,10 +603,10 @@ LevelParams level_params(bc_handle *h, const Csr &c) {
     p.pacc = h->pacc;
     p.pmask = h->pmask;
     p.counters = h->counters + h->cnt_off;
-    p.wgt = h->wgt;
+    p.wgt = c.wgt;
     p.lvl_ptrs = h->d_lvl_ptrs;
     p.live_base = h->live;
-    p.wmax = h->wmax;
+    p.wmax = c.wgt ? h->wmax : 1;
     p.G = h->alloc_groups;
     return p;
 }
@@ -625,7 +629,7 @@ HubParams hub_params(bc_handle *h, const Csr &c) {
     p.pmask = h->pmask;
     p.counters = h->counters + h->cnt_off;
     p.live_base = h->live;
-    p.wmax = h->wgt ? h->wmax : 1;
+    p.wmax = c.wgt ? h->wmax : 1;
     p.G = h->alloc_groups;
     return p;
 }
@@ -640,6 +644,7 @@ BorderGeom border_geom(bc_handle *h) {
     g.tab_off = h->d_tab_off;
     g.cin_off = h->d_cin_off;
     g.cin_src = h->d_cin_src;
+    g.cin_w = h->d_cin_w;
     return g;
 }
 
@@ -679,7 +684,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     p.live_cur = h->live + (size_t)L * h->alloc_groups;
     p.level = L;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
-    if (h->wgt != nullptr)
+    if (c.wgt != nullptr)
         level_kernel<false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     else
         level_kernel<false, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -712,9 +717,9 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     p.level = L;
     p.max_level = h->cur_depth - 1;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
-    if (h->wgt != nullptr && store_delta)
+    if (c.wgt != nullptr && store_delta)
         level_kernel<true, true, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
-    else if (h->wgt != nullptr)
+    else if (c.wgt != nullptr)
         level_kernel<true, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     else if (store_delta)
         level_kernel<true, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -767,10 +772,10 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
     std::vector<uint32_t> flags;
     const size_t G = (size_t)h->alloc_groups;
     const size_t lvl_bytes = G * (size_t)h->n * sizeof(uint32_t);
-    const int wmax = h->wgt ? h->wmax : 1;
+    const int wmax = c.wgt ? h->wmax : 1;
     for (;;) {
         TRY(ensure_levels(h, L + chunk));
-        if (h->wgt) TRY(upload_level_ptrs(h, L + chunk, st));   // weighted levels probe lvl[L - wt]
+        if (c.wgt) TRY(upload_level_ptrs(h, L + chunk, st));   // weighted levels probe lvl[L - wt]
         for (int j = 0; j < chunk; ++j) {
             if (seeded) CUDA_TRY(h, cudaMemsetAsync(h->lvl[L + j], 0, lvl_bytes, st));
             TRY(launch_forward(h, c, L + j, ng, st));
@@ -812,7 +817,7 @@ int backward_sweep(bc_handle *h, const Csr &c, int depth, int ng, bool debug, cu
     // (engine.py:147-148), so it is computed only for inspection.
     const int last = debug ? 0 : 1;
     h->cur_depth = depth;
-    if (h->wgt) TRY(upload_level_ptrs(h, depth, st));
+    if (c.wgt) TRY(upload_level_ptrs(h, depth, st));
     for (int L = depth - 1; L >= last; --L)
         TRY(launch_backward(h, c, L, L == depth - 1, ng, debug, !debug, st));
     return BC_OK;
@@ -1449,9 +1454,6 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         }
     if (mode != BC_MODE_DIRECT && h->k == 1) mode = BC_MODE_DIRECT;  // one part: no borders
     const bool hybir = mode == BC_MODE_HYBIR;
-    if (hybir && h->wgt != nullptr)
-        return h->fail(BC_ERR_INPUT, "weighted graphs run in direct or bsp-baseline mode (the border-table "
-                                     "path is unit-weight)");
     const bool want_reports = h->reports && mode != BC_MODE_DIRECT;
     if (hybir) TRY(build_border_tables(h));
 
@@ -1534,7 +1536,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const Csr &fwd_csr = hybir ? h->intra : h->full;
     // queue levels / push: the unpartitioned sweeps only (the partitioned modes
     // read dense level rows for borders and reports)
-    const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2) && h->wgt == nullptr;
+    const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2) && h->full.wgt == nullptr;
 
     // debug staging: one batch (<= 32 sources) of [lane][n] rows
     int32_t *dbg_dist = nullptr;
@@ -1634,7 +1636,11 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             if (hybir && h->B > 0) {
                 const size_t bcnt = (size_t)h->B * h->border_S;
                 const int W = (depth + 31) / 32 + 1;
-                const size_t words = (size_t)2 * W * h->border_S;
+                const int wm = h->full.wgt ? h->wmax : 1;
+                const size_t words = (size_t)2 * W * wm * h->border_S;
+                if (words > ((size_t)1 << 28))
+                    return h->fail(BC_ERR_INPUT, "per-source sync reports need too much memory for these weights "
+                                                 "and depths; run with reports = 0");
                 if (h->sync_bits_words < words) {
                     TRY(dev_alloc(h, &h->sync_bits, words));
                     h->sync_bits_words = words;
@@ -1645,9 +1651,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
                     h->d_lvl_ptrs, h->live, h->alloc_groups, depth, h->sigma, n, border_geom(h),
                     h->border_S, h->Dfin, nullptr);
                 sync_mark_kernel<<<grid1d(bcnt), 256, 0, st>>>(border_geom(h), h->border_S, h->Dfin,
-                                                               h->sync_flag, h->sync_bits, W);
+                                                               h->sync_flag, h->sync_bits, W, wm);
                 sync_count_kernel<<<grid1d((size_t)h->border_S, 128), 128, 0, st>>>(
-                    h->B, h->border_S, W, h->sync_flag, h->sync_bits, h->lane_sync, h->lane_bytes);
+                    h->B, h->border_S, W, wm, h->sync_flag, h->sync_bits, h->lane_sync, h->lane_bytes);
                 h->launches += 3;
                 CUDA_TRY(h, cudaMemcpyAsync(lsync.data(), h->lane_sync, h->border_S * sizeof(int64_t),
                                             cudaMemcpyDeviceToHost, st));
@@ -1886,8 +1892,11 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
 int bc_set_weights(bc_handle *h, const int32_t *weights) {
     if (h == nullptr) return BC_ERR_INPUT;
     CUDA_TRY(h, cudaSetDevice(h->device));
-    arena_free(h->wgt);
-    h->wgt = nullptr;
+    if (h->k > 1)
+        return h->fail(BC_ERR_INPUT, "bc_set_weights: set the weights before bc_set_partition");
+    arena_free(h->full.wgt);
+    h->full.wgt = nullptr;
+    h->h_wgt.clear();
     h->wmax = 1;
     if (weights == nullptr) return BC_OK;   // back to unit weights
     int64_t wmax = 1;
@@ -1895,11 +1904,12 @@ int bc_set_weights(bc_handle *h, const int32_t *weights) {
         if (weights[a] <= 0) return h->fail(BC_ERR_INPUT, "arc weights must be positive integers");
         wmax = std::max<int64_t>(wmax, weights[a]);
     }
-    if (wmax > 4096) return h->fail(BC_ERR_INPUT, "arc weights above 4096 are not supported (one level per distance value)");
-    bool unit = wmax == 1;
-    if (unit) return BC_OK;
-    CUDA_TRY(h, arena_malloc((void **)&h->wgt, std::max<int64_t>(h->n_arcs, 1) * sizeof(int32_t)));
-    CUDA_TRY(h, cudaMemcpy(h->wgt, weights, h->n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (wmax > 4096)
+        return h->fail(BC_ERR_INPUT, "arc weights above 4096 are not supported (one level per distance value)");
+    if (wmax == 1) return BC_OK;
+    CUDA_TRY(h, arena_malloc((void **)&h->full.wgt, std::max<int64_t>(h->n_arcs, 1) * sizeof(int32_t)));
+    CUDA_TRY(h, cudaMemcpy(h->full.wgt, weights, h->n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice));
+    h->h_wgt.assign(weights, weights + h->n_arcs);
     h->wmax = (int)wmax;
     return BC_OK;
 }
@@ -1988,14 +1998,18 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     const int32_t *col = h->h_col.data();
     // cut-free CSR + border lists (ascending vertex id inside each part)
     std::vector<int64_t> ioff((size_t)n + 1, 0);
-    std::vector<int32_t> icol;
+    std::vector<int32_t> icol, iwgt;
     icol.reserve((size_t)h->n_arcs);
+    const bool weighted = !h->h_wgt.empty();
+    if (weighted) iwgt.reserve((size_t)h->n_arcs);
     std::vector<std::vector<int32_t>> borders((size_t)k);
     for (int64_t v = 0; v < n; ++v) {
         bool is_border = false;
         for (int64_t a = off[v]; a < off[v + 1]; ++a) {
-            if (assignment[col[a]] == assignment[v]) icol.push_back(col[a]);
-            else is_border = true;
+            if (assignment[col[a]] == assignment[v]) {
+                icol.push_back(col[a]);
+                if (weighted) iwgt.push_back(h->h_wgt[(size_t)a]);
+            } else is_border = true;
         }
         ioff[(size_t)v + 1] = (int64_t)icol.size();
         if (is_border) borders[(size_t)assignment[v]].push_back((int32_t)v);
@@ -2022,11 +2036,14 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     for (int j = 0; j < h->B; ++j) index_of[(size_t)h->h_border_v[(size_t)j]] = j;
     // incoming cut arcs of every border, in arc order (the graph is symmetric)
     std::vector<int64_t> cin_off((size_t)h->B + 1, 0);
-    std::vector<int32_t> cin_src;
+    std::vector<int32_t> cin_src, cin_w;
     for (int j = 0; j < h->B; ++j) {
         const int64_t v = h->h_border_v[(size_t)j];
         for (int64_t a = off[v]; a < off[v + 1]; ++a)
-            if (assignment[col[a]] != assignment[v]) cin_src.push_back(index_of[(size_t)col[a]]);
+            if (assignment[col[a]] != assignment[v]) {
+                cin_src.push_back(index_of[(size_t)col[a]]);
+                cin_w.push_back(weighted ? h->h_wgt[(size_t)a] : 1);   // symmetric graph: w(u->v) = w(v->u)
+            }
         cin_off[(size_t)j + 1] = (int64_t)cin_src.size();
     }
     h->n_cut = (int64_t)cin_src.size();
@@ -2036,6 +2053,10 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     TRY(upload(h, &c.off, ioff));
     if (icol.empty()) icol.push_back(0);
     TRY(upload(h, &c.col, icol));
+    if (weighted) {
+        if (iwgt.empty()) iwgt.push_back(1);
+        TRY(upload(h, &c.wgt, iwgt));
+    }
     TRY(build_items(h, c, ioff.data(), h->item_arcs));
     TRY(upload(h, &h->d_part, h->h_part));
     TRY(upload(h, &h->d_border_v, h->h_border_v));
@@ -2043,8 +2064,9 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     TRY(upload(h, &h->d_part_off, h->h_part_off));
     TRY(upload(h, &h->d_tab_off, h->h_tab_off));
     TRY(upload(h, &h->d_cin_off, cin_off));
-    if (cin_src.empty()) cin_src.push_back(0);
+    if (cin_src.empty()) cin_src.push_back(0), cin_w.push_back(1);
     TRY(upload(h, &h->d_cin_src, cin_src));
+    TRY(upload(h, &h->d_cin_w, cin_w));
     return BC_OK;
 }
 
@@ -2340,7 +2362,6 @@ void bc_destroy(bc_handle *h) {
     free_state(h);
     free_partition(h);
     free_csr(h->full);
-    arena_free(h->wgt);
     arena_free(h->counters);
     arena_free(h->dflags);
     arena_free(h->d_maxlvl);

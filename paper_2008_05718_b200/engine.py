@@ -191,14 +191,10 @@ def run_bc(g: Graph, cfg: RunConfig | None = None, _pipeline: bool = False) -> R
     cfg = cfg or RunConfig()
     if g.num_vertices == 0:
         raise InputError("empty graph")
-    if not g.unit_weight:
-        # Weighted graphs (positive integer weights) run level = distance sweeps; the
-        # border-table forward phase and the graph-partitioned exchange are unit-weight.
-        if cfg.mode == "hybir" and cfg.num_partitions > 1 and (cfg.partition is None or cfg.partition.num_parts > 1):
-            raise InputError("weighted graph: use mode='bsp-baseline' or mode='direct' "
-                             "(the border-matrix path handles unit edge weights only)")
-        if cfg.num_gpus > 1 and cfg.gpu_mode == "graph-partitioned":
-            raise InputError("weighted graph: use gpu_mode='source-sharded'")
+    if not g.unit_weight and cfg.num_gpus > 1 and cfg.gpu_mode == "graph-partitioned":
+        # weighted graphs (positive integer weights) run level = distance sweeps in every
+        # single-GPU mode; the multi-GPU border exchange is unit-weight
+        raise InputError("weighted graph: use gpu_mode='source-sharded'")
     if cfg.num_gpus > 1:
         from .multigpu import run_bc_multi
         return run_bc_multi(g, cfg)

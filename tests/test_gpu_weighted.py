@@ -92,8 +92,38 @@ def test_run_bc_on_weighted_graphs(weighted_golden):
     assert got == [p["forward"]["supersteps"] for p in rec["per_source_bsp_baseline"]]
     res = P.run_bc(g, P.RunConfig(sources=rec["run_bc_sources"], mode="direct"))
     assert np.allclose(res.bc, rec["run_bc_bsp_baseline"], rtol=RTOL, atol=ATOL)
-    with pytest.raises(P.InputError):      # the border-matrix path is unit-weight
-        P.run_bc(g, P.RunConfig(sources=[0], mode="hybir", partition=part))
+    res = P.run_bc(g, P.RunConfig(sources=rec["run_bc_sources"], mode="hybir", partition=part))
+    assert np.allclose(res.bc, rec["run_bc_hybir"], rtol=RTOL, atol=ATOL)
+    assert res.per_source == rec["per_source_hybir"]
+
+
+def test_weighted_hybir_mode_matches_reference(weighted_golden):
+    # the paper's border-matrix forward phase on weighted graphs (forward.py:188-256 with weighted
+    # cut arcs and border tables): BC and every per-source report counter equal the reference's
+    from paper_2008_05718_b200._capi import MODE_HYBIR
+    for rec in weighted_golden["graphs"]:
+        g = graph_of(rec)
+        srcs = rec["run_bc_sources"]
+        with Engine(g) as e:
+            e.set_partition(2, rec["assignment"])
+            assert e.border_counts(2).tolist() == [len(b) for b in rec["borders"]], rec["name"]
+            bc, st = e.run(srcs, MODE_HYBIR)
+            reports = e.reports(len(srcs))
+            dist, sigma, delta = e.debug_sources(srcs[:32], MODE_HYBIR)
+        assert np.allclose(bc, rec["run_bc_hybir"], rtol=RTOL, atol=ATOL), rec["name"]
+        by_source = {sr["s"]: sr for sr in rec["sources"]}
+        for i, s in enumerate(srcs[:32]):
+            assert dist[i].tolist() == by_source[s]["dist"], (rec["name"], s)
+            assert sigma[i].tolist() == by_source[s]["sigma"], (rec["name"], s)
+            assert np.allclose(delta[i], by_source[s]["delta"], rtol=RTOL, atol=ATOL), (rec["name"], s)
+        for r, want in zip(reports, rec["per_source_hybir"]):
+            it, ce, ml0, ml1, se, cb, l0, l1 = (int(x) for x in r)
+            assert it == want["forward"]["iterations"], rec["name"]
+            assert ce == want["forward"]["comm_events"], rec["name"]
+            assert [ml0, ml1] == want["forward"]["max_level"], rec["name"]
+            assert se == want["backward"]["sync_events"], rec["name"]
+            assert cb == want["backward"]["comm_bytes"], rec["name"]
+            assert [l0, l1] == want["backward"]["levels"], rec["name"]
 
 
 @pytest.mark.parametrize("case", ["rc", "rmat_hubs", "grid", "two_components"])

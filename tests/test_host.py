@@ -135,8 +135,9 @@ def test_run_config_validation():
         P.RunConfig(gpu_mode="ring")
     with pytest.raises(P.InputError):
         P.run_bc(P.from_edges(0, []), P.RunConfig())
-    with pytest.raises(P.InputError):      # weighted graphs: bsp-baseline / direct only (default mode is hybir)
-        P.run_bc(P.from_edges(3, [(0, 1, 2), (1, 2, 1)]), P.RunConfig())
+    with pytest.raises(P.InputError):      # the multi-GPU border exchange is unit-weight
+        P.run_bc(P.from_edges(3, [(0, 1, 2), (1, 2, 1)]),
+                 P.RunConfig(num_gpus=2, gpu_mode="graph-partitioned"))
 
 
 def test_make_partition_modes():
