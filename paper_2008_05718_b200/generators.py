@@ -89,27 +89,32 @@ def path(n: int) -> Graph:
     return from_edge_arrays(n, a, a + 1)
 
 
-def random_connected(n: int, extra_edges: int = 0, seed: int = 0) -> Graph:
-    """Random spanning tree + extra edges, unit weights, always connected.
+def random_connected(n: int, extra_edges: int = 0, seed: int = 0, weighted: bool = False) -> Graph:
+    """Random spanning tree + extra edges, always connected; unit weights, or
+    integer weights 1..10 with ``weighted=True``.
 
     Same construction and the same ``random.Random(seed)`` draw order as the
-    reference test factory for its unweighted case (conftest.py:10-29), so a
-    given (n, extra_edges, seed) is the same graph on both sides.
+    reference test factory (conftest.py:10-29), so a given
+    (n, extra_edges, weighted, seed) is the same graph on both sides.
     """
     import random
 
     rng = random.Random(seed)
     nodes = list(range(n))
     rng.shuffle(nodes)
-    us, vs = [], []
+    us, vs, ws = [], [], []
     for i in range(1, n):
         us.append(nodes[rng.randrange(i)])
         vs.append(nodes[i])
+        if weighted:
+            ws.append(rng.randint(1, 10))
     added = 0
     while added < extra_edges:
         a, b = rng.randrange(n), rng.randrange(n)
         if a == b:
             continue
         us.append(a), vs.append(b)
+        if weighted:
+            ws.append(rng.randint(1, 10))
         added += 1
-    return from_edge_arrays(n, us, vs)
+    return from_edge_arrays(n, us, vs, ws if weighted else None)

@@ -173,3 +173,27 @@ def test_all_ones_weights_take_the_unit_path():
     with Engine(gw) as e:
         b, _ = e.run(srcs)
     assert np.array_equal(a, b)
+
+
+def test_reference_acceptance_corpus_on_the_gpu():
+    """The reference's own acceptance gate (pkg/tests/test_acceptance.py: 200 seeded graphs, every
+    second one weighted, 5 sources each) through the GPU engine in both partitioned modes: BC
+    within 1e-9 of the reference's and every per-source report counter equal."""
+    from paper_2008_05718_b200._capi import MODE_HYBIR
+    with open(os.path.join(HERE, "golden", "acceptance_corpus.json")) as fh:
+        doc = json.load(fh)
+    assert len(doc["records"]) == 200
+    for rec in doc["records"]:
+        g = G.random_connected(rec["n"], rec["extra"], seed=1000 + rec["i"], weighted=rec["weighted"])
+        assignment = np.array([int(c) for c in rec["assignment"]], dtype=np.int32)
+        with Engine(g) as e:
+            e.set_option("groups", 1)
+            e.set_partition(2, assignment)
+            bc_h, _ = e.run(rec["sources"], MODE_HYBIR)
+            rep_h = e.reports(len(rec["sources"])).tolist()
+            bc_b, _ = e.run(rec["sources"], MODE_BSP)
+            rep_b = e.reports(len(rec["sources"])).tolist()
+        assert np.allclose(bc_h, rec["bc"], rtol=RTOL, atol=ATOL), rec["i"]
+        assert np.allclose(bc_b, rec["bc"], rtol=RTOL, atol=ATOL), rec["i"]
+        assert rep_h == rec["hybir"], rec["i"]
+        assert rep_b == rec["bsp"], rec["i"]

@@ -178,3 +178,23 @@ def test_local_rows_for_graph_partitioned_mode():
                 g.col_idx[g.offsets[v]:g.offsets[v + 1]].tolist()
         total += len(lg.col_idx)
     assert total == g.num_arcs
+
+
+def test_reference_acceptance_corpus_host_side():
+    """The reference's acceptance corpus (test_acceptance.py:69-153; digest produced by
+    tests/golden/gen_acceptance_corpus.py): the generator builds the same 200 graphs, the restated
+    greedy_bipartition returns the reference's assignment on every one of them, and the CPU oracle
+    reproduces the reference's BC (half of the graphs are weighted)."""
+    import json
+    import os
+    import oracle as O
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "acceptance_corpus.json")) as fh:
+        doc = json.load(fh)
+    assert len(doc["records"]) == 200
+    for rec in doc["records"]:
+        g = G.random_connected(rec["n"], rec["extra"], seed=1000 + rec["i"], weighted=rec["weighted"])
+        assert g.num_edges == rec["m"] and g.unit_weight == (not rec["weighted"])
+        p = P.greedy_bipartition(g, rec["ratio"], seed=rec["i"], restarts=4)
+        assert "".join(str(int(x)) for x in p.assignment) == rec["assignment"], rec["i"]
+        bc, _ = O.brandes_bc(g, rec["sources"], threads=1)
+        assert np.allclose(bc, rec["bc"], rtol=1e-9, atol=1e-12), rec["i"]
