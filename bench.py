@@ -232,7 +232,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # launched by torchrun (even with one rank): join the NCCL job, so the N = 1 line of a scaling
+    # run goes through the same collectives as N > 1
+    use_dist = world > 1 or ("RANK" in os.environ and "MASTER_ADDR" in os.environ)
+    if use_dist:
         from paper_2008_05718_b200.multigpu import init_process_group
         init_process_group("nccl")
     if not torch.cuda.is_available():
@@ -257,12 +260,12 @@ def run_ours(args):
     def step():
         bc_dev.zero_()
         st = eng.run_device(mine, bc_dev.data_ptr(), stream.cuda_stream, MODE_DIRECT)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(bc_dev, op=dist.ReduceOp.SUM)
         return st
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -284,7 +287,7 @@ def run_ours(args):
     barrier()
     clocks = sampler.stop() if rank == 0 else {}
     ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_total = float(ms.item())
     value = m * len(all_sources) * args.steps / (ms_total / 1e3)
@@ -299,18 +302,24 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         res = P.run_bc(g, cfg)
-        if world > 1:
+        if use_dist:
             t = torch.from_numpy(res.bc).to(dev)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             res.bc[:] = t.cpu().numpy()
     barrier()
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = m * len(all_sources) * e2e_steps / float(e2e_s.item())
     h2d = g.offsets.nbytes + g.col_idx.nbytes + 8 * len(mine)
     d2h = 8 * n + 64
+    if use_dist:   # the host BC vector goes back to the device for the all-reduce and returns
+        h2d += 8 * n
+        d2h += 8 * n
 
+    if use_dist:
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
         return 0
     peak, peak_src = measured_peak_gbs()

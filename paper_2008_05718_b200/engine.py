@@ -149,9 +149,9 @@ def default_groups(g: Graph, n_sources: int) -> int:
     """Source groups per batch: enough lanes to fill the GPU on small graphs,
     few enough that one group's sigma slab stays L2-friendly on large ones."""
     want = max(1, (n_sources + 31) // 32)
-    budget = max(1, int(12e9 // max(1, g.num_vertices * 600)))   # ~12 GB of batch state
+    budget = max(1, int(24e9 // max(1, g.num_vertices * 600)))   # ~24 GB of batch state (180 GB HBM)
     if g.num_arcs >= 8_000_000:
-        return max(1, min(want, budget, 16))
+        return max(1, min(want, budget, 32))
     return max(1, min(want, budget, 128))
 
 
