@@ -74,3 +74,8 @@ if "c1" in which:
             mteps_e2e=res.mteps, bc_rel_vs_oracle=float(np.max(np.abs(res.bc - obc) / np.maximum(np.abs(obc), 1e-9))),
             iterations=res.stats["iterations"], comm_events=res.stats["comm_events"], sync_events=res.stats["sync_events"],
             cpu_port_s=cpu, cpu_threads=info["threads"])
+if "rmat24" in which:
+    # BASELINE config 5 graph on ONE GPU (the configuration itself is an 8-GPU run)
+    t = time.time(); g = G.rmat(24, 16, 1); log(built="rmat24", s=time.time() - t, n=g.num_vertices, m=g.num_edges)
+    run_direct("R-MAT s24 ef16, 256 of the 4096 sources, one GPU", g, 256, 4, check=4)
+    del g
