@@ -171,6 +171,35 @@ int bc_dist_set_live(bc_handle *h, int level, const uint32_t *live, void *stream
 /* bc_dev[v] += BC partials of the vertices this rank owns (others untouched). */
 int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream);
 
+/* ---- the paper's border-matrix forward phase across ranks (forward.py:188-256 with one part per
+ * GPU).  Every rank keeps ALL parts' border tables and runs the border refinement and the
+ * path-count composition redundantly, so the forward phase of a batch costs ONE exchange (the
+ * Step-1 seeds) instead of one per level; the backward phase uses bc_dist_backward_level /
+ * export / import as above.  Call order per batch: step1 -> (all-reduce the two seed arrays:
+ * MIN on distances, MAX on path counts) -> forward -> (all-reduce MAX of the depth) -> set_depth. */
+/* Global cut arcs: for border j (rank-major order of bc_dist_setup) the borders
+ * cin_src[cin_off[j] .. cin_off[j+1]) on the other side of its cut arcs; cin_w NULL = unit
+ * weights.  Builds the cut-free CSR of this rank's part and the border table of its own part. */
+int bc_dist_hybir_setup(bc_handle *h, const int64_t *cin_off, const int32_t *cin_src,
+                        const int32_t *cin_w);
+/* Border table of `part` (b_p x b_p distances and path counts, border_matrix.py:48-67) out of /
+ * into device buffers: each rank publishes its own part's table once. */
+int bc_dist_hybir_get_table(bc_handle *h, int part, int32_t *bm_dev, double *sm_dev);
+int bc_dist_hybir_set_table(bc_handle *h, int part, const int32_t *bm_dev, const double *sm_dev);
+/* Entries of the seed arrays: total borders x 32 x groups. */
+int64_t bc_dist_hybir_seed_count(bc_handle *h);
+/* Step 1 of a batch (BFS inside this rank's part from the sources it owns); writes the border
+ * seeds [border][lane] (distance, 0x3fffffff = unreached; path count) into device buffers. */
+int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, int64_t count, int32_t *seed_dist_dev,
+                        double *seed_sigma_dev, void *stream);
+/* Steps 2-5 + path-count composition on the reduced seeds (identical on every rank), then Step 6
+ * on this rank's part.  depth_out = levels seen by this rank; iterations_out = refinement
+ * iterations summed over the batch's sources. */
+int bc_dist_hybir_forward(bc_handle *h, const int32_t *seed_dist_dev, const double *seed_sigma_dev,
+                          int *depth_out, int64_t *iterations_out, void *stream);
+/* Extend this rank's level rows (empty) to the depth of the deepest rank. */
+int bc_dist_hybir_set_depth(bc_handle *h, int global_depth, void *stream);
+
 const char *bc_last_error(bc_handle *h);
 /* Releases the handle.  Its device blocks go to a per-device cache that the next
  * bc_create / bc_run reuses (run_bc() opens one handle per call, as the

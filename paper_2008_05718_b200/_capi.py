@@ -28,6 +28,8 @@ SYMBOLS = (
     "bc_get_border_frontier",
     "bc_dist_setup", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
     "bc_dist_export", "bc_dist_import", "bc_dist_get_live", "bc_dist_set_live", "bc_dist_finish",
+    "bc_dist_hybir_setup", "bc_dist_hybir_get_table", "bc_dist_hybir_set_table",
+    "bc_dist_hybir_seed_count", "bc_dist_hybir_seeds", "bc_dist_hybir_forward", "bc_dist_hybir_set_depth",
     "bc_last_error", "bc_destroy", "bc_release_cached_memory",
 )
 
@@ -106,6 +108,20 @@ def load():
     L.bc_dist_set_live.argtypes = [vp, cint, vp, vp]
     L.bc_dist_finish.restype = cint
     L.bc_dist_finish.argtypes = [vp, vp, vp]
+    L.bc_dist_hybir_setup.restype = cint
+    L.bc_dist_hybir_setup.argtypes = [vp, vp, vp, vp]
+    L.bc_dist_hybir_get_table.restype = cint
+    L.bc_dist_hybir_get_table.argtypes = [vp, cint, vp, vp]
+    L.bc_dist_hybir_set_table.restype = cint
+    L.bc_dist_hybir_set_table.argtypes = [vp, cint, vp, vp]
+    L.bc_dist_hybir_seed_count.restype = i64
+    L.bc_dist_hybir_seed_count.argtypes = [vp]
+    L.bc_dist_hybir_seeds.restype = cint
+    L.bc_dist_hybir_seeds.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.bc_dist_hybir_forward.restype = cint
+    L.bc_dist_hybir_forward.argtypes = [vp, vp, vp, ctypes.POINTER(cint), ctypes.POINTER(i64), vp]
+    L.bc_dist_hybir_set_depth.restype = cint
+    L.bc_dist_hybir_set_depth.argtypes = [vp, cint, vp]
     L.bc_last_error.restype = ctypes.c_char_p
     L.bc_last_error.argtypes = [vp]
     L.bc_destroy.restype = None
@@ -301,6 +317,38 @@ class Engine:
     def dist_set_live(self, level, live, stream=0):
         a = np.ascontiguousarray(live, dtype=np.uint32)
         self._ck(self._lib.bc_dist_set_live(self._h, int(level), _ptr(a), ctypes.c_void_p(stream or None)))
+
+    def dist_hybir_setup(self, cin_off, cin_src, cin_w=None):
+        co = np.ascontiguousarray(cin_off, dtype=np.int64)
+        cs = np.ascontiguousarray(cin_src, dtype=np.int32)
+        cw = None if cin_w is None else np.ascontiguousarray(cin_w, dtype=np.int32)
+        self._ck(self._lib.bc_dist_hybir_setup(self._h, _ptr(co), _ptr(cs), _ptr(cw)))
+
+    def dist_hybir_get_table(self, part, bm_ptr, sm_ptr):
+        self._ck(self._lib.bc_dist_hybir_get_table(self._h, int(part), ctypes.c_void_p(bm_ptr),
+                                                   ctypes.c_void_p(sm_ptr)))
+
+    def dist_hybir_set_table(self, part, bm_ptr, sm_ptr):
+        self._ck(self._lib.bc_dist_hybir_set_table(self._h, int(part), ctypes.c_void_p(bm_ptr),
+                                                   ctypes.c_void_p(sm_ptr)))
+
+    def dist_hybir_seed_count(self) -> int:
+        return int(self._lib.bc_dist_hybir_seed_count(self._h))
+
+    def dist_hybir_seeds(self, sources, seed_dist_ptr, seed_sigma_ptr, stream=0):
+        src = np.ascontiguousarray(sources, dtype=np.int64)
+        self._ck(self._lib.bc_dist_hybir_seeds(self._h, _ptr(src), len(src), ctypes.c_void_p(seed_dist_ptr),
+                                               ctypes.c_void_p(seed_sigma_ptr), ctypes.c_void_p(stream or None)))
+
+    def dist_hybir_forward(self, seed_dist_ptr, seed_sigma_ptr, stream=0):
+        depth, iters = ctypes.c_int(0), ctypes.c_int64(0)
+        self._ck(self._lib.bc_dist_hybir_forward(self._h, ctypes.c_void_p(seed_dist_ptr),
+                                                 ctypes.c_void_p(seed_sigma_ptr), ctypes.byref(depth),
+                                                 ctypes.byref(iters), ctypes.c_void_p(stream or None)))
+        return depth.value, iters.value
+
+    def dist_hybir_set_depth(self, depth, stream=0):
+        self._ck(self._lib.bc_dist_hybir_set_depth(self._h, int(depth), ctypes.c_void_p(stream or None)))
 
     def dist_finish(self, bc_dev_ptr, stream=0):
         self._ck(self._lib.bc_dist_finish(self._h, ctypes.c_void_p(bc_dev_ptr), ctypes.c_void_p(stream or None)))

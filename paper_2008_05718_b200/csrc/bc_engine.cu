@@ -239,6 +239,8 @@ struct bc_handle {
     double *bc_scratch = nullptr;  // device bc vector of bc_run
     // ---- graph-partitioned multi-GPU mode (one rank = one part)
     int dist_rank = -1, dist_world = 0, dist_ng = 0, dist_cnt = 0;
+    bool dist_hybir = false;      // border-matrix forward phase across ranks (bc_dist_hybir_*)
+    int dist_depth = 0;           // levels of the batch in flight (local, then global)
     std::vector<int64_t> dist_border_off;
     int32_t *dist_border_v = nullptr;   // all ranks' borders, rank-major
     int32_t *dist_counts = nullptr, *dist_offsets = nullptr;
@@ -1419,8 +1421,12 @@ int build_border_tables(bc_handle *h) {
     TRY(upload(h, &d_borders, src));
     const int per = 32 * groups;
     const BorderGeom geo = border_geom(h);
-    for (int first = 0; first < h->B; first += per) {
-        const int cnt = std::min(per, h->B - first);
+    // graph-partitioned multi-GPU runs build the rows of their own part only; the other parts'
+    // tables arrive through bc_dist_hybir_set_table
+    const int b_lo = h->dist_hybir ? h->h_part_off[(size_t)h->dist_rank] : 0;
+    const int b_hi = h->dist_hybir ? h->h_part_off[(size_t)h->dist_rank + 1] : h->B;
+    for (int first = b_lo; first < b_hi; first += per) {
+        const int cnt = std::min(per, b_hi - first);
         const int ng = (cnt + 31) / 32;
         TRY(begin_batch(h, d_borders + first, cnt, ng, st));
         int depth = 1;
@@ -1978,18 +1984,32 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     return h->fail(BC_ERR_INPUT, "unknown option '" + k + "'");
 }
 
-int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
-    if (h == nullptr) return BC_ERR_INPUT;
-    if (k < 1 || assignment == nullptr)
-        return h->fail(BC_ERR_INPUT, "bc_set_partition: need k >= 1 and an assignment");
+}  // extern "C"
+
+namespace {
+
+// Border geometry supplied by the caller (graph-partitioned multi-GPU runs: a rank holds the CSR
+// rows of its own part only, so the borders and cut arcs of the other parts cannot be derived
+// from its rows).  Borders are listed part by part, ascending vertex id inside a part.
+struct ExternalBorders {
+    const int64_t *border_off;   // [k + 1]
+    const int32_t *border_v;     // [B]
+    const int64_t *cin_off;      // [B + 1] incoming cut arcs per border
+    const int32_t *cin_src;      // [n_cut] border index of the arc's source
+    const int32_t *cin_w;        // [n_cut] weights, nullptr = all one
+};
+
+int install_partition(bc_handle *h, int k, const int32_t *assignment, const ExternalBorders *ext) {
     const int64_t n = h->n;
     for (int64_t v = 0; v < n; ++v)
         if (assignment[v] < 0 || assignment[v] >= k)
             return h->fail(BC_ERR_INPUT, "bc_set_partition: part id outside [0, k)");
     CUDA_TRY(h, cudaSetDevice(h->device));
+    std::vector<int32_t> part(assignment, assignment + n);   // `assignment` may alias h->h_part
     free_partition(h);
     h->k = k;
-    h->h_part.assign(assignment, assignment + n);
+    h->h_part.swap(part);
+    assignment = h->h_part.data();
     if (k == 1) return BC_OK;
     if ((int64_t)h->h_col.size() != h->n_arcs) {
         h->h_col.resize((size_t)h->n_arcs);
@@ -2015,8 +2035,11 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
             } else is_border = true;
         }
         ioff[(size_t)v + 1] = (int64_t)icol.size();
-        if (is_border) borders[(size_t)assignment[v]].push_back((int32_t)v);
+        if (is_border && ext == nullptr) borders[(size_t)assignment[v]].push_back((int32_t)v);
     }
+    if (ext != nullptr)
+        for (int p = 0; p < k; ++p)
+            borders[(size_t)p].assign(ext->border_v + ext->border_off[p], ext->border_v + ext->border_off[p + 1]);
     h->h_part_off.assign((size_t)k + 1, 0);
     h->h_tab_off.assign((size_t)k, 0);
     h->h_border_v.clear();
@@ -2028,6 +2051,8 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
         const int64_t b = (int64_t)borders[(size_t)p].size();
         tab += b * b;
         for (int32_t v : borders[(size_t)p]) {
+            if (v < 0 || v >= n || assignment[v] != p)
+                return h->fail(BC_ERR_INPUT, "border list names a vertex outside its part");
             h->h_border_v.push_back(v);
             h->h_border_p.push_back(p);
         }
@@ -2035,19 +2060,30 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     h->h_part_off[(size_t)k] = (int32_t)h->h_border_v.size();
     h->B = (int)h->h_border_v.size();
     h->tab_total = tab;
-    std::vector<int32_t> index_of((size_t)n, -1);
-    for (int j = 0; j < h->B; ++j) index_of[(size_t)h->h_border_v[(size_t)j]] = j;
     // incoming cut arcs of every border, in arc order (the graph is symmetric)
     std::vector<int64_t> cin_off((size_t)h->B + 1, 0);
     std::vector<int32_t> cin_src, cin_w;
-    for (int j = 0; j < h->B; ++j) {
-        const int64_t v = h->h_border_v[(size_t)j];
-        for (int64_t a = off[v]; a < off[v + 1]; ++a)
-            if (assignment[col[a]] != assignment[v]) {
-                cin_src.push_back(index_of[(size_t)col[a]]);
-                cin_w.push_back(weighted ? h->h_wgt[(size_t)a] : 1);   // symmetric graph: w(u->v) = w(v->u)
-            }
-        cin_off[(size_t)j + 1] = (int64_t)cin_src.size();
+    if (ext != nullptr) {
+        cin_off.assign(ext->cin_off, ext->cin_off + h->B + 1);
+        const int64_t nc = cin_off[(size_t)h->B];
+        cin_src.assign(ext->cin_src, ext->cin_src + nc);
+        if (ext->cin_w) cin_w.assign(ext->cin_w, ext->cin_w + nc);
+        else cin_w.assign((size_t)nc, 1);
+        for (int64_t c = 0; c < nc; ++c)
+            if (cin_src[(size_t)c] < 0 || cin_src[(size_t)c] >= h->B)
+                return h->fail(BC_ERR_INPUT, "cut arc list names a border outside [0, B)");
+    } else {
+        std::vector<int32_t> index_of((size_t)n, -1);
+        for (int j = 0; j < h->B; ++j) index_of[(size_t)h->h_border_v[(size_t)j]] = j;
+        for (int j = 0; j < h->B; ++j) {
+            const int64_t v = h->h_border_v[(size_t)j];
+            for (int64_t a = off[v]; a < off[v + 1]; ++a)
+                if (assignment[col[a]] != assignment[v]) {
+                    cin_src.push_back(index_of[(size_t)col[a]]);
+                    cin_w.push_back(weighted ? h->h_wgt[(size_t)a] : 1);   // symmetric graph: w(u->v) = w(v->u)
+                }
+            cin_off[(size_t)j + 1] = (int64_t)cin_src.size();
+        }
     }
     h->n_cut = (int64_t)cin_src.size();
     Csr &c = h->intra;
@@ -2071,6 +2107,18 @@ int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
     TRY(upload(h, &h->d_cin_src, cin_src));
     TRY(upload(h, &h->d_cin_w, cin_w));
     return BC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bc_set_partition(bc_handle *h, int k, const int32_t *assignment) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (k < 1 || assignment == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_set_partition: need k >= 1 and an assignment");
+    h->dist_hybir = false;
+    return install_partition(h, k, assignment, nullptr);
 }
 
 int bc_run_device(bc_handle *h, int mode, const int64_t *sources, int64_t n_sources,
@@ -2350,6 +2398,144 @@ int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream) {
         bc_dev, h->bcg, h->d_part, h->dist_rank, h->n, h->alloc_groups);
     ++h->launches;
     CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+// ---- border-matrix forward phase across ranks ------------------------------------------------
+// Every rank holds all parts' border tables and runs the (cheap, batched) border refinement and
+// path-count composition redundantly, so the forward phase of a batch needs ONE exchange: the
+// Step-1 border seeds (distance min-reduced, path count max-reduced over the ranks; only the
+// rank that owns a lane's source holds finite values).  Step 6 then runs on the rank's own part.
+
+int bc_dist_hybir_setup(bc_handle *h, const int64_t *cin_off, const int32_t *cin_src,
+                        const int32_t *cin_w) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (h->dist_rank < 0) return h->fail(BC_ERR_INPUT, "bc_dist_hybir_setup: call bc_dist_setup first");
+    if (cin_off == nullptr || (cin_off[h->dist_border_off[(size_t)h->dist_world]] > 0 && cin_src == nullptr))
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_setup: null cut-arc lists");
+    if (h->full.wgt != nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_setup: the multi-GPU border exchange is unit-weight");
+    std::vector<int32_t> bv((size_t)h->dist_border_off[(size_t)h->dist_world]);
+    if (!bv.empty())
+        CUDA_TRY(h, cudaMemcpy(bv.data(), h->dist_border_v, bv.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    ExternalBorders ext{h->dist_border_off.data(), bv.data(), cin_off, cin_src, cin_w};
+    h->dist_hybir = true;
+    std::vector<int32_t> part = h->h_part;
+    TRY(install_partition(h, h->dist_world, part.data(), &ext));
+    h->tables_ready = false;
+    return build_border_tables(h);   // rows of this rank's own part
+}
+
+int bc_dist_hybir_get_table(bc_handle *h, int part, int32_t *bm_dev, double *sm_dev) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir || !h->tables_ready || part < 0 || part >= h->k)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_get_table: no tables / bad part");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const int64_t b = h->h_part_off[(size_t)part + 1] - h->h_part_off[(size_t)part];
+    if (b == 0) return BC_OK;
+    CUDA_TRY(h, cudaMemcpy(bm_dev, h->bm + h->h_tab_off[(size_t)part], (size_t)(b * b) * sizeof(int32_t),
+                           cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaMemcpy(sm_dev, h->sm + h->h_tab_off[(size_t)part], (size_t)(b * b) * sizeof(double),
+                           cudaMemcpyDeviceToDevice));
+    return BC_OK;
+}
+
+int bc_dist_hybir_set_table(bc_handle *h, int part, const int32_t *bm_dev, const double *sm_dev) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir || !h->tables_ready || part < 0 || part >= h->k)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_set_table: no tables / bad part");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const int64_t b = h->h_part_off[(size_t)part + 1] - h->h_part_off[(size_t)part];
+    if (b == 0) return BC_OK;
+    CUDA_TRY(h, cudaMemcpy(h->bm + h->h_tab_off[(size_t)part], bm_dev, (size_t)(b * b) * sizeof(int32_t),
+                           cudaMemcpyDeviceToDevice));
+    CUDA_TRY(h, cudaMemcpy(h->sm + h->h_tab_off[(size_t)part], sm_dev, (size_t)(b * b) * sizeof(double),
+                           cudaMemcpyDeviceToDevice));
+    return BC_OK;
+}
+
+int64_t bc_dist_hybir_seed_count(bc_handle *h) {
+    if (h == nullptr || !h->dist_hybir) return -1;
+    return (int64_t)h->B * 32 * std::max(h->groups, 1);
+}
+
+int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, int64_t count, int32_t *seed_dist_dev,
+                        double *seed_sigma_dev, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir) return h->fail(BC_ERR_INPUT, "bc_dist_hybir_seeds: call bc_dist_hybir_setup first");
+    if (seed_dist_dev == nullptr || seed_sigma_dev == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_seeds: null seed buffers");
+    cudaStream_t st = (cudaStream_t)stream;
+    TRY(bc_dist_begin(h, sources, count, stream));   // state, lanes, level-0 seeds
+    const int S = 32 * h->groups;
+    TRY(ensure_border_state(h, S));
+    std::vector<int32_t> lp((size_t)h->border_S, 0);
+    for (int64_t i = 0; i < count; ++i) lp[(size_t)i] = h->h_part[(size_t)sources[i]];
+    CUDA_TRY(h, cudaMemcpyAsync(h->lane_part, lp.data(), h->border_S * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, st));
+    int depth = 1;
+    h->cnt_off = 4;   // Step 1 is a partial traversal: keep it out of the totals
+    const int rc = forward_sweep(h, h->intra, h->dist_ng, st, &depth);
+    h->cnt_off = 0;
+    TRY(rc);
+    const size_t bcnt = (size_t)h->B * h->border_S;
+    fill_border_kernel<<<grid1d(bcnt, 256, 4736), 256, 0, st>>>(h->D, h->seedD, h->seedS, h->sig, h->arr, bcnt);
+    TRY(upload_level_ptrs(h, depth, st));
+    if (h->B > 0)
+        border_gather_kernel<<<grid1d(bcnt), 256, 0, st>>>(h->d_lvl_ptrs, h->live, h->alloc_groups, depth,
+                                                           h->sigma, h->n, border_geom(h), h->border_S,
+                                                           h->seedD, h->seedS);
+    h->launches += 2;
+    CUDA_TRY(h, cudaGetLastError());
+    CUDA_TRY(h, cudaMemcpyAsync(seed_dist_dev, h->seedD, bcnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(seed_sigma_dev, h->seedS, bcnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    return BC_OK;
+}
+
+int bc_dist_hybir_forward(bc_handle *h, const int32_t *seed_dist_dev, const double *seed_sigma_dev,
+                          int *depth_out, int64_t *iterations_out, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir || h->dist_ng <= 0)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_forward: no batch in flight (bc_dist_hybir_seeds)");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bcnt = (size_t)h->B * h->border_S;
+    CUDA_TRY(h, cudaMemcpyAsync(h->seedD, seed_dist_dev, bcnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->seedS, seed_sigma_dev, bcnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    std::vector<int32_t> iters;
+    std::vector<uint32_t> entered;
+    int max_seed = -1;
+    TRY(refine_and_compose(h, h->dist_cnt, h->dist_ng, st, &iters, &entered, &max_seed));
+    // Step 6 on this rank's part: its own source lanes plus every border seed (seeds of other
+    // parts' borders only mark those vertices at their level: they have no rows here, and the
+    // backward sweep needs exactly those marks to find its cross-part children)
+    TRY(begin_batch(h, h->d_src, h->dist_cnt, h->dist_ng, st));
+    int depth = 1;
+    TRY(forward_sweep(h, h->intra, h->dist_ng, st, &depth, true, h->dist_cnt, max_seed));
+    h->dist_depth = depth;
+    if (depth_out) *depth_out = depth;
+    if (iterations_out) {
+        int64_t total = 0;
+        for (int i = 0; i < h->dist_cnt; ++i) total += iters[(size_t)i];
+        *iterations_out = total;
+    }
+    return BC_OK;
+}
+
+// Levels [local depth, global depth) exist on other ranks only: give them empty mask rows here.
+int bc_dist_hybir_set_depth(bc_handle *h, int global_depth, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir || global_depth < h->dist_depth)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_set_depth: global depth below the local one");
+    cudaStream_t st = (cudaStream_t)stream;
+    TRY(ensure_levels(h, global_depth + 1));
+    const size_t bytes = (size_t)h->alloc_groups * (size_t)h->n * sizeof(uint32_t);
+    for (int L = h->dist_depth; L < global_depth; ++L) {
+        CUDA_TRY(h, cudaMemsetAsync(h->lvl[(size_t)L], 0, bytes, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->live + (size_t)L * h->alloc_groups, 0,
+                                    h->alloc_groups * sizeof(uint32_t), st));
+    }
+    h->dist_depth = global_depth;
     return BC_OK;
 }
 

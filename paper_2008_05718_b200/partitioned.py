@@ -66,17 +66,56 @@ class _Transport:
         return torch.stack(parts).to(self.device)
 
     def all_reduce_sum(self, t):
+        return self.all_reduce(t, "sum")
+
+    def all_reduce(self, t, op: str):
+        red = {"sum": self.dist.ReduceOp.SUM, "min": self.dist.ReduceOp.MIN,
+               "max": self.dist.ReduceOp.MAX}[op]
         if self.on_device:
-            self.dist.all_reduce(t)
+            self.dist.all_reduce(t, op=red)
             return t
         host = t.cpu()
-        self.dist.all_reduce(host)
+        self.dist.all_reduce(host, op=red)
+        t.copy_(host)
+        return t
+
+    def broadcast(self, t, src: int):
+        if self.on_device:
+            self.dist.broadcast(t, src=src)
+            return t
+        host = t.cpu()
+        self.dist.broadcast(host, src=src)
         t.copy_(host)
         return t
 
 
+def incoming_cut_arcs(bs, border_arrays):
+    """(cin_off, cin_src): for every border, in the rank-major border order, the border
+    indices on the other side of its cut arcs (the graph is symmetric, so the incoming arcs
+    of a border are its own cut arcs reversed)."""
+    total = int(sum(len(b) for b in border_arrays))
+    cin_off = np.zeros(total + 1, dtype=np.int64)
+    if total == 0 or len(bs.cut_src) == 0:
+        return cin_off, np.zeros(0, dtype=np.int32)
+    all_borders = np.concatenate(border_arrays).astype(np.int64)
+    index_of = np.full(int(max(all_borders.max(), np.max(bs.cut_dst))) + 1, -1, dtype=np.int64)
+    index_of[all_borders] = np.arange(total)
+    at = index_of[np.asarray(bs.cut_src, dtype=np.int64)]
+    other = index_of[np.asarray(bs.cut_dst, dtype=np.int64)]
+    order = np.argsort(at, kind="stable")
+    np.cumsum(np.bincount(at, minlength=total), out=cin_off[1:])
+    return cin_off, other[order].astype(np.int32)
+
+
 class PartitionedRunner:
-    def __init__(self, g: Graph, part: Partition, device, groups: int = 4):
+    """``forward='bsp'``: level-synchronous forward phase, one border exchange per level
+    (bsp.py:22-103).  ``forward='hybir'``: the paper's border-matrix forward phase
+    (forward.py:188-256) -- Step 1 inside the source's part, ONE exchange of the border
+    seeds, refinement + path-count composition on the border tables (replicated on every
+    rank), Step 6 inside every part; the forward phase of a batch then costs two all-reduces
+    whatever the diameter.  The backward phase is level-synchronous in both."""
+
+    def __init__(self, g: Graph, part: Partition, device, groups: int = 4, forward: str = "bsp"):
         import torch
         import torch.distributed as dist
         from . import _capi
@@ -97,6 +136,32 @@ class PartitionedRunner:
         self.eng.set_option("groups", groups)
         self.eng.dist_setup(self.rank, self.world, part.assignment, self.border_off, border_v)
         self.tr = _Transport(device)
+        if forward not in ("bsp", "hybir"):
+            raise InputError("forward must be 'bsp' or 'hybir'")
+        self.forward = forward
+        self.iterations = 0
+        self.forward_exchanges = 0
+        self.backward_exchanges = 0
+        if forward == "hybir":
+            if not g.unit_weight:
+                raise InputError("the multi-GPU border exchange is unit-weight")
+            cin_off, cin_src = incoming_cut_arcs(bs, bs.border_arrays)
+            self.eng.dist_hybir_setup(cin_off, cin_src)
+            # every rank publishes the border table of its own part once
+            for p in range(self.world):
+                b = self.border_counts[p]
+                if b == 0:
+                    continue
+                bm = torch.empty(b * b, dtype=torch.int32, device=device)
+                sm = torch.empty(b * b, dtype=torch.float64, device=device)
+                if p == self.rank:
+                    self.eng.dist_hybir_get_table(p, bm.data_ptr(), sm.data_ptr())
+                if self.world > 1:
+                    self.tr.broadcast(bm, p)
+                    self.tr.broadcast(sm, p)
+                if p != self.rank:
+                    self.eng.dist_hybir_set_table(p, bm.data_ptr(), sm.data_ptr())
+                torch.cuda.synchronize(device)
         self.max_nb = max(self.border_counts + [1])
         self.stream = 0     # default stream: exports / imports and collectives stay ordered
         self.exchanged_bytes = 0
@@ -124,9 +189,40 @@ class PartitionedRunner:
                                  all_values[peer].data_ptr())
         self.torch.cuda.synchronize(self.device)   # buffers are freed on return
 
+    def _forward_hybir(self, sources):
+        torch = self.torch
+        cnt = self.eng.dist_hybir_seed_count()
+        sd = torch.empty(max(cnt, 1), dtype=torch.int32, device=self.device)
+        ss = torch.empty(max(cnt, 1), dtype=torch.float64, device=self.device)
+        self.eng.dist_hybir_seeds(sources, sd.data_ptr(), ss.data_ptr())
+        if self.world > 1:
+            # only the rank that owns a lane's source holds finite seeds for that lane
+            self.tr.all_reduce(sd, "min")
+            self.tr.all_reduce(ss, "max")
+            self.forward_exchanges += 2
+            self.exchanged_bytes += cnt * 12
+        depth, iters = self.eng.dist_hybir_forward(sd.data_ptr(), ss.data_ptr())
+        self.iterations += iters
+        d = torch.tensor([depth], dtype=torch.int64, device=self.device)
+        if self.world > 1:
+            self.tr.all_reduce(d, "max")
+        depth = int(d.item())
+        self.eng.dist_hybir_set_depth(depth)
+        torch.cuda.synchronize(self.device)
+        return depth
+
     def run_batch(self, sources):
         torch = self.torch
         ng = (len(sources) + 31) // 32
+        if self.forward == "hybir":
+            depth = self._forward_hybir(sources)
+            for lv in range(depth - 1, 0, -1):
+                self.eng.dist_backward_level(lv, lv == depth - 1)
+                if self.world > 1 and lv > 1:
+                    self._exchange(lv, 2, ng)
+                    self.backward_exchanges += 1
+            self.levels = max(self.levels, depth)
+            return depth
         self.eng.dist_begin(sources)
         depth = 1
         level = 1
@@ -134,6 +230,7 @@ class PartitionedRunner:
             self.eng.dist_forward_level(level)
             if self.world > 1:
                 self._exchange(level, 1, ng)
+                self.forward_exchanges += 1
             live = torch.from_numpy(self.eng.dist_get_live(level, ng).astype(np.int64)).to(self.device)
             if self.world > 1:
                 live = self.tr.all_gather(live)
@@ -151,6 +248,7 @@ class PartitionedRunner:
             self.eng.dist_backward_level(lv, lv == depth - 1)
             if self.world > 1 and lv > 1:
                 self._exchange(lv, 2, ng)
+                self.backward_exchanges += 1
         self.levels = max(self.levels, depth)
         return depth
 
@@ -184,14 +282,19 @@ def run_bc_partitioned(g: Graph, cfg):
     torch.cuda.set_device(device)
     part = cfg.partition if cfg.partition is not None else block_partition(g, world)
     sources = select_sources(g, cfg)
-    runner = PartitionedRunner(g, part, device, cfg.groups or 4)
+    # RunConfig.mode picks the forward phase as in the reference: 'hybir' = border matrices
+    # (weighted graphs and 'direct' fall back to the level-synchronous exchange)
+    forward = "hybir" if (cfg.mode == "hybir" and g.unit_weight) else "bsp"
+    runner = PartitionedRunner(g, part, device, cfg.groups or 4, forward)
     try:
         bc = runner.run(sources).cpu().numpy()
     finally:
         runner.close()
     elapsed = time.perf_counter() - t0
     bs = identify_borders(g, part)
-    stats = {"levels": runner.levels, "exchanged_bytes": runner.exchanged_bytes, "world": world}
+    stats = {"levels": runner.levels, "exchanged_bytes": runner.exchanged_bytes, "world": world,
+             "forward": runner.forward, "forward_exchanges": runner.forward_exchanges,
+             "backward_exchanges": runner.backward_exchanges, "iterations": runner.iterations}
     mteps = g.num_edges * len(sources) / elapsed / 1e6 if elapsed > 0 else 0.0
     return RunResult(bc, [], CommTotals(0, 0, runner.exchanged_bytes), mteps, elapsed, part, bs, cfg,
                      0, stats)

@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, kind, out):
+def _worker(rank, world, port, kind, mode, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0")
     import oracle as O
@@ -36,21 +36,31 @@ def _worker(rank, world, port, kind, out):
         g = G.road_like(30, 24, keep=0.25, seed=4)
         part = P.strip_partition(30, 24, world)
         sources = list(range(0, g.num_vertices, 17))
-    cfg = P.RunConfig(sources=sources, num_gpus=world, gpu_mode="graph-partitioned",
+    cfg = P.RunConfig(sources=sources, num_gpus=world, gpu_mode="graph-partitioned", mode=mode,
                       partition=part, groups=2, device=0)
     res = P.run_bc(g, cfg)
     want, _ = O.brandes_bc(g, sources)
     ok = bool(np.allclose(res.bc, want, rtol=1e-9, atol=1e-12))
-    np.save("%s.%d.npy" % (out, rank), np.array([ok, res.stats["levels"], res.stats["exchanged_bytes"]]))
+    batches = (len(sources) + 63) // 64
+    np.save("%s.%d.npy" % (out, rank), np.array([ok, res.stats["levels"], res.stats["exchanged_bytes"],
+                                                 res.stats["forward_exchanges"], batches,
+                                                 res.stats["forward"] == "hybir"]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "rmat"), (2, "road"), (3, "road")])
-def test_graph_partitioned_ranks_match_oracle(tmp_path, world, kind):
+@pytest.mark.parametrize("world,kind,mode", [
+    (2, "rmat", "bsp-baseline"), (2, "road", "bsp-baseline"), (3, "road", "bsp-baseline"),
+    (2, "rmat", "hybir"), (2, "road", "hybir"), (3, "road", "hybir")])
+def test_graph_partitioned_ranks_match_oracle(tmp_path, world, kind, mode):
     out = str(tmp_path / "res")
-    mp.spawn(_worker, args=(world, _free_port(), kind, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), kind, mode, out), nprocs=world, join=True)
     for r in range(world):
-        ok, levels, nbytes = np.load("%s.%d.npy" % (out, r))
+        ok, levels, nbytes, fwd_x, batches, is_hybir = np.load("%s.%d.npy" % (out, r))
         assert ok, "rank %d BC differs from the oracle" % r
         assert levels >= 3 and nbytes > 0
+        if mode == "hybir":
+            # the border-matrix forward phase: two all-reduces per batch, whatever the depth
+            assert is_hybir and fwd_x == 2 * batches
+        else:
+            assert not is_hybir and fwd_x >= batches * (levels - 1)
