@@ -171,7 +171,7 @@ def cpu_sample(g, sources, seconds_target=15.0):
     dt = time.perf_counter() - t0
     # one refinement so the sample lands near the target duration
     if dt < seconds_target / 3 and k < len(sources):
-        k2 = min(len(sources), int(k * min(8.0, seconds_target / max(dt, 1e-3))))
+        k2 = min(len(sources), int(k * min(64.0, seconds_target / max(dt, 1e-3))))
         k2 = max(threads, (k2 // threads) * threads)
         if k2 > k:
             k = k2
