@@ -11,8 +11,11 @@ def cached_graph(name):
     if os.path.exists(path):
         z = np.load(path)
         return Graph(int(z["n"]), int(z["m"]), z["off"], z["col"])
-    scale, ef = {"rmat20": (20, 16), "rmat22": (22, 16), "rmat18": (18, 16)}[name]
-    g = G.rmat(scale, ef, 1)
+    if name == "er22":
+        g = G.erdos_renyi(1 << 22, 1 << 26, 1)
+    else:
+        scale, ef = {"rmat20": (20, 16), "rmat22": (22, 16), "rmat18": (18, 16)}[name]
+        g = G.rmat(scale, ef, 1)
     np.savez(path, n=g.num_vertices, m=g.num_edges, off=g.offsets, col=g.col_idx)
     return g
 
