@@ -508,6 +508,9 @@ int ensure_queues(bc_handle *h) {
     TRY(dev_alloc(h, &h->d_qbeg, G));
     TRY(dev_alloc(h, &h->d_qend, G));
     TRY(dev_alloc(h, &h->d_qlbeg, G));
+    CUDA_TRY(h, cudaMemset(h->d_qbeg, 0, G * sizeof(int64_t)));
+    CUDA_TRY(h, cudaMemset(h->d_qend, 0, G * sizeof(int64_t)));
+    CUDA_TRY(h, cudaMemset(h->d_qlbeg, 0, G * sizeof(int64_t)));
     TRY(dev_alloc(h, &h->scrA, G * n));
     TRY(dev_alloc(h, &h->scrB, G * n));
     TRY(dev_alloc(h, &h->lstat, (size_t)4));
@@ -549,7 +552,8 @@ int ensure_deep(bc_handle *h) {
 // Queue entries are (vertex, level) pairs: a vertex can sit in up to 32 levels of
 // a group (one per lane), so deep graphs outgrow the initial 4n entries.  Grow
 // by doubling up to 33n.
-int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st, int64_t used) {
+int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
+                const std::vector<unsigned long long> &used) {
     const int64_t max_cap = 33 * h->n + 1024;
     if (h->q_cap >= max_cap || need_cap <= h->q_cap) return BC_OK;
     const int64_t cap = std::min(max_cap, std::max(need_cap, 2 * h->q_cap));
@@ -560,7 +564,7 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st, int64_t used) {
     CUDA_TRY(h, arena_malloc((void **)&nv, G * (size_t)cap * sizeof(int32_t)));
     CUDA_TRY(h, arena_malloc((void **)&nm, G * (size_t)cap * sizeof(uint32_t)));
     for (size_t g = 0; g < G; ++g) {
-        const size_t keep = (size_t)std::min<int64_t>(std::max<int64_t>(used, 0), h->q_cap);   // entries in use
+        const size_t keep = (size_t)std::min<int64_t>(g < used.size() ? (int64_t)used[g] : 0, h->q_cap);   // entries in use
         if (keep == 0) continue;
         CUDA_TRY(h, cudaMemcpy(nv + g * cap, h->q_v + g * h->q_cap, keep * sizeof(int32_t),
                                cudaMemcpyDeviceToDevice));
@@ -964,7 +968,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         bool push = prev.farcs * beta <= graph_arcs &&
                     (prev.maxdeg <= (unsigned long long)kHeavyDeg || prev.heavy >= 0 || !prev.queued);
         if (push && h->q_cap - used < want_room) {
-            TRY(grow_queues(h, used + want_room, st, used));
+            TRY(grow_queues(h, used + want_room, st, qcount));
             push = h->q_cap - used >= want_room;
         }
         if (push) {
