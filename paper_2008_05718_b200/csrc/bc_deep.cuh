@@ -241,7 +241,7 @@ struct DeepBwdParams {
     int64_t n;
     QueueParams q;               // q_v / q_m / cap
     const int64_t *range_table;  // [level][0: begin, 1: end][G]
-    const double *sigma;
+    double *sigma;
     double *coef;
     double *delta;               // only with STORE_DELTA
     double *bcg;
@@ -251,7 +251,7 @@ struct DeepBwdParams {
     uint32_t *erase_first;       // scratch array holding level hi + 1 (nullptr: dense array, keep)
     uint32_t *scr0, *scr1;       // all-zero scratch arrays (apart from erase_first's content)
     int first_write;             // scratch (0 / 1) that receives level hi
-    int accumulate;
+    int accumulate;              // bit 0: BC partials, bit 1: clear sigma (finalize_backward)
 };
 
 // Backward: consecutive queue levels, one thread per entry (bwd_queue_thin_kernel),
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepB
                 if (i >= end_t[g]) continue;
                 const size_t qbase = (size_t)g * p.q.cap;
                 const uint32_t *gn = nbr ? nbr + (size_t)g * n : nullptr;
-                const double *gsig = p.sigma + (size_t)g * n * 32;
+                double *gsig = p.sigma + (size_t)g * n * 32;
                 double *gcoef = p.coef + (size_t)g * n * 32;
                 const int64_t v = p.q.q_v[qbase + i];
                 const uint32_t m = p.q.q_m[qbase + i];
@@ -309,9 +309,10 @@ __global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepB
                     const double d = sv * acc;
                     gcoef[idx] = (1.0 + d) / sv;
                     if (STORE_DELTA) p.delta[(size_t)g * n * 32 + idx] = d;
+                    else if (p.accumulate & 2) clear_after_use(gsig + idx, sv);   // see finalize_backward
                     total_d += d;
                 }
-                if (p.accumulate) p.bcg[(size_t)g * n + v] += total_d;
+                if (p.accumulate & 1) p.bcg[(size_t)g * n + v] += total_d;
                 wr[(size_t)g * n + v] = m;   // level L becomes the children masks of level L - 1
             }
         }

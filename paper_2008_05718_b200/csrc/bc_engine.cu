@@ -213,6 +213,9 @@ struct bc_handle {
     uint32_t *vis = nullptr;
     std::vector<uint32_t *> lvl;
     double *sigma = nullptr, *coef = nullptr, *delta = nullptr;
+    bool sigma_clean = false;   // sigma is all zero (kept so by the backward sweeps of adaptive batches)
+    bool lazy_clear = false;    // this batch's backward sweep clears sigma behind itself
+    int last_depth = 0;         // levels of the previous batch (deep graphs: memset instead)
     double *bcg = nullptr;
     double *pacc = nullptr;
     uint32_t *pmask = nullptr;
@@ -446,6 +449,7 @@ int ensure_state(bc_handle *h, int groups, bool want_delta) {
         CUDA_TRY(h, arena_malloc((void **)&h->bcg, groups * n * sizeof(double)));
         CUDA_TRY(h, cudaMemset(h->bcg, 0, groups * n * sizeof(double)));
         h->alloc_groups = groups;
+        h->sigma_clean = false;
     }
     if (want_delta && h->delta == nullptr)
         CUDA_TRY(h, arena_malloc((void **)&h->delta, (size_t)h->alloc_groups * n * 32 * sizeof(double)));
@@ -722,7 +726,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     p.nbr = deepest ? nullptr : (nbr ? nbr : h->lvl[L + 1]);
     p.cur = cur ? cur : h->lvl[L];
     p.live_prev = h->live + (size_t)L * h->alloc_groups;
-    p.accumulate_bc = accumulate ? 1 : 0;
+    p.accumulate_bc = (accumulate ? 1 : 0) | (h->lazy_clear ? 2 : 0);
     p.level = L;
     p.max_level = h->cur_depth - 1;
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
@@ -757,8 +761,15 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
 int begin_batch(bc_handle *h, const int64_t *src_dev, int cnt, int ng, cudaStream_t st,
                 bool zero_sigma = false) {
     const int64_t n = h->n;
-    if (zero_sigma)  // push levels accumulate path counts with atomic adds
-        CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, (size_t)ng * n * 32 * sizeof(double), st));
+    // push levels accumulate path counts with atomic adds: they need zeros.  The backward sweep
+    // of a non-inspection batch leaves sigma all zero again (finalize_backward), so the memset runs
+    // only after something else touched the array.
+    // Deep graphs (previous batch above 64 levels) take the memset instead: there the extra dirty
+    // sector per (vertex, source) visit costs more than clearing the array.
+    h->lazy_clear = zero_sigma && h->last_depth <= 64;
+    if (zero_sigma && !(h->sigma_clean && h->lazy_clear))
+        CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, (size_t)h->alloc_groups * n * 32 * sizeof(double), st));
+    h->sigma_clean = false;
     CUDA_TRY(h, cudaMemsetAsync(h->live, 0, (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
     init_state_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vis, h->lvl[0], n, cnt);
     seed_sources_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(src_dev, cnt, n, h->vis, h->lvl[0],
@@ -1205,7 +1216,7 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             dp.scr0 = scr[0];
             dp.scr1 = scr[1];
             dp.first_write = holder == 0 ? 1 : 0;
-            dp.accumulate = debug ? 0 : 1;
+            dp.accumulate = (debug ? 0 : 1) | (h->lazy_clear ? 2 : 0);
             void *args[] = {&dp};
             if (debug)
                 CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_kernel<true>, dim3(h->deep_grid_b),
@@ -1232,13 +1243,13 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
                     c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 0);
             else if (thin)
                 bwd_queue_thin_kernel<false><<<grid, 128, 0, st>>>(
-                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 1);
+                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, h->lazy_clear ? 3 : 1);
             else if (debug)
                 bwd_queue_kernel<true><<<grid, kWarpsPerBlock * 32, 0, st>>>(
                     c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 0);
             else
                 bwd_queue_kernel<false><<<grid, kWarpsPerBlock * 32, 0, st>>>(
-                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, 1);
+                    c.off, c.col, h->n, q, nbr, h->sigma, h->coef, h->delta, h->bcg, h->lazy_clear ? 3 : 1);
             ++h->launches;
             CUDA_TRY(h, cudaGetLastError());
         } else {  // a queue level with heavy vertices: run it through the dense kernel (hub slices)
@@ -1621,6 +1632,14 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         const int64_t l_bwd = h->launches;
         if (adaptive) TRY(backward_adaptive(h, h->full, depth, reps, ng, debug, st));
         else TRY(backward_sweep(h, h->full, depth, ng, debug, st));
+        h->last_depth = depth;
+        if (adaptive && !debug && h->lazy_clear) {
+            // the sweep cleared every pair it visited; the sources (level 0) are left
+            clear_source_sigma_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * lanes_per_batch, cnt, n,
+                                                                        h->sigma);
+            ++h->launches;
+            h->sigma_clean = true;
+        }
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
         launches_b += h->launches - l_bwd;
 
@@ -1871,6 +1890,7 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
     h->device = device;
     h->n = n;
     h->n_arcs = n_arcs;
+    h->last_depth = n_arcs < 6 * n ? 1 << 20 : 0;   // low average degree: expect a deep graph (see begin_batch)
     auto bail = [&](int rc) {
         g_create_error = h->err;
         bc_destroy(h);

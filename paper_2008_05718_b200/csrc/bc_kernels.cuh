@@ -41,6 +41,7 @@ namespace bcb200 {
 #ifndef BC_WPB
 #define BC_WPB 4
 #endif
+
 constexpr int kWarpsPerBlock = BC_WPB;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -306,9 +307,27 @@ __device__ __forceinline__ void finalize_forward(int64_t v, uint32_t seen, uint3
 // Backward: lanes in `mine` sit at this level; acc = sum of coef over their
 // DAG children.  delta = sigma * acc (backward.py:95-103 with the division
 // hoisted: (sigma_v / sigma_u)(1 + delta_u) = sigma_v * coef_u).
+// *ptr = 0 once `loaded` (the value just read from *ptr) has arrived.  A store issued while
+// the same thread's load of that address is still in flight stalls the memory pipe for the
+// whole round trip (measured: the backward sweep went from 18 ms to 51 ms with the store placed
+// right behind the load), so the zero is tied to the loaded value.
+__device__ __forceinline__ void clear_after_use(double *ptr, double loaded) {
+    double zero = 0.0;
+    asm volatile("" : "+d"(zero) : "d"(loaded));
+    *ptr = zero;
+}
+
+// `accumulate`: bit 0 = add delta into the BC partials, bit 1 = clear sigma.
+// This is the last read of sigma[v][lane] in a batch, so shallow-graph runs
+// clear it on the way out: the top-down push levels add path counts with
+// atomics and need zeros under every pair they discover, and clearing the
+// pairs a batch reached costs less than a memset of the whole array (5 GB per
+// batch on R-MAT scale 20) at the start of the next batch.  On deep graphs the
+// extra dirty sector per visit costs more than the memset, so the host leaves
+// bit 1 off there.
 template <bool STORE_DELTA>
 __device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, double acc, int lane,
-                                                  const double *sigma, double *coef,
+                                                  double *sigma, double *coef,
                                                   double *delta, double *bcg, int accumulate) {
     double contrib = 0.0;
     if ((mine >> lane) & 1u) {
@@ -318,8 +337,9 @@ __device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, doub
         coef[idx] = (1.0 + d) / sv;
         if (STORE_DELTA) delta[idx] = d;
         contrib = d;
+        if (!STORE_DELTA && (accumulate & 2)) clear_after_use(sigma + idx, sv);
     }
-    if (accumulate) {
+    if (accumulate & 1) {
         const double s = warp_sum(contrib);
         if (lane == 0) bcg[v] += s;
     }
@@ -528,6 +548,15 @@ __global__ void seed_sources_kernel(const int64_t *src, int batch_count, int64_t
     atomicOr(vis + g * n + v, 1u << lane);
     atomicOr(lvl0 + g * n + v, 1u << lane);
     sigma[(g * n + v) * 32 + lane] = 1.0;
+}
+
+// The sources sit at level 0, which the backward sweep does not visit: clear their
+// path counts separately (see finalize_backward).
+__global__ void clear_source_sigma_kernel(const int64_t *src, int batch_count, int64_t n, double *sigma) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch_count) return;
+    const size_t g = i >> 5;
+    sigma[(g * n + src[i]) * 32 + (i & 31)] = 0.0;
 }
 
 // bc[v] += sum over groups, in group order; the per-group partials are reset.
@@ -932,7 +961,7 @@ __global__ void compact_level_kernel(const uint32_t *__restrict__ lvl, const uin
 template <bool STORE_DELTA>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) bwd_queue_kernel(
     const int64_t *__restrict__ off, const int32_t *__restrict__ col, int64_t n, QueueParams q,
-    const uint32_t *nbr, const double *sigma, double *coef, double *delta, double *bcg,
+    const uint32_t *nbr, double *sigma, double *coef, double *delta, double *bcg,
     int accumulate) {
     const size_t g = blockIdx.y;
     const int lane = threadIdx.x & 31;
@@ -961,12 +990,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bwd_queue_kernel(
 template <bool STORE_DELTA>
 __global__ void bwd_queue_thin_kernel(const int64_t *__restrict__ off,
                                       const int32_t *__restrict__ col, int64_t n, QueueParams q,
-                                      const uint32_t *nbr, const double *sigma, double *coef,
+                                      const uint32_t *nbr, double *sigma, double *coef,
                                       double *delta, double *bcg, int accumulate) {
     const size_t g = blockIdx.y;
     const int64_t beg = q.q_beg[g], end = q.q_end[g];
     const uint32_t *gn = nbr ? nbr + g * n : nullptr;
-    const double *gsig = sigma + g * n * 32;
+    double *gsig = sigma + g * n * 32;
     double *gcoef = coef + g * n * 32;
     for (int64_t i = beg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -988,9 +1017,10 @@ __global__ void bwd_queue_thin_kernel(const int64_t *__restrict__ off,
             const double d = sv * acc;
             gcoef[idx] = (1.0 + d) / sv;
             if (STORE_DELTA) delta[g * n * 32 + idx] = d;
+            else if (accumulate & 2) clear_after_use(gsig + idx, sv);   // see finalize_backward
             total += d;
         }
-        if (accumulate) bcg[g * n + v] += total;
+        if (accumulate & 1) bcg[g * n + v] += total;
     }
 }
 
