@@ -913,25 +913,25 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         r0.queued = true;
         r0.qb.assign(ng, 0);
         r0.qe.assign(ng, 0);
+        // all groups' level-0 entries go up in two pitched copies (32 entries per group at most)
+        std::vector<int32_t> qv_all((size_t)ng * 32, 0);
+        std::vector<uint32_t> qm_all((size_t)ng * 32, 0);
         for (int g = 0; g < ng; ++g) {
             std::vector<std::pair<int32_t, uint32_t>> ent;
             for (int i = g * 32; i < std::min(cnt, g * 32 + 32); ++i)
                 ent.emplace_back((int32_t)batch_src[i], 1u << (i & 31));
             std::sort(ent.begin(), ent.end());
-            std::vector<int32_t> qv;
-            std::vector<uint32_t> qm;
+            int32_t *qv = qv_all.data() + (size_t)g * 32;
+            uint32_t *qm = qm_all.data() + (size_t)g * 32;
+            size_t len = 0;
             for (auto &e : ent) {
-                if (!qv.empty() && qv.back() == e.first) qm.back() |= e.second;
-                else qv.push_back(e.first), qm.push_back(e.second);
+                if (len > 0 && qv[len - 1] == e.first) qm[len - 1] |= e.second;
+                else qv[len] = e.first, qm[len] = e.second, ++len;
             }
-            CUDA_TRY(h, cudaMemcpyAsync(h->q_v + (size_t)g * h->q_cap, qv.data(),
-                                        qv.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-            CUDA_TRY(h, cudaMemcpyAsync(h->q_m + (size_t)g * h->q_cap, qm.data(),
-                                        qm.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-            r0.qe[g] = (int64_t)qv.size();
-            qcount[g] = qv.size();
-            r0.nverts += qv.size();
-            for (size_t qi = 0; qi < qv.size(); ++qi) {
+            r0.qe[g] = (int64_t)len;
+            qcount[g] = len;
+            r0.nverts += len;
+            for (size_t qi = 0; qi < len; ++qi) {
                 const int32_t v = qv[qi];
                 const unsigned long long d = (unsigned long long)(c_off_host[v + 1] - c_off_host[v]);
                 r0.farcs += d;
@@ -939,6 +939,21 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 if (d > (unsigned long long)kHeavyDeg)
                     for (int sl = 0; sl < (int)((d + kHeavySlice - 1) / kHeavySlice); ++sl)
                         heavy0.push_back(HeavyRec{(int64_t)qi, g, sl});
+            }
+        }
+        if ((size_t)h->q_cap * sizeof(int32_t) < ((size_t)1 << 31)) {
+            CUDA_TRY(h, cudaMemcpy2DAsync(h->q_v, (size_t)h->q_cap * sizeof(int32_t), qv_all.data(),
+                                          32 * sizeof(int32_t), 32 * sizeof(int32_t), (size_t)ng,
+                                          cudaMemcpyHostToDevice, st));
+            CUDA_TRY(h, cudaMemcpy2DAsync(h->q_m, (size_t)h->q_cap * sizeof(uint32_t), qm_all.data(),
+                                          32 * sizeof(uint32_t), 32 * sizeof(uint32_t), (size_t)ng,
+                                          cudaMemcpyHostToDevice, st));
+        } else {   // queue rows further apart than the largest pitch a 2-D copy takes
+            for (int g = 0; g < ng; ++g) {
+                CUDA_TRY(h, cudaMemcpyAsync(h->q_v + (size_t)g * h->q_cap, qv_all.data() + (size_t)g * 32,
+                                            32 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+                CUDA_TRY(h, cudaMemcpyAsync(h->q_m + (size_t)g * h->q_cap, qm_all.data() + (size_t)g * 32,
+                                            32 * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             }
         }
         CUDA_TRY(h, cudaMemcpyAsync(h->q_count, qcount.data(), G * sizeof(unsigned long long),
