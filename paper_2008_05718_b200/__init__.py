@@ -12,7 +12,7 @@ from .errors import (ContractViolation, DomainError, EngineError, FormatError, H
                      InputError, ParseError)
 from .graph import (Graph, as_graph, from_edge_arrays, from_edges, graph_stats, load_edge_list,
                     write_edge_list)
-from .partition import (BorderSet, Partition, block_partition, greedy_bipartition,
+from .partition import (BorderSet, Partition, block_partition, greedy_bipartition, grow_partition,
                         identify_borders, import_partition, single_partition, strip_partition)
 from .engine import (CommTotals, RunConfig, RunResult, build_report, pipeline_sources, run_bc,
                      select_sources)

@@ -23,7 +23,7 @@ import numpy as np
 from . import _capi
 from .errors import InputError
 from .graph import Graph, graph_stats
-from .partition import (BorderSet, Partition, block_partition, greedy_bipartition,
+from .partition import (BorderSet, Partition, block_partition, greedy_bipartition, grow_partition,
                         identify_borders, import_partition, single_partition)
 
 MODES = ("hybir", "bsp-baseline", "direct")
@@ -54,6 +54,8 @@ class RunConfig:
     # -- new -------------------------------------------------------------------
     num_partitions: int = 2            # the reference's fixed value
     partition: Partition | None = None  # explicit assignment (tests, grid strips)
+    partitioner: str = "auto"          # "auto": the reference's grower for 2 parts, id blocks above;
+                                       # "grow": k regions grown breadth-first (grow_partition); "block"
     num_gpus: int = 1
     gpu_mode: str = "source-sharded"
     device: int | None = None          # CUDA ordinal; default LOCAL_RANK or 0
@@ -70,6 +72,8 @@ class RunConfig:
             raise InputError("num_sources must be >= 1")
         if self.num_partitions < 1:
             raise InputError("num_partitions must be >= 1")
+        if self.partitioner not in ("auto", "grow", "block"):
+            raise InputError("unknown partitioner %r; pick from auto, grow, block" % self.partitioner)
         if self.gpu_mode not in GPU_MODES:
             raise InputError("unknown gpu_mode %r; pick from %s" % (self.gpu_mode, GPU_MODES))
         if self.max_threads is None and os.environ.get("HYBIR_THREADS"):
@@ -137,6 +141,10 @@ def make_partition(g: Graph, cfg: RunConfig) -> Partition:
         return single_partition(g)
     if cfg.partition_file is not None:
         return import_partition(cfg.partition_file, g, cfg.num_partitions)
+    if cfg.partitioner == "grow":
+        return grow_partition(g, cfg.num_partitions, seed=cfg.seed)
+    if cfg.partitioner == "block":
+        return block_partition(g, cfg.num_partitions)
     if cfg.num_partitions == 2:
         # 'auto' calibrates a CPU-vs-GPU speed ratio in the reference
         # (partition.py:157-190); identical B200 parts always balance at 0.5.

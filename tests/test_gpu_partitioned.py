@@ -194,3 +194,19 @@ def test_partition_errors():
         e.set_partition(2, [0, 0, 0, 0, 0, 0])             # degenerate: one side empty
         bc, _ = e.run([0, 5], MODE_HYBIR)
         assert np.allclose(bc, O.brandes_bc(g, [0, 5])[0])
+
+
+def test_grown_partitions_in_both_modes():
+    # k regions grown breadth-first on a road-like graph whose ids carry no locality
+    base = G.road_like(40, 40, keep=0.25, seed=9)
+    perm = np.random.default_rng(4).permutation(base.num_vertices)
+    keep = base.arc_src < base.arc_dst
+    g = P.from_edge_arrays(base.num_vertices, perm[base.arc_src[keep]], perm[base.arc_dst[keep]])
+    srcs = list(range(0, g.num_vertices, 37))
+    want, info = O.brandes_bc(g, srcs)
+    for k in (3, 5):
+        for mode in ("hybir", "bsp-baseline"):
+            res = P.run_bc(g, P.RunConfig(sources=srcs, mode=mode, num_partitions=k, partitioner="grow",
+                                          per_source_reports=False))
+            assert res.partition.num_parts == k
+            assert np.allclose(res.bc, want, rtol=RTOL, atol=ATOL), (k, mode)

@@ -198,3 +198,30 @@ def test_reference_acceptance_corpus_host_side():
         assert "".join(str(int(x)) for x in p.assignment) == rec["assignment"], rec["i"]
         bc, _ = O.brandes_bc(g, rec["sources"], threads=1)
         assert np.allclose(bc, rec["bc"], rtol=1e-9, atol=1e-12), rec["i"]
+
+
+def test_grow_partition_regions():
+    """k regions grown breadth-first: valid, near-balanced on connected
+    graphs, far fewer borders than id blocks once vertex ids carry no locality."""
+    from paper_2008_05718_b200.partition import grow_partition
+    g = G.road_like(64, 64, keep=0.2, seed=3)
+    perm = np.random.default_rng(1).permutation(g.num_vertices)
+    keep = g.arc_src < g.arc_dst
+    gp = P.from_edge_arrays(g.num_vertices, perm[g.arc_src[keep]], perm[g.arc_dst[keep]])
+    for k in (2, 3, 8):
+        p = grow_partition(gp, k, seed=0)
+        sizes = np.bincount(p.assignment, minlength=k)
+        assert p.num_parts == k and len(p.assignment) == gp.num_vertices
+        assert sizes.min() > 0 and sizes.max() <= 1.6 * gp.num_vertices / k
+        grown = sum(P.identify_borders(gp, p).counts())
+        blocks = sum(P.identify_borders(gp, P.block_partition(gp, k)).counts())
+        assert grown * 5 < blocks
+        assert np.array_equal(p.assignment, grow_partition(gp, k, seed=0).assignment)      # deterministic
+    # disconnected graph with isolated vertices: every vertex gets a part
+    h = P.from_edge_arrays(300, list(range(0, 99)) + list(range(150, 249)), list(range(1, 100)) + list(range(151, 250)))
+    for k in (2, 5):
+        a = grow_partition(h, k, seed=2).assignment
+        assert a.min() >= 0 and a.max() < k
+    assert make_partition(gp, P.RunConfig(num_partitions=4, partitioner="grow")).num_parts == 4
+    with pytest.raises(P.InputError):
+        P.RunConfig(partitioner="metis")
