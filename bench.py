@@ -59,6 +59,12 @@ def workload(name: str):
     elif name == "rmat16":
         g = G.rmat(16, 16, 1)
         label = "R-MAT scale-16 edge-factor-16 (smoke-size)"
+    elif name == "road2048":
+        g = G.road_like(2048, 2048, keep=0.2, seed=1)
+        label = "road-like 2048x2048 (random spanning tree of the grid + 20% of the other grid edges)"
+    elif name == "road512":
+        g = G.road_like(512, 512, keep=0.2, seed=1)
+        label = "road-like 512x512 (smoke-size)"
     elif name == "er22":
         g = G.erdos_renyi(1 << 22, 1 << 26, 1)
         label = "Erdos-Renyi n=2^22, 2^26 random pairs (avg degree 32)"
@@ -218,6 +224,63 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+    return 0
+
+
+def run_partitioned(args):
+    """--gpu-mode graph-partitioned: one part per rank, strong scaling (all ranks work on the same
+    sources).  Forward phase per --forward: hybir = border matrices (two all-reduces per batch),
+    bsp = one border exchange per level.  Not the default line; for the multi-GPU record runs."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2008_05718_b200 as P
+    from paper_2008_05718_b200.multigpu import init_process_group
+    from paper_2008_05718_b200.partitioned import PartitionedRunner
+
+    rank, world = init_process_group("nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    g, label = workload(args.workload)
+    n, m = g.num_vertices, g.num_edges
+    sources = pick_sources(n, args.sources)
+    if args.workload.startswith("road"):
+        side = int(args.workload[4:])
+        part = P.strip_partition(side, side, world)
+    elif args.partitioner == "grow":
+        part = P.grow_partition(g, world, seed=0)
+    else:
+        part = P.block_partition(g, world)
+    runner = PartitionedRunner(g, part, dev, args.groups or 4, args.forward)
+    for _ in range(args.warmup):
+        runner.run(sources)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        bc = runner.run(sources)
+    ev1.record()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    line = {
+        "metric": METRIC, "value": m * len(sources) * args.steps / (float(ms.item()) / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(ms.item()) / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "n": n, "m": m, "sources": len(sources), "mode": "graph-partitioned",
+                   "forward": args.forward, "borders": runner.border_counts, "levels": runner.levels,
+                   "forward_exchanges_per_step": runner.forward_exchanges / max(1, args.steps + args.warmup),
+                   "backward_exchanges_per_step": runner.backward_exchanges / max(1, args.steps + args.warmup),
+                   "exchanged_bytes_per_step": runner.exchanged_bytes / max(1, args.steps + args.warmup)},
+        "bc_sum": float(bc.sum().item()),
+    }
+    runner.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
     return 0
 
 
@@ -387,9 +450,15 @@ def main():
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--item-arcs", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--gpu-mode", default="source-sharded", choices=("source-sharded", "graph-partitioned"))
+    ap.add_argument("--forward", default="hybir", choices=("hybir", "bsp"),
+                    help="forward phase of the graph-partitioned mode")
+    ap.add_argument("--partitioner", default="block", choices=("block", "grow"))
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpu_mode == "graph-partitioned":
+        return run_partitioned(args)
     return run_ours(args)
 
 

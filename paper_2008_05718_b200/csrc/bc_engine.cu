@@ -213,6 +213,8 @@ struct bc_handle {
     uint32_t *vis = nullptr;
     std::vector<uint32_t *> lvl;
     double *sigma = nullptr, *coef = nullptr, *delta = nullptr;
+    uint8_t *cand = nullptr;    // [alloc_groups][n] candidate flags of the dense forward sweeps (deep graphs)
+    bool use_cand = false;      // set by forward_sweep for the launches of its levels
     bool sigma_clean = false;   // sigma is all zero (kept so by the backward sweeps of adaptive batches)
     bool lazy_clear = false;    // this batch's backward sweep clears sigma behind itself
     int last_depth = 0;         // levels of the previous batch (deep graphs: memset instead)
@@ -388,6 +390,8 @@ void free_state(bc_handle *h) {
     arena_free(h->range_table);
     arena_free(h->deep_log), arena_free(h->deep_info);
     arena_free(h->heavy);
+    arena_free(h->cand);
+    h->cand = nullptr;
     h->heavy = nullptr;
     h->heavy_cap = 0;
     h->deep_log = nullptr;
@@ -617,6 +621,7 @@ LevelParams level_params(bc_handle *h, const Csr &c) {
     p.pmask = h->pmask;
     p.counters = h->counters + h->cnt_off;
     p.wgt = c.wgt;
+    p.cand = nullptr;
     p.lvl_ptrs = h->d_lvl_ptrs;
     p.live_base = h->live;
     p.wmax = c.wgt ? h->wmax : 1;
@@ -696,6 +701,12 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     p.live_prev = h->live + (size_t)(L - 1) * h->alloc_groups;
     p.live_cur = h->live + (size_t)L * h->alloc_groups;
     p.level = L;
+    if (h->use_cand && c.wgt == nullptr) {
+        mark_candidates_kernel<<<dim3(grid1d((size_t)c.n, 256, 1184), ng), 256, 0, st>>>(
+            c.off, c.col, c.n, p.nbr, p.live_prev, h->cand);
+        ++h->launches;
+        p.cand = h->cand;
+    }
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     if (c.wgt != nullptr)
         level_kernel<false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -793,6 +804,17 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
     const size_t G = (size_t)h->alloc_groups;
     const size_t lvl_bytes = G * (size_t)h->n * sizeof(uint32_t);
     const int wmax = c.wgt ? h->wmax : 1;
+    // low average degree = deep graph: pull only at vertices next to the previous level
+    struct CandScope {
+        bc_handle *h;
+        ~CandScope() { h->use_cand = false; }
+    } cand_scope{h};
+    if (c.wgt == nullptr && h->n_arcs < 6 * h->n) {
+        const size_t bytes = (size_t)h->alloc_groups * (size_t)h->n;
+        if (h->cand == nullptr) CUDA_TRY(h, arena_malloc((void **)&h->cand, bytes));
+        CUDA_TRY(h, cudaMemsetAsync(h->cand, 0, bytes, st));
+        h->use_cand = true;
+    }
     for (;;) {
         TRY(ensure_levels(h, L + chunk));
         if (c.wgt) TRY(upload_level_ptrs(h, L + chunk, st));   // weighted levels probe lvl[L - wt]

@@ -87,6 +87,9 @@ struct LevelParams {
     unsigned long long *counters;  // [0] n_r, [1] A_r, [2] T
     unsigned long long *lstat;     // forward: [0] vertices discovered, [1] their arcs, [2] largest degree (may be null)
     int accumulate_bc;
+    // forward sweeps of low-degree (deep) graphs without frontier queues: only vertices with a
+    // neighbour in the previous level are scanned (mark_candidates_kernel); nullptr = scan all
+    uint8_t *cand;   // [group][v]
     // weighted graphs (positive integer arc weights, WEIGHTED kernels only): level = distance,
     // an arc of weight wt ties level L to level L - wt (forward) / L + wt (backward)
     const int32_t *wgt;                  // per arc, CSR order
@@ -403,6 +406,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
             b = p.off[v];
             e = p.off[v + 1];
             mine = BWD ? cur[v] : (~vis[v] & live);
+            if (!BWD && p.cand != nullptr) {
+                uint8_t *c = p.cand + g * p.n + v;
+                if (*c) *c = 0;      // consumed
+                else mine = 0;       // no neighbour in the previous level
+            }
             if (!BWD && (mine == 0 || b == e)) cur[v] = 0;  // nothing to discover here
         }
         unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || e > b));
@@ -519,6 +527,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) hub_kernel(const HubParam
                 atomicMax(p.lstat + 2, (unsigned long long)(p.off[v + 1] - p.off[v]));
             }
         }
+    }
+}
+
+// cand[g][w] = 1 for every neighbour w of a vertex in the previous level.  A dense pull level
+// scans the arcs of every vertex some lane has not reached; on a road network that is the whole
+// graph at each of thousands of levels.  With the candidates marked first (work proportional to
+// the frontier) the pull only scans vertices that can be discovered.  One thread per vertex.
+__global__ void mark_candidates_kernel(const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                       int64_t n, const uint32_t *__restrict__ prev,
+                                       const uint32_t *live_prev, uint8_t *cand) {
+    const size_t g = blockIdx.y;
+    if (live_prev[g] == 0) return;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        if (prev[g * n + v] == 0) continue;
+        for (int64_t a = off[v]; a < off[v + 1]; ++a) cand[g * n + __ldg(col + a)] = 1;
     }
 }
 
