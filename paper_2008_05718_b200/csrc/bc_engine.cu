@@ -2071,7 +2071,7 @@ int install_partition(bc_handle *h, int k, const int32_t *assignment, const Exte
     h->k = k;
     h->h_part.swap(part);
     assignment = h->h_part.data();
-    if (k == 1) return BC_OK;
+    if (k == 1 && ext == nullptr) return BC_OK;   // (a one-rank partitioned run keeps the empty border set-up)
     if ((int64_t)h->h_col.size() != h->n_arcs) {
         h->h_col.resize((size_t)h->n_arcs);
         if (h->n_arcs > 0)
