@@ -225,3 +225,24 @@ def test_grow_partition_regions():
     assert make_partition(gp, P.RunConfig(num_partitions=4, partitioner="grow")).num_parts == 4
     with pytest.raises(P.InputError):
         P.RunConfig(partitioner="metis")
+
+
+def test_bench_reference_arm_line_shape():
+    """`bench.py --impl reference` runs on the host cores only (the CPU oracle port) and prints the
+    contract's JSON line; smoke-size workload so the CPU suite stays fast."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--workload", "rmat16",
+                          "--sources", "32", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-500:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["metric"] == "bc_teps" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    for key in ("unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "config"):
+        assert key in line
