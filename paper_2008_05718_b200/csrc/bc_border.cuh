@@ -137,10 +137,14 @@ __global__ void cut_relax_kernel(BorderGeom geo, int S, const int32_t *Din, int3
 }
 
 // Step 3 / Step 5 (forward.py:91-96): one Jacobi pass of the min-plus closure
-// Dout[j] = min(Din[j], min_i Din[i] + bm[i][j]) inside each part.  Block =
-// 32 lanes x 8 j-rows, 4 borders j per thread; the i-loop is tiled through
-// shared memory so a bm tile is reused by 32 lanes and a D tile by 32 borders.
-constexpr int kTJ = 32;  // borders j per block
+// Dout[j] = min(Din[j], min_i Din[i] + bm[i][j]) inside each part -- a min-plus
+// "matrix product" b_p x b_p by b_p x S.  Block = 64 borders j x 64 lanes, every
+// thread owns a 4 x 4 register tile; the i-loop is tiled through shared memory
+// (two 128-bit loads feed 16 fused add-min instructions, VIADDMNMX via
+// __viaddmin_s32), so the kernel is bound by integer issue, not by shared-memory
+// bandwidth.  The bound: 148 SMs x 128 lanes x 1.9 GHz = 36 T min-plus / s.
+constexpr int kTJ = 64;  // borders j per block
+constexpr int kTL = 64;  // lanes per block
 constexpr int kTI = 32;  // borders i per shared-memory tile
 __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S,
                                                            const int32_t *Din, int32_t *Dout,
@@ -148,60 +152,86 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
                                                            const int32_t *lane_part,
                                                            const uint32_t *lane_active, int which,
                                                            uint32_t *lane_changed) {
-    __shared__ int32_t sD[kTI][32];
-    __shared__ int32_t sB[kTI][kTJ + 1];
+    __shared__ __align__(16) int32_t sD[kTI][kTL];
+    __shared__ __align__(16) int32_t sB[kTI][kTJ];
     const int p = blockIdx.z;
     const int b = geo.part_off[p + 1] - geo.part_off[p];
     const int j0 = blockIdx.x * kTJ;
     if (j0 >= b) return;
     const int base = geo.part_off[p];
     const int32_t *tab = bm + geo.tab_off[p];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    const int lane = blockIdx.y * 32 + tx;
-    int32_t best[4], old[4];
+    const int tl = threadIdx.x & 15, tj = threadIdx.x >> 4;   // 16 lane quads x 16 border quads
+    const int lane4 = blockIdx.y * kTL + 4 * tl;              // first of this thread's 4 lanes
+    const bool lanes_in = lane4 < S;                           // S is a multiple of 32: a quad is in or out
+    int32_t best[4][4], old[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int j = j0 + ty + 8 * r;
-        old[r] = j < b ? Din[(size_t)(base + j) * S + lane] : kInf;
-        best[r] = old[r];
+        const int j = j0 + 4 * tj + r;
+        int4 v = make_int4(kInf, kInf, kInf, kInf);
+        if (j < b && lanes_in) v = *reinterpret_cast<const int4 *>(Din + (size_t)(base + j) * S + lane4);
+        old[r][0] = best[r][0] = v.x;
+        old[r][1] = best[r][1] = v.y;
+        old[r][2] = best[r][2] = v.z;
+        old[r][3] = best[r][3] = v.w;
     }
     for (int i0 = 0; i0 < b; i0 += kTI) {
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int i = i0 + ty + 8 * r;
-            sD[ty + 8 * r][tx] = i < b ? Din[(size_t)(base + i) * S + lane] : kInf;
-            const int j = j0 + tx;
-            sB[ty + 8 * r][tx] = (i < b && j < b) ? tab[(size_t)i * b + j] : kInf;
+        for (int k = 0; k < 2; ++k) {                          // 32 x 16 int4 slots of sD
+            const int slot = threadIdx.x + 256 * k, row = slot >> 4, c4 = slot & 15;
+            const int i = i0 + row, l4 = blockIdx.y * kTL + 4 * c4;
+            int4 v = make_int4(kInf, kInf, kInf, kInf);
+            if (i < b && l4 < S) v = *reinterpret_cast<const int4 *>(Din + (size_t)(base + i) * S + l4);
+            *reinterpret_cast<int4 *>(&sD[row][4 * c4]) = v;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {                          // 32 x 64 entries of sB, coalesced along j
+            const int e = threadIdx.x + 256 * k, row = e >> 6, cj = e & 63;
+            const int i = i0 + row, j = j0 + cj;
+            sB[row][cj] = (i < b && j < b) ? tab[(size_t)i * b + j] : kInf;
         }
         __syncthreads();
-#pragma unroll 8
+#pragma unroll 4
         for (int i = 0; i < kTI; ++i) {
-            const int32_t di = sD[i][tx];
+            const int4 d = *reinterpret_cast<const int4 *>(&sD[i][4 * tl]);
+            const int4 t = *reinterpret_cast<const int4 *>(&sB[i][4 * tj]);
+            const int dd[4] = {d.x, d.y, d.z, d.w}, tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-            for (int r = 0; r < 4; ++r) best[r] = min(best[r], di + sB[i][ty + 8 * r]);
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int l = 0; l < 4; ++l) best[r][l] = __viaddmin_s32(dd[l], tt[r], best[r][l]);
         }
     }
-    const bool on = lane_active[lane] && applies(which, p, lane_part[lane]);
-    bool changed = false;
+    if (!lanes_in) return;
+    bool on[4], changed[4] = {false, false, false, false};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) on[l] = lane_active[lane4 + l] && applies(which, p, lane_part[lane4 + l]);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int j = j0 + ty + 8 * r;
+        const int j = j0 + 4 * tj + r;
         if (j >= b) continue;
-        const int32_t v = on ? min(best[r], kInf) : old[r];
-        Dout[(size_t)(base + j) * S + lane] = v;
-        changed |= v != old[r];
+        int32_t v[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            v[l] = on[l] ? min(best[r][l], kInf) : old[r][l];
+            changed[l] |= v[l] != old[r][l];
+        }
+        *reinterpret_cast<int4 *>(Dout + (size_t)(base + j) * S + lane4) = make_int4(v[0], v[1], v[2], v[3]);
     }
-    if (changed && lane_changed) lane_changed[lane] = 1u;
+    if (lane_changed)
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+            if (changed[l]) lane_changed[lane4 + l] = 1u;
 }
 
 // arr[j] = sum of sig[i] over incoming cut arcs (i -> j) that are tight
 // (forward.py:170-174), in arc order.
 __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const double *sig,
-                               double *arr) {
+                               double *arr, const uint32_t *lane_run) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)geo.B * S) return;
     const int j = (int)(idx / S), lane = (int)(idx % S);
+    if (!lane_run[lane]) return;   // this lane's counts settled in an earlier round
     const int32_t dj = D[idx];
     double a = 0.0;
     if (dj < kInf)
@@ -215,14 +245,16 @@ __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const do
 // sig[j] = (seed count if j is on the source side and its Step-1 distance is
 // still optimal) + sum over same-part borders c with arr[c] != 0 and
 // D[c] + bm[c][j] == D[j] of arr[c] * sm[c][j]   (forward.py:176-184).
+// Same 64 x 64 block / 4 x 4 register tiling as matrix_relax_kernel; the sum over c runs
+// in ascending c, so the result does not depend on the tiling.
 __global__ void __launch_bounds__(256) compose_sigma_kernel(
     BorderGeom geo, int S, const int32_t *D, const int32_t *seedD, const double *seedS,
     const double *arr, const int32_t *bm, const double *sm, const int32_t *lane_part,
-    double *sig, uint32_t *changed_flag) {
-    __shared__ int32_t sD[kTI][32];
-    __shared__ double sA[kTI][32];
-    __shared__ int32_t sB[kTI][kTJ + 1];
-    __shared__ double sS[kTI][kTJ + 1];
+    double *sig, const uint32_t *lane_run, uint32_t *lane_changed) {
+    __shared__ __align__(16) int32_t sD[kTI][kTL];
+    __shared__ __align__(16) double sA[kTI][kTL];
+    __shared__ __align__(16) int32_t sB[kTI][kTJ];
+    __shared__ __align__(16) double sS[kTI][kTJ];
     const int p = blockIdx.z;
     const int b = geo.part_off[p + 1] - geo.part_off[p];
     const int j0 = blockIdx.x * kTJ;
@@ -230,57 +262,89 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
     const int base = geo.part_off[p];
     const int32_t *tbm = bm + geo.tab_off[p];
     const double *tsm = sm + geo.tab_off[p];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int lane = blockIdx.y * 32 + tx;
-    int32_t dj[4];
-    double acc[4];
+    const int tl = threadIdx.x & 15, tj = threadIdx.x >> 4;
+    const int lane4 = blockIdx.y * kTL + 4 * tl;
+    const bool lanes_in = lane4 < S;
+    // lanes are independent: one whose counts did not change in a round is final, and a block
+    // whose 64 lanes are all final has nothing left to do (the rounds a lane needs = the number
+    // of part crossings on its shortest paths, which differs from source to source)
+    bool run[4] = {false, false, false, false};
+    if (lanes_in)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) run[l] = lane_run[lane4 + l] != 0;
+    if (!__syncthreads_or(run[0] || run[1] || run[2] || run[3])) return;
+    int32_t dj[4][4];
+    double acc[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int j = j0 + ty + 8 * r;
-        dj[r] = kInf;
-        acc[r] = 0.0;
-        if (j < b) {
-            const size_t at = (size_t)(base + j) * S + lane;
-            dj[r] = D[at];
-            if (dj[r] < kInf && p == lane_part[lane] && seedD[at] == dj[r]) acc[r] = seedS[at];
+        const int j = j0 + 4 * tj + r;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            dj[r][l] = kInf;
+            acc[r][l] = 0.0;
+            if (j < b && lanes_in) {
+                const size_t at = (size_t)(base + j) * S + lane4 + l;
+                dj[r][l] = D[at];
+                if (dj[r][l] < kInf && p == lane_part[lane4 + l] && seedD[at] == dj[r][l]) acc[r][l] = seedS[at];
+            }
         }
     }
     for (int i0 = 0; i0 < b; i0 += kTI) {
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int i = i0 + ty + 8 * r;
+        for (int k = 0; k < 8; ++k) {
+            const int e = threadIdx.x + 256 * k, row = e >> 6, c = e & 63;
+            const int i = i0 + row, lane = blockIdx.y * kTL + c, j = j0 + c;
+            const bool lin = i < b && lane < S;
             const size_t at = (size_t)(base + i) * S + lane;
-            sD[ty + 8 * r][tx] = i < b ? D[at] : kInf;
-            sA[ty + 8 * r][tx] = i < b ? arr[at] : 0.0;
-            const int j = j0 + tx;
+            sD[row][c] = lin ? D[at] : kInf;
+            sA[row][c] = lin ? arr[at] : 0.0;
             const bool in = i < b && j < b;
-            sB[ty + 8 * r][tx] = in ? tbm[(size_t)i * b + j] : kInf;
-            sS[ty + 8 * r][tx] = in ? tsm[(size_t)i * b + j] : 0.0;
+            sB[row][c] = in ? tbm[(size_t)i * b + j] : kInf;
+            sS[row][c] = in ? tsm[(size_t)i * b + j] : 0.0;
         }
         __syncthreads();
         for (int i = 0; i < kTI; ++i) {
-            const double a = sA[i][tx];
-            if (a == 0.0) continue;
-            const int32_t dc = sD[i][tx];
+            const double a[4] = {sA[i][4 * tl], sA[i][4 * tl + 1], sA[i][4 * tl + 2], sA[i][4 * tl + 3]};
+            if (a[0] == 0.0 && a[1] == 0.0 && a[2] == 0.0 && a[3] == 0.0) continue;
+            const int4 d = *reinterpret_cast<const int4 *>(&sD[i][4 * tl]);
+            const int4 t = *reinterpret_cast<const int4 *>(&sB[i][4 * tj]);
+            const int dd[4] = {d.x, d.y, d.z, d.w}, tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (dc + sB[i][ty + 8 * r] == dj[r]) acc[r] += a * sS[i][ty + 8 * r];
+            for (int r = 0; r < 4; ++r) {
+                const double sv = sS[i][4 * tj + r];
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    if (a[l] != 0.0 && dd[l] + tt[r] == dj[r][l]) acc[r][l] += a[l] * sv;
+            }
         }
     }
-    bool changed = false;
+    if (!lanes_in) return;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const int j = j0 + ty + 8 * r;
+        const int j = j0 + 4 * tj + r;
         if (j >= b) continue;
-        const size_t at = (size_t)(base + j) * S + lane;
-        const double v = dj[r] < kInf ? acc[r] : 0.0;
-        if (sig[at] != v) {
-            sig[at] = v;
-            changed = true;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            if (!run[l]) continue;
+            const size_t at = (size_t)(base + j) * S + lane4 + l;
+            const double v = dj[r][l] < kInf ? acc[r][l] : 0.0;
+            if (sig[at] != v) {
+                sig[at] = v;
+                lane_changed[lane4 + l] = 1u;
+            }
         }
     }
-    if (changed) *changed_flag = 1u;
+}
+
+// End of a composition round: lanes that changed run again.
+__global__ void lane_round_kernel(int S, uint32_t *lane_run, uint32_t *lane_changed, uint32_t *any_running) {
+    const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+    if (lane >= S) return;
+    const uint32_t c = lane_changed[lane];
+    lane_run[lane] = c;
+    lane_changed[lane] = 0;
+    if (c) *any_running = 1u;
 }
 
 // Per-lane bookkeeping of the refinement loop (forward.py:113-135).
@@ -290,19 +354,22 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
 __global__ void lane_enter_kernel(BorderGeom geo, int S, int lanes, const int32_t *D,
                                   const int32_t *lane_part, uint32_t *lane_active,
                                   uint32_t *lane_entered, int64_t n_cut) {
-    const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = blockIdx.x;   // one block per lane, threads stride over the part's borders
     if (lane >= S) return;
-    uint32_t on = 0;
+    int found = 0;
     if (lane < lanes && n_cut > 0) {
         const int p = lane_part[lane];
-        for (int j = geo.part_off[p]; j < geo.part_off[p + 1]; ++j)
+        for (int j = geo.part_off[p] + threadIdx.x; j < geo.part_off[p + 1]; j += blockDim.x)
             if (D[(size_t)j * S + lane] < kInf) {
-                on = 1;
+                found = 1;
                 break;
             }
     }
-    lane_active[lane] = on;
-    lane_entered[lane] = on;
+    const uint32_t on = __syncthreads_or(found) ? 1u : 0u;
+    if (threadIdx.x == 0) {
+        lane_active[lane] = on;
+        lane_entered[lane] = on;
+    }
 }
 
 __global__ void lane_step_kernel(int S, uint32_t *lane_active, uint32_t *lane_changed,

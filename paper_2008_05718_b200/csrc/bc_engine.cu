@@ -1351,12 +1351,12 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
     int max_b = 0;
     for (int p = 0; p < h->k; ++p) max_b = std::max(max_b, h->h_part_off[p + 1] - h->h_part_off[p]);
     (void)ng;
-    const dim3 mgrid((max_b + kTJ - 1) / kTJ, S / 32, h->k);  // every allocated lane is kept defined
+    const dim3 mgrid((max_b + kTJ - 1) / kTJ, (S + kTL - 1) / kTL, h->k);  // every allocated lane is kept defined
 
     CUDA_TRY(h, cudaMemcpyAsync(h->D, h->seedD, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     CUDA_TRY(h, cudaMemsetAsync(h->lane_iters, 0, S * sizeof(int32_t), st));
     CUDA_TRY(h, cudaMemsetAsync(h->lane_changed, 0, S * sizeof(uint32_t), st));
-    lane_enter_kernel<<<gl, 128, 0, st>>>(geo, S, lanes, h->D, h->lane_part, h->lane_active,
+    lane_enter_kernel<<<S, 128, 0, st>>>(geo, S, lanes, h->D, h->lane_part, h->lane_active,
                                           h->lane_entered, h->n_cut);
     ++h->launches;
     if (h->B > 0 && h->n_cut > 0) {
@@ -1405,15 +1405,20 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
     // path counts at the borders: Jacobi rounds until nothing changes
     CUDA_TRY(h, cudaMemsetAsync(h->sig, 0, cnt * sizeof(double), st));
     if (h->B > 0) {
+        // every lane runs the first round; afterwards only those whose counts changed
+        CUDA_TRY(h, cudaMemsetAsync(h->lane_active, 1, S * sizeof(uint32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lane_changed, 0, S * sizeof(uint32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->arr, 0, cnt * sizeof(double), st));
         for (int round = 0;; ++round) {
             if (round > 2 * h->B + 4)
                 return h->fail(BC_ERR_INTERNAL, "border sigma composition did not settle");
-            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr);
+            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->lane_active);
             CUDA_TRY(h, cudaMemsetAsync(h->dflags + 1, 0, sizeof(uint32_t), st));
             compose_sigma_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->seedD, h->seedS, h->arr,
                                                         h->bm, h->sm, h->lane_part, h->sig,
-                                                        h->dflags + 1);
-            h->launches += 2;
+                                                        h->lane_active, h->lane_changed);
+            lane_round_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->dflags + 1);
+            h->launches += 3;
             uint32_t changed = 0;
             CUDA_TRY(h, cudaMemcpyAsync(&changed, h->dflags + 1, sizeof changed,
                                         cudaMemcpyDeviceToHost, st));
