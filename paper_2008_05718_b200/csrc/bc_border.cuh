@@ -226,12 +226,16 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
 
 // arr[j] = sum of sig[i] over incoming cut arcs (i -> j) that are tight
 // (forward.py:170-174), in arc order.
+// darr[j] = what the round adds to arr[j]: the composition only has to push the change on.
 __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const double *sig,
-                               double *arr, const uint32_t *lane_run) {
+                               double *arr, double *darr, const uint32_t *lane_run) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)geo.B * S) return;
     const int j = (int)(idx / S), lane = (int)(idx % S);
-    if (!lane_run[lane]) return;   // this lane's counts settled in an earlier round
+    if (!lane_run[lane]) {         // this lane's counts settled in an earlier round
+        darr[idx] = 0.0;
+        return;
+    }
     const int32_t dj = D[idx];
     double a = 0.0;
     if (dj < kInf)
@@ -239,18 +243,23 @@ __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const do
             const size_t at = (size_t)geo.cin_src[c] * S + lane;
             if (D[at] + geo.cin_w[c] == dj) a += sig[at];
         }
+    darr[idx] = a - arr[idx];
     arr[idx] = a;
 }
 
 // sig[j] = (seed count if j is on the source side and its Step-1 distance is
 // still optimal) + sum over same-part borders c with arr[c] != 0 and
 // D[c] + bm[c][j] == D[j] of arr[c] * sm[c][j]   (forward.py:176-184).
-// Same 64 x 64 block / 4 x 4 register tiling as matrix_relax_kernel; the sum over c runs
-// in ascending c, so the result does not depend on the tiling.
+// Same 64 x 64 block / 4 x 4 register tiling as matrix_relax_kernel.  Delta form: the tight
+// (c, j) structure is fixed once the distances are refined, so a round adds
+// sum_c darr[c] * sm[c][j] to sig[j], where darr is what the round changed in the arrival
+// counts; rows c whose four lanes did not change are skipped, which makes the later rounds
+// cheap (each border's arrival count changes in one or two rounds).  Path counts are
+// integer-valued, so the sum is exact in any order below 2^53.
 __global__ void __launch_bounds__(256) compose_sigma_kernel(
     BorderGeom geo, int S, const int32_t *D, const int32_t *seedD, const double *seedS,
-    const double *arr, const int32_t *bm, const double *sm, const int32_t *lane_part,
-    double *sig, const uint32_t *lane_run, uint32_t *lane_changed) {
+    const double *darr, const int32_t *bm, const double *sm, const int32_t *lane_part,
+    double *sig, const uint32_t *lane_run, uint32_t *lane_changed, int first_round) {
     __shared__ __align__(16) int32_t sD[kTI][kTL];
     __shared__ __align__(16) double sA[kTI][kTL];
     __shared__ __align__(16) int32_t sB[kTI][kTJ];
@@ -285,7 +294,8 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
             if (j < b && lanes_in) {
                 const size_t at = (size_t)(base + j) * S + lane4 + l;
                 dj[r][l] = D[at];
-                if (dj[r][l] < kInf && p == lane_part[lane4 + l] && seedD[at] == dj[r][l]) acc[r][l] = seedS[at];
+                if (first_round && dj[r][l] < kInf && p == lane_part[lane4 + l] && seedD[at] == dj[r][l])
+                    acc[r][l] = seedS[at];
             }
         }
     }
@@ -298,7 +308,7 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
             const bool lin = i < b && lane < S;
             const size_t at = (size_t)(base + i) * S + lane;
             sD[row][c] = lin ? D[at] : kInf;
-            sA[row][c] = lin ? arr[at] : 0.0;
+            sA[row][c] = lin ? darr[at] : 0.0;
             const bool in = i < b && j < b;
             sB[row][c] = in ? tbm[(size_t)i * b + j] : kInf;
             sS[row][c] = in ? tsm[(size_t)i * b + j] : 0.0;
@@ -326,13 +336,9 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
         if (j >= b) continue;
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            if (!run[l]) continue;
-            const size_t at = (size_t)(base + j) * S + lane4 + l;
-            const double v = dj[r][l] < kInf ? acc[r][l] : 0.0;
-            if (sig[at] != v) {
-                sig[at] = v;
-                lane_changed[lane4 + l] = 1u;
-            }
+            if (!run[l] || acc[r][l] == 0.0 || dj[r][l] >= kInf) continue;
+            sig[(size_t)(base + j) * S + lane4 + l] += acc[r][l];
+            lane_changed[lane4 + l] = 1u;
         }
     }
 }

@@ -195,7 +195,7 @@ struct bc_handle {
     // per-batch border state, [B][S]
     int border_S = 0;
     int32_t *D = nullptr, *D2 = nullptr, *seedD = nullptr, *Dfin = nullptr;
-    double *seedS = nullptr, *sig = nullptr, *arr = nullptr;
+    double *seedS = nullptr, *sig = nullptr, *arr = nullptr, *darr = nullptr;
     int32_t *lane_part = nullptr, *lane_iters = nullptr;
     uint32_t *lane_active = nullptr, *lane_entered = nullptr, *lane_changed = nullptr;
     uint32_t *dflags = nullptr;    // [0] any lane active, [1] sigma changed
@@ -413,7 +413,8 @@ void free_state(bc_handle *h) {
 
 void free_border_state(bc_handle *h) {
     arena_free(h->D), arena_free(h->D2), arena_free(h->seedD), arena_free(h->Dfin);
-    arena_free(h->seedS), arena_free(h->sig), arena_free(h->arr);
+    arena_free(h->seedS), arena_free(h->sig), arena_free(h->arr), arena_free(h->darr);
+    h->darr = nullptr;
     arena_free(h->lane_part), arena_free(h->lane_iters), arena_free(h->lane_active);
     arena_free(h->lane_entered), arena_free(h->lane_changed);
     arena_free(h->sync_flag), arena_free(h->sync_bits), arena_free(h->lane_sync), arena_free(h->lane_bytes);
@@ -1326,6 +1327,7 @@ int ensure_border_state(bc_handle *h, int S) {
     TRY(dev_alloc(h, &h->seedS, cnt));
     TRY(dev_alloc(h, &h->sig, cnt));
     TRY(dev_alloc(h, &h->arr, cnt));
+    TRY(dev_alloc(h, &h->darr, cnt));
     TRY(dev_alloc(h, &h->sync_flag, cnt));
     TRY(dev_alloc(h, &h->lane_part, (size_t)S));
     TRY(dev_alloc(h, &h->lane_iters, (size_t)S));
@@ -1412,11 +1414,11 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
         for (int round = 0;; ++round) {
             if (round > 2 * h->B + 4)
                 return h->fail(BC_ERR_INTERNAL, "border sigma composition did not settle");
-            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->lane_active);
+            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->darr, h->lane_active);
             CUDA_TRY(h, cudaMemsetAsync(h->dflags + 1, 0, sizeof(uint32_t), st));
-            compose_sigma_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->seedD, h->seedS, h->arr,
+            compose_sigma_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->seedD, h->seedS, h->darr,
                                                         h->bm, h->sm, h->lane_part, h->sig,
-                                                        h->lane_active, h->lane_changed);
+                                                        h->lane_active, h->lane_changed, round == 0);
             lane_round_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->dflags + 1);
             h->launches += 3;
             uint32_t changed = 0;
