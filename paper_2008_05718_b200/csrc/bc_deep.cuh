@@ -19,11 +19,148 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "bc_border.cuh"
 #include "bc_kernels.cuh"
 
 namespace bcb200 {
 
 namespace cg = cooperative_groups;
+
+// ---- Step-6 seeds on queue levels --------------------------------------------------------
+// Step 6 of the partitioned forward phase (forward.py:232-246) relaxes every part from its
+// borders at once: border j joins lane l's traversal at its refined distance D[j][l] with the
+// arrival count arr[j][l] (paths whose last arc is a cut arc) as base path count.  On queue
+// levels a seed is one more push into the level being produced: add the base count, set the
+// lane in next[], append the vertex when nobody else has yet.  The (border, lane) pairs are
+// sorted by level once per batch (seed_key_kernel + radix sort + seed_offsets_kernel).
+struct SeedPlan {
+    const int32_t *idx;        // border * S + lane, sorted by level (nullptr: no seeds)
+    const int64_t *off;        // [levels + 1] first seed of each level
+    int levels;                // seeds sit at levels [0, levels)
+    const double *arr;         // [B][S] arrival counts
+    const int32_t *border_v;   // [B] vertex of each border
+    int S;
+};
+
+__device__ __forceinline__ void inject_seed_entry(const SeedPlan &sp, int64_t s, int64_t n,
+                                                  const QueueParams &q, const uint32_t *vis,
+                                                  uint32_t *next, double *sigma) {
+    const int32_t idx = sp.idx[s];
+    const int j = idx / sp.S, lane_all = idx % sp.S;
+    const size_t g = (size_t)(lane_all >> 5);
+    const int lane = lane_all & 31;
+    const uint32_t bit = 1u << lane;
+    const int64_t v = sp.border_v[j];
+    if (vis[g * n + v] & bit) return;   // cannot happen while D is the exact distance
+    atomicAdd(sigma + (g * n + v) * 32 + lane, sp.arr[idx]);
+    const uint32_t old = atomicOr(next + g * n + v, bit);
+    if (old == 0) {
+        const unsigned long long pos = atomicAdd(q.q_count + g, 1ull);
+        q.q_v[g * q.cap + pos] = (int32_t)v;
+    }
+}
+
+// Seeds of one level, between the push kernels and push_post_kernel of that level.
+__global__ void inject_seeds_queue_kernel(SeedPlan sp, int level, int64_t n, QueueParams q,
+                                          const uint32_t *vis, uint32_t *next, double *sigma) {
+    if (level >= sp.levels) return;
+    const int64_t e = sp.off[level + 1];
+    for (int64_t s = sp.off[level] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < e;
+         s += (int64_t)gridDim.x * blockDim.x)
+        inject_seed_entry(sp, s, n, q, vis, next, sigma);
+}
+
+// Sort key of every (border, lane) pair: its level when it is a Step-6 seed (finite distance,
+// non-zero arrival count, lane in use), INT32_MAX otherwise.
+__global__ void seed_key_kernel(int B, int S, int lanes, const int32_t *D, const double *arr,
+                                int32_t *keys, int32_t *vals) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * S) return;
+    const bool seed = (int)(idx % S) < lanes && D[idx] < kInf && arr[idx] != 0.0;
+    keys[idx] = seed ? D[idx] : 0x7fffffff;
+    vals[idx] = (int32_t)idx;
+}
+
+// off[L] = first sorted pair whose level is >= L, L = 0 .. levels.
+__global__ void seed_offsets_kernel(const int32_t *keys, int64_t count, int levels, int64_t *off) {
+    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    if (L > levels) return;
+    int64_t lo = 0, hi = count;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < L) lo = mid + 1;
+        else hi = mid;
+    }
+    off[L] = lo;
+}
+
+// Level of queue entry i of group g: levels own consecutive entry ranges, level_end[L][g] is one
+// past the last entry of level L.
+__device__ __forceinline__ int level_of_entry(const int64_t *level_end, int depth, int G, size_t g,
+                                              int64_t i) {
+    int lo = 0, hi = depth - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (level_end[(size_t)mid * G + g] > i) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// (dist, sigma) of the border vertices out of a queue-level sweep (border_gather_kernel for the
+// dense level rows): one thread per queue entry, D_out / S_out pre-filled with kInf / 0.
+__global__ void border_gather_queue_kernel(QueueParams q, const int64_t *level_end, int depth, int G,
+                                           int64_t n, const int32_t *border_index,
+                                           const double *sigma, int S, int32_t *D_out,
+                                           double *S_out) {
+    const size_t g = blockIdx.y;
+    const int64_t end = (int64_t)q.q_count[g];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = q.q_v[g * q.cap + i];
+        const int j = border_index[v];
+        if (j < 0) continue;
+        uint32_t m = q.q_m[g * q.cap + i];
+        const int level = level_of_entry(level_end, depth, G, g, i);
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            const size_t at = (size_t)j * S + g * 32 + bit;
+            D_out[at] = level;
+            S_out[at] = sigma[(g * n + v) * 32 + bit];
+        }
+    }
+}
+
+// Border-table rows out of a queue-level sweep whose lanes are borders first .. first+count-1
+// (border_table_kernel for the dense level rows); bm / sm pre-filled with kInf / 0.
+__global__ void border_table_queue_kernel(QueueParams q, const int64_t *level_end, int depth, int G,
+                                          int64_t n, const int32_t *border_index,
+                                          const double *sigma, BorderGeom geo, int first, int count,
+                                          int32_t *bm, double *sm) {
+    const size_t g = blockIdx.y;
+    const int64_t end = (int64_t)q.q_count[g];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < end;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = q.q_v[g * q.cap + e];
+        const int j = border_index[v];
+        if (j < 0) continue;
+        uint32_t m = q.q_m[g * q.cap + e];
+        const int level = level_of_entry(level_end, depth, G, g, e);
+        const int p = geo.border_p[j];
+        const int b = geo.part_off[p + 1] - geo.part_off[p];
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            const int lane_all = (int)g * 32 + bit;
+            if (lane_all >= count) continue;
+            const int i = first + lane_all;   // from-border (the lane's source), same part as j
+            const size_t at = (size_t)geo.tab_off[p] + (size_t)(i - geo.part_off[p]) * b + (j - geo.part_off[p]);
+            bm[at] = level;
+            sm[at] = sigma[(g * n + v) * 32 + bit];
+        }
+    }
+}
 
 constexpr int kDeepThreads = 256;
 constexpr int kDeepWarps = kDeepThreads / 32;
@@ -50,6 +187,8 @@ struct DeepFwdParams {
     unsigned long long push_beta;
     unsigned long long thin_degree;
     unsigned long long max_degree;
+    SeedPlan seeds;              // Step-6 border seeds joining at their own level (idx == nullptr: none)
+    unsigned long long seed_room;   // queue entries the seeds of one level may add per group
 };
 
 // Forward: consecutive top-down levels, one THREAD per frontier entry.
@@ -141,6 +280,12 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
             const unsigned t = __reduce_add_sync(kFull, c_t);
             if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
         }
+        // border seeds of level L: more pushes into the same level (atomics on sigma / next)
+        if (p.seeds.idx != nullptr && L < p.seeds.levels) {
+            const int64_t se = p.seeds.off[L + 1];
+            for (int64_t s = p.seeds.off[L] + gtid; s < se; s += gthreads)
+                inject_seed_entry(p.seeds, s, n, p.q, p.vis, p.next, p.sigma);
+        }
         grid.sync();
 
         // ---- phase 2: the entries appended above become level L (same flattening)
@@ -219,7 +364,7 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
             __syncthreads();
             if (g == 0) {
                 p.lstat[0] = p.lstat[1] = p.lstat[2] = 0;
-                const unsigned long long room = min((unsigned long long)n, farcs) + 1;
+                const unsigned long long room = min((unsigned long long)n, farcs) + 1 + p.seed_room;
                 const bool go = alive_any != 0 && it + 1 < p.max_levels &&
                                 farcs * p.push_beta <= p.graph_arcs && maxdeg <= p.max_degree &&
                                 farcs <= p.thin_degree * nverts &&

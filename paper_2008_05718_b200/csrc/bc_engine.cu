@@ -12,6 +12,7 @@
 #include "bc_dist.cuh"
 #include "bc_kernels.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -181,6 +182,16 @@ struct bc_handle {
     std::vector<int32_t> h_part;
     int32_t *d_part = nullptr;
     Csr intra;                     // cut arcs removed
+    std::vector<int64_t> h_ioff;   // host copy of its offsets (queue sweeps inside the parts)
+    int64_t intra_maxdeg = 0;      // largest degree inside a part
+    int32_t *d_border_index = nullptr;   // [n] border number of a vertex, -1 for inner vertices
+    int hybir_queues = 1;          // partitioned sweeps of low-degree graphs on frontier queues
+    // Step-6 seeds sorted by level (queue sweeps)
+    int32_t *seed_keys = nullptr, *seed_keys2 = nullptr, *seed_vals = nullptr, *seed_vals2 = nullptr;
+    int64_t *seed_off = nullptr;
+    int64_t seed_off_cap = 0;
+    void *seed_tmp = nullptr;
+    size_t seed_tmp_bytes = 0;
     int B = 0;                     // borders over all parts
     int64_t n_cut = 0;
     std::vector<int32_t> h_border_v, h_border_p, h_part_off;
@@ -415,6 +426,11 @@ void free_border_state(bc_handle *h) {
     arena_free(h->D), arena_free(h->D2), arena_free(h->seedD), arena_free(h->Dfin);
     arena_free(h->seedS), arena_free(h->sig), arena_free(h->arr), arena_free(h->darr);
     h->darr = nullptr;
+    arena_free(h->seed_keys), arena_free(h->seed_keys2), arena_free(h->seed_vals), arena_free(h->seed_vals2);
+    arena_free(h->seed_off), arena_free(h->seed_tmp);
+    h->seed_keys = h->seed_keys2 = h->seed_vals = h->seed_vals2 = nullptr;
+    h->seed_off = nullptr, h->seed_tmp = nullptr;
+    h->seed_off_cap = 0, h->seed_tmp_bytes = 0;
     arena_free(h->lane_part), arena_free(h->lane_iters), arena_free(h->lane_active);
     arena_free(h->lane_entered), arena_free(h->lane_changed);
     arena_free(h->sync_flag), arena_free(h->sync_bits), arena_free(h->lane_sync), arena_free(h->lane_bytes);
@@ -433,6 +449,10 @@ void free_partition(bc_handle *h) {
     arena_free(h->d_cin_src), arena_free(h->d_tab_off), arena_free(h->d_cin_off), arena_free(h->d_cin_w);
     h->d_cin_w = nullptr;
     arena_free(h->bm), arena_free(h->sm);
+    arena_free(h->d_border_index);
+    h->d_border_index = nullptr;
+    h->h_ioff.clear();
+    h->intra_maxdeg = 0;
     h->d_part = h->d_border_v = h->d_border_p = h->d_part_off = h->d_cin_src = nullptr;
     h->d_tab_off = h->d_cin_off = nullptr;
     h->bm = nullptr;
@@ -563,7 +583,7 @@ int ensure_deep(bc_handle *h) {
 // by doubling up to 33n.
 int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
                 const std::vector<unsigned long long> &used) {
-    const int64_t max_cap = 33 * h->n + 1024;
+    const int64_t max_cap = 33 * h->n + 1024 + h->B;
     if (h->q_cap >= max_cap || need_cap <= h->q_cap) return BC_OK;
     const int64_t cap = std::min(max_cap, std::max(need_cap, 2 * h->q_cap));
     const size_t G = (size_t)h->alloc_groups;
@@ -919,12 +939,19 @@ int scatter_level(bc_handle *h, const LevelRep &r, uint32_t *dense, bool clear, 
 // per level (the choice needs the frontier's arc count): a single small read
 // of the level report that advance_level_kernel publishes.  Queue ranges stay
 // on the device between consecutive push levels.
+// `off_host`: host copy of c's offsets (default: the full graph).  `force_push`: every level is a
+// queue level (the partitioned sweeps of low-degree graphs; the caller has checked that no
+// vertex of c is heavy).  `seeds`: Step-6 border seeds joining the queue levels at their own
+// level (needs force_push).
 int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t *batch_src,
-                     cudaStream_t st, int *depth_out, std::vector<LevelRep> &reps) {
+                     cudaStream_t st, int *depth_out, std::vector<LevelRep> &reps,
+                     const std::vector<int64_t> *off_host = nullptr, bool force_push = false,
+                     const SeedPlan *seeds = nullptr) {
     const size_t G = (size_t)h->alloc_groups;
     const int64_t n = h->n;
     TRY(ensure_queues(h));
-    const std::vector<int64_t> &c_off_host = h->h_off;   // adaptive sweeps run on the full graph only
+    const std::vector<int64_t> &c_off_host = off_host ? *off_host : h->h_off;
+    const int64_t seed_room = seeds ? (int64_t)h->B : 0;
     reps.clear();
     reps.emplace_back();
     // level 0: the sources, as a dense array (begin_batch) and as a queue
@@ -1008,17 +1035,20 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         int64_t used = 0;
         for (int g = 0; g < ng; ++g) used = std::max<int64_t>(used, (int64_t)qcount[g]);
         const int64_t want_room = (int64_t)std::min<unsigned long long>((unsigned long long)n, prev.farcs) +
-                                  (prev.queued ? 0 : (int64_t)prev.nverts) + 1;
+                                  (prev.queued ? 0 : (int64_t)prev.nverts) + 1 + seed_room;
         // a queue entry is walked by one warp: keep vertices with very long adjacencies on the
         // dense kernels, which slice them
         // entries above kHeavyDeg arcs are pushed slice by slice from the heavy records of the
         // level (a level that came out of a persistent run has none: pull from it instead)
         const unsigned long long beta = (unsigned long long)(pulled ? h->push_beta_late : h->push_beta);
-        bool push = prev.farcs * beta <= graph_arcs &&
-                    (prev.maxdeg <= (unsigned long long)kHeavyDeg || prev.heavy >= 0 || !prev.queued);
+        bool push = force_push ||
+                    (prev.farcs * beta <= graph_arcs &&
+                     (prev.maxdeg <= (unsigned long long)kHeavyDeg || prev.heavy >= 0 || !prev.queued));
         if (push && h->q_cap - used < want_room) {
             TRY(grow_queues(h, used + want_room, st, qcount));
             push = h->q_cap - used >= want_room;
+            if (!push && force_push)
+                return h->fail(BC_ERR_INTERNAL, "frontier queues of a partitioned sweep cannot grow further");
         }
         if (push) {
             if (!prev.queued) {  // dense level -> queue
@@ -1071,6 +1101,8 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 dp.push_beta = beta;
                 dp.thin_degree = kThinDegree;
                 dp.max_degree = kHeavyDeg;
+                if (seeds) dp.seeds = *seeds;
+                dp.seed_room = (unsigned long long)seed_room;
                 void *args[] = {&dp};
                 CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_kernel, dim3(h->deep_grid_f),
                                                         dim3(kDeepThreads), args, 0, st));
@@ -1125,8 +1157,13 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                     h->sigma, h->counters + h->cnt_off);
                 ++h->launches;
             }
+            if (seeds && L < seeds->levels) {
+                inject_seeds_queue_kernel<<<296, 256, 0, st>>>(*seeds, L, n, queue_params(h), h->vis, h->scrA,
+                                                              h->sigma);
+                ++h->launches;
+            }
             push_post_kernel<<<dim3(std::min<unsigned>(grid1d((size_t)std::min<unsigned long long>(
-                                                           (unsigned long long)n, prev.farcs + 1)), 1184), ng),
+                                                           (unsigned long long)n, prev.farcs + 1 + seed_room)), 1184), ng),
                                256, 0, st>>>(c.off, n, queue_params(h), h->d_qlbeg, h->vis, h->scrA,
                                              h->live + (size_t)L * G, h->counters + h->cnt_off, h->lstat,
                                              h->heavy);
@@ -1316,6 +1353,87 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
 // partitioned forward phase
 // ------------------------------------------------------------------------------------
 
+// Frontier-queue sweeps inside the parts: unit weights, a low-degree (deep) graph, and no vertex
+// long enough to need the sliced heavy-entry push.
+bool partition_queue_sweeps(const bc_handle *h) {
+    return h->hybir_queues && h->sparse && h->full.wgt == nullptr && h->n_arcs < 6 * h->n &&
+           h->intra_maxdeg <= (int64_t)kHeavyDeg && !h->h_ioff.empty();
+}
+
+// Blocks of a kernel that walks every queue entry of a sweep (all levels).
+unsigned queue_blocks_all(const std::vector<LevelRep> &reps, int depth) {
+    int64_t longest = 1;
+    if (depth > 0)
+        for (size_t g = 0; g < reps[depth - 1].qe.size(); ++g) longest = std::max(longest, reps[depth - 1].qe[g]);
+    return (unsigned)std::min<int64_t>((longest + 255) / 256, 8 * 148);
+}
+
+// Queue sweeps of the partitioned modes: one past the last queue entry of every level,
+// [level][group], for the kernels that map a queue entry back to its level.
+int upload_level_ends(bc_handle *h, const std::vector<LevelRep> &reps, int depth, cudaStream_t st) {
+    const size_t G = (size_t)h->alloc_groups;
+    std::vector<int64_t> ends((size_t)depth * G, 0);
+    for (int L = 0; L < depth; ++L) {
+        if (!reps[L].queued) return h->fail(BC_ERR_INTERNAL, "partitioned queue sweep produced a dense level");
+        for (size_t g = 0; g < G; ++g)
+            ends[(size_t)L * G + g] = g < reps[L].qe.size() ? reps[L].qe[g] : 0;
+    }
+    if ((int64_t)ends.size() > h->range_table_cap) {
+        TRY(dev_alloc(h, &h->range_table, ends.size()));
+        h->range_table_cap = (int64_t)ends.size();
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(h->range_table, ends.data(), ends.size() * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));   // `ends` goes out of scope
+    return BC_OK;
+}
+
+// Step-6 seeds of the batch sorted by level (forward.py:232-241): every (border, lane) pair with a
+// finite refined distance and a non-zero arrival count.
+int build_seed_plan(bc_handle *h, int lanes, int max_seed_level, cudaStream_t st, SeedPlan *plan) {
+    const int S = h->border_S;
+    const size_t cnt = (size_t)h->B * S;
+    *plan = SeedPlan{};
+    plan->arr = h->arr;
+    plan->border_v = h->d_border_v;
+    plan->S = S;
+    plan->levels = 0;
+    if (cnt == 0 || max_seed_level < 0) return BC_OK;
+    if (cnt >= ((size_t)1 << 31)) return h->fail(BC_ERR_INPUT, "too many (border, lane) pairs in one batch");
+    if (h->seed_keys == nullptr) {
+        TRY(dev_alloc(h, &h->seed_keys, cnt));
+        TRY(dev_alloc(h, &h->seed_keys2, cnt));
+        TRY(dev_alloc(h, &h->seed_vals, cnt));
+        TRY(dev_alloc(h, &h->seed_vals2, cnt));
+    }
+    const int levels = max_seed_level + 1;
+    if (h->seed_off_cap < levels + 1) {
+        arena_free(h->seed_off);
+        h->seed_off = nullptr;
+        TRY(dev_alloc(h, &h->seed_off, (size_t)levels + 1));
+        h->seed_off_cap = levels + 1;
+    }
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, h->seed_keys, h->seed_keys2, h->seed_vals, h->seed_vals2,
+                                    (int)cnt, 0, 32, st);
+    if (need > h->seed_tmp_bytes) {
+        arena_free(h->seed_tmp);
+        h->seed_tmp = nullptr;
+        CUDA_TRY(h, arena_malloc(&h->seed_tmp, need));
+        h->seed_tmp_bytes = need;
+    }
+    seed_key_kernel<<<grid1d(cnt), 256, 0, st>>>(h->B, S, lanes, h->D, h->arr, h->seed_keys, h->seed_vals);
+    CUDA_TRY(h, cub::DeviceRadixSort::SortPairs(h->seed_tmp, need, h->seed_keys, h->seed_keys2, h->seed_vals,
+                                                h->seed_vals2, (int)cnt, 0, 32, st));
+    seed_offsets_kernel<<<(levels + 1 + 127) / 128, 128, 0, st>>>(h->seed_keys2, (int64_t)cnt, levels, h->seed_off);
+    h->launches += 3;
+    CUDA_TRY(h, cudaGetLastError());
+    plan->idx = h->seed_vals2;
+    plan->off = h->seed_off;
+    plan->levels = levels;
+    return BC_OK;
+}
+
 int ensure_border_state(bc_handle *h, int S) {
     if (h->border_S >= S && h->D != nullptr) return BC_OK;
     free_border_state(h);
@@ -1484,11 +1602,29 @@ int build_border_tables(bc_handle *h) {
     // tables arrive through bc_dist_hybir_set_table
     const int b_lo = h->dist_hybir ? h->h_part_off[(size_t)h->dist_rank] : 0;
     const int b_hi = h->dist_hybir ? h->h_part_off[(size_t)h->dist_rank + 1] : h->B;
+    const bool qsweep = partition_queue_sweeps(h);
+    if (qsweep) {
+        // queue sweeps write only the pairs they reach
+        fill_i32_kernel<<<grid1d((size_t)h->tab_total, 256, 4736), 256, 0, st>>>(h->bm, (size_t)h->tab_total, kInf);
+        CUDA_TRY(h, cudaMemsetAsync(h->sm, 0, (size_t)h->tab_total * sizeof(double), st));
+        ++h->launches;
+    }
     for (int first = b_lo; first < b_hi; first += per) {
         const int cnt = std::min(per, b_hi - first);
         const int ng = (cnt + 31) / 32;
-        TRY(begin_batch(h, d_borders + first, cnt, ng, st));
+        TRY(begin_batch(h, d_borders + first, cnt, ng, st, qsweep));
         int depth = 1;
+        if (qsweep) {
+            std::vector<LevelRep> reps;
+            TRY(forward_adaptive(h, h->intra, ng, cnt, src.data() + first, st, &depth, reps, &h->h_ioff, true));
+            TRY(upload_level_ends(h, reps, depth, st));
+            border_table_queue_kernel<<<dim3(queue_blocks_all(reps, depth), ng), 256, 0, st>>>(
+                queue_params(h), h->range_table, depth, h->alloc_groups, h->n, h->d_border_index, h->sigma,
+                geo, first, cnt, h->bm, h->sm);
+            ++h->launches;
+            CUDA_TRY(h, cudaGetLastError());
+            continue;
+        }
         TRY(forward_sweep(h, h->intra, ng, st, &depth));
         TRY(upload_level_ptrs(h, depth, st));
         const size_t work = (size_t)h->B * ((cnt + 31) / 32 * 32);
@@ -1605,6 +1741,11 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     // queue levels / push: the unpartitioned sweeps only (the partitioned modes
     // read dense level rows for borders and reports)
     const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2) && h->full.wgt == nullptr;
+    // hybir mode on low-degree (deep) graphs: Step 1 and Step 6 run on frontier queues inside the
+    // parts (the dense level rows cost levels x n x groups x 4 B there), the border seeds of
+    // Step 6 join the queue levels, and the backward sweep reads the same queues
+    const bool qsweep = hybir && partition_queue_sweeps(h) && !(want_reports && h->k == 2);
+    const bool queued = adaptive || qsweep;   // levels are LevelReps, not h->lvl[L]
 
     // debug staging: one batch (<= 32 sources) of [lane][n] rows
     int32_t *dbg_dist = nullptr;
@@ -1629,11 +1770,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         const int64_t l_start = h->launches;
 
         // ---- forward: Step 1 (or the whole BFS when there is no partition)
-        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, adaptive));
+        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, queued));
         int depth = 1;
         h->cnt_off = hybir ? 4 : 0;  // Step 1 is a partial traversal: keep it out of the totals
         std::vector<LevelRep> reps;
         if (adaptive) TRY(forward_adaptive(h, fwd_csr, ng, cnt, batch_src, st, &depth, reps));
+        else if (qsweep) TRY(forward_adaptive(h, h->intra, ng, cnt, batch_src, st, &depth, reps, &h->h_ioff, true));
         else TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
         h->cnt_off = 0;
         CUDA_TRY(h, cudaEventRecord(e.fwd_end, st));
@@ -1650,19 +1792,30 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
                                         cudaMemcpyHostToDevice, st));
             fill_border_kernel<<<grid1d(bcnt, 256, 4736), 256, 0, st>>>(h->D, h->seedD, h->seedS,
                                                                         h->sig, h->arr, bcnt);
-            TRY(upload_level_ptrs(h, depth, st));
-            if (h->B > 0)
-                border_gather_kernel<<<grid1d(bcnt), 256, 0, st>>>(
-                    h->d_lvl_ptrs, h->live, h->alloc_groups, depth, h->sigma, n, border_geom(h),
-                    h->border_S, h->seedD, h->seedS);
+            if (qsweep) {
+                TRY(upload_level_ends(h, reps, depth, st));
+                if (h->B > 0)
+                    border_gather_queue_kernel<<<dim3(queue_blocks_all(reps, depth), ng), 256, 0, st>>>(
+                        queue_params(h), h->range_table, depth, h->alloc_groups, n, h->d_border_index,
+                        h->sigma, h->border_S, h->seedD, h->seedS);
+            } else {
+                TRY(upload_level_ptrs(h, depth, st));
+                if (h->B > 0)
+                    border_gather_kernel<<<grid1d(bcnt), 256, 0, st>>>(
+                        h->d_lvl_ptrs, h->live, h->alloc_groups, depth, h->sigma, n, border_geom(h),
+                        h->border_S, h->seedD, h->seedS);
+            }
             h->launches += 2;
             int max_seed = -1;
             TRY(refine_and_compose(h, cnt, ng, st, &iters, &entered, &max_seed));
+            SeedPlan plan{};
+            if (qsweep) TRY(build_seed_plan(h, cnt, max_seed, st, &plan));
             CUDA_TRY(h, cudaEventRecord(e.border_end, st));
             // ---- Step 6: every part relaxes from its borders at once
             const int64_t l_step6 = h->launches;
-            TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st));
-            TRY(forward_sweep(h, h->intra, ng, st, &depth, true, cnt, max_seed));
+            TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, qsweep));
+            if (qsweep) TRY(forward_adaptive(h, h->intra, ng, cnt, batch_src, st, &depth, reps, &h->h_ioff, true, &plan));
+            else TRY(forward_sweep(h, h->intra, ng, st, &depth, true, cnt, max_seed));
             CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
             launches_f += h->launches - l_step6;
         } else {
@@ -1674,10 +1827,10 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         // ---- backward over the whole graph (cross-part children are final by
         // the time their parents' level runs: levels are global)
         const int64_t l_bwd = h->launches;
-        if (adaptive) TRY(backward_adaptive(h, h->full, depth, reps, ng, debug, st));
+        if (queued) TRY(backward_adaptive(h, h->full, depth, reps, ng, debug, st));
         else TRY(backward_sweep(h, h->full, depth, ng, debug, st));
         h->last_depth = depth;
-        if (adaptive && !debug && h->lazy_clear) {
+        if (queued && !debug && h->lazy_clear) {
             // the sweep cleared every pair it visited; the sources (level 0) are left
             clear_source_sigma_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * lanes_per_batch, cnt, n,
                                                                         h->sigma);
@@ -1789,13 +1942,13 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             if (dbg_sigma) CUDA_TRY(h, cudaMemsetAsync(dbg_sigma, 0, rows * sizeof(double), st));
             if (dbg_delta) CUDA_TRY(h, cudaMemsetAsync(dbg_delta, 0, rows * sizeof(double), st));
             for (int L = 0; L < depth; ++L) {
-                if (adaptive && reps[L].slot < 0) {
+                if (queued && reps[L].slot < 0) {
                     TRY(upload_ranges(h, reps[L], st));
                     extract_queue_kernel<<<dim3(queue_blocks(reps[L], 256), 1), 256, 0, st>>>(
                         queue_params(h), h->sigma, h->delta, n, L, dbg_dist, dbg_sigma, dbg_delta);
                 } else {
                     extract_level_kernel<<<dim3(grid1d((size_t)n, 256, 1184), 1), 256, 0, st>>>(
-                        h->lvl[adaptive ? reps[L].slot : L], h->live + (size_t)L * h->alloc_groups,
+                        h->lvl[queued ? reps[L].slot : L], h->live + (size_t)L * h->alloc_groups,
                         h->sigma, h->delta, n, L, dbg_dist, dbg_sigma, dbg_delta);
                 }
                 ++h->launches;
@@ -2031,6 +2184,10 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         h->deep = value ? 1 : 0;
         return BC_OK;
     }
+    if (k == "hybir_queues") {
+        h->hybir_queues = value ? 1 : 0;
+        return BC_OK;
+    }
     if (k == "deep_blocks_per_sm") {
         if (value < 0 || value > 32) return h->fail(BC_ERR_INPUT, "deep_blocks_per_sm must be in [0, 32]");
         h->deep_blocks_per_sm = (int)value;
@@ -2165,6 +2322,15 @@ int install_partition(bc_handle *h, int k, const int32_t *assignment, const Exte
         TRY(upload(h, &c.wgt, iwgt));
     }
     TRY(build_items(h, c, ioff.data(), h->item_arcs));
+    h->intra_maxdeg = 0;
+    for (int64_t v = 0; v < n; ++v)
+        h->intra_maxdeg = std::max(h->intra_maxdeg, ioff[(size_t)v + 1] - ioff[(size_t)v]);
+    h->h_ioff.swap(ioff);
+    {
+        std::vector<int32_t> index_of((size_t)n, -1);
+        for (int j = 0; j < h->B; ++j) index_of[(size_t)h->h_border_v[(size_t)j]] = j;
+        TRY(upload(h, &h->d_border_index, index_of));
+    }
     TRY(upload(h, &h->d_part, h->h_part));
     TRY(upload(h, &h->d_border_v, h->h_border_v));
     TRY(upload(h, &h->d_border_p, h->h_border_p));

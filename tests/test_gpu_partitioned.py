@@ -210,3 +210,35 @@ def test_grown_partitions_in_both_modes():
                                           per_source_reports=False))
             assert res.partition.num_parts == k
             assert np.allclose(res.bc, want, rtol=RTOL, atol=ATOL), (k, mode)
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_hybir_queue_sweeps_match_dense_sweeps(k):
+    # low-degree graphs run Step 1 / Step 6 / the border-table searches on frontier queues with
+    # the border seeds joining the queue levels; option hybir_queues = 0 keeps the dense level rows
+    import random
+    g = G.road_like(48, 40, keep=0.2, seed=3)
+    n = g.num_vertices
+    part = P.strip_partition(48, 40, k)
+    srcs = sorted(random.Random(1).sample(range(n), 75))       # two batches of 2 groups, ragged tail
+    want, info = O.brandes_bc(g, srcs)
+    out = {}
+    for queues in (1, 0):
+        with Engine(g) as e:
+            e.set_option("reports", 0)
+            e.set_option("groups", 2)
+            e.set_option("hybir_queues", queues)
+            e.set_partition(k, part.assignment)
+            counts = e.border_counts(k)
+            tables = [e.border_tables(p, int(counts[p])) for p in range(k)]
+            bc, st = e.run(srcs, MODE_HYBIR)
+            dist, sigma, delta = e.debug_sources(srcs[:40], MODE_HYBIR)
+        out[queues] = (tables, bc, st, dist, sigma, delta)
+        assert np.allclose(bc, want, rtol=RTOL, atol=ATOL), queues
+        _check_sources(g, srcs[:40], dist, sigma, delta)
+    for (b1, bm1, sm1), (b0, bm0, sm0) in zip(out[1][0], out[0][0]):
+        assert np.array_equal(b1, b0) and np.array_equal(bm1, bm0) and np.array_equal(sm1, sm0)
+    assert out[1][2]["iterations"] == out[0][2]["iterations"]
+    assert np.array_equal(out[1][3], out[0][3]) and np.array_equal(out[1][4], out[0][4])
+    # far fewer launches: thousands of dense levels against a few persistent sweeps
+    assert out[1][2]["launches"] < out[0][2]["launches"]
