@@ -120,9 +120,9 @@ __global__ void border_table_kernel(const uint32_t *const *lvl, const uint32_t *
 // destination sets are disjoint); k > 2 reads `Din` and writes `Dout`.
 __global__ void cut_relax_kernel(BorderGeom geo, int S, const int32_t *Din, int32_t *Dout,
                                  const int32_t *lane_part, const uint32_t *lane_active, int which,
-                                 uint32_t *lane_changed) {
+                                 uint32_t *lane_changed, uint32_t *rowflag) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)geo.B * S) return;
+    if (idx >= (size_t)geo.B * S) return;   // whole warps: B * S is a multiple of 32
     const int j = (int)(idx / S), lane = (int)(idx % S);
     const int32_t old = Din[idx];
     int32_t best = old;
@@ -134,6 +134,14 @@ __global__ void cut_relax_kernel(BorderGeom geo, int S, const int32_t *Din, int3
     }
     if (Dout != Din || best != old) Dout[idx] = best;
     if (best != old && lane_changed) lane_changed[lane] = 1u;
+    // rowflag[j][lane / 32]: some lane of the word was lowered.  The closure pass that follows
+    // only has to push these rows on: every other row was either pushed by the pass that
+    // followed its own change, or set by a closure pass / an intra-part search, and then
+    // D[i] + bm[i][j] cannot beat what is there (bm is a metric closure).
+    if (rowflag) {
+        const unsigned nz = __ballot_sync(0xffffffffu, best != old);
+        if ((threadIdx.x & 31) == 0) rowflag[idx >> 5] = nz;
+    }
 }
 
 // Step 3 / Step 5 (forward.py:91-96): one Jacobi pass of the min-plus closure
@@ -151,7 +159,8 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
                                                            const int32_t *bm,
                                                            const int32_t *lane_part,
                                                            const uint32_t *lane_active, int which,
-                                                           uint32_t *lane_changed) {
+                                                           uint32_t *lane_changed,
+                                                           const uint32_t *rowflag) {
     __shared__ __align__(16) int32_t sD[kTI][kTL];
     __shared__ __align__(16) int32_t sB[kTI][kTJ];
     const int p = blockIdx.z;
@@ -174,8 +183,15 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
         old[r][2] = best[r][2] = v.z;
         old[r][3] = best[r][3] = v.w;
     }
+    const int words = S >> 5;   // rowflag words per border row
     for (int i0 = 0; i0 < b; i0 += kTI) {
-        __syncthreads();
+        // rows the preceding cut-arc step did not lower cannot improve anything: skip the tile
+        bool live_tile = rowflag == nullptr;
+        if (rowflag != nullptr && threadIdx.x < 2 * kTI) {
+            const int i = i0 + (threadIdx.x >> 1), w = blockIdx.y * (kTL / 32) + (threadIdx.x & 1);
+            live_tile = i < b && w < words && rowflag[(size_t)(base + i) * words + w] != 0;
+        }
+        if (!__syncthreads_or(live_tile)) continue;   // (also the barrier that protects the tiles)
 #pragma unroll
         for (int k = 0; k < 2; ++k) {                          // 32 x 16 int4 slots of sD
             const int slot = threadIdx.x + 256 * k, row = slot >> 4, c4 = slot & 15;
@@ -227,24 +243,30 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
 // arr[j] = sum of sig[i] over incoming cut arcs (i -> j) that are tight
 // (forward.py:170-174), in arc order.
 // darr[j] = what the round adds to arr[j]: the composition only has to push the change on.
+// rowflag[j][lane / 32] = some lane of that 32-lane word changed (S is a multiple of 32, so a
+// warp covers one word of one border): compose_sigma_kernel skips the row tiles nothing
+// changed in without reading them.
 __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const double *sig,
-                               double *arr, double *darr, const uint32_t *lane_run) {
+                               double *arr, double *darr, const uint32_t *lane_run,
+                               uint32_t *rowflag) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)geo.B * S) return;
+    if (idx >= (size_t)geo.B * S) return;   // whole warps: B * S is a multiple of 32
     const int j = (int)(idx / S), lane = (int)(idx % S);
-    if (!lane_run[lane]) {         // this lane's counts settled in an earlier round
-        darr[idx] = 0.0;
-        return;
+    double delta = 0.0;
+    if (lane_run[lane]) {          // (a lane whose counts settled in an earlier round stays put)
+        const int32_t dj = D[idx];
+        double a = 0.0;
+        if (dj < kInf)
+            for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c) {
+                const size_t at = (size_t)geo.cin_src[c] * S + lane;
+                if (D[at] + geo.cin_w[c] == dj) a += sig[at];
+            }
+        delta = a - arr[idx];
+        arr[idx] = a;
     }
-    const int32_t dj = D[idx];
-    double a = 0.0;
-    if (dj < kInf)
-        for (int64_t c = geo.cin_off[j]; c < geo.cin_off[j + 1]; ++c) {
-            const size_t at = (size_t)geo.cin_src[c] * S + lane;
-            if (D[at] + geo.cin_w[c] == dj) a += sig[at];
-        }
-    darr[idx] = a - arr[idx];
-    arr[idx] = a;
+    darr[idx] = delta;
+    const unsigned nz = __ballot_sync(0xffffffffu, delta != 0.0);
+    if ((threadIdx.x & 31) == 0) rowflag[idx >> 5] = nz;
 }
 
 // sig[j] = (seed count if j is on the source side and its Step-1 distance is
@@ -259,7 +281,8 @@ __global__ void arrival_kernel(BorderGeom geo, int S, const int32_t *D, const do
 __global__ void __launch_bounds__(256) compose_sigma_kernel(
     BorderGeom geo, int S, const int32_t *D, const int32_t *seedD, const double *seedS,
     const double *darr, const int32_t *bm, const double *sm, const int32_t *lane_part,
-    double *sig, const uint32_t *lane_run, uint32_t *lane_changed, int first_round) {
+    double *sig, const uint32_t *lane_run, uint32_t *lane_changed, int first_round,
+    const uint32_t *rowflag) {
     __shared__ __align__(16) int32_t sD[kTI][kTL];
     __shared__ __align__(16) double sA[kTI][kTL];
     __shared__ __align__(16) int32_t sB[kTI][kTJ];
@@ -299,8 +322,15 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
             }
         }
     }
+    const int words = S >> 5;   // rowflag words per border row
     for (int i0 = 0; i0 < b; i0 += kTI) {
-        __syncthreads();
+        // nothing changed in these kTI rows for this block's 64 lanes: skip the tile unread
+        bool live_tile = false;
+        if (threadIdx.x < 2 * kTI) {
+            const int i = i0 + (threadIdx.x >> 1), w = blockIdx.y * (kTL / 32) + (threadIdx.x & 1);
+            live_tile = i < b && w < words && rowflag[(size_t)(base + i) * words + w] != 0;
+        }
+        if (!__syncthreads_or(live_tile)) continue;   // (also the barrier that protects the tiles)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int e = threadIdx.x + 256 * k, row = e >> 6, c = e & 63;

@@ -1464,6 +1464,7 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
                        std::vector<int32_t> *iters_out, std::vector<uint32_t> *entered_out,
                        int *max_seed_level) {
     const int S = h->border_S;
+    Trace tr;
     const BorderGeom geo = border_geom(h);
     const size_t cnt = (size_t)h->B * S;
     const unsigned gb = grid1d(cnt);
@@ -1486,23 +1487,24 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
                 return h->fail(BC_ERR_INTERNAL, "border refinement exceeded the border-count bound");
             if (h->k == 2) {
                 cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_active,
-                                                     kApplyOther, nullptr);
+                                                     kApplyOther, nullptr, h->sync_flag);
                 matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part,
-                                                           h->lane_active, kApplyOther, nullptr);
+                                                           h->lane_active, kApplyOther, nullptr, h->sync_flag);
                 std::swap(h->D, h->D2);
                 cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_active,
-                                                     kApplySource, h->lane_changed);
+                                                     kApplySource, h->lane_changed, h->sync_flag);
                 matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part,
                                                            h->lane_active, kApplySource,
-                                                           h->lane_changed);
+                                                           h->lane_changed, h->sync_flag);
                 std::swap(h->D, h->D2);
                 h->launches += 4;
             } else {
                 cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D2, h->lane_part, h->lane_active,
-                                                     kApplyAll, h->lane_changed);
+                                                     kApplyAll, h->lane_changed, h->sync_flag);
                 std::swap(h->D, h->D2);
                 matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part,
-                                                           h->lane_active, kApplyAll, h->lane_changed);
+                                                           h->lane_active, kApplyAll, h->lane_changed,
+                                                           h->sync_flag);
                 std::swap(h->D, h->D2);
                 h->launches += 2;
             }
@@ -1518,10 +1520,11 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
         if (h->k == 2) {
             // 'step2-final' (forward.py:134-135) for every lane that ran the loop
             cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_entered,
-                                                 kApplyOther, nullptr);
+                                                 kApplyOther, nullptr, nullptr);
             ++h->launches;
         }
     }
+    tr.mark("border: refinement");
     // path counts at the borders: Jacobi rounds until nothing changes
     CUDA_TRY(h, cudaMemsetAsync(h->sig, 0, cnt * sizeof(double), st));
     if (h->B > 0) {
@@ -1532,11 +1535,13 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
         for (int round = 0;; ++round) {
             if (round > 2 * h->B + 4)
                 return h->fail(BC_ERR_INTERNAL, "border sigma composition did not settle");
-            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->darr, h->lane_active);
+            arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->darr, h->lane_active,
+                                               h->sync_flag);   // (sync_flag is free until the reports)
             CUDA_TRY(h, cudaMemsetAsync(h->dflags + 1, 0, sizeof(uint32_t), st));
             compose_sigma_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->seedD, h->seedS, h->darr,
                                                         h->bm, h->sm, h->lane_part, h->sig,
-                                                        h->lane_active, h->lane_changed, round == 0);
+                                                        h->lane_active, h->lane_changed, round == 0,
+                                                        h->sync_flag);
             lane_round_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->dflags + 1);
             h->launches += 3;
             uint32_t changed = 0;
@@ -1546,6 +1551,7 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
             if (!changed) break;
         }
     }
+    tr.mark("border: composition");
     int m = -1;
     CUDA_TRY(h, cudaMemcpyAsync(h->d_maxlvl, &m, sizeof m, cudaMemcpyHostToDevice, st));
     if (h->B > 0) {
@@ -1780,6 +1786,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         h->cnt_off = 0;
         CUDA_TRY(h, cudaEventRecord(e.fwd_end, st));
         launches_f += h->launches - l_start;
+        tr.mark("batch: forward (Step 1)");
 
         std::vector<int32_t> iters;
         std::vector<uint32_t> entered;
@@ -1806,10 +1813,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
                         h->border_S, h->seedD, h->seedS);
             }
             h->launches += 2;
+            tr.mark("batch: border gather");
             int max_seed = -1;
             TRY(refine_and_compose(h, cnt, ng, st, &iters, &entered, &max_seed));
             SeedPlan plan{};
             if (qsweep) TRY(build_seed_plan(h, cnt, max_seed, st, &plan));
+            tr.mark("batch: seed plan");
             CUDA_TRY(h, cudaEventRecord(e.border_end, st));
             // ---- Step 6: every part relaxes from its borders at once
             const int64_t l_step6 = h->launches;
@@ -1818,6 +1827,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             else TRY(forward_sweep(h, h->intra, ng, st, &depth, true, cnt, max_seed));
             CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
             launches_f += h->launches - l_step6;
+            tr.mark("batch: Step 6");
         } else {
             CUDA_TRY(h, cudaEventRecord(e.border_end, st));
             CUDA_TRY(h, cudaEventRecord(e.fwd2_end, st));
@@ -1839,6 +1849,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         }
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
         launches_b += h->launches - l_bwd;
+        tr.mark("batch: backward");
 
         if (want_reports && h->k == 2) {
             // ---- per-source reports (forward.py:52-64, backward.py:33-43, bsp.py:96-103,137-141)

@@ -82,18 +82,22 @@ if "rmat24" in which:
 if "road2048_hybir" in which:
     # BASELINE config 3 on ONE GPU: the k strips that would sit on k GPUs run in one address space
     g = G.road_like(2048, 2048, keep=0.2, seed=1)
-    # dense level rows: levels x n x groups x 4 B, so deep graphs run the partitioned modes with one group
-    srcs = sorted(random.Random(0).sample(range(g.num_vertices), 128))
-    for k in (8,):
+    # Step 1 / Step 6 / the border-table searches run on frontier queues (no dense level rows), so
+    # all 512 sources of config 3 go in one batch of 16 groups
+    nsrc, groups = 512, 16
+    srcs = sorted(random.Random(0).sample(range(g.num_vertices), nsrc))
+    for k in (8, 2):
         part = P.strip_partition(2048, 2048, k)
         with Engine(g) as e:
-            e.set_option("groups", 1); e.set_option("reports", 0)
+            e.set_option("groups", groups); e.set_option("reports", 0)
             t0 = time.time(); e.set_partition(k, part.assignment); counts = e.border_counts(k).tolist()
             t1 = time.time(); bc, st = e.run(srcs[:32], MODE_HYBIR); t_tables = time.time() - t1   # builds the tables
             t2 = time.time(); bc, st = e.run(srcs, MODE_HYBIR); wall = time.time() - t2
             bcd, std = e.run(srcs, MODE_DIRECT)
-        log(config="road-like 2048x2048 hybir, %d strips, 128 sources, groups=1" % k, borders=counts, ms=st["ms_total"],
+        log(config="road-like 2048x2048 hybir (queue sweeps), %d strips, %d sources, groups=%d" % (k, nsrc, groups),
+            borders=counts, ms=st["ms_total"],
             ms_border=st["ms_border"], ms_forward=st["ms_forward"], ms_backward=st["ms_backward"], wall_s=wall,
             set_partition_s=t1 - t0, tables_and_first_batch_s=t_tables, iterations=st["iterations"],
-            levels=st["max_levels"], direct_ms=std["ms_total"],
+            levels=st["max_levels"], launches=st["launches"], direct_ms=std["ms_total"],
+            gteps=g.num_edges * nsrc / st["ms_total"] / 1e6,
             hybir_vs_direct=float(np.max(np.abs(bc - bcd) / np.maximum(np.abs(bcd), 1e-9))))
