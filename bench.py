@@ -340,7 +340,7 @@ def run_ours(args):
         sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     acc = {"ms_forward": 0.0, "ms_backward": 0.0, "launches": 0, "launches_forward": 0, "launches_backward": 0,
-           "launches_level": 0}
+           "launches_level": 0, "ms_level": 0.0, "launches_level_timed": 0}
     ev0.record(stream)
     for _ in range(args.steps):
         st = step()
@@ -399,15 +399,32 @@ def run_ours(args):
                 "avg_launch_ms": ms / max(launches, 1)}
 
     both = sweep(fwd_b + bwd_b, fwd_ms + bwd_ms, lf + lb)
+    # the dominant kernel alone: CUDA events around every level-kernel launch (bc_stats.ms_level)
+    traffic = ncu_traffic(args.workload)
+    lvl_ms = acc["ms_level"] / args.steps
+    lvl_n = acc["launches_level_timed"] / args.steps
+    lvl_avg = lvl_ms / max(lvl_n, 1)
+    level_kernel = {
+        "ms_per_step": lvl_ms, "launches_per_step": lvl_n, "avg_launch_ms": lvl_avg,
+        "share_of_step": lvl_ms / (ms_total / args.steps),
+        "algorithmic_bytes_per_launch": (fwd_b + bwd_b) / max(lvl_n, 1),
+        "algorithmic_achieved": (fwd_b + bwd_b) / max(lvl_ms, 1e-9) / 1e6,
+        "dram_bytes_per_launch": traffic,
+        "dram_achieved": (traffic / (lvl_avg / 1e3) / 1e9) if traffic and lvl_avg > 0 else None,
+        "dram_frac": (traffic / (lvl_avg / 1e3) / 1e9 / peak) if traffic and lvl_avg > 0 else None,
+        "note": "dram_* = DRAM bytes per launch from the committed ncu --set full capture (roofline.traffic) "
+                "over the live average launch time: what the kernel really pulls from HBM",
+    }
     roofline = {
         "bound": "hbm", "kernel": "level_kernel<forward | backward> and the push / queue kernels of the same sweeps",
         "achieved": both["achieved"], "peak": peak, "unit": "GB/s", "frac": both["frac"],
-        "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
+        "traffic": traffic, "peak_source": peak_src,
         "algorithmic_bytes_per_step": both["algorithmic_bytes_per_step"], "ms_per_step": both["ms_per_step"],
         "launches_per_step": both["launches_per_step"], "bytes_per_launch": both["bytes_per_launch"],
         "avg_launch_ms": both["avg_launch_ms"],
         "level_kernel_launches_per_step": acc["launches_level"] / args.steps,
         "algorithmic_bytes_per_level_kernel_launch": (fwd_b + bwd_b) / max(1.0, acc["launches_level"] / args.steps),
+        "level_kernel": level_kernel,
         "forward": sweep(fwd_b, fwd_ms, lf), "backward": sweep(bwd_b, bwd_ms, lb),
         "whole_step": {"achieved": (fwd_b + bwd_b + init_b) / (ms_total / args.steps / 1e3) / 1e9,
                        "frac": (fwd_b + bwd_b + init_b) / (ms_total / args.steps / 1e3) / 1e9 / peak},

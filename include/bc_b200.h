@@ -74,6 +74,9 @@ typedef struct bc_stats {
     int64_t launches_forward;  /* kernels launched between the events that bound ms_forward  */
     int64_t launches_backward; /* ... ms_backward                                           */
     int64_t launches_level;    /* of those, launches of the dense level kernel (both directions) */
+    double ms_level;           /* device time of those launches alone (level kernel + its hub pass;
+                                  at most 512 launches per call are timed, launches_level_timed)   */
+    int64_t launches_level_timed;
 } bc_stats;
 
 /* Replaces: construction of the device-side view of `Graph`
@@ -91,7 +94,11 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
 int bc_set_weights(bc_handle *h, const int32_t *weights);
 
 /* Tuning knobs ("groups": 32-lane source groups per batch; "item_arcs": arcs
- * per warp work item; "reports": 1 = keep per-source report counters). */
+ * per warp work item; "reports": 1 = keep per-source report counters;
+ * "sparse" / "deep": frontier-queue levels / persistent multi-level sweeps;
+ * "hybir_queues": 1 = BC_MODE_HYBIR sweeps of low-degree graphs run on frontier
+ * queues with the Step-6 border seeds joining the queue levels, 0 = dense level
+ * rows; "push_beta", "push_beta_late", "reorder": see csrc/bc_engine.cu). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);
 
 /* Replaces: `Partition` + `identify_borders` + `compute_border_matrices`

@@ -45,6 +45,7 @@ class BcStats(ctypes.Structure):
         ("sync_events", ctypes.c_int64), ("comm_bytes", ctypes.c_int64),
         ("launches_forward", ctypes.c_int64), ("launches_backward", ctypes.c_int64),
         ("launches_level", ctypes.c_int64),
+        ("ms_level", ctypes.c_double), ("launches_level_timed", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -266,6 +266,7 @@ struct bc_handle {
     std::string err;
     int64_t launches = 0;
     int64_t level_launches = 0;   // dense level kernel only
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> level_events;   // around those launches (<= 512 per call)
 
     int fail(int code, const std::string &msg) {
         err = msg;
@@ -710,6 +711,36 @@ void prof_dump(const char *what, int L, cudaStream_t st) {
 inline void prof_dump(const char *, int, cudaStream_t) {}
 #endif
 
+void drop_level_events(bc_handle *h) {
+    for (auto &pr : h->level_events) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    h->level_events.clear();
+}
+
+// CUDA events around one dense level launch (level kernel + hub pass): bc_stats.ms_level.
+struct LevelTimer {
+    bc_handle *h;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    LevelTimer(bc_handle *h_, cudaStream_t st_) : h(h_), st(st_) {
+        if (h->level_events.size() >= 512) return;
+        if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+            a = b = nullptr;
+            return;
+        }
+        cudaEventRecord(a, st);
+    }
+    void stop() {
+        if (a == nullptr) return;
+        cudaEventRecord(b, st);
+        h->level_events.emplace_back(a, b);
+        a = b = nullptr;
+    }
+    ~LevelTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
 // Forward level L on graph c for `ng` groups: pull from the masks `nbr` (level
 // L - 1) into the dense array `cur`.
 int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
@@ -728,6 +759,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
         ++h->launches;
         p.cand = h->cand;
     }
+    LevelTimer timer(h, st);
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     if (c.wgt != nullptr)
         level_kernel<false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -745,6 +777,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
         hub_kernel<false, false><<<dim3(blocks_for(c.n_hub), ng), kWarpsPerBlock * 32, 0, st>>>(q);
         ++h->launches;
     }
+    timer.stop();
     CUDA_TRY(h, cudaGetLastError());
     prof_dump("fwd", L, st);
     return BC_OK;
@@ -761,6 +794,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     p.accumulate_bc = (accumulate ? 1 : 0) | (h->lazy_clear ? 2 : 0);
     p.level = L;
     p.max_level = h->cur_depth - 1;
+    LevelTimer timer(h, st);
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     if (c.wgt != nullptr && store_delta)
         level_kernel<true, true, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -784,6 +818,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
             hub_kernel<true, false><<<hg, kWarpsPerBlock * 32, 0, st>>>(q);
         ++h->launches;
     }
+    timer.stop();
     CUDA_TRY(h, cudaGetLastError());
     prof_dump("bwd", L, st);
     return BC_OK;
@@ -1666,6 +1701,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const bool hybir = mode == BC_MODE_HYBIR;
     const bool want_reports = h->reports && mode != BC_MODE_DIRECT;
     if (hybir) TRY(build_border_tables(h));
+    drop_level_events(h);   // (table searches, graph-partitioned runs: not this call's launches)
 
     // Sources without arcs reach nothing: sigma = 1 at the source, delta = 0
     // everywhere.  In direct mode they stay in the result (and the counters)
@@ -1990,6 +2026,14 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     tr.mark("run: batches");
     arena_free(dbg_dist), arena_free(dbg_sigma), arena_free(dbg_delta);
 
+    double ms_level = 0;
+    const int64_t level_timed = (int64_t)h->level_events.size();
+    for (auto &pr : h->level_events) {
+        float t = 0;
+        if (cudaEventElapsedTime(&t, pr.first, pr.second) == cudaSuccess) ms_level += t;
+        cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    }
+    h->level_events.clear();
     double ms_f = 0, ms_b = 0, ms_border = 0;
     for (Events &e : ev) {
         float a = 0, bo = 0, f2 = 0, bw = 0;
@@ -2029,6 +2073,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         stats->launches_forward = launches_f;
         stats->launches_backward = launches_b;
         stats->launches_level = h->level_launches - level_launches0;
+        stats->ms_level = ms_level;
+        stats->launches_level_timed = level_timed;
     }
     return BC_OK;
 }
@@ -2793,6 +2839,7 @@ const char *bc_last_error(bc_handle *h) {
 void bc_destroy(bc_handle *h) {
     if (h == nullptr) return;
     cudaSetDevice(h->device);
+    drop_level_events(h);
     free_state(h);
     free_partition(h);
     free_csr(h->full);
