@@ -26,6 +26,17 @@ def test_header_and_binding_agree(lib_path):
         assert hasattr(L, name), name
 
 
+def test_stats_struct_layout_matches_the_header():
+    # bc_stats is filled by the library and read through ctypes: same fields, same order, same types
+    header = open(os.path.join(ROOT, "include", "bc_b200.h")).read()
+    body = re.search(r"typedef struct bc_stats \{(.*?)\} bc_stats;", header, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"\b(int64_t|double)\s+([a-z_0-9]+)\s*;", body)
+    ctype = {"int64_t": ctypes.c_int64, "double": ctypes.c_double}
+    assert [(name, ctype[t]) for t, name in fields] == list(_capi.BcStats._fields_)
+    assert ctypes.sizeof(_capi.BcStats) == 8 * len(fields)
+
+
 def test_library_is_sm100a(lib_path):
     import shutil
     import subprocess
