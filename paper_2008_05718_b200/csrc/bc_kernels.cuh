@@ -33,7 +33,8 @@ namespace bcb200 {
 #define BC_MIN_BLOCKS_BWD 16
 #endif
 #ifndef BC_GATHER
-#define BC_GATHER 2  // 0: per-slice choice, 1: rows only, 2: columns above BC_SPARSE_SLICE hit arcs
+#define BC_GATHER 3  // 0: per-slice choice, 1: rows only, 2: columns above BC_SPARSE_SLICE hit arcs,
+                     // 3: staged rows (BC_ROW_RATIO 0: always; > 0: columns below that many instances per hit arc)
 #endif
 #ifndef BC_SPARSE_SLICE
 #define BC_SPARSE_SLICE 2
@@ -148,6 +149,16 @@ constexpr int kSparseSlice = BC_SPARSE_SLICE;
 #ifndef BC_ROW_UNROLL
 #define BC_ROW_UNROLL ((BC_GATHER == 2 && BC_SPARSE_SLICE <= 2) ? 2 : 4)
 #endif
+#ifndef BC_ROW_RATIO
+#define BC_ROW_RATIO 0   // BC_GATHER 3: 0 = staged rows always, else only when a hit arc serves at least this many instances on average
+#endif
+#ifndef BC_STAGED_UNROLL_FWD
+#define BC_STAGED_UNROLL_FWD 8
+#endif
+#ifndef BC_STAGED_UNROLL_BWD
+#define BC_STAGED_UNROLL_BWD 4
+#endif
+constexpr int kStagedMax = BC_STAGED_UNROLL_FWD > BC_STAGED_UNROLL_BWD ? BC_STAGED_UNROLL_FWD : BC_STAGED_UNROLL_BWD;
 constexpr int kRowUnroll = BC_ROW_UNROLL;  // row loads in flight  // slices with at most this many hit arcs take the arc-serial path
 
 // Scan arcs [a0, a1) of one vertex.  `want` (warp-uniform) = lanes that still
@@ -172,7 +183,7 @@ struct WeightedProbe {
 
 // Mask of the lanes for which arc k ties its endpoint w to the level being computed.
 template <bool WEIGHTED, bool BWD>
-__device__ __forceinline__ uint32_t probe_arc(int64_t k, int32_t w, const uint32_t *__restrict__ nmask,
+__device__ __forceinline__ uint32_t probe_arc(int k, int32_t w, const uint32_t *__restrict__ nmask,
                                               const WeightedProbe &wp) {
     if (!WEIGHTED) return __ldg(nmask + w);
     const int wt = __ldg(wp.wgt + k);
@@ -182,26 +193,27 @@ __device__ __forceinline__ uint32_t probe_arc(int64_t k, int32_t w, const uint32
 }
 
 template <bool COUNT_T, bool WEIGHTED = false, bool BWD = false>
-__device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
+__device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const int32_t *__restrict__ col,
                                           const uint32_t *__restrict__ nmask,
                                           const double *__restrict__ val, int lane, double &acc,
                                           uint32_t &got, unsigned &tcount,
                                           const WeightedProbe &wp = WeightedProbe{}) {
+    // arcs are [0, n_arcs) relative to `col` (and to wp.wgt): 32-bit index arithmetic
     int32_t w_n = 0;
     uint32_t hit_n = 0;
-    if (a0 + lane < a1) {
-        w_n = __ldg(col + a0 + lane);
-        hit_n = probe_arc<WEIGHTED, BWD>(a0 + lane, w_n, nmask, wp) & want;
+    if (lane < n_arcs) {
+        w_n = __ldg(col + lane);
+        hit_n = probe_arc<WEIGHTED, BWD>(lane, w_n, nmask, wp) & want;
     }
     const double *myval = val + lane;
-    for (int64_t base = a0; base < a1; base += 32) {
+    for (int base = 0; base < n_arcs; base += 32) {
         const int32_t w = w_n;
         const uint32_t hit = hit_n;
-        const int64_t k2 = base + 32 + lane;
+        const int k2 = base + 32 + lane;
         w_n = 0;
         hit_n = 0;
-        if (k2 < a1) {
+        if (k2 < n_arcs) {
             w_n = __ldg(col + k2);
             hit_n = probe_arc<WEIGHTED, BWD>(k2, w_n, nmask, wp) & want;
         }
@@ -222,13 +234,50 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
         bool rows;
         if (BC_GATHER == 1) rows = true;
         else if (BC_GATHER == 2) rows = __popc(any) <= kSparseSlice;
-        else {
+        else if (BC_GATHER == 3) {
+            // staged rows (below): ~6 instructions and two L1 wavefronts per hit arc, against
+            // ~70 for the transpose plus ~14 per element of the longest column and one
+            // wavefront per (arc, instance) pair
+            const int nh = __popc(any);
+            const int ph = __popc(hit);
+            if (COUNT_T) tcount += ph;  // per-lane partial, lanes = arcs here
+            rows = BC_ROW_RATIO == 0 || nh <= kSparseSlice ||
+                   (int)__reduce_add_sync(kFull, ph) >= BC_ROW_RATIO * nh;
+        } else {
             // rows cost ~10 instructions per hit arc; columns ~66 for the transpose plus ~13
             // per element of the longest column, which is at least pairs / lanes hit
             const int nh = __popc(any);
             const unsigned lanes_hit = __reduce_or_sync(kFull, hit);
             const int pairs = __reduce_add_sync(kFull, __popc(hit));
             rows = 10 * nh <= 66 + 16 * (pairs / __popc(lanes_hit));
+        }
+        if (BC_GATHER == 3 && rows) {
+            // the hit arcs of the slice, compacted in arc order into a per-warp list in shared
+            // memory; every lane then reads one (neighbour, hit mask) entry per arc with a
+            // broadcast LDS instead of two shuffles and a find-first-set
+            PROF_ADD(6, 1);
+            constexpr int kU = BWD ? BC_STAGED_UNROLL_BWD : BC_STAGED_UNROLL_FWD;  // row loads in flight
+            __shared__ int2 s_rows[kWarpsPerBlock][32 + kStagedMax];
+            int2 *lst = s_rows[threadIdx.x >> 5];
+            const int nh = __popc(any);
+            const uint32_t lbit = 1u << lane;
+            got |= __reduce_or_sync(kFull, hit);
+            if (hit != 0) lst[__popc(any & (lbit - 1u))] = make_int2(w, (int)hit);
+            if (lane < kU) lst[nh + lane] = make_int2(0, 0);  // pad the last round: predicate off
+            __syncwarp();
+            for (int i = 0; i < nh; i += kU) {
+                int2 e[kU];
+                double x[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) e[u] = lst[i + u];
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    x[u] = ldg_if(myval + (size_t)e[u].x * 32, (uint32_t)e[u].y & lbit);
+#pragma unroll
+                for (int u = 0; u < kU; ++u) acc += x[u];  // ascending arc order
+            }
+            __syncwarp();  // the next slice overwrites the list
+            continue;
         }
         if (rows) {
             const uint32_t lbit = 1u << lane;
@@ -262,7 +311,7 @@ __device__ __forceinline__ void scan_arcs(int64_t a0, int64_t a1, uint32_t want,
         } else {
             got |= __reduce_or_sync(kFull, hit);
             uint32_t c = transpose32(hit, lane);  // arcs that hit this lane's BFS instance
-            if (COUNT_T) tcount += __popc(c);
+            if (COUNT_T && BC_GATHER != 3) tcount += __popc(c);
             PROF_ADD(7, 1);
             while (__any_sync(kFull, c != 0)) {
                 PROF_ADD(8, 1);
@@ -377,10 +426,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
     double *delta = STORE_DELTA ? p.delta + g * p.n * 32 : nullptr;
     const double *val = BWD ? coef : sigma;
 
-    // per-item counters fit 32 bits (an item holds <= 32 vertices and <= 2 * item_arcs arcs)
-    unsigned c_nr = 0, c_ar = 0, c_nv = 0, c_fa = 0, c_md = 0;
-    unsigned c_t = 0;  // per-lane partial
-    uint32_t any_new = 0;
+    unsigned c_t = 0;  // per-lane partial count of (arc, instance) hits
 
     if (item < p.n_chk) {
         // ---- a slice of a hub's adjacency: partial sum into the hub buffers
@@ -388,72 +434,102 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         const uint32_t want = BWD ? cur[v] : (~vis[v] & live);
         double acc = 0.0;
         uint32_t got = 0;
-        if (want != 0 && nbr != nullptr)
-            scan_arcs<!BWD, WEIGHTED, BWD>(p.chk_a0[item], p.chk_a1[item], want, p.col, nbr, val, lane,
-                                           acc, got, c_t, wp);
+        if (want != 0 && nbr != nullptr) {
+            const int64_t a0 = p.chk_a0[item];
+            if (WEIGHTED) wp.wgt += a0;
+            scan_arcs<!BWD, WEIGHTED, BWD>((int)(p.chk_a1[item] - a0), want, p.col + a0, nbr, val,
+                                           lane, acc, got, c_t, wp);
+        }
         const size_t slot = g * (size_t)p.n_chk + item;
         if (want != 0) p.pacc[slot * 32 + lane] = acc;
         if (lane == 0) p.pmask[slot] = got;
+        if (!BWD) {
+            const unsigned t = __reduce_add_sync(kFull, c_t);
+            if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
+        }
     } else {
-        // ---- up to 32 consecutive non-hub vertices, one per lane for the set-up
+        // ---- up to 32 consecutive non-hub vertices, one per lane for the set-up and for what
+        // is written per vertex afterwards (level bits, visited bits, counters)
         const int64_t r = item - p.n_chk;
         const int32_t v0 = p.rng_v0[r];
         const int32_t nv = p.rng_nv[r];
-        uint32_t mine = 0;
-        int64_t b = 0, e = 0;
+        const int64_t a0 = p.off[v0];  // arcs of the item are consecutive: 32-bit offsets from here
+        uint32_t mine = 0, seen = 0;
+        int rb = 0, deg = 0;
         if (lane < nv) {
             const int64_t v = (int64_t)v0 + lane;
-            b = p.off[v];
-            e = p.off[v + 1];
-            mine = BWD ? cur[v] : (~vis[v] & live);
-            if (!BWD && p.cand != nullptr) {
-                uint8_t *c = p.cand + g * p.n + v;
-                if (*c) *c = 0;      // consumed
-                else mine = 0;       // no neighbour in the previous level
+            rb = (int)(p.off[v] - a0);
+            deg = (int)(p.off[v + 1] - a0) - rb;
+            if (BWD) {
+                mine = cur[v];
+            } else {
+                seen = vis[v];
+                mine = ~seen & live;
+                if (p.cand != nullptr) {
+                    uint8_t *c = p.cand + g * p.n + v;
+                    if (*c) *c = 0;      // consumed
+                    else mine = 0;       // no neighbour in the previous level
+                }
             }
-            if (!BWD && (mine == 0 || b == e)) cur[v] = 0;  // nothing to discover here
         }
-        unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || e > b));
+        const int32_t *colp = p.col + a0;
+        if (WEIGHTED) wp.wgt += a0;
+        uint32_t mygot = 0;  // forward: what this lane's vertex discovered
+        unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || deg > 0));
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
             const int64_t v = (int64_t)v0 + i;
             const uint32_t want = __shfl_sync(kFull, mine, i);
-            const int64_t vb = __shfl_sync(kFull, b, i);
-            const int64_t ve = __shfl_sync(kFull, e, i);
+            const int vb = __shfl_sync(kFull, rb, i);
+            const int vd = __shfl_sync(kFull, deg, i);
             double acc = 0.0;
             uint32_t got = 0;
-            if (nbr != nullptr)
-                scan_arcs<!BWD, WEIGHTED, BWD>(vb, ve, want, p.col, nbr, val, lane, acc, got, c_t, wp);
+            if (nbr != nullptr) {
+                WeightedProbe wv = wp;
+                if (WEIGHTED) wv.wgt += vb;
+                scan_arcs<!BWD, WEIGHTED, BWD>(vd, want, colp + vb, nbr, val, lane, acc, got, c_t, wv);
+            }
             if (BWD) {
                 finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma, coef, delta,
                                                p.bcg + g * p.n, p.accumulate_bc);
             } else {
-                finalize_forward(v, vis[v], got, acc, lane, vis, cur, sigma);
-                any_new |= got;
-                const unsigned deg = (unsigned)(ve - vb);
-                c_nr += __popc(got);
-                c_ar += __popc(got) * deg;
-                if (got) {
-                    c_nv += 1;
-                    c_fa += deg;
-                    c_md = max(c_md, deg);
-                }
+                if ((got >> lane) & 1u) sigma[(size_t)v * 32 + lane] = acc;
+                if (lane == i) mygot = got;
             }
         }
-    }
-    if (!BWD) {
-        const unsigned t = __reduce_add_sync(kFull, c_t);
-        if (lane == 0) {
-            if (any_new) atomicOr(p.live_cur + g, any_new);
-            if (c_nr) atomicAdd(p.counters + 0, (unsigned long long)c_nr);
-            if (c_ar) atomicAdd(p.counters + 1, (unsigned long long)c_ar);
-            if (t) atomicAdd(p.counters + 2, (unsigned long long)t);
-            if (c_nv && p.lstat) {
-                atomicAdd(p.lstat + 0, (unsigned long long)c_nv);
-                atomicAdd(p.lstat + 1, (unsigned long long)c_fa);
-                atomicMax(p.lstat + 2, (unsigned long long)c_md);
+        if (!BWD) {
+            // one coalesced store per array instead of two lane-0 stores per vertex
+            if (lane < nv) {
+                const int64_t v = (int64_t)v0 + lane;
+                cur[v] = mygot;
+                if (mygot) vis[v] = seen | mygot;
             }
+            // counters, once per item (an item holds <= 32 vertices and <= 2 * item_arcs arcs)
+            const unsigned newv = __ballot_sync(kFull, mygot != 0);
+            const unsigned t = __reduce_add_sync(kFull, c_t);
+            if (newv) {
+                const unsigned pc = __popc(mygot);
+                const unsigned c_nr = __reduce_add_sync(kFull, pc);
+                const unsigned c_ar = __reduce_add_sync(kFull, pc * (unsigned)deg);
+                const uint32_t any_new = __reduce_or_sync(kFull, mygot);
+                unsigned c_fa = 0, c_md = 0;
+                if (p.lstat) {
+                    c_fa = __reduce_add_sync(kFull, mygot ? (unsigned)deg : 0u);
+                    c_md = __reduce_max_sync(kFull, mygot ? (unsigned)deg : 0u);
+                }
+                if (lane == 0) {
+                    atomicOr(p.live_cur + g, any_new);
+                    atomicAdd(p.counters + 0, (unsigned long long)c_nr);
+                    atomicAdd(p.counters + 1, (unsigned long long)c_ar);
+                    if (p.lstat) {
+                        atomicAdd(p.lstat + 0, (unsigned long long)__popc(newv));
+                        atomicAdd(p.lstat + 1, (unsigned long long)c_fa);
+                        atomicMax(p.lstat + 2, (unsigned long long)c_md);
+                    }
+                }
+            }
+            if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
         }
     }
 }
@@ -1000,8 +1076,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bwd_queue_kernel(
         double acc = 0.0;
         uint32_t got = 0;
         if (gn != nullptr)
-            scan_arcs<false>(off[v], off[v + 1], want, col, gn, coef + g * n * 32, lane, acc, got,
-                             unused);
+            scan_arcs<false>((int)(off[v + 1] - off[v]), want, col + off[v], gn, coef + g * n * 32, lane,
+                             acc, got, unused);
         finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma + g * n * 32, coef + g * n * 32,
                                        STORE_DELTA ? delta + g * n * 32 : nullptr, bcg + g * n,
                                        accumulate);
