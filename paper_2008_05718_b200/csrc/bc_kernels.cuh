@@ -42,6 +42,9 @@ namespace bcb200 {
 #ifndef BC_WPB
 #define BC_WPB 4
 #endif
+#ifndef BC_PREFETCH2
+#define BC_PREFETCH2 1
+#endif
 
 constexpr int kWarpsPerBlock = BC_WPB;
 constexpr unsigned kFull = 0xffffffffu;
@@ -192,6 +195,36 @@ __device__ __forceinline__ uint32_t probe_arc(int k, int32_t w, const uint32_t *
     return __ldg(wp.lvl_ptrs[ls] + wp.goff + w);
 }
 
+// Staged row gather of one 32-arc slice: the hit arcs, compacted in arc order into a per-warp
+// list in shared memory; every lane then reads one (neighbour, hit mask) entry per arc with a
+// broadcast LDS (instead of two shuffles and a find-first-set) and adds the neighbour's row
+// under its own bit.  ~6 instructions and two L1 wavefronts per hit arc.
+template <bool BWD>
+__device__ __forceinline__ void gather_staged(unsigned any, uint32_t hit, int32_t w,
+                                              const double *__restrict__ myval, int lane,
+                                              double &acc) {
+    constexpr int kU = BWD ? BC_STAGED_UNROLL_BWD : BC_STAGED_UNROLL_FWD;  // row loads in flight
+    __shared__ int2 s_rows[kWarpsPerBlock][32 + kStagedMax];
+    int2 *lst = s_rows[threadIdx.x >> 5];
+    const int nh = __popc(any);
+    const uint32_t lbit = 1u << lane;
+    if (hit != 0) lst[__popc(any & (lbit - 1u))] = make_int2(w, (int)hit);
+    if (lane < kU) lst[nh + lane] = make_int2(0, 0);  // pad the last round: predicate off
+    __syncwarp();
+    for (int i = 0; i < nh; i += kU) {
+        int2 e[kU];
+        double x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) e[u] = lst[i + u];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            x[u] = ldg_if(myval + (size_t)e[u].x * 32, (uint32_t)e[u].y & lbit);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) acc += x[u];  // ascending arc order
+    }
+    __syncwarp();  // the next slice overwrites the list
+}
+
 template <bool COUNT_T, bool WEIGHTED = false, bool BWD = false>
 __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const int32_t *__restrict__ col,
@@ -199,7 +232,26 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const double *__restrict__ val, int lane, double &acc,
                                           uint32_t &got, unsigned &tcount,
                                           const WeightedProbe &wp = WeightedProbe{}) {
-    // arcs are [0, n_arcs) relative to `col` (and to wp.wgt): 32-bit index arithmetic
+    // arcs are [0, n_arcs) relative to `col` (and to wp.wgt): 32-bit index arithmetic.
+    // Two loads deep: the neighbour ids are fetched two slices ahead and the masks one slice
+    // ahead, so the mask probe of the next slice never waits for its own address, and the
+    // `& want` is applied where the mask is consumed, not where it is loaded.
+#if BC_PREFETCH2
+    int32_t w_c = 0, w_n = 0;
+    uint32_t m_c = 0;
+    if (lane < n_arcs) w_c = __ldg(col + lane);
+    if (lane + 32 < n_arcs) w_n = __ldg(col + 32 + lane);
+    if (lane < n_arcs) m_c = probe_arc<WEIGHTED, BWD>(lane, w_c, nmask, wp);
+    const double *myval = val + lane;
+    for (int base = 0; base < n_arcs; base += 32) {
+        const int32_t w = w_c;
+        const uint32_t hit = m_c & want;
+        w_c = w_n;
+        m_c = 0;
+        if (base + 32 + lane < n_arcs) m_c = probe_arc<WEIGHTED, BWD>(base + 32 + lane, w_c, nmask, wp);
+        w_n = 0;
+        if (base + 64 + lane < n_arcs) w_n = __ldg(col + base + 64 + lane);
+#else
     int32_t w_n = 0;
     uint32_t hit_n = 0;
     if (lane < n_arcs) {
@@ -217,6 +269,7 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
             w_n = __ldg(col + k2);
             hit_n = probe_arc<WEIGHTED, BWD>(k2, w_n, nmask, wp) & want;
         }
+#endif
         unsigned any = __ballot_sync(kFull, hit != 0);
         PROF_ADD(0, 1);
         if (any == 0) continue;
@@ -252,31 +305,9 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
             rows = 10 * nh <= 66 + 16 * (pairs / __popc(lanes_hit));
         }
         if (BC_GATHER == 3 && rows) {
-            // the hit arcs of the slice, compacted in arc order into a per-warp list in shared
-            // memory; every lane then reads one (neighbour, hit mask) entry per arc with a
-            // broadcast LDS instead of two shuffles and a find-first-set
             PROF_ADD(6, 1);
-            constexpr int kU = BWD ? BC_STAGED_UNROLL_BWD : BC_STAGED_UNROLL_FWD;  // row loads in flight
-            __shared__ int2 s_rows[kWarpsPerBlock][32 + kStagedMax];
-            int2 *lst = s_rows[threadIdx.x >> 5];
-            const int nh = __popc(any);
-            const uint32_t lbit = 1u << lane;
             got |= __reduce_or_sync(kFull, hit);
-            if (hit != 0) lst[__popc(any & (lbit - 1u))] = make_int2(w, (int)hit);
-            if (lane < kU) lst[nh + lane] = make_int2(0, 0);  // pad the last round: predicate off
-            __syncwarp();
-            for (int i = 0; i < nh; i += kU) {
-                int2 e[kU];
-                double x[kU];
-#pragma unroll
-                for (int u = 0; u < kU; ++u) e[u] = lst[i + u];
-#pragma unroll
-                for (int u = 0; u < kU; ++u)
-                    x[u] = ldg_if(myval + (size_t)e[u].x * 32, (uint32_t)e[u].y & lbit);
-#pragma unroll
-                for (int u = 0; u < kU; ++u) acc += x[u];  // ascending arc order
-            }
-            __syncwarp();  // the next slice overwrites the list
+            gather_staged<BWD>(any, hit, w, myval, lane, acc);
             continue;
         }
         if (rows) {
