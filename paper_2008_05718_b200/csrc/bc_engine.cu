@@ -166,7 +166,7 @@ struct bc_handle {
     int cur_depth = 0;        // levels of the batch being swept backward (weighted kernels)
     // options
     int groups = 4;
-    int item_arcs = 512;
+    int item_arcs = 1024;
     int reports = 1;
     int sparse = 1;        // allow queue levels + top-down push (direction-optimising switch)
     int reorder = 1;       // group sources by the size of their 2-hop neighbourhood
@@ -701,9 +701,8 @@ void prof_dump(const char *what, int L, cudaStream_t st) {
     unsigned long long v[16];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(v, g_prof, sizeof v);
-    fprintf(stderr, "[prof] %s L=%d slices=%llu any=%llu hit_arcs=%llu want_lanes=%llu pairs=%llu hit_lanes=%llu "
-                    "row_slices=%llu col_slices=%llu col_iters=%llu\n",
-            what, L, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]);
+    fprintf(stderr, "[prof] %s L=%d slices=%llu any=%llu hit_arcs=%llu want_lanes=%llu pairs=%llu hit_lanes=%llu\n",
+            what, L, v[0], v[1], v[2], v[3], v[4], v[5]);
     memset(v, 0, sizeof v);
     cudaMemcpyToSymbol(g_prof, v, sizeof v);
 }

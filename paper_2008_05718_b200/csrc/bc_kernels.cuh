@@ -8,8 +8,9 @@
 //   coef [g][v][32] f64   (1 + delta) / sigma, the value parents pull backward
 // A warp owns a vertex (or a 32-arc-aligned chunk of a hub's adjacency): it
 // filters 32 arcs at a time with lanes = arcs (one coalesced col_idx load, one
-// 4 B mask probe per arc), then for every arc that hit it switches to lanes =
-// BFS instances and gathers the neighbour's 256 B row, predicated per lane.
+// 4 B mask probe per arc), stages the arcs that hit in shared memory, then
+// switches to lanes = BFS instances and adds the neighbours' 256 B rows, one
+// row per hit arc, predicated per lane.
 // Pull direction on both phases: no atomics on fp64, sums run in CSR arc
 // order, results are bit-reproducible.
 //
@@ -24,26 +25,16 @@
 namespace bcb200 {
 
 // resident blocks per SM the compiler must allow (register cap = 65536 / (threads * blocks)):
-// the forward kernel keeps 40 registers (it spills below that), the backward kernel runs
-// better at 32 registers and full occupancy
+// the forward kernel keeps 40 registers, the backward kernel runs better at 32 registers and
+// full occupancy (measured both ways after every change of the gather loop)
 #ifndef BC_MIN_BLOCKS_FWD
 #define BC_MIN_BLOCKS_FWD 12
 #endif
 #ifndef BC_MIN_BLOCKS_BWD
 #define BC_MIN_BLOCKS_BWD 16
 #endif
-#ifndef BC_GATHER
-#define BC_GATHER 3  // 0: per-slice choice, 1: rows only, 2: columns above BC_SPARSE_SLICE hit arcs,
-                     // 3: staged rows (BC_ROW_RATIO 0: always; > 0: columns below that many instances per hit arc)
-#endif
-#ifndef BC_SPARSE_SLICE
-#define BC_SPARSE_SLICE 2
-#endif
 #ifndef BC_WPB
 #define BC_WPB 4
-#endif
-#ifndef BC_PREFETCH2
-#define BC_PREFETCH2 1
 #endif
 
 constexpr int kWarpsPerBlock = BC_WPB;
@@ -128,33 +119,6 @@ __device__ __forceinline__ double ldg_if(const double *ptr, uint32_t pred) {
     return x;
 }
 
-// 32 x 32 bit-matrix transpose across the warp: on return bit j of lane l is
-// bit l of lane j's input (five butterfly exchanges).
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-    // 16- and 8-bit stages are byte permutes (PRMT), the rest one shift + one LOP3 each
-    uint32_t o = __shfl_xor_sync(kFull, x, 16);
-    x = __byte_perm(x, o, (lane & 16) ? 0x3276 : 0x5410);
-    o = __shfl_xor_sync(kFull, x, 8);
-    x = __byte_perm(x, o, (lane & 8) ? 0x3715 : 0x6240);
-#pragma unroll
-    for (int j = 4; j != 0; j >>= 1) {
-        const uint32_t m = j == 4 ? 0x0f0f0f0fu : (j == 2 ? 0x33333333u : 0x55555555u);
-        o = __shfl_xor_sync(kFull, x, j);
-        const bool upper = lane & j;
-        const uint32_t t = upper ? (o >> j) : (o << j);
-        const uint32_t keep = upper ? ~m : m;
-        x = (x & keep) | (t & ~keep);
-    }
-    return x;
-}
-
-constexpr int kSparseSlice = BC_SPARSE_SLICE;
-#ifndef BC_ROW_UNROLL
-#define BC_ROW_UNROLL ((BC_GATHER == 2 && BC_SPARSE_SLICE <= 2) ? 2 : 4)
-#endif
-#ifndef BC_ROW_RATIO
-#define BC_ROW_RATIO 0   // BC_GATHER 3: 0 = staged rows always, else only when a hit arc serves at least this many instances on average
-#endif
 #ifndef BC_STAGED_UNROLL_FWD
 #define BC_STAGED_UNROLL_FWD 8
 #endif
@@ -162,21 +126,7 @@ constexpr int kSparseSlice = BC_SPARSE_SLICE;
 #define BC_STAGED_UNROLL_BWD 4
 #endif
 constexpr int kStagedMax = BC_STAGED_UNROLL_FWD > BC_STAGED_UNROLL_BWD ? BC_STAGED_UNROLL_FWD : BC_STAGED_UNROLL_BWD;
-constexpr int kRowUnroll = BC_ROW_UNROLL;  // row loads in flight  // slices with at most this many hit arcs take the arc-serial path
 
-// Scan arcs [a0, a1) of one vertex.  `want` (warp-uniform) = lanes that still
-// need a value.  Filter: lanes = arcs, hit = mask[neighbour] & want.  Gather,
-// two shapes:
-//   sparse slice (few arcs hit): arc-serial, lanes = BFS instances read one
-//     neighbour row, predicated per lane;
-//   dense slice: the 32 x 32 hit matrix is transposed so that lane l holds
-//     the set of arcs that hit *its* BFS instance, and every lane walks its own
-//     arc list -- the trip count is the longest column, not the number of hit
-//     arcs, and every load instruction keeps up to 32 sectors in flight.
-// Both shapes add in ascending arc order, so the sum is identical and
-// deterministic.  Four gathers are issued before the four dependent adds; the
-// next 32-arc slice is loaded before the current one is consumed.
-// tcount is a per-lane partial count of (arc, instance) hits (COUNT_T only).
 struct WeightedProbe {
     const int32_t *wgt;
     const uint32_t *const *lvl_ptrs;
@@ -225,6 +175,15 @@ __device__ __forceinline__ void gather_staged(unsigned any, uint32_t hit, int32_
     __syncwarp();  // the next slice overwrites the list
 }
 
+// Scan arcs [0, n_arcs) of one vertex, relative to `col` (and to wp.wgt): 32-bit index
+// arithmetic.  `want` (warp-uniform) = instances that still need a value.
+//   filter, lanes = arcs: one coalesced col_idx load and one 4 B mask probe per arc,
+//     hit = mask[neighbour] & want.  Two loads deep: neighbour ids are fetched two slices
+//     ahead and masks one slice ahead, so the probe of the next slice never waits for its own
+//     address, and `& want` is applied where the mask is consumed, not where it is loaded;
+//   gather, lanes = instances: gather_staged() adds the rows of the arcs that hit, in
+//     ascending arc order -- sums are deterministic and independent of the slice shape.
+// tcount is a per-lane partial count of (arc, instance) hits (COUNT_T only).
 template <bool COUNT_T, bool WEIGHTED = false, bool BWD = false>
 __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const int32_t *__restrict__ col,
@@ -232,11 +191,6 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const double *__restrict__ val, int lane, double &acc,
                                           uint32_t &got, unsigned &tcount,
                                           const WeightedProbe &wp = WeightedProbe{}) {
-    // arcs are [0, n_arcs) relative to `col` (and to wp.wgt): 32-bit index arithmetic.
-    // Two loads deep: the neighbour ids are fetched two slices ahead and the masks one slice
-    // ahead, so the mask probe of the next slice never waits for its own address, and the
-    // `& want` is applied where the mask is consumed, not where it is loaded.
-#if BC_PREFETCH2
     int32_t w_c = 0, w_n = 0;
     uint32_t m_c = 0;
     if (lane < n_arcs) w_c = __ldg(col + lane);
@@ -251,26 +205,7 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
         if (base + 32 + lane < n_arcs) m_c = probe_arc<WEIGHTED, BWD>(base + 32 + lane, w_c, nmask, wp);
         w_n = 0;
         if (base + 64 + lane < n_arcs) w_n = __ldg(col + base + 64 + lane);
-#else
-    int32_t w_n = 0;
-    uint32_t hit_n = 0;
-    if (lane < n_arcs) {
-        w_n = __ldg(col + lane);
-        hit_n = probe_arc<WEIGHTED, BWD>(lane, w_n, nmask, wp) & want;
-    }
-    const double *myval = val + lane;
-    for (int base = 0; base < n_arcs; base += 32) {
-        const int32_t w = w_n;
-        const uint32_t hit = hit_n;
-        const int k2 = base + 32 + lane;
-        w_n = 0;
-        hit_n = 0;
-        if (k2 < n_arcs) {
-            w_n = __ldg(col + k2);
-            hit_n = probe_arc<WEIGHTED, BWD>(k2, w_n, nmask, wp) & want;
-        }
-#endif
-        unsigned any = __ballot_sync(kFull, hit != 0);
+        const unsigned any = __ballot_sync(kFull, hit != 0);
         PROF_ADD(0, 1);
         if (any == 0) continue;
         PROF_ADD(1, 1);
@@ -284,94 +219,9 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
             PROF_ADD(5, prof_lanes);
         }
 #endif
-        bool rows;
-        if (BC_GATHER == 1) rows = true;
-        else if (BC_GATHER == 2) rows = __popc(any) <= kSparseSlice;
-        else if (BC_GATHER == 3) {
-            // staged rows (below): ~6 instructions and two L1 wavefronts per hit arc, against
-            // ~70 for the transpose plus ~14 per element of the longest column and one
-            // wavefront per (arc, instance) pair
-            const int nh = __popc(any);
-            const int ph = __popc(hit);
-            if (COUNT_T) tcount += ph;  // per-lane partial, lanes = arcs here
-            rows = BC_ROW_RATIO == 0 || nh <= kSparseSlice ||
-                   (int)__reduce_add_sync(kFull, ph) >= BC_ROW_RATIO * nh;
-        } else {
-            // rows cost ~10 instructions per hit arc; columns ~66 for the transpose plus ~13
-            // per element of the longest column, which is at least pairs / lanes hit
-            const int nh = __popc(any);
-            const unsigned lanes_hit = __reduce_or_sync(kFull, hit);
-            const int pairs = __reduce_add_sync(kFull, __popc(hit));
-            rows = 10 * nh <= 66 + 16 * (pairs / __popc(lanes_hit));
-        }
-        if (BC_GATHER == 3 && rows) {
-            PROF_ADD(6, 1);
-            got |= __reduce_or_sync(kFull, hit);
-            gather_staged<BWD>(any, hit, w, myval, lane, acc);
-            continue;
-        }
-        if (rows) {
-            const uint32_t lbit = 1u << lane;
-            PROF_ADD(6, 1);
-            while (any) {
-                int j[kRowUnroll];
-                int32_t wj[kRowUnroll];
-                uint32_t hj[kRowUnroll];
-                double x[kRowUnroll];
-#pragma unroll
-                for (int u = 0; u < kRowUnroll; ++u) {
-                    j[u] = __ffs(any) - 1;  // -1 when exhausted
-                    any &= any - 1;
-                }
-#pragma unroll
-                for (int u = 0; u < kRowUnroll; ++u) {
-                    wj[u] = __shfl_sync(kFull, w, j[u] & 31);
-                    hj[u] = __shfl_sync(kFull, hit, j[u] & 31);
-                    if (j[u] < 0) hj[u] = 0;
-                }
-#pragma unroll
-                for (int u = 0; u < kRowUnroll; ++u)
-                    x[u] = ldg_if(myval + (size_t)wj[u] * 32, hj[u] & lbit);
-#pragma unroll
-                for (int u = 0; u < kRowUnroll; ++u) {
-                    acc += x[u];  // arc order is kept: j[0] < j[1] < ...
-                    got |= hj[u];
-                    if (COUNT_T) tcount += (hj[u] & lbit) != 0;
-                }
-            }
-        } else {
-            got |= __reduce_or_sync(kFull, hit);
-            uint32_t c = transpose32(hit, lane);  // arcs that hit this lane's BFS instance
-            if (COUNT_T && BC_GATHER != 3) tcount += __popc(c);
-            PROF_ADD(7, 1);
-            while (__any_sync(kFull, c != 0)) {
-                PROF_ADD(8, 1);
-                const int j0 = __ffs(c) - 1;
-                const bool p0 = c != 0;
-                c &= c - 1;
-                const int j1 = __ffs(c) - 1;
-                const bool p1 = c != 0;
-                c &= c - 1;
-                const int j2 = __ffs(c) - 1;
-                const bool p2 = c != 0;
-                c &= c - 1;
-                const int j3 = __ffs(c) - 1;
-                const bool p3 = c != 0;
-                c &= c - 1;
-                const int32_t w0 = __shfl_sync(kFull, w, j0 & 31);
-                const int32_t w1 = __shfl_sync(kFull, w, j1 & 31);
-                const int32_t w2 = __shfl_sync(kFull, w, j2 & 31);
-                const int32_t w3 = __shfl_sync(kFull, w, j3 & 31);
-                const double x0 = ldg_if(myval + (size_t)w0 * 32, p0 ? 1u : 0u);
-                const double x1 = ldg_if(myval + (size_t)w1 * 32, p1 ? 1u : 0u);
-                const double x2 = ldg_if(myval + (size_t)w2 * 32, p2 ? 1u : 0u);
-                const double x3 = ldg_if(myval + (size_t)w3 * 32, p3 ? 1u : 0u);
-                acc += x0;  // ascending arc order within the lane
-                acc += x1;
-                acc += x2;
-                acc += x3;
-            }
-        }
+        if (COUNT_T) tcount += __popc(hit);  // lanes = arcs here: a per-lane partial
+        got |= __reduce_or_sync(kFull, hit);
+        gather_staged<BWD>(any, hit, w, myval, lane, acc);
     }
 }
 
