@@ -114,6 +114,26 @@ def test_hub_slices_and_item_sizes():
             assert np.allclose(bc, ref, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("b", [1, 7, 8, 9, 31, 32, 33, 40, 64, 65, 100])
+def test_staged_gather_round_boundaries(b):
+    # complete bipartite K_{a,b}: from a source in A every other vertex of A has all b vertices
+    # of B as parents, so the 32-arc slices of the level kernel carry b mod 32 (or 32) hit arcs --
+    # every fill of the staged hit-arc list around the round sizes (4 backward, 8 forward) and
+    # its padding; sources in B give single-hit slices.  sparse = 0 keeps every level on the
+    # dense pull kernel.
+    a = 6
+    edges = [(i, a + j, 1) for i in range(a) for j in range(b)]
+    g = P.from_edges(a + b, edges)
+    srcs = list(range(a + b))
+    for sparse in (0, 1):
+        with Engine(g) as e:
+            e.set_option("sparse", sparse)
+            dist, sigma, delta = e.debug_sources(srcs)
+            bc, _ = e.run(srcs)
+        assert_sources_match_oracle(g, srcs, dist, sigma, delta)
+        assert np.allclose(bc, O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
+
+
 def test_edge_cases():
     # single vertex, isolated sources, duplicate sources, empty source list,
     # disconnected components, partial last group
