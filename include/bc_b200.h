@@ -98,7 +98,9 @@ int bc_set_weights(bc_handle *h, const int32_t *weights);
  * "sparse" / "deep": frontier-queue levels / persistent multi-level sweeps;
  * "hybir_queues": 1 = BC_MODE_HYBIR sweeps of low-degree graphs run on frontier
  * queues with the Step-6 border seeds joining the queue levels, 0 = dense level
- * rows; "push_beta", "push_beta_late", "reorder": see csrc/bc_engine.cu). */
+ * rows; "row_cache": 1 = sigma / coef row gathers allocate in L1, 0 = bypass
+ * L1, -1 (default) = chosen from the degree skew of the graph; "push_beta",
+ * "push_beta_late", "reorder": see csrc/bc_engine.cu). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);
 
 /* Replaces: `Partition` + `identify_borders` + `compute_border_matrices`

@@ -110,12 +110,23 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 // Predicated read-only load: one LDG under a predicate, never a branch (the
 // compiler turns `if (p) x = __ldg(..)` into divergent control flow here).
+// NOALLOC: the line is not kept in L1.  Row gathers of a graph without hubs (Erdos-Renyi) never
+// come back to a row while it is still in L1, and allocating them only evicts the level masks:
+// -9 % on the whole pass there; on R-MAT the hubs' rows are re-read constantly and bypassing
+// L1 costs +13 %, so the host picks the variant per graph (bc_engine.cu, `row_cache`).
+template <bool NOALLOC>
 __device__ __forceinline__ double ldg_if(const double *ptr, uint32_t pred) {
     double x;
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
-        "@q ld.global.nc.f64 %0, [%1];\n\t}"
-        : "=d"(x)
-        : "l"(ptr), "r"(pred));
+    if (NOALLOC)
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
+            "@q ld.global.nc.L1::no_allocate.f64 %0, [%1];\n\t}"
+            : "=d"(x)
+            : "l"(ptr), "r"(pred));
+    else
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
+            "@q ld.global.nc.f64 %0, [%1];\n\t}"
+            : "=d"(x)
+            : "l"(ptr), "r"(pred));
     return x;
 }
 
@@ -149,7 +160,7 @@ __device__ __forceinline__ uint32_t probe_arc(int k, int32_t w, const uint32_t *
 // list in shared memory; every lane then reads one (neighbour, hit mask) entry per arc with a
 // broadcast LDS (instead of two shuffles and a find-first-set) and adds the neighbour's row
 // under its own bit.  ~6 instructions and two L1 wavefronts per hit arc.
-template <bool BWD>
+template <bool BWD, bool NOALLOC>
 __device__ __forceinline__ void gather_staged(unsigned any, uint32_t hit, int32_t w,
                                               const double *__restrict__ myval, int lane,
                                               double &acc) {
@@ -168,7 +179,7 @@ __device__ __forceinline__ void gather_staged(unsigned any, uint32_t hit, int32_
         for (int u = 0; u < kU; ++u) e[u] = lst[i + u];
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-            x[u] = ldg_if(myval + (size_t)e[u].x * 32, (uint32_t)e[u].y & lbit);
+            x[u] = ldg_if<NOALLOC>(myval + (size_t)e[u].x * 32, (uint32_t)e[u].y & lbit);
 #pragma unroll
         for (int u = 0; u < kU; ++u) acc += x[u];  // ascending arc order
     }
@@ -184,7 +195,7 @@ __device__ __forceinline__ void gather_staged(unsigned any, uint32_t hit, int32_
 //   gather, lanes = instances: gather_staged() adds the rows of the arcs that hit, in
 //     ascending arc order -- sums are deterministic and independent of the slice shape.
 // tcount is a per-lane partial count of (arc, instance) hits (COUNT_T only).
-template <bool COUNT_T, bool WEIGHTED = false, bool BWD = false>
+template <bool COUNT_T, bool WEIGHTED = false, bool BWD = false, bool NOALLOC = false>
 __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const int32_t *__restrict__ col,
                                           const uint32_t *__restrict__ nmask,
@@ -221,7 +232,7 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
 #endif
         if (COUNT_T) tcount += __popc(hit);  // lanes = arcs here: a per-lane partial
         got |= __reduce_or_sync(kFull, hit);
-        gather_staged<BWD>(any, hit, w, myval, lane, acc);
+        gather_staged<BWD, NOALLOC>(any, hit, w, myval, lane, acc);
     }
 }
 
@@ -280,7 +291,7 @@ __device__ __forceinline__ void finalize_backward(int64_t v, uint32_t mine, doub
 
 // One BFS level, forward (discover level L from level L-1) or backward
 // (accumulate level L from level L+1).  grid = (ceil(items / 8), groups).
-template <bool BWD, bool STORE_DELTA, bool WEIGHTED = false>
+template <bool BWD, bool STORE_DELTA, bool WEIGHTED = false, bool NOALLOC = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD : BC_MIN_BLOCKS_FWD) level_kernel(const LevelParams p) {
     const size_t g = blockIdx.y;
     // forward: instances still expanding; backward: instances present at this level
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         if (want != 0 && nbr != nullptr) {
             const int64_t a0 = p.chk_a0[item];
             if (WEIGHTED) wp.wgt += a0;
-            scan_arcs<!BWD, WEIGHTED, BWD>((int)(p.chk_a1[item] - a0), want, p.col + a0, nbr, val,
+            scan_arcs<!BWD, WEIGHTED, BWD, NOALLOC>((int)(p.chk_a1[item] - a0), want, p.col + a0, nbr, val,
                                            lane, acc, got, c_t, wp);
         }
         const size_t slot = g * (size_t)p.n_chk + item;
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
             if (nbr != nullptr) {
                 WeightedProbe wv = wp;
                 if (WEIGHTED) wv.wgt += vb;
-                scan_arcs<!BWD, WEIGHTED, BWD>(vd, want, colp + vb, nbr, val, lane, acc, got, c_t, wv);
+                scan_arcs<!BWD, WEIGHTED, BWD, NOALLOC>(vd, want, colp + vb, nbr, val, lane, acc, got, c_t, wv);
             }
             if (BWD) {
                 finalize_backward<STORE_DELTA>(v, want, acc, lane, sigma, coef, delta,

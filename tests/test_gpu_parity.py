@@ -125,9 +125,10 @@ def test_staged_gather_round_boundaries(b):
     edges = [(i, a + j, 1) for i in range(a) for j in range(b)]
     g = P.from_edges(a + b, edges)
     srcs = list(range(a + b))
-    for sparse in (0, 1):
+    for sparse, row_cache in ((0, 1), (0, 0), (1, -1)):   # row_cache 0: gathers bypass L1
         with Engine(g) as e:
             e.set_option("sparse", sparse)
+            e.set_option("row_cache", row_cache)
             dist, sigma, delta = e.debug_sources(srcs)
             bc, _ = e.run(srcs)
         assert_sources_match_oracle(g, srcs, dist, sigma, delta)
