@@ -172,6 +172,7 @@ struct bc_handle {
     int sparse = 1;        // allow queue levels + top-down push (direction-optimising switch)
     int reorder = 1;       // group sources by the size of their 2-hop neighbourhood
     int row_cache = -1;    // sigma / coef row gathers: 1 = allocate in L1, 0 = bypass L1, -1 = by degree skew
+    uint32_t row_bypass_mask = 0;  // dev: bit L = forward level L bypasses L1, bit 16 + L = backward level L
     int push_beta_late = 24;   // same, once a pull level has run: a late pull scans unvisited vertices only
     int push_beta = 4;     // push when frontier arcs * beta <= arcs of the graph
     int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
@@ -748,7 +749,8 @@ struct LevelTimer {
 // +13 % without).  Without hubs and at a degree that spreads the neighbours over the whole array
 // (Erdos-Renyi n = 2^22, degree 32) a row is never re-read in time and allocating it only evicts
 // the level masks: the whole pass is 9 % faster with the gathers bypassing L1.
-bool rows_bypass_l1(const bc_handle *h, const Csr &c) {
+bool rows_bypass_l1(const bc_handle *h, const Csr &c, int L, bool bwd) {
+    if (h->row_bypass_mask != 0 && L < 16) return (h->row_bypass_mask >> (L + (bwd ? 16 : 0))) & 1u;
     if (h->row_cache >= 0) return h->row_cache == 0;
     return c.n > 0 && c.n_arcs >= 8 * c.n && c.max_deg * c.n <= 16 * c.n_arcs;
 }
@@ -775,7 +777,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     if (c.wgt != nullptr)
         level_kernel<false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
-    else if (rows_bypass_l1(h, c))
+    else if (rows_bypass_l1(h, c, L, false))
         level_kernel<false, false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     else
         level_kernel<false, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -816,7 +818,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
         level_kernel<true, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     else if (store_delta)
         level_kernel<true, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
-    else if (rows_bypass_l1(h, c))
+    else if (rows_bypass_l1(h, c, L, true))
         level_kernel<true, false, false, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
     else
         level_kernel<true, false><<<grid, kWarpsPerBlock * 32, 0, st>>>(p);
@@ -2251,6 +2253,10 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     }
     if (k == "reorder") {
         h->reorder = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "row_bypass_mask") {
+        h->row_bypass_mask = (uint32_t)value;
         return BC_OK;
     }
     if (k == "row_cache") {
