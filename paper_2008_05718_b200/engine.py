@@ -157,10 +157,13 @@ def default_groups(g: Graph, n_sources: int) -> int:
     """Source groups per batch: enough lanes to fill the GPU on small graphs,
     few enough that one group's sigma slab stays L2-friendly on large ones."""
     want = max(1, (n_sources + 31) // 32)
-    budget = max(1, int(24e9 // max(1, g.num_vertices * 600)))   # ~24 GB of batch state (180 GB HBM)
-    if g.num_arcs >= 8_000_000:
-        return max(1, min(want, budget, 32))
-    return max(1, min(want, budget, 128))
+    # batch state out of 180 GB HBM: ~64 GB on shallow (high-degree) graphs, ~24 GB on low-degree
+    # ones, whose sweeps keep one mask array per level on top of it
+    shallow = g.num_arcs >= 8 * g.num_vertices
+    budget = max(1, int((64e9 if shallow else 24e9) // max(1, g.num_vertices * 600)))
+    cap = min(budget, 32 if g.num_arcs >= 8_000_000 else 128)
+    batches = (want + cap - 1) // cap
+    return max(1, (want + batches - 1) // batches)               # batches of equal size
 
 
 def open_engine(g: Graph, cfg: RunConfig, n_sources: int) -> _capi.Engine:
