@@ -19,7 +19,7 @@
  *     `bc_last_error()` returns the message;
  *   - one handle is driven by one host thread (reference is single-threaded);
  *     results are deterministic for a fixed (graph, sources, options);
- *   - unit edge weights only (every BASELINE configuration is unweighted).
+ *   - unit weights by default; positive integer arc weights through bc_set_weights.
  *
  * There is no CPU implementation behind these entry points: if the CUDA
  * runtime or a device is missing, `bc_create` fails.
@@ -77,6 +77,15 @@ typedef struct bc_stats {
     double ms_level;           /* device time of those launches alone (level kernel + its hub pass;
                                   at most 512 launches per call are timed, launches_level_timed)   */
     int64_t launches_level_timed;
+    /* batched byte model of those launches: what one launch has to move
+     * when the 32 lanes of a group share every adjacency read */
+    int64_t level_scan_arcs;    /* arcs scanned per (vertex, group): col_idx word + mask probe, 8 B */
+    int64_t level_pairs;        /* (DAG arc, lane) pairs gathered: one fp64 of sigma / coef, 8 B      */
+    int64_t level_vertex_lanes; /* fp64 values read or written per (vertex, lane), 8 B each          */
+    int64_t level_dense_words;  /* level / visited mask words swept per (vertex, group), 4 B each    */
+    int64_t level_entries;      /* (vertex, group) entries of the backward launches: 16 B BC partial */
+    int64_t level_model_bytes;  /* the sum in bytes, plus 8 B of row offsets per vertex and launch   */
+    int64_t lookahead_batches;  /* batches whose Step 1 ran ahead, beside the previous border phase  */
 } bc_stats;
 
 /* Replaces: construction of the device-side view of `Graph`
@@ -99,8 +108,11 @@ int bc_set_weights(bc_handle *h, const int32_t *weights);
  * "hybir_queues": 1 = BC_MODE_HYBIR sweeps of low-degree graphs run on frontier
  * queues with the Step-6 border seeds joining the queue levels, 0 = dense level
  * rows; "row_cache": 1 = sigma / coef row gathers allocate in L1, 0 = bypass
- * L1, -1 (default) = chosen from the degree skew of the graph; "push_beta",
- * "push_beta_late", "reorder": see csrc/bc_engine.cu). */
+ * L1, -1 (default) = chosen from the degree skew of the graph; "lookahead": 1 =
+ * BC_MODE_HYBIR issues Step 1 of the next source batch on a second stream while
+ * the border phase of the current batch runs (`pipeline_sources`, engine.py:135-143,
+ * 156-161); "l2_fetch": 32 / 64 / 128, L2 fill granularity of the device;
+ * "push_beta", "push_beta_late", "reorder": see csrc/bc_engine.cu). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);
 
 /* Replaces: `Partition` + `identify_borders` + `compute_border_matrices`
@@ -142,6 +154,13 @@ int bc_get_reports(bc_handle *h, int64_t *out, int64_t n_sources);
 int bc_get_border_counts(bc_handle *h, int64_t *counts);
 int bc_get_border_tables(bc_handle *h, int part, int32_t *borders, int32_t *bm, double *sm);
 
+/* Install the border table of `part` from host arrays (b_p x b_p row-major; bm with
+ * BC_UNREACHED = unreachable): the border-table disk cache of the reference
+ * (`load_border_matrices`, border_matrix.py:109-125) hands cached tables back
+ * through this call instead of recomputing them.  Once every part is set, BC_MODE_HYBIR
+ * runs use them as they are. */
+int bc_set_border_tables(bc_handle *h, int part, const int32_t *bm, const double *sm);
+
 /* Border frontier of the LAST batch of the last BC_MODE_HYBIR call, the
  * reference's `BorderFrontier` (forward.py:45-48): for each of the first
  * `n_lanes` sources of that batch, refined distance (BC_UNREACHED = inf), path
@@ -151,16 +170,22 @@ int bc_get_border_frontier(bc_handle *h, int64_t n_lanes, int32_t *dist, double 
                            double *arrival);
 
 /* ---- graph-partitioned multi-GPU mode: one rank = one part = one GPU -------
- * The handle is created on the rank's own CSR rows (global vertex ids, empty
- * rows for vertices of other parts).  The host code (one process per GPU,
- * torch.distributed) drives a batch level by level and moves the exported
- * buffers with NCCL all-gathers; these calls are the device side of the
- * reference's cross-worker transfers (bsp.py:83-87,128-135, ledger.py:28-31).
- * `assignment` is the global part map; border_off[world+1] / border_v list every
- * rank's border vertices (ascending ids per rank, partition.py:148). */
+ * The handle is created on the rank's LOCAL graph: its own vertices first, then its halo (the
+ * other parts' border vertices its cut arcs reach, with empty rows) and one catch-all vertex
+ * per other part for borders it has no arc to; the host code numbers them
+ * (paper_2008_05718_b200/partitioned.py: local_graph).  State arrays are therefore sized
+ * owned + halo, not n.  The host code (one process per GPU, torch.distributed) drives a batch
+ * and moves the exported buffers with NCCL; these calls are the device side of the reference's
+ * cross-worker transfers (bsp.py:83-87,128-135, backward.py:121-139, ledger.py:28-31).
+ * `assignment` maps every local vertex to its part; border_off[world+1] / border_v list every
+ * rank's border vertices in local ids (ascending global ids per rank, partition.py:148). */
 int bc_dist_setup(bc_handle *h, int rank, int world, const int32_t *assignment,
                   const int64_t *border_off, const int32_t *border_v);
-/* Start a batch of `count` sources (<= 32 * groups): every rank plants all seeds. */
+/* Cut arcs of this rank's own borders: far ends cut_dst[cut_off[j] .. cut_off[j+1]) (local halo
+ * ids) of border j -- the arcs `_cross_dependencies` walks (backward.py:46-56). */
+int bc_dist_set_cut_arcs(bc_handle *h, const int64_t *cut_off, const int32_t *cut_dst);
+/* Start a batch of `count` sources (<= 32 * groups, local ids; -1 = the source is neither owned
+ * by this rank nor in its halo: the lane exists, nothing is planted here). */
 int bc_dist_begin(bc_handle *h, const int64_t *sources, int64_t count, void *stream);
 /* Local work of forward level L (pull from level L-1) / backward level L. */
 int bc_dist_forward_level(bc_handle *h, int level, void *stream);
@@ -174,6 +199,22 @@ int bc_dist_export(bc_handle *h, int level, int what, void *masks_dev, void *val
  * the lanes visited; backward: coef under the masks exported on the way forward). */
 int bc_dist_import(bc_handle *h, int level, int what, int from, const void *masks_dev,
                    const void *values_dev, void *stream);
+/* Backward exchange at the paper's minimal sync points (backward.py:46-56,121-139).  After the
+ * forward phase of a batch, ONE call lists -- level by level -- the (border, lanes) values of
+ * this rank that a vertex of another part will pull: counts_out[2 L] entries and
+ * counts_out[2 L + 1] fp64 values at level L.  Levels where no rank has an entry need no
+ * exchange.  pack / unpack move exactly the listed values of one level through a message of
+ * [cap_values fp64][3 x cap_entries int32] (the caps are the maxima over ranks, so every rank
+ * sends the same size and one all-gather moves them); nothing in the per-level path reads
+ * back to the host. */
+int bc_dist_plan_backward(bc_handle *h, int depth, int64_t *counts_out, void *stream);
+int bc_dist_pack(bc_handle *h, int level, void *send_dev, int64_t cap_entries, int64_t cap_values,
+                 void *stream);
+int bc_dist_unpack(bc_handle *h, int level, int from, const void *recv_dev, int64_t cap_entries,
+                   int64_t cap_values, int64_t n_entries, void *stream);
+/* Kernel launches, CUDA-event time of the dense level kernel and its byte model since the last
+ * call (drains the device). */
+int bc_dist_get_stats(bc_handle *h, bc_stats *stats);
 /* live[level][g] (lanes with a non-empty frontier), read / overwrite with the OR over ranks. */
 int bc_dist_get_live(bc_handle *h, int level, uint32_t *live_out, void *stream);
 int bc_dist_set_live(bc_handle *h, int level, const uint32_t *live, void *stream);
@@ -197,10 +238,11 @@ int bc_dist_hybir_get_table(bc_handle *h, int part, int32_t *bm_dev, double *sm_
 int bc_dist_hybir_set_table(bc_handle *h, int part, const int32_t *bm_dev, const double *sm_dev);
 /* Entries of the seed arrays: total borders x 32 x groups. */
 int64_t bc_dist_hybir_seed_count(bc_handle *h);
-/* Step 1 of a batch (BFS inside this rank's part from the sources it owns); writes the border
- * seeds [border][lane] (distance, 0x3fffffff = unreached; path count) into device buffers. */
-int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, int64_t count, int32_t *seed_dist_dev,
-                        double *seed_sigma_dev, void *stream);
+/* Step 1 of a batch (BFS inside this rank's part from the sources it owns; source_part[i] = part
+ * of source i, whichever rank holds it); writes the border seeds [border][lane] (distance,
+ * 0x3fffffff = unreached; path count) into device buffers. */
+int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, const int32_t *source_part, int64_t count,
+                        int32_t *seed_dist_dev, double *seed_sigma_dev, void *stream);
 /* Steps 2-5 + path-count composition on the reduced seeds (identical on every rank), then Step 6
  * on this rank's part.  depth_out = levels seen by this rank; iterations_out = refinement
  * iterations summed over the batch's sources. */

@@ -10,11 +10,12 @@ need a GPU, calling ``run_bc`` does (there is no CPU fallback).
 
 from .errors import (ContractViolation, DomainError, EngineError, FormatError, HybirError,
                      InputError, ParseError)
-from .graph import (Graph, as_graph, from_edge_arrays, from_edges, graph_stats, load_edge_list,
-                    write_edge_list)
+from .graph import (Graph, as_graph, from_edge_arrays, from_edges, graph_stats, load_dimacs_gr,
+                    load_edge_list, write_edge_list)
 from .partition import (BorderSet, Partition, block_partition, greedy_bipartition, grow_partition,
-                        identify_borders, import_partition, single_partition, strip_partition)
-from .engine import (CommTotals, RunConfig, RunResult, build_report, pipeline_sources, run_bc,
-                     select_sources)
+                        identify_borders, import_partition, mincut_partition, refine_partition,
+                        single_partition, strip_partition)
+from .engine import (CommTotals, RunConfig, RunResult, border_table_bytes, build_report, choose_mode,
+                     pipeline_sources, run_bc, select_sources)
 
 __version__ = "0.1.0"

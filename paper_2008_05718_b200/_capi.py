@@ -25,8 +25,9 @@ MODE_DIRECT, MODE_HYBIR, MODE_BSP = 0, 1, 2
 SYMBOLS = (
     "bc_create", "bc_set_weights", "bc_set_option", "bc_set_partition", "bc_run", "bc_run_device",
     "bc_debug_sources", "bc_get_reports", "bc_get_border_counts", "bc_get_border_tables",
-    "bc_get_border_frontier",
-    "bc_dist_setup", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
+    "bc_get_border_frontier", "bc_set_border_tables",
+    "bc_dist_setup", "bc_dist_set_cut_arcs", "bc_dist_plan_backward", "bc_dist_pack", "bc_dist_unpack",
+    "bc_dist_get_stats", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
     "bc_dist_export", "bc_dist_import", "bc_dist_get_live", "bc_dist_set_live", "bc_dist_finish",
     "bc_dist_hybir_setup", "bc_dist_hybir_get_table", "bc_dist_hybir_set_table",
     "bc_dist_hybir_seed_count", "bc_dist_hybir_seeds", "bc_dist_hybir_forward", "bc_dist_hybir_set_depth",
@@ -46,6 +47,10 @@ class BcStats(ctypes.Structure):
         ("launches_forward", ctypes.c_int64), ("launches_backward", ctypes.c_int64),
         ("launches_level", ctypes.c_int64),
         ("ms_level", ctypes.c_double), ("launches_level_timed", ctypes.c_int64),
+        ("level_scan_arcs", ctypes.c_int64), ("level_pairs", ctypes.c_int64),
+        ("level_vertex_lanes", ctypes.c_int64), ("level_dense_words", ctypes.c_int64),
+        ("level_entries", ctypes.c_int64), ("level_model_bytes", ctypes.c_int64),
+        ("lookahead_batches", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -89,10 +94,22 @@ def load():
     L.bc_get_border_counts.argtypes = [vp, vp]
     L.bc_get_border_tables.restype = cint
     L.bc_get_border_tables.argtypes = [vp, cint, vp, vp, vp]
+    L.bc_set_border_tables.restype = cint
+    L.bc_set_border_tables.argtypes = [vp, cint, vp, vp]
     L.bc_get_border_frontier.restype = cint
     L.bc_get_border_frontier.argtypes = [vp, i64, vp, vp, vp]
     L.bc_dist_setup.restype = cint
     L.bc_dist_setup.argtypes = [vp, cint, cint, vp, vp, vp]
+    L.bc_dist_set_cut_arcs.restype = cint
+    L.bc_dist_set_cut_arcs.argtypes = [vp, vp, vp]
+    L.bc_dist_plan_backward.restype = cint
+    L.bc_dist_plan_backward.argtypes = [vp, cint, vp, vp]
+    L.bc_dist_pack.restype = cint
+    L.bc_dist_pack.argtypes = [vp, cint, vp, i64, i64, vp]
+    L.bc_dist_unpack.restype = cint
+    L.bc_dist_unpack.argtypes = [vp, cint, cint, vp, i64, i64, i64, vp]
+    L.bc_dist_get_stats.restype = cint
+    L.bc_dist_get_stats.argtypes = [vp, ctypes.POINTER(BcStats)]
     L.bc_dist_begin.restype = cint
     L.bc_dist_begin.argtypes = [vp, vp, i64, vp]
     L.bc_dist_forward_level.restype = cint
@@ -118,7 +135,7 @@ def load():
     L.bc_dist_hybir_seed_count.restype = i64
     L.bc_dist_hybir_seed_count.argtypes = [vp]
     L.bc_dist_hybir_seeds.restype = cint
-    L.bc_dist_hybir_seeds.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.bc_dist_hybir_seeds.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     L.bc_dist_hybir_forward.restype = cint
     L.bc_dist_hybir_forward.argtypes = [vp, vp, vp, ctypes.POINTER(cint), ctypes.POINTER(i64), vp]
     L.bc_dist_hybir_set_depth.restype = cint
@@ -266,6 +283,17 @@ class Engine:
             self._raise(rc)
         return borders, bm, sm
 
+    def set_border_tables(self, part: int, bm, sm):
+        """Install the border table of one part from host arrays (a cache hit): bm int32 with
+        -1 = unreachable, sm float64, both b_p x b_p."""
+        bm = np.ascontiguousarray(bm, dtype=np.int32)
+        sm = np.ascontiguousarray(sm, dtype=np.float64)
+        if bm.shape != sm.shape or bm.ndim != 2 or bm.shape[0] != bm.shape[1]:
+            raise InputError("border tables must be square and of equal shape")
+        rc = self._lib.bc_set_border_tables(self._h, int(part), _ptr(bm), _ptr(sm))
+        if rc != BC_OK:
+            self._raise(rc)
+
     def border_frontier(self, n_lanes: int, total_borders: int):
         """(dist, sigma, arrival) of the last hybir batch, each [B, n_lanes]."""
         d = np.zeros((total_borders, n_lanes), dtype=np.int32)
@@ -336,10 +364,37 @@ class Engine:
     def dist_hybir_seed_count(self) -> int:
         return int(self._lib.bc_dist_hybir_seed_count(self._h))
 
-    def dist_hybir_seeds(self, sources, seed_dist_ptr, seed_sigma_ptr, stream=0):
+    def dist_hybir_seeds(self, sources, source_part, seed_dist_ptr, seed_sigma_ptr, stream=0):
         src = np.ascontiguousarray(sources, dtype=np.int64)
-        self._ck(self._lib.bc_dist_hybir_seeds(self._h, _ptr(src), len(src), ctypes.c_void_p(seed_dist_ptr),
-                                               ctypes.c_void_p(seed_sigma_ptr), ctypes.c_void_p(stream or None)))
+        sp = np.ascontiguousarray(source_part, dtype=np.int32)
+        self._ck(self._lib.bc_dist_hybir_seeds(self._h, _ptr(src), _ptr(sp), len(src),
+                                               ctypes.c_void_p(seed_dist_ptr), ctypes.c_void_p(seed_sigma_ptr),
+                                               ctypes.c_void_p(stream or None)))
+
+    def dist_set_cut_arcs(self, cut_off, cut_dst):
+        co = np.ascontiguousarray(cut_off, dtype=np.int64)
+        cd = np.ascontiguousarray(cut_dst, dtype=np.int32)
+        self._ck(self._lib.bc_dist_set_cut_arcs(self._h, _ptr(co), _ptr(cd)))
+
+    def dist_plan_backward(self, depth, stream=0):
+        """(entries, values) per level this rank has to publish on the way back: int64[depth, 2]."""
+        out = np.zeros((int(depth), 2), dtype=np.int64)
+        self._ck(self._lib.bc_dist_plan_backward(self._h, int(depth), _ptr(out), ctypes.c_void_p(stream or None)))
+        return out
+
+    def dist_pack(self, level, send_ptr, cap_entries, cap_values, stream=0):
+        self._ck(self._lib.bc_dist_pack(self._h, int(level), ctypes.c_void_p(send_ptr), int(cap_entries),
+                                        int(cap_values), ctypes.c_void_p(stream or None)))
+
+    def dist_unpack(self, level, peer, recv_ptr, cap_entries, cap_values, n_entries, stream=0):
+        self._ck(self._lib.bc_dist_unpack(self._h, int(level), int(peer), ctypes.c_void_p(recv_ptr),
+                                          int(cap_entries), int(cap_values), int(n_entries),
+                                          ctypes.c_void_p(stream or None)))
+
+    def dist_stats(self) -> dict:
+        st = BcStats()
+        self._ck(self._lib.bc_dist_get_stats(self._h, ctypes.byref(st)))
+        return st.as_dict()
 
     def dist_hybir_forward(self, seed_dist_ptr, seed_sigma_ptr, stream=0):
         depth, iters = ctypes.c_int(0), ctypes.c_int64(0)

@@ -63,6 +63,15 @@ __global__ void fill_border_kernel(int32_t *D, int32_t *seedD, double *seedS, do
     }
 }
 
+// Step-1 border seeds of a batch before the gather: unreached everywhere.
+__global__ void fill_seed_kernel(int32_t *seedD, double *seedS, size_t count) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (size_t)gridDim.x * blockDim.x) {
+        seedD[i] = kInf;
+        seedS[i] = 0.0;
+    }
+}
+
 // Read (dist, sigma) of every border vertex out of the BFS state: lvl[L][g][v]
 // bit = "lane is at distance L".  One thread per (border, lane).
 // A group whose lanes all died before level L never wrote lvl[L] (the level
@@ -422,12 +431,14 @@ __global__ void lane_step_kernel(int S, uint32_t *lane_active, uint32_t *lane_ch
 
 // Largest finite border distance that carries an arrival count: Step 6 must
 // keep stepping levels at least that far even through empty frontiers.
+// all_finite: every border with a finite distance counts (graph-partitioned runs mark the other
+// parts' borders at their level whether or not a cut arc arrives there, see inject_seeds_kernel).
 __global__ void max_seed_level_kernel(const int32_t *D, const double *arr, size_t count,
-                                      int *out) {
+                                      int *out, int all_finite) {
     int m = -1;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (size_t)gridDim.x * blockDim.x)
-        if (D[i] < kInf && arr[i] != 0.0) m = max(m, D[i]);
+        if (D[i] < kInf && (all_finite || arr[i] != 0.0)) m = max(m, D[i]);
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(out, m);
 }
@@ -436,16 +447,20 @@ __global__ void max_seed_level_kernel(const int32_t *D, const double *arr, size_
 // arr[j] when D[j] is finite and arr[j] != 0.  Runs after the pull of level L:
 // a border the pull just discovered at L keeps its pulled count and adds the
 // base (relax.py:70-71,95-99); one found at a smaller level ignores the seed.
+// own_part >= 0 (graph-partitioned runs, one part per rank): borders of the OTHER parts have no
+// rows on this rank; they are only marked at their level -- all of them, also those no cut arc
+// arrives at -- because the backward exchange plan reads those marks to find the cross-part
+// parents of this rank's borders (dist_plan_kernel).
 __global__ void inject_seeds_kernel(BorderGeom geo, int S, int lanes, const int32_t *D,
                                     const double *arr, int level, int64_t n, uint32_t *vis,
-                                    uint32_t *cur, double *sigma, uint32_t *live_cur) {
+                                    uint32_t *cur, double *sigma, uint32_t *live_cur, int own_part) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)geo.B * S) return;
     const int lane_all = (int)(idx % S);
     if (lane_all >= lanes || D[idx] != level) return;
     const double base = arr[idx];
-    if (base == 0.0) return;
     const int j = (int)(idx / S);
+    if (base == 0.0 && (own_part < 0 || geo.border_p[j] == own_part)) return;
     const size_t g = lane_all >> 5;
     const uint32_t bit = 1u << (lane_all & 31);
     const int64_t v = geo.border_v[j];

@@ -1,8 +1,9 @@
 // bc_dist.cuh -- border exchange kernels of the graph-partitioned multi-GPU mode.
 //
-// One rank = one part = one GPU.  A rank holds the CSR rows of its own vertices
-// and full-length state arrays; after every level only the *border* vertices'
-// new state crosses the NVLink fabric (the paper's exchange points, reference
+// One rank = one part = one GPU.  A rank holds the CSR rows of its own vertices and
+// state arrays over its own vertices plus a halo (the other parts' border vertices next to
+// them; the host numbers them locally, paper_2008_05718_b200/partitioned.py); after a level
+// only the *border* vertices' new state crosses the NVLink fabric (the paper's exchange points, reference
 // PAPER.md:408-458; the level-synchronous schedule is the reference's
 // bsp_forward / bsp_backward, bsp.py:22-142, batched over 32 * groups sources):
 //   forward  level L : masks lvl[L][g][b] of my borders b, then sigma[b][lane]
@@ -77,6 +78,90 @@ __global__ void dist_import_values_kernel(const double *values, const int32_t *b
     const size_t g = i % ng;
     double *row = val + (g * n + border_v[j]) * 32;
     const double *in = values + offsets[i];
+    while (m) {
+        const int lane = __ffs(m) - 1;
+        m &= m - 1;
+        row[lane] = *in++;
+    }
+}
+
+// ---- backward exchange plan ("minimal sync points", reference backward.py:46-56,121-139) ------
+// A rank has to publish coef of its border vertex b at level L for lane l only if a vertex of
+// ANOTHER part at level L - 1 pulls it: some cut arc (b, u) with lvl[L-1][u] holding l.  The plan
+// lists those (border, group, lanes) entries level by level once per batch; levels without an
+// entry on any rank need no exchange at all, and the others move exactly the listed values.
+// One thread per (own border, group) walks the levels.  fill = 0: count entries / values per
+// level; fill = 1: write the entries at eoff[L] + cursor and reserve their value slots.
+struct DistPlan {
+    int32_t *ent_idx;    // border * ng + group (border = index among this rank's borders)
+    uint32_t *ent_mask;  // lanes to publish
+    int32_t *ent_voff;   // first value slot inside the level's message
+    const int32_t *eoff; // [depth + 1] first entry of each level
+    int32_t *cnt_e;      // [depth] entries per level (fill = 0) / cursors (fill = 1)
+    int32_t *cnt_v;      // [depth] values per level / cursors
+};
+
+__global__ void dist_plan_kernel(const uint32_t *const *lvl, const uint32_t *live, int G, int depth,
+                                 const int32_t *border_v, int nb, int ng, int64_t n,
+                                 const int64_t *cut_off, const int32_t *cut_dst, int fill,
+                                 DistPlan plan) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb * ng) return;
+    const int j = i / ng;
+    const size_t g = i % ng;
+    const int64_t b = border_v[j];
+    const int64_t c0 = cut_off[j], c1 = cut_off[j + 1];
+    for (int L = 2; L < depth; ++L) {      // level 1 is pulled by the sources only (level 0: not run)
+        if (live[(size_t)L * G + g] == 0) continue;
+        const uint32_t m = lvl[L][g * n + b];
+        if (m == 0) continue;
+        uint32_t parents = 0;
+        for (int64_t c = c0; c < c1; ++c) parents |= lvl[L - 1][g * n + cut_dst[c]];
+        const uint32_t need = m & parents;
+        if (need == 0) continue;
+        if (!fill) {
+            atomicAdd(plan.cnt_e + L, 1);
+            atomicAdd(plan.cnt_v + L, __popc(need));
+        } else {
+            const int at = plan.eoff[L] + atomicAdd(plan.cnt_e + L, 1);
+            plan.ent_idx[at] = i;
+            plan.ent_mask[at] = need;
+            plan.ent_voff[at] = atomicAdd(plan.cnt_v + L, __popc(need));
+        }
+    }
+}
+
+// Message of one level: [cap_v fp64 values][3 x cap_e int32: idx, mask, value offset].
+__global__ void dist_pack_kernel(const double *val, const int32_t *border_v, int ng, int64_t n,
+                                 const int32_t *ent_idx, const uint32_t *ent_mask,
+                                 const int32_t *ent_voff, int count, double *values, int32_t *head,
+                                 int64_t cap_e) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    const int i = ent_idx[e];
+    uint32_t m = ent_mask[e];
+    const int voff = ent_voff[e];
+    head[e] = i;
+    head[cap_e + e] = (int32_t)m;
+    head[2 * cap_e + e] = voff;
+    const double *row = val + ((size_t)(i % ng) * n + border_v[i / ng]) * 32;
+    double *out = values + voff;
+    while (m) {
+        const int lane = __ffs(m) - 1;
+        m &= m - 1;
+        *out++ = row[lane];
+    }
+}
+
+__global__ void dist_unpack_kernel(double *val, const int32_t *border_v, int ng, int64_t n,
+                                   const double *values, const int32_t *head, int64_t cap_e,
+                                   int count) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    const int i = head[e];
+    uint32_t m = (uint32_t)head[cap_e + e];
+    const double *in = values + head[2 * cap_e + e];
+    double *row = val + ((size_t)(i % ng) * n + border_v[i / ng]) * 32;
     while (m) {
         const int lane = __ffs(m) - 1;
         m &= m - 1;

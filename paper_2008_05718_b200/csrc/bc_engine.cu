@@ -16,6 +16,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -23,6 +24,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -143,8 +145,26 @@ struct Csr {
     int32_t *hub_v = nullptr, *hub_c0 = nullptr, *hub_nc = nullptr;
 };
 
+// Events of one batch; destroyed with the vector that holds them, on every exit path.
 struct Events {
-    cudaEvent_t start, fwd_end, border_end, fwd2_end, bwd_end;
+    cudaEvent_t start = nullptr, fwd_end = nullptr, border_end = nullptr, fwd2_end = nullptr, bwd_end = nullptr;
+    Events() = default;
+    Events(const Events &) = delete;
+    Events &operator=(const Events &) = delete;
+    ~Events() {
+        for (cudaEvent_t e : {start, fwd_end, border_end, fwd2_end, bwd_end})
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+// Arena block released when the scope ends (error exits included).
+template <typename T>
+struct ScopedBlock {
+    T *p = nullptr;
+    ScopedBlock() = default;
+    ScopedBlock(const ScopedBlock &) = delete;
+    ScopedBlock &operator=(const ScopedBlock &) = delete;
+    ~ScopedBlock() { arena_free(p); }
 };
 
 constexpr unsigned long long kQueueMaxDegree = 8192;
@@ -211,6 +231,14 @@ struct bc_handle {
     int32_t *D = nullptr, *D2 = nullptr, *seedD = nullptr, *Dfin = nullptr;
     double *seedS = nullptr, *sig = nullptr, *arr = nullptr, *darr = nullptr;
     int32_t *lane_part = nullptr, *lane_iters = nullptr;
+    // look-ahead (engine.py:135-143): Step 1 of the next batch runs on a second stream while the
+    // border phase of the current one is in flight and leaves its border seeds here
+    int lookahead = 0;
+    int32_t *seedD_alt = nullptr, *lane_part_alt = nullptr;
+    double *seedS_alt = nullptr;
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t side_go = nullptr, side_done = nullptr;
+    std::vector<bool> table_set;   // parts whose border table was installed by bc_set_border_tables
     uint32_t *lane_active = nullptr, *lane_entered = nullptr, *lane_changed = nullptr;
     uint32_t *dflags = nullptr;    // [0] any lane active, [1] sigma changed
     int *d_maxlvl = nullptr;
@@ -233,6 +261,7 @@ struct bc_handle {
     bool lazy_clear = false;    // this batch's backward sweep clears sigma behind itself
     int last_depth = 0;         // levels of the previous batch (deep graphs: memset instead)
     double *bcg = nullptr;
+    bool bcg_dirty = true;      // partial sums of an unfinished (failed) run are in there: clear first
     double *pacc = nullptr;
     uint32_t *pmask = nullptr;
     int pacc_chunks = 0;
@@ -266,9 +295,19 @@ struct bc_handle {
     void *dist_scan_tmp = nullptr;
     size_t dist_scan_bytes = 0;
     int64_t dist_entries_cap = 0;
+    // backward exchange plan of the batch in flight (bc_dist_plan_backward)
+    int64_t *dist_cut_off = nullptr;    // [own borders + 1] cut arcs of this rank's borders
+    int32_t *dist_cut_dst = nullptr;    // their far ends (local vertex ids of the halo)
+    int32_t *plan_idx = nullptr, *plan_voff = nullptr, *plan_eoff = nullptr, *plan_cnt_e = nullptr, *plan_cnt_v = nullptr;
+    uint32_t *plan_mask = nullptr;
+    int64_t plan_cap = 0;
+    int plan_levels_cap = 0, plan_depth = 0;
+    std::vector<int32_t> plan_eoff_h, plan_cnt_e_h, plan_cnt_v_h;
     std::string err;
-    int64_t launches = 0;
+    std::atomic<int64_t> launches{0};   // (the look-ahead thread launches too)
     int64_t level_launches = 0;   // dense level kernel only
+    // batched byte model of the dense level-kernel launches of the current call
+    int64_t model_scan = 0, model_pairs = 0, model_vlanes = 0, model_dense_words = 0, model_entries = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> level_events;   // around those launches (<= 512 per call)
 
     int fail(int code, const std::string &msg) {
@@ -431,6 +470,9 @@ void free_state(bc_handle *h) {
 void free_border_state(bc_handle *h) {
     arena_free(h->D), arena_free(h->D2), arena_free(h->seedD), arena_free(h->Dfin);
     arena_free(h->seedS), arena_free(h->sig), arena_free(h->arr), arena_free(h->darr);
+    arena_free(h->seedD_alt), arena_free(h->seedS_alt), arena_free(h->lane_part_alt);
+    h->seedD_alt = h->lane_part_alt = nullptr;
+    h->seedS_alt = nullptr;
     h->darr = nullptr;
     arena_free(h->seed_keys), arena_free(h->seed_keys2), arena_free(h->seed_vals), arena_free(h->seed_vals2);
     arena_free(h->seed_off), arena_free(h->seed_tmp);
@@ -464,6 +506,7 @@ void free_partition(bc_handle *h) {
     h->bm = nullptr;
     h->sm = nullptr;
     h->tables_ready = false;
+    h->table_set.clear();
     h->k = 1;
     h->B = 0;
     h->n_cut = 0;
@@ -478,7 +521,7 @@ int ensure_state(bc_handle *h, int groups, bool want_delta) {
         CUDA_TRY(h, arena_malloc((void **)&h->sigma, groups * n * 32 * sizeof(double)));
         CUDA_TRY(h, arena_malloc((void **)&h->coef, groups * n * 32 * sizeof(double)));
         CUDA_TRY(h, arena_malloc((void **)&h->bcg, groups * n * sizeof(double)));
-        CUDA_TRY(h, cudaMemset(h->bcg, 0, groups * n * sizeof(double)));
+        h->bcg_dirty = true;   // cleared on the caller's stream by the run that uses it
         h->alloc_groups = groups;
         h->sigma_clean = false;
     }
@@ -548,8 +591,8 @@ int ensure_queues(bc_handle *h) {
     CUDA_TRY(h, cudaMemset(h->d_qlbeg, 0, G * sizeof(int64_t)));
     TRY(dev_alloc(h, &h->scrA, G * n));
     TRY(dev_alloc(h, &h->scrB, G * n));
-    TRY(dev_alloc(h, &h->lstat, (size_t)4));
-    TRY(dev_alloc(h, &h->report, 4 + 2 * G));
+    TRY(dev_alloc(h, &h->lstat, (size_t)8));
+    TRY(dev_alloc(h, &h->report, 8 + 2 * G));
     h->heavy_cap = (int64_t)G * std::max(h->full.heavy_slices, h->intra.heavy_slices) + 1;
     TRY(dev_alloc(h, &h->heavy, (size_t)h->heavy_cap));
     CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
@@ -764,6 +807,11 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     p.nbr = nbr ? nbr : h->lvl[L - 1];
     p.cur = cur ? cur : h->lvl[L];
     p.lstat = lstat;
+    if (h->dist_rank >= 0 && lstat == nullptr) {
+        // graph-partitioned runs: running totals for the byte model (bc_dist_get_stats)
+        p.lstat = h->lstat;
+        h->model_dense_words += 2 * c.n * ng;
+    }
     p.live_prev = h->live + (size_t)(L - 1) * h->alloc_groups;
     p.live_cur = h->live + (size_t)L * h->alloc_groups;
     p.level = L;
@@ -810,6 +858,7 @@ int launch_backward(bc_handle *h, const Csr &c, int L, bool deepest, int ng, boo
     p.accumulate_bc = (accumulate ? 1 : 0) | (h->lazy_clear ? 2 : 0);
     p.level = L;
     p.max_level = h->cur_depth - 1;
+    if (h->dist_rank >= 0) h->model_dense_words += c.n * ng;
     LevelTimer timer(h, st);
     const dim3 grid(blocks_for((int64_t)c.n_chk + c.n_rng), ng);
     if (c.wgt != nullptr && store_delta)
@@ -899,7 +948,8 @@ int forward_sweep(bc_handle *h, const Csr &c, int ng, cudaStream_t st, int *dept
                 const size_t cnt = (size_t)h->B * h->border_S;
                 inject_seeds_kernel<<<grid1d(cnt), 256, 0, st>>>(
                     border_geom(h), h->border_S, lanes, h->D, h->arr, L + j, h->n, h->vis,
-                    h->lvl[L + j], h->sigma, h->live + (size_t)(L + j) * G);
+                    h->lvl[L + j], h->sigma, h->live + (size_t)(L + j) * G,
+                    h->dist_hybir ? h->dist_rank : -1);
                 ++h->launches;
             }
         }
@@ -951,6 +1001,9 @@ struct LevelRep {
     unsigned long long nverts = 0, farcs = 0;  // vertices in the level, their arcs (all groups)
     unsigned long long maxdeg = 0;             // largest degree in the level
     long long heavy = 0;   // slice records of its heavy entries in h->heavy (-1: not built)
+    // batched byte model; -1 = not recorded (levels of a persistent run)
+    long long vlanes = -1;   // (vertex, lane) pairs sitting at this level
+    long long pairs = -1;    // (DAG arc, lane) pairs between the previous level and this one
 };
 
 QueueParams queue_params(bc_handle *h) {
@@ -1061,11 +1114,13 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         }
         CUDA_TRY(h, cudaMemcpyAsync(h->q_count, qcount.data(), G * sizeof(unsigned long long),
                                     cudaMemcpyHostToDevice, st));
-        CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 4 * sizeof(unsigned long long), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 8 * sizeof(unsigned long long), st));
         if (!heavy0.empty())
             CUDA_TRY(h, cudaMemcpyAsync(h->heavy, heavy0.data(), heavy0.size() * sizeof(HeavyRec),
                                         cudaMemcpyHostToDevice, st));
         r0.heavy = (long long)heavy0.size();
+        r0.vlanes = cnt;
+        r0.pairs = 0;
         CUDA_TRY(h, cudaStreamSynchronize(st));  // the staging vectors go out of scope
     }
     auto upload_lbeg = [&]() -> int {
@@ -1079,7 +1134,8 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
     int device_level = -1;  // level whose ranges sit in d_qbeg / d_qend (and d_qlbeg = q_count)
     int next_slot = 1;
     const unsigned long long graph_arcs = (unsigned long long)std::max<int64_t>(c.n_arcs, 1) * ng;
-    std::vector<unsigned long long> report(4 + 2 * G);
+    std::vector<unsigned long long> report(8 + 2 * G);
+    unsigned long long seen_vl = 0, seen_pairs = 0;   // running totals at the previous level
     for (int L = 1;; ++L) {
         TRY(ensure_live(h, L + 1));
         reps.emplace_back();
@@ -1240,7 +1296,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         }
         advance_level_kernel<<<1, (unsigned)std::max<size_t>(G, 32), 0, st>>>(
             h->lstat, h->q_count, h->live + (size_t)L * G, h->d_qbeg, h->d_qend, h->d_qlbeg, (int)G,
-            h->report);
+            h->report, h->counters + h->cnt_off);
         ++h->launches;
         CUDA_TRY(h, cudaGetLastError());
         CUDA_TRY(h, cudaMemcpyAsync(report.data(), h->report, report.size() * sizeof(unsigned long long),
@@ -1257,6 +1313,19 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
         cur.farcs = report[1];
         cur.maxdeg = report[2];
         cur.heavy = (long long)report[3 + 2 * G];
+        cur.vlanes = (long long)(report[4 + 2 * G] - seen_vl);
+        cur.pairs = (long long)(report[5 + 2 * G] - seen_pairs);
+        seen_vl = report[4 + 2 * G];
+        seen_pairs = report[5 + 2 * G];
+        if (!cur.queued) {
+            // a dense pull produced this level: arcs scanned (col_idx + mask probe), sigma rows
+            // gathered per (hit arc, lane), sigma written per (vertex, lane), vis read + level
+            // mask written per (vertex, group)
+            h->model_scan += (int64_t)report[6 + 2 * G];
+            h->model_pairs += cur.pairs;
+            h->model_vlanes += cur.vlanes;
+            h->model_dense_words += 2 * n * ng;
+        }
         for (size_t g = 0; g < G; ++g) qcount[g] = report[3 + g];
         if (cur.queued) cur.qe.assign(qcount.begin(), qcount.begin() + ng);
     }
@@ -1358,7 +1427,19 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             L = lo;
             continue;
         }
+        auto model_backward = [&]() {
+            // dense backward launch at level L: arcs of the (vertex, group) entries at L scanned,
+            // coef gathered per (DAG arc, lane) towards L + 1, sigma read + coef written (+ sigma
+            // cleared) per (vertex, lane), level mask read per (vertex, group), BC partial
+            // read + written per entry
+            h->model_scan += (int64_t)r.farcs;
+            if (!deepest && reps[L + 1].pairs >= 0) h->model_pairs += reps[L + 1].pairs;
+            if (r.vlanes >= 0) h->model_vlanes += (h->lazy_clear ? 3 : 2) * r.vlanes;
+            h->model_dense_words += h->n * ng;
+            h->model_entries += (int64_t)r.nverts;
+        };
         if (r.slot >= 0) {
+            model_backward();
             TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, h->lvl[r.slot], nbr));
         } else if (r.farcs * (unsigned long long)h->push_beta <= graph_arcs && r.maxdeg <= kQueueMaxDegree) {
             QueueParams q = queue_params(h);
@@ -1382,6 +1463,7 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             CUDA_TRY(h, cudaGetLastError());
         } else {  // a queue level with heavy vertices: run it through the dense kernel (hub slices)
             cur_holder = holder == 0 ? 1 : 0;
+            model_backward();
             TRY(swap_scatter(-1, -1, L, cur_holder));
             TRY(launch_backward(h, c, L, deepest, ng, debug, !debug, st, scr[cur_holder], nbr));
         }
@@ -1501,6 +1583,9 @@ int ensure_border_state(bc_handle *h, int S) {
     TRY(dev_alloc(h, &h->darr, cnt));
     TRY(dev_alloc(h, &h->sync_flag, cnt));
     TRY(dev_alloc(h, &h->lane_part, (size_t)S));
+    TRY(dev_alloc(h, &h->seedD_alt, cnt));
+    TRY(dev_alloc(h, &h->seedS_alt, cnt));
+    TRY(dev_alloc(h, &h->lane_part_alt, (size_t)S));
     TRY(dev_alloc(h, &h->lane_iters, (size_t)S));
     TRY(dev_alloc(h, &h->lane_active, (size_t)S));
     TRY(dev_alloc(h, &h->lane_entered, (size_t)S));
@@ -1534,10 +1619,16 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
                                           h->lane_entered, h->n_cut);
     ++h->launches;
     if (h->B > 0 && h->n_cut > 0) {
-        const int max_iter = max_b + 2;
+        // Two parts: the reference's bound max(b0, b1) + 2 (forward.py:118,130-133).  k > 2: one
+        // iteration settles one more part crossing of the shortest paths, and a path enters a
+        // distinct border at every crossing, so the bound is the total border count.
+        const int max_iter = (h->k == 2 ? max_b : h->B) + 2;
+        // The host looks at the "any lane still active" flag only every `poll` iterations (1, 1,
+        // 2, 3, 4, 4, ...): an iteration without active lanes changes nothing (inactive lanes are
+        // masked in every kernel and lane_step_kernel counts iterations of active lanes only), so
+        // running a few past convergence costs less than a device round trip per iteration.
+        int poll = 1, since_poll = 0;
         for (int it = 0;; ++it) {
-            if (it > max_iter)
-                return h->fail(BC_ERR_INTERNAL, "border refinement exceeded the border-count bound");
             if (h->k == 2) {
                 cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D, h->lane_part, h->lane_active,
                                                      kApplyOther, nullptr, h->sync_flag);
@@ -1565,10 +1656,15 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
             lane_step_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->lane_iters,
                                                  h->dflags);
             ++h->launches;
+            if (++since_poll < poll) continue;
+            since_poll = 0;
+            poll = std::min(4, 1 + (it + 1) / 2);
             uint32_t any = 0;
             CUDA_TRY(h, cudaMemcpyAsync(&any, h->dflags, sizeof any, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(h, cudaStreamSynchronize(st));
             if (!any) break;
+            if (it > max_iter + 4)
+                return h->fail(BC_ERR_INTERNAL, "border refinement exceeded the border-count bound");
         }
         if (h->k == 2) {
             // 'step2-final' (forward.py:134-135) for every lane that ran the loop
@@ -1585,8 +1681,9 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
         CUDA_TRY(h, cudaMemsetAsync(h->lane_active, 1, S * sizeof(uint32_t), st));
         CUDA_TRY(h, cudaMemsetAsync(h->lane_changed, 0, S * sizeof(uint32_t), st));
         CUDA_TRY(h, cudaMemsetAsync(h->arr, 0, cnt * sizeof(double), st));
+        int poll = 1, since_poll = 0;   // as above: a round without running lanes is a no-op
         for (int round = 0;; ++round) {
-            if (round > 2 * h->B + 4)
+            if (round > 2 * h->B + 8)
                 return h->fail(BC_ERR_INTERNAL, "border sigma composition did not settle");
             arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->darr, h->lane_active,
                                                h->sync_flag);   // (sync_flag is free until the reports)
@@ -1597,6 +1694,9 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
                                                         h->sync_flag);
             lane_round_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->dflags + 1);
             h->launches += 3;
+            if (++since_poll < poll) continue;
+            since_poll = 0;
+            poll = std::min(4, 1 + (round + 1) / 2);
             uint32_t changed = 0;
             CUDA_TRY(h, cudaMemcpyAsync(&changed, h->dflags + 1, sizeof changed,
                                         cudaMemcpyDeviceToHost, st));
@@ -1608,7 +1708,8 @@ int refine_and_compose(bc_handle *h, int lanes, int ng, cudaStream_t st,
     int m = -1;
     CUDA_TRY(h, cudaMemcpyAsync(h->d_maxlvl, &m, sizeof m, cudaMemcpyHostToDevice, st));
     if (h->B > 0) {
-        max_seed_level_kernel<<<grid1d(cnt, 256, 1184), 256, 0, st>>>(h->D, h->arr, cnt, h->d_maxlvl);
+        max_seed_level_kernel<<<grid1d(cnt, 256, 1184), 256, 0, st>>>(h->D, h->arr, cnt, h->d_maxlvl,
+                                                                      h->dist_hybir ? 1 : 0);
         ++h->launches;
     }
     CUDA_TRY(h, cudaMemcpyAsync(&m, h->d_maxlvl, sizeof m, cudaMemcpyDeviceToHost, st));
@@ -1643,6 +1744,7 @@ int build_border_tables(bc_handle *h) {
                  "this partition", bytes / 1e9);
         return h->fail(BC_ERR_INPUT, buf);
     }
+    h->table_set.clear();   // (a partial set of installed tables is rebuilt from scratch)
     TRY(dev_alloc(h, &h->bm, (size_t)h->tab_total));
     TRY(dev_alloc(h, &h->sm, (size_t)h->tab_total));
     if (h->B == 0) {
@@ -1653,8 +1755,9 @@ int build_border_tables(bc_handle *h) {
     TRY(ensure_state(h, groups, false));
     TRY(ensure_levels(h, 2));
     std::vector<int64_t> src(h->h_border_v.begin(), h->h_border_v.end());
-    int64_t *d_borders = nullptr;
-    TRY(upload(h, &d_borders, src));
+    ScopedBlock<int64_t> d_borders_blk;
+    TRY(upload(h, &d_borders_blk.p, src));
+    int64_t *const d_borders = d_borders_blk.p;
     const int per = 32 * groups;
     const BorderGeom geo = border_geom(h);
     // graph-partitioned multi-GPU runs build the rows of their own part only; the other parts'
@@ -1694,7 +1797,6 @@ int build_border_tables(bc_handle *h) {
         CUDA_TRY(h, cudaGetLastError());
     }
     CUDA_TRY(h, cudaStreamSynchronize(st));
-    arena_free(d_borders);
     h->tables_ready = true;
     return BC_OK;
 }
@@ -1742,8 +1844,9 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         // caller's order because its output rows follow it.
         std::vector<int64_t> key(active.size());
         if (!active.empty()) {
-            int64_t *d_tmp = nullptr;
-            CUDA_TRY(h, arena_malloc((void **)&d_tmp, 2 * active.size() * sizeof(int64_t)));
+            ScopedBlock<int64_t> d_tmp_blk;
+            CUDA_TRY(h, arena_malloc((void **)&d_tmp_blk.p, 2 * active.size() * sizeof(int64_t)));
+            int64_t *const d_tmp = d_tmp_blk.p;
             CUDA_TRY(h, cudaMemcpyAsync(d_tmp, active.data(), active.size() * sizeof(int64_t),
                                         cudaMemcpyHostToDevice, st));
             source_key_kernel<<<grid1d(active.size() * 32, 256), 256, 0, st>>>(
@@ -1752,7 +1855,6 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             CUDA_TRY(h, cudaMemcpyAsync(key.data(), d_tmp + active.size(), active.size() * sizeof(int64_t),
                                         cudaMemcpyDeviceToHost, st));
             CUDA_TRY(h, cudaStreamSynchronize(st));
-            arena_free(d_tmp);
         }
         std::vector<size_t> order(active.size());
         for (size_t i = 0; i < order.size(); ++i) order[i] = i;
@@ -1781,8 +1883,15 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         h->d_src_cap = k;
     }
     tr.mark("run: state allocation");
+    // The per-group BC partials are zeroed by reduce_bc_kernel at the end of a run.  After a fresh
+    // allocation, or after a run that failed half way (its batches are already in there), clear
+    // them here, on the caller's stream.
+    if (h->bcg_dirty)
+        CUDA_TRY(h, cudaMemsetAsync(h->bcg, 0, (size_t)h->alloc_groups * (size_t)n * sizeof(double), st));
+    h->bcg_dirty = !debug;   // until reduce_bc_kernel has run
     const int64_t launches0 = h->launches;
     const int64_t level_launches0 = h->level_launches;
+    h->model_scan = h->model_pairs = h->model_vlanes = h->model_dense_words = h->model_entries = 0;
     int64_t h2d = 0, d2h = 0;
     if (k > 0) {
         CUDA_TRY(h, cudaMemcpyAsync(h->d_src, sources, k * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -1808,13 +1917,76 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const bool queued = adaptive || qsweep;   // levels are LevelReps, not h->lvl[L]
 
     // debug staging: one batch (<= 32 sources) of [lane][n] rows
-    int32_t *dbg_dist = nullptr;
-    double *dbg_sigma = nullptr, *dbg_delta = nullptr;
+    ScopedBlock<int32_t> dbg_dist_blk;
+    ScopedBlock<double> dbg_sigma_blk, dbg_delta_blk;
     if (debug) {
-        if (dist_out) CUDA_TRY(h, arena_malloc((void **)&dbg_dist, 32 * (size_t)n * sizeof(int32_t)));
-        if (sigma_out) CUDA_TRY(h, arena_malloc((void **)&dbg_sigma, 32 * (size_t)n * sizeof(double)));
-        if (delta_out) CUDA_TRY(h, arena_malloc((void **)&dbg_delta, 32 * (size_t)n * sizeof(double)));
+        if (dist_out) CUDA_TRY(h, arena_malloc((void **)&dbg_dist_blk.p, 32 * (size_t)n * sizeof(int32_t)));
+        if (sigma_out) CUDA_TRY(h, arena_malloc((void **)&dbg_sigma_blk.p, 32 * (size_t)n * sizeof(double)));
+        if (delta_out) CUDA_TRY(h, arena_malloc((void **)&dbg_delta_blk.p, 32 * (size_t)n * sizeof(double)));
     }
+    int32_t *const dbg_dist = dbg_dist_blk.p;
+    double *const dbg_sigma = dbg_sigma_blk.p, *const dbg_delta = dbg_delta_blk.p;
+
+    // ---- Step 1 of a hybir batch + its border seeds, on stream `s`, into the given seed buffers.
+    // Runs inline on the caller's stream, or -- look-ahead, engine.py:135-143 -- for batch b + 1 on
+    // the side stream from a helper thread while the border phase of batch b is in flight: Step 1
+    // needs the BFS state only, the border phase the border state only.
+    struct Step1Out {
+        int depth = 1;
+        std::vector<LevelRep> reps;
+        int rc = BC_OK;
+    };
+    auto step1 = [&](int64_t b, cudaStream_t s, int32_t *seedD, double *seedS, int32_t *lane_part,
+                     Step1Out &out) -> int {
+        const int cnt = (int)std::min<int64_t>(lanes_per_batch, k - b * lanes_per_batch);
+        const int ng = (cnt + 31) / 32;
+        const int64_t *batch_src = sources + b * lanes_per_batch;
+        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, s, queued));
+        h->cnt_off = 4;   // Step 1 is a partial traversal: keep it out of the totals
+        const int rc = qsweep ? forward_adaptive(h, h->intra, ng, cnt, batch_src, s, &out.depth, out.reps,
+                                                 &h->h_ioff, true)
+                              : forward_sweep(h, h->intra, ng, s, &out.depth);
+        h->cnt_off = 0;
+        TRY(rc);
+        const size_t bcnt = (size_t)h->B * h->border_S;
+        std::vector<int32_t> lp(h->border_S, 0);
+        for (int i = 0; i < cnt; ++i) lp[i] = h->h_part[batch_src[i]];
+        CUDA_TRY(h, cudaMemcpyAsync(lane_part, lp.data(), h->border_S * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(h, cudaStreamSynchronize(s));   // `lp` goes out of scope
+        fill_seed_kernel<<<grid1d(bcnt, 256, 4736), 256, 0, s>>>(seedD, seedS, bcnt);
+        if (qsweep) {
+            TRY(upload_level_ends(h, out.reps, out.depth, s));
+            if (h->B > 0)
+                border_gather_queue_kernel<<<dim3(queue_blocks_all(out.reps, out.depth), ng), 256, 0, s>>>(
+                    queue_params(h), h->range_table, out.depth, h->alloc_groups, n, h->d_border_index,
+                    h->sigma, h->border_S, seedD, seedS);
+        } else {
+            TRY(upload_level_ptrs(h, out.depth, s));
+            if (h->B > 0)
+                border_gather_kernel<<<grid1d(bcnt), 256, 0, s>>>(
+                    h->d_lvl_ptrs, h->live, h->alloc_groups, out.depth, h->sigma, n, border_geom(h),
+                    h->border_S, seedD, seedS);
+        }
+        h->launches += 2;
+        CUDA_TRY(h, cudaGetLastError());
+        return BC_OK;
+    };
+    const bool lookahead = hybir && h->lookahead && !debug && n_batches > 1;
+    if (lookahead && h->side_stream == nullptr) {
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->side_go, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->side_done, cudaEventDisableTiming));
+    }
+    Step1Out ahead;            // Step 1 of batch b + 1, filled by the look-ahead thread
+    bool ahead_ready = false;
+    int64_t lookahead_batches = 0;
+    std::thread helper;
+    struct Joiner {
+        std::thread &t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } joiner{helper};
 
     for (int64_t b = 0; b < n_batches; ++b) {
         const int cnt = (int)std::min<int64_t>(lanes_per_batch, k - b * lanes_per_batch);
@@ -1830,14 +2002,27 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         const int64_t l_start = h->launches;
 
         // ---- forward: Step 1 (or the whole BFS when there is no partition)
-        TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, queued));
         int depth = 1;
-        h->cnt_off = hybir ? 4 : 0;  // Step 1 is a partial traversal: keep it out of the totals
         std::vector<LevelRep> reps;
-        if (adaptive) TRY(forward_adaptive(h, fwd_csr, ng, cnt, batch_src, st, &depth, reps));
-        else if (qsweep) TRY(forward_adaptive(h, h->intra, ng, cnt, batch_src, st, &depth, reps, &h->h_ioff, true));
-        else TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
-        h->cnt_off = 0;
+        if (!hybir) {
+            TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, queued));
+            if (adaptive) TRY(forward_adaptive(h, fwd_csr, ng, cnt, batch_src, st, &depth, reps));
+            else TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
+        } else if (ahead_ready) {
+            // issued ahead while the previous batch's border phase ran: its seeds sit in the
+            // alternate buffers
+            std::swap(h->seedD, h->seedD_alt);
+            std::swap(h->seedS, h->seedS_alt);
+            std::swap(h->lane_part, h->lane_part_alt);
+            depth = ahead.depth;
+            reps.swap(ahead.reps);
+            ahead_ready = false;
+        } else {
+            Step1Out now;
+            TRY(step1(b, st, h->seedD, h->seedS, h->lane_part, now));
+            depth = now.depth;
+            reps.swap(now.reps);
+        }
         CUDA_TRY(h, cudaEventRecord(e.fwd_end, st));
         launches_f += h->launches - l_start;
         tr.mark("batch: forward (Step 1)");
@@ -1845,34 +2030,35 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         std::vector<int32_t> iters;
         std::vector<uint32_t> entered;
         if (hybir) {
-            // ---- Steps 2-5 + path-count composition on the border tables
-            const size_t bcnt = (size_t)h->B * h->border_S;
-            std::vector<int32_t> lp(h->border_S, 0);
-            for (int i = 0; i < cnt; ++i) lp[i] = h->h_part[batch_src[i]];
-            CUDA_TRY(h, cudaMemcpyAsync(h->lane_part, lp.data(), h->border_S * sizeof(int32_t),
-                                        cudaMemcpyHostToDevice, st));
-            fill_border_kernel<<<grid1d(bcnt, 256, 4736), 256, 0, st>>>(h->D, h->seedD, h->seedS,
-                                                                        h->sig, h->arr, bcnt);
-            if (qsweep) {
-                TRY(upload_level_ends(h, reps, depth, st));
-                if (h->B > 0)
-                    border_gather_queue_kernel<<<dim3(queue_blocks_all(reps, depth), ng), 256, 0, st>>>(
-                        queue_params(h), h->range_table, depth, h->alloc_groups, n, h->d_border_index,
-                        h->sigma, h->border_S, h->seedD, h->seedS);
-            } else {
-                TRY(upload_level_ptrs(h, depth, st));
-                if (h->B > 0)
-                    border_gather_kernel<<<grid1d(bcnt), 256, 0, st>>>(
-                        h->d_lvl_ptrs, h->live, h->alloc_groups, depth, h->sigma, n, border_geom(h),
-                        h->border_S, h->seedD, h->seedS);
+            if (lookahead && b + 1 < n_batches) {
+                // the BFS state is free until Step 6: Step 1 of the next batch takes it now
+                CUDA_TRY(h, cudaEventRecord(h->side_go, st));
+                CUDA_TRY(h, cudaStreamWaitEvent(h->side_stream, h->side_go, 0));
+                ahead = Step1Out{};
+                helper = std::thread([&, b]() {
+                    cudaSetDevice(h->device);
+                    ahead.rc = step1(b + 1, h->side_stream, h->seedD_alt, h->seedS_alt, h->lane_part_alt, ahead);
+                    if (ahead.rc == BC_OK && cudaEventRecord(h->side_done, h->side_stream) != cudaSuccess)
+                        ahead.rc = BC_ERR_INTERNAL;
+                });
             }
-            h->launches += 2;
-            tr.mark("batch: border gather");
+            // ---- Steps 2-5 + path-count composition on the border tables
             int max_seed = -1;
-            TRY(refine_and_compose(h, cnt, ng, st, &iters, &entered, &max_seed));
+            const int rc_border = refine_and_compose(h, cnt, ng, st, &iters, &entered, &max_seed);
             SeedPlan plan{};
-            if (qsweep) TRY(build_seed_plan(h, cnt, max_seed, st, &plan));
-            tr.mark("batch: seed plan");
+            int rc_plan = BC_OK;
+            if (rc_border == BC_OK && qsweep) rc_plan = build_seed_plan(h, cnt, max_seed, st, &plan);
+            if (helper.joinable()) {
+                helper.join();
+                if (ahead.rc != BC_OK) return ahead.rc;
+                // Step 6 below takes the BFS state over: wait for the look-ahead's gather
+                CUDA_TRY(h, cudaStreamWaitEvent(st, h->side_done, 0));
+                ahead_ready = true;
+                ++lookahead_batches;
+            }
+            TRY(rc_border);
+            TRY(rc_plan);
+            tr.mark("batch: border phase");
             CUDA_TRY(h, cudaEventRecord(e.border_end, st));
             // ---- Step 6: every part relaxes from its borders at once
             const int64_t l_step6 = h->launches;
@@ -2036,13 +2222,13 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         reduce_bc_kernel<<<grid1d((size_t)n, 256, 1184), 256, 0, st>>>(bc_dev, h->bcg, n, h->alloc_groups);
         ++h->launches;
         CUDA_TRY(h, cudaGetLastError());
+        h->bcg_dirty = false;
     }
     unsigned long long cnts[8] = {0};
     CUDA_TRY(h, cudaMemcpyAsync(cnts, h->counters, sizeof cnts, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));
     d2h += sizeof cnts;
     tr.mark("run: batches");
-    arena_free(dbg_dist), arena_free(dbg_sigma), arena_free(dbg_delta);
 
     double ms_level = 0;
     const int64_t level_timed = (int64_t)h->level_events.size();
@@ -2062,8 +2248,6 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         ms_f += a + f2;
         ms_border += bo;
         ms_b += bw;
-        cudaEventDestroy(e.start), cudaEventDestroy(e.fwd_end), cudaEventDestroy(e.border_end);
-        cudaEventDestroy(e.fwd2_end), cudaEventDestroy(e.bwd_end);
     }
     if (stats) {
         memset(stats, 0, sizeof *stats);
@@ -2093,6 +2277,18 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         stats->launches_level = h->level_launches - level_launches0;
         stats->ms_level = ms_level;
         stats->launches_level_timed = level_timed;
+        stats->lookahead_batches = lookahead_batches;
+        stats->level_scan_arcs = h->model_scan;
+        stats->level_pairs = h->model_pairs;
+        stats->level_vertex_lanes = h->model_vlanes;
+        stats->level_dense_words = h->model_dense_words;
+        stats->level_entries = h->model_entries;
+        // col_idx word + mask probe per scanned arc; one fp64 per gathered pair and per
+        // (vertex, lane) value; 4 B per dense mask word; 16 B of BC partial per backward entry;
+        // row offsets once per launch
+        stats->level_model_bytes = 8 * h->model_scan + 8 * h->model_pairs + 8 * h->model_vlanes +
+                                   4 * h->model_dense_words + 16 * h->model_entries +
+                                   8 * h->n * stats->launches_level;
     }
     return BC_OK;
 }
@@ -2184,9 +2380,23 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
         if (n_arcs > 0)
             CUDA_TRY(h, cudaMemcpyAsync(c.col, col_idx, n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice, 0));
         h->h_off.assign(offsets, offsets + n + 1);
-        const int rc_items = build_items(h, c, offsets, h->item_arcs);
+        for (int64_t v = 0; v < n; ++v)
+            if (offsets[v + 1] < offsets[v])
+                return h->fail(BC_ERR_INPUT, "malformed CSR: offsets decrease at vertex " + std::to_string(v));
+        TRY(build_items(h, c, offsets, h->item_arcs));
+        // neighbour ids are checked on the device, behind the upload (a bad id would be an
+        // out-of-bounds read in every kernel)
+        if (n_arcs > 0) {
+            ScopedBlock<int> d_bad;
+            CUDA_TRY(h, arena_malloc((void **)&d_bad.p, sizeof(int)));
+            CUDA_TRY(h, cudaMemsetAsync(d_bad.p, 0, sizeof(int), 0));
+            validate_col_kernel<<<grid1d((size_t)n_arcs, 256, 2368), 256>>>(c.col, n_arcs, n, d_bad.p);
+            int bad = 0;
+            CUDA_TRY(h, cudaMemcpy(&bad, d_bad.p, sizeof bad, cudaMemcpyDeviceToHost));
+            if (bad) return h->fail(BC_ERR_INPUT, "malformed CSR: col_idx holds a vertex id outside [0, n)");
+        }
         tr.mark("create: CSR upload + work items");
-        return rc_items;
+        return BC_OK;
     };
     int rc = body();
     if (rc) return bail(rc);
@@ -2278,6 +2488,18 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         arena_free(h->deep_log), arena_free(h->deep_info);
         h->deep_log = nullptr;
         h->deep_info = nullptr;
+        return BC_OK;
+    }
+    if (k == "lookahead") {
+        h->lookahead = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "l2_fetch") {
+        // granularity of L2 fills from HBM (32 / 64 / 128 B; the driver default is 64): random
+        // 8-byte accesses of the deep-graph sweeps use a quarter of a 32-byte sector as it is
+        if (value != 32 && value != 64 && value != 128)
+            return h->fail(BC_ERR_INPUT, "l2_fetch must be 32, 64 or 128");
+        CUDA_TRY(h, cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)value));
         return BC_OK;
     }
     if (k == "push_beta_late") {
@@ -2516,6 +2738,34 @@ int bc_get_border_tables(bc_handle *h, int part, int32_t *borders, int32_t *bm, 
     return BC_OK;
 }
 
+int bc_set_border_tables(bc_handle *h, int part, const int32_t *bm, const double *sm) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (h->k < 2 || part < 0 || part >= h->k || bm == nullptr || sm == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_set_border_tables: no such part / null table");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    if (h->bm == nullptr) {
+        TRY(dev_alloc(h, &h->bm, (size_t)h->tab_total));
+        TRY(dev_alloc(h, &h->sm, (size_t)h->tab_total));
+        h->table_set.assign((size_t)h->k, false);
+    }
+    if ((int)h->table_set.size() != h->k) h->table_set.assign((size_t)h->k, false);
+    const int64_t b = h->h_part_off[(size_t)part + 1] - h->h_part_off[(size_t)part];
+    if (b > 0) {
+        std::vector<int32_t> d(bm, bm + b * b);
+        for (int32_t &x : d)
+            if (x < 0) x = kInf;   // BC_UNREACHED
+        CUDA_TRY(h, cudaMemcpy(h->bm + h->h_tab_off[(size_t)part], d.data(), (size_t)(b * b) * sizeof(int32_t),
+                               cudaMemcpyHostToDevice));
+        CUDA_TRY(h, cudaMemcpy(h->sm + h->h_tab_off[(size_t)part], sm, (size_t)(b * b) * sizeof(double),
+                               cudaMemcpyHostToDevice));
+    }
+    h->table_set[(size_t)part] = true;
+    bool all = true;
+    for (bool x : h->table_set) all = all && x;
+    h->tables_ready = all;
+    return BC_OK;
+}
+
 int bc_get_border_frontier(bc_handle *h, int64_t n_lanes, int32_t *dist, double *sigma,
                            double *arrival) {
     if (h == nullptr) return BC_ERR_INPUT;
@@ -2573,12 +2823,21 @@ int bc_dist_begin(bc_handle *h, const int64_t *sources, int64_t count, void *str
     if (count < 1 || count > 32 * (int64_t)h->groups || sources == nullptr)
         return h->fail(BC_ERR_INPUT, "bc_dist_begin: need 1 <= count <= 32 * groups sources");
     for (int64_t i = 0; i < count; ++i)
-        if (sources[i] < 0 || sources[i] >= h->n)
+        if (sources[i] < -1 || sources[i] >= h->n)   // -1: the lane's source is not on this rank
             return h->fail(BC_ERR_INPUT, "bc_dist_begin: source out of range");
     CUDA_TRY(h, cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)stream;
     TRY(ensure_state(h, h->groups, false));
     TRY(ensure_levels(h, 2));
+    if (h->bcg_dirty) {
+        CUDA_TRY(h, cudaMemsetAsync(h->bcg, 0, (size_t)h->alloc_groups * (size_t)h->n * sizeof(double), st));
+        h->bcg_dirty = false;
+    }
+    if (h->lstat == nullptr) {
+        TRY(dev_alloc(h, &h->lstat, (size_t)8));
+        CUDA_TRY(h, cudaMemsetAsync(h->lstat, 0, 8 * sizeof(unsigned long long), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned long long), st));
+    }
     if (h->d_src_cap < count) {
         arena_free(h->d_src);
         h->d_src = nullptr;
@@ -2707,6 +2966,180 @@ int bc_dist_set_live(bc_handle *h, int level, const uint32_t *live, void *stream
     return BC_OK;
 }
 
+int bc_dist_set_cut_arcs(bc_handle *h, const int64_t *cut_off, const int32_t *cut_dst) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (h->dist_rank < 0 || cut_off == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_set_cut_arcs: call bc_dist_setup first");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const int r = h->dist_rank;
+    const int64_t nb = h->dist_border_off[(size_t)r + 1] - h->dist_border_off[(size_t)r];
+    if (cut_off[0] != 0) return h->fail(BC_ERR_INPUT, "bc_dist_set_cut_arcs: cut_off[0] must be 0");
+    const int64_t total = cut_off[nb];
+    for (int64_t c = 0; c < total; ++c)
+        if (cut_dst == nullptr || cut_dst[c] < 0 || cut_dst[c] >= h->n)
+            return h->fail(BC_ERR_INPUT, "bc_dist_set_cut_arcs: far end out of range");
+    std::vector<int64_t> off(cut_off, cut_off + nb + 1);
+    std::vector<int32_t> dst(cut_dst, cut_dst + total);
+    if (dst.empty()) dst.push_back(0);
+    TRY(upload(h, &h->dist_cut_off, off));
+    TRY(upload(h, &h->dist_cut_dst, dst));
+    return BC_OK;
+}
+
+int bc_dist_plan_backward(bc_handle *h, int depth, int64_t *counts_out, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, 0));
+    if (depth < 1 || depth > (int)h->lvl.size() || counts_out == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_plan_backward: bad depth / null output");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int r = h->dist_rank, ng = h->dist_ng;
+    const int nb = (int)(h->dist_border_off[(size_t)r + 1] - h->dist_border_off[(size_t)r]);
+    h->plan_depth = depth;
+    h->plan_eoff_h.assign((size_t)depth + 1, 0);
+    h->plan_cnt_e_h.assign((size_t)depth, 0);
+    h->plan_cnt_v_h.assign((size_t)depth, 0);
+    for (int L = 0; L < depth; ++L) counts_out[2 * L] = counts_out[2 * L + 1] = 0;
+    if (nb == 0 || h->dist_world == 1) return BC_OK;
+    if (h->dist_cut_off == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_plan_backward: call bc_dist_set_cut_arcs first");
+    if (h->plan_levels_cap < depth + 1) {
+        const int cap = std::max(depth + 1, 2 * h->plan_levels_cap);
+        TRY(dev_alloc(h, &h->plan_eoff, (size_t)cap));
+        TRY(dev_alloc(h, &h->plan_cnt_e, (size_t)cap));
+        TRY(dev_alloc(h, &h->plan_cnt_v, (size_t)cap));
+        h->plan_levels_cap = cap;
+    }
+    TRY(upload_level_ptrs(h, depth, st));
+    const int32_t *bv = h->dist_border_v + h->dist_border_off[(size_t)r];
+    DistPlan plan{h->plan_idx, h->plan_mask, h->plan_voff, h->plan_eoff, h->plan_cnt_e, h->plan_cnt_v};
+    CUDA_TRY(h, cudaMemsetAsync(h->plan_cnt_e, 0, depth * sizeof(int32_t), st));
+    CUDA_TRY(h, cudaMemsetAsync(h->plan_cnt_v, 0, depth * sizeof(int32_t), st));
+    const unsigned blocks = grid1d((size_t)nb * ng);
+    dist_plan_kernel<<<blocks, 256, 0, st>>>(h->d_lvl_ptrs, h->live, h->alloc_groups, depth, bv, nb, ng, h->n,
+                                             h->dist_cut_off, h->dist_cut_dst, 0, plan);
+    CUDA_TRY(h, cudaMemcpyAsync(h->plan_cnt_e_h.data(), h->plan_cnt_e, depth * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaMemcpyAsync(h->plan_cnt_v_h.data(), h->plan_cnt_v, depth * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));   // the one host round trip of a batch's backward phase
+    int64_t total = 0;
+    for (int L = 0; L < depth; ++L) {
+        h->plan_eoff_h[(size_t)L] = (int32_t)total;
+        total += h->plan_cnt_e_h[(size_t)L];
+        counts_out[2 * L] = h->plan_cnt_e_h[(size_t)L];
+        counts_out[2 * L + 1] = h->plan_cnt_v_h[(size_t)L];
+    }
+    h->plan_eoff_h[(size_t)depth] = (int32_t)total;
+    if (total > h->plan_cap) {
+        const int64_t cap = std::max(total, 2 * h->plan_cap);
+        TRY(dev_alloc(h, &h->plan_idx, (size_t)cap));
+        TRY(dev_alloc(h, &h->plan_mask, (size_t)cap));
+        TRY(dev_alloc(h, &h->plan_voff, (size_t)cap));
+        h->plan_cap = cap;
+    }
+    if (total > 0) {
+        plan = DistPlan{h->plan_idx, h->plan_mask, h->plan_voff, h->plan_eoff, h->plan_cnt_e, h->plan_cnt_v};
+        CUDA_TRY(h, cudaMemcpyAsync(h->plan_eoff, h->plan_eoff_h.data(), (depth + 1) * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->plan_cnt_e, 0, depth * sizeof(int32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->plan_cnt_v, 0, depth * sizeof(int32_t), st));
+        dist_plan_kernel<<<blocks, 256, 0, st>>>(h->d_lvl_ptrs, h->live, h->alloc_groups, depth, bv, nb, ng,
+                                                 h->n, h->dist_cut_off, h->dist_cut_dst, 1, plan);
+    }
+    h->launches += 2;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+int bc_dist_pack(bc_handle *h, int level, void *send_dev, int64_t cap_entries, int64_t cap_values,
+                 void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (level >= h->plan_depth || send_dev == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_pack: no plan for this level / null buffer");
+    const int count = h->plan_cnt_e_h[(size_t)level];
+    if (count > cap_entries || h->plan_cnt_v_h[(size_t)level] > cap_values)
+        return h->fail(BC_ERR_INPUT, "bc_dist_pack: message buffer too small");
+    if (count == 0) return BC_OK;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const int r = h->dist_rank;
+    const int32_t eo = h->plan_eoff_h[(size_t)level];
+    double *values = (double *)send_dev;
+    int32_t *head = (int32_t *)(values + cap_values);
+    dist_pack_kernel<<<grid1d((size_t)count), 256, 0, (cudaStream_t)stream>>>(
+        h->coef, h->dist_border_v + h->dist_border_off[(size_t)r], h->dist_ng, h->n, h->plan_idx + eo,
+        h->plan_mask + eo, h->plan_voff + eo, count, values, head, cap_entries);
+    ++h->launches;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+int bc_dist_unpack(bc_handle *h, int level, int from, const void *recv_dev, int64_t cap_entries,
+                   int64_t cap_values, int64_t n_entries, void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (from < 0 || from >= h->dist_world || from == h->dist_rank || recv_dev == nullptr ||
+        n_entries < 0 || n_entries > cap_entries)
+        return h->fail(BC_ERR_INPUT, "bc_dist_unpack: bad peer / buffer / entry count");
+    if (n_entries == 0) return BC_OK;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const double *values = (const double *)recv_dev;
+    const int32_t *head = (const int32_t *)(values + cap_values);
+    dist_unpack_kernel<<<grid1d((size_t)n_entries), 256, 0, (cudaStream_t)stream>>>(
+        h->coef, h->dist_border_v + h->dist_border_off[(size_t)from], h->dist_ng, h->n, values, head,
+        cap_entries, (int)n_entries);
+    ++h->launches;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
+int bc_dist_get_stats(bc_handle *h, bc_stats *stats) {
+    if (h == nullptr || stats == nullptr) return BC_ERR_INPUT;
+    memset(stats, 0, sizeof *stats);
+    stats->launches = h->launches;
+    stats->launches_level = h->level_launches;
+    // CUDA-event time of the dense level-kernel launches since the last call
+    double ms = 0;
+    int64_t timed = 0;
+    for (auto &pr : h->level_events) {
+        float t = 0;
+        if (cudaEventSynchronize(pr.second) == cudaSuccess &&
+            cudaEventElapsedTime(&t, pr.first, pr.second) == cudaSuccess) {
+            ms += t;
+            ++timed;
+        }
+        cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    }
+    h->level_events.clear();
+    stats->ms_level = ms;
+    stats->launches_level_timed = timed;
+    // byte model of the dense launches since the last call: running device totals
+    if (h->lstat != nullptr && h->counters != nullptr) {
+        unsigned long long ls[8] = {0}, cn[8] = {0};
+        CUDA_TRY(h, cudaSetDevice(h->device));
+        CUDA_TRY(h, cudaDeviceSynchronize());
+        CUDA_TRY(h, cudaMemcpy(ls, h->lstat, sizeof ls, cudaMemcpyDeviceToHost));
+        CUDA_TRY(h, cudaMemcpy(cn, h->counters, sizeof cn, cudaMemcpyDeviceToHost));
+        CUDA_TRY(h, cudaMemset(h->lstat, 0, sizeof ls));
+        CUDA_TRY(h, cudaMemset(h->counters, 0, sizeof cn));
+        const int64_t vl = (int64_t)(cn[0] + cn[4]), pairs = (int64_t)(cn[2] + cn[6]);
+        stats->level_scan_arcs = (int64_t)(ls[4] + ls[1]);   // forward pulls + backward entries' arcs
+        stats->level_pairs = 2 * pairs;                        // gathered forward and backward
+        stats->level_vertex_lanes = 3 * vl;                    // sigma written; sigma read + coef written
+        stats->level_dense_words = h->model_dense_words;
+        stats->level_entries = (int64_t)ls[0];
+        stats->level_model_bytes = 8 * stats->level_scan_arcs + 8 * stats->level_pairs +
+                                   8 * stats->level_vertex_lanes + 4 * stats->level_dense_words +
+                                   16 * stats->level_entries + 8 * h->n * stats->launches_level;
+        stats->reached = vl;
+        stats->dag_arcs = pairs;
+        h->model_dense_words = 0;
+    }
+    h->level_launches = 0;
+    return BC_OK;
+}
+
 int bc_dist_finish(bc_handle *h, double *bc_dev, void *stream) {
     if (h == nullptr) return BC_ERR_INPUT;
     if (h->dist_rank < 0 || bc_dev == nullptr || h->bcg == nullptr)
@@ -2777,18 +3210,21 @@ int64_t bc_dist_hybir_seed_count(bc_handle *h) {
     return (int64_t)h->B * 32 * std::max(h->groups, 1);
 }
 
-int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, int64_t count, int32_t *seed_dist_dev,
-                        double *seed_sigma_dev, void *stream) {
+int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, const int32_t *source_part, int64_t count,
+                        int32_t *seed_dist_dev, double *seed_sigma_dev, void *stream) {
     if (h == nullptr) return BC_ERR_INPUT;
     if (!h->dist_hybir) return h->fail(BC_ERR_INPUT, "bc_dist_hybir_seeds: call bc_dist_hybir_setup first");
-    if (seed_dist_dev == nullptr || seed_sigma_dev == nullptr)
-        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_seeds: null seed buffers");
+    if (seed_dist_dev == nullptr || seed_sigma_dev == nullptr || source_part == nullptr)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_seeds: null buffers");
+    for (int64_t i = 0; i < count; ++i)
+        if (source_part[i] < 0 || source_part[i] >= h->dist_world)
+            return h->fail(BC_ERR_INPUT, "bc_dist_hybir_seeds: source part outside [0, world)");
     cudaStream_t st = (cudaStream_t)stream;
     TRY(bc_dist_begin(h, sources, count, stream));   // state, lanes, level-0 seeds
     const int S = 32 * h->groups;
     TRY(ensure_border_state(h, S));
     std::vector<int32_t> lp((size_t)h->border_S, 0);
-    for (int64_t i = 0; i < count; ++i) lp[(size_t)i] = h->h_part[(size_t)sources[i]];
+    for (int64_t i = 0; i < count; ++i) lp[(size_t)i] = source_part[i];
     CUDA_TRY(h, cudaMemcpyAsync(h->lane_part, lp.data(), h->border_S * sizeof(int32_t),
                                 cudaMemcpyHostToDevice, st));
     int depth = 1;
@@ -2879,6 +3315,12 @@ void bc_destroy(bc_handle *h) {
     arena_free(h->presence);
     arena_free(h->dist_border_v), arena_free(h->dist_counts), arena_free(h->dist_offsets);
     arena_free(h->dist_scan_tmp);
+    arena_free(h->dist_cut_off), arena_free(h->dist_cut_dst);
+    arena_free(h->plan_idx), arena_free(h->plan_mask), arena_free(h->plan_voff);
+    arena_free(h->plan_eoff), arena_free(h->plan_cnt_e), arena_free(h->plan_cnt_v);
+    if (h->side_stream) cudaStreamDestroy(h->side_stream);
+    if (h->side_go) cudaEventDestroy(h->side_go);
+    if (h->side_done) cudaEventDestroy(h->side_done);
     delete h;
 }
 

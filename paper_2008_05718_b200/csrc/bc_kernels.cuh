@@ -80,7 +80,8 @@ struct LevelParams {
     const uint32_t *live_prev;  // forward: live[L-1]; backward: live[L]
     uint32_t *live_cur;         // forward: live[L], OR-ed by this launch
     unsigned long long *counters;  // [0] n_r, [1] A_r, [2] T
-    unsigned long long *lstat;     // forward: [0] vertices discovered, [1] their arcs, [2] largest degree (may be null)
+    unsigned long long *lstat;     // forward: [0] vertices discovered, [1] their arcs, [2] largest degree,
+                                   // [4] arcs scanned by this launch (byte model of the roofline); may be null
     int accumulate_bc;
     // forward sweeps of low-degree (deep) graphs without frontier queues: only vertices with a
     // neighbour in the previous level are scanned (mark_candidates_kernel); nullptr = scan all
@@ -338,6 +339,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         if (!BWD) {
             const unsigned t = __reduce_add_sync(kFull, c_t);
             if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
+            if (lane == 0 && p.lstat != nullptr && want != 0 && nbr != nullptr)
+                atomicAdd(p.lstat + 4, (unsigned long long)(p.chk_a1[item] - p.chk_a0[item]));
         }
     } else {
         // ---- up to 32 consecutive non-hub vertices, one per lane for the set-up and for what
@@ -368,6 +371,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         if (WEIGHTED) wp.wgt += a0;
         uint32_t mygot = 0;  // forward: what this lane's vertex discovered
         unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || deg > 0));
+        if (!BWD && p.lstat != nullptr && need != 0 && nbr != nullptr) {
+            // arcs this item scans (one col_idx word + one mask probe each): byte model of the roofline
+            const unsigned c_scan = __reduce_add_sync(kFull, (mine != 0) ? (unsigned)deg : 0u);
+            if (lane == 0) atomicAdd(p.lstat + 4, (unsigned long long)c_scan);
+        }
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
@@ -537,6 +545,7 @@ __global__ void seed_sources_kernel(const int64_t *src, int batch_count, int64_t
     const int lane = i & 31;
     const int64_t v = src[i];
     atomicOr(live0 + g, 1u << lane);
+    if (v < 0) return;   // graph-partitioned runs: the lane's source lives on another rank
     atomicOr(vis + g * n + v, 1u << lane);
     atomicOr(lvl0 + g * n + v, 1u << lane);
     sigma[(g * n + v) * 32 + lane] = 1.0;
@@ -548,6 +557,7 @@ __global__ void clear_source_sigma_kernel(const int64_t *src, int batch_count, i
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= batch_count) return;
     const size_t g = i >> 5;
+    if (src[i] < 0) return;
     sigma[(g * n + src[i]) * 32 + (i & 31)] = 0.0;
 }
 
@@ -877,14 +887,21 @@ __global__ void push_post_kernel(const int64_t *__restrict__ off, int64_t n, Que
 // host ([0..2] lstat, then q_count per group, then live per group), reset the
 // statistics, and make the level just produced the frontier of the next push
 // (device-resident ranges: consecutive push levels need no host uploads).
+// report[4 + 2G ..]: running totals of (vertex, lane) pairs reached and of DAG arcs (the traversal
+// counters) and the arcs the level's dense pull scanned -- the per-level inputs of the batched
+// byte model.
 __global__ void advance_level_kernel(unsigned long long *lstat, unsigned long long *q_count,
                                      const uint32_t *live_cur, int64_t *q_beg, int64_t *q_end,
-                                     int64_t *q_lbeg, int G, unsigned long long *report) {
+                                     int64_t *q_lbeg, int G, unsigned long long *report,
+                                     const unsigned long long *counters) {
     const int g = threadIdx.x;
     if (g < 3) report[g] = lstat[g];
     if (g == 3) report[3 + 2 * G] = lstat[3];   // heavy records of the level just produced
+    if (g == 4) report[4 + 2 * G] = counters[0];
+    if (g == 5) report[5 + 2 * G] = counters[2];
+    if (g == 6) report[6 + 2 * G] = lstat[4];
     __syncthreads();
-    if (g < 4) lstat[g] = 0;
+    if (g < 8) lstat[g] = 0;
     if (g < G) {
         const unsigned long long c = q_count[g];
         report[3 + g] = c;
@@ -1053,6 +1070,17 @@ __global__ void source_key_kernel(const int64_t *__restrict__ off, const int32_t
     }
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
     if (lane == 0) key[i] = sum;
+}
+
+// bc_create: every neighbour id must name a vertex.
+__global__ void validate_col_kernel(const int32_t *__restrict__ col, int64_t n_arcs, int64_t n, int *bad) {
+    bool any = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_arcs;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t w = col[i];
+        any |= w < 0 || w >= n;
+    }
+    if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) *bad = 1;
 }
 
 __global__ void fill_i32_kernel(int32_t *p, size_t count, int32_t value) {

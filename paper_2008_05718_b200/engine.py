@@ -13,9 +13,11 @@ library behind ``_capi.Engine``.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import random
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -24,7 +26,7 @@ from . import _capi
 from .errors import InputError
 from .graph import Graph, graph_stats
 from .partition import (BorderSet, Partition, block_partition, greedy_bipartition, grow_partition,
-                        identify_borders, import_partition, single_partition)
+                        identify_borders, import_partition, mincut_partition, single_partition)
 
 MODES = ("hybir", "bsp-baseline", "direct")
 GPU_MODES = ("source-sharded", "graph-partitioned")
@@ -55,7 +57,10 @@ class RunConfig:
     num_partitions: int = 2            # the reference's fixed value
     partition: Partition | None = None  # explicit assignment (tests, grid strips)
     partitioner: str = "auto"          # "auto": the reference's grower for 2 parts, id blocks above;
-                                       # "grow": k regions grown breadth-first (grow_partition); "block"
+                                       # "grow": k regions grown breadth-first (grow_partition); "block";
+                                       # "mincut": grown regions + boundary refinement (mincut_partition)
+    table_budget_bytes: float = 64e9   # border tables above this size: hybir falls back to bsp-baseline
+    table_cache_dir: str | None = None  # border-table disk cache (border_matrix.py:85-125)
     num_gpus: int = 1
     gpu_mode: str = "source-sharded"
     device: int | None = None          # CUDA ordinal; default LOCAL_RANK or 0
@@ -72,8 +77,8 @@ class RunConfig:
             raise InputError("num_sources must be >= 1")
         if self.num_partitions < 1:
             raise InputError("num_partitions must be >= 1")
-        if self.partitioner not in ("auto", "grow", "block"):
-            raise InputError("unknown partitioner %r; pick from auto, grow, block" % self.partitioner)
+        if self.partitioner not in ("auto", "grow", "block", "mincut"):
+            raise InputError("unknown partitioner %r; pick from auto, grow, block, mincut" % self.partitioner)
         if self.gpu_mode not in GPU_MODES:
             raise InputError("unknown gpu_mode %r; pick from %s" % (self.gpu_mode, GPU_MODES))
         if self.max_threads is None and os.environ.get("HYBIR_THREADS"):
@@ -145,9 +150,14 @@ def make_partition(g: Graph, cfg: RunConfig) -> Partition:
         return grow_partition(g, cfg.num_partitions, seed=cfg.seed)
     if cfg.partitioner == "block":
         return block_partition(g, cfg.num_partitions)
+    if cfg.partitioner == "mincut":
+        return mincut_partition(g, cfg.num_partitions, seed=cfg.seed)
     if cfg.num_partitions == 2:
         # 'auto' calibrates a CPU-vs-GPU speed ratio in the reference
         # (partition.py:157-190); identical B200 parts always balance at 0.5.
+        if cfg.ratio == "auto":
+            warnings.warn("ratio='auto' calibrates a CPU/GPU speed ratio in the reference; every part is an "
+                          "identical B200 here, so the split is 0.5", stacklevel=3)
         ratio = 0.5 if cfg.ratio == "auto" else float(cfg.ratio)
         return greedy_bipartition(g, ratio, seed=cfg.seed)
     return block_partition(g, cfg.num_partitions)
@@ -185,6 +195,59 @@ def prepare(g: Graph, cfg: RunConfig):
     return p, bs
 
 
+def border_table_bytes(bs: BorderSet) -> float:
+    """Device bytes of the border tables: per part b_p x b_p entries of int32 distance + fp64
+    path count (the b^2 term of the reference's memory model, border_matrix.py:70-82)."""
+    return float(sum(12.0 * b * b for b in bs.counts()))
+
+
+def choose_mode(mode: str, bs: BorderSet, budget_bytes: float) -> str:
+    """``hybir`` needs the border tables; when they do not fit the budget the run falls back to
+    the reference's other partitioned mode, which is pinned to give the same BC
+    (test_acceptance.py:288-297) and needs no tables (SURVEY.md hard part 2)."""
+    if mode == "hybir" and border_table_bytes(bs) > budget_bytes:
+        warnings.warn("border tables need %.1f GB (borders per part: %s), above the %.1f GB budget: "
+                      "running mode 'bsp-baseline' instead of 'hybir'"
+                      % (border_table_bytes(bs) / 1e9, list(bs.counts()), budget_bytes / 1e9), stacklevel=3)
+        return "bsp-baseline"
+    return mode
+
+
+def _table_cache_path(g: Graph, p: Partition, cache_dir: str) -> str:
+    h = hashlib.sha256()
+    h.update(g.content_hash().encode())
+    h.update(np.ascontiguousarray(p.assignment, dtype=np.int32).tobytes())
+    return os.path.join(cache_dir, "border_tables_%s.npz" % h.hexdigest()[:32])
+
+
+def load_border_tables(eng, g: Graph, p: Partition, bs: BorderSet, cache_dir: str) -> bool:
+    """Install cached border tables (keyed by graph + partition); False when there is no match."""
+    path = _table_cache_path(g, p, cache_dir)
+    try:
+        data = np.load(path)
+    except (OSError, ValueError):
+        return False
+    counts = bs.counts()
+    if int(data["version"]) != 1 or list(data["counts"]) != list(counts):
+        return False
+    for part, b in enumerate(counts):
+        eng.set_border_tables(part, data["bm%d" % part], data["sm%d" % part])
+    return True
+
+
+def save_border_tables(eng, g: Graph, p: Partition, bs: BorderSet, cache_dir: str) -> str:
+    os.makedirs(cache_dir, exist_ok=True)
+    path = _table_cache_path(g, p, cache_dir)
+    arrays = {"version": np.int64(1), "counts": np.asarray(bs.counts(), dtype=np.int64)}
+    for part, b in enumerate(bs.counts()):
+        _, bm, sm = eng.border_tables(part, b)
+        arrays["bm%d" % part], arrays["sm%d" % part] = bm, sm
+    tmp = path + ".tmp.npz"
+    np.savez(tmp, **arrays)
+    os.replace(tmp, path)
+    return path
+
+
 def _per_source(sources, reports, mode):
     out = []
     for s, r in zip(sources, reports):
@@ -212,26 +275,39 @@ def run_bc(g: Graph, cfg: RunConfig | None = None, _pipeline: bool = False) -> R
     t0 = time.perf_counter()
     sources = select_sources(g, cfg)
     p, bs = prepare(g, cfg)
-    mode = cfg.mode if p.num_parts > 1 else "direct"
+    mode = choose_mode(cfg.mode, bs, cfg.table_budget_bytes) if p.num_parts > 1 else "direct"
     with open_engine(g, cfg, len(sources)) as eng:
         if p.num_parts > 1:
             eng.set_partition(p.num_parts, p.assignment)
+        cached = False
+        if mode == "hybir" and cfg.table_cache_dir:
+            cached = load_border_tables(eng, g, p, bs, cfg.table_cache_dir)
+        if _pipeline:
+            eng.set_option("lookahead", 1)
         bc, stats = eng.run(sources, _MODE_CODE[mode])
+        stats["mode"] = mode
+        stats["border_tables_from_cache"] = cached
+        if mode == "hybir" and cfg.table_cache_dir and not cached:
+            save_border_tables(eng, g, p, bs, cfg.table_cache_dir)
         per_source = []
         if cfg.per_source_reports and p.num_parts > 1:
-            per_source = _per_source(sources, eng.reports(len(sources)), cfg.mode)
+            per_source = _per_source(sources, eng.reports(len(sources)), mode)
         elif cfg.per_source_reports:
             per_source = [{"source": int(s), "forward": {"source": int(s)}, "backward": {}} for s in sources]
     elapsed = time.perf_counter() - t0
     mteps = (g.num_edges * len(sources) / elapsed / 1e6) if elapsed > 0 else 0.0
     ledger = CommTotals(stats.get("comm_events", 0), stats.get("sync_events", 0),
                         stats.get("comm_bytes", 0))
-    return RunResult(bc, per_source, ledger, mteps, elapsed, p, bs, cfg, 0, stats)
+    return RunResult(bc, per_source, ledger, mteps, elapsed, p, bs, cfg,
+                     int(stats.get("lookahead_batches", 0)), stats)
 
 
 def pipeline_sources(g: Graph, cfg: RunConfig) -> RunResult:
-    """Look-ahead variant (engine.py:156-161).  Sources already advance 32 x
-    groups at a time on the device, so the result is the same call."""
+    """Look-ahead variant (engine.py:135-143,156-161): Step 1 of the NEXT source batch runs on a
+    second CUDA stream while the border refinement / path-count composition of the current
+    batch is in flight (it only needs the BFS state, which the border phase does not touch);
+    ``pipeline_overlaps`` counts the batches whose Step 1 was issued ahead.  Results are
+    identical to ``run_bc`` (test_engine.py:57-64)."""
     if cfg.mode != "hybir":
         raise InputError("pipelining applies to hybir mode only")
     return run_bc(g, cfg, _pipeline=True)

@@ -29,6 +29,7 @@ __all__ = [
     "from_edges",
     "from_edge_arrays",
     "load_edge_list",
+    "load_dimacs_gr",
     "write_edge_list",
     "graph_stats",
     "as_graph",
@@ -188,7 +189,12 @@ def from_edge_arrays(num_vertices: int, u, v, w=None) -> Graph:
     hi = np.maximum(u, v)[keep]
     key = lo * max(n, 1) + hi
     if w is None:
-        key = np.unique(key)
+        # sort + neighbour compare (np.unique on 10^8 keys is two orders of magnitude slower)
+        key = np.sort(key)
+        if len(key):
+            firsts = np.ones(len(key), dtype=bool)
+            np.not_equal(key[1:], key[:-1], out=firsts[1:])
+            key = key[firsts]
         wk = None
     else:
         wk = w[keep]
@@ -203,16 +209,24 @@ def from_edge_arrays(num_vertices: int, u, v, w=None) -> Graph:
     lo = key // max(n, 1)
     hi = key - lo * max(n, 1)
 
+    nn = max(n, 1)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    if wk is None:
+        # arcs are unique: sorting the packed (src, dst) keys is the whole job
+        arcs = np.concatenate([key, hi * nn + lo])
+        arcs.sort()
+        src = arcs // nn
+        dst_sorted = (arcs - src * nn).astype(np.int32)
+        counts = np.bincount(src, minlength=n) if n else np.zeros(0, dtype=np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        return Graph(n, m, offsets, dst_sorted, None)
     src = np.concatenate([lo, hi])
     dst = np.concatenate([hi, lo])
-    order = np.argsort(src * max(n, 1) + dst, kind="stable")
+    order = np.argsort(src * nn + dst, kind="stable")
     dst_sorted = dst[order]
     counts = np.bincount(src, minlength=n) if n else np.zeros(0, dtype=np.int64)
-    offsets = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(counts, out=offsets[1:])
-    weights = None
-    if wk is not None:
-        weights = np.concatenate([wk, wk])[order]
+    weights = np.concatenate([wk, wk])[order]
     return Graph(n, m, offsets, dst_sorted.astype(np.int32), weights)
 
 
@@ -254,6 +268,38 @@ def load_edge_list(path, weighted: bool = False) -> Graph:
                 raise DomainError("line %d: negative weight %d" % (lineno, c))
             us.append(a), vs.append(b), ws.append(c)
     n = (max(max(us), max(vs)) + 1) if us else 0
+    return from_edge_arrays(n, us, vs, ws)
+
+
+def load_dimacs_gr(path) -> Graph:
+    """DIMACS shortest-path format (graph.py:139-173): ``c`` comments, one ``p sp n m`` problem
+    line, then ``a u v w`` arcs with 1-based vertex ids; the arc count must match the header."""
+    n = declared = None
+    us, vs, ws = [], [], []
+    with open(path) as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            tok = raw.split()
+            if not tok or tok[0].startswith("c"):
+                continue
+            if tok[0] == "p":
+                if len(tok) != 4 or tok[1] != "sp":
+                    raise ParseError("bad problem line %r" % raw.strip(), lineno)
+                n, declared = int(tok[2]), int(tok[3])
+            elif tok[0] == "a":
+                if n is None:
+                    raise ParseError("arc line before problem line", lineno)
+                if len(tok) != 4:
+                    raise ParseError("bad arc line %r" % raw.strip(), lineno)
+                a, b, c = int(tok[1]), int(tok[2]), int(tok[3])
+                if not (1 <= a <= n and 1 <= b <= n):
+                    raise FormatError("line %d: vertex out of range in %r (n=%d)" % (lineno, raw.strip(), n))
+                us.append(a - 1), vs.append(b - 1), ws.append(c)
+            else:
+                raise ParseError("unknown line type %r" % tok[0], lineno)
+    if n is None:
+        raise FormatError("missing problem line")
+    if declared != len(us):
+        raise FormatError("header declares %d arcs, file has %d" % (declared, len(us)))
     return from_edge_arrays(n, us, vs, ws)
 
 

@@ -86,7 +86,10 @@ def run_bc_multi(g, cfg):
     sources = select_sources(g, cfg)
     p, bs = prepare(g, cfg)
     mode = cfg.mode if p.num_parts > 1 else "direct"
-    device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    # the BC vector NCCL reduces must live on the device the engine runs on (open_engine's rule)
+    ordinal = cfg.device if cfg.device is not None else int(os.environ.get("LOCAL_RANK", "0"))
+    device = torch.device("cuda", ordinal)
+    torch.cuda.set_device(device)
     stats = {}
     with open_engine(g, cfg, (len(sources) + world - 1) // world) as eng:
         if p.num_parts > 1:

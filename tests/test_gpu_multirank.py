@@ -32,6 +32,11 @@ def _worker(rank, world, port, kind, mode, out):
         g = G.rmat(11, 8, 2)
         part = P.block_partition(g, world)
         sources = list(range(0, g.num_vertices, 23))
+    elif kind == "path":
+        # one cut edge: a source's backward sweep needs exactly ONE border value from the other part
+        g = G.path(240)
+        part = P.block_partition(g, world)
+        sources = [3, 50, 119, 120, 200, 239]
     else:
         g = G.road_like(30, 24, keep=0.25, seed=4)
         part = P.strip_partition(30, 24, world)
@@ -48,7 +53,9 @@ def _worker(rank, world, port, kind, mode, out):
     batches = (len(sources) + 63) // 64
     np.save("%s.%d.npy" % (out, rank), np.array([ok, res.stats["levels"], res.stats["exchanged_bytes"],
                                                  res.stats["forward_exchanges"], batches,
-                                                 res.stats["forward"] == "hybir"]))
+                                                 res.stats["forward"] == "hybir",
+                                                 res.stats["backward_exchanges"], res.stats["backward_levels"],
+                                                 res.stats["state_vertices"], g.num_vertices]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -56,17 +63,24 @@ def _worker(rank, world, port, kind, mode, out):
 @pytest.mark.parametrize("world,kind,mode", [
     (1, "road", "hybir"), (1, "rmat", "bsp-baseline"),
     (2, "rmat", "bsp-baseline"), (2, "road", "bsp-baseline"), (3, "road", "bsp-baseline"),
-    (2, "rmat", "hybir"), (2, "road", "hybir"), (3, "road", "hybir")])
+    (2, "rmat", "hybir"), (2, "road", "hybir"), (3, "road", "hybir"),
+    (2, "path", "bsp-baseline"), (2, "path", "hybir"), (4, "path", "hybir")])
 def test_graph_partitioned_ranks_match_oracle(tmp_path, world, kind, mode):
     out = str(tmp_path / "res")
     mp.spawn(_worker, args=(world, _free_port(), kind, mode, out), nprocs=world, join=True)
     for r in range(world):
-        ok, levels, nbytes, fwd_x, batches, is_hybir = np.load("%s.%d.npy" % (out, r))
+        ok, levels, nbytes, fwd_x, batches, is_hybir, bwd_x, bwd_levels, state_n, n = np.load("%s.%d.npy" % (out, r))
         assert ok, "rank %d BC differs from the oracle" % r
         if world == 1:          # one part, no borders: nothing crosses
-            assert nbytes == 0 and fwd_x == 0
+            assert nbytes == 0 and fwd_x == 0 and bwd_x == 0
             continue
         assert levels >= 3 and nbytes > 0
+        # backward: border values cross only at the levels some part pulls from another one
+        assert 0 < bwd_x <= bwd_levels - batches
+        if kind == "road":      # state arrays are owned + halo, not the whole graph
+            assert state_n < 0.75 * n
+        if kind == "path":      # ~240 levels, 6 sources, world - 1 cut edges: a handful of exchanges
+            assert bwd_levels >= 200 and bwd_x <= 6 * (world - 1)
         if mode == "hybir":
             # the border-matrix forward phase: two all-reduces per batch, whatever the depth
             assert is_hybir and fwd_x == 2 * batches

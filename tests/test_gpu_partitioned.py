@@ -242,3 +242,124 @@ def test_hybir_queue_sweeps_match_dense_sweeps(k):
     assert np.array_equal(out[1][3], out[0][3]) and np.array_equal(out[1][4], out[0][4])
     # far fewer launches: thousands of dense levels against a few persistent sweeps
     assert out[1][2]["launches"] < out[0][2]["launches"]
+
+
+def test_refinement_bound_with_many_thin_parts():
+    """k > 2: a shortest path crosses up to k - 1 cuts and one refinement iteration settles one
+    crossing, so the iteration bound is the total border count, not the largest part's
+    (path(64) in 8 blocks: 2 borders per part, source 0 needs 7 crossings + 1 settling round)."""
+    g = G.path(64)
+    part = P.block_partition(g, 8)
+    srcs = [0, 63, 31, 5]
+    with Engine(g) as e:
+        e.set_partition(8, part.assignment)
+        assert max(e.border_counts(8)) == 2
+        dist, sigma, delta = e.debug_sources(srcs, MODE_HYBIR)
+        bc, st = e.run(list(range(64)), MODE_HYBIR)
+    _check_sources(g, srcs, dist, sigma, delta)
+    obc, _ = O.brandes_bc(g, list(range(64)))
+    assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+    assert st["iterations"] >= 8          # source 0 alone needs 8
+    # a tree-like graph in many parts
+    g = G.random_connected(300, 310, seed=5)
+    part = P.block_partition(g, 12)
+    srcs = list(range(0, 300, 7))
+    with Engine(g) as e:
+        e.set_partition(12, part.assignment)
+        bc, _ = e.run(srcs, MODE_HYBIR)
+    obc, _ = O.brandes_bc(g, srcs)
+    assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("shape", ["road", "rmat"])
+def test_lookahead_gives_the_same_result(shape):
+    """pipeline_sources (engine.py:156-161; reference test_engine.py:57-64): Step 1 of the next
+    batch runs beside the border phase of the current one; BC is identical, bit for bit."""
+    if shape == "road":
+        g = G.road_like(48, 48, keep=0.2, seed=2)
+        part = P.strip_partition(48, 48, 3)
+    else:
+        g = G.rmat(10, 8, 3)
+        part = P.block_partition(g, 2)
+    srcs = list(range(0, g.num_vertices, 5))[:200]
+    cfg = P.RunConfig(sources=srcs, mode="hybir", partition=part, num_partitions=part.num_parts, groups=2,
+                      per_source_reports=False)
+    plain = P.run_bc(g, cfg)
+    ahead = P.pipeline_sources(g, cfg)
+    assert plain.pipeline_overlaps == 0
+    assert ahead.pipeline_overlaps == (len(srcs) + 63) // 64 - 1
+    assert np.array_equal(plain.bc, ahead.bc)
+    obc, _ = O.brandes_bc(g, srcs)
+    assert np.allclose(ahead.bc, obc, rtol=RTOL, atol=ATOL)
+    with pytest.raises(P.InputError):
+        P.pipeline_sources(g, P.RunConfig(sources=srcs, mode="bsp-baseline"))
+
+
+def test_border_table_cache_round_trip(tmp_path):
+    """Border-table disk cache keyed by (graph, partition) (border_matrix.py:85-125)."""
+    g = G.road_like(40, 40, keep=0.2, seed=4)
+    part = P.strip_partition(40, 40, 4)
+    srcs = list(range(0, g.num_vertices, 37))
+    cfg = P.RunConfig(sources=srcs, mode="hybir", partition=part, num_partitions=4,
+                      table_cache_dir=str(tmp_path), per_source_reports=False)
+    first = P.run_bc(g, cfg)
+    assert first.stats["border_tables_from_cache"] is False
+    files = list(tmp_path.iterdir())
+    assert len(files) == 1 and files[0].name.startswith("border_tables_")
+    second = P.run_bc(g, cfg)
+    assert second.stats["border_tables_from_cache"] is True
+    assert np.array_equal(first.bc, second.bc)
+    # another partition of the same graph misses the cache
+    other = P.RunConfig(sources=srcs, mode="hybir", partition=P.strip_partition(40, 40, 2), num_partitions=2,
+                        table_cache_dir=str(tmp_path), per_source_reports=False)
+    assert P.run_bc(g, other).stats["border_tables_from_cache"] is False
+    assert len(list(tmp_path.iterdir())) == 2
+    # installed tables equal computed ones
+    with Engine(g) as e:
+        e.set_partition(4, part.assignment)
+        counts = e.border_counts(4)
+        tabs = [e.border_tables(p, int(counts[p])) for p in range(4)]
+    with Engine(g) as e:
+        e.set_partition(4, part.assignment)
+        for p in range(4):
+            e.set_border_tables(p, tabs[p][1], tabs[p][2])
+        bc, _ = e.run(srcs, MODE_HYBIR)
+    assert np.array_equal(bc, first.bc)
+
+
+def test_hybir_falls_back_to_bsp_when_tables_exceed_the_budget():
+    g = G.rmat(10, 8, 1)
+    srcs = list(range(0, 1024, 9))
+    cfg = P.RunConfig(sources=srcs, mode="hybir", num_partitions=2, table_budget_bytes=1e3)
+    with pytest.warns(UserWarning, match="bsp-baseline"):
+        res = P.run_bc(g, cfg)
+    assert res.stats["mode"] == "bsp-baseline"
+    assert "supersteps" in res.per_source[0]["forward"]
+    obc, _ = O.brandes_bc(g, srcs)
+    assert np.allclose(res.bc, obc, rtol=RTOL, atol=ATOL)
+
+
+def test_malformed_csr_is_refused():
+    from paper_2008_05718_b200.graph import Graph
+    g = G.path(5)
+    bad = Graph(5, g.num_edges, g.offsets.copy(), g.col_idx.copy())
+    bad.col_idx[3] = 7
+    with pytest.raises(P.InputError, match="col_idx"):
+        Engine(bad)
+    off = g.offsets.copy()
+    off[2], off[3] = off[3], off[2] - 1
+    with pytest.raises(P.InputError, match="offsets"):
+        Engine(Graph(5, g.num_edges, off, g.col_idx.copy()))
+
+
+def test_failed_run_leaves_no_partial_sums_behind():
+    """A run that fails after some batches must not leak their BC partials into the next run."""
+    g = G.rmat(10, 8, 1)
+    srcs = list(range(0, 1024, 3))
+    with Engine(g) as e:
+        e.set_option("groups", 2)
+        good, _ = e.run(srcs)
+        with pytest.raises(P.InputError):
+            e.run(srcs + [g.num_vertices + 5])
+        again, _ = e.run(srcs)
+    assert np.array_equal(good, again)

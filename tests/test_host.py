@@ -2,6 +2,7 @@
 selection and configuration errors -- the reference's behaviour for each is
 cited next to the check."""
 
+import os
 import random
 
 import numpy as np
@@ -180,6 +181,61 @@ def test_local_rows_for_graph_partitioned_mode():
     assert total == g.num_arcs
 
 
+def test_local_graph_owned_plus_halo_numbering():
+    """A rank's state arrays cover its own vertices + the other parts' borders next to them, not
+    the whole graph; every rank lists all borders and its own cut arcs in local ids."""
+    from paper_2008_05718_b200.partitioned import LocalGraph, incoming_cut_arcs
+    for g, part in ((G.grid(8, 6), P.strip_partition(8, 6, 4)), (G.rmat(9, 6, 1), None)):
+        if part is None:
+            part = P.block_partition(g, 3)
+        k = part.num_parts
+        bs = P.identify_borders(g, part)
+        a = np.asarray(part.assignment)
+        covered = 0
+        for r in range(k):
+            lg = LocalGraph(g, part, bs, r)
+            assert lg.n_local == lg.n_own + lg.n_halo + (k - 1)
+            assert lg.n_own == int((a == r).sum())
+            # halo = exactly the foreign endpoints of this rank's cut arcs
+            src, dst = np.asarray(bs.cut_src), np.asarray(bs.cut_dst)
+            want_halo = np.unique(dst[a[src] == r])
+            assert sorted(lg.halo.tolist()) == want_halo.tolist()
+            # rows: owned vertices keep their adjacency (mapped), the rest is empty
+            deg = np.diff(lg.graph.offsets)
+            assert (deg[lg.n_own:] == 0).all()
+            back = np.concatenate([lg.owned, lg.halo])
+            for i in range(0, lg.n_own, max(1, lg.n_own // 7)):
+                v = lg.owned[i]
+                mine = back[lg.graph.col_idx[lg.graph.offsets[i]:lg.graph.offsets[i + 1]]]
+                assert mine.tolist() == g.col_idx[g.offsets[v]:g.offsets[v + 1]].tolist()
+            # border lists: own borders are owned ids, foreign ones halo ids or the part's catch-all
+            assert lg.border_off.tolist() == np.concatenate(([0], np.cumsum(bs.counts()))).tolist()
+            for q in range(k):
+                lv = lg.border_v[lg.border_off[q]:lg.border_off[q + 1]]
+                glob = np.asarray(bs.border_arrays[q])
+                if q == r:
+                    assert (lv < lg.n_own).all() and (lg.owned[lv] == glob).all()
+                else:
+                    in_halo = np.isin(glob, lg.halo)
+                    assert (back[lv[in_halo]] == glob[in_halo]).all()
+                    assert (lv[~in_halo] == lg.catch_all[q]).all()
+                    assert (lg.assignment[lv] == q).all()
+            # own cut arcs, border by border
+            mine = np.asarray(bs.border_arrays[r])
+            assert len(lg.cut_off) == len(mine) + 1 and lg.cut_off[-1] == int((a[src] == r).sum())
+            for j in range(0, len(mine), max(1, len(mine) // 5)):
+                far = back[lg.cut_dst[lg.cut_off[j]:lg.cut_off[j + 1]]]
+                assert far.tolist() == dst[src == mine[j]].tolist()
+            # sources: owned or halo ids, -1 elsewhere
+            loc = lg.local_of[np.arange(g.num_vertices)]
+            assert ((loc >= 0) == (np.isin(np.arange(g.num_vertices), back))).all()
+            covered += lg.n_own
+            assert lg.n_local < g.num_vertices or k == 1 or g.num_vertices < 64
+        assert covered == g.num_vertices
+        cin_off, cin_src = incoming_cut_arcs(bs, bs.border_arrays)
+        assert cin_off[-1] == len(bs.cut_src) == len(cin_src)
+
+
 def test_reference_acceptance_corpus_host_side():
     """The reference's acceptance corpus (test_acceptance.py:69-153; digest produced by
     tests/golden/gen_acceptance_corpus.py): the generator builds the same 200 graphs, the restated
@@ -246,3 +302,102 @@ def test_bench_reference_arm_line_shape():
                            "d2h_bytes_per_step": 0}
     for key in ("unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "config"):
         assert key in line
+
+
+def test_import_partition_file(tmp_path):
+    """METIS-style partition files (reference partition.py:112-136; test_engine.py:118-123)."""
+    g = G.path(6)
+    f = tmp_path / "p.txt"
+    f.write_text("0\n0\n\n1\n1\n2\n2\n")           # blank lines are skipped
+    p = P.import_partition(str(f), g, 3)
+    assert p.assignment.tolist() == [0, 0, 1, 1, 2, 2] and p.num_parts == 3
+    assert abs(p.ratio - 2 / 6) < 1e-12
+    bs = P.identify_borders(g, p)
+    assert [b.tolist() for b in bs.border_arrays] == [[1], [2, 3], [4]]
+    f.write_text("0\n1\nx\n")
+    with pytest.raises(P.FormatError, match="line 3"):
+        P.import_partition(str(f), g, 2)
+    f.write_text("0\n1\n2\n0\n0\n0\n")
+    with pytest.raises(P.FormatError, match="outside"):
+        P.import_partition(str(f), g, 2)
+    f.write_text("0\n1\n")
+    with pytest.raises(P.FormatError, match="2 lines"):
+        P.import_partition(str(f), g, 2)
+    f.write_text("0\n" * 6)
+    with pytest.warns(UserWarning, match="empty"):
+        assert P.import_partition(str(f), g, 2).degenerate
+    # through the front door: partition_file feeds make_partition
+    from paper_2008_05718_b200.engine import make_partition
+    f.write_text("0\n0\n0\n1\n1\n1\n")
+    cfg = P.RunConfig(partition_file=str(f), num_partitions=2)
+    assert make_partition(g, cfg).assignment.tolist() == [0, 0, 0, 1, 1, 1]
+
+
+def test_mode_falls_back_when_the_border_tables_do_not_fit():
+    """hybir needs b_p^2 x 12 B of tables per part; above the budget run_bc switches to the
+    reference's other partitioned mode instead of failing (SURVEY.md hard part 2)."""
+    g = G.rmat(10, 8, 1)
+    bs = P.identify_borders(g, P.block_partition(g, 2))
+    need = P.border_table_bytes(bs)
+    assert need == sum(12.0 * b * b for b in bs.counts()) and need > 0
+    assert P.choose_mode("hybir", bs, need) == "hybir"
+    with pytest.warns(UserWarning, match="bsp-baseline"):
+        assert P.choose_mode("hybir", bs, need - 1) == "bsp-baseline"
+    assert P.choose_mode("bsp-baseline", bs, 0) == "bsp-baseline"
+    assert P.choose_mode("direct", bs, 0) == "direct"
+
+
+def test_load_dimacs_gr(tmp_path):
+    f = tmp_path / "g.gr"
+    f.write_text("c comment\np sp 4 4\na 1 2 3\na 2 1 3\na 2 3 1\na 4 3 2\n")
+    g = P.load_dimacs_gr(str(f))
+    assert (g.num_vertices, g.num_edges) == (4, 3)
+    assert g.offsets.tolist() == [0, 1, 3, 5, 6]
+    assert g.arc_weight.tolist() == [3, 3, 1, 1, 2, 2]
+    f.write_text("p sp 2 2\na 1 2 1\n")
+    with pytest.raises(P.FormatError, match="declares 2 arcs"):
+        P.load_dimacs_gr(str(f))
+    f.write_text("a 1 2 1\n")
+    with pytest.raises(P.ParseError):
+        P.load_dimacs_gr(str(f))
+    f.write_text("p sp 2 1\na 1 3 1\n")
+    with pytest.raises(P.FormatError, match="out of range"):
+        P.load_dimacs_gr(str(f))
+
+
+def test_refine_partition_lowers_the_cut_and_keeps_the_balance():
+    from paper_2008_05718_b200.partition import cut_size
+    for g, k in ((G.road_like(96, 96, keep=0.2, seed=3), 4), (G.grid(40, 40), 3), (G.rmat(11, 8, 2), 4)):
+        n = g.num_vertices
+        for start in (P.block_partition(g, k), P.grow_partition(g, k, seed=1)):
+            out = P.refine_partition(g, start)
+            assert out.num_parts == k and len(out.assignment) == n
+            assert cut_size(g, out) <= cut_size(g, start)
+            assert max(out.sizes) <= int(1.05 * n / k) + 1 or max(out.sizes) <= max(start.sizes)
+        best = P.mincut_partition(g, k, seed=0)
+        assert cut_size(g, best) <= cut_size(g, P.grow_partition(g, k, seed=0))
+    # a scrambled grid: refinement must recover most of the locality
+    g = G.grid(32, 32)
+    rng = np.random.default_rng(0)
+    noisy = P.strip_partition(32, 32, 2).assignment.copy()
+    flip = rng.random(len(noisy)) < 0.1
+    noisy[flip] = 1 - noisy[flip]
+    start = P.Partition(noisy, 0.5, 2)
+    assert cut_size(g, P.refine_partition(g, start)) < cut_size(g, start) // 2
+
+
+def test_bench_samples_are_strided():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    srcs = list(range(0, 2048, 2))
+    s = bench.strided_sample(srcs, 16)
+    assert len(s) == 16 and s[0] == srcs[0] and s == sorted(set(s))
+    assert max(np.diff(s)) == min(np.diff(s)) == 128           # evenly spread, not a prefix
+    assert bench.strided_sample(srcs, 5000) == srcs
+    g = G.rmat(12, 8, 1)
+    all_src = bench.pick_sources(g.num_vertices, 1024)
+    full = bench.isolated_fraction(g, all_src)
+    assert abs(bench.isolated_fraction(g, bench.strided_sample(all_src, 256)) - full) < 0.08
