@@ -196,6 +196,8 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
     cg::grid_group grid = cg::this_grid();
     __shared__ int32_t stage[kDeepWarps][kStage];
     __shared__ int64_t s_pref[kDeepMaxGroups + 1];
+    __shared__ unsigned long long s_stat[8];
+    __shared__ uint32_t s_live[kDeepMaxGroups];
     __shared__ int s_cont;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
@@ -218,8 +220,26 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
         {
             const int64_t total = s_pref[p.ng];
             int g = 0;
+            // Appends to a group's queue cost one atomic on q_count[g] per flush, and every warp of
+            // the grid hits the same few words: the staging buffer is carried over the iterations
+            // of a group and flushed only when it runs full, the group changes or the phase ends.
+            int staged = 0;       // warp-uniform
+            int staged_g = 0;     // group the staged vertices belong to
+            auto flush = [&]() {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(p.q.q_count + staged_g, (unsigned long long)staged);
+                base = __shfl_sync(kFull, base, 0);
+                const size_t qb = (size_t)staged_g * p.q.cap;
+                for (int k = lane; k < staged; k += 32) p.q.q_v[qb + base + k] = stage[warp][k];
+                staged = 0;
+                __syncwarp();
+            };
             for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
                 while (f0 >= s_pref[g + 1]) ++g;   // f0 only grows
+                if (g != staged_g) {
+                    if (staged) flush();
+                    staged_g = g;
+                }
                 const int64_t end = p.q.q_end[g];
                 const int64_t i = p.q.q_beg[g] + (f0 - s_pref[g]) + lane;
                 const uint32_t *gvis = p.vis + (size_t)g * n;
@@ -238,47 +258,28 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
                 int rounds = (int)(e - a);
                 rounds = __reduce_max_sync(kFull, rounds);
                 const double *urow = gsig + (size_t)u * 32;
-                int staged = 0;  // warp-uniform
-                auto flush = [&]() {
-                    unsigned long long base = 0;
-                    if (lane == 0) base = atomicAdd(p.q.q_count + g, (unsigned long long)staged);
-                    base = __shfl_sync(kFull, base, 0);
-                    for (int k = lane; k < staged; k += 32) p.q.q_v[qbase + base + k] = stage[warp][k];
-                    staged = 0;
-                    __syncwarp();
-                };
-                for (int r = 0; r < rounds; ++r, ++a) {
-                    bool fresh_vertex = false;
-                    int32_t w = 0;
-                    if (a < e) {
-                        w = __ldg(p.col + a);
-                        uint32_t fresh = mask & ~gvis[w];
-                        if (fresh) {
-                            const uint32_t old = atomicOr(gnext + w, fresh);
-                            fresh_vertex = old == 0;
-                            double *wrow = gsig + (size_t)w * 32;
-                            while (fresh) {
-                                const int bit = __ffs(fresh) - 1;
-                                fresh &= fresh - 1;
-                                atomicAdd(wrow + bit, urow[bit]);  // exact: integer-valued fp64
-                                ++c_t;
-                            }
-                        }
-                    }
-                    const unsigned newm = __ballot_sync(kFull, fresh_vertex);
-                    if (newm) {
-                        if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
-                        staged += __popc(newm);
-                        __syncwarp();
-                        if (staged > kStage - 32) flush();
-                    }
-                }
-                if (staged) flush();
+                push_entry_thin(a, e, rounds, mask, p.col, gvis, gnext, gsig, urow, c_t,
+                                [&](bool fresh_vertex, int32_t w) {
+                                    const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+                                    if (newm) {
+                                        if (fresh_vertex)
+                                            stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
+                                        staged += __popc(newm);
+                                        __syncwarp();
+                                        if (staged > kStage - 32) flush();
+                                    }
+                                });
             }
+            if (staged) flush();
         }
         {
+            // DAG arcs of the level: one global atomic per block
+            if (threadIdx.x == 0) s_stat[5] = 0ull;
+            __syncthreads();
             const unsigned t = __reduce_add_sync(kFull, c_t);
-            if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
+            if (lane == 0 && t) atomicAdd(&s_stat[5], (unsigned long long)t);
+            __syncthreads();
+            if (threadIdx.x == 0 && s_stat[5]) atomicAdd(p.counters + 2, s_stat[5]);
         }
         // border seeds of level L: more pushes into the same level (atomics on sigma / next)
         if (p.seeds.idx != nullptr && L < p.seeds.levels) {
@@ -297,14 +298,21 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
         }
         __syncthreads();
         {
+            // The level's statistics are five counters shared by the whole grid: every thread
+            // keeps its own partial sums over the level, the block adds them up in shared memory
+            // and issues ONE set of global atomics per level (a warp-per-iteration atomic on the
+            // same five words serialises the whole grid at one L2 slice).
+            if (threadIdx.x < 8) s_stat[threadIdx.x] = 0ull;
+            for (int k = threadIdx.x; k < p.ng; k += blockDim.x) s_live[k] = 0u;
+            __syncthreads();
             const int64_t total = s_pref[p.ng];
             int g = 0;
+            unsigned long long nr = 0, ar = 0, nv = 0, fa = 0, md = 0;
             for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
                 while (f0 >= s_pref[g + 1]) ++g;
                 const int64_t end = (int64_t)p.q.q_count[g];
                 const int64_t i = p.q_lbeg[g] + (f0 - s_pref[g]) + lane;
                 const size_t qbase = (size_t)g * p.q.cap;
-                unsigned long long nr = 0, ar = 0, nv = 0, fa = 0, md = 0;
                 uint32_t any = 0;
                 if (i < end) {
                     const int32_t w = p.q.q_v[qbase + i];
@@ -314,29 +322,39 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
                     p.next[(size_t)g * n + w] = 0u;
                     const unsigned long long deg = (unsigned long long)(p.off[w + 1] - p.off[w]);
                     any = m;
-                    nr = __popc(m);
-                    ar = __popc(m) * deg;
-                    nv = 1;
-                    fa = deg;
-                    md = deg;
+                    nr += __popc(m);
+                    ar += __popc(m) * deg;
+                    nv += 1;
+                    fa += deg;
+                    md = max(md, deg);
                 }
                 any = __reduce_or_sync(kFull, any);
-                for (int o = 16; o > 0; o >>= 1) {
-                    nr += __shfl_xor_sync(kFull, nr, o);
-                    ar += __shfl_xor_sync(kFull, ar, o);
-                    nv += __shfl_xor_sync(kFull, nv, o);
-                    fa += __shfl_xor_sync(kFull, fa, o);
-                    md = max(md, __shfl_xor_sync(kFull, md, o));
-                }
-                if (lane == 0) {
-                    atomicOr(p.live + (size_t)L * p.G + g, any);
-                    atomicAdd(p.counters + 0, nr);
-                    atomicAdd(p.counters + 1, ar);
-                    atomicAdd(p.lstat + 0, nv);
-                    atomicAdd(p.lstat + 1, fa);
-                    atomicMax(p.lstat + 2, md);
-                }
+                if (lane == 0 && any) atomicOr(&s_live[g], any);
             }
+            for (int o = 16; o > 0; o >>= 1) {
+                nr += __shfl_xor_sync(kFull, nr, o);
+                ar += __shfl_xor_sync(kFull, ar, o);
+                nv += __shfl_xor_sync(kFull, nv, o);
+                fa += __shfl_xor_sync(kFull, fa, o);
+                md = max(md, __shfl_xor_sync(kFull, md, o));
+            }
+            if (lane == 0 && nv) {
+                atomicAdd(&s_stat[0], nr);
+                atomicAdd(&s_stat[1], ar);
+                atomicAdd(&s_stat[2], nv);
+                atomicAdd(&s_stat[3], fa);
+                atomicMax(&s_stat[4], md);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && s_stat[2]) {
+                atomicAdd(p.counters + 0, s_stat[0]);
+                atomicAdd(p.counters + 1, s_stat[1]);
+                atomicAdd(p.lstat + 0, s_stat[2]);
+                atomicAdd(p.lstat + 1, s_stat[3]);
+                atomicMax(p.lstat + 2, s_stat[4]);
+            }
+            for (int k = threadIdx.x; k < p.ng; k += blockDim.x)
+                if (s_live[k]) atomicOr(p.live + (size_t)L * p.G + k, s_live[k]);
         }
         grid.sync();
 
@@ -437,28 +455,11 @@ __global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepB
                 double *gcoef = p.coef + (size_t)g * n * 32;
                 const int64_t v = p.q.q_v[qbase + i];
                 const uint32_t m = p.q.q_m[qbase + i];
-                uint32_t want = m;
-                const int64_t a0 = p.off[v], a1 = p.off[v + 1];
-                double total_d = 0.0;
-                while (want) {
-                    const int bit = __ffs(want) - 1;
-                    want &= want - 1;
-                    double acc = 0.0;
-                    if (gn != nullptr)
-                        for (int64_t a = a0; a < a1; ++a) {
-                            const int32_t w = __ldg(p.col + a);
-                            if ((gn[w] >> bit) & 1u) acc += gcoef[(size_t)w * 32 + bit];
-                        }
-                    const size_t idx = (size_t)v * 32 + bit;
-                    const double sv = gsig[idx];
-                    const double d = sv * acc;
-                    gcoef[idx] = (1.0 + d) / sv;
-                    if (STORE_DELTA) p.delta[(size_t)g * n * 32 + idx] = d;
-                    else if (p.accumulate & 2) clear_after_use(gsig + idx, sv);   // see finalize_backward
-                    total_d += d;
-                }
-                if (p.accumulate & 1) p.bcg[(size_t)g * n + v] += total_d;
                 wr[(size_t)g * n + v] = m;   // level L becomes the children masks of level L - 1
+                if (m != 0)
+                    pull_entry_thin<STORE_DELTA>(v, m, p.off[v], p.off[v + 1], p.col, gn, gsig, gcoef,
+                                                 STORE_DELTA ? p.delta + (size_t)g * n * 32 : nullptr,
+                                                 p.bcg + (size_t)g * n, p.accumulate);
             }
         }
         __syncthreads();   // s_pref is rewritten by the next level

@@ -703,6 +703,131 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_kernel(
     if (lane == 0 && t) atomicAdd(counters + 2, (unsigned long long)t);
 }
 
+// ---- thread-per-entry work of the thin (low-degree) levels ---------------------------------
+// These levels are latency-bound: a thread's work is a chain of dependent random accesses
+// (adjacency word -> visited word -> atomic on the next-level word), and with one arc per loop
+// trip the chain is 3 round trips PER ARC.  The helpers below take the arcs kThinArcs at a
+// time and issue each stage for all of them before anything is consumed, so a whole entry of a
+// road-like graph (degree <= 4) costs 3 round trips in all (ncu of the persistent sweeps:
+// 5-8 % issue utilisation, long-scoreboard + barrier stalls; profiles/r2_deep_kernels_ncu.md).
+constexpr int kThinArcs = 4;
+
+// Top-down push of one frontier entry (u, mask) along its arcs [a, e): new lanes are OR-ed into
+// next[w], path counts added with red.global.add.f64 (integer-valued, exact in any order), and
+// every vertex that was not in the next level yet is handed to `stage_vertex` under a
+// warp-wide ballot (all 32 threads of the warp call this together; `rounds` = largest degree
+// in the warp).
+template <typename StageFn>
+__device__ __forceinline__ void push_entry_thin(int64_t a, int64_t e, int rounds, uint32_t mask,
+                                                const int32_t *__restrict__ col,
+                                                const uint32_t *__restrict__ gvis, uint32_t *gnext,
+                                                double *gsig, const double *urow, unsigned &c_t,
+                                                StageFn stage_vertex) {
+    // path count of the entry's first lane, fetched beside the adjacency (most entries of a
+    // thin level carry one lane)
+    const int bit0 = mask ? __ffs(mask) - 1 : 0;
+    const double s0 = (a < e) ? urow[bit0] : 0.0;
+    for (int r0 = 0; r0 < rounds; r0 += kThinArcs) {
+        int32_t w[kThinArcs];
+        uint32_t fresh[kThinArcs], old[kThinArcs];
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) w[k] = (a + r0 + k < e) ? __ldg(col + a + r0 + k) : -1;
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) fresh[k] = (w[k] >= 0) ? (mask & ~gvis[w[k]]) : 0u;
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) old[k] = fresh[k] ? atomicOr(gnext + w[k], fresh[k]) : 1u;
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) {
+            uint32_t f = fresh[k];
+            if (f == 0) continue;
+            double *wrow = gsig + (size_t)w[k] * 32;
+            while (f) {
+                const int bit = __ffs(f) - 1;
+                f &= f - 1;
+                atomicAdd(wrow + bit, bit == bit0 ? s0 : urow[bit]);
+                ++c_t;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) {
+            if (r0 + k >= rounds) break;                      // warp-uniform
+            stage_vertex(fresh[k] != 0 && old[k] == 0, w[k]);
+        }
+    }
+}
+
+// Backward pull of one queue entry (v, want) over its arcs [a0, a1): per lane of the entry the
+// children's coef summed in arc order (process_level vertex-pull, backward.py:95-103), then
+// delta, coef and the BC partial -- the arithmetic of scan_arcs + finalize_backward, serial.
+template <bool STORE_DELTA>
+__device__ __forceinline__ void pull_entry_thin(int64_t v, uint32_t want, int64_t a0, int64_t a1,
+                                                const int32_t *__restrict__ col, const uint32_t *gn,
+                                                double *gsig, double *gcoef, double *gdelta,
+                                                double *gbcg, int accumulate) {
+    double total = 0.0;
+    const int bit_first = __ffs(want) - 1;
+    const double sv_first = gsig[(size_t)v * 32 + bit_first];   // independent of the arc chain
+    if (a1 - a0 <= kThinArcs || gn == nullptr) {
+        // the whole adjacency in registers: one round trip per stage
+        int32_t w[kThinArcs];
+        uint32_t nm[kThinArcs];
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) w[k] = (gn != nullptr && a0 + k < a1) ? __ldg(col + a0 + k) : -1;
+#pragma unroll
+        for (int k = 0; k < kThinArcs; ++k) nm[k] = (w[k] >= 0) ? __ldg(gn + w[k]) : 0u;
+        uint32_t rest = want;
+        while (rest) {
+            const int bit = __ffs(rest) - 1;
+            rest &= rest - 1;
+            double c[kThinArcs];
+#pragma unroll
+            for (int k = 0; k < kThinArcs; ++k)
+                c[k] = ((nm[k] >> bit) & 1u) ? gcoef[(size_t)w[k] * 32 + bit] : 0.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < kThinArcs; ++k)
+                if ((nm[k] >> bit) & 1u) acc += c[k];            // ascending arc order
+            const size_t idx = (size_t)v * 32 + bit;
+            const double sv = bit == bit_first ? sv_first : gsig[idx];
+            const double d = sv * acc;
+            gcoef[idx] = (1.0 + d) / sv;
+            if (STORE_DELTA) gdelta[idx] = d;
+            else if (accumulate & 2) clear_after_use(gsig + idx, sv);   // see finalize_backward
+            total += d;
+        }
+    } else {
+        uint32_t rest = want;
+        while (rest) {
+            const int bit = __ffs(rest) - 1;
+            rest &= rest - 1;
+            double acc = 0.0;
+            for (int64_t b = a0; b < a1; b += kThinArcs) {
+                int32_t w[kThinArcs];
+                uint32_t nm[kThinArcs];
+                double c[kThinArcs];
+#pragma unroll
+                for (int k = 0; k < kThinArcs; ++k) w[k] = (b + k < a1) ? __ldg(col + b + k) : -1;
+#pragma unroll
+                for (int k = 0; k < kThinArcs; ++k) nm[k] = (w[k] >= 0) ? __ldg(gn + w[k]) : 0u;
+#pragma unroll
+                for (int k = 0; k < kThinArcs; ++k)
+                    c[k] = ((nm[k] >> bit) & 1u) ? gcoef[(size_t)w[k] * 32 + bit] : 0.0;
+#pragma unroll
+                for (int k = 0; k < kThinArcs; ++k)
+                    if ((nm[k] >> bit) & 1u) acc += c[k];
+            }
+            const size_t idx = (size_t)v * 32 + bit;
+            const double sv = bit == bit_first ? sv_first : gsig[idx];
+            const double d = sv * acc;
+            gcoef[idx] = (1.0 + d) / sv;
+            if (STORE_DELTA) gdelta[idx] = d;
+            else if (accumulate & 2) clear_after_use(gsig + idx, sv);
+            total += d;
+        }
+    }
+    if (accumulate & 1) gbcg[v] += total;
+}
+
 // Thin variant for levels of low-degree vertices (road-like graphs): one THREAD
 // per queue entry walks its few arcs, so a warp advances 32 frontier vertices
 // at once instead of leaving 29 of 32 lanes idle on a 3-arc adjacency.
@@ -744,32 +869,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) fwd_push_thin_kernel(
         int rounds = (int)(e - a);
         rounds = __reduce_max_sync(kFull, rounds);
         const double *urow = gsig + (size_t)u * 32;
-        for (int r = 0; r < rounds; ++r, ++a) {
-            bool fresh_vertex = false;
-            int32_t w = 0;
-            if (a < e) {
-                w = __ldg(col + a);
-                uint32_t fresh = mask & ~gvis[w];
-                if (fresh) {
-                    const uint32_t old = atomicOr(gnext + w, fresh);
-                    fresh_vertex = old == 0;
-                    double *wrow = gsig + (size_t)w * 32;
-                    while (fresh) {
-                        const int bit = __ffs(fresh) - 1;
-                        fresh &= fresh - 1;
-                        atomicAdd(wrow + bit, urow[bit]);
-                        ++c_t;
-                    }
-                }
-            }
-            const unsigned newm = __ballot_sync(kFull, fresh_vertex);
-            if (newm) {
-                if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
-                staged += __popc(newm);
-                __syncwarp();
-                if (staged > kStage - 32) flush();
-            }
-        }
+        push_entry_thin(a, e, rounds, mask, col, gvis, gnext, gsig, urow, c_t,
+                        [&](bool fresh_vertex, int32_t w) {
+                            const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+                            if (newm) {
+                                if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w;
+                                staged += __popc(newm);
+                                __syncwarp();
+                                if (staged > kStage - 32) flush();
+                            }
+                        });
     }
     if (staged) flush();
     const unsigned t = __reduce_add_sync(kFull, c_t);
@@ -1009,27 +1118,10 @@ __global__ void bwd_queue_thin_kernel(const int64_t *__restrict__ off,
     for (int64_t i = beg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = q.q_v[g * q.cap + i];
-        uint32_t want = q.q_m[g * q.cap + i];
-        const int64_t a0 = off[v], a1 = off[v + 1];
-        double total = 0.0;
-        while (want) {
-            const int bit = __ffs(want) - 1;
-            want &= want - 1;
-            double acc = 0.0;
-            if (gn != nullptr)
-                for (int64_t a = a0; a < a1; ++a) {
-                    const int32_t w = __ldg(col + a);
-                    if ((__ldg(gn + w) >> bit) & 1u) acc += gcoef[(size_t)w * 32 + bit];
-                }
-            const size_t idx = (size_t)v * 32 + bit;
-            const double sv = gsig[idx];
-            const double d = sv * acc;
-            gcoef[idx] = (1.0 + d) / sv;
-            if (STORE_DELTA) delta[g * n * 32 + idx] = d;
-            else if (accumulate & 2) clear_after_use(gsig + idx, sv);   // see finalize_backward
-            total += d;
-        }
-        if (accumulate & 1) bcg[g * n + v] += total;
+        const uint32_t want = q.q_m[g * q.cap + i];
+        if (want == 0) continue;
+        pull_entry_thin<STORE_DELTA>(v, want, off[v], off[v + 1], col, gn, gsig, gcoef,
+                                     STORE_DELTA ? delta + g * n * 32 : nullptr, bcg + g * n, accumulate);
     }
 }
 

@@ -1,0 +1,765 @@
+// engine_state.cuh -- device memory arena, the handle (bc_handle) and its state: CSR + work items, per-batch
+// BFS state, frontier queues, border state; allocation / release helpers and the kernel-parameter builders.
+// Part of the single translation unit bc_engine.cu (included from there, in this order: engine_state,
+// engine_sweeps, engine_border, engine_run, engine_dist).
+#pragma once
+namespace {
+
+thread_local std::string g_create_error;
+
+
+// ------------------------------------------------------------------------------------
+// Device memory arena.  cudaMalloc / cudaFree of the multi-GB batch state cost
+// 15-20 ms per run_bc() call (and cudaFree drains the device); blocks released by
+// a handle are kept per device and handed to the next handle that asks for a
+// similar size.  bc_release_cached_memory() returns them to the driver, and an
+// allocation that fails flushes the cache before it gives up.
+// ------------------------------------------------------------------------------------
+struct Arena {
+    std::mutex mu;
+    std::unordered_map<void *, std::pair<int, size_t>> live;   // ptr -> (device, bytes)
+    std::multimap<size_t, void *> spare[64];                   // per device, by size
+    size_t spare_bytes = 0;
+
+    static size_t round_up(size_t b) {
+        const size_t g = b < (1u << 20) ? 512 : (size_t)2 << 20;   // driver granularity for big blocks
+        return (std::max<size_t>(b, 1) + g - 1) / g * g;
+    }
+    void flush_locked(int dev) {
+        for (auto &kv : spare[dev]) {
+            cudaFree(kv.second);
+            spare_bytes -= kv.first;
+        }
+        spare[dev].clear();
+    }
+    cudaError_t alloc(void **out, size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        dev &= 63;
+        const size_t want = round_up(bytes);
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = spare[dev].lower_bound(want);
+        if (it != spare[dev].end() && it->first <= want + want / 4 + (1u << 16)) {
+            *out = it->second;
+            live[*out] = {dev, it->first};
+            spare_bytes -= it->first;
+            spare[dev].erase(it);
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaMalloc(out, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            flush_locked(dev);
+            e = cudaMalloc(out, want);
+        }
+        if (e == cudaSuccess) live[*out] = {dev, want};
+        return e;
+    }
+    void release(void *p) {
+        if (p == nullptr) return;
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = live.find(p);
+        if (it == live.end()) {  // not ours
+            cudaFree(p);
+            return;
+        }
+        spare[it->second.first].emplace(it->second.second, p);
+        spare_bytes += it->second.second;
+        live.erase(it);
+    }
+    void flush_all() {
+        std::lock_guard<std::mutex> lock(mu);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (int d = 0; d < 64; ++d)
+            if (!spare[d].empty()) {
+                cudaSetDevice(d);
+                flush_locked(d);
+            }
+        cudaSetDevice(cur);
+    }
+};
+Arena &arena() {
+    static Arena *a = new Arena();  // leaked on purpose: the driver may be gone at exit
+    return *a;
+}
+inline cudaError_t arena_malloc(void **out, size_t bytes) { return arena().alloc(out, bytes); }
+template <typename T>
+inline void arena_free(T *p) { arena().release((void *)p); }
+
+// BC_B200_TRACE=1: host wall clock per stage on stderr (the device is drained at
+// every mark, so traced runs are for attribution only, never for a bench number).
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    Trace() : on(getenv("BC_B200_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+    void mark(const char *what) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[bc_b200] %-28s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
+// Device-side CSR plus the work items of the level kernels.
+struct Csr {
+    int64_t n = 0, n_arcs = 0;
+    int64_t *off = nullptr;
+    int32_t *col = nullptr;
+    int32_t *wgt = nullptr;   // arc weights (nullptr: unit weights)
+    int n_chk = 0, n_rng = 0, n_hub = 0;
+    int64_t heavy_slices = 0;   // kHeavySlice-arc slices over all vertices above kHeavyDeg arcs
+    int64_t max_deg = 0;        // largest degree (build_items)
+    int32_t *chk_v = nullptr;
+    int64_t *chk_a0 = nullptr, *chk_a1 = nullptr;
+    int32_t *rng_v0 = nullptr, *rng_nv = nullptr;
+    int32_t *hub_v = nullptr, *hub_c0 = nullptr, *hub_nc = nullptr;
+};
+
+// Events of one batch; destroyed with the vector that holds them, on every exit path.
+struct Events {
+    cudaEvent_t start = nullptr, fwd_end = nullptr, border_end = nullptr, fwd2_end = nullptr, bwd_end = nullptr;
+    Events() = default;
+    Events(const Events &) = delete;
+    Events &operator=(const Events &) = delete;
+    ~Events() {
+        for (cudaEvent_t e : {start, fwd_end, border_end, fwd2_end, bwd_end})
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+// Arena block released when the scope ends (error exits included).
+template <typename T>
+struct ScopedBlock {
+    T *p = nullptr;
+    ScopedBlock() = default;
+    ScopedBlock(const ScopedBlock &) = delete;
+    ScopedBlock &operator=(const ScopedBlock &) = delete;
+    ~ScopedBlock() { arena_free(p); }
+};
+
+constexpr unsigned long long kQueueMaxDegree = 8192;
+constexpr unsigned long long kThinDegree = 8;  // average degree up to which a level runs thread-per-entry
+constexpr int kDeepLevels = 1024;              // levels one persistent launch may produce
+
+// Border-table feasibility: b_p^2 entries of 12 B per part.
+constexpr double kMaxTableBytes = 64e9;
+
+}  // namespace
+
+struct bc_handle {
+    int device = 0;
+    int64_t n = 0, n_arcs = 0;
+    std::vector<int64_t> h_off;   // host copy of the offsets (item building, partition set-up)
+    std::vector<int32_t> h_col;   // host copy of col_idx, fetched from the device when a partition is set
+    Csr full;
+    std::vector<int32_t> h_wgt;   // host copy of the arc weights (empty: unit weights)
+    int wmax = 1;                 // largest arc weight
+    int cur_depth = 0;        // levels of the batch being swept backward (weighted kernels)
+    // options
+    int groups = 4;
+    int item_arcs = 1024;
+    int reports = 1;
+    int sparse = 1;        // allow queue levels + top-down push (direction-optimising switch)
+    int reorder = 1;       // group sources by the size of their 2-hop neighbourhood
+    int row_cache = -1;    // sigma / coef row gathers: 1 = allocate in L1, 0 = bypass L1, -1 = by degree skew
+    uint32_t row_bypass_mask = 0;  // dev: bit L = forward level L bypasses L1, bit 16 + L = backward level L
+    int push_beta_late = 24;   // same, once a pull level has run: a late pull scans unvisited vertices only
+    int push_beta = 4;     // push when frontier arcs * beta <= arcs of the graph
+    int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
+    int deep_blocks_per_sm = 0;   // 0 = what the occupancy calculator allows
+    int deep_grid_f = 0, deep_grid_b = 0;
+    unsigned long long *deep_log = nullptr;
+    int *deep_info = nullptr;
+    // ---- partition ------------------------------------------------------
+    int k = 1;
+    std::vector<int32_t> h_part;
+    int32_t *d_part = nullptr;
+    Csr intra;                     // cut arcs removed
+    std::vector<int64_t> h_ioff;   // host copy of its offsets (queue sweeps inside the parts)
+    int64_t intra_maxdeg = 0;      // largest degree inside a part
+    int32_t *d_border_index = nullptr;   // [n] border number of a vertex, -1 for inner vertices
+    int hybir_queues = 1;          // partitioned sweeps of low-degree graphs on frontier queues
+    // Step-6 seeds sorted by level (queue sweeps)
+    int32_t *seed_keys = nullptr, *seed_keys2 = nullptr, *seed_vals = nullptr, *seed_vals2 = nullptr;
+    int64_t *seed_off = nullptr;
+    int64_t seed_off_cap = 0;
+    void *seed_tmp = nullptr;
+    size_t seed_tmp_bytes = 0;
+    int B = 0;                     // borders over all parts
+    int64_t n_cut = 0;
+    std::vector<int32_t> h_border_v, h_border_p, h_part_off;
+    std::vector<int64_t> h_tab_off;
+    int64_t tab_total = 0;
+    int32_t *d_border_v = nullptr, *d_border_p = nullptr, *d_part_off = nullptr, *d_cin_src = nullptr;
+    int32_t *d_cin_w = nullptr;   // weight of each incoming cut arc
+    int64_t *d_tab_off = nullptr, *d_cin_off = nullptr;
+    int32_t *bm = nullptr;         // border distance tables
+    double *sm = nullptr;          // border path-count tables
+    bool tables_ready = false;
+    // per-batch border state, [B][S]
+    int border_S = 0;
+    int32_t *D = nullptr, *D2 = nullptr, *seedD = nullptr, *Dfin = nullptr;
+    double *seedS = nullptr, *sig = nullptr, *arr = nullptr, *darr = nullptr;
+    int32_t *lane_part = nullptr, *lane_iters = nullptr;
+    // look-ahead (engine.py:135-143): Step 1 of the next batch runs on a second stream while the
+    // border phase of the current one is in flight and leaves its border seeds here
+    int lookahead = 0;
+    int32_t *seedD_alt = nullptr, *lane_part_alt = nullptr;
+    double *seedS_alt = nullptr;
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t side_go = nullptr, side_done = nullptr;
+    std::vector<bool> table_set;   // parts whose border table was installed by bc_set_border_tables
+    uint32_t *lane_active = nullptr, *lane_entered = nullptr, *lane_changed = nullptr;
+    uint32_t *dflags = nullptr;    // [0] any lane active, [1] sigma changed
+    int *d_maxlvl = nullptr;
+    uint32_t *sync_flag = nullptr, *sync_bits = nullptr;
+    int64_t *lane_sync = nullptr, *lane_bytes = nullptr;
+    size_t sync_bits_words = 0;
+    const uint32_t **d_lvl_ptrs = nullptr;
+    int lvl_ptrs_cap = 0;
+    uint32_t *presence = nullptr;
+    size_t presence_words = 0;
+    std::vector<int64_t> reports_host;  // 8 per source of the last run
+    // ---- per-batch BFS state ------------------------------------------------
+    int alloc_groups = 0;
+    uint32_t *vis = nullptr;
+    std::vector<uint32_t *> lvl;
+    double *sigma = nullptr, *coef = nullptr, *delta = nullptr;
+    uint8_t *cand = nullptr;    // [alloc_groups][n] candidate flags of the dense forward sweeps (deep graphs)
+    bool use_cand = false;      // set by forward_sweep for the launches of its levels
+    bool sigma_clean = false;   // sigma is all zero (kept so by the backward sweeps of adaptive batches)
+    bool lazy_clear = false;    // this batch's backward sweep clears sigma behind itself
+    int last_depth = 0;         // levels of the previous batch (deep graphs: memset instead)
+    double *bcg = nullptr;
+    bool bcg_dirty = true;      // partial sums of an unfinished (failed) run are in there: clear first
+    double *pacc = nullptr;
+    uint32_t *pmask = nullptr;
+    int pacc_chunks = 0;
+    uint32_t *live = nullptr;  // [level][alloc_groups] lanes with a non-empty frontier
+    int live_cap = 0;          // levels
+    // sparse levels: per-group frontier queues + two all-zero scratch mask arrays
+    int32_t *q_v = nullptr;
+    uint32_t *q_m = nullptr;
+    int64_t q_cap = 0;
+    unsigned long long *q_count = nullptr;
+    int64_t *d_qbeg = nullptr, *d_qend = nullptr, *d_qlbeg = nullptr;
+    uint32_t *scrA = nullptr, *scrB = nullptr;
+    unsigned long long *lstat = nullptr;
+    HeavyRec *heavy = nullptr;      // slices of the heavy entries of the current frontier level
+    int64_t heavy_cap = 0;
+    unsigned long long *report = nullptr;   // per-level report read by the host (forward_adaptive)
+    int64_t *range_table = nullptr;        // queue ranges of every level (backward_adaptive)
+    int64_t range_table_cap = 0;
+    unsigned long long *counters = nullptr;
+    int cnt_off = 0;  // 0: traversal counters of the result; 4: scratch (Step 1 of hybir mode)
+    int64_t *d_src = nullptr;
+    int64_t d_src_cap = 0;
+    double *bc_scratch = nullptr;  // device bc vector of bc_run
+    // ---- graph-partitioned multi-GPU mode (one rank = one part)
+    int dist_rank = -1, dist_world = 0, dist_ng = 0, dist_cnt = 0;
+    bool dist_hybir = false;      // border-matrix forward phase across ranks (bc_dist_hybir_*)
+    int dist_depth = 0;           // levels of the batch in flight (local, then global)
+    std::vector<int64_t> dist_border_off;
+    int32_t *dist_border_v = nullptr;   // all ranks' borders, rank-major
+    int32_t *dist_counts = nullptr, *dist_offsets = nullptr;
+    void *dist_scan_tmp = nullptr;
+    size_t dist_scan_bytes = 0;
+    int64_t dist_entries_cap = 0;
+    // backward exchange plan of the batch in flight (bc_dist_plan_backward)
+    int64_t *dist_cut_off = nullptr;    // [own borders + 1] cut arcs of this rank's borders
+    int32_t *dist_cut_dst = nullptr;    // their far ends (local vertex ids of the halo)
+    int32_t *plan_idx = nullptr, *plan_voff = nullptr, *plan_eoff = nullptr, *plan_cnt_e = nullptr, *plan_cnt_v = nullptr;
+    uint32_t *plan_mask = nullptr;
+    int64_t plan_cap = 0;
+    int plan_levels_cap = 0, plan_depth = 0;
+    std::vector<int32_t> plan_eoff_h, plan_cnt_e_h, plan_cnt_v_h;
+    std::string err;
+    std::atomic<int64_t> launches{0};   // (the look-ahead thread launches too)
+    int64_t level_launches = 0;   // dense level kernel only
+    // batched byte model of the dense level-kernel launches of the current call
+    int64_t model_scan = 0, model_pairs = 0, model_vlanes = 0, model_dense_words = 0, model_entries = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> level_events;   // around those launches (<= 512 per call)
+
+    int fail(int code, const std::string &msg) {
+        err = msg;
+        return code;
+    }
+};
+
+#define CUDA_TRY(h, call)                                                                  \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            char buf_[512];                                                                \
+            snprintf(buf_, sizeof buf_, "%s failed: %s (%s:%d)", #call,                    \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+            return (h)->fail(BC_ERR_INTERNAL, buf_);                                       \
+        }                                                                                  \
+    } while (0)
+
+#define TRY(expr)                 \
+    do {                          \
+        int rc_ = (expr);         \
+        if (rc_) return rc_;      \
+    } while (0)
+
+namespace {
+
+template <typename T>
+int upload(bc_handle *h, T **dst, const std::vector<T> &src) {
+    arena_free(*dst);
+    *dst = nullptr;
+    if (src.empty()) return BC_OK;
+    CUDA_TRY(h, arena_malloc((void **)dst, src.size() * sizeof(T)));
+    CUDA_TRY(h, cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return BC_OK;
+}
+
+template <typename T>
+int dev_alloc(bc_handle *h, T **dst, size_t count) {
+    arena_free(*dst);
+    *dst = nullptr;
+    CUDA_TRY(h, arena_malloc((void **)dst, std::max<size_t>(count, 1) * sizeof(T)));
+    return BC_OK;
+}
+
+void free_items(Csr &c) {
+    arena_free(c.chk_v), arena_free(c.chk_a0), arena_free(c.chk_a1);
+    arena_free(c.rng_v0), arena_free(c.rng_nv);
+    arena_free(c.hub_v), arena_free(c.hub_c0), arena_free(c.hub_nc);
+    c.chk_v = c.rng_v0 = c.rng_nv = c.hub_v = c.hub_c0 = c.hub_nc = nullptr;
+    c.chk_a0 = c.chk_a1 = nullptr;
+    c.n_chk = c.n_rng = c.n_hub = 0;
+}
+
+void free_csr(Csr &c) {
+    arena_free(c.off);
+    arena_free(c.col);
+    arena_free(c.wgt);
+    free_items(c);
+    c = Csr();
+}
+
+// Cut the vertex set into warp work items: runs of <= 32 consecutive vertices
+// holding <= item_arcs arcs, and, for vertices above 2 * item_arcs arcs
+// ("hubs"), slices of item_arcs arcs whose partial sums a second kernel adds
+// in order.
+int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
+    std::vector<int32_t> chk_v, rng_v0, rng_nv, hub_v, hub_c0, hub_nc;
+    std::vector<int64_t> chk_a0, chk_a1;
+    const int64_t hub_deg = 2 * (int64_t)item_arcs;
+    int64_t run_v0 = -1, run_arcs = 0;
+    int run_nv = 0;
+    auto flush = [&]() {
+        if (run_nv > 0) {
+            rng_v0.push_back((int32_t)run_v0);
+            rng_nv.push_back(run_nv);
+        }
+        run_v0 = -1;
+        run_nv = 0;
+        run_arcs = 0;
+    };
+    int64_t heavy_slices = 0, max_deg = 0;
+    for (int64_t v = 0; v < c.n; ++v) {
+        const int64_t deg = off[v + 1] - off[v];
+        max_deg = std::max(max_deg, deg);
+        if (deg > kHeavyDeg) heavy_slices += (deg + kHeavySlice - 1) / kHeavySlice;
+        if (deg > hub_deg) {
+            flush();
+            hub_v.push_back((int32_t)v);
+            hub_c0.push_back((int32_t)chk_v.size());
+            int nc = 0;
+            for (int64_t a = off[v]; a < off[v + 1]; a += item_arcs) {
+                chk_v.push_back((int32_t)v);
+                chk_a0.push_back(a);
+                chk_a1.push_back(std::min<int64_t>(a + item_arcs, off[v + 1]));
+                ++nc;
+            }
+            hub_nc.push_back(nc);
+            continue;
+        }
+        if (run_nv == 32 || (run_nv > 0 && run_arcs + deg > item_arcs)) flush();
+        if (run_nv == 0) run_v0 = v;
+        ++run_nv;
+        run_arcs += deg;
+    }
+    flush();
+    free_items(c);
+    c.n_chk = (int)chk_v.size();
+    c.n_rng = (int)rng_v0.size();
+    c.n_hub = (int)hub_v.size();
+    c.heavy_slices = heavy_slices;
+    c.max_deg = max_deg;
+    TRY(upload(h, &c.chk_v, chk_v));
+    TRY(upload(h, &c.chk_a0, chk_a0));
+    TRY(upload(h, &c.chk_a1, chk_a1));
+    TRY(upload(h, &c.rng_v0, rng_v0));
+    TRY(upload(h, &c.rng_nv, rng_nv));
+    TRY(upload(h, &c.hub_v, hub_v));
+    TRY(upload(h, &c.hub_c0, hub_c0));
+    TRY(upload(h, &c.hub_nc, hub_nc));
+    return BC_OK;
+}
+
+void free_state(bc_handle *h) {
+    arena_free(h->vis);
+    for (uint32_t *p : h->lvl) arena_free(p);
+    h->lvl.clear();
+    arena_free(h->sigma), arena_free(h->coef), arena_free(h->delta), arena_free(h->bcg);
+    arena_free(h->pacc), arena_free(h->pmask);
+    arena_free(h->live);
+    h->live = nullptr;
+    h->live_cap = 0;
+    arena_free(h->q_v), arena_free(h->q_m), arena_free(h->q_count);
+    arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
+    arena_free(h->scrA), arena_free(h->scrB), arena_free(h->lstat), arena_free(h->report);
+    arena_free(h->range_table);
+    arena_free(h->deep_log), arena_free(h->deep_info);
+    arena_free(h->heavy);
+    arena_free(h->cand);
+    h->cand = nullptr;
+    h->heavy = nullptr;
+    h->heavy_cap = 0;
+    h->deep_log = nullptr;
+    h->deep_info = nullptr;
+    h->report = nullptr;
+    h->range_table = nullptr;
+    h->range_table_cap = 0;
+    h->q_v = nullptr;
+    h->q_m = h->scrA = h->scrB = nullptr;
+    h->q_count = h->lstat = nullptr;
+    h->d_qbeg = h->d_qend = h->d_qlbeg = nullptr;
+    h->q_cap = 0;
+    h->vis = nullptr;
+    h->sigma = h->coef = h->delta = h->bcg = h->pacc = nullptr;
+    h->pmask = nullptr;
+    h->alloc_groups = 0;
+    h->pacc_chunks = 0;
+}
+
+void free_border_state(bc_handle *h) {
+    arena_free(h->D), arena_free(h->D2), arena_free(h->seedD), arena_free(h->Dfin);
+    arena_free(h->seedS), arena_free(h->sig), arena_free(h->arr), arena_free(h->darr);
+    arena_free(h->seedD_alt), arena_free(h->seedS_alt), arena_free(h->lane_part_alt);
+    h->seedD_alt = h->lane_part_alt = nullptr;
+    h->seedS_alt = nullptr;
+    h->darr = nullptr;
+    arena_free(h->seed_keys), arena_free(h->seed_keys2), arena_free(h->seed_vals), arena_free(h->seed_vals2);
+    arena_free(h->seed_off), arena_free(h->seed_tmp);
+    h->seed_keys = h->seed_keys2 = h->seed_vals = h->seed_vals2 = nullptr;
+    h->seed_off = nullptr, h->seed_tmp = nullptr;
+    h->seed_off_cap = 0, h->seed_tmp_bytes = 0;
+    arena_free(h->lane_part), arena_free(h->lane_iters), arena_free(h->lane_active);
+    arena_free(h->lane_entered), arena_free(h->lane_changed);
+    arena_free(h->sync_flag), arena_free(h->sync_bits), arena_free(h->lane_sync), arena_free(h->lane_bytes);
+    h->D = h->D2 = h->seedD = h->Dfin = h->lane_part = h->lane_iters = nullptr;
+    h->seedS = h->sig = h->arr = nullptr;
+    h->lane_active = h->lane_entered = h->lane_changed = h->sync_flag = h->sync_bits = nullptr;
+    h->lane_sync = h->lane_bytes = nullptr;
+    h->border_S = 0;
+    h->sync_bits_words = 0;
+}
+
+void free_partition(bc_handle *h) {
+    free_csr(h->intra);
+    free_border_state(h);
+    arena_free(h->d_part), arena_free(h->d_border_v), arena_free(h->d_border_p), arena_free(h->d_part_off);
+    arena_free(h->d_cin_src), arena_free(h->d_tab_off), arena_free(h->d_cin_off), arena_free(h->d_cin_w);
+    h->d_cin_w = nullptr;
+    arena_free(h->bm), arena_free(h->sm);
+    arena_free(h->d_border_index);
+    h->d_border_index = nullptr;
+    h->h_ioff.clear();
+    h->intra_maxdeg = 0;
+    h->d_part = h->d_border_v = h->d_border_p = h->d_part_off = h->d_cin_src = nullptr;
+    h->d_tab_off = h->d_cin_off = nullptr;
+    h->bm = nullptr;
+    h->sm = nullptr;
+    h->tables_ready = false;
+    h->table_set.clear();
+    h->k = 1;
+    h->B = 0;
+    h->n_cut = 0;
+}
+
+int ensure_state(bc_handle *h, int groups, bool want_delta) {
+    const size_t n = (size_t)h->n;
+    const int n_chk = std::max(h->full.n_chk, h->intra.n_chk);
+    if (h->alloc_groups < groups) {
+        free_state(h);
+        CUDA_TRY(h, arena_malloc((void **)&h->vis, groups * n * sizeof(uint32_t)));
+        CUDA_TRY(h, arena_malloc((void **)&h->sigma, groups * n * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->coef, groups * n * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->bcg, groups * n * sizeof(double)));
+        h->bcg_dirty = true;   // cleared on the caller's stream by the run that uses it
+        h->alloc_groups = groups;
+        h->sigma_clean = false;
+    }
+    if (want_delta && h->delta == nullptr)
+        CUDA_TRY(h, arena_malloc((void **)&h->delta, (size_t)h->alloc_groups * n * 32 * sizeof(double)));
+    if (h->pacc_chunks < n_chk || (n_chk > 0 && h->pacc == nullptr)) {
+        arena_free(h->pacc), arena_free(h->pmask);
+        h->pacc = nullptr, h->pmask = nullptr;
+        const size_t slots = (size_t)h->alloc_groups * n_chk;
+        CUDA_TRY(h, arena_malloc((void **)&h->pacc, slots * 32 * sizeof(double)));
+        CUDA_TRY(h, arena_malloc((void **)&h->pmask, slots * sizeof(uint32_t)));
+        h->pacc_chunks = n_chk;
+    }
+    if (h->counters == nullptr)
+        CUDA_TRY(h, arena_malloc((void **)&h->counters, 8 * sizeof(unsigned long long)));
+    if (h->dflags == nullptr) CUDA_TRY(h, arena_malloc((void **)&h->dflags, 4 * sizeof(uint32_t)));
+    if (h->d_maxlvl == nullptr) CUDA_TRY(h, arena_malloc((void **)&h->d_maxlvl, sizeof(int)));
+    return BC_OK;
+}
+
+int ensure_pool(bc_handle *h, int count) {
+    const size_t bytes = (size_t)h->alloc_groups * (size_t)h->n * sizeof(uint32_t);
+    while ((int)h->lvl.size() < count) {
+        uint32_t *p = nullptr;
+        CUDA_TRY(h, arena_malloc((void **)&p, bytes));
+        h->lvl.push_back(p);
+    }
+    return BC_OK;
+}
+
+int ensure_live(bc_handle *h, int count) {
+    if (h->live_cap < count + 1) {
+        const int cap = std::max(count + 1, 2 * h->live_cap);
+        const size_t G = (size_t)h->alloc_groups;
+        uint32_t *p = nullptr;
+        CUDA_TRY(h, arena_malloc((void **)&p, cap * G * sizeof(uint32_t)));
+        CUDA_TRY(h, cudaMemset(p, 0, cap * G * sizeof(uint32_t)));
+        if (h->live) {
+            CUDA_TRY(h, cudaMemcpy(p, h->live, h->live_cap * G * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToDevice));
+            arena_free(h->live);
+        }
+        h->live = p;
+        h->live_cap = cap;
+    }
+    return BC_OK;
+}
+
+int ensure_levels(bc_handle *h, int count) {
+    TRY(ensure_pool(h, count));
+    return ensure_live(h, count);
+}
+
+int ensure_queues(bc_handle *h) {
+    if (h->q_v != nullptr) return BC_OK;
+    const size_t G = (size_t)h->alloc_groups, n = (size_t)h->n;
+    h->q_cap = (int64_t)(4 * n + 1024);
+    TRY(dev_alloc(h, &h->q_v, G * (size_t)h->q_cap));
+    TRY(dev_alloc(h, &h->q_m, G * (size_t)h->q_cap));
+    TRY(dev_alloc(h, &h->q_count, G));
+    CUDA_TRY(h, cudaMemset(h->q_count, 0, G * sizeof(unsigned long long)));
+    TRY(dev_alloc(h, &h->d_qbeg, G));
+    TRY(dev_alloc(h, &h->d_qend, G));
+    TRY(dev_alloc(h, &h->d_qlbeg, G));
+    CUDA_TRY(h, cudaMemset(h->d_qbeg, 0, G * sizeof(int64_t)));
+    CUDA_TRY(h, cudaMemset(h->d_qend, 0, G * sizeof(int64_t)));
+    CUDA_TRY(h, cudaMemset(h->d_qlbeg, 0, G * sizeof(int64_t)));
+    TRY(dev_alloc(h, &h->scrA, G * n));
+    TRY(dev_alloc(h, &h->scrB, G * n));
+    TRY(dev_alloc(h, &h->lstat, (size_t)8));
+    TRY(dev_alloc(h, &h->report, 8 + 2 * G));
+    h->heavy_cap = (int64_t)G * std::max(h->full.heavy_slices, h->intra.heavy_slices) + 1;
+    TRY(dev_alloc(h, &h->heavy, (size_t)h->heavy_cap));
+    CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
+    CUDA_TRY(h, cudaMemset(h->scrB, 0, G * n * sizeof(uint32_t)));
+    return BC_OK;
+}
+
+// Buffers and grid size of the persistent sweeps (bc_deep.cuh).  The grid must be
+// fully resident for the grid-wide barrier, so it comes from the occupancy
+// calculator (the backward kernel is the heavier of the two).
+int ensure_deep(bc_handle *h) {
+    if (h->deep_log != nullptr) return BC_OK;
+    const size_t G = (size_t)h->alloc_groups;
+    TRY(dev_alloc(h, &h->deep_log, (size_t)kDeepLevels * (3 + 2 * G)));
+    TRY(dev_alloc(h, &h->deep_info, (size_t)4));
+    int per_sm_f = 0, per_sm_b = 0, per_sm_d = 0, sms = 0;
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, deep_forward_kernel, kDeepThreads, 0));
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, deep_backward_kernel<false>,
+                                                              kDeepThreads, 0));
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, deep_backward_kernel<true>,
+                                                              kDeepThreads, 0));
+    CUDA_TRY(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    per_sm_b = std::min(per_sm_b, per_sm_d);
+    if (h->deep_blocks_per_sm > 0) {
+        per_sm_f = std::min(per_sm_f, h->deep_blocks_per_sm);
+        per_sm_b = std::min(per_sm_b, h->deep_blocks_per_sm);
+    }
+    if (per_sm_f < 1 || per_sm_b < 1 || sms < 1)
+        return h->fail(BC_ERR_INTERNAL, "persistent sweep kernels do not fit on an SM");
+    h->deep_grid_f = per_sm_f * sms;
+    h->deep_grid_b = per_sm_b * sms;
+    return BC_OK;
+}
+
+// Queue entries are (vertex, level) pairs: a vertex can sit in up to 32 levels of
+// a group (one per lane), so deep graphs outgrow the initial 4n entries.  Grow
+// by doubling up to 33n.
+int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
+                const std::vector<unsigned long long> &used) {
+    const int64_t max_cap = 33 * h->n + 1024 + h->B;
+    if (h->q_cap >= max_cap || need_cap <= h->q_cap) return BC_OK;
+    const int64_t cap = std::min(max_cap, std::max(need_cap, 2 * h->q_cap));
+    const size_t G = (size_t)h->alloc_groups;
+    int32_t *nv = nullptr;
+    uint32_t *nm = nullptr;
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    CUDA_TRY(h, arena_malloc((void **)&nv, G * (size_t)cap * sizeof(int32_t)));
+    CUDA_TRY(h, arena_malloc((void **)&nm, G * (size_t)cap * sizeof(uint32_t)));
+    for (size_t g = 0; g < G; ++g) {
+        const size_t keep = (size_t)std::min<int64_t>(g < used.size() ? (int64_t)used[g] : 0, h->q_cap);   // entries in use
+        if (keep == 0) continue;
+        CUDA_TRY(h, cudaMemcpy(nv + g * cap, h->q_v + g * h->q_cap, keep * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice));
+        CUDA_TRY(h, cudaMemcpy(nm + g * cap, h->q_m + g * h->q_cap, keep * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice));
+    }
+    arena_free(h->q_v), arena_free(h->q_m);
+    h->q_v = nv;
+    h->q_m = nm;
+    h->q_cap = cap;
+    return BC_OK;
+}
+
+// Device table of the level-mask pointers (the border gathers walk levels).
+int upload_level_ptrs(bc_handle *h, int depth, cudaStream_t st) {
+    if (h->lvl_ptrs_cap < depth) {
+        arena_free((void *)h->d_lvl_ptrs);
+        h->d_lvl_ptrs = nullptr;
+        const int cap = std::max(depth, 2 * h->lvl_ptrs_cap);
+        CUDA_TRY(h, arena_malloc((void **)&h->d_lvl_ptrs, cap * sizeof(uint32_t *)));
+        h->lvl_ptrs_cap = cap;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync((void *)h->d_lvl_ptrs, h->lvl.data(), depth * sizeof(uint32_t *),
+                                cudaMemcpyHostToDevice, st));
+    return BC_OK;
+}
+
+LevelParams level_params(bc_handle *h, const Csr &c) {
+    LevelParams p{};
+    p.off = c.off;
+    p.col = c.col;
+    p.chk_v = c.chk_v;
+    p.chk_a0 = c.chk_a0;
+    p.chk_a1 = c.chk_a1;
+    p.n_chk = c.n_chk;
+    p.rng_v0 = c.rng_v0;
+    p.rng_nv = c.rng_nv;
+    p.n_rng = c.n_rng;
+    p.n = c.n;
+    p.vis = h->vis;
+    p.sigma = h->sigma;
+    p.coef = h->coef;
+    p.delta = h->delta;
+    p.bcg = h->bcg;
+    p.pacc = h->pacc;
+    p.pmask = h->pmask;
+    p.counters = h->counters + h->cnt_off;
+    p.wgt = c.wgt;
+    p.cand = nullptr;
+    p.lvl_ptrs = h->d_lvl_ptrs;
+    p.live_base = h->live;
+    p.wmax = c.wgt ? h->wmax : 1;
+    p.G = h->alloc_groups;
+    return p;
+}
+
+HubParams hub_params(bc_handle *h, const Csr &c) {
+    HubParams p{};
+    p.off = c.off;
+    p.hub_v = c.hub_v;
+    p.hub_c0 = c.hub_c0;
+    p.hub_nc = c.hub_nc;
+    p.n_hub = c.n_hub;
+    p.n_chk = c.n_chk;
+    p.n = c.n;
+    p.vis = h->vis;
+    p.sigma = h->sigma;
+    p.coef = h->coef;
+    p.delta = h->delta;
+    p.bcg = h->bcg;
+    p.pacc = h->pacc;
+    p.pmask = h->pmask;
+    p.counters = h->counters + h->cnt_off;
+    p.live_base = h->live;
+    p.wmax = c.wgt ? h->wmax : 1;
+    p.G = h->alloc_groups;
+    return p;
+}
+
+BorderGeom border_geom(bc_handle *h) {
+    BorderGeom g{};
+    g.k = h->k;
+    g.B = h->B;
+    g.border_v = h->d_border_v;
+    g.border_p = h->d_border_p;
+    g.part_off = h->d_part_off;
+    g.tab_off = h->d_tab_off;
+    g.cin_off = h->d_cin_off;
+    g.cin_src = h->d_cin_src;
+    g.cin_w = h->d_cin_w;
+    return g;
+}
+
+inline unsigned blocks_for(int64_t items) {
+    return (unsigned)((items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+}
+
+inline unsigned grid1d(size_t count, int block = 256, size_t cap = 1u << 30) {
+    return (unsigned)std::max<size_t>(1, std::min<size_t>((count + block - 1) / block, cap));
+}
+
+#ifdef BC_PROFILE
+void prof_dump(const char *what, int L, cudaStream_t st) {
+    unsigned long long v[16];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(v, g_prof, sizeof v);
+    fprintf(stderr, "[prof] %s L=%d slices=%llu any=%llu hit_arcs=%llu want_lanes=%llu pairs=%llu hit_lanes=%llu\n",
+            what, L, v[0], v[1], v[2], v[3], v[4], v[5]);
+    memset(v, 0, sizeof v);
+    cudaMemcpyToSymbol(g_prof, v, sizeof v);
+}
+#else
+inline void prof_dump(const char *, int, cudaStream_t) {}
+#endif
+
+void drop_level_events(bc_handle *h) {
+    for (auto &pr : h->level_events) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    h->level_events.clear();
+}
+
+// CUDA events around one dense level launch (level kernel + hub pass): bc_stats.ms_level.
+struct LevelTimer {
+    bc_handle *h;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    LevelTimer(bc_handle *h_, cudaStream_t st_) : h(h_), st(st_) {
+        if (h->level_events.size() >= 512) return;
+        if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+            a = b = nullptr;
+            return;
+        }
+        cudaEventRecord(a, st);
+    }
+    void stop() {
+        if (a == nullptr) return;
+        cudaEventRecord(b, st);
+        h->level_events.emplace_back(a, b);
+        a = b = nullptr;
+    }
+    ~LevelTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+
+}  // namespace

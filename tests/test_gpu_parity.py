@@ -12,7 +12,7 @@ import pytest
 import oracle as O
 import paper_2008_05718_b200 as P
 from paper_2008_05718_b200 import generators as G
-from paper_2008_05718_b200._capi import Engine, MODE_DIRECT
+from paper_2008_05718_b200._capi import Engine, MODE_BSP, MODE_DIRECT, MODE_HYBIR
 
 pytestmark = pytest.mark.gpu
 
@@ -275,6 +275,90 @@ def test_config2_rmat20_sample():
     deg = np.diff(g.offsets)
     assert not bc[deg == 0].any() and bc.min() >= 0.0
     assert st["sources"] == 1024 and st["max_levels"] >= 5
+
+
+def test_path_counts_beyond_2_53_against_the_bigint_reference():
+    """sigma above 2^53 (SURVEY.md hard part 1) pinned to the reference's exact-integer oracle
+    (golden vectors of tests/golden/gen_golden_bigsigma.py, 40 x 32 lattice, max sigma 2^66):
+    distances exact, GPU path counts within 1e-12 relative, delta / BC within 1e-9."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bigsigma_vectors.npz"))
+    g = G.grid(int(z["rows"]), int(z["cols"]))
+    srcs = z["sources"].tolist()
+    assert z["sigma_max_log2"].max() > 53
+    with Engine(g) as e:
+        dist, sigma, delta = e.debug_sources(srcs)
+        bc, _ = e.run(srcs)
+        e.set_option("sparse", 0)                      # dense pull levels only
+        dist2, sigma2, delta2 = e.debug_sources(srcs)
+    for d_, s_, dl_ in ((dist, sigma, delta), (dist2, sigma2, delta2)):
+        assert np.array_equal(d_, z["dist"])
+        assert np.allclose(s_, z["sigma"], rtol=1e-12, atol=0)
+        assert np.allclose(dl_, z["delta"], rtol=RTOL, atol=ATOL)
+    assert np.allclose(bc, z["bc"], rtol=RTOL, atol=ATOL)
+    # the partitioned modes on the same graph (border tables hold path counts above 2^53 too)
+    part = P.strip_partition(int(z["rows"]), int(z["cols"]), 2)
+    for mode in (MODE_HYBIR, MODE_BSP):
+        with Engine(g) as e:
+            e.set_partition(2, part.assignment)
+            e.set_option("reports", 0)
+            bcp, _ = e.run(srcs, mode)
+        assert np.allclose(bcp, z["bc"], rtol=RTOL, atol=ATOL), mode
+
+
+@pytest.mark.slow
+def test_config3_road2048_sample():
+    """BASELINE config 3's graph at full size (road-like 2048 x 2048, ~4,100 levels, path counts far
+    above 2^53) at a reduced source count: oracle port on a 4-source sample, direct == hybir in 8
+    strips, and the distance-histogram identity on the inspected sources."""
+    g = G.road_like(2048, 2048, keep=0.2, seed=1)
+    assert g.num_vertices == 1 << 22
+    srcs = pick = sorted(__import__("random").Random(0).sample(range(g.num_vertices), 64))
+    with Engine(g) as e:
+        e.set_option("groups", 2)
+        bc, st = e.run(srcs)
+        bc4, _ = e.run(pick[:4])
+        dist, sigma, delta = e.debug_sources(pick[:2])
+    obc, info = O.brandes_bc(g, pick[:4])
+    assert info["sigma_max"] > 2.0 ** 53
+    assert np.allclose(bc4, obc, rtol=RTOL, atol=ATOL)
+    for i in range(2):
+        od, osg, odl, _ = O.brandes_single_source(g, pick[i])
+        assert np.array_equal(dist[i], od)
+        assert np.allclose(sigma[i], osg, rtol=1e-12, atol=0)
+        assert np.allclose(delta[i], odl, rtol=RTOL, atol=ATOL)
+        d = dist[i][dist[i] > 0]
+        assert delta[i].sum() - delta[i][pick[i]] == pytest.approx(float((d - 1).sum()), rel=1e-9)
+    assert st["max_levels"] > 3000
+    part = P.strip_partition(2048, 2048, 8)
+    with Engine(g) as e:
+        e.set_option("groups", 2)
+        e.set_option("reports", 0)
+        e.set_partition(8, part.assignment)
+        bch, sth = e.run(srcs, MODE_HYBIR)
+    assert np.allclose(bch, bc, rtol=RTOL, atol=ATOL)
+    assert sth["iterations"] >= len(srcs)
+
+
+@pytest.mark.slow
+def test_config4_erdos_renyi_sample():
+    """BASELINE config 4's graph at full size (Erdos-Renyi n = 2^22, average degree 32) at a reduced
+    source count: oracle on a sample, linearity over a split of the source list."""
+    g = G.erdos_renyi(1 << 22, 1 << 26, 1)
+    srcs = sorted(__import__("random").Random(0).sample(range(g.num_vertices), 128))
+    with Engine(g) as e:
+        e.set_option("groups", 4)
+        bc, st = e.run(srcs)
+        bc_a, _ = e.run(srcs[:64])
+        bc_b, _ = e.run(srcs[64:])
+        bc8, _ = e.run(srcs[:8])
+        dist, sigma, delta = e.debug_sources(srcs[:2])
+    assert np.allclose(bc_a + bc_b, bc, rtol=1e-12, atol=1e-9)
+    obc, info = O.brandes_bc(g, srcs[:8])
+    assert info["sigma_max"] < 2.0 ** 53
+    assert np.allclose(bc8, obc, rtol=RTOL, atol=ATOL)
+    assert_sources_match_oracle(g, srcs[:2], dist, sigma, delta)
+    assert 5 <= st["max_levels"] <= 12
 
 
 def test_push_pull_switch_equivalence():

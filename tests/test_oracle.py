@@ -170,3 +170,25 @@ def test_weighted_oracle_matches_reference_golden():
         bc_s, _ = O.brandes_bc(g, rec["run_bc_sources"], threads=1)
         assert np.allclose(bc_s, rec["run_bc_hybir"], rtol=1e-9, atol=1e-12)
         assert np.allclose(bc_s, rec["run_bc_bsp_baseline"], rtol=1e-9, atol=1e-12)
+
+
+def test_path_counts_beyond_2_53_match_the_bigint_reference():
+    """Above 2^53 the reference oracle keeps exact Python integers (oracle.py:56-61); the C port
+    carries fp64.  Golden vectors from the reference itself on a 40 x 32 lattice (max sigma 2^66,
+    tests/golden/gen_golden_bigsigma.py): distances exact, path counts within 1e-12 of the
+    correctly rounded integers, dependencies / BC within 1e-9."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bigsigma_vectors.npz"))
+    g = G.grid(int(z["rows"]), int(z["cols"]))
+    srcs = z["sources"].tolist()
+    assert z["sigma_max_log2"].max() > 53
+    for i, s in enumerate(srcs):
+        d, sg, dl, info = O.brandes_single_source(g, s)
+        assert np.array_equal(d, z["dist"][i])
+        assert np.allclose(sg, z["sigma"][i], rtol=1e-12, atol=0)
+        assert np.allclose(dl, z["delta"][i], rtol=1e-9, atol=1e-12)
+        # the recorded maximum really is the exact integer the reference computed
+        assert float(int(str(z["sigma_max_digits"][i]))) == z["sigma"][i].max() == info["sigma_max"] or \
+            abs(info["sigma_max"] / z["sigma"][i].max() - 1) < 1e-12
+    bc, _ = O.brandes_bc(g, srcs)
+    assert np.allclose(bc, z["bc"], rtol=1e-9, atol=1e-12)

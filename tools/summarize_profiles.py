@@ -27,7 +27,7 @@ for r in rows[hi + 1:]:
     a[1] += us
     order.append((name, r[8], us))
 total = sum(a[1] for a in agg.values())
-cmd = "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 1 --warmup 0 --no-cpu"
+cmd = "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 1 --warmup 0 --no-cpu --no-extra"
 with open(os.path.join(out, rnd + "_launches_summary.md"), "w") as fh:
     fh.write("# ncu launch list, %s (cold-cache, serialised: compare shares, not absolutes)\n\n" % rnd)
     fh.write("Command: `%s`\n(the bench workload, one step: R-MAT scale-20 EF-16, 1024 sources in batches of 16 groups; "
@@ -46,8 +46,12 @@ with open(os.path.join(out, rnd + "_launches_summary.md"), "w") as fh:
     fh.write("```\n")
 
 rep = os.path.join(src, "prof_level.ncu-rep")
-if os.path.exists(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rawcsv = os.path.join(src, "prof_level.raw.csv")      # exported on the GPU box (the .ncu-rep stays there)
+if os.path.exists(rep) or os.path.exists(rawcsv):
+    if os.path.exists(rawcsv):
+        raw = open(rawcsv).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
     hdr = rr[0]
     want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -68,7 +72,11 @@ if os.path.exists(rep):
     per = [to_bytes(r[idx[2]], units[idx[2]]) + to_bytes(r[idx[3]], units[idx[3]]) for r in lev]
     rec = {"rmat20": sum(per) / len(per) if per else None,
            "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the %d level_kernel launches "
-                   "(forward and backward) captured with ncu --set full from bench.py --steps 1 --warmup 0" % len(per),
-           "per_launch_bytes": per}
+                   "(forward and backward) of exactly one step, captured with ncu --set full from "
+                   "bench.py --steps 1 --warmup 0 --no-cpu --no-extra" % len(per),
+           "per_launch_bytes": per,
+           "per_launch_ms": [float(r[idx[1]]) * {"ms": 1.0, "us": 1e-3, "s": 1e3, "ns": 1e-6}.get(units[idx[1]], 1.0)
+                             for r in lev],
+           "kernels": [r[idx[0]].split("(")[0] for r in lev]}
     json.dump(rec, open(os.path.join(out, rnd + "_traffic.json"), "w"), indent=1)
 print(open(os.path.join(out, rnd + "_launches_summary.md")).read()[:3000])
