@@ -189,6 +189,14 @@ struct DeepFwdParams {
     unsigned long long max_degree;
     SeedPlan seeds;              // Step-6 border seeds joining at their own level (idx == nullptr: none)
     unsigned long long seed_room;   // queue entries the seeds of one level may add per group
+    // level-ordered copy of the path counts (nullptr: off).  Entry i of group g owns the slots
+    // q_off[g][i] .. + popc(q_m[i]) of qs[g][..], one per set lane in lane order: the backward
+    // sweep of a deep graph then reads sigma (and writes coef) sequentially instead of one random
+    // 8-byte access into the 256-byte row of the vertex (deep_backward_compact_kernel).
+    double *qs;
+    uint32_t *q_off;
+    unsigned long long *v_count;   // [G] value slots handed out so far
+    int64_t vcap;                  // value slots per group
 };
 
 // Forward: consecutive top-down levels, one THREAD per frontier entry.
@@ -314,8 +322,9 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
                 const int64_t i = p.q_lbeg[g] + (f0 - s_pref[g]) + lane;
                 const size_t qbase = (size_t)g * p.q.cap;
                 uint32_t any = 0;
+                int32_t w = 0;
                 if (i < end) {
-                    const int32_t w = p.q.q_v[qbase + i];
+                    w = p.q.q_v[qbase + i];
                     const uint32_t m = p.next[(size_t)g * n + w];
                     p.q.q_m[qbase + i] = m;
                     p.vis[(size_t)g * n + w] |= m;
@@ -327,6 +336,34 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
                     nv += 1;
                     fa += deg;
                     md = max(md, deg);
+                }
+                if (p.qs != nullptr) {
+                    // value slots of the warp's entries: warp prefix of popc + one atomic per warp
+                    const unsigned pc = __popc(any);
+                    unsigned incl = pc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned t = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    const unsigned total = __shfl_sync(kFull, incl, 31);
+                    unsigned long long base = 0;
+                    if (lane == 0 && total) base = atomicAdd(p.v_count + g, (unsigned long long)total);
+                    base = __shfl_sync(kFull, base, 0);
+                    if (i < end) {
+                        const unsigned long long at = base + incl - pc;
+                        p.q_off[qbase + i] = (uint32_t)at;
+                        if (at + pc <= (unsigned long long)p.vcap) {
+                            const double *row = p.sigma + ((size_t)g * n + w) * 32;
+                            double *out = p.qs + (size_t)g * p.vcap + at;
+                            uint32_t m = any;
+                            while (m) {
+                                const int bit = __ffs(m) - 1;
+                                m &= m - 1;
+                                *out++ = row[bit];   // final: every push of the level is behind the barrier
+                            }
+                        }
+                    }
                 }
                 any = __reduce_or_sync(kFull, any);
                 if (lane == 0 && any) atomicOr(&s_live[g], any);
@@ -486,6 +523,163 @@ __global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepB
         nbr = wr;
         erase = wr;
         widx ^= 1;
+    }
+}
+
+// ---- backward over level-ordered values ---------------------------------------------------
+// Deep graphs are bound by random DRAM transactions: deep_backward_kernel touches ~10 64-byte
+// lines per (vertex, lane) visit (sigma row, coef row, children's coef rows, BC partial, mask
+// scratch; ncu: 687 B of DRAM traffic per visit at 2.8 TB/s, profiles/r2_deep_kernels_ncu.md).
+// This variant keeps sigma and coef per queue ENTRY, in level order (DeepFwdParams::qs):
+//   - an entry reads its sigma and writes its coef at q_off[i] + rank: sequential traffic;
+//   - the scratch array maps a vertex to the queue entry it has at the level below (index + 1),
+//     so a parent finds a child's lanes (q_m[j]) and coef (qc[q_off[j] + rank]) inside the
+//     few-MB window of that level, which stays in L2;
+//   - BC partials are added with atomics into ONE vector per batch (bc_acc, n doubles: L2
+//     resident) instead of a read-modify-write of the 8-byte partial of (group, vertex) in a
+//     G x n array: the per-vertex sums then depend on the order the atomics land in (last-bit
+//     differences between runs), which is why only deep graphs take this path.
+struct DeepBwdCompactParams {
+    const int64_t *off;
+    const int32_t *col;
+    int64_t n;
+    QueueParams q;               // q_v / q_m / cap
+    const uint32_t *q_off;       // [G][cap] first value slot of an entry
+    const int64_t *range_table;  // [level][0: begin, 1: end][G]
+    const double *qs;            // [G][vcap] path counts in entry order
+    double *qc;                  // [G][vcap] coef in entry order
+    int64_t vcap;
+    double *bc_acc;              // [n] BC partial of the batch (atomics), or nullptr
+    double *bcg;                 // [G][n] per-group partials (used when bc_acc == nullptr)
+    int ng, G;
+    int hi, lo;                  // levels hi (the deepest level of the batch), hi - 1, ..., lo
+    uint32_t *scr0, *scr1;       // all-zero scratch arrays on entry and on exit
+};
+
+__global__ void __launch_bounds__(kDeepThreads) deep_backward_compact_kernel(const DeepBwdCompactParams p) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int64_t s_pref[kDeepMaxGroups + 1];
+    const int lane = threadIdx.x & 31;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = p.n;
+    const uint32_t *below = nullptr;   // scratch holding entry index + 1 of the level below
+    uint32_t *erase = nullptr;
+    int widx = 0;
+    for (int L = p.hi; L >= p.lo - 1; --L) {
+        // iteration L = lo - 1 only erases what level lo left in the scratch array
+        if (L >= p.lo) {
+            uint32_t *wr = widx ? p.scr1 : p.scr0;
+            const int64_t *beg_t = p.range_table + ((size_t)L * 2 + 0) * p.G;
+            const int64_t *end_t = p.range_table + ((size_t)L * 2 + 1) * p.G;
+            if (threadIdx.x <= p.ng) {
+                int64_t acc = 0;
+                for (int g = 0; g < (int)threadIdx.x; ++g) acc += (end_t[g] - beg_t[g] + 31) & ~(int64_t)31;
+                s_pref[threadIdx.x] = acc;
+            }
+            __syncthreads();
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t i = beg_t[g] + (f0 - s_pref[g]) + lane;
+                if (i >= end_t[g]) continue;
+                const size_t qbase = (size_t)g * p.q.cap;
+                const size_t vbase = (size_t)g * p.vcap;
+                const int64_t v = p.q.q_v[qbase + i];
+                const uint32_t m = p.q.q_m[qbase + i];
+                const uint32_t at = p.q_off[qbase + i];
+                wr[(size_t)g * n + v] = (uint32_t)i + 1u;
+                if (m == 0) continue;
+                const int64_t a0 = p.off[v], a1 = p.off[v + 1];
+                double total_d = 0.0;
+                // children: entry (index + 1) of every neighbour at the level below, its lanes and
+                // its first value slot -- kThinArcs arcs at a time, one round trip per stage
+                uint32_t rest = m;
+                int rank = 0;
+                if (a1 - a0 <= kThinArcs || below == nullptr) {
+                    uint32_t cj[kThinArcs], cm[kThinArcs], co[kThinArcs];
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k) {
+                        cj[k] = 0;
+                        if (below != nullptr && a0 + k < a1) cj[k] = below[(size_t)g * n + __ldg(p.col + a0 + k)];
+                    }
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k) {
+                        cm[k] = cj[k] ? p.q.q_m[qbase + cj[k] - 1] : 0u;
+                        co[k] = cj[k] ? p.q_off[qbase + cj[k] - 1] : 0u;
+                    }
+                    while (rest) {
+                        const int bit = __ffs(rest) - 1;
+                        rest &= rest - 1;
+                        const uint32_t lower = (1u << bit) - 1u;
+                        double c[kThinArcs];
+#pragma unroll
+                        for (int k = 0; k < kThinArcs; ++k)
+                            c[k] = ((cm[k] >> bit) & 1u) ? p.qc[vbase + co[k] + __popc(cm[k] & lower)] : 0.0;
+                        double acc = 0.0;
+#pragma unroll
+                        for (int k = 0; k < kThinArcs; ++k)
+                            if ((cm[k] >> bit) & 1u) acc += c[k];   // ascending arc order
+                        const double sv = p.qs[vbase + at + rank];
+                        const double d = sv * acc;
+                        p.qc[vbase + at + rank] = (1.0 + d) / sv;
+                        total_d += d;
+                        ++rank;
+                    }
+                } else {
+                    while (rest) {
+                        const int bit = __ffs(rest) - 1;
+                        rest &= rest - 1;
+                        const uint32_t lower = (1u << bit) - 1u;
+                        double acc = 0.0;
+                        for (int64_t a = a0; a < a1; ++a) {
+                            const uint32_t j = below[(size_t)g * n + __ldg(p.col + a)];
+                            if (j == 0) continue;
+                            const uint32_t mj = p.q.q_m[qbase + j - 1];
+                            if ((mj >> bit) & 1u) acc += p.qc[vbase + p.q_off[qbase + j - 1] + __popc(mj & lower)];
+                        }
+                        const double sv = p.qs[vbase + at + rank];
+                        const double d = sv * acc;
+                        p.qc[vbase + at + rank] = (1.0 + d) / sv;
+                        total_d += d;
+                        ++rank;
+                    }
+                }
+                if (p.bc_acc != nullptr) {
+                    if (total_d != 0.0) atomicAdd(p.bc_acc + v, total_d);
+                } else {
+                    p.bcg[(size_t)g * n + v] += total_d;
+                }
+            }
+            __syncthreads();   // s_pref is rewritten below
+        }
+        grid.sync();
+        if (erase != nullptr) {
+            const int64_t *eb = p.range_table + ((size_t)(L + 1) * 2 + 0) * p.G;
+            const int64_t *ee = p.range_table + ((size_t)(L + 1) * 2 + 1) * p.G;
+            if (threadIdx.x <= p.ng) {
+                int64_t acc = 0;
+                for (int g = 0; g < (int)threadIdx.x; ++g) acc += (ee[g] - eb[g] + 31) & ~(int64_t)31;
+                s_pref[threadIdx.x] = acc;
+            }
+            __syncthreads();
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t i = eb[g] + (f0 - s_pref[g]) + lane;
+                if (i < ee[g]) erase[(size_t)g * n + p.q.q_v[(size_t)g * p.q.cap + i]] = 0u;
+            }
+            __syncthreads();
+            grid.sync();
+        }
+        if (L >= p.lo) {
+            uint32_t *wr = widx ? p.scr1 : p.scr0;
+            below = wr;
+            erase = wr;
+            widx ^= 1;
+        }
     }
 }
 

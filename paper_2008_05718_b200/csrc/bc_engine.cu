@@ -193,6 +193,13 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         h->deep = value ? 1 : 0;
         return BC_OK;
     }
+    if (k == "deep_compact") {
+        // 0: row layout everywhere; 1 (default): deep graphs sweep backward over level-ordered
+        // values with one atomically-updated BC vector; 2: same, BC kept in per-group partials
+        if (value < 0 || value > 2) return h->fail(BC_ERR_INPUT, "deep_compact must be 0, 1 or 2");
+        h->deep_compact = (int)value;
+        return BC_OK;
+    }
     if (k == "hybir_queues") {
         h->hybir_queues = value ? 1 : 0;
         return BC_OK;

@@ -574,6 +574,19 @@ __global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups)
     }
 }
 
+// Deep graphs: the batch's BC partial (one vector, filled with atomics by
+// deep_backward_compact_kernel) joins the per-group partials of group 0 and is reset.
+__global__ void bc_acc_flush_kernel(double *bc_acc, double *bcg0, int64_t n) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const double x = bc_acc[v];
+        if (x != 0.0) {
+            bcg0[v] += x;
+            bc_acc[v] = 0.0;
+        }
+    }
+}
+
 // Inspection: scatter level L of every lane into per-source rows.
 __global__ void extract_level_kernel(const uint32_t *lvl, const uint32_t *live_level,
                                      const double *sigma, const double *delta, int64_t n, int level,

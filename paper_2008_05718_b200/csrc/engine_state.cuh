@@ -170,7 +170,7 @@ struct bc_handle {
     int push_beta = 4;     // push when frontier arcs * beta <= arcs of the graph
     int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
     int deep_blocks_per_sm = 0;   // 0 = what the occupancy calculator allows
-    int deep_grid_f = 0, deep_grid_b = 0;
+    int deep_grid_f = 0, deep_grid_b = 0, deep_grid_c = 0;
     unsigned long long *deep_log = nullptr;
     int *deep_info = nullptr;
     // ---- partition ------------------------------------------------------
@@ -244,6 +244,13 @@ struct bc_handle {
     int32_t *q_v = nullptr;
     uint32_t *q_m = nullptr;
     int64_t q_cap = 0;
+    // level-ordered values of the deep sweeps (bc_deep.cuh: DeepFwdParams::qs, deep_backward_compact_kernel)
+    int deep_compact = 1;          // option: backward sweeps of deep graphs run on them
+    double *qs = nullptr;          // [G][q_vcap] path counts in queue-entry order
+    uint32_t *q_off = nullptr;     // [G][q_cap] first value slot of an entry
+    unsigned long long *v_count = nullptr;   // [G]
+    int64_t q_vcap = 0;
+    double *bc_acc = nullptr;      // [n] BC partial of a batch, added with atomics
     unsigned long long *q_count = nullptr;
     int64_t *d_qbeg = nullptr, *d_qend = nullptr, *d_qlbeg = nullptr;
     uint32_t *scrA = nullptr, *scrB = nullptr;
@@ -414,6 +421,9 @@ void free_state(bc_handle *h) {
     h->live = nullptr;
     h->live_cap = 0;
     arena_free(h->q_v), arena_free(h->q_m), arena_free(h->q_count);
+    arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
+    h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
+    h->q_vcap = 0;
     arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
     arena_free(h->scrA), arena_free(h->scrB), arena_free(h->lstat), arena_free(h->report);
     arena_free(h->range_table);
@@ -589,6 +599,11 @@ int ensure_deep(bc_handle *h) {
                                                               kDeepThreads, 0));
     CUDA_TRY(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
     per_sm_b = std::min(per_sm_b, per_sm_d);
+    int per_sm_c = 0;
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_c, deep_backward_compact_kernel,
+                                                              kDeepThreads, 0));
+    if (h->deep_blocks_per_sm > 0) per_sm_c = std::min(per_sm_c, h->deep_blocks_per_sm);
+    h->deep_grid_c = std::max(per_sm_c, 0) * sms;
     if (h->deep_blocks_per_sm > 0) {
         per_sm_f = std::min(per_sm_f, h->deep_blocks_per_sm);
         per_sm_b = std::min(per_sm_b, h->deep_blocks_per_sm);
@@ -598,6 +613,35 @@ int ensure_deep(bc_handle *h) {
     h->deep_grid_f = per_sm_f * sms;
     h->deep_grid_b = per_sm_b * sms;
     return BC_OK;
+}
+
+// Level-ordered value arrays of the deep sweeps.  Fails softly: without the memory the sweeps
+// keep the row layout (returns false).
+bool ensure_deep_compact(bc_handle *h) {
+    if (!h->deep_compact || h->q_v == nullptr) return false;
+    if (h->qs != nullptr) return true;
+    const size_t G = (size_t)h->alloc_groups;
+    const int64_t vcap = 32 * h->n;
+    if (vcap >= ((int64_t)1 << 32)) return false;   // value offsets are 32-bit
+    if (arena_malloc((void **)&h->qs, G * (size_t)vcap * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        h->qs = nullptr;
+        h->deep_compact = 0;
+        return false;
+    }
+    if (arena_malloc((void **)&h->q_off, G * (size_t)h->q_cap * sizeof(uint32_t)) != cudaSuccess ||
+        arena_malloc((void **)&h->v_count, G * sizeof(unsigned long long)) != cudaSuccess ||
+        arena_malloc((void **)&h->bc_acc, (size_t)h->n * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
+        h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
+        h->deep_compact = 0;
+        return false;
+    }
+    cudaMemset(h->v_count, 0, G * sizeof(unsigned long long));
+    cudaMemset(h->bc_acc, 0, (size_t)h->n * sizeof(double));
+    h->q_vcap = vcap;
+    return true;
 }
 
 // Queue entries are (vertex, level) pairs: a vertex can sit in up to 32 levels of
@@ -621,6 +665,18 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
                                cudaMemcpyDeviceToDevice));
         CUDA_TRY(h, cudaMemcpy(nm + g * cap, h->q_m + g * h->q_cap, keep * sizeof(uint32_t),
                                cudaMemcpyDeviceToDevice));
+    }
+    if (h->q_off != nullptr) {
+        uint32_t *no = nullptr;
+        CUDA_TRY(h, arena_malloc((void **)&no, G * (size_t)cap * sizeof(uint32_t)));
+        for (size_t g = 0; g < G; ++g) {
+            const size_t keep = (size_t)std::min<int64_t>(g < used.size() ? (int64_t)used[g] : 0, h->q_cap);
+            if (keep == 0) continue;
+            CUDA_TRY(h, cudaMemcpy(no + g * cap, h->q_off + g * h->q_cap, keep * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToDevice));
+        }
+        arena_free(h->q_off);
+        h->q_off = no;
     }
     arena_free(h->q_v), arena_free(h->q_m);
     h->q_v = nv;

@@ -222,6 +222,7 @@ struct LevelRep {
     // batched byte model; -1 = not recorded (levels of a persistent run)
     long long vlanes = -1;   // (vertex, lane) pairs sitting at this level
     long long pairs = -1;    // (DAG arc, lane) pairs between the previous level and this one
+    bool compact = false;    // its path counts also sit in the level-ordered value array (h->qs)
 };
 
 QueueParams queue_params(bc_handle *h) {
@@ -348,6 +349,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                                     cudaMemcpyHostToDevice, st));
         return BC_OK;
     };
+    bool compact_started = false;
     bool pulled = false;    // a pull level has run (the frontier is past its peak)
     int device_level = -1;  // level whose ranges sit in d_qbeg / d_qend (and d_qlbeg = q_count)
     int next_slot = 1;
@@ -430,6 +432,16 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 dp.max_degree = kHeavyDeg;
                 if (seeds) dp.seeds = *seeds;
                 dp.seed_room = (unsigned long long)seed_room;
+                if (ensure_deep_compact(h)) {
+                    if (!compact_started) {   // value slots are handed out per batch
+                        CUDA_TRY(h, cudaMemsetAsync(h->v_count, 0, G * sizeof(unsigned long long), st));
+                        compact_started = true;
+                    }
+                    dp.qs = h->qs;
+                    dp.q_off = h->q_off;
+                    dp.v_count = h->v_count;
+                    dp.vcap = h->q_vcap;
+                }
                 void *args[] = {&dp};
                 CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_kernel, dim3(h->deep_grid_f),
                                                         dim3(kDeepThreads), args, 0, st));
@@ -464,6 +476,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                     lr.farcs = rep[1];
                     lr.maxdeg = rep[2];
                     lr.heavy = rep[2] > (unsigned long long)kHeavyDeg ? -1 : 0;   // no records built in there
+                    lr.compact = dp.qs != nullptr;
                 }
                 L += done - 1;
                 device_level = L;
@@ -574,6 +587,45 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
     auto beg_of = [&](int L) { return h->range_table + ((size_t)L * 2 + 0) * G; };
     auto end_of = [&](int L) { return h->range_table + ((size_t)L * 2 + 1) * G; };
     uint32_t *scr[2] = {h->scrA, h->scrB};
+    {
+        // ---- deep graphs: the whole sweep in one cooperative launch over level-ordered values
+        bool all_thin = !debug && h->deep && h->deep_compact && h->qs != nullptr && !h->lazy_clear &&
+                        ng <= kDeepMaxGroups && depth >= 3;
+        for (int L = 1; all_thin && L < depth; ++L) {
+            const LevelRep &x = reps[L];
+            all_thin = x.queued && x.slot < 0 && x.compact && x.maxdeg <= kQueueMaxDegree &&
+                       x.farcs * (unsigned long long)h->push_beta <= graph_arcs &&
+                       x.farcs <= kThinDegree * x.nverts;
+        }
+        if (all_thin) {
+            TRY(ensure_deep(h));
+            DeepBwdCompactParams dp{};
+            dp.off = c.off;
+            dp.col = c.col;
+            dp.n = h->n;
+            dp.q = queue_params(h);
+            dp.q_off = h->q_off;
+            dp.range_table = h->range_table;
+            dp.qs = h->qs;
+            dp.qc = h->coef;             // the coef rows are not used on this path: same size
+            dp.vcap = h->q_vcap;
+            dp.bc_acc = h->deep_compact == 2 ? nullptr : h->bc_acc;
+            dp.bcg = h->bcg;
+            dp.ng = ng;
+            dp.G = (int)G;
+            dp.hi = depth - 1;
+            dp.lo = last;
+            dp.scr0 = scr[0];
+            dp.scr1 = scr[1];
+            void *args[] = {&dp};
+            CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_compact_kernel, dim3(h->deep_grid_c),
+                                                    dim3(kDeepThreads), args, 0, st));
+            bc_acc_flush_kernel<<<grid1d((size_t)h->n, 256, 1184), 256, 0, st>>>(h->bc_acc, h->bcg, h->n);
+            h->launches += 2;
+            CUDA_TRY(h, cudaGetLastError());
+            return BC_OK;
+        }
+    }
     int holder = -1, held_level = -1;  // scratch array holding the masks of queue level held_level
     auto swap_scatter = [&](int erase_level, int erase_idx, int write_level, int write_idx) -> int {
         if (erase_idx < 0 && write_idx < 0) return BC_OK;

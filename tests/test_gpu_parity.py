@@ -277,6 +277,43 @@ def test_config2_rmat20_sample():
     assert st["sources"] == 1024 and st["max_levels"] >= 5
 
 
+def test_level_ordered_backward_of_deep_graphs():
+    """Deep graphs sweep backward over level-ordered sigma / coef values (deep_backward_compact_kernel):
+    same BC as the row layout -- bit for bit with per-group BC partials (deep_compact = 2), within
+    rounding order with the atomically updated BC vector (deep_compact = 1, the default)."""
+    cases = [(G.path(2500), [0, 17, 1250, 2499] + list(range(3, 2500, 97))),
+             (G.road_like(96, 96, keep=0.2, seed=5), list(range(0, 9216, 41))),
+             (G.grid(48, 30), list(range(0, 1440, 7)))]
+    for g, srcs in cases:
+        out = {}
+        for mode in (0, 1, 2):
+            with Engine(g) as e:
+                e.set_option("groups", 3)
+                e.set_option("deep_compact", mode)
+                bc, st = e.run(srcs)
+                bc2, _ = e.run(srcs)           # a second run on the same handle (buffers reused)
+            out[mode] = (bc, st)
+            assert np.allclose(bc, bc2, rtol=1e-12, atol=1e-12)
+        assert np.array_equal(out[0][0], out[2][0])
+        assert np.allclose(out[0][0], out[1][0], rtol=1e-12, atol=1e-9)
+        obc, _ = O.brandes_bc(g, srcs)
+        assert np.allclose(out[1][0], obc, rtol=RTOL, atol=ATOL)
+    # the partitioned sweeps on frontier queues take the same path
+    g = G.road_like(64, 64, keep=0.2, seed=3)
+    srcs = list(range(0, 4096, 29))
+    part = P.strip_partition(64, 64, 4)
+    res = {}
+    for mode in (0, 1):
+        with Engine(g) as e:
+            e.set_option("groups", 2)
+            e.set_option("reports", 0)
+            e.set_option("deep_compact", mode)
+            e.set_partition(4, part.assignment)
+            res[mode], _ = e.run(srcs, MODE_HYBIR)
+    assert np.allclose(res[0], res[1], rtol=1e-12, atol=1e-9)
+    assert np.allclose(res[1], O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
+
+
 def test_path_counts_beyond_2_53_against_the_bigint_reference():
     """sigma above 2^53 (SURVEY.md hard part 1) pinned to the reference's exact-integer oracle
     (golden vectors of tests/golden/gen_golden_bigsigma.py, 40 x 32 lattice, max sigma 2^66):
