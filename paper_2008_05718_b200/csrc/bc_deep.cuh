@@ -109,10 +109,20 @@ __device__ __forceinline__ int level_of_entry(const int64_t *level_end, int dept
 
 // (dist, sigma) of the border vertices out of a queue-level sweep (border_gather_kernel for the
 // dense level rows): one thread per queue entry, D_out / S_out pre-filled with kInf / 0.
+// Path count of lane `bit` of queue entry i (mask m): from the level-ordered value array of a
+// compact sweep (qs != nullptr) or from the row of its vertex.
+__device__ __forceinline__ double entry_sigma(const double *qs, const uint32_t *q_off, int64_t vcap,
+                                              const double *sigma, size_t g, int64_t n, size_t qslot,
+                                              int64_t v, uint32_t m, int bit) {
+    if (qs != nullptr) return qs[g * (size_t)vcap + q_off[qslot] + __popc(m & ((1u << bit) - 1u))];
+    return sigma[(g * n + v) * 32 + bit];
+}
+
 __global__ void border_gather_queue_kernel(QueueParams q, const int64_t *level_end, int depth, int G,
                                            int64_t n, const int32_t *border_index,
                                            const double *sigma, int S, int32_t *D_out,
-                                           double *S_out) {
+                                           double *S_out, const double *qs, const uint32_t *q_off,
+                                           int64_t vcap) {
     const size_t g = blockIdx.y;
     const int64_t end = (int64_t)q.q_count[g];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
@@ -120,14 +130,15 @@ __global__ void border_gather_queue_kernel(QueueParams q, const int64_t *level_e
         const int64_t v = q.q_v[g * q.cap + i];
         const int j = border_index[v];
         if (j < 0) continue;
-        uint32_t m = q.q_m[g * q.cap + i];
+        const uint32_t mask = q.q_m[g * q.cap + i];
+        uint32_t m = mask;
         const int level = level_of_entry(level_end, depth, G, g, i);
         while (m) {
             const int bit = __ffs(m) - 1;
             m &= m - 1;
             const size_t at = (size_t)j * S + g * 32 + bit;
             D_out[at] = level;
-            S_out[at] = sigma[(g * n + v) * 32 + bit];
+            S_out[at] = entry_sigma(qs, q_off, vcap, sigma, g, n, g * q.cap + i, v, mask, bit);
         }
     }
 }
@@ -137,7 +148,8 @@ __global__ void border_gather_queue_kernel(QueueParams q, const int64_t *level_e
 __global__ void border_table_queue_kernel(QueueParams q, const int64_t *level_end, int depth, int G,
                                           int64_t n, const int32_t *border_index,
                                           const double *sigma, BorderGeom geo, int first, int count,
-                                          int32_t *bm, double *sm) {
+                                          int32_t *bm, double *sm, const double *qs,
+                                          const uint32_t *q_off, int64_t vcap) {
     const size_t g = blockIdx.y;
     const int64_t end = (int64_t)q.q_count[g];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < end;
@@ -145,7 +157,8 @@ __global__ void border_table_queue_kernel(QueueParams q, const int64_t *level_en
         const int64_t v = q.q_v[g * q.cap + e];
         const int j = border_index[v];
         if (j < 0) continue;
-        uint32_t m = q.q_m[g * q.cap + e];
+        const uint32_t mask = q.q_m[g * q.cap + e];
+        uint32_t m = mask;
         const int level = level_of_entry(level_end, depth, G, g, e);
         const int p = geo.border_p[j];
         const int b = geo.part_off[p + 1] - geo.part_off[p];
@@ -157,7 +170,7 @@ __global__ void border_table_queue_kernel(QueueParams q, const int64_t *level_en
             const int i = first + lane_all;   // from-border (the lane's source), same part as j
             const size_t at = (size_t)geo.tab_off[p] + (size_t)(i - geo.part_off[p]) * b + (j - geo.part_off[p]);
             bm[at] = level;
-            sm[at] = sigma[(g * n + v) * 32 + bit];
+            sm[at] = entry_sigma(qs, q_off, vcap, sigma, g, n, g * q.cap + e, v, mask, bit);
         }
     }
 }
@@ -189,14 +202,6 @@ struct DeepFwdParams {
     unsigned long long max_degree;
     SeedPlan seeds;              // Step-6 border seeds joining at their own level (idx == nullptr: none)
     unsigned long long seed_room;   // queue entries the seeds of one level may add per group
-    // level-ordered copy of the path counts (nullptr: off).  Entry i of group g owns the slots
-    // q_off[g][i] .. + popc(q_m[i]) of qs[g][..], one per set lane in lane order: the backward
-    // sweep of a deep graph then reads sigma (and writes coef) sequentially instead of one random
-    // 8-byte access into the 256-byte row of the vertex (deep_backward_compact_kernel).
-    double *qs;
-    uint32_t *q_off;
-    unsigned long long *v_count;   // [G] value slots handed out so far
-    int64_t vcap;                  // value slots per group
 };
 
 // Forward: consecutive top-down levels, one THREAD per frontier entry.
@@ -337,34 +342,6 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
                     fa += deg;
                     md = max(md, deg);
                 }
-                if (p.qs != nullptr) {
-                    // value slots of the warp's entries: warp prefix of popc + one atomic per warp
-                    const unsigned pc = __popc(any);
-                    unsigned incl = pc;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const unsigned t = __shfl_up_sync(kFull, incl, o);
-                        if (lane >= o) incl += t;
-                    }
-                    const unsigned total = __shfl_sync(kFull, incl, 31);
-                    unsigned long long base = 0;
-                    if (lane == 0 && total) base = atomicAdd(p.v_count + g, (unsigned long long)total);
-                    base = __shfl_sync(kFull, base, 0);
-                    if (i < end) {
-                        const unsigned long long at = base + incl - pc;
-                        p.q_off[qbase + i] = (uint32_t)at;
-                        if (at + pc <= (unsigned long long)p.vcap) {
-                            const double *row = p.sigma + ((size_t)g * n + w) * 32;
-                            double *out = p.qs + (size_t)g * p.vcap + at;
-                            uint32_t m = any;
-                            while (m) {
-                                const int bit = __ffs(m) - 1;
-                                m &= m - 1;
-                                *out++ = row[bit];   // final: every push of the level is behind the barrier
-                            }
-                        }
-                    }
-                }
                 any = __reduce_or_sync(kFull, any);
                 if (lane == 0 && any) atomicOr(&s_live[g], any);
             }
@@ -433,6 +410,426 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
         __syncthreads();
         if (!s_cont) break;
     }
+}
+
+// ---- forward over level-ordered path counts ---------------------------------------------------
+// deep_forward_kernel adds path counts into the 256-byte row of the vertex: one random DRAM
+// read-modify-write per discovered (vertex, lane) pair plus one random read of the parent's row
+// (the rows of a 2048 x 2048 road graph span 17 GB per batch).  Here a level's path counts live in
+// the slots of its queue entries (qs[g][q_off[i] + rank of the lane in q_m[i]]), a window of a few
+// MB that stays in L2, and a level takes three phases:
+//   A  discover: frontier entries walk their arcs, OR the fresh lanes into next[], append new
+//      vertices to the queue and record the entry index in pos[g][w]; every frontier entry
+//      keeps a bit per arc that found something (q_arc);
+//   A2 post: the new entries get their lane masks (next[] -> q_m, vis |=, next = 0), their value
+//      slots (zeroed) and the level statistics;
+//   B  accumulate: the frontier entries walk the arcs marked in q_arc, look the child's entry up
+//      through pos[], and add their own path counts into the child's slots (red.global.add.f64
+//      on an L2-resident window; integer-valued, exact in any order).
+// The three per-(group, vertex) words the phases touch -- visited lanes, lanes being discovered at
+// this level, queue entry of the vertex -- sit side by side in one 16-byte record (VertexState), so
+// the visited probe of an arc, the OR into the next-level word and the entry index of the child
+// share a 32-byte sector: these dense arrays are what is left of the random DRAM traffic.
+// `pos` is never cleared inside a batch: queue indices only grow, so an index below the start of
+// the level being produced is a stale one.  The host initialises the records per sweep.
+struct __align__(16) VertexState {
+    uint32_t vis;    // lanes that reached the vertex
+    uint32_t next;   // lanes discovering it at the level being produced (zero between levels)
+    uint32_t pos;    // queue entry (index + 1) the vertex got most recently
+    uint32_t pad;
+};
+struct DeepFwdCompactParams {
+    const int64_t *off;
+    const int32_t *col;
+    int64_t n;
+    QueueParams q;
+    int64_t *q_beg, *q_end, *q_lbeg;
+    VertexState *vs;           // [G][n]
+    double *qs;                // [G][vcap]
+    uint32_t *q_off;           // [G][cap]
+    uint32_t *q_arc;           // [G][cap] arcs of a frontier entry that reached a fresh lane
+    unsigned long long *v_count;   // [G] value slots handed out so far
+    int64_t vcap;
+    uint32_t *live;
+    unsigned long long *counters;
+    unsigned long long *lstat;
+    unsigned long long *log;
+    int *run_info;
+    int ng, G;
+    int first_level;
+    int max_levels;
+    unsigned long long graph_arcs;
+    unsigned long long push_beta;
+    unsigned long long thin_degree;
+    unsigned long long max_degree;
+    SeedPlan seeds;
+    unsigned long long seed_room;
+};
+
+__global__ void __launch_bounds__(kDeepThreads) deep_forward_compact_kernel(const DeepFwdCompactParams p) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t stage[kDeepWarps][kStage];
+    __shared__ int64_t s_pref[kDeepMaxGroups + 1];
+    __shared__ int64_t s_beg[kDeepMaxGroups], s_end[kDeepMaxGroups], s_lbeg[kDeepMaxGroups];
+    __shared__ unsigned long long s_stat[8];
+    __shared__ uint32_t s_live[kDeepMaxGroups];
+    __shared__ int s_cont;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = p.n;
+    int *cont_flag = p.run_info + 1;
+
+    auto frontier_prefix = [&]() {   // flattened (group, entry) space of the frontier, groups padded to warps
+        if (threadIdx.x <= p.ng) {
+            int64_t acc = 0;
+            for (int g = 0; g < (int)threadIdx.x; ++g) acc += (s_end[g] - s_beg[g] + 31) & ~(int64_t)31;
+            s_pref[threadIdx.x] = acc;
+        }
+        __syncthreads();
+    };
+
+    for (int it = 0;; ++it) {
+        const int L = p.first_level + it;
+        for (int k = threadIdx.x; k < p.ng; k += blockDim.x) {
+            s_beg[k] = p.q.q_beg[k];
+            s_end[k] = p.q.q_end[k];
+            s_lbeg[k] = p.q_lbeg[k];
+        }
+        __syncthreads();
+        frontier_prefix();
+        // ---- phase A: discover
+        {
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            int staged = 0, staged_g = 0;   // warp-uniform
+            auto flush = [&]() {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(p.q.q_count + staged_g, (unsigned long long)staged);
+                base = __shfl_sync(kFull, base, 0);
+                const size_t qb = (size_t)staged_g * p.q.cap;
+                for (int k = lane; k < staged; k += 32) {
+                    const int32_t w = stage[warp][k];
+                    p.q.q_v[qb + base + k] = w;
+                    p.vs[(size_t)staged_g * n + w].pos = (uint32_t)(base + k) + 1u;
+                }
+                staged = 0;
+                __syncwarp();
+            };
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                if (g != staged_g) {
+                    if (staged) flush();
+                    staged_g = g;
+                }
+                const int64_t end = s_end[g];
+                const int64_t i = s_beg[g] + (f0 - s_pref[g]) + lane;
+                VertexState *gvs = p.vs + (size_t)g * n;
+                const size_t qbase = (size_t)g * p.q.cap;
+                uint32_t mask = 0;
+                int64_t a = 0, e = 0;
+                if (i < end) {
+                    const int32_t u = p.q.q_v[qbase + i];
+                    mask = p.q.q_m[qbase + i];
+                    a = p.off[u];
+                    e = p.off[u + 1];
+                }
+                int rounds = (int)(e - a);
+                rounds = __reduce_max_sync(kFull, rounds);
+                uint32_t arcbits = 0;
+                for (int r0 = 0; r0 < rounds; r0 += kThinArcs) {
+                    int32_t w[kThinArcs];
+                    uint32_t fresh[kThinArcs], old[kThinArcs];
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k) w[k] = (a + r0 + k < e) ? __ldg(p.col + a + r0 + k) : -1;
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k) fresh[k] = (w[k] >= 0) ? (mask & ~gvs[w[k]].vis) : 0u;
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k) old[k] = fresh[k] ? atomicOr(&gvs[w[k]].next, fresh[k]) : 1u;
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k) {
+                        if (r0 + k >= rounds) break;   // warp-uniform
+                        if (fresh[k] && r0 + k < 32) arcbits |= 1u << (r0 + k);
+                        const bool fresh_vertex = fresh[k] != 0 && old[k] == 0;
+                        const unsigned newm = __ballot_sync(kFull, fresh_vertex);
+                        if (newm) {
+                            if (fresh_vertex) stage[warp][staged + __popc(newm & ((1u << lane) - 1u))] = w[k];
+                            staged += __popc(newm);
+                            __syncwarp();
+                            if (staged > kStage - 32) flush();
+                        }
+                    }
+                }
+                if (i < end) p.q_arc[qbase + i] = arcbits;
+            }
+            if (staged) flush();
+        }
+        // border seeds of level L: discovered like any other vertex, their counts join in phase B
+        if (p.seeds.idx != nullptr && L < p.seeds.levels) {
+            const int64_t se = p.seeds.off[L + 1];
+            for (int64_t s = p.seeds.off[L] + gtid; s < se; s += gthreads) {
+                const int32_t idx = p.seeds.idx[s];
+                const int j = idx / p.seeds.S, lane_all = idx % p.seeds.S;
+                const size_t g = (size_t)(lane_all >> 5);
+                const uint32_t bit = 1u << (lane_all & 31);
+                const int64_t v = p.seeds.border_v[j];
+                VertexState *rec = p.vs + g * n + v;
+                if (rec->vis & bit) continue;   // cannot happen while D is the exact distance
+                const uint32_t old = atomicOr(&rec->next, bit);
+                if (old == 0) {
+                    const unsigned long long at = atomicAdd(p.q.q_count + g, 1ull);
+                    p.q.q_v[g * p.q.cap + at] = (int32_t)v;
+                    rec->pos = (uint32_t)at + 1u;
+                }
+            }
+        }
+        grid.sync();
+
+        // ---- phase A2: the entries appended above become level L
+        if (threadIdx.x <= p.ng) {
+            int64_t acc = 0;
+            for (int g = 0; g < (int)threadIdx.x; ++g)
+                acc += ((int64_t)p.q.q_count[g] - s_lbeg[g] + 31) & ~(int64_t)31;
+            s_pref[threadIdx.x] = acc;
+        }
+        if (threadIdx.x < 8) s_stat[threadIdx.x] = 0ull;
+        for (int k = threadIdx.x; k < p.ng; k += blockDim.x) s_live[k] = 0u;
+        __syncthreads();
+        {
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            unsigned long long nr = 0, ar = 0, nv = 0, fa = 0, md = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t end = (int64_t)p.q.q_count[g];
+                const int64_t i = s_lbeg[g] + (f0 - s_pref[g]) + lane;
+                const size_t qbase = (size_t)g * p.q.cap;
+                uint32_t m = 0;
+                if (i < end) {
+                    const int32_t w = p.q.q_v[qbase + i];
+                    uint2 *vn = reinterpret_cast<uint2 *>(p.vs + (size_t)g * n + w);   // (vis, next)
+                    const uint2 cur = *vn;
+                    m = cur.y;
+                    p.q.q_m[qbase + i] = m;
+                    *vn = make_uint2(cur.x | m, 0u);
+                    const unsigned long long deg = (unsigned long long)(p.off[w + 1] - p.off[w]);
+                    nr += __popc(m);
+                    ar += __popc(m) * deg;
+                    nv += 1;
+                    fa += deg;
+                    md = max(md, deg);
+                }
+                // value slots of the warp's entries: warp prefix of popc + one atomic per warp
+                const unsigned pc = __popc(m);
+                unsigned incl = pc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned wtotal = __shfl_sync(kFull, incl, 31);
+                unsigned long long base = 0;
+                if (lane == 0 && wtotal) base = atomicAdd(p.v_count + g, (unsigned long long)wtotal);
+                base = __shfl_sync(kFull, base, 0);
+                if (i < end) {
+                    const unsigned long long at = base + incl - pc;
+                    p.q_off[qbase + i] = (uint32_t)at;
+                    if (at + pc <= (unsigned long long)p.vcap)
+                        for (unsigned k = 0; k < pc; ++k) p.qs[(size_t)g * p.vcap + at + k] = 0.0;
+                }
+                const uint32_t any = __reduce_or_sync(kFull, m);
+                if (lane == 0 && any) atomicOr(&s_live[g], any);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                nr += __shfl_xor_sync(kFull, nr, o);
+                ar += __shfl_xor_sync(kFull, ar, o);
+                nv += __shfl_xor_sync(kFull, nv, o);
+                fa += __shfl_xor_sync(kFull, fa, o);
+                md = max(md, __shfl_xor_sync(kFull, md, o));
+            }
+            if (lane == 0 && nv) {
+                atomicAdd(&s_stat[0], nr);
+                atomicAdd(&s_stat[1], ar);
+                atomicAdd(&s_stat[2], nv);
+                atomicAdd(&s_stat[3], fa);
+                atomicMax(&s_stat[4], md);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && s_stat[2]) {
+                atomicAdd(p.counters + 0, s_stat[0]);
+                atomicAdd(p.counters + 1, s_stat[1]);
+                atomicAdd(p.lstat + 0, s_stat[2]);
+                atomicAdd(p.lstat + 1, s_stat[3]);
+                atomicMax(p.lstat + 2, s_stat[4]);
+            }
+            for (int k = threadIdx.x; k < p.ng; k += blockDim.x)
+                if (s_live[k]) atomicOr(p.live + (size_t)L * p.G + k, s_live[k]);
+        }
+        grid.sync();
+
+        // ---- phase B: the frontier adds its path counts into the new entries' slots
+        frontier_prefix();
+        unsigned c_t = 0;
+        {
+            const int64_t total = s_pref[p.ng];
+            int g = 0;
+            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+                while (f0 >= s_pref[g + 1]) ++g;
+                const int64_t i = s_beg[g] + (f0 - s_pref[g]) + lane;
+                if (i >= s_end[g]) continue;
+                const size_t qbase = (size_t)g * p.q.cap;
+                const size_t vbase = (size_t)g * p.vcap;
+                const uint32_t mask = p.q.q_m[qbase + i];
+                const int32_t u = p.q.q_v[qbase + i];
+                const int64_t a = p.off[u], e = p.off[u + 1];
+                const uint32_t at_u = p.q_off[qbase + i];
+                const VertexState *gvs = p.vs + (size_t)g * n;
+                const uint32_t lbeg = (uint32_t)s_lbeg[g];
+                auto add_into = [&](int32_t w) {
+                    const uint32_t pj = gvs[w].pos;
+                    if (pj <= lbeg) return;                 // no entry in the level being produced
+                    const uint32_t mj = p.q.q_m[qbase + pj - 1];
+                    uint32_t lanes = mask & mj;
+                    if (lanes == 0) return;
+                    const uint32_t oj = p.q_off[qbase + pj - 1];
+                    while (lanes) {
+                        const int bit = __ffs(lanes) - 1;
+                        lanes &= lanes - 1;
+                        const uint32_t lower = (1u << bit) - 1u;
+                        atomicAdd(p.qs + vbase + oj + __popc(mj & lower), p.qs[vbase + at_u + __popc(mask & lower)]);
+                        ++c_t;
+                    }
+                };
+                if (e - a <= 32) {
+                    uint32_t bits = p.q_arc[qbase + i];
+                    while (bits) {
+                        const int k = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        add_into(__ldg(p.col + a + k));
+                    }
+                } else {
+                    for (int64_t b = a; b < e; ++b) add_into(__ldg(p.col + b));
+                }
+            }
+        }
+        if (p.seeds.idx != nullptr && L < p.seeds.levels) {
+            const int64_t se = p.seeds.off[L + 1];
+            for (int64_t s = p.seeds.off[L] + gtid; s < se; s += gthreads) {
+                const int32_t idx = p.seeds.idx[s];
+                const int j = idx / p.seeds.S, lane_all = idx % p.seeds.S;
+                const size_t g = (size_t)(lane_all >> 5);
+                const int bit = lane_all & 31;
+                const int64_t v = p.seeds.border_v[j];
+                const uint32_t pj = p.vs[g * n + v].pos;
+                if (pj <= (uint32_t)s_lbeg[g]) continue;
+                const uint32_t mj = p.q.q_m[g * p.q.cap + pj - 1];
+                if (!((mj >> bit) & 1u)) continue;
+                atomicAdd(p.qs + g * (size_t)p.vcap + p.q_off[g * p.q.cap + pj - 1] + __popc(mj & ((1u << bit) - 1u)),
+                          p.seeds.arr[idx]);
+            }
+        }
+        {
+            if (threadIdx.x == 0) s_stat[5] = 0ull;
+            __syncthreads();
+            const unsigned t = __reduce_add_sync(kFull, c_t);
+            if (lane == 0 && t) atomicAdd(&s_stat[5], (unsigned long long)t);
+            __syncthreads();
+            if (threadIdx.x == 0 && s_stat[5]) atomicAdd(p.counters + 2, s_stat[5]);
+        }
+        // ---- publish the level, rotate the ranges, decide whether to go on (block 0; the other
+        // blocks only read their shared copies of the ranges in phase B)
+        if (blockIdx.x == 0) {
+            unsigned long long *rep = p.log + (size_t)it * (3 + 2 * p.G);
+            const int g = threadIdx.x;
+            unsigned long long nverts = p.lstat[0], farcs = p.lstat[1], maxdeg = p.lstat[2];
+            uint32_t alive_any = 0;
+            unsigned long long used = 0;
+            for (int j = 0; j < p.ng; ++j) {
+                alive_any |= p.live[(size_t)L * p.G + j];
+                used = max(used, p.q.q_count[j]);
+            }
+            __syncthreads();
+            if (g < 3) rep[g] = p.lstat[g];
+            if (g < p.G) {
+                const unsigned long long c = p.q.q_count[g];
+                rep[3 + g] = c;
+                rep[3 + p.G + g] = p.live[(size_t)L * p.G + g];
+                p.q_beg[g] = p.q_lbeg[g];
+                p.q_end[g] = (int64_t)c;
+                p.q_lbeg[g] = (int64_t)c;
+            }
+            __syncthreads();
+            if (g == 0) {
+                p.lstat[0] = p.lstat[1] = p.lstat[2] = 0;
+                const unsigned long long room = min((unsigned long long)n, farcs) + 1 + p.seed_room;
+                const bool go = alive_any != 0 && it + 1 < p.max_levels &&
+                                farcs * p.push_beta <= p.graph_arcs && maxdeg <= p.max_degree &&
+                                farcs <= p.thin_degree * nverts &&
+                                (unsigned long long)p.q.cap - used >= room;
+                p.run_info[0] = it + 1;
+                *cont_flag = go ? 1 : 0;
+            }
+        }
+        grid.sync();
+        if (threadIdx.x == 0) s_cont = *(volatile int *)cont_flag;
+        __syncthreads();
+        if (!s_cont) break;
+    }
+}
+
+// Rows from level-ordered values (a compact sweep that has to continue on the row layout): every
+// queue entry writes its path counts back into the row of its vertex.
+__global__ void decompact_sigma_kernel(QueueParams q, const uint32_t *q_off, const double *qs,
+                                       int64_t vcap, int64_t n, double *sigma) {
+    const size_t g = blockIdx.y;
+    const int64_t end = (int64_t)q.q_count[g];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = q.q_v[g * q.cap + i];
+        uint32_t m = q.q_m[g * q.cap + i];
+        const double *in = qs + g * (size_t)vcap + q_off[g * q.cap + i];
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            sigma[(g * n + v) * 32 + bit] = *in++;
+        }
+    }
+}
+
+// Per-vertex records of a compact sweep: lanes the batch does not use count as visited.
+__global__ void compact_init_kernel(VertexState *vs, int64_t n, int batch_count) {
+    const size_t g = blockIdx.y;
+    const int lanes = min(32, batch_count - (int)g * 32);
+    const uint32_t dead = lanes >= 32 ? 0u : ~((1u << lanes) - 1u);
+    uint4 *out = reinterpret_cast<uint4 *>(vs + g * n);
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = make_uint4(dead, 0u, 0u, 0u);
+}
+
+// ... and the visited words out of the vertex records, for the row-based kernels that take over.
+__global__ void vis_from_records_kernel(const VertexState *vs, uint32_t *vis, int64_t n) {
+    const size_t g = blockIdx.y;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        vis[g * n + v] = vs[g * n + v].vis;
+}
+
+// Level 0 of a compact sweep: every set lane of a source entry carries one path.
+__global__ void compact_level0_kernel(QueueParams q, uint32_t *q_off, double *qs, int64_t vcap,
+                                      unsigned long long *v_count, VertexState *vs, int64_t n) {
+    const size_t g = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    const int64_t end = (int64_t)q.q_count[g];
+    uint32_t at = 0;
+    for (int64_t i = 0; i < end; ++i) {     // <= 32 entries
+        const uint32_t m = q.q_m[g * q.cap + i];
+        vs[g * n + q.q_v[g * q.cap + i]].vis |= m;
+        q_off[g * q.cap + i] = at;
+        for (int k = 0; k < __popc(m); ++k) qs[g * (size_t)vcap + at + k] = 1.0;
+        at += __popc(m);
+    }
+    v_count[g] = at;
 }
 
 struct DeepBwdParams {
@@ -532,9 +929,11 @@ __global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepB
 // scratch; ncu: 687 B of DRAM traffic per visit at 2.8 TB/s, profiles/r2_deep_kernels_ncu.md).
 // This variant keeps sigma and coef per queue ENTRY, in level order (DeepFwdParams::qs):
 //   - an entry reads its sigma and writes its coef at q_off[i] + rank: sequential traffic;
-//   - the scratch array maps a vertex to the queue entry it has at the level below (index + 1),
-//     so a parent finds a child's lanes (q_m[j]) and coef (qc[q_off[j] + rank]) inside the
-//     few-MB window of that level, which stays in L2;
+//   - the vertex record (VertexState::pos) maps a vertex to the queue entry it has at the level
+//     below (index + 1; every entry re-writes it when its level is processed, and an index
+//     outside that level's range is a stale one, so nothing is ever erased), and a parent finds a
+//     child's lanes (q_m[j]) and coef (qc[q_off[j] + rank]) inside the few-MB window of that
+//     level, which stays in L2;
 //   - BC partials are added with atomics into ONE vector per batch (bc_acc, n doubles: L2
 //     resident) instead of a read-modify-write of the 8-byte partial of (group, vertex) in a
 //     G x n array: the per-vertex sums then depend on the order the atomics land in (last-bit
@@ -553,133 +952,123 @@ struct DeepBwdCompactParams {
     double *bcg;                 // [G][n] per-group partials (used when bc_acc == nullptr)
     int ng, G;
     int hi, lo;                  // levels hi (the deepest level of the batch), hi - 1, ..., lo
-    uint32_t *scr0, *scr1;       // all-zero scratch arrays on entry and on exit
+    VertexState *vs;             // [G][n] (pos field)
 };
 
 __global__ void __launch_bounds__(kDeepThreads) deep_backward_compact_kernel(const DeepBwdCompactParams p) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int64_t s_pref[kDeepMaxGroups + 1];
+    __shared__ uint32_t s_cb[kDeepMaxGroups], s_ce[kDeepMaxGroups];   // entry range (+1) of the level below
     const int lane = threadIdx.x & 31;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n = p.n;
-    const uint32_t *below = nullptr;   // scratch holding entry index + 1 of the level below
-    uint32_t *erase = nullptr;
-    int widx = 0;
-    for (int L = p.hi; L >= p.lo - 1; --L) {
-        // iteration L = lo - 1 only erases what level lo left in the scratch array
-        if (L >= p.lo) {
-            uint32_t *wr = widx ? p.scr1 : p.scr0;
-            const int64_t *beg_t = p.range_table + ((size_t)L * 2 + 0) * p.G;
-            const int64_t *end_t = p.range_table + ((size_t)L * 2 + 1) * p.G;
-            if (threadIdx.x <= p.ng) {
-                int64_t acc = 0;
-                for (int g = 0; g < (int)threadIdx.x; ++g) acc += (end_t[g] - beg_t[g] + 31) & ~(int64_t)31;
-                s_pref[threadIdx.x] = acc;
-            }
-            __syncthreads();
-            const int64_t total = s_pref[p.ng];
-            int g = 0;
-            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
-                while (f0 >= s_pref[g + 1]) ++g;
-                const int64_t i = beg_t[g] + (f0 - s_pref[g]) + lane;
-                if (i >= end_t[g]) continue;
-                const size_t qbase = (size_t)g * p.q.cap;
-                const size_t vbase = (size_t)g * p.vcap;
-                const int64_t v = p.q.q_v[qbase + i];
-                const uint32_t m = p.q.q_m[qbase + i];
-                const uint32_t at = p.q_off[qbase + i];
-                wr[(size_t)g * n + v] = (uint32_t)i + 1u;
-                if (m == 0) continue;
-                const int64_t a0 = p.off[v], a1 = p.off[v + 1];
-                double total_d = 0.0;
-                // children: entry (index + 1) of every neighbour at the level below, its lanes and
-                // its first value slot -- kThinArcs arcs at a time, one round trip per stage
-                uint32_t rest = m;
-                int rank = 0;
-                if (a1 - a0 <= kThinArcs || below == nullptr) {
-                    uint32_t cj[kThinArcs], cm[kThinArcs], co[kThinArcs];
-#pragma unroll
-                    for (int k = 0; k < kThinArcs; ++k) {
-                        cj[k] = 0;
-                        if (below != nullptr && a0 + k < a1) cj[k] = below[(size_t)g * n + __ldg(p.col + a0 + k)];
-                    }
-#pragma unroll
-                    for (int k = 0; k < kThinArcs; ++k) {
-                        cm[k] = cj[k] ? p.q.q_m[qbase + cj[k] - 1] : 0u;
-                        co[k] = cj[k] ? p.q_off[qbase + cj[k] - 1] : 0u;
-                    }
-                    while (rest) {
-                        const int bit = __ffs(rest) - 1;
-                        rest &= rest - 1;
-                        const uint32_t lower = (1u << bit) - 1u;
-                        double c[kThinArcs];
-#pragma unroll
-                        for (int k = 0; k < kThinArcs; ++k)
-                            c[k] = ((cm[k] >> bit) & 1u) ? p.qc[vbase + co[k] + __popc(cm[k] & lower)] : 0.0;
-                        double acc = 0.0;
-#pragma unroll
-                        for (int k = 0; k < kThinArcs; ++k)
-                            if ((cm[k] >> bit) & 1u) acc += c[k];   // ascending arc order
-                        const double sv = p.qs[vbase + at + rank];
-                        const double d = sv * acc;
-                        p.qc[vbase + at + rank] = (1.0 + d) / sv;
-                        total_d += d;
-                        ++rank;
-                    }
-                } else {
-                    while (rest) {
-                        const int bit = __ffs(rest) - 1;
-                        rest &= rest - 1;
-                        const uint32_t lower = (1u << bit) - 1u;
-                        double acc = 0.0;
-                        for (int64_t a = a0; a < a1; ++a) {
-                            const uint32_t j = below[(size_t)g * n + __ldg(p.col + a)];
-                            if (j == 0) continue;
-                            const uint32_t mj = p.q.q_m[qbase + j - 1];
-                            if ((mj >> bit) & 1u) acc += p.qc[vbase + p.q_off[qbase + j - 1] + __popc(mj & lower)];
-                        }
-                        const double sv = p.qs[vbase + at + rank];
-                        const double d = sv * acc;
-                        p.qc[vbase + at + rank] = (1.0 + d) / sv;
-                        total_d += d;
-                        ++rank;
-                    }
-                }
-                if (p.bc_acc != nullptr) {
-                    if (total_d != 0.0) atomicAdd(p.bc_acc + v, total_d);
-                } else {
-                    p.bcg[(size_t)g * n + v] += total_d;
-                }
-            }
-            __syncthreads();   // s_pref is rewritten below
+    for (int L = p.hi; L >= p.lo; --L) {
+        const bool deepest = L == p.hi;
+        const int64_t *beg_t = p.range_table + ((size_t)L * 2 + 0) * p.G;
+        const int64_t *end_t = p.range_table + ((size_t)L * 2 + 1) * p.G;
+        if (threadIdx.x <= p.ng) {
+            int64_t acc = 0;
+            for (int g = 0; g < (int)threadIdx.x; ++g) acc += (end_t[g] - beg_t[g] + 31) & ~(int64_t)31;
+            s_pref[threadIdx.x] = acc;
         }
+        for (int k = threadIdx.x; k < p.ng; k += blockDim.x) {
+            s_cb[k] = deepest ? 1u : (uint32_t)p.range_table[((size_t)(L + 1) * 2 + 0) * p.G + k] + 1u;
+            s_ce[k] = deepest ? 0u : (uint32_t)p.range_table[((size_t)(L + 1) * 2 + 1) * p.G + k];
+        }
+        __syncthreads();
+        const int64_t total = s_pref[p.ng];
+        int g = 0;
+        for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
+            while (f0 >= s_pref[g + 1]) ++g;
+            const int64_t i = beg_t[g] + (f0 - s_pref[g]) + lane;
+            if (i >= end_t[g]) continue;
+            const size_t qbase = (size_t)g * p.q.cap;
+            const size_t vbase = (size_t)g * p.vcap;
+            VertexState *gvs = p.vs + (size_t)g * n;
+            const int64_t v = p.q.q_v[qbase + i];
+            const uint32_t m = p.q.q_m[qbase + i];
+            const uint32_t at = p.q_off[qbase + i];
+            if (m == 0) continue;
+            const int64_t a0 = p.off[v], a1 = p.off[v + 1];
+            const uint32_t cb = s_cb[g], ce = s_ce[g];   // a child's entry index + 1 lies in [cb, ce]
+            double total_d = 0.0;
+            uint32_t rest = m;
+            int rank = 0;
+            if (a1 - a0 <= kThinArcs || deepest) {
+                // children: entry of every neighbour at the level below, its lanes and its first
+                // value slot -- kThinArcs arcs at a time, one round trip per stage
+                uint32_t cj[kThinArcs], cm[kThinArcs], co[kThinArcs];
+#pragma unroll
+                for (int k = 0; k < kThinArcs; ++k) {
+                    cj[k] = 0;
+                    if (!deepest && a0 + k < a1) {
+                        const uint32_t pj = gvs[__ldg(p.col + a0 + k)].pos;
+                        if (pj >= cb && pj <= ce) cj[k] = pj;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kThinArcs; ++k) {
+                    cm[k] = cj[k] ? p.q.q_m[qbase + cj[k] - 1] : 0u;
+                    co[k] = cj[k] ? p.q_off[qbase + cj[k] - 1] : 0u;
+                }
+                while (rest) {
+                    const int bit = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    const uint32_t lower = (1u << bit) - 1u;
+                    double c[kThinArcs];
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k)
+                        c[k] = ((cm[k] >> bit) & 1u) ? p.qc[vbase + co[k] + __popc(cm[k] & lower)] : 0.0;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < kThinArcs; ++k)
+                        if ((cm[k] >> bit) & 1u) acc += c[k];   // ascending arc order
+                    const double sv = p.qs[vbase + at + rank];
+                    const double d = sv * acc;
+                    p.qc[vbase + at + rank] = (1.0 + d) / sv;
+                    total_d += d;
+                    ++rank;
+                }
+            } else {
+                while (rest) {
+                    const int bit = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    const uint32_t lower = (1u << bit) - 1u;
+                    double acc = 0.0;
+                    for (int64_t a = a0; a < a1; ++a) {
+                        const uint32_t pj = gvs[__ldg(p.col + a)].pos;
+                        if (pj < cb || pj > ce) continue;
+                        const uint32_t mj = p.q.q_m[qbase + pj - 1];
+                        if ((mj >> bit) & 1u) acc += p.qc[vbase + p.q_off[qbase + pj - 1] + __popc(mj & lower)];
+                    }
+                    const double sv = p.qs[vbase + at + rank];
+                    const double d = sv * acc;
+                    p.qc[vbase + at + rank] = (1.0 + d) / sv;
+                    total_d += d;
+                    ++rank;
+                }
+            }
+            if (p.bc_acc != nullptr) {
+                if (total_d != 0.0) atomicAdd(p.bc_acc + v, total_d);
+            } else {
+                p.bcg[(size_t)g * n + v] += total_d;
+            }
+        }
+        __syncthreads();   // the shared ranges are rewritten by the next level
         grid.sync();
-        if (erase != nullptr) {
-            const int64_t *eb = p.range_table + ((size_t)(L + 1) * 2 + 0) * p.G;
-            const int64_t *ee = p.range_table + ((size_t)(L + 1) * 2 + 1) * p.G;
-            if (threadIdx.x <= p.ng) {
-                int64_t acc = 0;
-                for (int g = 0; g < (int)threadIdx.x; ++g) acc += (ee[g] - eb[g] + 31) & ~(int64_t)31;
-                s_pref[threadIdx.x] = acc;
-            }
-            __syncthreads();
-            const int64_t total = s_pref[p.ng];
-            int g = 0;
+        // level L becomes the level below: its entries take over the vertex records
+        {
+            int g2 = 0;
             for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
-                while (f0 >= s_pref[g + 1]) ++g;
-                const int64_t i = eb[g] + (f0 - s_pref[g]) + lane;
-                if (i < ee[g]) erase[(size_t)g * n + p.q.q_v[(size_t)g * p.q.cap + i]] = 0u;
+                while (f0 >= s_pref[g2 + 1]) ++g2;
+                const int64_t i = beg_t[g2] + (f0 - s_pref[g2]) + lane;
+                if (i < end_t[g2])
+                    p.vs[(size_t)g2 * n + p.q.q_v[(size_t)g2 * p.q.cap + i]].pos = (uint32_t)i + 1u;
             }
-            __syncthreads();
-            grid.sync();
         }
-        if (L >= p.lo) {
-            uint32_t *wr = widx ? p.scr1 : p.scr0;
-            below = wr;
-            erase = wr;
-            widx ^= 1;
-        }
+        __syncthreads();
+        grid.sync();
     }
 }
 

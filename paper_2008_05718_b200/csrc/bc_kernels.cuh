@@ -551,6 +551,15 @@ __global__ void seed_sources_kernel(const int64_t *src, int batch_count, int64_t
     sigma[(g * n + v) * 32 + lane] = 1.0;
 }
 
+// sigma = 1 at the sources (rows cleared after begin_batch: see forward_adaptive).
+__global__ void source_sigma_kernel(const int64_t *src, int batch_count, int64_t n, double *sigma) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch_count) return;
+    const size_t g = i >> 5;
+    if (src[i] < 0) return;
+    sigma[(g * n + src[i]) * 32 + (i & 31)] = 1.0;
+}
+
 // The sources sit at level 0, which the backward sweep does not visit: clear their
 // path counts separately (see finalize_backward).
 __global__ void clear_source_sigma_kernel(const int64_t *src, int batch_count, int64_t n, double *sigma) {

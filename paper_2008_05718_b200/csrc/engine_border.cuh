@@ -291,6 +291,12 @@ int build_border_tables(bc_handle *h) {
         CUDA_TRY(h, cudaMemsetAsync(h->sm, 0, (size_t)h->tab_total * sizeof(double), st));
         ++h->launches;
     }
+    struct AllowScope {   // the table searches read their path counts through the queue entries
+        bc_handle *h;
+        bool was;
+        ~AllowScope() { h->fwd_compact_allowed = was; }
+    } allow_scope{h, h->fwd_compact_allowed};
+    h->fwd_compact_allowed = qsweep;
     for (int first = b_lo; first < b_hi; first += per) {
         const int cnt = std::min(per, b_hi - first);
         const int ng = (cnt + 31) / 32;
@@ -302,7 +308,7 @@ int build_border_tables(bc_handle *h) {
             TRY(upload_level_ends(h, reps, depth, st));
             border_table_queue_kernel<<<dim3(queue_blocks_all(reps, depth), ng), 256, 0, st>>>(
                 queue_params(h), h->range_table, depth, h->alloc_groups, h->n, h->d_border_index, h->sigma,
-                geo, first, cnt, h->bm, h->sm);
+                geo, first, cnt, h->bm, h->sm, reps.back().compact ? h->qs : nullptr, h->q_off, h->q_vcap);
             ++h->launches;
             CUDA_TRY(h, cudaGetLastError());
             continue;

@@ -92,6 +92,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     if (h->bcg_dirty)
         CUDA_TRY(h, cudaMemsetAsync(h->bcg, 0, (size_t)h->alloc_groups * (size_t)n * sizeof(double), st));
     h->bcg_dirty = !debug;   // until reduce_bc_kernel has run
+    // inspection reads sigma / delta rows; everything else may keep deep sweeps in level order
+    struct AllowScope {
+        bc_handle *h;
+        ~AllowScope() { h->fwd_compact_allowed = false; }
+    } allow_scope{h};
+    h->fwd_compact_allowed = !debug;
     const int64_t launches0 = h->launches;
     const int64_t level_launches0 = h->level_launches;
     h->model_scan = h->model_pairs = h->model_vlanes = h->model_dense_words = h->model_entries = 0;
@@ -162,7 +168,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             if (h->B > 0)
                 border_gather_queue_kernel<<<dim3(queue_blocks_all(out.reps, out.depth), ng), 256, 0, s>>>(
                     queue_params(h), h->range_table, out.depth, h->alloc_groups, n, h->d_border_index,
-                    h->sigma, h->border_S, seedD, seedS);
+                    h->sigma, h->border_S, seedD, seedS, out.reps.back().compact ? h->qs : nullptr, h->q_off,
+                    h->q_vcap);
         } else {
             TRY(upload_level_ptrs(h, out.depth, s));
             if (h->B > 0)

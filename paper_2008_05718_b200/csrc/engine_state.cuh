@@ -170,7 +170,7 @@ struct bc_handle {
     int push_beta = 4;     // push when frontier arcs * beta <= arcs of the graph
     int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
     int deep_blocks_per_sm = 0;   // 0 = what the occupancy calculator allows
-    int deep_grid_f = 0, deep_grid_b = 0, deep_grid_c = 0;
+    int deep_grid_f = 0, deep_grid_b = 0, deep_grid_c = 0, deep_grid_fc = 0;
     unsigned long long *deep_log = nullptr;
     int *deep_info = nullptr;
     // ---- partition ------------------------------------------------------
@@ -251,6 +251,12 @@ struct bc_handle {
     unsigned long long *v_count = nullptr;   // [G]
     int64_t q_vcap = 0;
     double *bc_acc = nullptr;      // [n] BC partial of a batch, added with atomics
+    VertexState *vs = nullptr;     // [G][n] visited / next-level / queue-entry words of the compact sweeps
+    uint32_t *q_arc = nullptr;     // [G][q_cap] arcs of a frontier entry that reached a fresh lane
+    bool fwd_compact_allowed = false;   // set by the caller of a sweep: nobody reads sigma rows afterwards
+    bool sigma_stale = false;      // the sigma rows were not cleared for this batch (compact sweep expected)
+    const int64_t *batch_src_dev = nullptr;   // sources of the batch in flight (begin_batch)
+    int batch_cnt = 0;
     unsigned long long *q_count = nullptr;
     int64_t *d_qbeg = nullptr, *d_qend = nullptr, *d_qlbeg = nullptr;
     uint32_t *scrA = nullptr, *scrB = nullptr;
@@ -422,6 +428,8 @@ void free_state(bc_handle *h) {
     h->live_cap = 0;
     arena_free(h->q_v), arena_free(h->q_m), arena_free(h->q_count);
     arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
+    arena_free(h->vs), arena_free(h->q_arc);
+    h->vs = nullptr, h->q_arc = nullptr;
     h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
     h->q_vcap = 0;
     arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
@@ -604,6 +612,11 @@ int ensure_deep(bc_handle *h) {
                                                               kDeepThreads, 0));
     if (h->deep_blocks_per_sm > 0) per_sm_c = std::min(per_sm_c, h->deep_blocks_per_sm);
     h->deep_grid_c = std::max(per_sm_c, 0) * sms;
+    int per_sm_fc = 0;
+    CUDA_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fc, deep_forward_compact_kernel,
+                                                              kDeepThreads, 0));
+    if (h->deep_blocks_per_sm > 0) per_sm_fc = std::min(per_sm_fc, h->deep_blocks_per_sm);
+    h->deep_grid_fc = std::max(per_sm_fc, 0) * sms;
     if (h->deep_blocks_per_sm > 0) {
         per_sm_f = std::min(per_sm_f, h->deep_blocks_per_sm);
         per_sm_b = std::min(per_sm_b, h->deep_blocks_per_sm);
@@ -630,11 +643,15 @@ bool ensure_deep_compact(bc_handle *h) {
         return false;
     }
     if (arena_malloc((void **)&h->q_off, G * (size_t)h->q_cap * sizeof(uint32_t)) != cudaSuccess ||
+        arena_malloc((void **)&h->q_arc, G * (size_t)h->q_cap * sizeof(uint32_t)) != cudaSuccess ||
+        arena_malloc((void **)&h->vs, G * (size_t)h->n * sizeof(VertexState)) != cudaSuccess ||
         arena_malloc((void **)&h->v_count, G * sizeof(unsigned long long)) != cudaSuccess ||
         arena_malloc((void **)&h->bc_acc, (size_t)h->n * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
         arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
+        arena_free(h->vs), arena_free(h->q_arc);
         h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
+        h->vs = nullptr, h->q_arc = nullptr;
         h->deep_compact = 0;
         return false;
     }
@@ -666,17 +683,18 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
         CUDA_TRY(h, cudaMemcpy(nm + g * cap, h->q_m + g * h->q_cap, keep * sizeof(uint32_t),
                                cudaMemcpyDeviceToDevice));
     }
-    if (h->q_off != nullptr) {
+    for (uint32_t **arr : {&h->q_off, &h->q_arc}) {
+        if (*arr == nullptr) continue;
         uint32_t *no = nullptr;
         CUDA_TRY(h, arena_malloc((void **)&no, G * (size_t)cap * sizeof(uint32_t)));
         for (size_t g = 0; g < G; ++g) {
             const size_t keep = (size_t)std::min<int64_t>(g < used.size() ? (int64_t)used[g] : 0, h->q_cap);
             if (keep == 0) continue;
-            CUDA_TRY(h, cudaMemcpy(no + g * cap, h->q_off + g * h->q_cap, keep * sizeof(uint32_t),
+            CUDA_TRY(h, cudaMemcpy(no + g * cap, *arr + g * h->q_cap, keep * sizeof(uint32_t),
                                    cudaMemcpyDeviceToDevice));
         }
-        arena_free(h->q_off);
-        h->q_off = no;
+        arena_free(*arr);
+        *arr = no;
     }
     arena_free(h->q_v), arena_free(h->q_m);
     h->q_v = nv;

@@ -119,9 +119,16 @@ int begin_batch(bc_handle *h, const int64_t *src_dev, int cnt, int ng, cudaStrea
     // Deep graphs (previous batch above 64 levels) take the memset instead: there the extra dirty
     // sector per (vertex, source) visit costs more than clearing the array.
     h->lazy_clear = zero_sigma && h->last_depth <= 64;
-    if (zero_sigma && !(h->sigma_clean && h->lazy_clear))
+    // Deep graphs keep their path counts in level order (deep_forward_compact_kernel) and never
+    // touch the rows: the memset (17 GB per batch on the 2048^2 road graph) is skipped when the
+    // sweep is expected to take that path; forward_adaptive clears the rows itself if it does not.
+    h->sigma_stale = zero_sigma && !h->lazy_clear && h->fwd_compact_allowed && h->deep && h->deep_compact &&
+                     h->sparse && h->full.wgt == nullptr && h->n_arcs < 6 * h->n && ng <= kDeepMaxGroups;
+    if (zero_sigma && !h->sigma_stale && !(h->sigma_clean && h->lazy_clear))
         CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, (size_t)h->alloc_groups * n * 32 * sizeof(double), st));
     h->sigma_clean = false;
+    h->batch_src_dev = src_dev;
+    h->batch_cnt = cnt;
     CUDA_TRY(h, cudaMemsetAsync(h->live, 0, (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
     init_state_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vis, h->lvl[0], n, cnt);
     seed_sources_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(src_dev, cnt, n, h->vis, h->lvl[0],
@@ -349,7 +356,31 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                                     cudaMemcpyHostToDevice, st));
         return BC_OK;
     };
-    bool compact_started = false;
+    // Level-ordered path counts (deep graphs).  The sweep starts in compact mode when level 1 is a
+    // thin level the persistent kernel takes; it leaves it (values written back into the rows,
+    // every level so far marked row-based) the first time a level has to go through a kernel
+    // that works on rows.
+    bool compact_mode = false;
+    auto rows_from_values = [&]() -> int {      // compact -> row layout for everything produced so far
+        CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, G * (size_t)n * 32 * sizeof(double), st));
+        decompact_sigma_kernel<<<dim3(1184, ng), 256, 0, st>>>(queue_params(h), h->q_off, h->qs, h->q_vcap, n,
+                                                               h->sigma);
+        vis_from_records_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vs, h->vis, n);
+        h->launches += 2;
+        CUDA_TRY(h, cudaGetLastError());
+        for (LevelRep &x : reps) x.compact = false;
+        compact_mode = false;
+        h->sigma_stale = false;
+        return BC_OK;
+    };
+    auto rows_for_level0 = [&]() -> int {       // the sweep stays on rows: clear them now, re-plant the sources
+        CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, G * (size_t)n * 32 * sizeof(double), st));
+        source_sigma_kernel<<<(h->batch_cnt + 127) / 128, 128, 0, st>>>(h->batch_src_dev, h->batch_cnt, n, h->sigma);
+        ++h->launches;
+        CUDA_TRY(h, cudaGetLastError());
+        h->sigma_stale = false;
+        return BC_OK;
+    };
     bool pulled = false;    // a pull level has run (the frontier is past its peak)
     int device_level = -1;  // level whose ranges sit in d_qbeg / d_qend (and d_qlbeg = q_count)
     int next_slot = 1;
@@ -402,7 +433,95 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 TRY(upload_lbeg());
             }
             const bool thin = prev.farcs <= kThinDegree * prev.nverts;
-            if (thin && h->deep && ng <= kDeepMaxGroups && prev.maxdeg <= (unsigned long long)kHeavyDeg) {
+            const bool deep_run = thin && h->deep && ng <= kDeepMaxGroups &&
+                                  prev.maxdeg <= (unsigned long long)kHeavyDeg;
+            if (L == 1 && deep_run && h->sigma_stale) TRY(ensure_deep(h));
+            if (L == 1 && deep_run && h->sigma_stale && ensure_deep_compact(h) && h->deep_grid_fc > 0) {
+                // level 0 in level order: one path per source lane
+                compact_init_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vs, n, cnt);
+                compact_level0_kernel<<<ng, 32, 0, st>>>(queue_params(h), h->q_off, h->qs, h->q_vcap, h->v_count,
+                                                         h->vs, n);
+                h->launches += 2;
+                reps[0].compact = true;
+                compact_mode = true;
+            } else if (L == 1 && h->sigma_stale) {
+                TRY(rows_for_level0());
+            }
+            if (compact_mode && !deep_run) TRY(rows_from_values());
+            if (deep_run && compact_mode) {
+                // ---- a run of thin levels over level-ordered path counts
+                TRY(ensure_deep(h));
+                TRY(ensure_live(h, L + kDeepLevels + 1));
+                DeepFwdCompactParams dp{};
+                dp.off = c.off;
+                dp.col = c.col;
+                dp.n = n;
+                dp.q = queue_params(h);
+                dp.q_beg = h->d_qbeg;
+                dp.q_end = h->d_qend;
+                dp.q_lbeg = h->d_qlbeg;
+                dp.vs = h->vs;
+                dp.qs = h->qs;
+                dp.q_off = h->q_off;
+                dp.q_arc = h->q_arc;
+                dp.v_count = h->v_count;
+                dp.vcap = h->q_vcap;
+                dp.live = h->live;
+                dp.counters = h->counters + h->cnt_off;
+                dp.lstat = h->lstat;
+                dp.log = h->deep_log;
+                dp.run_info = h->deep_info;
+                dp.ng = ng;
+                dp.G = (int)G;
+                dp.first_level = L;
+                dp.max_levels = kDeepLevels;
+                dp.graph_arcs = graph_arcs;
+                dp.push_beta = beta;
+                dp.thin_degree = kThinDegree;
+                dp.max_degree = kHeavyDeg;
+                if (seeds) dp.seeds = *seeds;
+                dp.seed_room = (unsigned long long)seed_room;
+                void *args[] = {&dp};
+                CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_compact_kernel, dim3(h->deep_grid_fc),
+                                                        dim3(kDeepThreads), args, 0, st));
+                ++h->launches;
+                int info[2] = {0, 0};
+                CUDA_TRY(h, cudaMemcpyAsync(info, h->deep_info, sizeof info, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaStreamSynchronize(st));
+                const int done = info[0];
+                if (done < 1 || done > kDeepLevels)
+                    return h->fail(BC_ERR_INTERNAL, "persistent forward sweep returned no level");
+                const size_t rw = 3 + 2 * G;
+                std::vector<unsigned long long> log((size_t)done * rw);
+                CUDA_TRY(h, cudaMemcpyAsync(log.data(), h->deep_log, log.size() * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(h, cudaStreamSynchronize(st));
+                reps.pop_back();  // `cur` is re-created below, level by level
+                for (int j = 0; j < done; ++j) {
+                    const unsigned long long *rep = log.data() + (size_t)j * rw;
+                    bool alive = false;
+                    for (int g = 0; g < ng; ++g) alive |= rep[3 + G + g] != 0;
+                    if (!alive) {
+                        *depth_out = L + j;
+                        return BC_OK;
+                    }
+                    reps.emplace_back();
+                    LevelRep &lr = reps.back();
+                    lr.queued = true;
+                    lr.qb.assign(qcount.begin(), qcount.begin() + ng);
+                    for (size_t g = 0; g < G; ++g) qcount[g] = rep[3 + g];
+                    lr.qe.assign(qcount.begin(), qcount.begin() + ng);
+                    lr.nverts = rep[0];
+                    lr.farcs = rep[1];
+                    lr.maxdeg = rep[2];
+                    lr.heavy = rep[2] > (unsigned long long)kHeavyDeg ? -1 : 0;
+                    lr.compact = true;
+                }
+                L += done - 1;
+                device_level = L;
+                continue;
+            }
+            if (deep_run) {
                 // ---- a run of thin levels inside one cooperative launch
                 TRY(ensure_deep(h));
                 TRY(ensure_live(h, L + kDeepLevels + 1));
@@ -432,16 +551,6 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 dp.max_degree = kHeavyDeg;
                 if (seeds) dp.seeds = *seeds;
                 dp.seed_room = (unsigned long long)seed_room;
-                if (ensure_deep_compact(h)) {
-                    if (!compact_started) {   // value slots are handed out per batch
-                        CUDA_TRY(h, cudaMemsetAsync(h->v_count, 0, G * sizeof(unsigned long long), st));
-                        compact_started = true;
-                    }
-                    dp.qs = h->qs;
-                    dp.q_off = h->q_off;
-                    dp.v_count = h->v_count;
-                    dp.vcap = h->q_vcap;
-                }
                 void *args[] = {&dp};
                 CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_kernel, dim3(h->deep_grid_f),
                                                         dim3(kDeepThreads), args, 0, st));
@@ -476,7 +585,6 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                     lr.farcs = rep[1];
                     lr.maxdeg = rep[2];
                     lr.heavy = rep[2] > (unsigned long long)kHeavyDeg ? -1 : 0;   // no records built in there
-                    lr.compact = dp.qs != nullptr;
                 }
                 L += done - 1;
                 device_level = L;
@@ -512,6 +620,8 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
             cur.qb.assign(qcount.begin(), qcount.begin() + ng);
             device_level = L;
         } else {
+            if (L == 1 && h->sigma_stale) TRY(rows_for_level0());
+            if (compact_mode) TRY(rows_from_values());
             const uint32_t *nbr;
             if (prev.slot >= 0) nbr = h->lvl[prev.slot];
             else {
@@ -597,6 +707,18 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
                        x.farcs * (unsigned long long)h->push_beta <= graph_arcs &&
                        x.farcs <= kThinDegree * x.nverts;
         }
+        bool any_compact = false;
+        for (int L = 0; L < depth; ++L) any_compact |= reps[L].compact;
+        if (any_compact && !all_thin) {
+            // the forward sweep ran on level-ordered values but this sweep works on rows
+            CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, G * (size_t)h->n * 32 * sizeof(double), st));
+            decompact_sigma_kernel<<<dim3(1184, ng), 256, 0, st>>>(queue_params(h), h->q_off, h->qs, h->q_vcap,
+                                                                   h->n, h->sigma);
+            ++h->launches;
+            CUDA_TRY(h, cudaGetLastError());
+            for (LevelRep &x : reps) x.compact = false;
+            h->sigma_stale = false;
+        }
         if (all_thin) {
             TRY(ensure_deep(h));
             DeepBwdCompactParams dp{};
@@ -615,8 +737,7 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             dp.G = (int)G;
             dp.hi = depth - 1;
             dp.lo = last;
-            dp.scr0 = scr[0];
-            dp.scr1 = scr[1];
+            dp.vs = h->vs;
             void *args[] = {&dp};
             CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_compact_kernel, dim3(h->deep_grid_c),
                                                     dim3(kDeepThreads), args, 0, st));
