@@ -361,7 +361,9 @@ def north_star_block(check: int = 8):
     groups = default_groups(g, len(srcs))
     with Engine(g) as e:
         e.set_option("groups", groups)
-        e.run(srcs[:32 * groups])
+        e.set_option("model_counters", 1)
+        _, model = e.run(srcs)                      # untimed: warm-up + byte-model counters
+        e.set_option("model_counters", 0)
         bc, st = e.run(srcs)
         bcs, _ = e.run(sample)
     obc, info = O.brandes_bc(g, sample)
@@ -369,7 +371,8 @@ def north_star_block(check: int = 8):
     return {"workload": label, "n": g.num_vertices, "m": g.num_edges, "sources": len(srcs), "groups": groups,
             "ms": st["ms_total"], "teps": g.num_edges * len(srcs) / st["ms_total"] * 1e3,
             "levels": int(st["max_levels"]), "launches": int(st["launches"]), "graph_build_s": t_build,
-            "level_kernel_ms": st["ms_level"], "level_model_bytes": int(st["level_model_bytes"]),
+            "level_kernel_ms": st["ms_level"], "level_model_bytes": int(model["level_model_bytes"]),
+            "level_kernel_model_gbs": model["level_model_bytes"] / max(st["ms_level"], 1e-9) / 1e6,
             "parity_sources": len(sample), "bc_rel_vs_oracle": err, "parity": bool(err <= 1e-9),
             "oracle_sigma_max": info["sigma_max"]}
 
@@ -539,14 +542,18 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         st = step()
+    # one untimed step with the byte-model counters on (the forward pulls then count the arcs they
+    # scan: one more atomic per work item, so the timed steps run without it)
+    eng.set_option("model_counters", 1)
+    model = step()
+    eng.set_option("model_counters", 0)
     sampler = ClockSampler(local)
     barrier()
     if rank == 0:
         sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     keys = ("ms_forward", "ms_backward", "launches", "launches_forward", "launches_backward", "launches_level",
-            "ms_level", "launches_level_timed", "level_model_bytes", "level_scan_arcs", "level_pairs",
-            "level_vertex_lanes", "level_dense_words", "level_entries")
+            "ms_level", "launches_level_timed")
     acc = {k: 0.0 for k in keys}
     ev0.record(stream)
     for _ in range(args.steps):
@@ -600,7 +607,7 @@ def run_ours(args):
     lvl_ms = acc["ms_level"] / steps
     lvl_n = acc["launches_level_timed"] / steps
     lvl_avg = lvl_ms / max(lvl_n, 1)
-    model_per_launch = acc["level_model_bytes"] / max(acc["launches_level"], 1)
+    model_per_launch = model["level_model_bytes"] / max(model["launches_level"], 1)
     achieved = model_per_launch / max(lvl_avg, 1e-9) / 1e6
     fwd_b, bwd_b, init_b = per_source_bytes(st, n)
     roofline = {
@@ -612,8 +619,8 @@ def run_ours(args):
                  "4 B per dense mask word swept, 16 B of BC partial per backward entry, 8 B of row offsets per vertex",
         "bytes_per_launch": model_per_launch, "avg_launch_ms": lvl_avg, "launches_per_step": lvl_n,
         "ms_per_step": lvl_ms, "share_of_step": lvl_ms / (ms_total / steps),
-        "components_per_step": {k: acc[k] / steps for k in ("level_scan_arcs", "level_pairs", "level_vertex_lanes",
-                                                             "level_dense_words", "level_entries")},
+        "components_per_step": {k: model[k] for k in ("level_scan_arcs", "level_pairs", "level_vertex_lanes",
+                                                       "level_dense_words", "level_entries")},
         "dram_bytes_per_launch": traffic,
         "dram_achieved": (traffic / (lvl_avg / 1e3) / 1e9) if traffic and lvl_avg > 0 else None,
         "dram_frac": (traffic / (lvl_avg / 1e3) / 1e9 / peak) if traffic and lvl_avg > 0 else None,

@@ -84,7 +84,8 @@ typedef struct bc_stats {
     int64_t level_vertex_lanes; /* fp64 values read or written per (vertex, lane), 8 B each          */
     int64_t level_dense_words;  /* level / visited mask words swept per (vertex, group), 4 B each    */
     int64_t level_entries;      /* (vertex, group) entries of the backward launches: 16 B BC partial */
-    int64_t level_model_bytes;  /* the sum in bytes, plus 8 B of row offsets per vertex and launch   */
+    int64_t level_model_bytes;  /* the sum in bytes, plus 8 B of row offsets per vertex and launch; 0
+                                   unless option "model_counters" is on (one more atomic per work item) */
     int64_t lookahead_batches;  /* batches whose Step 1 ran ahead, beside the previous border phase  */
 } bc_stats;
 
@@ -112,6 +113,11 @@ int bc_set_weights(bc_handle *h, const int32_t *weights);
  * BC_MODE_HYBIR issues Step 1 of the next source batch on a second stream while
  * the border phase of the current batch runs (`pipeline_sources`, engine.py:135-143,
  * 156-161); "l2_fetch": 32 / 64 / 128, L2 fill granularity of the device;
+ * "model_counters": 1 = the forward pulls count the arcs they scan, which completes
+ * bc_stats.level_model_bytes (bench.py turns it on for one untimed step);
+ * "deep_compact": 1 (default) = deep (road-like) graphs sweep over level-ordered path
+ * counts with one atomically updated BC vector per batch, 2 = same with per-group BC
+ * partials, 0 = row layout everywhere;
  * "push_beta", "push_beta_late", "reorder": see csrc/bc_engine.cu). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);
 

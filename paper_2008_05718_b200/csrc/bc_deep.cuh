@@ -175,6 +175,14 @@ __global__ void border_table_queue_kernel(QueueParams q, const int64_t *level_en
     }
 }
 
+// resident blocks per SM the compact sweeps ask the compiler for (register cap = 65536 / (256 * blocks)):
+// they are bound by the latency of random memory accesses, so more resident warps = more of them in flight
+#ifndef BC_DEEP_MIN_BLOCKS_F
+#define BC_DEEP_MIN_BLOCKS_F 4
+#endif
+#ifndef BC_DEEP_MIN_BLOCKS_B
+#define BC_DEEP_MIN_BLOCKS_B 4
+#endif
 constexpr int kDeepThreads = 256;
 constexpr int kDeepWarps = kDeepThreads / 32;
 constexpr int kDeepMaxGroups = 128;   // groups per batch the persistent sweeps accept
@@ -466,7 +474,7 @@ struct DeepFwdCompactParams {
     unsigned long long seed_room;
 };
 
-__global__ void __launch_bounds__(kDeepThreads) deep_forward_compact_kernel(const DeepFwdCompactParams p) {
+__global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forward_compact_kernel(const DeepFwdCompactParams p) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int32_t stage[kDeepWarps][kStage];
     __shared__ int64_t s_pref[kDeepMaxGroups + 1];
@@ -955,7 +963,7 @@ struct DeepBwdCompactParams {
     VertexState *vs;             // [G][n] (pos field)
 };
 
-__global__ void __launch_bounds__(kDeepThreads) deep_backward_compact_kernel(const DeepBwdCompactParams p) {
+__global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backward_compact_kernel(const DeepBwdCompactParams p) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int64_t s_pref[kDeepMaxGroups + 1];
     __shared__ uint32_t s_cb[kDeepMaxGroups], s_ce[kDeepMaxGroups];   // entry range (+1) of the level below

@@ -193,6 +193,10 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         h->deep = value ? 1 : 0;
         return BC_OK;
     }
+    if (k == "model_counters") {
+        h->model_counters = value ? 1 : 0;
+        return BC_OK;
+    }
     if (k == "deep_compact") {
         // 0: row layout everywhere; 1 (default): deep graphs sweep backward over level-ordered
         // values with one atomically-updated BC vector; 2: same, BC kept in per-group partials

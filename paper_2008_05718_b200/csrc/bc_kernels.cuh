@@ -83,6 +83,7 @@ struct LevelParams {
     unsigned long long *lstat;     // forward: [0] vertices discovered, [1] their arcs, [2] largest degree,
                                    // [4] arcs scanned by this launch (byte model of the roofline); may be null
     int accumulate_bc;
+    int count_scan;   // forward: add the arcs scanned into lstat[4] (one more atomic per item: off on timed runs)
     // forward sweeps of low-degree (deep) graphs without frontier queues: only vertices with a
     // neighbour in the previous level are scanned (mark_candidates_kernel); nullptr = scan all
     uint8_t *cand;   // [group][v]
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         if (!BWD) {
             const unsigned t = __reduce_add_sync(kFull, c_t);
             if (lane == 0 && t) atomicAdd(p.counters + 2, (unsigned long long)t);
-            if (lane == 0 && p.lstat != nullptr && want != 0 && nbr != nullptr)
+            if (lane == 0 && p.count_scan && p.lstat != nullptr && want != 0 && nbr != nullptr)
                 atomicAdd(p.lstat + 4, (unsigned long long)(p.chk_a1[item] - p.chk_a0[item]));
         }
     } else {
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BWD ? BC_MIN_BLOCKS_BWD :
         if (WEIGHTED) wp.wgt += a0;
         uint32_t mygot = 0;  // forward: what this lane's vertex discovered
         unsigned need = __ballot_sync(kFull, mine != 0 && (BWD || deg > 0));
-        if (!BWD && p.lstat != nullptr && need != 0 && nbr != nullptr) {
+        if (!BWD && p.count_scan && p.lstat != nullptr && need != 0 && nbr != nullptr) {
             // arcs this item scans (one col_idx word + one mask probe each): byte model of the roofline
             const unsigned c_scan = __reduce_add_sync(kFull, (mine != 0) ? (unsigned)deg : 0u);
             if (lane == 0) atomicAdd(p.lstat + 4, (unsigned long long)c_scan);

@@ -496,9 +496,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         // col_idx word + mask probe per scanned arc; one fp64 per gathered pair and per
         // (vertex, lane) value; 4 B per dense mask word; 16 B of BC partial per backward entry;
         // row offsets once per launch
-        stats->level_model_bytes = 8 * h->model_scan + 8 * h->model_pairs + 8 * h->model_vlanes +
-                                   4 * h->model_dense_words + 16 * h->model_entries +
-                                   8 * h->n * stats->launches_level;
+        // (complete only with option model_counters = 1: the forward pulls count their scanned arcs then)
+        stats->level_model_bytes = h->model_counters
+                                       ? 8 * h->model_scan + 8 * h->model_pairs + 8 * h->model_vlanes +
+                                             4 * h->model_dense_words + 16 * h->model_entries +
+                                             8 * h->n * stats->launches_level
+                                       : 0;
     }
     return BC_OK;
 }

@@ -294,6 +294,7 @@ struct bc_handle {
     int64_t level_launches = 0;   // dense level kernel only
     // batched byte model of the dense level-kernel launches of the current call
     int64_t model_scan = 0, model_pairs = 0, model_vlanes = 0, model_dense_words = 0, model_entries = 0;
+    int model_counters = 0;   // option: count the arcs the forward pulls scan (level_model_bytes is complete)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> level_events;   // around those launches (<= 512 per call)
 
     int fail(int code, const std::string &msg) {
@@ -737,6 +738,7 @@ LevelParams level_params(bc_handle *h, const Csr &c) {
     p.pacc = h->pacc;
     p.pmask = h->pmask;
     p.counters = h->counters + h->cnt_off;
+    p.count_scan = h->model_counters;
     p.wgt = c.wgt;
     p.cand = nullptr;
     p.lvl_ptrs = h->d_lvl_ptrs;

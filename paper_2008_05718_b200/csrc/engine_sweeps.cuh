@@ -28,6 +28,7 @@ int launch_forward(bc_handle *h, const Csr &c, int L, int ng, cudaStream_t st,
     if (h->dist_rank >= 0 && lstat == nullptr) {
         // graph-partitioned runs: running totals for the byte model (bc_dist_get_stats)
         p.lstat = h->lstat;
+        p.count_scan = 1;
         h->model_dense_words += 2 * c.n * ng;
     }
     p.live_prev = h->live + (size_t)(L - 1) * h->alloc_groups;

@@ -1,0 +1,18 @@
+#!/bin/bash
+# One GPU-box session of round 2: tests, smoke, bench (both arms), ncu of the compact deep kernels, full-size records.
+set -x
+mkdir -p gpurun_out
+T=/tmp/r2prof; mkdir -p $T
+timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -6 | tee gpurun_out/pytest_gpu_final.log
+python __graft_entry__.py --smoke 2>&1 | tail -3 | tee gpurun_out/smoke.log
+python bench.py 2> gpurun_out/bench.err | tee gpurun_out/bench.json
+python bench.py --impl reference --steps 2 --warmup 1 2>> gpurun_out/bench.err | tee gpurun_out/bench_ref.json
+tail -5 gpurun_out/bench.err
+timeout 900 ncu --set full --clock-control none -k regex:deep_forward_compact -c 2 -o $T/r2_deep_fc -f \
+    python tools/road_probe.py 2048 128 4 > gpurun_out/ncu_deep_fc.log 2>&1
+ncu -i $T/r2_deep_fc.ncu-rep --page raw --csv > gpurun_out/r2_deep_forward_compact.raw.csv
+timeout 900 ncu --set full --clock-control none -k regex:deep_backward_compact -c 1 -o $T/r2_deep_bc -f \
+    python tools/road_probe.py 2048 128 4 > gpurun_out/ncu_deep_bc.log 2>&1
+ncu -i $T/r2_deep_bc.ncu-rep --page raw --csv > gpurun_out/r2_deep_backward_compact.raw.csv
+timeout 2400 python tools/fullsize.py c1 rmat22 er22 road2048 road2048_hybir rmat24 2>&1 | grep "^{" | tee gpurun_out/r2_fullsize.jsonl
+du -sh gpurun_out
