@@ -1,9 +1,9 @@
 """CPU oracle -- TEST INFRASTRUCTURE, NOT PRODUCT CODE.
 
 ctypes front end of ``oracle/liboracle.so`` (built from ``brandes_oracle.c``
-by ``make -C oracle`` or ``__graft_entry__.build()``), plus ``hybir_port.py``,
-a numpy restatement of the reference's partitioned (border-matrix) forward
-phase.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+by ``make -C oracle`` or ``__graft_entry__.build()``).  The partitioned
+(border-matrix) phases have no port here: they are pinned by golden vectors the
+reference itself produced (``tests/golden/``).  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 ``cpu_baseline`` / ``--impl reference`` legs may import this package; nothing
 under ``paper_2008_05718_b200/`` does.
 

@@ -576,11 +576,23 @@ __global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups)
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
-        for (int g = 0; g < groups; ++g) {
-            s += bcg[(size_t)g * n + v];
-            bcg[(size_t)g * n + v] = 0.0;
+        int g = 0;
+        for (; g + 4 <= groups; g += 4) {     // four loads in flight, added in group order
+            double x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = bcg[(size_t)(g + k) * n + v];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                s += x[k];
+                if (x[k] != 0.0) bcg[(size_t)(g + k) * n + v] = 0.0;
+            }
         }
-        bc[v] += s;
+        for (; g < groups; ++g) {
+            const double x = bcg[(size_t)g * n + v];
+            s += x;
+            if (x != 0.0) bcg[(size_t)g * n + v] = 0.0;
+        }
+        if (s != 0.0) bc[v] += s;
     }
 }
 

@@ -429,7 +429,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         }
     }
     if (!debug && bc_dev != nullptr) {
-        reduce_bc_kernel<<<grid1d((size_t)n, 256, 1184), 256, 0, st>>>(bc_dev, h->bcg, n, h->alloc_groups);
+        // (groups beyond the ones this run used hold zeros)
+        reduce_bc_kernel<<<grid1d((size_t)n, 256, 4736), 256, 0, st>>>(bc_dev, h->bcg, n, groups);
         ++h->launches;
         CUDA_TRY(h, cudaGetLastError());
         h->bcg_dirty = false;

@@ -51,7 +51,9 @@ class Graph:
     # -- reference-compatible views (graph.py:21-61) ----------------------
     @property
     def num_arcs(self) -> int:
-        return 2 * self.num_edges
+        # = 2 * num_edges for a normalised graph; a rank-local view (rows of one part only,
+        # partitioned.py) holds every cut arc once, so count what is stored
+        return int(len(self.col_idx))
 
     @property
     def unit_weight(self) -> bool:

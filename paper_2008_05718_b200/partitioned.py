@@ -53,9 +53,7 @@ def local_rows(g: Graph, assignment, rank: int) -> Graph:
     np.cumsum(deg, out=offsets[1:])
     keep = np.repeat(own, np.diff(g.offsets))
     col = g.col_idx[keep]
-    out = Graph(g.num_vertices, len(col) // 2, offsets, col)
-    out.num_arcs_exact = int(len(col))
-    return out
+    return Graph(g.num_vertices, len(col) // 2, offsets, col)
 
 
 class LocalGraph:
@@ -127,11 +125,6 @@ class LocalGraph:
         if len(cs):
             np.cumsum(np.bincount(pos, minlength=len(mine)), out=self.cut_off[1:])
         self.cut_dst = local_of[cd].astype(np.int32)
-
-    def local_sources(self, sources):
-        """Local ids of a batch's sources (-1: neither owned nor in the halo) and their parts."""
-        s = np.asarray(sources, dtype=np.int64)
-        return self.local_of[s], None
 
 
 def local_graph(g: Graph, part: Partition, rank: int, bs=None) -> LocalGraph:

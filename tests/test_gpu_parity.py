@@ -315,6 +315,42 @@ def test_level_ordered_backward_of_deep_graphs():
     assert np.allclose(res[1], O.brandes_bc(g, srcs)[0], rtol=RTOL, atol=ATOL)
 
 
+def test_level_ordered_sweeps_edge_cases():
+    """Level-ordered deep sweeps with awkward source lists: duplicates (two lanes of one group on
+    the same vertex), isolated sources, sources in different components, a single source, none."""
+    from paper_2008_05718_b200 import from_edge_arrays
+    base = G.road_like(64, 64, keep=0.2, seed=7)
+    # two disjoint copies + a few isolated vertices
+    n0 = base.num_vertices
+    und = base.arc_src < base.arc_dst
+    u = np.concatenate([base.arc_src[und], base.arc_src[und] + n0])
+    v = np.concatenate([base.arc_dst[und], base.arc_dst[und] + n0])
+    g = from_edge_arrays(2 * n0 + 5, u, v)
+    iso = 2 * n0 + 2
+    for srcs in ([5, 5, 900, n0 + 17, iso, 5, 4000, n0 + 4000, iso, 77],
+                 [123], [iso], [], list(range(0, 2 * n0, 257)) + [iso]):
+        obc, _ = O.brandes_bc(g, srcs)
+        for mode in (1, 0):
+            with Engine(g) as e:
+                e.set_option("groups", 2)
+                e.set_option("deep_compact", mode)
+                bc, st = e.run(srcs)
+            assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL), (srcs[:4], mode)
+            assert st["sources"] == len(srcs)
+    # the same through the partitioned mode (isolated and duplicate sources keep their lanes there)
+    part = P.Partition((np.arange(g.num_vertices) >= n0).astype(np.int32), 0.5, 2)   # no cut edges at all
+    strips = P.Partition(((np.arange(g.num_vertices) % n0) // (n0 // 2) % 2).astype(np.int32), 0.5, 2)
+    srcs = [5, 5, 900, n0 + 17, iso, 4000, n0 + 4000, 77]
+    obc, _ = O.brandes_bc(g, srcs)
+    for p in (part, strips):
+        with Engine(g) as e:
+            e.set_option("groups", 1)
+            e.set_option("reports", 0)
+            e.set_partition(2, p.assignment)
+            bc, _ = e.run(srcs, MODE_HYBIR)
+        assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+
+
 def test_path_counts_beyond_2_53_against_the_bigint_reference():
     """sigma above 2^53 (SURVEY.md hard part 1) pinned to the reference's exact-integer oracle
     (golden vectors of tests/golden/gen_golden_bigsigma.py, 40 x 32 lattice, max sigma 2^66):
