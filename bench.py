@@ -410,7 +410,17 @@ def run_partitioned(args):
         part = P.refine_partition(g, P.grow_partition(g, world, seed=0))
     else:
         part = P.block_partition(g, world)
-    runner = PartitionedRunner(g, part, dev, args.groups or 4, args.forward)
+    # the border-matrix forward phase needs every part's b_p x b_p table on every rank: above the
+    # budget (R-MAT: ~57 % of the vertices are borders) the run takes the level-synchronous forward
+    # phase, as run_bc does
+    forward = args.forward
+    if forward == "hybir":
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            if P.choose_mode("hybir", P.identify_borders(g, part), 64e9) != "hybir":
+                forward = "bsp"
+    runner = PartitionedRunner(g, part, dev, args.groups or 4, forward)
     for _ in range(args.warmup):
         runner.run(sources)
     runner.reset_counters()
@@ -433,7 +443,7 @@ def run_partitioned(args):
     counters = runner.counters()
     # ---- end to end through the public call: host CSR in, host BC vector out on every rank
     runner.close()
-    cfg = P.RunConfig(sources=sources, mode="hybir" if args.forward == "hybir" else "bsp-baseline",
+    cfg = P.RunConfig(sources=sources, mode="hybir" if forward == "hybir" else "bsp-baseline",
                       num_gpus=world, gpu_mode="graph-partitioned", partition=part, device=local,
                       groups=args.groups or 4, per_source_reports=False)
     dist.barrier()
@@ -464,7 +474,7 @@ def run_partitioned(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "n": n, "m": m, "sources": len(sources), "mode": "graph-partitioned",
-                   "forward": args.forward, "partitioner": "strips" if args.workload.startswith("road") else args.partitioner,
+                   "forward": forward, "forward_requested": args.forward, "partitioner": "strips" if args.workload.startswith("road") else args.partitioner,
                    "borders": runner.border_counts, "levels": runner.levels,
                    "state_vertices_per_rank": runner.local_n, "owned_vertices_rank0": own,
                    "forward_exchanges_per_step": counters["forward_exchanges"] / steps_all,
