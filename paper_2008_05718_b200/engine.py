@@ -167,10 +167,12 @@ def default_groups(g: Graph, n_sources: int) -> int:
     """Source groups per batch: enough lanes to fill the GPU on small graphs,
     few enough that one group's sigma slab stays L2-friendly on large ones."""
     want = max(1, (n_sources + 31) // 32)
-    # batch state out of 180 GB HBM: ~64 GB on shallow (high-degree) graphs, ~24 GB on low-degree
-    # ones, whose sweeps keep one mask array per level on top of it
+    # batch state out of 180 GB HBM: ~64 GB on shallow (high-degree) graphs at 600 B per vertex and
+    # group (sigma + coef rows, masks); low-degree (deep) graphs sweep on frontier queues over
+    # level-ordered values on top of the rows -- ~1,400 B per vertex and group, ~96 GB
     shallow = g.num_arcs >= 8 * g.num_vertices
-    budget = max(1, int((64e9 if shallow else 24e9) // max(1, g.num_vertices * 600)))
+    budget = max(1, int(64e9 // max(1, g.num_vertices * 600)) if shallow
+                 else int(96e9 // max(1, g.num_vertices * 1400)))
     cap = min(budget, 32 if g.num_arcs >= 8_000_000 else 128)
     batches = (want + cap - 1) // cap
     return max(1, (want + batches - 1) // batches)               # batches of equal size
