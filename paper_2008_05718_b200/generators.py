@@ -23,14 +23,19 @@ def rmat_edges(scale: int, edge_factor: int, seed: int = 1, a=0.57, b=0.19, c=0.
     rng = np.random.default_rng(seed)
     n = 1 << scale
     m = n * edge_factor
-    u = np.zeros(m, dtype=np.int64)
-    v = np.zeros(m, dtype=np.int64)
+    if scale > 31:
+        raise ValueError("R-MAT scale above 31 is not supported")
+    # endpoint bits are collected in 32-bit words (half the memory traffic of int64)
+    u = np.zeros(m, dtype=np.uint32)
+    v = np.zeros(m, dtype=np.uint32)
+    r = np.empty(m, dtype=np.float64)
     for bit in range(scale):
-        r = rng.random(m)
+        rng.random(m, out=r)                       # (same stream as rng.random(m))
         ub = r >= a + b
         vb = ((r >= a) & (r < a + b)) | (r >= a + b + c)
-        u |= ub.astype(np.int64) << bit
-        v |= vb.astype(np.int64) << bit
+        u |= ub.astype(np.uint32) << np.uint32(bit)
+        v |= vb.astype(np.uint32) << np.uint32(bit)
+    u, v = u.astype(np.int64), v.astype(np.int64)
     return n, u, v
 
 
