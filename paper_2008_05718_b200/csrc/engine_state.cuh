@@ -585,6 +585,8 @@ int ensure_queues(bc_handle *h) {
     TRY(dev_alloc(h, &h->scrB, G * n));
     TRY(dev_alloc(h, &h->lstat, (size_t)8));
     TRY(dev_alloc(h, &h->report, 8 + 2 * G));
+    CUDA_TRY(h, cudaMemset(h->report, 0, (8 + 2 * G) * sizeof(unsigned long long)));
+    CUDA_TRY(h, cudaMemset(h->lstat, 0, 8 * sizeof(unsigned long long)));
     h->heavy_cap = (int64_t)G * std::max(h->full.heavy_slices, h->intra.heavy_slices) + 1;
     TRY(dev_alloc(h, &h->heavy, (size_t)h->heavy_cap));
     CUDA_TRY(h, cudaMemset(h->scrA, 0, G * n * sizeof(uint32_t)));
@@ -658,6 +660,10 @@ bool ensure_deep_compact(bc_handle *h) {
     }
     cudaMemset(h->v_count, 0, G * sizeof(unsigned long long));
     cudaMemset(h->bc_acc, 0, (size_t)h->n * sizeof(double));
+    // (entries of the last level never become a frontier: their arc words are copied, unwritten,
+    // when the queues grow)
+    cudaMemset(h->q_off, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
+    cudaMemset(h->q_arc, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
     h->q_vcap = vcap;
     return true;
 }
@@ -688,6 +694,7 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
         if (*arr == nullptr) continue;
         uint32_t *no = nullptr;
         CUDA_TRY(h, arena_malloc((void **)&no, G * (size_t)cap * sizeof(uint32_t)));
+        CUDA_TRY(h, cudaMemset(no, 0, G * (size_t)cap * sizeof(uint32_t)));
         for (size_t g = 0; g < G; ++g) {
             const size_t keep = (size_t)std::min<int64_t>(g < used.size() ? (int64_t)used[g] : 0, h->q_cap);
             if (keep == 0) continue;

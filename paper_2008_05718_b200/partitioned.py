@@ -251,18 +251,18 @@ class PartitionedRunner:
                     self.eng.dist_hybir_set_table(p, bm.data_ptr(), sm.data_ptr())
                 torch.cuda.synchronize(device)
             cnt = self.eng.dist_hybir_seed_count()
-            self.seed_d = torch.empty(max(cnt, 1), dtype=torch.int32, device=device)
-            self.seed_s = torch.empty(max(cnt, 1), dtype=torch.float64, device=device)
+            self.seed_d = torch.zeros(max(cnt, 1), dtype=torch.int32, device=device)
+            self.seed_s = torch.zeros(max(cnt, 1), dtype=torch.float64, device=device)
         self.max_nb = max(self.border_counts + [1])
         self.stream = 0     # default stream: kernels, packs / unpacks and collectives stay ordered
         # forward (bsp) exchange buffers, grown on demand and kept
         self._masks = torch.zeros(self.max_nb * groups, dtype=torch.int32, device=device)
         self._all_masks = torch.zeros(self.world * self.max_nb * groups, dtype=torch.int32, device=device)
-        self._values = torch.empty(max(self.max_nb * groups * 32, 1), dtype=torch.float64, device=device)
-        self._all_values = torch.empty(1, dtype=torch.float64, device=device)
+        self._values = torch.zeros(max(self.max_nb * groups * 32, 1), dtype=torch.float64, device=device)
+        self._all_values = torch.zeros(1, dtype=torch.float64, device=device)
         # backward messages: [cap_values fp64][3 x cap_entries int32] as one int64 buffer
-        self._send = torch.empty(1, dtype=torch.int64, device=device)
-        self._recv = torch.empty(1, dtype=torch.int64, device=device)
+        self._send = torch.zeros(1, dtype=torch.int64, device=device)
+        self._recv = torch.zeros(1, dtype=torch.int64, device=device)
         self._counts = torch.zeros(1, dtype=torch.int64, device=device)
         self.levels = 0
         self.reset_counters()
@@ -287,8 +287,8 @@ class PartitionedRunner:
         self.eng.close()
 
     def _grown(self, t, count, dtype):
-        if t.numel() < count:
-            t = self.torch.empty(int(count), dtype=dtype, device=self.device)
+        if t.numel() < count:     # zero-filled: the padding of a message travels with it
+            t = self.torch.zeros(int(count), dtype=dtype, device=self.device)
         return t
 
     # -- forward -------------------------------------------------------------------------------
