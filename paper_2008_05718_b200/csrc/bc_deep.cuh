@@ -175,6 +175,31 @@ __global__ void border_table_queue_kernel(QueueParams q, const int64_t *level_en
     }
 }
 
+// s_pref[g] = sum over j < g of len(j) rounded up to whole warps, g = 0 .. ng (the flattened
+// (group, entry) space of a level: every group padded to a multiple of 32 so a warp never
+// straddles two groups).  One load per group and a two-stage scan instead of a serial loop per
+// thread; ng <= kDeepMaxGroups = 128, every thread of the 256-thread block calls it.
+template <typename LenFn>
+__device__ __forceinline__ void padded_prefix(int64_t *s_pref, int ng, LenFn len) {
+    __shared__ int64_t s_warp_total[4];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int64_t x = (t < ng) ? ((len(t) + 31) & ~(int64_t)31) : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (warp < 4 && lane == 31) s_warp_total[warp] = x;
+    __syncthreads();
+    if (t < ng) {
+        int64_t base = 0;
+        for (int w = 0; w < warp; ++w) base += s_warp_total[w];
+        s_pref[t + 1] = base + x;
+    }
+    if (t == 0) s_pref[0] = 0;
+    __syncthreads();
+}
+
 // resident blocks per SM the compact sweeps ask the compiler for (register cap = 65536 / (256 * blocks)):
 // they are bound by the latency of random memory accesses, so more resident warps = more of them in flight
 #ifndef BC_DEEP_MIN_BLOCKS_F
@@ -489,12 +514,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
     int *cont_flag = p.run_info + 1;
 
     auto frontier_prefix = [&]() {   // flattened (group, entry) space of the frontier, groups padded to warps
-        if (threadIdx.x <= p.ng) {
-            int64_t acc = 0;
-            for (int g = 0; g < (int)threadIdx.x; ++g) acc += (s_end[g] - s_beg[g] + 31) & ~(int64_t)31;
-            s_pref[threadIdx.x] = acc;
-        }
-        __syncthreads();
+        padded_prefix(s_pref, p.ng, [&](int g) { return s_end[g] - s_beg[g]; });
     };
 
     for (int it = 0;; ++it) {
@@ -594,15 +614,9 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
         grid.sync();
 
         // ---- phase A2: the entries appended above become level L
-        if (threadIdx.x <= p.ng) {
-            int64_t acc = 0;
-            for (int g = 0; g < (int)threadIdx.x; ++g)
-                acc += ((int64_t)p.q.q_count[g] - s_lbeg[g] + 31) & ~(int64_t)31;
-            s_pref[threadIdx.x] = acc;
-        }
         if (threadIdx.x < 8) s_stat[threadIdx.x] = 0ull;
         for (int k = threadIdx.x; k < p.ng; k += blockDim.x) s_live[k] = 0u;
-        __syncthreads();
+        padded_prefix(s_pref, p.ng, [&](int g) { return (int64_t)p.q.q_count[g] - s_lbeg[g]; });
         {
             const int64_t total = s_pref[p.ng];
             int g = 0;
@@ -975,16 +989,11 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
         const bool deepest = L == p.hi;
         const int64_t *beg_t = p.range_table + ((size_t)L * 2 + 0) * p.G;
         const int64_t *end_t = p.range_table + ((size_t)L * 2 + 1) * p.G;
-        if (threadIdx.x <= p.ng) {
-            int64_t acc = 0;
-            for (int g = 0; g < (int)threadIdx.x; ++g) acc += (end_t[g] - beg_t[g] + 31) & ~(int64_t)31;
-            s_pref[threadIdx.x] = acc;
-        }
         for (int k = threadIdx.x; k < p.ng; k += blockDim.x) {
             s_cb[k] = deepest ? 1u : (uint32_t)p.range_table[((size_t)(L + 1) * 2 + 0) * p.G + k] + 1u;
             s_ce[k] = deepest ? 0u : (uint32_t)p.range_table[((size_t)(L + 1) * 2 + 1) * p.G + k];
         }
-        __syncthreads();
+        padded_prefix(s_pref, p.ng, [&](int g) { return end_t[g] - beg_t[g]; });
         const int64_t total = s_pref[p.ng];
         int g = 0;
         for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
