@@ -254,6 +254,21 @@ int bc_dist_hybir_seeds(bc_handle *h, const int64_t *sources, const int32_t *sou
  * iterations summed over the batch's sources. */
 int bc_dist_hybir_forward(bc_handle *h, const int32_t *seed_dist_dev, const double *seed_sigma_dev,
                           int *depth_out, int64_t *iterations_out, void *stream);
+/* The same forward phase with ONE border table per rank (memory b_p^2 x 12 B instead of the sum
+ * over all parts; the min-plus closure and the composition of a part run on its owner only).
+ * bc_dist_hybir_shard_tables drops the other parts' tables after bc_dist_hybir_setup.  A batch is
+ * then driven step by step, the caller all-reducing the exchange buffers between the steps
+ * (xchg_values: B x 32 x groups int32 distances [MIN] in steps 1-2, fp64 path counts [MAX] in steps
+ * 4-5; xchg_flags: 32 x groups u32 "lane changed" words [MAX]):
+ *   0 begin refinement from the reduced seeds       1 refinement iteration -> exchange buffers
+ *   2 merged buffers -> state; *flag_out = some lane is still active (NULL: do not read back)
+ *   3 begin composition                              4 composition round -> exchange buffers
+ *   5 merged buffers -> state; *flag_out = some path count changed
+ *   6 Step 6 on this rank's part; *flag_out = levels seen by this rank */
+int bc_dist_hybir_shard_tables(bc_handle *h);
+int bc_dist_hybir_border_step(bc_handle *h, int step, void *xchg_values_dev, void *xchg_flags_dev,
+                              const int32_t *seed_dist_dev, const double *seed_sigma_dev, int *flag_out,
+                              void *stream);
 /* Extend this rank's level rows (empty) to the depth of the deepest rank. */
 int bc_dist_hybir_set_depth(bc_handle *h, int global_depth, void *stream);
 

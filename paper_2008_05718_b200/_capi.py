@@ -31,6 +31,7 @@ SYMBOLS = (
     "bc_dist_export", "bc_dist_import", "bc_dist_get_live", "bc_dist_set_live", "bc_dist_finish",
     "bc_dist_hybir_setup", "bc_dist_hybir_get_table", "bc_dist_hybir_set_table",
     "bc_dist_hybir_seed_count", "bc_dist_hybir_seeds", "bc_dist_hybir_forward", "bc_dist_hybir_set_depth",
+    "bc_dist_hybir_shard_tables", "bc_dist_hybir_border_step",
     "bc_last_error", "bc_destroy", "bc_release_cached_memory",
 )
 
@@ -138,6 +139,10 @@ def load():
     L.bc_dist_hybir_seeds.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     L.bc_dist_hybir_forward.restype = cint
     L.bc_dist_hybir_forward.argtypes = [vp, vp, vp, ctypes.POINTER(cint), ctypes.POINTER(i64), vp]
+    L.bc_dist_hybir_shard_tables.restype = cint
+    L.bc_dist_hybir_shard_tables.argtypes = [vp]
+    L.bc_dist_hybir_border_step.restype = cint
+    L.bc_dist_hybir_border_step.argtypes = [vp, cint, vp, vp, vp, vp, ctypes.POINTER(cint), vp]
     L.bc_dist_hybir_set_depth.restype = cint
     L.bc_dist_hybir_set_depth.argtypes = [vp, cint, vp]
     L.bc_last_error.restype = ctypes.c_char_p
@@ -402,6 +407,19 @@ class Engine:
                                                  ctypes.c_void_p(seed_sigma_ptr), ctypes.byref(depth),
                                                  ctypes.byref(iters), ctypes.c_void_p(stream or None)))
         return depth.value, iters.value
+
+    def dist_hybir_shard_tables(self):
+        self._ck(self._lib.bc_dist_hybir_shard_tables(self._h))
+
+    def dist_hybir_border_step(self, step, values_ptr=0, flags_ptr=0, seed_dist_ptr=0, seed_sigma_ptr=0,
+                               want_flag=False, stream=0):
+        """One step of the sharded-table border phase; returns the step's flag (or None)."""
+        flag = ctypes.c_int(0)
+        self._ck(self._lib.bc_dist_hybir_border_step(
+            self._h, int(step), ctypes.c_void_p(values_ptr or None), ctypes.c_void_p(flags_ptr or None),
+            ctypes.c_void_p(seed_dist_ptr or None), ctypes.c_void_p(seed_sigma_ptr or None),
+            ctypes.byref(flag) if want_flag else None, ctypes.c_void_p(stream or None)))
+        return flag.value if want_flag else None
 
     def dist_hybir_set_depth(self, depth, stream=0):
         self._ck(self._lib.bc_dist_hybir_set_depth(self._h, int(depth), ctypes.c_void_p(stream or None)))

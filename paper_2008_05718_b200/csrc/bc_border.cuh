@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
                                                            const int32_t *lane_part,
                                                            const uint32_t *lane_active, int which,
                                                            uint32_t *lane_changed,
-                                                           const uint32_t *rowflag) {
+                                                           const uint32_t *rowflag, int only_part = -1) {
     __shared__ __align__(16) int32_t sD[kTI][kTL];
     __shared__ __align__(16) int32_t sB[kTI][kTJ];
     const int p = blockIdx.z;
@@ -177,6 +177,16 @@ __global__ void __launch_bounds__(256) matrix_relax_kernel(BorderGeom geo, int S
     const int j0 = blockIdx.x * kTJ;
     if (j0 >= b) return;
     const int base = geo.part_off[p];
+    if (only_part >= 0 && p != only_part) {
+        // graph-partitioned runs with one table per rank: the closure of another part is its
+        // owner's work; its rows pass through (Din and Dout are swapped by the caller)
+        const int l0 = blockIdx.y * kTL;
+        for (int e = threadIdx.x; e < kTJ * kTL; e += blockDim.x) {
+            const int j = j0 + e / kTL, l = l0 + e % kTL;
+            if (j < b && l < S) Dout[(size_t)(base + j) * S + l] = Din[(size_t)(base + j) * S + l];
+        }
+        return;
+    }
     const int32_t *tab = bm + geo.tab_off[p];
     const int tl = threadIdx.x & 15, tj = threadIdx.x >> 4;   // 16 lane quads x 16 border quads
     const int lane4 = blockIdx.y * kTL + 4 * tl;              // first of this thread's 4 lanes
@@ -291,12 +301,13 @@ __global__ void __launch_bounds__(256) compose_sigma_kernel(
     BorderGeom geo, int S, const int32_t *D, const int32_t *seedD, const double *seedS,
     const double *darr, const int32_t *bm, const double *sm, const int32_t *lane_part,
     double *sig, const uint32_t *lane_run, uint32_t *lane_changed, int first_round,
-    const uint32_t *rowflag) {
+    const uint32_t *rowflag, int only_part = -1) {
     __shared__ __align__(16) int32_t sD[kTI][kTL];
     __shared__ __align__(16) double sA[kTI][kTL];
     __shared__ __align__(16) int32_t sB[kTI][kTJ];
     __shared__ __align__(16) double sS[kTI][kTJ];
     const int p = blockIdx.z;
+    if (only_part >= 0 && p != only_part) return;   // another rank composes that part's counts
     const int b = geo.part_off[p + 1] - geo.part_off[p];
     const int j0 = blockIdx.x * kTJ;
     if (j0 >= b) return;

@@ -521,6 +521,153 @@ int bc_dist_hybir_forward(bc_handle *h, const int32_t *seed_dist_dev, const doub
     return BC_OK;
 }
 
+// ---- the same forward phase with ONE border table per rank --------------------------------------
+// bc_dist_hybir_forward runs refinement and composition redundantly on every rank, which needs every
+// part's table everywhere and does not shrink with the number of GPUs.  With sharded tables a rank
+// closes / composes its own part only, and the border state is merged after every iteration:
+//   refinement : cut-arc relaxation for all borders (cheap, replicated), min-plus closure of the
+//                rank's own part, then all-reduce MIN of the border distances [B][S] and MAX of
+//                the per-lane "changed" words;
+//   composition: arrival counts for all borders (cheap, replicated), composition for the own
+//                part, then all-reduce MAX of the path counts (they only grow) and of "changed".
+// The collectives are the caller's (torch.distributed on exchange buffers it owns); the steps:
+//   0 begin refinement (seeds already reduced)   1 refinement: compute -> exchange buffers
+//   2 refinement: merged buffers -> state, lane step (flag = a lane is still active)
+//   3 begin composition                          4 composition: compute -> exchange buffers
+//   5 composition: merged -> state, lane round (flag = some count changed)
+//   6 Step 6 on the rank's part (flag = levels seen by this rank)
+int bc_dist_hybir_shard_tables(bc_handle *h) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir) return h->fail(BC_ERR_INPUT, "bc_dist_hybir_shard_tables: call bc_dist_hybir_setup first");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const int r = h->dist_rank;
+    const int64_t b = h->h_part_off[(size_t)r + 1] - h->h_part_off[(size_t)r];
+    // keep the own part's table only (bc_dist_hybir_setup built exactly those rows)
+    int32_t *bm = nullptr;
+    double *sm = nullptr;
+    TRY(dev_alloc(h, &bm, (size_t)(b * b)));
+    TRY(dev_alloc(h, &sm, (size_t)(b * b)));
+    if (b > 0) {
+        CUDA_TRY(h, cudaMemcpy(bm, h->bm + h->h_tab_off[(size_t)r], (size_t)(b * b) * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice));
+        CUDA_TRY(h, cudaMemcpy(sm, h->sm + h->h_tab_off[(size_t)r], (size_t)(b * b) * sizeof(double),
+                               cudaMemcpyDeviceToDevice));
+    }
+    arena_free(h->bm), arena_free(h->sm);
+    h->bm = bm;
+    h->sm = sm;
+    h->h_tab_off.assign((size_t)h->k, 0);
+    h->tab_total = b * b;
+    TRY(upload(h, &h->d_tab_off, h->h_tab_off));
+    h->dist_sharded = true;
+    return BC_OK;
+}
+
+int bc_dist_hybir_border_step(bc_handle *h, int step, void *xchg_values_dev, void *xchg_flags_dev,
+                              const int32_t *seed_dist_dev, const double *seed_sigma_dev, int *flag_out,
+                              void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    if (!h->dist_hybir || !h->dist_sharded || h->dist_ng <= 0)
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_border_step: sharded tables and a batch in flight needed");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int S = h->border_S, lanes = h->dist_cnt, r = h->dist_rank;
+    const BorderGeom geo = border_geom(h);
+    const size_t cnt = (size_t)h->B * S;
+    const unsigned gb = grid1d(cnt), gl = grid1d((size_t)S, 128);
+    int max_b = 0;
+    for (int p = 0; p < h->k; ++p) max_b = std::max(max_b, h->h_part_off[p + 1] - h->h_part_off[p]);
+    const dim3 mgrid((max_b + kTJ - 1) / kTJ, (S + kTL - 1) / kTL, h->k);
+    auto read_flag = [&](const uint32_t *dev) -> int {
+        if (flag_out == nullptr) return BC_OK;
+        uint32_t v = 0;
+        CUDA_TRY(h, cudaMemcpyAsync(&v, dev, sizeof v, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+        *flag_out = (int)v;
+        return BC_OK;
+    };
+    if ((step == 1 || step == 2 || step == 4 || step == 5) && (xchg_values_dev == nullptr || xchg_flags_dev == nullptr))
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_border_step: null exchange buffers");
+    switch (step) {
+    case 0:
+        if (seed_dist_dev == nullptr || seed_sigma_dev == nullptr)
+            return h->fail(BC_ERR_INPUT, "bc_dist_hybir_border_step: null seeds");
+        CUDA_TRY(h, cudaMemcpyAsync(h->seedD, seed_dist_dev, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemcpyAsync(h->seedS, seed_sigma_dev, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemcpyAsync(h->D, h->seedD, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lane_iters, 0, S * sizeof(int32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lane_changed, 0, S * sizeof(uint32_t), st));
+        lane_enter_kernel<<<S, 128, 0, st>>>(geo, S, lanes, h->D, h->lane_part, h->lane_active, h->lane_entered,
+                                              h->n_cut);
+        ++h->launches;
+        break;
+    case 1:
+        cut_relax_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->D2, h->lane_part, h->lane_active, kApplyAll,
+                                             h->lane_changed, h->sync_flag);
+        std::swap(h->D, h->D2);
+        matrix_relax_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->D2, h->bm, h->lane_part, h->lane_active,
+                                                   kApplyAll, h->lane_changed, h->sync_flag, r);
+        std::swap(h->D, h->D2);
+        h->launches += 2;
+        CUDA_TRY(h, cudaMemcpyAsync(xchg_values_dev, h->D, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemcpyAsync(xchg_flags_dev, h->lane_changed, S * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        break;
+    case 2:
+        CUDA_TRY(h, cudaMemcpyAsync(h->D, xchg_values_dev, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemcpyAsync(h->lane_changed, xchg_flags_dev, S * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->dflags, 0, 4 * sizeof(uint32_t), st));
+        lane_step_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->lane_iters, h->dflags);
+        ++h->launches;
+        TRY(read_flag(h->dflags));
+        break;
+    case 3:
+        CUDA_TRY(h, cudaMemsetAsync(h->sig, 0, cnt * sizeof(double), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lane_active, 1, S * sizeof(uint32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->lane_changed, 0, S * sizeof(uint32_t), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->arr, 0, cnt * sizeof(double), st));
+        h->dist_round = 0;
+        break;
+    case 4:
+        arrival_kernel<<<gb, 256, 0, st>>>(geo, S, h->D, h->sig, h->arr, h->darr, h->lane_active, h->sync_flag);
+        compose_sigma_kernel<<<mgrid, 256, 0, st>>>(geo, S, h->D, h->seedD, h->seedS, h->darr, h->bm, h->sm,
+                                                    h->lane_part, h->sig, h->lane_active, h->lane_changed,
+                                                    h->dist_round == 0, h->sync_flag, r);
+        ++h->dist_round;
+        h->launches += 2;
+        CUDA_TRY(h, cudaMemcpyAsync(xchg_values_dev, h->sig, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemcpyAsync(xchg_flags_dev, h->lane_changed, S * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        break;
+    case 5:
+        CUDA_TRY(h, cudaMemcpyAsync(h->sig, xchg_values_dev, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemcpyAsync(h->lane_changed, xchg_flags_dev, S * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->dflags + 1, 0, sizeof(uint32_t), st));
+        lane_round_kernel<<<gl, 128, 0, st>>>(S, h->lane_active, h->lane_changed, h->dflags + 1);
+        ++h->launches;
+        TRY(read_flag(h->dflags + 1));
+        break;
+    case 6: {
+        int m = -1;
+        CUDA_TRY(h, cudaMemcpyAsync(h->d_maxlvl, &m, sizeof m, cudaMemcpyHostToDevice, st));
+        if (h->B > 0) {
+            max_seed_level_kernel<<<grid1d(cnt, 256, 1184), 256, 0, st>>>(h->D, h->arr, cnt, h->d_maxlvl, 1);
+            ++h->launches;
+        }
+        CUDA_TRY(h, cudaMemcpyAsync(&m, h->d_maxlvl, sizeof m, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+        TRY(begin_batch(h, h->d_src, h->dist_cnt, h->dist_ng, st));
+        int depth = 1;
+        TRY(forward_sweep(h, h->intra, h->dist_ng, st, &depth, true, h->dist_cnt, m));
+        h->dist_depth = depth;
+        if (flag_out) *flag_out = depth;
+        break;
+    }
+    default:
+        return h->fail(BC_ERR_INPUT, "bc_dist_hybir_border_step: unknown step");
+    }
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
 // Levels [local depth, global depth) exist on other ranks only: give them empty mask rows here.
 int bc_dist_hybir_set_depth(bc_handle *h, int global_depth, void *stream) {
     if (h == nullptr) return BC_ERR_INPUT;

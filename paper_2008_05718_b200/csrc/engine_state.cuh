@@ -274,6 +274,8 @@ struct bc_handle {
     // ---- graph-partitioned multi-GPU mode (one rank = one part)
     int dist_rank = -1, dist_world = 0, dist_ng = 0, dist_cnt = 0;
     bool dist_hybir = false;      // border-matrix forward phase across ranks (bc_dist_hybir_*)
+    bool dist_sharded = false;    // ... with the own part's border table only (bc_dist_hybir_shard_tables)
+    int dist_round = 0;           // composition round of the batch in flight (sharded tables)
     int dist_depth = 0;           // levels of the batch in flight (local, then global)
     std::vector<int64_t> dist_border_off;
     int32_t *dist_border_v = nullptr;   // all ranks' borders, rank-major

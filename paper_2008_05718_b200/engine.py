@@ -61,6 +61,7 @@ class RunConfig:
                                        # "mincut": grown regions + boundary refinement (mincut_partition)
     table_budget_bytes: float = 64e9   # border tables above this size: hybir falls back to bsp-baseline
     table_cache_dir: str | None = None  # border-table disk cache (border_matrix.py:85-125)
+    shard_border_tables: bool = True   # graph-partitioned hybir: one border table per rank (False: all on all)
     num_gpus: int = 1
     gpu_mode: str = "source-sharded"
     device: int | None = None          # CUDA ordinal; default LOCAL_RANK or 0

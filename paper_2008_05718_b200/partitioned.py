@@ -204,7 +204,8 @@ def incoming_cut_arcs(bs, border_arrays):
 class PartitionedRunner:
     """One rank of a graph-partitioned run (see the module docstring)."""
 
-    def __init__(self, g: Graph, part: Partition, device, groups: int = 4, forward: str = "bsp"):
+    def __init__(self, g: Graph, part: Partition, device, groups: int = 4, forward: str = "bsp",
+                 shard_tables: bool = True):
         import torch
         import torch.distributed as dist
         from . import _capi
@@ -232,11 +233,16 @@ class PartitionedRunner:
         self.eng.dist_set_cut_arcs(self.lg.cut_off, self.lg.cut_dst)
         self.tr = _Transport(device)
         self.forward = forward
+        self.shard_tables = bool(shard_tables) and forward == "hybir" and self.world > 1
         if forward == "hybir":
             cin_off, cin_src = incoming_cut_arcs(bs, bs.border_arrays)
             self.eng.dist_hybir_setup(cin_off, cin_src)
-            # every rank publishes the border table of its own part once
-            for p in range(self.world):
+            if self.shard_tables:
+                # one table per rank: refinement / composition of a part run on its owner, the
+                # border state is all-reduced after every iteration (_border_phase_sharded)
+                self.eng.dist_hybir_shard_tables()
+            # (replicated tables) every rank publishes the border table of its own part once
+            for p in range(self.world if not self.shard_tables else 0):
                 b = self.border_counts[p]
                 if b == 0:
                     continue
@@ -253,6 +259,10 @@ class PartitionedRunner:
             cnt = self.eng.dist_hybir_seed_count()
             self.seed_d = torch.zeros(max(cnt, 1), dtype=torch.int32, device=device)
             self.seed_s = torch.zeros(max(cnt, 1), dtype=torch.float64, device=device)
+            if self.shard_tables:
+                self._xd = torch.zeros(max(cnt, 1), dtype=torch.int32, device=device)
+                self._xs = torch.zeros(max(cnt, 1), dtype=torch.float64, device=device)
+                self._xf = torch.zeros(32 * groups, dtype=torch.int32, device=device)
         self.max_nb = max(self.border_counts + [1])
         self.stream = 0     # default stream: kernels, packs / unpacks and collectives stay ordered
         # forward (bsp) exchange buffers, grown on demand and kept
@@ -347,14 +357,48 @@ class PartitionedRunner:
             self.tr.all_reduce(ss, "max")
             self.forward_exchanges += 2
             self.exchanged_bytes += cnt * 12
-        depth, iters = self.eng.dist_hybir_forward(sd.data_ptr(), ss.data_ptr())
-        self.iterations += iters
+        if self.shard_tables:
+            depth = self._border_phase_sharded(sd, ss, cnt)
+        else:
+            depth, iters = self.eng.dist_hybir_forward(sd.data_ptr(), ss.data_ptr())
+            self.iterations += iters
         d = torch.tensor([depth], dtype=torch.int64, device=self.device)
         if self.world > 1:
             self.tr.all_reduce(d, "max")
         depth = int(d.item())
         self.eng.dist_hybir_set_depth(depth)
         return depth
+
+    def _border_phase_sharded(self, sd, ss, cnt):
+        """Steps 2-5 + path-count composition with one border table per rank, then Step 6.  The
+        "still active" flag is read back every 1, 1, 2, 3, 4, 4 ... iterations only (an iteration
+        without active lanes changes nothing)."""
+        eng, tr = self.eng, self.tr
+        xd, xs, xf = self._xd, self._xs, self._xf
+        eng.dist_hybir_border_step(0, seed_dist_ptr=sd.data_ptr(), seed_sigma_ptr=ss.data_ptr())
+        total_borders = sum(self.border_counts)
+        for compute, merge, values, op in ((1, 2, xd, "min"), (4, 5, xs, "max")):
+            if compute == 4:
+                eng.dist_hybir_border_step(3)
+            it, poll = 0, 1
+            while True:
+                for j in range(poll):
+                    eng.dist_hybir_border_step(compute, values.data_ptr(), xf.data_ptr())
+                    tr.all_reduce(values, op)
+                    tr.all_reduce(xf, "max")
+                    self.forward_exchanges += 2
+                    self.exchanged_bytes += cnt * (4 if compute == 1 else 8) + xf.numel() * 4
+                    active = eng.dist_hybir_border_step(merge, values.data_ptr(), xf.data_ptr(),
+                                                        want_flag=(j == poll - 1))
+                    it += 1
+                if compute == 1:
+                    self.iterations += poll
+                if not active:
+                    break
+                if it > 2 * total_borders + 16:
+                    raise EngineError("border phase did not settle")
+                poll = min(4, 1 + it // 2)
+        return eng.dist_hybir_border_step(6, want_flag=True)
 
     # -- backward ------------------------------------------------------------------------------
     def _backward(self, depth, ng):
@@ -439,7 +483,7 @@ def run_bc_partitioned(g: Graph, cfg):
     # exchange, as run_bc does); 'direct' has no partitioned meaning and takes the same fallback
     mode = choose_mode(cfg.mode, bs, cfg.table_budget_bytes) if cfg.mode == "hybir" else "bsp-baseline"
     forward = "hybir" if mode == "hybir" else "bsp"
-    runner = PartitionedRunner(g, part, device, cfg.groups or 4, forward)
+    runner = PartitionedRunner(g, part, device, cfg.groups or 4, forward, cfg.shard_border_tables)
     try:
         bc = runner.run(sources).cpu().numpy()
         counters = runner.counters()
@@ -451,7 +495,9 @@ def run_bc_partitioned(g: Graph, cfg):
              "backward_exchanges": runner.backward_exchanges, "backward_levels": runner.backward_levels,
              "iterations": runner.iterations, "state_vertices": runner.local_n,
              "owned_vertices": runner.lg.n_own, "halo_vertices": runner.lg.n_halo,
-             "table_bytes": border_table_bytes(bs) if forward == "hybir" else 0.0,
+             "table_bytes": (0.0 if forward != "hybir" else
+                             12.0 * runner.border_counts[rank] ** 2 if runner.shard_tables else border_table_bytes(bs)),
+             "sharded_tables": runner.shard_tables,
              "launches": counters["launches"]}
     mteps = g.num_edges * len(sources) / elapsed / 1e6 if elapsed > 0 else 0.0
     return RunResult(bc, [], CommTotals(runner.forward_exchanges, runner.backward_exchanges,

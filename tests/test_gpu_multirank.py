@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, kind, mode, out):
+def _worker(rank, world, port, kind, mode, out, shard=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0")
     import oracle as O
@@ -42,7 +42,7 @@ def _worker(rank, world, port, kind, mode, out):
         part = P.strip_partition(30, 24, world)
         sources = list(range(0, g.num_vertices, 17))
     cfg = P.RunConfig(sources=sources, num_gpus=world, gpu_mode="graph-partitioned", mode=mode,
-                      partition=part, groups=2, device=0)
+                      partition=part, groups=2, device=0, shard_border_tables=shard)
     if world == 1:      # run_bc only takes the multi-rank path above one GPU: drive the runner directly
         from paper_2008_05718_b200.partitioned import run_bc_partitioned
         res = run_bc_partitioned(g, cfg)
@@ -55,7 +55,8 @@ def _worker(rank, world, port, kind, mode, out):
                                                  res.stats["forward_exchanges"], batches,
                                                  res.stats["forward"] == "hybir",
                                                  res.stats["backward_exchanges"], res.stats["backward_levels"],
-                                                 res.stats["state_vertices"], g.num_vertices]))
+                                                 res.stats["state_vertices"], g.num_vertices,
+                                                 res.stats["table_bytes"], res.stats["iterations"]]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -69,7 +70,8 @@ def test_graph_partitioned_ranks_match_oracle(tmp_path, world, kind, mode):
     out = str(tmp_path / "res")
     mp.spawn(_worker, args=(world, _free_port(), kind, mode, out), nprocs=world, join=True)
     for r in range(world):
-        ok, levels, nbytes, fwd_x, batches, is_hybir, bwd_x, bwd_levels, state_n, n = np.load("%s.%d.npy" % (out, r))
+        (ok, levels, nbytes, fwd_x, batches, is_hybir, bwd_x, bwd_levels, state_n, n, table_bytes,
+         iters) = np.load("%s.%d.npy" % (out, r))
         assert ok, "rank %d BC differs from the oracle" % r
         if world == 1:          # one part, no borders: nothing crosses
             assert nbytes == 0 and fwd_x == 0 and bwd_x == 0
@@ -82,7 +84,25 @@ def test_graph_partitioned_ranks_match_oracle(tmp_path, world, kind, mode):
         if kind == "path":      # ~240 levels, 6 sources, world - 1 cut edges: a handful of exchanges
             assert bwd_levels >= 200 and bwd_x <= 6 * (world - 1)
         if mode == "hybir":
-            # the border-matrix forward phase: two all-reduces per batch, whatever the depth
-            assert is_hybir and fwd_x == 2 * batches
+            # the border-matrix forward phase with one table per rank: two all-reduces for the seeds
+            # and two per refinement iteration / composition round, whatever the depth
+            assert is_hybir and fwd_x >= 2 * batches and fwd_x % 2 == 0 and iters >= batches
+            assert fwd_x < batches * (levels - 1) or kind == "rmat"
         else:
             assert not is_hybir and fwd_x >= batches * (levels - 1)
+
+
+def test_replicated_border_tables_still_work(tmp_path):
+    """shard_border_tables=False: every rank holds every part's table and runs the whole border
+    phase itself -- the forward phase of a batch is then exactly two all-reduces."""
+    out = str(tmp_path / "res")
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), "road", "hybir", out, False), nprocs=world, join=True)
+    sharded = str(tmp_path / "shard")
+    mp.spawn(_worker, args=(world, _free_port(), "road", "hybir", sharded, True), nprocs=world, join=True)
+    for r in range(world):
+        rec = np.load("%s.%d.npy" % (out, r))
+        rec_s = np.load("%s.%d.npy" % (sharded, r))
+        assert rec[0] and rec_s[0]
+        assert rec[3] == 2 * rec[4]                  # forward exchanges = 2 per batch
+        assert rec_s[10] < rec[10]                   # one table instead of all of them

@@ -65,7 +65,7 @@ if "c1" in which:
     srcs = list(range(g.num_vertices))
     t0 = time.time(); obc, info = O.brandes_bc(g, srcs); cpu = time.time() - t0
     for mode in ("direct", "bsp-baseline", "hybir"):
-        P.run_bc(g, P.RunConfig(sources=srcs[:64], mode=mode, num_partitions=2, per_source_reports=False))
+        P.run_bc(g, P.RunConfig(sources=srcs, mode=mode, num_partitions=2, per_source_reports=True))   # warm-up at full size
         t0 = time.time()
         res = P.run_bc(g, P.RunConfig(sources=srcs, mode=mode, num_partitions=2, per_source_reports=True))
         wall = time.time() - t0

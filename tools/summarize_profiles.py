@@ -30,7 +30,7 @@ total = sum(a[1] for a in agg.values())
 cmd = "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 1 --warmup 0 --no-cpu --no-extra"
 with open(os.path.join(out, rnd + "_launches_summary.md"), "w") as fh:
     fh.write("# ncu launch list, %s (cold-cache, serialised: compare shares, not absolutes)\n\n" % rnd)
-    fh.write("Command: `%s`\n(the bench workload, one step: R-MAT scale-20 EF-16, 1024 sources in batches of 16 groups; "
+    fh.write("Command: `%s`\n(the bench workload: R-MAT scale-20 EF-16, 1024 sources of which 612 have arcs = one batch of 20 lane groups per pass; the command makes four identical passes -- the untimed byte-model step, the timed step and two run_bc calls of the e2e leg; "
              "raw list: `%s_launches.csv`)\n\n" % (cmd, rnd))
     fh.write("| kernel | launches | total us | share |\n|---|---:|---:|---:|\n")
     for name, (cnt, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -72,7 +72,7 @@ if os.path.exists(rep) or os.path.exists(rawcsv):
     per = [to_bytes(r[idx[2]], units[idx[2]]) + to_bytes(r[idx[3]], units[idx[3]]) for r in lev]
     rec = {"rmat20": sum(per) / len(per) if per else None,
            "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the %d level_kernel launches "
-                   "(forward and backward) of exactly one step, captured with ncu --set full from "
+                   "(forward and backward) = whole passes of 8 launches each (identical work), captured with ncu --set full from "
                    "bench.py --steps 1 --warmup 0 --no-cpu --no-extra" % len(per),
            "per_launch_bytes": per,
            "per_launch_ms": [float(r[idx[1]]) * {"ms": 1.0, "us": 1e-3, "s": 1e3, "ns": 1e-6}.get(units[idx[1]], 1.0)
