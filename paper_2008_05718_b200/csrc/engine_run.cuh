@@ -245,12 +245,16 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
                 CUDA_TRY(h, cudaEventRecord(h->side_go, st));
                 CUDA_TRY(h, cudaStreamWaitEvent(h->side_stream, h->side_go, 0));
                 ahead = Step1Out{};
-                helper = std::thread([&, b]() {
-                    cudaSetDevice(h->device);
-                    ahead.rc = step1(b + 1, h->side_stream, h->seedD_alt, h->seedS_alt, h->lane_part_alt, ahead);
-                    if (ahead.rc == BC_OK && cudaEventRecord(h->side_done, h->side_stream) != cudaSuccess)
-                        ahead.rc = BC_ERR_INTERNAL;
-                });
+                try {
+                    helper = std::thread([&, b]() {
+                        cudaSetDevice(h->device);
+                        ahead.rc = step1(b + 1, h->side_stream, h->seedD_alt, h->seedS_alt, h->lane_part_alt, ahead);
+                        if (ahead.rc == BC_OK && cudaEventRecord(h->side_done, h->side_stream) != cudaSuccess)
+                            ahead.rc = BC_ERR_INTERNAL;
+                    });
+                } catch (const std::exception &) {
+                    // no thread to be had: the next batch runs its Step 1 inline, as without look-ahead
+                }
             }
             // ---- Steps 2-5 + path-count composition on the border tables
             int max_seed = -1;
