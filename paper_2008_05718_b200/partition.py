@@ -286,42 +286,65 @@ def grow_partition(g: Graph, k: int, seed: int = 0, refine_rounds: int = 4) -> P
             size[p] += len(nb)
             frontiers[p] = nb
             active = active or len(nb) > 0
-    # leftovers.  (1) vertices sealed off by parts that filled up join the part of an assigned
-    # neighbour; (2) components no seed fell into go, largest first, to the part that is
-    # smallest at that moment; isolated vertices are dealt out the same way in bulk.
+    # leftovers: vertices no region reached before it filled up (sealed off behind full parts, or in
+    # components no seed fell into).  Joining the neighbouring part regardless of its size -- what a
+    # plain flood would do -- wrecks the balance on trees and other thin graphs, so every leftover
+    # component is dealt out in breadth-first order: chunk by chunk to the part with the most room
+    # (an adjacent one while it has room), which keeps the pieces connected and the sizes level.
     src_all = g.arc_src
-    while True:
-        open_arc = (owner[src_all] < 0) & (owner[col] >= 0)
-        if not open_arc.any():
-            break
-        owner[src_all[open_arc]] = owner[col[open_arc]]
     size = np.bincount(owner[owner >= 0], minlength=k).astype(np.int64)
     left = np.flatnonzero(owner < 0)
     if len(left):
-        comp_of = np.arange(len(left))
-        linked = left[deg[left] > 0]
-        if len(linked):
-            from scipy.sparse import csr_matrix
-            from scipy.sparse.csgraph import connected_components
-            pos = np.full(n, -1, dtype=np.int64)
-            pos[left] = np.arange(len(left))
-            m = owner[src_all] < 0          # both ends are unassigned here (step 1 closed the rest)
-            sub = csr_matrix((np.ones(int(m.sum()), dtype=np.int8), (pos[src_all[m]], pos[col[m]])),
-                             shape=(len(left), len(left)))
-            _, comp_of = connected_components(sub, directed=False)
-        comp_size = np.bincount(comp_of)
+        from scipy.sparse import csr_matrix
+        from scipy.sparse.csgraph import breadth_first_order, connected_components
+        pos = np.full(n, -1, dtype=np.int64)
+        pos[left] = np.arange(len(left))
+        m = (owner[src_all] < 0) & (owner[col] < 0)
+        sub = csr_matrix((np.ones(int(m.sum()), dtype=np.int8), (pos[src_all[m]], pos[col[m]])),
+                         shape=(len(left), len(left)))
+        ncomp, comp_of = connected_components(sub, directed=False)
+        comp_size = np.bincount(comp_of, minlength=ncomp)
+        # a vertex of each component that touches an assigned part (if any), and that part
+        touch = (owner[src_all] < 0) & (owner[col] >= 0)
+        gate = np.full(ncomp, -1, dtype=np.int64)
+        gate_part = np.full(ncomp, -1, dtype=np.int64)
+        if touch.any():
+            tc = comp_of[pos[src_all[touch]]]
+            first = np.unique(tc, return_index=True)
+            gate[first[0]] = pos[src_all[touch]][first[1]]
+            gate_part[first[0]] = owner[col[touch]][first[1]]
+        target = -(-n // k)
+        by_comp = np.argsort(comp_of, kind="stable")            # members of a component, contiguous
+        comp_start = np.concatenate(([0], np.cumsum(comp_size)))
+        singles = np.flatnonzero(comp_size == 1)
         for c in np.argsort(-comp_size, kind="stable"):
-            if comp_size[c] == 1:
+            if comp_size[c] <= 1:
                 break
-            p = int(np.argmin(size))
-            owner[left[comp_of == c]] = p
-            size[p] += comp_size[c]
-        singles = left[owner[left] < 0]
+            members = by_comp[comp_start[c]:comp_start[c + 1]]
+            prefer = int(gate_part[c])
+            if comp_size[c] <= 64:
+                # small piece: whole, to the neighbouring part while it has room
+                p = prefer if prefer >= 0 and size[prefer] + comp_size[c] <= target else int(np.argmin(size))
+                owner[left[members]] = p
+                size[p] += comp_size[c]
+                continue
+            start = int(gate[c]) if gate[c] >= 0 else int(members[0])
+            order = breadth_first_order(sub, start, directed=False, return_predecessors=False)
+            done = 0
+            while done < len(order):
+                p = prefer if prefer >= 0 and size[prefer] < target else int(np.argmin(size))
+                room = int(max(target - size[p], 1))
+                take = order[done:done + room]
+                owner[left[take]] = p
+                size[p] += len(take)
+                done += len(take)
+                prefer = -1
         if len(singles):
-            # fill the parts up to a common level, smallest first
+            # isolated leftovers: fill the parts up to a common level, smallest first
+            one = left[np.isin(comp_of, singles)]
             order = np.argsort(size, kind="stable")
             give = np.zeros(k, dtype=np.int64)
-            remaining = len(singles)
+            remaining = len(one)
             level = size[order].astype(np.int64)
             for i in range(k):
                 nxt = level[i + 1] if i + 1 < k else None
@@ -334,7 +357,7 @@ def grow_partition(g: Graph, k: int, seed: int = 0, refine_rounds: int = 4) -> P
                 remaining -= take
                 if remaining == 0:
                     break
-            owner[singles] = np.repeat(np.arange(k), give).astype(np.int32)[: len(singles)]
+            owner[one] = np.repeat(np.arange(k), give).astype(np.int32)[: len(one)]
             size += give
     # border smoothing
     src = g.arc_src

@@ -386,6 +386,17 @@ def test_refine_partition_lowers_the_cut_and_keeps_the_balance():
     assert cut_size(g, P.refine_partition(g, start)) < cut_size(g, start) // 2
 
 
+def test_grown_partitions_stay_balanced_on_trees():
+    """Regions that fill up seal subtrees off; the leftovers are dealt out by room, not flooded into
+    the neighbouring (full) part."""
+    g = G.random_connected(20000, 150, seed=3)
+    for k in (2, 4, 8):
+        for p in (P.grow_partition(g, k, seed=0), P.mincut_partition(g, k, seed=0)):
+            sizes = np.asarray(p.sizes)
+            assert sizes.sum() == g.num_vertices and sizes.min() > 0
+            assert sizes.max() <= 1.12 * g.num_vertices / k, (k, p.sizes)
+
+
 def test_bench_samples_are_strided():
     import importlib.util
     spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(os.path.dirname(
