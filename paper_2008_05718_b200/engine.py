@@ -309,8 +309,12 @@ def pipeline_sources(g: Graph, cfg: RunConfig) -> RunResult:
     """Look-ahead variant (engine.py:135-143,156-161): Step 1 of the NEXT source batch runs on a
     second CUDA stream while the border refinement / path-count composition of the current
     batch is in flight (it only needs the BFS state, which the border phase does not touch);
-    ``pipeline_overlaps`` counts the batches whose Step 1 was issued ahead.  Results are
-    identical to ``run_bc`` (test_engine.py:57-64)."""
+    ``pipeline_overlaps`` counts the batches whose Step 1 was issued ahead.  Same result as
+    ``run_bc`` (test_engine.py:57-64): bit for bit on the row layout, up to the rounding order of
+    the atomically accumulated BC vector on deep graphs (level-ordered sweeps).  On one GPU the
+    overlap buys no device time -- Step 1 and the border phase compete for the same memory system
+    (road-like 2048^2 in 8 strips, 4 batches: 1,309 vs 1,298 ms) -- it is there for interface parity
+    and for ranks whose border phase waits on collectives."""
     if cfg.mode != "hybir":
         raise InputError("pipelining applies to hybir mode only")
     return run_bc(g, cfg, _pipeline=True)
