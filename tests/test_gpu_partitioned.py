@@ -363,3 +363,29 @@ def test_failed_run_leaves_no_partial_sums_behind():
             e.run(srcs + [g.num_vertices + 5])
         again, _ = e.run(srcs)
     assert np.array_equal(good, again)
+
+
+def test_property_random_graphs_all_modes_match_oracle():
+    """The reference's property test (test_forward.py:199-223, test_acceptance.py:164-183) on the GPU:
+    random connected graphs, random two- and three-way assignments, every mode -- distances and path
+    counts exact, dependencies within 1e-9, and the refinement stays inside its iteration bound."""
+    from hypothesis import HealthCheck, given, settings, strategies as st
+
+    @settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+    @given(n=st.integers(6, 160), extra=st.integers(0, 200), seed=st.integers(0, 10 ** 6), k=st.integers(2, 3))
+    def check(n, extra, seed, k):
+        g = G.random_connected(n, extra, seed=seed)
+        rng = np.random.default_rng(seed)
+        assign = rng.integers(0, k, size=n).astype(np.int32)
+        assign[:k] = np.arange(k)                       # no empty part
+        srcs = rng.choice(n, size=min(5, n), replace=False).tolist()
+        with Engine(g) as e:
+            e.set_partition(k, assign)
+            borders = int(e.border_counts(k).sum())
+            for mode in (MODE_DIRECT, MODE_HYBIR, MODE_BSP):
+                dist, sigma, delta = e.debug_sources(srcs, mode)
+                _check_sources(g, srcs, dist, sigma, delta)
+                if mode == MODE_HYBIR:
+                    reports = e.reports(len(srcs))
+                    assert (reports[:, 0] <= borders + 2).all()
+    check()
