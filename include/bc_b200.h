@@ -218,6 +218,12 @@ int bc_dist_pack(bc_handle *h, int level, void *send_dev, int64_t cap_entries, i
                  void *stream);
 int bc_dist_unpack(bc_handle *h, int level, int from, const void *recv_dev, int64_t cap_entries,
                    int64_t cap_values, int64_t n_entries, void *stream);
+/* Unpack every peer's message of one level in ONE launch out of the all-gathered buffer
+ * (world x words_per_rank int64 words); the entry counts are read on the device from the
+ * all-gathered plan table plan_dev[world][depth][2] (what bc_dist_plan_backward returned, gathered). */
+int bc_dist_unpack_all(bc_handle *h, int level, const void *recv_dev, int64_t words_per_rank,
+                       int64_t cap_entries, int64_t cap_values, const int64_t *plan_dev, int depth,
+                       void *stream);
 /* Kernel launches, CUDA-event time of the dense level kernel and its byte model since the last
  * call (drains the device). */
 int bc_dist_get_stats(bc_handle *h, bc_stats *stats);

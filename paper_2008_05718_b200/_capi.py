@@ -27,6 +27,7 @@ SYMBOLS = (
     "bc_debug_sources", "bc_get_reports", "bc_get_border_counts", "bc_get_border_tables",
     "bc_get_border_frontier", "bc_set_border_tables",
     "bc_dist_setup", "bc_dist_set_cut_arcs", "bc_dist_plan_backward", "bc_dist_pack", "bc_dist_unpack",
+    "bc_dist_unpack_all",
     "bc_dist_get_stats", "bc_dist_begin", "bc_dist_forward_level", "bc_dist_backward_level",
     "bc_dist_export", "bc_dist_import", "bc_dist_get_live", "bc_dist_set_live", "bc_dist_finish",
     "bc_dist_hybir_setup", "bc_dist_hybir_get_table", "bc_dist_hybir_set_table",
@@ -109,6 +110,8 @@ def load():
     L.bc_dist_pack.argtypes = [vp, cint, vp, i64, i64, vp]
     L.bc_dist_unpack.restype = cint
     L.bc_dist_unpack.argtypes = [vp, cint, cint, vp, i64, i64, i64, vp]
+    L.bc_dist_unpack_all.restype = cint
+    L.bc_dist_unpack_all.argtypes = [vp, cint, vp, i64, i64, i64, vp, cint, vp]
     L.bc_dist_get_stats.restype = cint
     L.bc_dist_get_stats.argtypes = [vp, ctypes.POINTER(BcStats)]
     L.bc_dist_begin.restype = cint
@@ -395,6 +398,11 @@ class Engine:
         self._ck(self._lib.bc_dist_unpack(self._h, int(level), int(peer), ctypes.c_void_p(recv_ptr),
                                           int(cap_entries), int(cap_values), int(n_entries),
                                           ctypes.c_void_p(stream or None)))
+
+    def dist_unpack_all(self, level, recv_ptr, words_per_rank, cap_entries, cap_values, plan_ptr, depth, stream=0):
+        self._ck(self._lib.bc_dist_unpack_all(self._h, int(level), ctypes.c_void_p(recv_ptr), int(words_per_rank),
+                                              int(cap_entries), int(cap_values), ctypes.c_void_p(plan_ptr),
+                                              int(depth), ctypes.c_void_p(stream or None)))
 
     def dist_stats(self) -> dict:
         st = BcStats()

@@ -169,6 +169,31 @@ __global__ void dist_unpack_kernel(double *val, const int32_t *border_v, int ng,
     }
 }
 
+// All peers' messages of one level in one launch: blockIdx.y = sender; its entry count comes from
+// the all-gathered plan table plan[sender][level][0] (int64 [world][depth][2], on the device).
+__global__ void dist_unpack_all_kernel(double *val, const int32_t *border_v_all, const int64_t *border_off,
+                                       int ng, int64_t n, const int64_t *recv, int64_t words_per_rank,
+                                       int64_t cap_e, int64_t cap_v, const int64_t *plan, int depth,
+                                       int level, int self) {
+    const int from = blockIdx.y;
+    if (from == self) return;
+    const int count = (int)plan[((size_t)from * depth + level) * 2];
+    const double *values = reinterpret_cast<const double *>(recv + (size_t)from * words_per_rank);
+    const int32_t *head = reinterpret_cast<const int32_t *>(values + cap_v);
+    const int32_t *border_v = border_v_all + border_off[from];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
+        const int i = head[e];
+        uint32_t m = (uint32_t)head[cap_e + e];
+        const double *in = values + head[2 * cap_e + e];
+        double *row = val + ((size_t)(i % ng) * n + border_v[i / ng]) * 32;
+        while (m) {
+            const int lane = __ffs(m) - 1;
+            m &= m - 1;
+            row[lane] = *in++;
+        }
+    }
+}
+
 // bc[v] += per-group partials of the vertices this rank owns
 __global__ void dist_finish_kernel(double *bc, double *bcg, const int32_t *part, int rank,
                                    int64_t n, int groups) {

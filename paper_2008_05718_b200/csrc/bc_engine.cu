@@ -545,7 +545,7 @@ void bc_destroy(bc_handle *h) {
     arena_free(h->presence);
     arena_free(h->dist_border_v), arena_free(h->dist_counts), arena_free(h->dist_offsets);
     arena_free(h->dist_scan_tmp);
-    arena_free(h->dist_cut_off), arena_free(h->dist_cut_dst);
+    arena_free(h->dist_cut_off), arena_free(h->dist_cut_dst), arena_free(h->dist_border_off_dev);
     arena_free(h->plan_idx), arena_free(h->plan_mask), arena_free(h->plan_voff);
     arena_free(h->plan_eoff), arena_free(h->plan_cnt_e), arena_free(h->plan_cnt_v);
     if (h->side_stream) cudaStreamDestroy(h->side_stream);

@@ -339,6 +339,29 @@ int bc_dist_unpack(bc_handle *h, int level, int from, const void *recv_dev, int6
     return BC_OK;
 }
 
+int bc_dist_unpack_all(bc_handle *h, int level, const void *recv_dev, int64_t words_per_rank,
+                       int64_t cap_entries, int64_t cap_values, const int64_t *plan_dev, int depth,
+                       void *stream) {
+    if (h == nullptr) return BC_ERR_INPUT;
+    TRY(dist_check(h, level));
+    if (recv_dev == nullptr || plan_dev == nullptr || level >= depth || cap_entries < 0 || cap_values < 0 ||
+        words_per_rank < cap_values + (3 * cap_entries + 1) / 2)
+        return h->fail(BC_ERR_INPUT, "bc_dist_unpack_all: bad buffers / sizes");
+    if (cap_entries == 0 || h->dist_world < 2) return BC_OK;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    if (h->dist_border_off_dev == nullptr) {
+        std::vector<int64_t> off(h->dist_border_off.begin(), h->dist_border_off.end());
+        TRY(upload(h, &h->dist_border_off_dev, off));
+    }
+    const dim3 grid(std::min<unsigned>(grid1d((size_t)cap_entries), 1184), (unsigned)h->dist_world);
+    dist_unpack_all_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        h->coef, h->dist_border_v, h->dist_border_off_dev, h->dist_ng, h->n, (const int64_t *)recv_dev,
+        words_per_rank, cap_entries, cap_values, plan_dev, depth, level, h->dist_rank);
+    ++h->launches;
+    CUDA_TRY(h, cudaGetLastError());
+    return BC_OK;
+}
+
 int bc_dist_get_stats(bc_handle *h, bc_stats *stats) {
     if (h == nullptr || stats == nullptr) return BC_ERR_INPUT;
     memset(stats, 0, sizeof *stats);

@@ -284,6 +284,7 @@ struct bc_handle {
     size_t dist_scan_bytes = 0;
     int64_t dist_entries_cap = 0;
     // backward exchange plan of the batch in flight (bc_dist_plan_backward)
+    int64_t *dist_border_off_dev = nullptr;   // device copy of dist_border_off (bc_dist_unpack_all)
     int64_t *dist_cut_off = nullptr;    // [own borders + 1] cut arcs of this rank's borders
     int32_t *dist_cut_dst = nullptr;    // their far ends (local vertex ids of the halo)
     int32_t *plan_idx = nullptr, *plan_voff = nullptr, *plan_eoff = nullptr, *plan_cnt_e = nullptr, *plan_cnt_v = nullptr;

@@ -407,7 +407,8 @@ class PartitionedRunner:
         plan = None
         if self.world > 1 and depth > 2:
             mine = torch.from_numpy(self.eng.dist_plan_backward(depth)).to(self.device)     # [depth, 2]
-            plan = self.tr.all_gather(mine).cpu().numpy()                                   # [world, depth, 2]
+            plan_dev = self.tr.all_gather(mine).contiguous()                                # [world, depth, 2]
+            plan = plan_dev.cpu().numpy()
             cap = plan.max(axis=0)                                                          # per level
             cap_e, cap_v = int(cap[:, 0].max()), int(cap[:, 1].max())
             words = cap_v + (3 * cap_e + 1) // 2                                            # int64 words per message
@@ -425,11 +426,8 @@ class PartitionedRunner:
             recv = self._recv[:self.world * words]
             self.eng.dist_pack(lv, send.data_ptr(), le, lvv)
             self.tr.all_gather_into(recv, send)
-            for peer in range(self.world):
-                n_ent = int(plan[peer, lv, 0])
-                if peer == self.rank or n_ent == 0:
-                    continue
-                self.eng.dist_unpack(lv, peer, recv[peer * words:].data_ptr(), le, lvv, n_ent)
+            # every peer's values land in the halo rows in one launch (counts read on the device)
+            self.eng.dist_unpack_all(lv, recv.data_ptr(), words, le, lvv, plan_dev.data_ptr(), depth)
             self.backward_exchanges += 1
             self.exchanged_bytes += int(plan[self.rank, lv, 0]) * 12 + int(plan[self.rank, lv, 1]) * 8
 
