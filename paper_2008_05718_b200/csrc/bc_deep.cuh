@@ -200,15 +200,20 @@ __device__ __forceinline__ void padded_prefix(int64_t *s_pref, int ng, LenFn len
     __syncthreads();
 }
 
-// resident blocks per SM the compact sweeps ask the compiler for (register cap = 65536 / (256 * blocks)):
-// they are bound by the latency of random memory accesses, so more resident warps = more of them in flight
+// Shape of the persistent kernels: 1024 resident threads per SM (64 registers each) measured best
+// (road-like 2048^2 x 512 sources: 743 / 780 / 878 ms at 1280 / 1536 / 2048 threads per SM, 748 / 849 at
+// 768 / 512), and one block of 1024 threads per SM beats four of 256 by ~1 % (709 vs 719 ms: four times
+// fewer participants in the grid-wide barriers).
+#ifndef BC_DEEP_THREADS
+#define BC_DEEP_THREADS 1024
+#endif
 #ifndef BC_DEEP_MIN_BLOCKS_F
-#define BC_DEEP_MIN_BLOCKS_F 4
+#define BC_DEEP_MIN_BLOCKS_F 1
 #endif
 #ifndef BC_DEEP_MIN_BLOCKS_B
-#define BC_DEEP_MIN_BLOCKS_B 4
+#define BC_DEEP_MIN_BLOCKS_B 1
 #endif
-constexpr int kDeepThreads = 256;
+constexpr int kDeepThreads = BC_DEEP_THREADS;
 constexpr int kDeepWarps = kDeepThreads / 32;
 constexpr int kDeepMaxGroups = 128;   // groups per batch the persistent sweeps accept
 
