@@ -504,8 +504,15 @@ struct DeepFwdCompactParams {
     unsigned long long seed_room;
 };
 
+#ifdef BC_DEEP_PHASE_TIMING
+__device__ unsigned long long g_phase_ns[8];   // dev build: time per phase (A, A2, B) as seen by block 0
+#endif
 __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forward_compact_kernel(const DeepFwdCompactParams p) {
     cg::grid_group grid = cg::this_grid();
+#ifdef BC_DEEP_PHASE_TIMING
+    unsigned long long t_last;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_last));
+#endif
     __shared__ int32_t stage[kDeepWarps][kStage];
     __shared__ int64_t s_pref[kDeepMaxGroups + 1];
     __shared__ int64_t s_beg[kDeepMaxGroups], s_end[kDeepMaxGroups], s_lbeg[kDeepMaxGroups];
@@ -617,6 +624,9 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
             }
         }
         grid.sync();
+#ifdef BC_DEEP_PHASE_TIMING
+        if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t_now; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_now)); g_phase_ns[0] += t_now - t_last; t_last = t_now; }
+#endif
 
         // ---- phase A2: the entries appended above become level L
         if (threadIdx.x < 8) s_stat[threadIdx.x] = 0ull;
@@ -693,6 +703,9 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                 if (s_live[k]) atomicOr(p.live + (size_t)L * p.G + k, s_live[k]);
         }
         grid.sync();
+#ifdef BC_DEEP_PHASE_TIMING
+        if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t_now; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_now)); g_phase_ns[1] += t_now - t_last; t_last = t_now; }
+#endif
 
         // ---- phase B: the frontier adds its path counts into the new entries' slots
         frontier_prefix();
@@ -798,6 +811,9 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
             }
         }
         grid.sync();
+#ifdef BC_DEEP_PHASE_TIMING
+        if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t_now; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_now)); g_phase_ns[2] += t_now - t_last; t_last = t_now; }
+#endif
         if (threadIdx.x == 0) s_cont = *(volatile int *)cont_flag;
         __syncthreads();
         if (!s_cont) break;

@@ -486,6 +486,15 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_forward_compact_kernel, dim3(h->deep_grid_fc),
                                                         dim3(kDeepThreads), args, 0, st));
                 ++h->launches;
+#ifdef BC_DEEP_PHASE_TIMING
+                {
+                    unsigned long long ns[8];
+                    cudaStreamSynchronize(st);
+                    cudaMemcpyFromSymbol(ns, g_phase_ns, sizeof ns);
+                    fprintf(stderr, "[phase] forward compact, cumulative ms: A %.1f  A2 %.1f  B+publish %.1f\n",
+                            ns[0] / 1e6, ns[1] / 1e6, ns[2] / 1e6);
+                }
+#endif
                 int info[2] = {0, 0};
                 CUDA_TRY(h, cudaMemcpyAsync(info, h->deep_info, sizeof info, cudaMemcpyDeviceToHost, st));
                 CUDA_TRY(h, cudaStreamSynchronize(st));
