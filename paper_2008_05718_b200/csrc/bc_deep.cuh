@@ -474,7 +474,7 @@ struct __align__(16) VertexState {
     uint32_t vis;    // lanes that reached the vertex
     uint32_t next;   // lanes discovering it at the level being produced (zero between levels)
     uint32_t pos;    // queue entry (index + 1) the vertex got most recently
-    uint32_t pad;
+    uint32_t pos2;   // backward sweep: entries of odd levels write here, of even levels into `pos`
 };
 struct DeepFwdCompactParams {
     const int64_t *off;
@@ -972,9 +972,11 @@ __global__ void __launch_bounds__(kDeepThreads) deep_backward_kernel(const DeepB
 // scratch; ncu: 687 B of DRAM traffic per visit at 2.8 TB/s, profiles/r2_deep_kernels_ncu.md).
 // This variant keeps sigma and coef per queue ENTRY, in level order (DeepFwdParams::qs):
 //   - an entry reads its sigma and writes its coef at q_off[i] + rank: sequential traffic;
-//   - the vertex record (VertexState::pos) maps a vertex to the queue entry it has at the level
-//     below (index + 1; every entry re-writes it when its level is processed, and an index
-//     outside that level's range is a stale one, so nothing is ever erased), and a parent finds a
+//   - the vertex record maps a vertex to the queue entry it has at the level below (index + 1:
+//     every entry writes it while its level is processed, into one of two words chosen by the
+//     level's parity so that the probes of the level in flight are not disturbed; an index
+//     outside the probed level's range is a stale one, so nothing is ever erased and one
+//     grid-wide barrier per level is enough), and a parent finds a
 //     child's lanes (q_m[j]) and coef (qc[q_off[j] + rank]) inside the few-MB window of that
 //     level, which stays in L2;
 //   - BC partials are added with atomics into ONE vector per batch (bc_acc, n doubles: L2
@@ -1027,6 +1029,10 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
             const int64_t v = p.q.q_v[qbase + i];
             const uint32_t m = p.q.q_m[qbase + i];
             const uint32_t at = p.q_off[qbase + i];
+            // this entry is what level L - 1 will look for: the two index words alternate by level
+            // parity, so the parents' probes of the level below (other word) are not disturbed
+            if (L & 1) gvs[v].pos2 = (uint32_t)i + 1u;
+            else gvs[v].pos = (uint32_t)i + 1u;
             if (m == 0) continue;
             const int64_t a0 = p.off[v], a1 = p.off[v + 1];
             const uint32_t cb = s_cb[g], ce = s_ce[g];   // a child's entry index + 1 lies in [cb, ce]
@@ -1041,7 +1047,8 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
                 for (int k = 0; k < kThinArcs; ++k) {
                     cj[k] = 0;
                     if (!deepest && a0 + k < a1) {
-                        const uint32_t pj = gvs[__ldg(p.col + a0 + k)].pos;
+                        const VertexState *child = gvs + __ldg(p.col + a0 + k);
+                        const uint32_t pj = ((L + 1) & 1) ? child->pos2 : child->pos;
                         if (pj >= cb && pj <= ce) cj[k] = pj;
                     }
                 }
@@ -1075,7 +1082,8 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
                     const uint32_t lower = (1u << bit) - 1u;
                     double acc = 0.0;
                     for (int64_t a = a0; a < a1; ++a) {
-                        const uint32_t pj = gvs[__ldg(p.col + a)].pos;
+                        const VertexState *child = gvs + __ldg(p.col + a);
+                        const uint32_t pj = ((L + 1) & 1) ? child->pos2 : child->pos;
                         if (pj < cb || pj > ce) continue;
                         const uint32_t mj = p.q.q_m[qbase + pj - 1];
                         if ((mj >> bit) & 1u) acc += p.qc[vbase + p.q_off[qbase + pj - 1] + __popc(mj & lower)];
@@ -1094,18 +1102,6 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
             }
         }
         __syncthreads();   // the shared ranges are rewritten by the next level
-        grid.sync();
-        // level L becomes the level below: its entries take over the vertex records
-        {
-            int g2 = 0;
-            for (int64_t f0 = gtid - lane; f0 < total; f0 += gthreads) {
-                while (f0 >= s_pref[g2 + 1]) ++g2;
-                const int64_t i = beg_t[g2] + (f0 - s_pref[g2]) + lane;
-                if (i < end_t[g2])
-                    p.vs[(size_t)g2 * n + p.q.q_v[(size_t)g2 * p.q.cap + i]].pos = (uint32_t)i + 1u;
-            }
-        }
-        __syncthreads();
         grid.sync();
     }
 }

@@ -1,0 +1,21 @@
+#!/bin/bash
+# Last session of round 2: the records the profiles/ directory quotes, regenerated with the final code.
+set -x
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -4 | tee gpurun_out/pytest_gpu_final.log
+python __graft_entry__.py --smoke 2>&1 | tail -2 | tee gpurun_out/smoke.log
+python bench.py 2> gpurun_out/bench.err | tee gpurun_out/bench.json | cut -c1-200
+python bench.py --impl reference --steps 2 --warmup 1 2>> gpurun_out/bench.err | tee gpurun_out/bench_ref.json | cut -c1-200
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
+    bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu --no-extra 2> gpurun_out/bench_torchrun.err | grep "^{" > gpurun_out/bench_torchrun_n1.json
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29612 \
+    bench.py --gpus 1 --gpu-mode graph-partitioned --forward bsp --workload rmat16 --sources 256 --steps 3 --warmup 1 \
+    2>> gpurun_out/bench_torchrun.err | grep "^{" > gpurun_out/bench_gp_bsp_n1.json
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29613 \
+    bench.py --gpus 1 --gpu-mode graph-partitioned --forward hybir --workload road512 --sources 128 --steps 2 --warmup 1 \
+    2>> gpurun_out/bench_torchrun.err | grep "^{" > gpurun_out/bench_gp_hybir_n1.json
+wc -c gpurun_out/bench_torchrun_n1.json gpurun_out/bench_gp_bsp_n1.json gpurun_out/bench_gp_hybir_n1.json
+: > gpurun_out/r2_fullsize_new.jsonl
+for w in c1 rmat22 er22 road2048 road2048_hybir rmat24; do
+  timeout 1500 python tools/fullsize.py $w 2>&1 | grep "^{" | tee -a gpurun_out/r2_fullsize_new.jsonl | cut -c1-160
+done
