@@ -464,10 +464,13 @@ __global__ void __launch_bounds__(kDeepThreads) deep_forward_kernel(const DeepFw
 //   B  accumulate: the frontier entries walk the arcs marked in q_arc, look the child's entry up
 //      through pos[], and add their own path counts into the child's slots (red.global.add.f64
 //      on an L2-resident window; integer-valued, exact in any order).
-// The three per-(group, vertex) words the phases touch -- visited lanes, lanes being discovered at
-// this level, queue entry of the vertex -- sit side by side in one 16-byte record (VertexState), so
-// the visited probe of an arc, the OR into the next-level word and the entry index of the child
-// share a 32-byte sector: these dense arrays are what is left of the random DRAM traffic.
+// The per-(group, vertex) words the phases touch -- visited lanes, lanes being discovered at this
+// level, queue entry of the vertex -- sit side by side in one 16-byte record (VertexState), so the
+// visited probe of an arc, the OR into the next-level word and the entry index of the child share a
+// 32-byte sector: these dense arrays are what is left of the random DRAM traffic.  (Carrying the
+// entry's lane mask and value slot in the record as well -- 32 bytes, one hop less per child -- was
+// measured and lost: road-like 2048^2, 662 -> 692 ms, the doubled footprint costs more L2 misses on
+// the probes than the hop saves.)
 // `pos` is never cleared inside a batch: queue indices only grow, so an index below the start of
 // the level being produced is a stale one.  The host initialises the records per sweep.
 struct __align__(16) VertexState {
@@ -476,6 +479,7 @@ struct __align__(16) VertexState {
     uint32_t pos;    // queue entry (index + 1) the vertex got most recently
     uint32_t pos2;   // backward sweep: entries of odd levels write here, of even levels into `pos`
 };
+
 struct DeepFwdCompactParams {
     const int64_t *off;
     const int32_t *col;
@@ -485,7 +489,9 @@ struct DeepFwdCompactParams {
     VertexState *vs;           // [G][n]
     double *qs;                // [G][vcap]
     uint32_t *q_off;           // [G][cap]
-    uint32_t *q_arc;           // [G][cap] arcs of a frontier entry that reached a fresh lane
+    uint32_t *q_arc;           // [G][cap] (degree, 255 = look it up) << 24 | arcs 0..23 that reached a fresh lane
+    uint32_t *q_a;             // [G][cap] first arc of the entry's vertex (the sweeps then never read the
+                               // row offsets of a frontier vertex: one random access and one hop less)
     unsigned long long *v_count;   // [G] value slots handed out so far
     int64_t vcap;
     uint32_t *live;
@@ -566,13 +572,18 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                 const int64_t i = s_beg[g] + (f0 - s_pref[g]) + lane;
                 VertexState *gvs = p.vs + (size_t)g * n;
                 const size_t qbase = (size_t)g * p.q.cap;
-                uint32_t mask = 0;
+                uint32_t mask = 0, word = 0;
                 int64_t a = 0, e = 0;
                 if (i < end) {
-                    const int32_t u = p.q.q_v[qbase + i];
                     mask = p.q.q_m[qbase + i];
-                    a = p.off[u];
-                    e = p.off[u + 1];
+                    word = p.q_arc[qbase + i];
+                    a = p.q_a[qbase + i];
+                    e = a + (word >> 24);
+                    if ((word >> 24) == 255u) {     // long adjacency: the degree did not fit
+                        const int32_t u = p.q.q_v[qbase + i];
+                        a = p.off[u];
+                        e = p.off[u + 1];
+                    }
                 }
                 int rounds = (int)(e - a);
                 rounds = __reduce_max_sync(kFull, rounds);
@@ -589,7 +600,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
 #pragma unroll
                     for (int k = 0; k < kThinArcs; ++k) {
                         if (r0 + k >= rounds) break;   // warp-uniform
-                        if (fresh[k] && r0 + k < 32) arcbits |= 1u << (r0 + k);
+                        if (fresh[k] && r0 + k < 24) arcbits |= 1u << (r0 + k);
                         const bool fresh_vertex = fresh[k] != 0 && old[k] == 0;
                         const unsigned newm = __ballot_sync(kFull, fresh_vertex);
                         if (newm) {
@@ -600,7 +611,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                         }
                     }
                 }
-                if (i < end) p.q_arc[qbase + i] = arcbits;
+                if (i < end) p.q_arc[qbase + i] = (word & 0xff000000u) | arcbits;
             }
             if (staged) flush();
         }
@@ -649,7 +660,10 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                     m = cur.y;
                     p.q.q_m[qbase + i] = m;
                     *vn = make_uint2(cur.x | m, 0u);
-                    const unsigned long long deg = (unsigned long long)(p.off[w + 1] - p.off[w]);
+                    const int64_t w_a = p.off[w];
+                    const unsigned long long deg = (unsigned long long)(p.off[w + 1] - w_a);
+                    p.q_a[qbase + i] = (uint32_t)w_a;
+                    p.q_arc[qbase + i] = (uint32_t)min(deg, 255ull) << 24;
                     nr += __popc(m);
                     ar += __popc(m) * deg;
                     nv += 1;
@@ -720,8 +734,13 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                 const size_t qbase = (size_t)g * p.q.cap;
                 const size_t vbase = (size_t)g * p.vcap;
                 const uint32_t mask = p.q.q_m[qbase + i];
-                const int32_t u = p.q.q_v[qbase + i];
-                const int64_t a = p.off[u], e = p.off[u + 1];
+                const uint32_t word = p.q_arc[qbase + i];
+                int64_t a = p.q_a[qbase + i], e = a + (word >> 24);
+                if ((word >> 24) == 255u) {
+                    const int32_t u = p.q.q_v[qbase + i];
+                    a = p.off[u];
+                    e = p.off[u + 1];
+                }
                 const uint32_t at_u = p.q_off[qbase + i];
                 const VertexState *gvs = p.vs + (size_t)g * n;
                 const uint32_t lbeg = (uint32_t)s_lbeg[g];
@@ -740,8 +759,8 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                         ++c_t;
                     }
                 };
-                if (e - a <= 32) {
-                    uint32_t bits = p.q_arc[qbase + i];
+                if (e - a <= 24) {
+                    uint32_t bits = word & 0x00ffffffu;
                     while (bits) {
                         const int k = __ffs(bits) - 1;
                         bits &= bits - 1;
@@ -846,8 +865,9 @@ __global__ void compact_init_kernel(VertexState *vs, int64_t n, int batch_count)
     const uint32_t dead = lanes >= 32 ? 0u : ~((1u << lanes) - 1u);
     uint4 *out = reinterpret_cast<uint4 *>(vs + g * n);
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x)
+         v += (int64_t)gridDim.x * blockDim.x) {
         out[v] = make_uint4(dead, 0u, 0u, 0u);
+    }
 }
 
 // ... and the visited words out of the vertex records, for the row-based kernels that take over.
@@ -860,14 +880,18 @@ __global__ void vis_from_records_kernel(const VertexState *vs, uint32_t *vis, in
 
 // Level 0 of a compact sweep: every set lane of a source entry carries one path.
 __global__ void compact_level0_kernel(QueueParams q, uint32_t *q_off, double *qs, int64_t vcap,
-                                      unsigned long long *v_count, VertexState *vs, int64_t n) {
+                                      unsigned long long *v_count, VertexState *vs, int64_t n,
+                                      const int64_t *off, uint32_t *q_a, uint32_t *q_arc) {
     const size_t g = blockIdx.x;
     if (threadIdx.x != 0) return;
     const int64_t end = (int64_t)q.q_count[g];
     uint32_t at = 0;
     for (int64_t i = 0; i < end; ++i) {     // <= 32 entries
         const uint32_t m = q.q_m[g * q.cap + i];
-        vs[g * n + q.q_v[g * q.cap + i]].vis |= m;
+        const int64_t v = q.q_v[g * q.cap + i];
+        vs[g * n + v].vis |= m;
+        q_a[g * q.cap + i] = (uint32_t)off[v];
+        q_arc[g * q.cap + i] = (uint32_t)min((long long)(off[v + 1] - off[v]), 255ll) << 24;
         q_off[g * q.cap + i] = at;
         for (int k = 0; k < __popc(m); ++k) qs[g * (size_t)vcap + at + k] = 1.0;
         at += __popc(m);
@@ -998,6 +1022,8 @@ struct DeepBwdCompactParams {
     int ng, G;
     int hi, lo;                  // levels hi (the deepest level of the batch), hi - 1, ..., lo
     VertexState *vs;             // [G][n] (pos field)
+    const uint32_t *q_a;         // first arc / degree of every entry as the forward sweep recorded them
+    const uint32_t *q_arc;       // (nullptr when that sweep ran on another CSR: the cut-free one of hybir mode)
 };
 
 __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backward_compact_kernel(const DeepBwdCompactParams p) {
@@ -1034,7 +1060,14 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
             if (L & 1) gvs[v].pos2 = (uint32_t)i + 1u;
             else gvs[v].pos = (uint32_t)i + 1u;
             if (m == 0) continue;
-            const int64_t a0 = p.off[v], a1 = p.off[v + 1];
+            int64_t a0, a1;
+            if (p.q_a != nullptr && (p.q_arc[qbase + i] >> 24) != 255u) {
+                a0 = p.q_a[qbase + i];
+                a1 = a0 + (p.q_arc[qbase + i] >> 24);
+            } else {
+                a0 = p.off[v];
+                a1 = p.off[v + 1];
+            }
             const uint32_t cb = s_cb[g], ce = s_ce[g];   // a child's entry index + 1 lies in [cb, ce]
             double total_d = 0.0;
             uint32_t rest = m;

@@ -252,7 +252,9 @@ struct bc_handle {
     int64_t q_vcap = 0;
     double *bc_acc = nullptr;      // [n] BC partial of a batch, added with atomics
     VertexState *vs = nullptr;     // [G][n] visited / next-level / queue-entry words of the compact sweeps
-    uint32_t *q_arc = nullptr;     // [G][q_cap] arcs of a frontier entry that reached a fresh lane
+    uint32_t *q_arc = nullptr;     // [G][q_cap] degree << 24 | arcs of a frontier entry that reached a fresh lane
+    uint32_t *q_a = nullptr;       // [G][q_cap] first arc of the entry's vertex
+    const int64_t *q_a_csr = nullptr;   // ... in the CSR with these offsets (the last compact forward sweep's)
     bool fwd_compact_allowed = false;   // set by the caller of a sweep: nobody reads sigma rows afterwards
     bool sigma_stale = false;      // the sigma rows were not cleared for this batch (compact sweep expected)
     const int64_t *batch_src_dev = nullptr;   // sources of the batch in flight (begin_batch)
@@ -432,8 +434,8 @@ void free_state(bc_handle *h) {
     h->live_cap = 0;
     arena_free(h->q_v), arena_free(h->q_m), arena_free(h->q_count);
     arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
-    arena_free(h->vs), arena_free(h->q_arc);
-    h->vs = nullptr, h->q_arc = nullptr;
+    arena_free(h->vs), arena_free(h->q_arc), arena_free(h->q_a);
+    h->vs = nullptr, h->q_arc = nullptr, h->q_a = nullptr;
     h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
     h->q_vcap = 0;
     arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
@@ -641,7 +643,7 @@ bool ensure_deep_compact(bc_handle *h) {
     if (h->qs != nullptr) return true;
     const size_t G = (size_t)h->alloc_groups;
     const int64_t vcap = 32 * h->n;
-    if (vcap >= ((int64_t)1 << 32)) return false;   // value offsets are 32-bit
+    if (vcap >= ((int64_t)1 << 32) || h->n_arcs >= ((int64_t)1 << 32)) return false;   // 32-bit value / arc offsets
     if (arena_malloc((void **)&h->qs, G * (size_t)vcap * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
         h->qs = nullptr;
@@ -650,14 +652,15 @@ bool ensure_deep_compact(bc_handle *h) {
     }
     if (arena_malloc((void **)&h->q_off, G * (size_t)h->q_cap * sizeof(uint32_t)) != cudaSuccess ||
         arena_malloc((void **)&h->q_arc, G * (size_t)h->q_cap * sizeof(uint32_t)) != cudaSuccess ||
+        arena_malloc((void **)&h->q_a, G * (size_t)h->q_cap * sizeof(uint32_t)) != cudaSuccess ||
         arena_malloc((void **)&h->vs, G * (size_t)h->n * sizeof(VertexState)) != cudaSuccess ||
         arena_malloc((void **)&h->v_count, G * sizeof(unsigned long long)) != cudaSuccess ||
         arena_malloc((void **)&h->bc_acc, (size_t)h->n * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
         arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
-        arena_free(h->vs), arena_free(h->q_arc);
+        arena_free(h->vs), arena_free(h->q_arc), arena_free(h->q_a);
         h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
-        h->vs = nullptr, h->q_arc = nullptr;
+        h->vs = nullptr, h->q_arc = nullptr, h->q_a = nullptr;
         h->deep_compact = 0;
         return false;
     }
@@ -667,6 +670,7 @@ bool ensure_deep_compact(bc_handle *h) {
     // when the queues grow)
     cudaMemset(h->q_off, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
     cudaMemset(h->q_arc, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
+    cudaMemset(h->q_a, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
     h->q_vcap = vcap;
     return true;
 }
@@ -693,7 +697,7 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
         CUDA_TRY(h, cudaMemcpy(nm + g * cap, h->q_m + g * h->q_cap, keep * sizeof(uint32_t),
                                cudaMemcpyDeviceToDevice));
     }
-    for (uint32_t **arr : {&h->q_off, &h->q_arc}) {
+    for (uint32_t **arr : {&h->q_off, &h->q_arc, &h->q_a}) {
         if (*arr == nullptr) continue;
         uint32_t *no = nullptr;
         CUDA_TRY(h, arena_malloc((void **)&no, G * (size_t)cap * sizeof(uint32_t)));

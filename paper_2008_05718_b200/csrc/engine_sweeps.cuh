@@ -441,7 +441,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 // level 0 in level order: one path per source lane
                 compact_init_kernel<<<dim3(grid1d((size_t)n, 256, 1184), ng), 256, 0, st>>>(h->vs, n, cnt);
                 compact_level0_kernel<<<ng, 32, 0, st>>>(queue_params(h), h->q_off, h->qs, h->q_vcap, h->v_count,
-                                                         h->vs, n);
+                                                         h->vs, n, c.off, h->q_a, h->q_arc);
                 h->launches += 2;
                 reps[0].compact = true;
                 compact_mode = true;
@@ -465,6 +465,8 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 dp.qs = h->qs;
                 dp.q_off = h->q_off;
                 dp.q_arc = h->q_arc;
+                dp.q_a = h->q_a;
+                h->q_a_csr = c.off;
                 dp.v_count = h->v_count;
                 dp.vcap = h->q_vcap;
                 dp.live = h->live;
@@ -748,6 +750,10 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             dp.hi = depth - 1;
             dp.lo = last;
             dp.vs = h->vs;
+            if (h->q_a_csr == c.off) {     // the forward sweep walked this very CSR
+                dp.q_a = h->q_a;
+                dp.q_arc = h->q_arc;
+            }
             void *args[] = {&dp};
             CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_compact_kernel, dim3(h->deep_grid_c),
                                                     dim3(kDeepThreads), args, 0, st));
