@@ -19,3 +19,10 @@ wc -c gpurun_out/bench_torchrun_n1.json gpurun_out/bench_gp_bsp_n1.json gpurun_o
 for w in c1 rmat22 er22 road2048 road2048_hybir rmat24; do
   timeout 1500 python tools/fullsize.py $w 2>&1 | grep "^{" | tee -a gpurun_out/r2_fullsize_new.jsonl | cut -c1-160
 done
+T=/tmp/r2prof; mkdir -p $T
+timeout 900 ncu --set full --clock-control none -k regex:deep_forward_compact -c 4 -o $T/r2_deep_fc -f \
+    python tools/road_probe.py 2048 128 4 > gpurun_out/ncu_deep_fc.log 2>&1
+ncu -i $T/r2_deep_fc.ncu-rep --page raw --csv > gpurun_out/r2_deep_forward_compact.raw.csv
+timeout 900 ncu --set full --clock-control none -k regex:deep_backward_compact -c 1 -o $T/r2_deep_bc -f \
+    python tools/road_probe.py 2048 128 4 > gpurun_out/ncu_deep_bc.log 2>&1
+ncu -i $T/r2_deep_bc.ncu-rep --page raw --csv > gpurun_out/r2_deep_backward_compact.raw.csv
