@@ -84,6 +84,13 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
         h->err = "cudaSetDevice failed";
         return bail(BC_ERR_INTERNAL);
     }
+#ifdef BC_CARVEOUT
+    // shared-memory carve-out of the dense pull kernels, in percent of the SM's 228 KB
+    cudaFuncSetAttribute(level_kernel<false, false, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, BC_CARVEOUT);
+    cudaFuncSetAttribute(level_kernel<true, false, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, BC_CARVEOUT);
+    cudaFuncSetAttribute(level_kernel<false, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, BC_CARVEOUT);
+    cudaFuncSetAttribute(level_kernel<true, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, BC_CARVEOUT);
+#endif
     Csr &c = h->full;
     c.n = n;
     c.n_arcs = n_arcs;

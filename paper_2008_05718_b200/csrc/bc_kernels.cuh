@@ -132,6 +132,17 @@ __device__ __forceinline__ double ldg_if(const double *ptr, uint32_t pred) {
     return x;
 }
 
+// Neighbour ids are streamed: every 128-byte line of col_idx is used once by one warp.
+__device__ __forceinline__ int32_t ld_col(const int32_t *ptr) {
+#ifdef BC_COL_NOALLOC
+    int32_t x;
+    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(x) : "l"(ptr));
+    return x;
+#else
+    return __ldg(ptr);
+#endif
+}
+
 #ifndef BC_STAGED_UNROLL_FWD
 #define BC_STAGED_UNROLL_FWD 8
 #endif
@@ -167,12 +178,20 @@ __device__ __forceinline__ void gather_staged(unsigned any, uint32_t hit, int32_
                                               const double *__restrict__ myval, int lane,
                                               double &acc) {
     constexpr int kU = BWD ? BC_STAGED_UNROLL_BWD : BC_STAGED_UNROLL_FWD;  // row loads in flight
+#ifdef BC_EXACT_PAD
+    __shared__ __align__(16) int2 s_rows[kWarpsPerBlock][32];
+#else
     __shared__ int2 s_rows[kWarpsPerBlock][32 + kStagedMax];
+#endif
     int2 *lst = s_rows[threadIdx.x >> 5];
     const int nh = __popc(any);
     const uint32_t lbit = 1u << lane;
     if (hit != 0) lst[__popc(any & (lbit - 1u))] = make_int2(w, (int)hit);
+#ifdef BC_EXACT_PAD
+    if (lane < ((-nh) & (kU - 1))) lst[nh + lane] = make_int2(0, 0);  // pad the last round: predicate off
+#else
     if (lane < kU) lst[nh + lane] = make_int2(0, 0);  // pad the last round: predicate off
+#endif
     __syncwarp();
     for (int i = 0; i < nh; i += kU) {
         int2 e[kU];
@@ -206,8 +225,8 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
                                           const WeightedProbe &wp = WeightedProbe{}) {
     int32_t w_c = 0, w_n = 0;
     uint32_t m_c = 0;
-    if (lane < n_arcs) w_c = __ldg(col + lane);
-    if (lane + 32 < n_arcs) w_n = __ldg(col + 32 + lane);
+    if (lane < n_arcs) w_c = ld_col(col + lane);
+    if (lane + 32 < n_arcs) w_n = ld_col(col + 32 + lane);
     if (lane < n_arcs) m_c = probe_arc<WEIGHTED, BWD>(lane, w_c, nmask, wp);
     const double *myval = val + lane;
     for (int base = 0; base < n_arcs; base += 32) {
@@ -217,7 +236,7 @@ __device__ __forceinline__ void scan_arcs(int n_arcs, uint32_t want,
         m_c = 0;
         if (base + 32 + lane < n_arcs) m_c = probe_arc<WEIGHTED, BWD>(base + 32 + lane, w_c, nmask, wp);
         w_n = 0;
-        if (base + 64 + lane < n_arcs) w_n = __ldg(col + base + 64 + lane);
+        if (base + 64 + lane < n_arcs) w_n = ld_col(col + base + 64 + lane);
         const unsigned any = __ballot_sync(kFull, hit != 0);
         PROF_ADD(0, 1);
         if (any == 0) continue;

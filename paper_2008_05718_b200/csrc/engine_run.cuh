@@ -299,7 +299,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             clear_source_sigma_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * lanes_per_batch, cnt, n,
                                                                         h->sigma);
             ++h->launches;
-            h->sigma_clean = true;
+            h->sigma_clean_groups = h->sigma_clean_after;
         }
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
         launches_b += h->launches - l_bwd;

@@ -19,6 +19,7 @@ struct Arena {
     std::mutex mu;
     std::unordered_map<void *, std::pair<int, size_t>> live;   // ptr -> (device, bytes)
     std::multimap<size_t, void *> spare[64];                   // per device, by size
+    std::unordered_map<void *, size_t> zeroed;                 // spare block -> leading bytes known to be zero
     size_t spare_bytes = 0;
 
     static size_t round_up(size_t b) {
@@ -28,11 +29,14 @@ struct Arena {
     void flush_locked(int dev) {
         for (auto &kv : spare[dev]) {
             cudaFree(kv.second);
+            zeroed.erase(kv.second);
             spare_bytes -= kv.first;
         }
         spare[dev].clear();
     }
-    cudaError_t alloc(void **out, size_t bytes) {
+    // *zero_prefix (optional) = leading bytes of the block its last owner left zeroed (release())
+    cudaError_t alloc(void **out, size_t bytes, size_t *zero_prefix = nullptr) {
+        if (zero_prefix) *zero_prefix = 0;
         int dev = 0;
         cudaGetDevice(&dev);
         dev &= 63;
@@ -41,6 +45,11 @@ struct Arena {
         auto it = spare[dev].lower_bound(want);
         if (it != spare[dev].end() && it->first <= want + want / 4 + (1u << 16)) {
             *out = it->second;
+            auto z = zeroed.find(*out);
+            if (z != zeroed.end()) {
+                if (zero_prefix) *zero_prefix = z->second;
+                zeroed.erase(z);
+            }
             live[*out] = {dev, it->first};
             spare_bytes -= it->first;
             spare[dev].erase(it);
@@ -55,7 +64,7 @@ struct Arena {
         if (e == cudaSuccess) live[*out] = {dev, want};
         return e;
     }
-    void release(void *p) {
+    void release(void *p, size_t zero_prefix = 0) {
         if (p == nullptr) return;
         std::lock_guard<std::mutex> lock(mu);
         auto it = live.find(p);
@@ -63,6 +72,7 @@ struct Arena {
             cudaFree(p);
             return;
         }
+        if (zero_prefix) zeroed[p] = std::min(zero_prefix, it->second.second);
         spare[it->second.first].emplace(it->second.second, p);
         spare_bytes += it->second.second;
         live.erase(it);
@@ -230,7 +240,8 @@ struct bc_handle {
     double *sigma = nullptr, *coef = nullptr, *delta = nullptr;
     uint8_t *cand = nullptr;    // [alloc_groups][n] candidate flags of the dense forward sweeps (deep graphs)
     bool use_cand = false;      // set by forward_sweep for the launches of its levels
-    bool sigma_clean = false;   // sigma is all zero (kept so by the backward sweeps of adaptive batches)
+    int sigma_clean_groups = 0; // leading groups of sigma that are all zero (kept so by the backward sweeps of adaptive batches)
+    int sigma_clean_after = 0;  // its value once the running batch has cleared what it touched
     bool lazy_clear = false;    // this batch's backward sweep clears sigma behind itself
     int last_depth = 0;         // levels of the previous batch (deep graphs: memset instead)
     double *bcg = nullptr;
@@ -427,7 +438,11 @@ void free_state(bc_handle *h) {
     arena_free(h->vis);
     for (uint32_t *p : h->lvl) arena_free(p);
     h->lvl.clear();
-    arena_free(h->sigma), arena_free(h->coef), arena_free(h->delta), arena_free(h->bcg);
+    // the path-count rows a finished run left zeroed (begin_batch) stay tagged in the arena: the
+    // next handle that gets the block skips that part of its first memset
+    arena().release((void *)h->sigma, (size_t)h->sigma_clean_groups * (size_t)h->n * 32 * sizeof(double));
+    h->sigma_clean_groups = 0;
+    arena_free(h->coef), arena_free(h->delta), arena_free(h->bcg);
     arena_free(h->pacc), arena_free(h->pmask);
     arena_free(h->live);
     h->live = nullptr;
@@ -515,12 +530,13 @@ int ensure_state(bc_handle *h, int groups, bool want_delta) {
     if (h->alloc_groups < groups) {
         free_state(h);
         CUDA_TRY(h, arena_malloc((void **)&h->vis, groups * n * sizeof(uint32_t)));
-        CUDA_TRY(h, arena_malloc((void **)&h->sigma, groups * n * 32 * sizeof(double)));
+        size_t zero_prefix = 0;
+        CUDA_TRY(h, arena().alloc((void **)&h->sigma, groups * n * 32 * sizeof(double), &zero_prefix));
         CUDA_TRY(h, arena_malloc((void **)&h->coef, groups * n * 32 * sizeof(double)));
         CUDA_TRY(h, arena_malloc((void **)&h->bcg, groups * n * sizeof(double)));
         h->bcg_dirty = true;   // cleared on the caller's stream by the run that uses it
         h->alloc_groups = groups;
-        h->sigma_clean = false;
+        h->sigma_clean_groups = (int)std::min<size_t>(groups, zero_prefix / (n * 32 * sizeof(double)));
     }
     if (want_delta && h->delta == nullptr)
         CUDA_TRY(h, arena_malloc((void **)&h->delta, (size_t)h->alloc_groups * n * 32 * sizeof(double)));

@@ -125,9 +125,21 @@ int begin_batch(bc_handle *h, const int64_t *src_dev, int cnt, int ng, cudaStrea
     // sweep is expected to take that path; forward_adaptive clears the rows itself if it does not.
     h->sigma_stale = zero_sigma && !h->lazy_clear && h->fwd_compact_allowed && h->deep && h->deep_compact &&
                      h->sparse && h->full.wgt == nullptr && h->n_arcs < 6 * h->n && ng <= kDeepMaxGroups;
-    if (zero_sigma && !h->sigma_stale && !(h->sigma_clean && h->lazy_clear))
-        CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, (size_t)h->alloc_groups * n * 32 * sizeof(double), st));
-    h->sigma_clean = false;
+    // sigma_clean_groups: leading groups whose rows are all zero.  A lazily cleared batch only needs
+    // zeros under the groups it uses, so a fresh engine clears ng groups, not the whole allocation.
+    const int clean = h->sigma_clean_groups;
+    const size_t group_bytes = (size_t)n * 32 * sizeof(double);
+    h->sigma_clean_groups = 0;   // rows are in use while the batch runs
+    h->sigma_clean_after = 0;
+    if (zero_sigma && !h->sigma_stale) {
+        if (h->lazy_clear) {
+            if (ng > clean)
+                CUDA_TRY(h, cudaMemsetAsync(h->sigma + (size_t)clean * n * 32, 0, (size_t)(ng - clean) * group_bytes, st));
+            h->sigma_clean_after = std::max(clean, ng);
+        } else {
+            CUDA_TRY(h, cudaMemsetAsync(h->sigma, 0, (size_t)h->alloc_groups * group_bytes, st));
+        }
+    }
     h->batch_src_dev = src_dev;
     h->batch_cnt = cnt;
     CUDA_TRY(h, cudaMemsetAsync(h->live, 0, (size_t)h->live_cap * h->alloc_groups * sizeof(uint32_t), st));
