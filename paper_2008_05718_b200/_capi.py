@@ -185,9 +185,9 @@ class Engine:
         self.h2d_bytes_graph = off.nbytes + col.nbytes
         if not g.unit_weight:
             w = np.ascontiguousarray(g.arc_weight, dtype=np.int64)
-            if len(w) and (w.max() > 4096 or w.min() < 1):
+            if len(w) and (w.max() >= 2 ** 31 or w.min() < 1):
                 self.close()
-                raise InputError("arc weights must be integers in [1, 4096] on the GPU path")
+                raise InputError("arc weights must be integers in [1, 2^31) on the GPU path")
             w32 = w.astype(np.int32)
             rc = self._lib.bc_set_weights(self._h, _ptr(w32))
             if rc != BC_OK:

@@ -11,6 +11,7 @@
 #include "bc_deep.cuh"
 #include "bc_dist.cuh"
 #include "bc_kernels.cuh"
+#include "bc_sssp.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -34,6 +35,7 @@ using namespace bcb200;
 #include "engine_state.cuh"
 #include "engine_sweeps.cuh"
 #include "engine_border.cuh"
+#include "engine_sssp.cuh"
 #include "engine_run.cuh"
 
 namespace {
@@ -137,13 +139,13 @@ int bc_set_weights(bc_handle *h, const int32_t *weights) {
     h->h_wgt.clear();
     h->wmax = 1;
     if (weights == nullptr) return BC_OK;   // back to unit weights
-    int64_t wmax = 1;
+    int64_t wmax = 1, wsum = 0;
     for (int64_t a = 0; a < h->n_arcs; ++a) {
         if (weights[a] <= 0) return h->fail(BC_ERR_INPUT, "arc weights must be positive integers");
         wmax = std::max<int64_t>(wmax, weights[a]);
+        wsum += weights[a];
     }
-    if (wmax > 4096)
-        return h->fail(BC_ERR_INPUT, "arc weights above 4096 are not supported (one level per distance value)");
+    h->wsum = wsum;
     if (wmax == 1) return BC_OK;
     CUDA_TRY(h, arena_malloc((void **)&h->full.wgt, std::max<int64_t>(h->n_arcs, 1) * sizeof(int32_t)));
     CUDA_TRY(h, cudaMemcpy(h->full.wgt, weights, h->n_arcs * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -182,6 +184,16 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     }
     if (k == "sparse") {
         h->sparse = value ? 1 : 0;
+        return BC_OK;
+    }
+    if (k == "sssp") {
+        if (value < -1 || value > 1) return h->fail(BC_ERR_INPUT, "sssp must be -1 (by weight range), 0 or 1");
+        h->wgt_mode = (int)value;
+        return BC_OK;
+    }
+    if (k == "sssp_delta") {
+        if (value < 0) return h->fail(BC_ERR_INPUT, "sssp_delta must be >= 0 (0 = mean arc weight)");
+        h->sp_delta = value;
         return BC_OK;
     }
     if (k == "reorder") {

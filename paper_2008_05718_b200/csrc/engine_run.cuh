@@ -21,6 +21,15 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
             return h->fail(BC_ERR_INPUT, buf);
         }
     if (mode != BC_MODE_DIRECT && h->k == 1) mode = BC_MODE_DIRECT;  // one part: no borders
+    if (general_weights(h)) {
+        // weights beyond the level-per-distance kernels: label-correcting distances and
+        // dependency-counted sweeps (engine_sssp.cuh)
+        if (mode != BC_MODE_DIRECT)
+            return h->fail(BC_ERR_INPUT, "arc weights above 4096 (or option sssp = 1): BC_MODE_DIRECT only");
+        return run_sources_sssp(h, sources_in, k_all, bc_dev, st, stats, debug, dist_out, sigma_out, delta_out);
+    }
+    if (h->full.wgt != nullptr && h->wmax > 4096)
+        return h->fail(BC_ERR_INPUT, "arc weights above 4096 need the general-weight sweeps (option sssp = -1 or 1)");
     const bool hybir = mode == BC_MODE_HYBIR;
     const bool want_reports = h->reports && mode != BC_MODE_DIRECT;
     if (hybir) TRY(build_border_tables(h));

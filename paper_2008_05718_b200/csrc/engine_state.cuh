@@ -167,6 +167,16 @@ struct bc_handle {
     Csr full;
     std::vector<int32_t> h_wgt;   // host copy of the arc weights (empty: unit weights)
     int wmax = 1;                 // largest arc weight
+    int wgt_mode = -1;            // option "sssp": 1 = general-weight sweeps (bc_sssp.cuh), 0 = one level per distance value, -1 = by weight range
+    // general-weight sweeps: rows [G][n][32] of distances and tight-arc counts, frontier masks [G][n]
+    long long *sp_dist = nullptr;
+    int *sp_npar = nullptr, *sp_nchild = nullptr;
+    uint32_t *sp_maskA = nullptr, *sp_maskB = nullptr, *sp_leaf = nullptr;
+    int *sp_flags = nullptr;
+    long long *sp_bound = nullptr;   // per round: distance bound, smallest waiting distance (phase A)
+    long long sp_delta = 0;          // option "sssp_delta": step of the bound (0 = mean arc weight)
+    long long wsum = 0;              // sum of the arc weights
+    int sp_groups = 0;
     int cur_depth = 0;        // levels of the batch being swept backward (weighted kernels)
     // options
     int groups = 4;
@@ -434,7 +444,21 @@ int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
     return BC_OK;
 }
 
+// state of the general-weight sweeps (engine_sssp.cuh)
+void free_sssp_state(bc_handle *h) {
+    arena_free(h->sp_dist), arena_free(h->sp_npar), arena_free(h->sp_nchild);
+    arena_free(h->sp_maskA), arena_free(h->sp_maskB), arena_free(h->sp_leaf), arena_free(h->sp_flags);
+    arena_free(h->sp_bound);
+    h->sp_bound = nullptr;
+    h->sp_dist = nullptr;
+    h->sp_npar = h->sp_nchild = nullptr;
+    h->sp_maskA = h->sp_maskB = h->sp_leaf = nullptr;
+    h->sp_flags = nullptr;
+    h->sp_groups = 0;
+}
+
 void free_state(bc_handle *h) {
+    free_sssp_state(h);
     arena_free(h->vis);
     for (uint32_t *p : h->lvl) arena_free(p);
     h->lvl.clear();

@@ -204,6 +204,9 @@ def border_table_bytes(bs: BorderSet) -> float:
     return float(sum(12.0 * b * b for b in bs.counts()))
 
 
+GENERAL_WEIGHT_LIMIT = 4096   # largest arc weight of the level-per-distance kernels (bc_set_weights)
+
+
 def choose_mode(mode: str, bs: BorderSet, budget_bytes: float) -> str:
     """``hybir`` needs the border tables; when they do not fit the budget the run falls back to
     the reference's other partitioned mode, which is pinned to give the same BC
@@ -279,8 +282,14 @@ def run_bc(g: Graph, cfg: RunConfig | None = None, _pipeline: bool = False) -> R
     sources = select_sources(g, cfg)
     p, bs = prepare(g, cfg)
     mode = choose_mode(cfg.mode, bs, cfg.table_budget_bytes) if p.num_parts > 1 else "direct"
+    if mode != "direct" and not g.unit_weight and int(g.arc_weight.max()) > GENERAL_WEIGHT_LIMIT:
+        # the partitioned modes take one level per distance value; beyond that the engine has the
+        # label-correcting sweeps of csrc/bc_sssp.cuh, which are unpartitioned (same BC)
+        warnings.warn("arc weights above %d: running mode 'direct' instead of '%s'"
+                      % (GENERAL_WEIGHT_LIMIT, mode), stacklevel=2)
+        mode = "direct"
     with open_engine(g, cfg, len(sources)) as eng:
-        if p.num_parts > 1:
+        if p.num_parts > 1 and mode != "direct":
             eng.set_partition(p.num_parts, p.assignment)
         cached = False
         if mode == "hybir" and cfg.table_cache_dir:
@@ -293,7 +302,7 @@ def run_bc(g: Graph, cfg: RunConfig | None = None, _pipeline: bool = False) -> R
         if mode == "hybir" and cfg.table_cache_dir and not cached:
             save_border_tables(eng, g, p, bs, cfg.table_cache_dir)
         per_source = []
-        if cfg.per_source_reports and p.num_parts > 1:
+        if cfg.per_source_reports and p.num_parts > 1 and mode != "direct":
             per_source = _per_source(sources, eng.reports(len(sources)), mode)
         elif cfg.per_source_reports:
             per_source = [{"source": int(s), "forward": {"source": int(s)}, "backward": {}} for s in sources]

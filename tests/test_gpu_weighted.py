@@ -197,3 +197,114 @@ def test_reference_acceptance_corpus_on_the_gpu():
         assert np.allclose(bc_b, rec["bc"], rtol=RTOL, atol=ATOL), rec["i"]
         assert rep_h == rec["hybir"], rec["i"]
         assert rep_b == rec["bsp"], rec["i"]
+
+
+# ---- general positive integer weights: label-correcting distances + dependency-counted sweeps
+# (csrc/bc_sssp.cuh).  The same oracle, the same bars: dist and sigma exact, delta / BC to 1e-9.
+
+def check_against_oracle(g, srcs, e, n_inspect=40):
+    dist, sigma, delta = e.debug_sources(srcs[:n_inspect])
+    bc, st = e.run(srcs)
+    for i, s in enumerate(srcs[:n_inspect]):
+        od, osg, odl, info = O.brandes_single_source(g, int(s))
+        assert info["sigma_max"] < 2.0 ** 53
+        assert np.array_equal(dist[i], od), s
+        assert np.array_equal(sigma[i], osg), s
+        assert np.allclose(delta[i], odl, rtol=RTOL, atol=ATOL), s
+    obc, info = O.brandes_bc(g, srcs)
+    assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL)
+    assert st["reached"] == info["reached"] and st["dag_arcs"] == info["dag_arcs"]
+    return st
+
+
+@pytest.mark.parametrize("case", ["rc", "rmat_hubs", "grid", "two_components"])
+def test_general_weight_sweeps_on_small_weights(case):
+    # the graphs of test_weighted_seeded_graphs_vs_oracle, forced onto the general-weight path
+    if case == "rc":
+        g = with_weights(G.random_connected(600, 900, seed=11), 1, 10)
+        srcs = list(range(0, 600, 7))
+    elif case == "rmat_hubs":
+        g = with_weights(G.rmat(12, 16, 5), 2, 4)
+        srcs = sorted(random.Random(3).sample(range(g.num_vertices), 70))
+    elif case == "grid":
+        g = with_weights(G.grid(30, 20), 3, 3)
+        srcs = list(range(0, 600, 17))
+    else:
+        a = with_weights(G.random_connected(40, 30, seed=2), 4, 9)
+        src, dst, w = a.arc_src, a.arc_dst, a.arc_weight
+        keep = src < dst
+        g = P.from_edge_arrays(90, np.concatenate([src[keep], src[keep] + 45]),
+                               np.concatenate([dst[keep], dst[keep] + 45]), np.concatenate([w[keep], w[keep]]))
+        srcs = [0, 5, 44, 45, 60, 88, 89]
+    with Engine(g) as e:
+        e.set_option("groups", 2)
+        e.set_option("sssp", 1)
+        check_against_oracle(g, srcs, e)
+        e.set_option("sssp", 0)           # and the level-per-distance kernels give the same BC
+        bc_levels, _ = e.run(srcs)
+        e.set_option("sssp", 1)
+        bc_general, _ = e.run(srcs)
+    assert np.allclose(bc_levels, bc_general, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("case", ["road", "rc", "ties"])
+def test_large_weights_vs_oracle(case):
+    # DIMACS-style weights (no option set: the engine picks the general-weight sweeps)
+    if case == "road":
+        g = with_weights(G.road_like(40, 30, seed=3), 5, 200000)
+        srcs = list(range(0, 1200, 23))
+    elif case == "rc":
+        g = with_weights(G.random_connected(500, 1500, seed=7), 6, 10 ** 6)
+        srcs = list(range(0, 500, 5))
+    else:
+        # many equal-length paths under large weights: every edge weighs 5000
+        base = G.grid(20, 15)
+        src, dst = base.arc_src, base.arc_dst
+        keep = src < dst
+        g = P.from_edge_arrays(300, src[keep], dst[keep], np.full(int(keep.sum()), 5000, dtype=np.int64))
+        srcs = list(range(0, 300, 7))
+    assert int(g.arc_weight.max()) > 4096
+    with Engine(g) as e:
+        e.set_option("groups", 2)
+        st = check_against_oracle(g, srcs, e)
+    assert st["max_levels"] >= 2
+
+
+def test_general_weight_sweeps_on_the_reference_golden_vectors(weighted_golden):
+    for rec in weighted_golden["graphs"]:
+        g = graph_of(rec)
+        srcs = [s["s"] for s in rec["sources"]]
+        with Engine(g) as e:
+            e.set_option("sssp", 1)
+            dist, sigma, delta = e.debug_sources(srcs)
+            bc_all, _ = e.run(list(range(rec["n"])))
+        for i, sr in enumerate(rec["sources"]):
+            assert dist[i].tolist() == sr["dist"], (rec["name"], sr["s"])
+            assert sigma[i].tolist() == sr["sigma"], (rec["name"], sr["s"])
+            assert np.allclose(delta[i], sr["delta"], rtol=RTOL, atol=ATOL), (rec["name"], sr["s"])
+        assert np.allclose(bc_all, rec["bc_all_sources"], rtol=RTOL, atol=ATOL), rec["name"]
+
+
+def test_large_weights_through_run_bc_and_the_dimacs_loader(tmp_path):
+    # a DIMACS .gr file with road-style weights (graph.py:139-173) through the public call; the
+    # default partitioned mode steps down to 'direct' with a warning, a partitioned C call is refused
+    g0 = with_weights(G.road_like(24, 24, seed=9), 8, 50000)
+    src, dst, w = g0.arc_src, g0.arc_dst, g0.arc_weight
+    path = tmp_path / "road.gr"
+    with open(path, "w") as fh:
+        fh.write("c test graph\np sp %d %d\n" % (g0.num_vertices, len(src)))
+        for u, v, x in zip(src.tolist(), dst.tolist(), w.tolist()):
+            fh.write("a %d %d %d\n" % (u + 1, v + 1, x))
+    g = P.load_dimacs_gr(str(path))
+    assert g.num_edges == g0.num_edges and int(g.arc_weight.max()) > 4096
+    srcs = list(range(0, g.num_vertices, 11))
+    obc, _ = O.brandes_bc(g, srcs)
+    with pytest.warns(UserWarning, match="running mode 'direct'"):
+        res = P.run_bc(g, P.RunConfig(sources=srcs))
+    assert np.allclose(res.bc, obc, rtol=RTOL, atol=ATOL)
+    res = P.run_bc(g, P.RunConfig(sources=srcs, mode="direct"))
+    assert np.allclose(res.bc, obc, rtol=RTOL, atol=ATOL)
+    with Engine(g) as e:
+        e.set_partition(2, (np.arange(g.num_vertices) % 2).astype(np.int32))
+        with pytest.raises(P.InputError, match="BC_MODE_DIRECT only"):
+            e.run(srcs, MODE_BSP)
