@@ -19,7 +19,7 @@
  *     `bc_last_error()` returns the message;
  *   - one handle is driven by one host thread (reference is single-threaded);
  *     results are deterministic for a fixed (graph, sources, options);
- *   - unit weights by default; positive integer arc weights through bc_set_weights.
+ *   - unit weights by default; positive integer arc weights (int32) through bc_set_weights.
  *
  * There is no CPU implementation behind these entry points: if the CUDA
  * runtime or a device is missing, `bc_create` fails.
@@ -97,10 +97,14 @@ int bc_create(int64_t n, int64_t n_arcs, const int64_t *offsets, const int32_t *
 
 /* Positive integer arc weights, int32[n_arcs] in CSR arc order (`Graph.arc_weight`,
  * graph.py:21-61; both directions of an edge carry the same weight).  NULL or
- * all-ones selects the unit-weight kernels.  With weights a level is a distance
- * value: the forward sweep is the reference's Dijkstra order (relax.py:75-101,
- * oracle.py:44-61) taken one distance at a time.  BC_MODE_DIRECT and BC_MODE_BSP
- * only; weights above 4096 are refused. */
+ * all-ones selects the unit-weight kernels.  With weights up to 4096 a level is a
+ * distance value: the forward sweep is the reference's Dijkstra order (relax.py:75-101,
+ * oracle.py:44-61) taken one distance at a time, in every mode.  Larger weights
+ * (DIMACS road graphs, graph.py:139-173), or low-degree graphs with weights above 16
+ * where a level per distance value is out of reach, take the general-weight sweeps of
+ * csrc/bc_sssp.cuh -- label-correcting distances, then path counts and dependencies in
+ * dependency-counted order -- in BC_MODE_DIRECT only (option "sssp" overrides the
+ * choice).  Same results: dist and sigma exact, delta / BC to 1e-9. */
 int bc_set_weights(bc_handle *h, const int32_t *weights);
 
 /* Tuning knobs ("groups": 32-lane source groups per batch; "item_arcs": arcs
@@ -118,6 +122,9 @@ int bc_set_weights(bc_handle *h, const int32_t *weights);
  * "deep_compact": 1 (default) = deep (road-like) graphs sweep over level-ordered path
  * counts with one atomically updated BC vector per batch, 2 = same with per-group BC
  * partials, 0 = row layout everywhere;
+ * "sssp": weighted graphs, 1 = general-weight sweeps (csrc/bc_sssp.cuh), 0 = one level
+ * per distance value (weights up to 4096), -1 (default) = by weight range;
+ * "sssp_delta": step of the near-far distance bound there (0 = 16 mean arc weights);
  * "push_beta", "push_beta_late", "reorder": see csrc/bc_engine.cu). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);
 

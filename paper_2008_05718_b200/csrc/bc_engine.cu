@@ -192,7 +192,7 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         return BC_OK;
     }
     if (k == "sssp_delta") {
-        if (value < 0) return h->fail(BC_ERR_INPUT, "sssp_delta must be >= 0 (0 = mean arc weight)");
+        if (value < 0) return h->fail(BC_ERR_INPUT, "sssp_delta must be >= 0 (0 = 16 mean arc weights)");
         h->sp_delta = value;
         return BC_OK;
     }

@@ -9,7 +9,7 @@
 //   A  label-correcting distances, near-far style: a (vertex, source) pair whose distance dropped
 //      is dirty; dirty pairs below a threshold push dist + w to their neighbours with a 64-bit
 //      atomic min, the others wait.  When a round finds nothing below the threshold, the threshold
-//      moves to the smallest waiting distance plus delta (the mean arc weight); when nothing is
+//      moves to the smallest waiting distance plus a step (16 mean arc weights); when nothing is
 //      dirty the distances are final -- the same array Dijkstra produces.  Every round works out
 //      its threshold from what the previous round recorded, so there is no host round trip and
 //      no control kernel in between.
@@ -65,10 +65,8 @@ struct SsspParams {
 };
 
 constexpr int kSsspWarps = 4;
-// vertices per warp and round.  A warp walks its frontier vertices one after the other, each a
-// chain of dependent loads (arcs -> neighbour's row -> atomic), so a narrow chunk keeps the
-// slowest warp of a round short: 32 -> 8 vertices took the rounds of a 1024^2 road grid from
-// ~100 us to the launch floor.
+// vertices per warp and chunk (8 instead of 32 was tried: four times the warps scanning the mask
+// array cost more than the shorter visit chains gained on a 1024^2 road grid)
 constexpr int kSsspChunk = 32;
 
 // One warp owns kSsspChunk consecutive vertices; returns the first one and this lane's frontier mask
@@ -85,6 +83,49 @@ __device__ __forceinline__ bool sssp_take_chunk(const SsspParams &p, size_t g, i
         if (mask) *w = 0;
     }
     return true;
+}
+
+// Sparse frontiers (a road network: a couple of sources per frontier vertex) leave most lanes of
+// a row-per-vertex visit idle while the warp walks its frontier vertices one after the other, each
+// visit a chain of dependent loads.  When a chunk holds fewer than kSsspPairLanes frontier pairs
+// per frontier vertex, its pairs are dealt out one per thread instead: every chain runs at once.
+constexpr int kSsspPairLanes = 16;
+
+struct ChunkPairs {
+    int total;    // frontier pairs in the chunk
+    int excl;     // pairs of the vertices before this lane's vertex
+    uint32_t mask;
+    // pair t of the chunk -> vertex index in the chunk and source lane (all threads call it)
+    __device__ __forceinline__ bool get(int t, int &i, int &src_lane) const {
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int cand = lo + step;
+            const int e = __shfl_sync(kFull, excl, cand & 31);
+            if (e <= t) lo = cand;
+        }
+        const uint32_t m = __shfl_sync(kFull, mask, lo);
+        const int first = __shfl_sync(kFull, excl, lo);
+        i = lo;
+        if (t >= total) return false;
+        src_lane = (int)__fns(m, 0, t - first + 1);
+        return true;
+    }
+};
+
+__device__ __forceinline__ ChunkPairs chunk_pairs(uint32_t mask, int lane) {
+    ChunkPairs c;
+    const int mine = __popc(mask);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+    }
+    c.excl = incl - mine;
+    c.total = __shfl_sync(kFull, incl, 31);
+    c.mask = mask;
+    return c;
 }
 
 __global__ void fill_i64_kernel(long long *p, size_t count, long long value) {
@@ -143,6 +184,31 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_relax_kernel(const SsspP
         uint32_t mask;
         if (!sssp_take_chunk(p, g, lane, chunk, v0, mask)) break;
         unsigned need = __ballot_sync(kFull, mask != 0);
+        if (need == 0) continue;
+        const ChunkPairs cp = chunk_pairs(mask, lane);
+        if (__popc(need) > 1 && cp.total < kSsspPairLanes * __popc(need)) {
+            // ---- one dirty pair per thread
+            for (int t0 = 0; t0 < cp.total; t0 += 32) {
+                int i, sl;
+                if (!cp.get(t0 + lane, i, sl)) continue;
+                const int64_t u = v0 + i;
+                const long long du = dist[u * 32 + sl];
+                if (du >= bound) {
+                    atomicOr(next + u, 1u << sl);   // still dirty next round
+                    waiting = min(waiting, du);
+                    produced |= 1;
+                    continue;
+                }
+                produced |= 2;
+                for (int64_t a = p.off[u]; a < p.off[u + 1]; ++a) {
+                    const int32_t w = __ldg(p.col + a);
+                    const long long cand = du + __ldg(p.wgt + a);
+                    long long *d = dist + (size_t)w * 32 + sl;
+                    if (cand < *d && cand < atomicMin(d, cand)) atomicOr(next + w, 1u << sl);
+                }
+            }
+            continue;
+        }
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
@@ -277,6 +343,31 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_forward_kernel(const Sss
         uint32_t mask;
         if (!sssp_take_chunk(p, g, lane, chunk, v0, mask)) break;
         unsigned need = __ballot_sync(kFull, mask != 0);
+        if (need == 0) continue;
+        const ChunkPairs cp = chunk_pairs(mask, lane);
+        if (__popc(need) > 1 && cp.total < kSsspPairLanes * __popc(need)) {
+            // ---- one ready pair per thread (same arc order, so the same sums)
+            for (int t0 = 0; t0 < cp.total; t0 += 32) {
+                int i, sl;
+                if (!cp.get(t0 + lane, i, sl)) continue;
+                const int64_t v = v0 + i;
+                const long long dv = dist[v * 32 + sl];
+                double acc = 0.0;
+                for (int64_t a = p.off[v]; a < p.off[v + 1]; ++a) {
+                    const int32_t w = __ldg(p.col + a);
+                    const int32_t wt = __ldg(p.wgt + a);
+                    const size_t idx = (size_t)w * 32 + sl;
+                    const long long dw = dist[idx];
+                    if (dw + wt == dv) acc += sigma[idx];
+                    else if (dv + wt == dw && atomicSub(npar + idx, 1) == 1) {
+                        atomicOr(next + w, 1u << sl);
+                        produced = true;
+                    }
+                }
+                sigma[v * 32 + sl] = dv == 0 ? 1.0 : acc;
+            }
+            continue;
+        }
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
@@ -313,7 +404,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_forward_kernel(const Sss
             if (on) sigma[v * 32 + lane] = dv == 0 ? 1.0 : acc;
         }
     }
-    if (produced && lane == 0) p.flags[p.round] = 1;
+    if (__any_sync(kFull, produced) && lane == 0) p.flags[p.round] = 1;   // (per thread in the pair branch)
 }
 
 // Phase D, one round: ready pairs pull coef from their children, release their parents.
@@ -334,6 +425,36 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_backward_kernel(const Ss
         uint32_t mask;
         if (!sssp_take_chunk(p, g, lane, chunk, v0, mask)) break;
         unsigned need = __ballot_sync(kFull, mask != 0);
+        if (need == 0) continue;
+        const ChunkPairs cp = chunk_pairs(mask, lane);
+        if (__popc(need) > 1 && cp.total < kSsspPairLanes * __popc(need)) {
+            // ---- one ready pair per thread; the BC partial takes the pair's delta with an atomic add
+            for (int t0 = 0; t0 < cp.total; t0 += 32) {
+                int i, sl;
+                if (!cp.get(t0 + lane, i, sl)) continue;
+                const int64_t v = v0 + i;
+                const size_t me = (size_t)v * 32 + sl;
+                const long long dv = dist[me];
+                double acc = 0.0;
+                for (int64_t a = p.off[v]; a < p.off[v + 1]; ++a) {
+                    const int32_t w = __ldg(p.col + a);
+                    const int32_t wt = __ldg(p.wgt + a);
+                    const size_t idx = (size_t)w * 32 + sl;
+                    const long long dw = dist[idx];
+                    if (dv + wt == dw) acc += coef[idx];
+                    else if (dw + wt == dv && atomicSub(nchild + idx, 1) == 1) {
+                        atomicOr(next + w, 1u << sl);
+                        produced = true;
+                    }
+                }
+                const double sv = sigma[me];
+                const double d = sv * acc;
+                coef[me] = (1.0 + d) / sv;
+                if (p.delta) p.delta[g * p.n * 32 + me] = d;
+                if (p.accumulate && dv != 0 && d != 0.0) atomicAdd(p.bcg + g * p.n + v, d);
+            }
+            continue;
+        }
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
@@ -382,7 +503,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_backward_kernel(const Ss
             }
         }
     }
-    if (produced && lane == 0) p.flags[p.round] = 1;
+    if (__any_sync(kFull, produced) && lane == 0) p.flags[p.round] = 1;   // (per thread in the pair branch)
 }
 
 // Inspection: rows [v][32] of one group -> [lane][n] arrays (BC_UNREACHED / 0 where unreached).

@@ -173,7 +173,9 @@ int run_sources_sssp(bc_handle *h, const int64_t *sources_in, int64_t k_all, dou
         p.flags = h->sp_flags;
         p.threshold = h->sp_bound;
         p.far_min = h->sp_bound + kSsspFlagCap;
-        p.step = h->sp_delta > 0 ? h->sp_delta : std::max<long long>(1, h->wsum / std::max<int64_t>(h->n_arcs, 1));
+        // bound step: small = little wasted relaxation but many rounds; 16 mean weights was the best
+        // of 1 .. 60 on a 1024^2 road grid with weights up to 10^5 (419 / 221 / 162 / 170 ms)
+        p.step = h->sp_delta > 0 ? h->sp_delta : std::max<long long>(1, 16 * (h->wsum / std::max<int64_t>(h->n_arcs, 1)));
         p.accumulate = debug ? 0 : 1;
         p.counters = h->counters;
         sssp_init_kernel<<<dim3(grid1d((size_t)n * 32, 256, 2368), ng), 256, 0, st>>>(p.dist, p.cur, p.next, p.leaf, n);

@@ -174,7 +174,7 @@ struct bc_handle {
     uint32_t *sp_maskA = nullptr, *sp_maskB = nullptr, *sp_leaf = nullptr;
     int *sp_flags = nullptr;
     long long *sp_bound = nullptr;   // per round: distance bound, smallest waiting distance (phase A)
-    long long sp_delta = 0;          // option "sssp_delta": step of the bound (0 = mean arc weight)
+    long long sp_delta = 0;          // option "sssp_delta": step of the bound (0 = 16 mean arc weights)
     long long wsum = 0;              // sum of the arc weights
     int sp_groups = 0;
     int cur_depth = 0;        // levels of the batch being swept backward (weighted kernels)
