@@ -191,6 +191,10 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         h->wgt_mode = (int)value;
         return BC_OK;
     }
+    if (k == "sssp_blocks") {
+        h->sp_blocks = (int)std::max<int64_t>(0, std::min<int64_t>(value, 1 << 16));
+        return BC_OK;
+    }
     if (k == "sssp_delta") {
         if (value < 0) return h->fail(BC_ERR_INPUT, "sssp_delta must be >= 0 (0 = 16 mean arc weights)");
         h->sp_delta = value;

@@ -24,10 +24,11 @@
 //      division hoisted, as in finalize_backward) and releases its parents.
 //
 // 32 sources share a warp as everywhere else: per group g, rows [v][32] of dist / sigma / coef /
-// counts and one 32-bit lane mask per vertex for "in this round's frontier".  Rounds of C and D
-// are as many as the DAG is deep in arcs; every round is one launch over the mask array, and a
-// launch whose predecessor produced nothing returns at once (the host launches rounds in
-// chunks and reads the flags afterwards, as forward_sweep does).
+// counts, one 32-bit lane mask per vertex for "in this round's frontier" and a queue of the
+// vertices whose mask is not empty (a vertex enters when its mask goes from zero to non-zero).
+// Rounds of C and D are as many as the DAG is deep in arcs; every round is one launch over the
+// queue, and a launch whose predecessor produced nothing returns at once (the host launches
+// rounds in chunks and reads the flags afterwards, as forward_sweep does).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -52,6 +53,14 @@ struct SsspParams {
     uint32_t *cur;     // [G][n] lanes in this round's frontier (cleared as they are consumed)
     uint32_t *next;    // [G][n] lanes in the next round's frontier
     uint32_t *leaf;    // [G][n] pairs without children (phase B -> first frontier of phase D)
+    // frontier queues: the vertices whose word in cur / next is not zero, in the order they got there
+    int32_t *q_cur;    // [G][n]
+    int32_t *q_next;   // [G][n]
+    int32_t *q_leaf;   // [G][n] (phase B -> first queue of phase D)
+    int *q_count;      // [3][G] queue lengths, rotating: this round reads slot qs_in, fills qs_out, clears qs_zero
+    int *q_leaf_count; // [G]
+    int qs_in, qs_out, qs_zero;
+    int G;             // groups the state arrays were sized for (stride of q_count)
     double *bcg;       // [G][n] BC partial of the group
     int *flags;        // flags[r] != 0: round r put something into `next`
     int round;
@@ -65,24 +74,39 @@ struct SsspParams {
 };
 
 constexpr int kSsspWarps = 4;
-// vertices per warp and chunk (8 instead of 32 was tried: four times the warps scanning the mask
-// array cost more than the shorter visit chains gained on a 1024^2 road grid)
+// A warp takes 32 queue entries at a time: lane i holds vertex myv and its frontier mask (consumed:
+// the word is cleared so the mask array is empty when it becomes `next` again).  Scanning the
+// whole mask array every round instead (the first version) cost 0.7 us of load latency per
+// 32-vertex chunk and warp slot, empty or not: ~100 us per round on a 1024^2 grid with four groups.
 constexpr int kSsspChunk = 32;
 
-// One warp owns kSsspChunk consecutive vertices; returns the first one and this lane's frontier mask
-// (consumed: the word is cleared so the buffer is empty when it becomes `next` again).
-__device__ __forceinline__ bool sssp_take_chunk(const SsspParams &p, size_t g, int lane, int64_t chunk,
-                                                int64_t &v0, uint32_t &mask) {
-    v0 = chunk * kSsspChunk;
-    if (v0 >= p.n) return false;
-    const int64_t v = v0 + lane;
+__device__ __forceinline__ void sssp_take_items(const SsspParams &p, size_t g, int lane, int base, int count,
+                                                int32_t &myv, uint32_t &mask) {
+    myv = -1;
     mask = 0;
-    if (lane < kSsspChunk && v < p.n) {
-        uint32_t *w = p.cur + g * p.n + v;
+    if (base + lane < count) {
+        myv = p.q_cur[g * p.n + base + lane];
+        uint32_t *w = p.cur + g * p.n + myv;
         mask = *w;
-        if (mask) *w = 0;
+        *w = 0;
     }
+}
+
+// Round prologue: false = the sweep ended before this round.  One thread clears the queue length
+// slot nobody uses in this round (it was the input of the previous one).
+__device__ __forceinline__ bool sssp_round_begin(const SsspParams &p, size_t g, int &count) {
+    if (p.round > 0 && p.flags[p.round - 1] == 0) return false;
+    count = p.q_count[p.qs_in * p.G + g];
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.q_count[p.qs_zero * p.G + g] = 0;
     return true;
+}
+
+// lanes `bits` of vertex w join the next frontier
+__device__ __forceinline__ void sssp_push(const SsspParams &p, size_t g, int32_t w, uint32_t bits) {
+    if (atomicOr(p.next + g * p.n + w, bits) == 0) {
+        const int pos = atomicAdd(p.q_count + p.qs_out * p.G + g, 1);
+        p.q_next[g * p.n + pos] = w;
+    }
 }
 
 // Sparse frontiers (a road network: a couple of sources per frontier vertex) leave most lanes of
@@ -95,8 +119,9 @@ struct ChunkPairs {
     int total;    // frontier pairs in the chunk
     int excl;     // pairs of the vertices before this lane's vertex
     uint32_t mask;
-    // pair t of the chunk -> vertex index in the chunk and source lane (all threads call it)
-    __device__ __forceinline__ bool get(int t, int &i, int &src_lane) const {
+    int32_t myv;  // this lane's vertex
+    // pair t of the chunk -> its vertex and source lane (all threads call it)
+    __device__ __forceinline__ bool get(int t, int64_t &vertex, int &src_lane) const {
         int lo = 0;
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1) {
@@ -106,14 +131,14 @@ struct ChunkPairs {
         }
         const uint32_t m = __shfl_sync(kFull, mask, lo);
         const int first = __shfl_sync(kFull, excl, lo);
-        i = lo;
+        vertex = __shfl_sync(kFull, myv, lo);
         if (t >= total) return false;
         src_lane = (int)__fns(m, 0, t - first + 1);
         return true;
     }
 };
 
-__device__ __forceinline__ ChunkPairs chunk_pairs(uint32_t mask, int lane) {
+__device__ __forceinline__ ChunkPairs chunk_pairs(uint32_t mask, int32_t myv, int lane) {
     ChunkPairs c;
     const int mine = __popc(mask);
     int incl = mine;
@@ -125,8 +150,34 @@ __device__ __forceinline__ ChunkPairs chunk_pairs(uint32_t mask, int lane) {
     c.excl = incl - mine;
     c.total = __shfl_sync(kFull, incl, 31);
     c.mask = mask;
+    c.myv = myv;
     return c;
 }
+
+// A pair's visit is a chain of dependent loads per arc (neighbour id -> its distance -> its value
+// or counter); arcs are taken kSsspArcBatch at a time so the chains of a batch overlap.
+constexpr int kSsspArcBatch = 4;
+
+struct ArcBatch {
+    int32_t w[kSsspArcBatch];
+    int32_t wt[kSsspArcBatch];
+    long long dw[kSsspArcBatch];
+    int cnt;
+    __device__ __forceinline__ void load(const SsspParams &p, const long long *dist, int64_t a, int64_t a1, int sl) {
+        cnt = (int)min((int64_t)kSsspArcBatch, a1 - a);
+#pragma unroll
+        for (int j = 0; j < kSsspArcBatch; ++j) {
+            w[j] = 0;
+            wt[j] = 0;
+            if (j < cnt) {
+                w[j] = __ldg(p.col + a + j);
+                wt[j] = __ldg(p.wgt + a + j);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kSsspArcBatch; ++j) dw[j] = j < cnt ? dist[(size_t)w[j] * 32 + sl] : kSsspInf;
+    }
+};
 
 __global__ void fill_i64_kernel(long long *p, size_t count, long long value) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
@@ -149,7 +200,8 @@ __global__ void sssp_init_kernel(long long *dist, uint32_t *cur, uint32_t *next,
 }
 
 // Sources: distance 0, in the first frontier of phase A.
-__global__ void sssp_seed_kernel(const int64_t *src, int count, int64_t n, long long *dist, uint32_t *cur) {
+__global__ void sssp_seed_kernel(const int64_t *src, int count, int64_t n, long long *dist, uint32_t *cur,
+                                 int32_t *q_cur, int *q_count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     const size_t g = i >> 5;
@@ -157,7 +209,7 @@ __global__ void sssp_seed_kernel(const int64_t *src, int count, int64_t n, long 
     const int64_t v = src[i];
     if (v < 0) return;
     dist[(g * n + v) * 32 + lane] = 0;
-    atomicOr(cur + g * n + v, 1u << lane);
+    if (atomicOr(cur + g * n + v, 1u << lane) == 0) q_cur[g * n + atomicAdd(q_count + g, 1)] = (int32_t)v;
 }
 
 // Phase A, one round: dirty pairs below the round's distance bound relax their arcs; the others
@@ -166,45 +218,54 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_relax_kernel(const SsspP
     const size_t g = blockIdx.y;
     const int lane = threadIdx.x & 31;
     long long bound = p.threshold[0];
+    int count;
+    if (!sssp_round_begin(p, g, count)) return;   // nothing dirty: the distances are final
     if (p.round > 0) {
-        if (p.flags[p.round - 1] == 0) return;   // nothing dirty: the distances are final
         bound = p.threshold[p.round - 1];
         // the previous round relaxed nothing: move the bound past the nearest waiting pair
         if (p.flags[p.round - 1] == 1) bound = p.far_min[p.round - 1] + p.step;
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) p.threshold[p.round] = bound;
     }
     long long *dist = p.dist + g * p.n * 32;
-    uint32_t *next = p.next + g * p.n;
     int produced = 0;             // 2: relaxed something, 1: left pairs waiting
     long long waiting = kSsspInf;  // smallest distance left waiting (this lane)
-    const int64_t n_chunks = (p.n + kSsspChunk - 1) / kSsspChunk;
-    for (int64_t chunk = (int64_t)blockIdx.x * kSsspWarps + (threadIdx.x >> 5); chunk < n_chunks;
-         chunk += (int64_t)gridDim.x * kSsspWarps) {
-        int64_t v0;
+    for (int base = (blockIdx.x * kSsspWarps + (threadIdx.x >> 5)) * 32; base < count;
+         base += gridDim.x * kSsspWarps * 32) {
+        int32_t myv;
         uint32_t mask;
-        if (!sssp_take_chunk(p, g, lane, chunk, v0, mask)) break;
+        sssp_take_items(p, g, lane, base, count, myv, mask);
         unsigned need = __ballot_sync(kFull, mask != 0);
         if (need == 0) continue;
-        const ChunkPairs cp = chunk_pairs(mask, lane);
+        const ChunkPairs cp = chunk_pairs(mask, myv, lane);
         if (__popc(need) > 1 && cp.total < kSsspPairLanes * __popc(need)) {
             // ---- one dirty pair per thread
             for (int t0 = 0; t0 < cp.total; t0 += 32) {
-                int i, sl;
-                if (!cp.get(t0 + lane, i, sl)) continue;
-                const int64_t u = v0 + i;
+                int sl;
+                int64_t u;
+                if (!cp.get(t0 + lane, u, sl)) continue;
                 const long long du = dist[u * 32 + sl];
                 if (du >= bound) {
-                    atomicOr(next + u, 1u << sl);   // still dirty next round
+                    sssp_push(p, g, (int32_t)u, 1u << sl);   // still dirty next round
                     waiting = min(waiting, du);
                     produced |= 1;
                     continue;
                 }
                 produced |= 2;
-                for (int64_t a = p.off[u]; a < p.off[u + 1]; ++a) {
-                    const int32_t w = __ldg(p.col + a);
-                    const long long cand = du + __ldg(p.wgt + a);
-                    long long *d = dist + (size_t)w * 32 + sl;
-                    if (cand < *d && cand < atomicMin(d, cand)) atomicOr(next + w, 1u << sl);
+                const int64_t a1 = p.off[u + 1];
+                for (int64_t a = p.off[u]; a < a1; a += kSsspArcBatch) {
+                    ArcBatch ab;
+                    ab.load(p, dist, a, a1, sl);
+                    long long old[kSsspArcBatch];
+#pragma unroll
+                    for (int j = 0; j < kSsspArcBatch; ++j) {
+                        old[j] = 0;
+                        if (j < ab.cnt && du + ab.wt[j] < ab.dw[j])
+                            old[j] = atomicMin(dist + (size_t)ab.w[j] * 32 + sl, du + ab.wt[j]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < kSsspArcBatch; ++j)
+                        if (j < ab.cnt && du + ab.wt[j] < ab.dw[j] && du + ab.wt[j] < old[j])
+                            sssp_push(p, g, ab.w[j], 1u << sl);
                 }
             }
             continue;
@@ -212,14 +273,14 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_relax_kernel(const SsspP
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
-            const int64_t u = v0 + i;
+            const int64_t u = __shfl_sync(kFull, myv, i);
             const uint32_t mu = __shfl_sync(kFull, mask, i);
             const bool dirty = (mu >> lane) & 1u;
             const long long du = dirty ? dist[u * 32 + lane] : kSsspInf;
             const bool on = dirty && du < bound;
             const unsigned far = __ballot_sync(kFull, dirty && !on);
             if (far) {
-                if (lane == 0) atomicOr(next + u, far);   // still dirty next round
+                if (lane == 0) sssp_push(p, g, (int32_t)u, far);   // still dirty next round
                 if (dirty && !on) waiting = min(waiting, du);
                 produced |= 1;
             }
@@ -243,7 +304,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_relax_kernel(const SsspP
                         if (cand < *d) better = cand < atomicMin(d, cand);
                     }
                     const unsigned b = __ballot_sync(kFull, better);
-                    if (b && lane == 0) atomicOr(next + w, b);
+                    if (b && lane == 0) sssp_push(p, g, w, b);
                 }
             }
         }
@@ -312,6 +373,15 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_count_kernel(const SsspP
     if (lane < nv) {
         p.cur[g * p.n + v0 + lane] = src_mask;
         p.leaf[g * p.n + v0 + lane] = leaf_mask;
+        if (src_mask) p.q_cur[g * p.n + atomicAdd(p.q_count + p.qs_in * p.G + g, 1)] = (int32_t)(v0 + lane);
+    }
+    {
+        // leaves in one reservation per warp
+        const unsigned has = __ballot_sync(kFull, leaf_mask != 0);
+        int qbase = 0;
+        if (lane == 0 && has) qbase = atomicAdd(p.q_leaf_count + g, __popc(has));
+        qbase = __shfl_sync(kFull, qbase, 0);
+        if (leaf_mask) p.q_leaf[g * p.n + qbase + __popc(has & ((1u << lane) - 1u))] = (int32_t)(v0 + lane);
     }
     c_reached = __reduce_add_sync(kFull, (unsigned)c_reached);
     // (per-lane partials are below 2^32 only for the first; the others go through 64-bit adds)
@@ -330,38 +400,49 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_count_kernel(const SsspP
 __global__ void __launch_bounds__(kSsspWarps * 32) sssp_forward_kernel(const SsspParams p) {
     const size_t g = blockIdx.y;
     const int lane = threadIdx.x & 31;
-    if (p.round > 0 && p.flags[p.round - 1] == 0) return;   // the sweep ended before this round
+    int count;
+    if (!sssp_round_begin(p, g, count)) return;   // the sweep ended before this round
     bool produced = false;
     const long long *dist = p.dist + g * p.n * 32;
     double *sigma = p.sigma + g * p.n * 32;
     int *npar = p.npar + g * p.n * 32;
-    uint32_t *next = p.next + g * p.n;
-    const int64_t n_chunks = (p.n + kSsspChunk - 1) / kSsspChunk;
-    for (int64_t chunk = (int64_t)blockIdx.x * kSsspWarps + (threadIdx.x >> 5); chunk < n_chunks;
-         chunk += (int64_t)gridDim.x * kSsspWarps) {
-        int64_t v0;
+    for (int base = (blockIdx.x * kSsspWarps + (threadIdx.x >> 5)) * 32; base < count;
+         base += gridDim.x * kSsspWarps * 32) {
+        int32_t myv;
         uint32_t mask;
-        if (!sssp_take_chunk(p, g, lane, chunk, v0, mask)) break;
+        sssp_take_items(p, g, lane, base, count, myv, mask);
         unsigned need = __ballot_sync(kFull, mask != 0);
         if (need == 0) continue;
-        const ChunkPairs cp = chunk_pairs(mask, lane);
+        const ChunkPairs cp = chunk_pairs(mask, myv, lane);
         if (__popc(need) > 1 && cp.total < kSsspPairLanes * __popc(need)) {
             // ---- one ready pair per thread (same arc order, so the same sums)
             for (int t0 = 0; t0 < cp.total; t0 += 32) {
-                int i, sl;
-                if (!cp.get(t0 + lane, i, sl)) continue;
-                const int64_t v = v0 + i;
+                int sl;
+                int64_t v;
+                if (!cp.get(t0 + lane, v, sl)) continue;
                 const long long dv = dist[v * 32 + sl];
                 double acc = 0.0;
-                for (int64_t a = p.off[v]; a < p.off[v + 1]; ++a) {
-                    const int32_t w = __ldg(p.col + a);
-                    const int32_t wt = __ldg(p.wgt + a);
-                    const size_t idx = (size_t)w * 32 + sl;
-                    const long long dw = dist[idx];
-                    if (dw + wt == dv) acc += sigma[idx];
-                    else if (dv + wt == dw && atomicSub(npar + idx, 1) == 1) {
-                        atomicOr(next + w, 1u << sl);
-                        produced = true;
+                const int64_t a1 = p.off[v + 1];
+                for (int64_t a = p.off[v]; a < a1; a += kSsspArcBatch) {
+                    ArcBatch ab;
+                    ab.load(p, dist, a, a1, sl);
+                    double x[kSsspArcBatch];
+                    int left[kSsspArcBatch];
+#pragma unroll
+                    for (int j = 0; j < kSsspArcBatch; ++j) {
+                        const size_t idx = (size_t)ab.w[j] * 32 + sl;
+                        x[j] = 0.0;
+                        left[j] = 0;
+                        if (j < ab.cnt && ab.dw[j] + ab.wt[j] == dv) x[j] = sigma[idx];               // a parent
+                        else if (j < ab.cnt && dv + ab.wt[j] == ab.dw[j]) left[j] = atomicSub(npar + idx, 1);  // a child
+                    }
+#pragma unroll
+                    for (int j = 0; j < kSsspArcBatch; ++j) {
+                        acc += x[j];   // arc order
+                        if (left[j] == 1) {
+                            sssp_push(p, g, ab.w[j], 1u << sl);
+                            produced = true;
+                        }
                     }
                 }
                 sigma[v * 32 + sl] = dv == 0 ? 1.0 : acc;
@@ -371,7 +452,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_forward_kernel(const Sss
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
-            const int64_t v = v0 + i;
+            const int64_t v = __shfl_sync(kFull, myv, i);
             const uint32_t mv = __shfl_sync(kFull, mask, i);
             const bool on = (mv >> lane) & 1u;
             const long long dv = on ? dist[v * 32 + lane] : kSsspInf;
@@ -396,7 +477,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_forward_kernel(const Sss
                     }
                     const unsigned b = __ballot_sync(kFull, released);
                     if (b) {
-                        if (lane == 0) atomicOr(next + w, b);
+                        if (lane == 0) sssp_push(p, g, w, b);
                         produced = true;
                     }
                 }
@@ -411,40 +492,51 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_forward_kernel(const Sss
 __global__ void __launch_bounds__(kSsspWarps * 32) sssp_backward_kernel(const SsspParams p) {
     const size_t g = blockIdx.y;
     const int lane = threadIdx.x & 31;
-    if (p.round > 0 && p.flags[p.round - 1] == 0) return;   // the sweep ended before this round
+    int count;
+    if (!sssp_round_begin(p, g, count)) return;   // the sweep ended before this round
     bool produced = false;
     const long long *dist = p.dist + g * p.n * 32;
     const double *sigma = p.sigma + g * p.n * 32;
     double *coef = p.coef + g * p.n * 32;
     int *nchild = p.nchild + g * p.n * 32;
-    uint32_t *next = p.next + g * p.n;
-    const int64_t n_chunks = (p.n + kSsspChunk - 1) / kSsspChunk;
-    for (int64_t chunk = (int64_t)blockIdx.x * kSsspWarps + (threadIdx.x >> 5); chunk < n_chunks;
-         chunk += (int64_t)gridDim.x * kSsspWarps) {
-        int64_t v0;
+    for (int base = (blockIdx.x * kSsspWarps + (threadIdx.x >> 5)) * 32; base < count;
+         base += gridDim.x * kSsspWarps * 32) {
+        int32_t myv;
         uint32_t mask;
-        if (!sssp_take_chunk(p, g, lane, chunk, v0, mask)) break;
+        sssp_take_items(p, g, lane, base, count, myv, mask);
         unsigned need = __ballot_sync(kFull, mask != 0);
         if (need == 0) continue;
-        const ChunkPairs cp = chunk_pairs(mask, lane);
+        const ChunkPairs cp = chunk_pairs(mask, myv, lane);
         if (__popc(need) > 1 && cp.total < kSsspPairLanes * __popc(need)) {
             // ---- one ready pair per thread; the BC partial takes the pair's delta with an atomic add
             for (int t0 = 0; t0 < cp.total; t0 += 32) {
-                int i, sl;
-                if (!cp.get(t0 + lane, i, sl)) continue;
-                const int64_t v = v0 + i;
+                int sl;
+                int64_t v;
+                if (!cp.get(t0 + lane, v, sl)) continue;
                 const size_t me = (size_t)v * 32 + sl;
                 const long long dv = dist[me];
                 double acc = 0.0;
-                for (int64_t a = p.off[v]; a < p.off[v + 1]; ++a) {
-                    const int32_t w = __ldg(p.col + a);
-                    const int32_t wt = __ldg(p.wgt + a);
-                    const size_t idx = (size_t)w * 32 + sl;
-                    const long long dw = dist[idx];
-                    if (dv + wt == dw) acc += coef[idx];
-                    else if (dw + wt == dv && atomicSub(nchild + idx, 1) == 1) {
-                        atomicOr(next + w, 1u << sl);
-                        produced = true;
+                const int64_t a1 = p.off[v + 1];
+                for (int64_t a = p.off[v]; a < a1; a += kSsspArcBatch) {
+                    ArcBatch ab;
+                    ab.load(p, dist, a, a1, sl);
+                    double x[kSsspArcBatch];
+                    int left[kSsspArcBatch];
+#pragma unroll
+                    for (int j = 0; j < kSsspArcBatch; ++j) {
+                        const size_t idx = (size_t)ab.w[j] * 32 + sl;
+                        x[j] = 0.0;
+                        left[j] = 0;
+                        if (j < ab.cnt && dv + ab.wt[j] == ab.dw[j]) x[j] = coef[idx];                   // a child
+                        else if (j < ab.cnt && ab.dw[j] + ab.wt[j] == dv) left[j] = atomicSub(nchild + idx, 1);  // a parent
+                    }
+#pragma unroll
+                    for (int j = 0; j < kSsspArcBatch; ++j) {
+                        acc += x[j];   // arc order
+                        if (left[j] == 1) {
+                            sssp_push(p, g, ab.w[j], 1u << sl);
+                            produced = true;
+                        }
                     }
                 }
                 const double sv = sigma[me];
@@ -458,7 +550,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_backward_kernel(const Ss
         while (need) {
             const int i = __ffs(need) - 1;
             need &= need - 1;
-            const int64_t v = v0 + i;
+            const int64_t v = __shfl_sync(kFull, myv, i);
             const uint32_t mv = __shfl_sync(kFull, mask, i);
             const bool on = (mv >> lane) & 1u;
             const long long dv = on ? dist[v * 32 + lane] : kSsspInf;
@@ -483,7 +575,7 @@ __global__ void __launch_bounds__(kSsspWarps * 32) sssp_backward_kernel(const Ss
                     }
                     const unsigned b = __ballot_sync(kFull, released);
                     if (b) {
-                        if (lane == 0) atomicOr(next + w, b);
+                        if (lane == 0) sssp_push(p, g, w, b);
                         produced = true;
                     }
                 }

@@ -28,6 +28,8 @@ int ensure_sssp_state(bc_handle *h, int groups) {
     CUDA_TRY(h, arena_malloc((void **)&h->sp_leaf, groups * n * sizeof(uint32_t)));
     CUDA_TRY(h, arena_malloc((void **)&h->sp_flags, kSsspFlagCap * sizeof(int)));
     CUDA_TRY(h, arena_malloc((void **)&h->sp_bound, 2 * kSsspFlagCap * sizeof(long long)));
+    CUDA_TRY(h, arena_malloc((void **)&h->sp_queue, 3 * groups * n * sizeof(int32_t)));
+    CUDA_TRY(h, arena_malloc((void **)&h->sp_qcount, 4 * (size_t)groups * sizeof(int)));
     h->sp_groups = groups;
     return BC_OK;
 }
@@ -38,8 +40,10 @@ int ensure_sssp_state(bc_handle *h, int groups) {
 template <typename Kernel>
 int sssp_rounds(bc_handle *h, Kernel kernel, SsspParams &p, int ng, cudaStream_t st, int64_t *rounds_out,
                 bool near_far = false) {
+    // one wave of blocks over all groups; a warp takes 32 queue entries per step
     const int64_t warps = (h->n + kSsspChunk - 1) / kSsspChunk;
-    const unsigned blocks = (unsigned)std::min<int64_t>((warps + kSsspWarps - 1) / kSsspWarps, 148 * 8);
+    const unsigned blocks = (unsigned)std::min<int64_t>((warps + kSsspWarps - 1) / kSsspWarps,
+                                                        std::max(h->sp_blocks > 0 ? h->sp_blocks : 296, 148 * 8 / ng));
     const dim3 grid(blocks, (unsigned)ng);
     int64_t rounds = 0;
     int chunk = 8;
@@ -61,6 +65,10 @@ int sssp_rounds(bc_handle *h, Kernel kernel, SsspParams &p, int ng, cudaStream_t
                 p.round = r + j;
                 kernel<<<grid, kSsspWarps * 32, 0, st>>>(p);
                 std::swap(p.cur, p.next);
+                std::swap(p.q_cur, p.q_next);
+                p.qs_zero = p.qs_in;              // consumed: cleared by the round after next
+                p.qs_in = p.qs_out;
+                p.qs_out = 3 - p.qs_zero - p.qs_in;
                 ++h->launches;
             }
             flags.assign(m, 0);
@@ -178,8 +186,23 @@ int run_sources_sssp(bc_handle *h, const int64_t *sources_in, int64_t k_all, dou
         p.step = h->sp_delta > 0 ? h->sp_delta : std::max<long long>(1, 16 * (h->wsum / std::max<int64_t>(h->n_arcs, 1)));
         p.accumulate = debug ? 0 : 1;
         p.counters = h->counters;
+        const size_t G = (size_t)h->sp_groups;
+        p.G = (int)G;
+        p.q_cur = h->sp_queue;
+        p.q_next = h->sp_queue + G * (size_t)n;
+        p.q_leaf = h->sp_queue + 2 * G * (size_t)n;
+        p.q_count = h->sp_qcount;
+        p.q_leaf_count = h->sp_qcount + 3 * G;
+        // queue length slots: a phase starts with its first frontier in slot 0, the others empty
+        auto reset_slots = [&]() -> int {
+            CUDA_TRY(h, cudaMemsetAsync(p.q_count, 0, 3 * G * sizeof(int), st));
+            p.qs_in = 0, p.qs_out = 1, p.qs_zero = 2;
+            return BC_OK;
+        };
+        TRY(reset_slots());
+        CUDA_TRY(h, cudaMemsetAsync(p.q_leaf_count, 0, G * sizeof(int), st));
         sssp_init_kernel<<<dim3(grid1d((size_t)n * 32, 256, 2368), ng), 256, 0, st>>>(p.dist, p.cur, p.next, p.leaf, n);
-        sssp_seed_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * S, cnt, n, p.dist, p.cur);
+        sssp_seed_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(h->d_src + b * S, cnt, n, p.dist, p.cur, p.q_cur, p.q_count);
         h->launches += 2;
         // ---- A: distances
         int64_t rounds_a = 0, rounds_c = 0, rounds_d = 0;
@@ -187,6 +210,7 @@ int run_sources_sssp(bc_handle *h, const int64_t *sources_in, int64_t k_all, dou
         tr.mark("batch: distances");
         // ---- B: tight-arc counts, first frontiers
         const dim3 grid((unsigned)((n + 32 * kSsspWarps - 1) / (32 * kSsspWarps)), (unsigned)ng);
+        TRY(reset_slots());
         sssp_count_kernel<<<grid, kSsspWarps * 32, 0, st>>>(p);
         ++h->launches;
         // ---- C: path counts
@@ -196,7 +220,12 @@ int run_sources_sssp(bc_handle *h, const int64_t *sources_in, int64_t k_all, dou
         tr.mark("batch: tight-arc counts + path counts");
         // ---- D: dependencies from the leaves
         const int64_t l1 = h->launches;
-        CUDA_TRY(h, cudaMemcpyAsync(p.cur, p.leaf, (size_t)ng * n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        // the leaf masks and the leaf queue are the first frontier as they are (both mask arrays and
+        // both queues of phase C are empty by now; the leaf buffers are rebuilt by the next batch)
+        TRY(reset_slots());
+        p.cur = p.leaf;
+        p.q_cur = p.q_leaf;
+        CUDA_TRY(h, cudaMemcpyAsync(p.q_count, p.q_leaf_count, G * sizeof(int), cudaMemcpyDeviceToDevice, st));
         TRY(sssp_rounds(h, sssp_backward_kernel, p, ng, st, &rounds_d));
         CUDA_TRY(h, cudaEventRecord(e.bwd_end, st));
         launches_b += h->launches - l1;

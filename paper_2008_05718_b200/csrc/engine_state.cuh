@@ -174,6 +174,9 @@ struct bc_handle {
     uint32_t *sp_maskA = nullptr, *sp_maskB = nullptr, *sp_leaf = nullptr;
     int *sp_flags = nullptr;
     long long *sp_bound = nullptr;   // per round: distance bound, smallest waiting distance (phase A)
+    int32_t *sp_queue = nullptr;     // three frontier queues [G][n]: this round, next round, leaves
+    int *sp_qcount = nullptr;        // their lengths: [3][G] rotating + [G] leaves
+    int sp_blocks = 0;               // dev option "sssp_blocks": blocks per group of a round (0 = default)
     long long sp_delta = 0;          // option "sssp_delta": step of the bound (0 = 16 mean arc weights)
     long long wsum = 0;              // sum of the arc weights
     int sp_groups = 0;
@@ -448,8 +451,10 @@ int build_items(bc_handle *h, Csr &c, const int64_t *off, int item_arcs) {
 void free_sssp_state(bc_handle *h) {
     arena_free(h->sp_dist), arena_free(h->sp_npar), arena_free(h->sp_nchild);
     arena_free(h->sp_maskA), arena_free(h->sp_maskB), arena_free(h->sp_leaf), arena_free(h->sp_flags);
-    arena_free(h->sp_bound);
+    arena_free(h->sp_bound), arena_free(h->sp_queue), arena_free(h->sp_qcount);
     h->sp_bound = nullptr;
+    h->sp_queue = nullptr;
+    h->sp_qcount = nullptr;
     h->sp_dist = nullptr;
     h->sp_npar = h->sp_nchild = nullptr;
     h->sp_maskA = h->sp_maskB = h->sp_leaf = nullptr;

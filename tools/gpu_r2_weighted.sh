@@ -10,3 +10,4 @@ run python -m pytest tests -m gpu -x -q
 run python tools/weighted_probe.py 1024 128 100000
 run python tools/weighted_probe.py 1024 512 100000
 run python tools/weighted_probe.py 2048 128 1000000
+run python tools/weighted_probe.py 1024 128 100

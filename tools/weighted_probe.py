@@ -20,6 +20,8 @@ srcs = sorted(np.random.default_rng(2).choice(g.num_vertices, n_src, replace=Fal
 print("n", g.num_vertices, "m", g.num_edges, "sources", n_src, "wmax", int(g.arc_weight.max()), flush=True)
 with Engine(g) as e:
     e.set_option("groups", max(1, min(16, n_src // 32)))
+    if os.environ.get("SSSP_BLOCKS"):
+        e.set_option("sssp_blocks", int(os.environ["SSSP_BLOCKS"]))
     if os.environ.get("SSSP_DELTA"):
         e.set_option("sssp_delta", int(os.environ["SSSP_DELTA"]))
     e.run(srcs[:32])
