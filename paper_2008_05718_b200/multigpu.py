@@ -71,7 +71,8 @@ def run_bc_multi(g, cfg):
     import torch.distributed as dist
 
     from . import _capi
-    from .engine import (CommTotals, RunResult, _MODE_CODE, open_engine, prepare, select_sources)
+    from .engine import (GENERAL_WEIGHT_LIMIT, CommTotals, RunResult, _MODE_CODE, open_engine, prepare,
+                         select_sources)
 
     rank, world = init_process_group()
     if world != cfg.num_gpus:
@@ -86,13 +87,15 @@ def run_bc_multi(g, cfg):
     sources = select_sources(g, cfg)
     p, bs = prepare(g, cfg)
     mode = cfg.mode if p.num_parts > 1 else "direct"
+    if mode != "direct" and not g.unit_weight and int(g.arc_weight.max()) > GENERAL_WEIGHT_LIMIT:
+        mode = "direct"     # general-weight sweeps are unpartitioned (run_bc warns about the same step)
     # the BC vector NCCL reduces must live on the device the engine runs on (open_engine's rule)
     ordinal = cfg.device if cfg.device is not None else int(os.environ.get("LOCAL_RANK", "0"))
     device = torch.device("cuda", ordinal)
     torch.cuda.set_device(device)
     stats = {}
     with open_engine(g, cfg, (len(sources) + world - 1) // world) as eng:
-        if p.num_parts > 1:
+        if p.num_parts > 1 and mode != "direct":
             eng.set_partition(p.num_parts, p.assignment)
 
         def compute_local(shard, bc_tensor):
