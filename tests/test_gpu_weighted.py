@@ -308,3 +308,13 @@ def test_large_weights_through_run_bc_and_the_dimacs_loader(tmp_path):
         e.set_partition(2, (np.arange(g.num_vertices) % 2).astype(np.int32))
         with pytest.raises(P.InputError, match="BC_MODE_DIRECT only"):
             e.run(srcs, MODE_BSP)
+
+
+def test_general_weight_sweeps_deeper_than_one_flag_epoch():
+    # a weighted path: the shortest-path DAG is ~20,000 arcs deep, beyond the 16,384 rounds one
+    # epoch of round flags covers (engine_sssp.cuh: sssp_rounds restarts its round index)
+    g = with_weights(G.path(20000), 12, 50000)
+    srcs = [0, 7, 19999]
+    with Engine(g) as e:
+        st = check_against_oracle(g, srcs, e)
+    assert st["max_levels"] > 16384
