@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 SO_PATH = os.path.join(HERE, "libbc_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", "bc_engine.cu")]
 HEADERS = [os.path.join(HERE, "csrc", f) for f in (
-    "bc_kernels.cuh", "bc_deep.cuh", "bc_border.cuh", "bc_dist.cuh", "bc_sssp.cuh",            # kernels
+    "bc_kernels.cuh", "bc_deep.cuh", "bc_border.cuh", "bc_dist.cuh", "bc_sssp.cuh", "bc_relabel.cuh",            # kernels
     "engine_state.cuh", "engine_sweeps.cuh", "engine_border.cuh", "engine_sssp.cuh", "engine_run.cuh",
     "engine_dist.cuh",  # host side
 )] + [os.path.join(ROOT, "include", "bc_b200.h")]

@@ -11,10 +11,12 @@
 #include "bc_deep.cuh"
 #include "bc_dist.cuh"
 #include "bc_kernels.cuh"
+#include "bc_relabel.cuh"
 #include "bc_sssp.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -169,6 +171,7 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
         if (value != h->item_arcs) {
             h->item_arcs = (int)value;
             TRY(build_items(h, h->full, h->h_off.data(), h->item_arcs));
+            if (h->relab_ready) TRY(build_items(h, h->relab, h->h_off_relab.data(), h->item_arcs));
             if (h->k > 1) {
                 std::vector<int64_t> ioff((size_t)h->n + 1);
                 CUDA_TRY(h, cudaMemcpy(ioff.data(), h->intra.off, (h->n + 1) * sizeof(int64_t),
@@ -189,6 +192,11 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     if (k == "sssp") {
         if (value < -1 || value > 1) return h->fail(BC_ERR_INPUT, "sssp must be -1 (by weight range), 0 or 1");
         h->wgt_mode = (int)value;
+        return BC_OK;
+    }
+    if (k == "relabel") {
+        if (value < -1 || value > 1) return h->fail(BC_ERR_INPUT, "relabel must be -1 (by degree skew), 0 or 1");
+        h->relabel = (int)value;
         return BC_OK;
     }
     if (k == "sssp_blocks") {
@@ -559,6 +567,8 @@ void bc_destroy(bc_handle *h) {
     free_state(h);
     free_partition(h);
     free_csr(h->full);
+    free_csr(h->relab);
+    arena_free(h->d_old_of_new), arena_free(h->d_new_of_old);
     arena_free(h->counters);
     arena_free(h->dflags);
     arena_free(h->d_maxlvl);

@@ -591,7 +591,8 @@ __global__ void clear_source_sigma_kernel(const int64_t *src, int batch_count, i
 }
 
 // bc[v] += sum over groups, in group order; the per-group partials are reset.
-__global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups) {
+// old_of_new (or nullptr): the partials are indexed by renumbered vertices (bc_relabel.cuh), bc by the caller's.
+__global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups, const int32_t *old_of_new = nullptr) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -611,7 +612,7 @@ __global__ void reduce_bc_kernel(double *bc, double *bcg, int64_t n, int groups)
             s += x;
             if (x != 0.0) bcg[(size_t)g * n + v] = 0.0;
         }
-        if (s != 0.0) bc[v] += s;
+        if (s != 0.0) bc[old_of_new ? old_of_new[v] : v] += s;
     }
 }
 

@@ -82,6 +82,24 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     }
     tr.mark("run: source ordering");
     const int64_t k = (int64_t)active.size();
+    // Unpartitioned unit-weight sweeps of a skewed graph run on the copy renumbered by descending
+    // degree (bc_relabel.cuh): sources are renamed here, the BC vector on the way out.
+    const bool relabelled = !debug && mode == BC_MODE_DIRECT && h->k == 1 && h->dist_rank < 0 && k > 0 &&
+                            relabel_wanted(h, k);
+    if (!debug && mode == BC_MODE_DIRECT && h->k == 1) h->sources_seen += k;
+    if (relabelled) {
+        TRY(ensure_relabelled(h, st));
+        ScopedBlock<int64_t> d_ids;
+        CUDA_TRY(h, arena_malloc((void **)&d_ids.p, 2 * (size_t)k * sizeof(int64_t)));
+        CUDA_TRY(h, cudaMemcpyAsync(d_ids.p, active.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        relabel_sources_kernel<<<grid1d((size_t)k, 256), 256, 0, st>>>(d_ids.p, k, h->d_new_of_old, d_ids.p + k);
+        ++h->launches;
+        CUDA_TRY(h, cudaMemcpyAsync(active.data(), d_ids.p + k, k * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+        tr.mark("run: renumbered graph");
+    }
+    const Csr &whole = relabelled ? h->relab : h->full;                       // the unpartitioned graph of this run
+    const std::vector<int64_t> &whole_off = relabelled ? h->h_off_relab : h->h_off;
     const int64_t *sources = active.data();
     const int groups = debug ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(h->groups, (k + 31) / 32));
     TRY(ensure_state(h, groups, debug));
@@ -124,7 +142,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     int max_depth = 0;
     int64_t launches_f = 0, launches_b = 0;
     int64_t tot_iters = 0, tot_comm = 0, tot_sync = 0, tot_bytes = 0;
-    const Csr &fwd_csr = hybir ? h->intra : h->full;
+    const Csr &fwd_csr = hybir ? h->intra : whole;
     // queue levels / push: the unpartitioned sweeps only (the partitioned modes
     // read dense level rows for borders and reports)
     const bool adaptive = h->sparse && !hybir && !(want_reports && h->k == 2) && h->full.wgt == nullptr;
@@ -225,7 +243,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         std::vector<LevelRep> reps;
         if (!hybir) {
             TRY(begin_batch(h, h->d_src + b * lanes_per_batch, cnt, ng, st, queued));
-            if (adaptive) TRY(forward_adaptive(h, fwd_csr, ng, cnt, batch_src, st, &depth, reps));
+            if (adaptive) TRY(forward_adaptive(h, fwd_csr, ng, cnt, batch_src, st, &depth, reps, &whole_off));
             else TRY(forward_sweep(h, fwd_csr, ng, st, &depth));
         } else if (ahead_ready) {
             // issued ahead while the previous batch's border phase ran: its seeds sit in the
@@ -300,8 +318,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         // ---- backward over the whole graph (cross-part children are final by
         // the time their parents' level runs: levels are global)
         const int64_t l_bwd = h->launches;
-        if (queued) TRY(backward_adaptive(h, h->full, depth, reps, ng, debug, st));
-        else TRY(backward_sweep(h, h->full, depth, ng, debug, st));
+        if (queued) TRY(backward_adaptive(h, whole, depth, reps, ng, debug, st));
+        else TRY(backward_sweep(h, whole, depth, ng, debug, st));
         h->last_depth = depth;
         if (queued && !debug && h->lazy_clear) {
             // the sweep cleared every pair it visited; the sources (level 0) are left
@@ -443,7 +461,8 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     }
     if (!debug && bc_dev != nullptr) {
         // (groups beyond the ones this run used hold zeros)
-        reduce_bc_kernel<<<grid1d((size_t)n, 256, 4736), 256, 0, st>>>(bc_dev, h->bcg, n, groups);
+        reduce_bc_kernel<<<grid1d((size_t)n, 256, 4736), 256, 0, st>>>(bc_dev, h->bcg, n, groups,
+                                                                       relabelled ? h->d_old_of_new : nullptr);
         ++h->launches;
         CUDA_TRY(h, cudaGetLastError());
         h->bcg_dirty = false;
@@ -482,7 +501,7 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
         // the totals count Step 6 (arcs inside the parts; cut arcs are not walked)
         stats->reached = (int64_t)cnts[0] + k_all;
         int64_t src_arcs = 0;
-        for (int64_t i = 0; i < k; ++i) src_arcs += h->h_off[sources[i] + 1] - h->h_off[sources[i]];
+        for (int64_t i = 0; i < k; ++i) src_arcs += whole_off[sources[i] + 1] - whole_off[sources[i]];
         stats->arcs_reached = (int64_t)cnts[1] + src_arcs;
         stats->dag_arcs = (int64_t)cnts[2];
         stats->launches = h->launches - launches0;

@@ -459,3 +459,73 @@ def test_push_pull_switch_equivalence():
             e.set_option("push_beta", 1)
             bc1, _ = e.run(srcs)
         assert np.allclose(bc1, out[0][3], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["rmat12", "rmat14_batches", "star_and_isolated", "small_forced"])
+def test_degree_renumbered_sweeps(case):
+    """Unpartitioned unit-weight runs of skewed graphs sweep a copy of the graph renumbered by
+    descending degree (csrc/bc_relabel.cuh): sources are renamed on the way in, BC on the way
+    out.  Same BC as on the caller's ids (and as the oracle), same traversal counters."""
+    if case == "rmat12":
+        g = G.rmat(12, 8, 1)
+        srcs = list(range(0, 4096, 3))
+        groups = 8
+    elif case == "rmat14_batches":
+        g = G.rmat(14, 16, 3)
+        srcs = sorted(np.random.default_rng(4).choice(g.num_vertices, 300, replace=False).tolist())
+        groups = 2                                  # several batches, the last one partial
+    elif case == "star_and_isolated":
+        # one hub, leaves, a tail, isolated vertices (also as sources)
+        edges = [(0, i) for i in range(1, 200)] + [(200 + i, 201 + i) for i in range(20)] + [(5, 200)]
+        g = P.from_edges(260, edges)
+        srcs = [0, 1, 5, 199, 200, 220, 221, 259]
+        groups = 1
+    else:
+        g = G.random_connected(300, 500, seed=5)
+        srcs = list(range(0, 300, 2))
+        groups = 2
+    with Engine(g) as e:
+        e.set_option("groups", groups)
+        e.set_option("relabel", 0)
+        bc_plain, st_plain = e.run(srcs)
+        e.set_option("relabel", 1)
+        bc_ren, st_ren = e.run(srcs)
+        bc_ren2, _ = e.run(srcs)
+        dist, sigma, delta = e.debug_sources(srcs[:8])      # inspection stays on the caller's ids
+    obc, info = O.brandes_bc(g, srcs)
+    assert np.allclose(bc_ren, obc, rtol=1e-9, atol=1e-12)
+    assert np.allclose(bc_ren, bc_plain, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(bc_ren, bc_ren2)
+    for key in ("reached", "arcs_reached", "dag_arcs", "max_levels"):
+        assert st_ren[key] == st_plain[key], key
+    assert st_ren["reached"] == info["reached"] and st_ren["dag_arcs"] == info["dag_arcs"]
+    for i, s in enumerate(srcs[:8]):
+        od, osg, odl, _ = O.brandes_single_source(g, int(s))
+        assert np.array_equal(dist[i], od) and np.array_equal(sigma[i], osg)
+
+
+def test_degree_renumbering_is_chosen_by_skew_and_work():
+    # R-MAT (hubs) is renumbered by default once the handle has seen 2048 sources, a grid never:
+    # the default run equals the forced one bit for bit when it applies and the plain one otherwise
+    g = G.rmat(13, 16, 2)
+    srcs = np.nonzero(np.diff(g.offsets) > 0)[0][:2100].tolist()     # (sources without arcs take no lane: not counted)
+    with Engine(g) as e:
+        first, _ = e.run(srcs[:200])            # 200 sources: not yet
+        many, _ = e.run(srcs)                   # 2300 seen: renumbered from here on
+        again, _ = e.run(srcs[:200])
+        e.set_option("relabel", 0)
+        plain_few, _ = e.run(srcs[:200])
+        e.set_option("relabel", 1)
+        forced_few, _ = e.run(srcs[:200])
+        forced_many, _ = e.run(srcs)
+    assert np.array_equal(first, plain_few)
+    assert np.array_equal(again, forced_few)
+    assert np.array_equal(many, forced_many)
+    g = G.grid(40, 40)
+    srcs = list(range(g.num_vertices))
+    with Engine(g) as e:
+        e.run(srcs)
+        default, _ = e.run(srcs)
+        e.set_option("relabel", 0)
+        plain, _ = e.run(srcs)
+    assert np.array_equal(default, plain)
