@@ -568,6 +568,8 @@ def run_ours(args):
     eng.set_option("groups", groups)
     if args.item_arcs:
         eng.set_option("item_arcs", args.item_arcs)
+    if args.relabel >= 0:
+        eng.set_option("relabel", args.relabel)
     bc_dev = torch.zeros(n, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -691,6 +693,8 @@ def run_ours(args):
                    "sources_per_gpu": len(mine), "mode": "source-sharded" if world > 1 else "single-gpu",
                    "groups": groups, "max_levels": st["max_levels"],
                    "isolated_fraction_sources": isolated_fraction(g, all_sources),
+                   "renumbering": {-1: "engine default: vertices renumbered by descending degree once the handle has swept 2048 sources (warm-up)",
+                                   0: "off", 1: "forced from the first step"}[args.relabel],
                    "l2": "per-batch state %.1f GB >> 126 MB L2, no flush needed"
                          % (groups * n * 560 / 1e9)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -751,6 +755,9 @@ def main():
     ap.add_argument("--sources", type=int, default=1024, help="sources per GPU (source-sharded) / in total (graph-partitioned)")
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--item-arcs", type=int, default=0)
+    ap.add_argument("--relabel", type=int, default=-1, choices=(-1, 0, 1),
+                    help="degree-descending renumbering of the resident graph: -1 = the engine's rule (skewed graphs, "
+                         "once a handle has swept 2048 sources: from the fourth step on here), 0 = never, 1 = from the first step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the partitioned / north-star extra records")
     ap.add_argument("--gpu-mode", default="source-sharded", choices=("source-sharded", "graph-partitioned"))

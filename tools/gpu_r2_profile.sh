@@ -6,9 +6,9 @@ set -x
 mkdir -p gpurun_out
 T=/tmp/r2prof; mkdir -p $T
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra > gpurun_out/bench_under_ncu.log 2>&1
+    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra --relabel 1 > gpurun_out/bench_under_ncu.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:^level_kernel -c 8 -o $T/prof_level -f \
-    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra > gpurun_out/bench_under_ncu2.log 2>&1
+    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra --relabel 1 > gpurun_out/bench_under_ncu2.log 2>&1
 ncu -i $T/prof_level.ncu-rep --page raw --csv > gpurun_out/prof_level.raw.csv
 timeout 900 ncu --set full --clock-control none -k regex:compose_sigma -c 6 -o $T/r2_compose -f \
     python tools/road_hybir_profile.py 2048 8 > gpurun_out/ncu_compose.log 2>&1

@@ -28,9 +28,9 @@ timeout 900 ncu --set full --clock-control none -k regex:deep_backward_compact -
 ncu -i $T/r2_deep_bc.ncu-rep --page raw --csv > gpurun_out/r2_deep_backward_compact.raw.csv
 # launch list + full capture of the level kernel with the final code (profiles/r2_launches*, r2_level_kernel_ncu_full.csv, r2_traffic.json)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra > gpurun_out/bench_under_ncu.log 2>&1
+    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra --relabel 1 > gpurun_out/bench_under_ncu.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:^level_kernel -c 8 -o $T/prof_level -f \
-    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra > gpurun_out/bench_under_ncu2.log 2>&1
+    python bench.py --steps 1 --warmup 0 --no-cpu --no-extra --relabel 1 > gpurun_out/bench_under_ncu2.log 2>&1
 ncu -i $T/prof_level.ncu-rep --page raw --csv > gpurun_out/prof_level.raw.csv
 # general-weight sweeps: sanitizer + records, and a full capture of mid-sweep rounds (four groups)
 bash tools/gpu_r2_weighted.sh

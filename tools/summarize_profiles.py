@@ -27,10 +27,10 @@ for r in rows[hi + 1:]:
     a[1] += us
     order.append((name, r[8], us))
 total = sum(a[1] for a in agg.values())
-cmd = "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 1 --warmup 0 --no-cpu --no-extra"
+cmd = "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 1 --warmup 0 --no-cpu --no-extra --relabel 1"
 with open(os.path.join(out, rnd + "_launches_summary.md"), "w") as fh:
     fh.write("# ncu launch list, %s (cold-cache, serialised: compare shares, not absolutes)\n\n" % rnd)
-    fh.write("Command: `%s`\n(the bench workload: R-MAT scale-20 EF-16, 1024 sources of which 612 have arcs = one batch of 20 lane groups per pass; the command makes four identical passes -- the untimed byte-model step, the timed step and two run_bc calls of the e2e leg; "
+    fh.write("Command: `%s`\n(the bench workload: R-MAT scale-20 EF-16, 1024 sources of which 612 have arcs = one batch of 20 lane groups per pass; the command makes four passes -- the untimed byte-model step and the timed step on the graph renumbered by descending degree (`--relabel 1`: the default rule renumbers after 2048 sources, i.e. during the warm-up of a normal run; the renumbering kernels are in the list), then two run_bc calls of the e2e leg, each a fresh handle on the caller's ids; "
              "raw list: `%s_launches.csv`)\n\n" % (cmd, rnd))
     fh.write("| kernel | launches | total us | share |\n|---|---:|---:|---:|\n")
     for name, (cnt, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
