@@ -122,6 +122,10 @@ int bc_set_weights(bc_handle *h, const int32_t *weights);
  * "deep_compact": 1 (default) = deep (road-like) graphs sweep over level-ordered path
  * counts with one atomically updated BC vector per batch, 2 = same with per-group BC
  * partials, 0 = row layout everywhere;
+ * "relabel": unpartitioned unit-weight runs sweep a copy of the graph renumbered by
+ * descending degree (csrc/bc_relabel.cuh; sources and the BC vector keep the caller's ids):
+ * 1 = from the first run, 0 = never, -1 (default) = graphs whose largest degree exceeds 16
+ * average degrees, once the handle has been given 2048 sources;
  * "sssp": weighted graphs, 1 = general-weight sweeps (csrc/bc_sssp.cuh), 0 = one level
  * per distance value (weights up to 4096), -1 (default) = by weight range;
  * "sssp_delta": step of the near-far distance bound there (0 = 16 mean arc weights);
