@@ -84,11 +84,23 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     const int64_t k = (int64_t)active.size();
     // Unpartitioned unit-weight sweeps of a skewed graph run on the copy renumbered by descending
     // degree (bc_relabel.cuh): sources are renamed here, the BC vector on the way out.
-    const bool relabelled = !debug && mode == BC_MODE_DIRECT && h->k == 1 && h->dist_rank < 0 && k > 0 &&
-                            relabel_wanted(h, k);
+    bool relabelled = !debug && mode == BC_MODE_DIRECT && h->k == 1 && h->dist_rank < 0 && k > 0 &&
+                      relabel_wanted(h, k);
     if (!debug && mode == BC_MODE_DIRECT && h->k == 1) h->sources_seen += k;
     if (relabelled) {
-        TRY(ensure_relabelled(h, st));
+        const int rc = ensure_relabelled(h, st);
+        if (rc == BC_ERR_INPUT) return rc;   // an arc without its reverse
+        if (rc != BC_OK) {
+            // no room for the second copy (it needs ~5 x the arc array while it is built): this
+            // handle stays on the caller's ids
+            cudaGetLastError();
+            free_csr(h->relab);
+            h->relab_ready = false;
+            h->relabel = 0;
+            relabelled = false;
+        }
+    }
+    if (relabelled) {
         ScopedBlock<int64_t> d_ids;
         CUDA_TRY(h, arena_malloc((void **)&d_ids.p, 2 * (size_t)k * sizeof(int64_t)));
         CUDA_TRY(h, cudaMemcpyAsync(d_ids.p, active.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, st));

@@ -350,6 +350,17 @@ def test_malformed_csr_is_refused():
     off[2], off[3] = off[3], off[2] - 1
     with pytest.raises(P.InputError, match="offsets"):
         Engine(Graph(5, g.num_edges, off, g.col_idx.copy()))
+    # an arc without its reverse: caught where the renumbered copy is built (csrc/bc_relabel.cuh)
+    star = G.rmat(8, 8, 1)
+    col = star.col_idx.copy()
+    v = int(np.argmax(np.diff(star.offsets)))
+    a = int(star.offsets[v])
+    others = np.setdiff1d(np.arange(star.num_vertices), np.append(col[star.offsets[v]:star.offsets[v + 1]], v))
+    col[a] = others[0]                                   # v -> x without x -> v
+    with Engine(Graph(star.num_vertices, star.num_edges, star.offsets.copy(), col)) as e:
+        e.set_option("relabel", 1)
+        with pytest.raises(P.InputError, match="reverse"):
+            e.run([0, 1, 2, 3])
 
 
 def test_failed_run_leaves_no_partial_sums_behind():
