@@ -480,6 +480,17 @@ struct __align__(16) VertexState {
     uint32_t pos2;   // backward sweep: entries of odd levels write here, of even levels into `pos`
 };
 
+__device__ __forceinline__ int32_t nb_at(const int4 &nb, int k) {
+    return k == 0 ? nb.x : k == 1 ? nb.y : k == 2 ? nb.z : nb.w;
+}
+
+// Degree byte of a queue entry (top byte of q_arc): the degree itself below 240, 255 = look it up
+// in the offsets, 0xF0 | d = degree d <= 4 with the neighbour ids in q_nb.
+constexpr uint32_t kNbCached = 0xF0u;
+__device__ __forceinline__ uint32_t degree_byte(unsigned long long deg) { return deg < 240ull ? (uint32_t)deg : 255u; }
+__device__ __forceinline__ bool entry_cached(uint32_t byte) { return byte >= kNbCached && byte != 255u; }
+__device__ __forceinline__ uint32_t entry_degree(uint32_t byte) { return entry_cached(byte) ? (byte & 0x0Fu) : byte; }
+
 struct DeepFwdCompactParams {
     const int64_t *off;
     const int32_t *col;
@@ -489,9 +500,12 @@ struct DeepFwdCompactParams {
     VertexState *vs;           // [G][n]
     double *qs;                // [G][vcap]
     uint32_t *q_off;           // [G][cap]
-    uint32_t *q_arc;           // [G][cap] (degree, 255 = look it up) << 24 | arcs 0..23 that reached a fresh lane
+    uint32_t *q_arc;           // [G][cap] degree byte (degree_byte / kNbCached) << 24 | arcs 0..23 that reached a fresh lane
     uint32_t *q_a;             // [G][cap] first arc of the entry's vertex (the sweeps then never read the
                                // row offsets of a frontier vertex: one random access and one hop less)
+    int4 *q_nb;                // [G][cap] the neighbour ids of an entry's vertex when it has at most four (-1 = none):
+                               // left by the discover pass, read in entry order by the accumulate pass and the
+                               // backward sweep instead of a random col_idx sector each
     unsigned long long *v_count;   // [G] value slots handed out so far
     int64_t vcap;
     uint32_t *live;
@@ -574,11 +588,12 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                 const size_t qbase = (size_t)g * p.q.cap;
                 uint32_t mask = 0, word = 0;
                 int64_t a = 0, e = 0;
+                int4 first4 = make_int4(-1, -1, -1, -1);   // neighbours 0..3 of the entry's vertex
                 if (i < end) {
                     mask = p.q.q_m[qbase + i];
                     word = p.q_arc[qbase + i];
                     a = p.q_a[qbase + i];
-                    e = a + (word >> 24);
+                    e = a + entry_degree(word >> 24);   // (flagged already if the level is being re-run after a relaunch)
                     if ((word >> 24) == 255u) {     // long adjacency: the degree did not fit
                         const int32_t u = p.q.q_v[qbase + i];
                         a = p.off[u];
@@ -593,6 +608,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                     uint32_t fresh[kThinArcs], old[kThinArcs];
 #pragma unroll
                     for (int k = 0; k < kThinArcs; ++k) w[k] = (a + r0 + k < e) ? __ldg(p.col + a + r0 + k) : -1;
+                    if (r0 == 0) first4 = make_int4(w[0], w[1], w[2], w[3]);
 #pragma unroll
                     for (int k = 0; k < kThinArcs; ++k) fresh[k] = (w[k] >= 0) ? (mask & ~gvs[w[k]].vis) : 0u;
 #pragma unroll
@@ -611,7 +627,17 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                         }
                     }
                 }
-                if (i < end) p.q_arc[qbase + i] = (word & 0xff000000u) | arcbits;
+                if (i < end) {
+                    // a vertex with at most four arcs leaves its neighbour ids with the entry: the
+                    // accumulate pass below and the backward sweep read them in entry order instead of
+                    // one random col_idx sector each (degree byte 0xF0 | degree marks such an entry)
+                    uint32_t byte = word >> 24;
+                    if (p.q_nb != nullptr && byte != 255u && entry_degree(byte) <= 4u) {
+                        p.q_nb[qbase + i] = first4;
+                        byte = kNbCached | entry_degree(byte);
+                    }
+                    p.q_arc[qbase + i] = (byte << 24) | arcbits;
+                }
             }
             if (staged) flush();
         }
@@ -663,7 +689,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                     const int64_t w_a = p.off[w];
                     const unsigned long long deg = (unsigned long long)(p.off[w + 1] - w_a);
                     p.q_a[qbase + i] = (uint32_t)w_a;
-                    p.q_arc[qbase + i] = (uint32_t)min(deg, 255ull) << 24;
+                    p.q_arc[qbase + i] = degree_byte(deg) << 24;
                     nr += __popc(m);
                     ar += __popc(m) * deg;
                     nv += 1;
@@ -735,12 +761,15 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                 const size_t vbase = (size_t)g * p.vcap;
                 const uint32_t mask = p.q.q_m[qbase + i];
                 const uint32_t word = p.q_arc[qbase + i];
-                int64_t a = p.q_a[qbase + i], e = a + (word >> 24);
+                int64_t a = p.q_a[qbase + i], e = a + entry_degree(word >> 24);
                 if ((word >> 24) == 255u) {
                     const int32_t u = p.q.q_v[qbase + i];
                     a = p.off[u];
                     e = p.off[u + 1];
                 }
+                const bool cached = p.q_nb != nullptr && entry_cached(word >> 24);     // (set by phase A above)
+                int4 nbv = make_int4(-1, -1, -1, -1);
+                if (cached) nbv = p.q_nb[qbase + i];
                 const uint32_t at_u = p.q_off[qbase + i];
                 const VertexState *gvs = p.vs + (size_t)g * n;
                 const uint32_t lbeg = (uint32_t)s_lbeg[g];
@@ -764,7 +793,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_F) deep_forwa
                     while (bits) {
                         const int k = __ffs(bits) - 1;
                         bits &= bits - 1;
-                        add_into(__ldg(p.col + a + k));
+                        add_into(cached ? nb_at(nbv, k) : __ldg(p.col + a + k));
                     }
                 } else {
                     for (int64_t b = a; b < e; ++b) add_into(__ldg(p.col + b));
@@ -891,7 +920,7 @@ __global__ void compact_level0_kernel(QueueParams q, uint32_t *q_off, double *qs
         const int64_t v = q.q_v[g * q.cap + i];
         vs[g * n + v].vis |= m;
         q_a[g * q.cap + i] = (uint32_t)off[v];
-        q_arc[g * q.cap + i] = (uint32_t)min((long long)(off[v + 1] - off[v]), 255ll) << 24;
+        q_arc[g * q.cap + i] = degree_byte((unsigned long long)(off[v + 1] - off[v])) << 24;
         q_off[g * q.cap + i] = at;
         for (int k = 0; k < __popc(m); ++k) qs[g * (size_t)vcap + at + k] = 1.0;
         at += __popc(m);
@@ -1024,6 +1053,7 @@ struct DeepBwdCompactParams {
     VertexState *vs;             // [G][n] (pos field)
     const uint32_t *q_a;         // first arc / degree of every entry as the forward sweep recorded them
     const uint32_t *q_arc;       // (nullptr when that sweep ran on another CSR: the cut-free one of hybir mode)
+    const int4 *q_nb;            // neighbour ids of the entries of vertices with at most four arcs (nullptr with q_a)
 };
 
 __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backward_compact_kernel(const DeepBwdCompactParams p) {
@@ -1061,9 +1091,16 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
             else gvs[v].pos = (uint32_t)i + 1u;
             if (m == 0) continue;
             int64_t a0, a1;
+            bool cached = false;
+            int4 nbv = make_int4(-1, -1, -1, -1);
             if (p.q_a != nullptr && (p.q_arc[qbase + i] >> 24) != 255u) {
+                const uint32_t byte = p.q_arc[qbase + i] >> 24;
                 a0 = p.q_a[qbase + i];
-                a1 = a0 + (p.q_arc[qbase + i] >> 24);
+                a1 = a0 + entry_degree(byte);
+                if (p.q_nb != nullptr && entry_cached(byte)) {
+                    nbv = p.q_nb[qbase + i];
+                    cached = true;
+                }
             } else {
                 a0 = p.off[v];
                 a1 = p.off[v + 1];
@@ -1080,7 +1117,7 @@ __global__ void __launch_bounds__(kDeepThreads, BC_DEEP_MIN_BLOCKS_B) deep_backw
                 for (int k = 0; k < kThinArcs; ++k) {
                     cj[k] = 0;
                     if (!deepest && a0 + k < a1) {
-                        const VertexState *child = gvs + __ldg(p.col + a0 + k);
+                        const VertexState *child = gvs + (cached ? nb_at(nbv, k) : __ldg(p.col + a0 + k));
                         const uint32_t pj = ((L + 1) & 1) ? child->pos2 : child->pos;
                         if (pj >= cb && pj <= ce) cj[k] = pj;
                     }

@@ -287,6 +287,7 @@ struct bc_handle {
     VertexState *vs = nullptr;     // [G][n] visited / next-level / queue-entry words of the compact sweeps
     uint32_t *q_arc = nullptr;     // [G][q_cap] degree << 24 | arcs of a frontier entry that reached a fresh lane
     uint32_t *q_a = nullptr;       // [G][q_cap] first arc of the entry's vertex
+    int4 *q_nb = nullptr;          // [G][q_cap] neighbour ids of entries whose vertex has at most four arcs (optional)
     const int64_t *q_a_csr = nullptr;   // ... in the CSR with these offsets (the last compact forward sweep's)
     bool fwd_compact_allowed = false;   // set by the caller of a sweep: nobody reads sigma rows afterwards
     bool sigma_stale = false;      // the sigma rows were not cleared for this batch (compact sweep expected)
@@ -489,6 +490,8 @@ void free_state(bc_handle *h) {
     arena_free(h->qs), arena_free(h->q_off), arena_free(h->v_count), arena_free(h->bc_acc);
     arena_free(h->vs), arena_free(h->q_arc), arena_free(h->q_a);
     h->vs = nullptr, h->q_arc = nullptr, h->q_a = nullptr;
+    arena_free(h->q_nb);
+    h->q_nb = nullptr;
     h->qs = nullptr, h->q_off = nullptr, h->v_count = nullptr, h->bc_acc = nullptr;
     h->q_vcap = 0;
     arena_free(h->d_qbeg), arena_free(h->d_qend), arena_free(h->d_qlbeg);
@@ -725,6 +728,13 @@ bool ensure_deep_compact(bc_handle *h) {
     cudaMemset(h->q_off, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
     cudaMemset(h->q_arc, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
     cudaMemset(h->q_a, 0, G * (size_t)h->q_cap * sizeof(uint32_t));
+    // optional: without it the sweeps read col_idx
+    if (arena_malloc((void **)&h->q_nb, G * (size_t)h->q_cap * sizeof(int4)) != cudaSuccess) {
+        cudaGetLastError();
+        h->q_nb = nullptr;
+    } else {
+        cudaMemset(h->q_nb, 0, G * (size_t)h->q_cap * sizeof(int4));
+    }
     h->q_vcap = vcap;
     return true;
 }
@@ -764,6 +774,24 @@ int grow_queues(bc_handle *h, int64_t need_cap, cudaStream_t st,
         }
         arena_free(*arr);
         *arr = no;
+    }
+    if (h->q_nb != nullptr) {
+        int4 *nn = nullptr;
+        if (arena_malloc((void **)&nn, G * (size_t)cap * sizeof(int4)) != cudaSuccess) {
+            cudaGetLastError();
+            h->q_a_csr = nullptr;          // entries so far have no neighbour cache any more: sweeps of this batch
+            arena_free(h->q_nb);           // (the forward kernel is relaunched with q_nb = nullptr) read col_idx
+            h->q_nb = nullptr;
+        } else {
+            CUDA_TRY(h, cudaMemset(nn, 0, G * (size_t)cap * sizeof(int4)));
+            for (size_t g = 0; g < G; ++g) {
+                const size_t keep = (size_t)std::min<int64_t>(g < used.size() ? (int64_t)used[g] : 0, h->q_cap);
+                if (keep == 0) continue;
+                CUDA_TRY(h, cudaMemcpy(nn + g * cap, h->q_nb + g * h->q_cap, keep * sizeof(int4), cudaMemcpyDeviceToDevice));
+            }
+            arena_free(h->q_nb);
+            h->q_nb = nn;
+        }
     }
     arena_free(h->q_v), arena_free(h->q_m);
     h->q_v = nv;

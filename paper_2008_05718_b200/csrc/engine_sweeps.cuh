@@ -478,6 +478,7 @@ int forward_adaptive(bc_handle *h, const Csr &c, int ng, int cnt, const int64_t 
                 dp.q_off = h->q_off;
                 dp.q_arc = h->q_arc;
                 dp.q_a = h->q_a;
+                dp.q_nb = h->q_nb;
                 h->q_a_csr = c.off;
                 dp.v_count = h->v_count;
                 dp.vcap = h->q_vcap;
@@ -765,6 +766,7 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             if (h->q_a_csr == c.off) {     // the forward sweep walked this very CSR
                 dp.q_a = h->q_a;
                 dp.q_arc = h->q_arc;
+                dp.q_nb = h->q_nb;
             }
             void *args[] = {&dp};
             CUDA_TRY(h, cudaLaunchCooperativeKernel((void *)deep_backward_compact_kernel, dim3(h->deep_grid_c),
