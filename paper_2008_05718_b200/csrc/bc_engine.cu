@@ -8,6 +8,7 @@
 // bc_border.cuh or fails.
 #include "bc_b200.h"
 #include "bc_border.cuh"
+#include "bc_bwd_push.cuh"
 #include "bc_deep.cuh"
 #include "bc_dist.cuh"
 #include "bc_kernels.cuh"
@@ -263,6 +264,13 @@ int bc_set_option(bc_handle *h, const char *key, int64_t value) {
     if (k == "push_beta_late") {
         if (value < 1) return h->fail(BC_ERR_INPUT, "push_beta_late must be >= 1");
         h->push_beta_late = (int)value;
+        return BC_OK;
+    }
+    if (k == "bwd_push") {
+        // child-driven backward levels (bc_bwd_push.cuh): 0 = every level parent-driven, else the
+        // factor by which the children's arcs must undercut the parents' arcs
+        if (value < 0) return h->fail(BC_ERR_INPUT, "bwd_push must be >= 0");
+        h->bwd_push = (int)value;
         return BC_OK;
     }
     if (k == "push_beta") {

@@ -486,10 +486,12 @@ int run_sources(bc_handle *h, int mode, const int64_t *sources_in, int64_t k_all
     tr.mark("run: batches");
 
     double ms_level = 0;
+    const bool level_trace = getenv("BC_LEVEL_TRACE") != nullptr;   // dev: one line per timed level launch
     const int64_t level_timed = (int64_t)h->level_events.size();
     for (auto &pr : h->level_events) {
         float t = 0;
         if (cudaEventElapsedTime(&t, pr.first, pr.second) == cudaSuccess) ms_level += t;
+        if (level_trace) fprintf(stderr, "[bc level %d] %.3f ms\n", (int)(&pr - h->level_events.data()), t);
         cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     }
     h->level_events.clear();

@@ -200,6 +200,11 @@ struct bc_handle {
     uint32_t row_bypass_mask = 0;  // dev: bit L = forward level L bypasses L1, bit 16 + L = backward level L
     int push_beta_late = 24;   // same, once a pull level has run: a late pull scans unvisited vertices only
     int push_beta = 4;     // push when frontier arcs * beta <= arcs of the graph
+    // backward: children drive a level when their arcs * bwd_push <= the parents' arcs (0: never).
+    // 16 = the far tail only: at 4 the level behind the peak of R-MAT scale 20 switches too and
+    // loses (7.3 against 5.0 ms: 155 M scattered fp64 atomics run at 37 G/s)
+    int bwd_push = 16;
+    int bwd_push_levels = 0;   // levels of the last run that took that path
     int deep = 1;          // run consecutive thin levels inside one cooperative launch (bc_deep.cuh)
     int deep_blocks_per_sm = 0;   // 0 = what the occupancy calculator allows
     int deep_grid_f = 0, deep_grid_b = 0, deep_grid_c = 0, deep_grid_fc = 0;
@@ -260,6 +265,11 @@ struct bc_handle {
     uint32_t *vis = nullptr;
     std::vector<uint32_t *> lvl;
     double *sigma = nullptr, *coef = nullptr, *delta = nullptr;
+    // child-driven backward levels (bc_bwd_push.cuh): children above kBwdPushHeavyDegree arcs are
+    // listed per group and walked by the whole grid
+    uint4 *bp_list = nullptr;   // [alloc_groups][bp_cap] (vertex, lane mask, slice of its arcs)
+    unsigned *bp_count = nullptr;   // [alloc_groups]
+    int64_t bp_cap = -1;        // slices of all vertices of the graph above that degree (-1: not counted yet)
     uint8_t *cand = nullptr;    // [alloc_groups][n] candidate flags of the dense forward sweeps (deep graphs)
     bool use_cand = false;      // set by forward_sweep for the launches of its levels
     int sigma_clean_groups = 0; // leading groups of sigma that are all zero (kept so by the backward sweeps of adaptive batches)
@@ -501,6 +511,8 @@ void free_state(bc_handle *h) {
     arena_free(h->heavy);
     arena_free(h->cand);
     h->cand = nullptr;
+    arena_free(h->bp_list), arena_free(h->bp_count);
+    h->bp_list = nullptr, h->bp_count = nullptr;
     h->heavy = nullptr;
     h->heavy_cap = 0;
     h->deep_log = nullptr;

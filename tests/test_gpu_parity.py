@@ -223,16 +223,19 @@ def test_device_block_cache_reuse_and_release(rmat12):
     srcs = list(range(0, 4096, 5))
     small = G.grid(9, 5)
     with Engine(rmat12) as e:
+        e.set_option("bwd_push", 0)          # bit-for-bit comparisons below: sums in arc order
         first, _ = e.run(srcs)
     for _ in range(2):
         with Engine(small) as e:
             bc_small, _ = e.run(list(range(45)))
         with Engine(rmat12) as e:
+            e.set_option("bwd_push", 0)
             again, _ = e.run(srcs)
         assert np.array_equal(first, again)
         assert np.allclose(bc_small, O.brandes_bc(small, list(range(45)))[0], rtol=RTOL, atol=ATOL)
         _capi.release_cached_memory()
     with Engine(rmat12) as e:
+        e.set_option("bwd_push", 0)
         assert np.array_equal(first, e.run(srcs)[0])
 
 
@@ -241,11 +244,15 @@ def test_deterministic_and_linear(rmat12):
     a = list(range(0, 4096, 9))
     b = list(range(1, 4096, 13))
     with Engine(g) as e:
+        e.set_option("bwd_push", 0)      # every backward level parent-driven: sums in CSR arc order
         bc_a, _ = e.run(a)
         bc_a2, _ = e.run(a)
         bc_b, _ = e.run(b)
         bc_ab, _ = e.run(a + b)
     assert np.array_equal(bc_a, bc_a2)                       # bit-reproducible
+    with Engine(g) as e:                 # default: child-driven levels add in atomic order
+        bc_d, _ = e.run(a)
+    assert np.allclose(bc_d, bc_a, rtol=1e-12, atol=1e-9)
     assert np.allclose(bc_a + bc_b, bc_ab, rtol=1e-12)       # BC is a sum over sources
     assert bc_ab.min() >= 0.0
 
@@ -486,6 +493,7 @@ def test_degree_renumbered_sweeps(case):
         groups = 2
     with Engine(g) as e:
         e.set_option("groups", groups)
+        e.set_option("bwd_push", 0)                 # bc_ren == bc_ren2 bit for bit needs arc-order sums
         e.set_option("relabel", 0)
         bc_plain, st_plain = e.run(srcs)
         e.set_option("relabel", 1)
@@ -510,6 +518,7 @@ def test_degree_renumbering_is_chosen_by_skew_and_work():
     g = G.rmat(13, 16, 2)
     srcs = np.nonzero(np.diff(g.offsets) > 0)[0][:2100].tolist()     # (sources without arcs take no lane: not counted)
     with Engine(g) as e:
+        e.set_option("bwd_push", 0)             # bit-for-bit comparisons
         first, _ = e.run(srcs[:200])            # 200 sources: not yet
         many, _ = e.run(srcs)                   # 2300 seen: renumbered from here on
         again, _ = e.run(srcs[:200])
@@ -524,8 +533,53 @@ def test_degree_renumbering_is_chosen_by_skew_and_work():
     g = G.grid(40, 40)
     srcs = list(range(g.num_vertices))
     with Engine(g) as e:
+        e.set_option("bwd_push", 0)
         e.run(srcs)
         default, _ = e.run(srcs)
         e.set_option("relabel", 0)
         plain, _ = e.run(srcs)
     assert np.array_equal(default, plain)
+
+
+@pytest.mark.parametrize("case", ["rmat13", "rmat12_batches", "tree", "grid"])
+def test_child_driven_backward_levels(case):
+    """Direction switch of the dependency sweep (csrc/bc_bwd_push.cuh): past the peak level the
+    children add their coef into their parents (atomic adds) instead of every parent scanning all
+    its arcs (backward.py:95-103).  Same BC as the parent-driven sweep to rounding, same as the
+    oracle within the 1e-9 of the specification; delta per source through the inspection path."""
+    if case == "rmat13":
+        g = G.rmat(13, 16, 5)
+        srcs = np.nonzero(np.diff(g.offsets) > 0)[0][::7][:512].tolist()
+        groups = 0
+    elif case == "rmat12_batches":
+        g = G.rmat(12, 8, 1)
+        srcs = list(range(0, 4096, 3))
+        groups = 4                              # several batches, the last one partial
+    elif case == "tree":
+        # a broom: long handle, then a wide fan -- levels shrink and grow by large factors
+        edges = [(i, i + 1) for i in range(40)] + [(40, 41 + i) for i in range(600)]
+        edges += [(41 + i, 641 + (i % 7)) for i in range(600)]
+        g = P.from_edges(660, edges)
+        srcs = list(range(0, 660, 5))
+        groups = 0
+    else:
+        g = G.grid(24, 31)
+        srcs = list(range(0, g.num_vertices, 3))
+        groups = 0
+    out = {}
+    for beta in (0, 1, 4, 16):
+        with Engine(g) as e:
+            if groups:
+                e.set_option("groups", groups)
+            e.set_option("bwd_push", beta)
+            out[beta] = e.run(srcs)
+    obc, info = O.brandes_bc(g, srcs)
+    for beta in (0, 1, 4, 16):
+        bc, st = out[beta]
+        assert np.allclose(bc, obc, rtol=RTOL, atol=ATOL), beta
+        assert np.allclose(bc, out[0][0], rtol=1e-12, atol=1e-9), beta
+        for key in ("reached", "arcs_reached", "dag_arcs", "max_levels"):
+            assert st[key] == out[0][1][key], (beta, key)
+    if case.startswith("rmat"):
+        # the switch did fire on the small-world graphs: three launches per child-driven level
+        assert out[1][1]["launches"] != out[0][1]["launches"]
