@@ -129,6 +129,10 @@ int bc_set_weights(bc_handle *h, const int32_t *weights);
  * "sssp": weighted graphs, 1 = general-weight sweeps (csrc/bc_sssp.cuh), 0 = one level
  * per distance value (weights up to 4096), -1 (default) = by weight range;
  * "sssp_delta": step of the near-far distance bound there (0 = 16 mean arc weights);
+ * "bwd_push": direction switch of the dependency sweep (csrc/bc_bwd_push.cuh): a backward level
+ * is driven by its children (atomic adds into the parents' sums) when the children's arcs
+ * times this factor do not exceed the parents' arcs; default 16, 0 = every level parent-driven
+ * (sums in CSR arc order: BC reproducible bit for bit from run to run);
  * "push_beta", "push_beta_late", "reorder": see csrc/bc_engine.cu). */
 int bc_set_option(bc_handle *h, const char *key, int64_t value);
 

@@ -4,16 +4,23 @@
 // in some lane scans ALL its arcs for children at level L + 1 (backward.py:95-103, vertex pull).
 // Past the peak of a small-world graph that is the wrong side to drive from: on R-MAT scale 20 the
 // vertices at level 3 hold 99.5 % of the arcs while their children at level 4 hold 10 %, and one
-// level further down 10 % against 0.04 %.  There the children walk their arcs instead:
-//   1. bwd_push_zero_kernel      coef[v][lane] = 0 for the (vertex, lane) pairs of level L;
-//   2. bwd_push_kernel           every (w, lane) at level L + 1 adds coef[w][lane] into
-//                                coef[v][lane] of its parents v at level L (red.global.add.f64;
-//                                the arcs of 32 consecutive vertices are dealt out one per thread);
-//   3. bwd_push_finalize_kernel  delta = sigma * sum, coef = (1 + delta) / sigma, BC partial --
-//                                finalize_backward's arithmetic with the sum read from coef.
-// A (vertex, lane) pair sits at exactly one level, so the sums of step 2 never alias the values
-// they read.  Sums arrive in atomic order: results agree with the parent-driven kernel to rounding
-// (1e-16 relative per add), not bit for bit; option "bwd_push" 0 keeps every level parent-driven.
+// level further down 10 % against 0.04 %.  There the children walk their arcs instead.  With
+// S = sum of coef over the children, coef[v] = (1 + sigma S) / sigma = 1 / sigma + S, so:
+//   1. bwd_child_init_kernel     every (vertex, lane) pair of level L as if it had no children:
+//                                coef = 1 / sigma, sigma cleared (its last read, as in
+//                                finalize_backward) -- the freed sigma slot is the accumulator;
+//   2. bwd_push_kernel           every (w, lane) at level L + 1 adds coef[w][lane] into the sigma
+//                                slot of its parents at level L (red.global.add.f64; the arcs of
+//                                32 consecutive vertices are dealt out one per thread) and ORs
+//                                the lanes it served into the parent's word of a `recv` mask array
+//                                (a list of served pairs was tried first: its counters serialise,
+//                                0.13 -> 1.15 ms for the push of R-MAT scale 20's level 4);
+//   3. bwd_child_apply_kernel    sweeps `recv`; the served pairs only: coef += S,
+//                                delta = S / (1 / sigma) into the BC partial, slot and word back to zero.
+// Pairs without children (most of a tail level) cost what the parent-driven kernel moves for them
+// and nothing else.  A (vertex, lane) pair sits at exactly one level, so the sums never alias the
+// values they read.  Sums arrive in atomic order: results agree with the parent-driven kernel to
+// rounding, not bit for bit; option "bwd_push" 0 keeps every level parent-driven.
 #pragma once
 
 #include "bc_kernels.cuh"
@@ -29,13 +36,22 @@ constexpr int kBwdPushWarps = kBwdPushThreads / 32;
 constexpr int kBwdPushHeavyDegree = 256;
 constexpr int kBwdPushSliceArcs = 4096;
 
-// One child arc: w (lanes `mw` at level L + 1) -> x.  Adds coef[w][b] into coef[x][b] for the
-// lanes b where x sits at level L.
+// One child arc: w (lanes `mw` at level L + 1) -> x.  Adds coef[w][b] into the accumulator (the
+// cleared sigma slot) of x for the lanes b where x sits at level L and marks them in recv[x].
+struct BwdPushLists {
+    uint4 *heavy;                  // [group][heavy_cap] (vertex, lane mask, slice of its arcs)
+    unsigned *heavy_count;         // [group]
+    long long heavy_cap;
+    uint32_t *recv;                // [group][n] lanes of each parent that were handed a sum; zero between levels
+};
+
 __device__ __forceinline__ void bwd_push_arc(int64_t w, uint32_t mw, int64_t x, const uint32_t *gc,
-                                             double *gcoef) {
+                                             double *gs, const double *gcoef, uint32_t *grecv) {
     uint32_t p = gc[x] & mw;
+    if (p == 0) return;
+    atomicOr(grecv + x, p);
     const double *src = gcoef + (size_t)w * 32;
-    double *dst = gcoef + (size_t)x * 32;
+    double *dst = gs + (size_t)x * 32;
     while (p) {
         const int b = __ffs(p) - 1;
         p &= p - 1;
@@ -44,12 +60,14 @@ __device__ __forceinline__ void bwd_push_arc(int64_t w, uint32_t mw, int64_t x, 
 }
 
 // grid = (blocks, groups); a warp takes chunks of 32 consecutive vertices, grid-stride.
-__global__ void __launch_bounds__(kBwdPushThreads) bwd_push_zero_kernel(const uint32_t *__restrict__ cur, int64_t n,
-                                                                 double *coef, const uint32_t *__restrict__ live) {
+__global__ void __launch_bounds__(kBwdPushThreads) bwd_child_init_kernel(const uint32_t *__restrict__ cur, int64_t n,
+                                                                  double *sigma, double *coef,
+                                                                  const uint32_t *__restrict__ live) {
     const size_t g = blockIdx.y;
     if (live[g] == 0) return;
     const int lane = threadIdx.x & 31;
     const uint32_t *gc = cur + g * n;
+    double *gs = sigma + g * n * 32;
     double *gcoef = coef + g * n * 32;
     const int64_t chunks = (n + 31) / 32;
     for (int64_t ch = (int64_t)blockIdx.x * kBwdPushWarps + (threadIdx.x >> 5); ch < chunks;
@@ -58,10 +76,27 @@ __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_zero_kernel(const ui
         const uint32_t m = (v0 + lane < n) ? gc[v0 + lane] : 0u;
         unsigned any = __ballot_sync(kFull, m != 0);
         while (any) {
-            const int i = __ffs(any) - 1;
-            any &= any - 1;
-            const uint32_t mi = __shfl_sync(kFull, m, i);
-            if ((mi >> lane) & 1u) gcoef[(size_t)(v0 + i) * 32 + lane] = 0.0;
+            // four vertices per round: all loads issued before the first dependent store
+            size_t o[4];
+            bool on[4];
+            double sv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = any ? __ffs(any) - 1 : 0;
+                const bool have = any != 0;
+                any &= any - 1;
+                const uint32_t mk = __shfl_sync(kFull, m, i);
+                on[k] = have && ((mk >> lane) & 1u);
+                o[k] = (size_t)(v0 + i) * 32 + lane;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sv[k] = on[k] ? gs[o[k]] : 1.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (on[k]) {
+                    gcoef[o[k]] = 1.0 / sv[k];
+                    clear_after_use(gs + o[k], sv[k]);
+                }
         }
     }
 }
@@ -70,16 +105,18 @@ __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_zero_kernel(const ui
 __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_kernel(const int64_t *__restrict__ off,
                                                             const int32_t *__restrict__ col, int64_t n,
                                                             const uint32_t *__restrict__ nbr,
-                                                            const uint32_t *__restrict__ cur, double *coef,
+                                                            const uint32_t *__restrict__ cur, double *sigma,
+                                                            const double *coef,
                                                             const uint32_t *__restrict__ live_child,
-                                                            uint4 *heavy_list, unsigned *heavy_count,
-                                                            int64_t heavy_cap) {
+                                                            const BwdPushLists l) {
     const size_t g = blockIdx.y;
     if (live_child[g] == 0) return;
     const int lane = threadIdx.x & 31;
     const uint32_t *gn = nbr + g * n;
     const uint32_t *gc = cur + g * n;
-    double *gcoef = coef + g * n * 32;
+    double *gs = sigma + g * n * 32;
+    const double *gcoef = coef + g * n * 32;
+    uint32_t *grecv = l.recv + g * n;
     const int64_t chunks = (n + 31) / 32;
     for (int64_t ch = (int64_t)blockIdx.x * kBwdPushWarps + (threadIdx.x >> 5); ch < chunks;
          ch += (int64_t)gridDim.x * kBwdPushWarps) {
@@ -94,9 +131,9 @@ __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_kernel(const int64_t
             const long long d = off[w + 1] - a0;
             if (d > kBwdPushHeavyDegree) {
                 const unsigned ns = (unsigned)((d + kBwdPushSliceArcs - 1) / kBwdPushSliceArcs);
-                const unsigned slot = atomicAdd(heavy_count + g, ns);
-                for (unsigned k = 0; k < ns && (int64_t)(slot + k) < heavy_cap; ++k)
-                    heavy_list[g * heavy_cap + slot + k] = make_uint4((unsigned)w, m, k, 0u);
+                const unsigned slot = atomicAdd(l.heavy_count + g, ns);
+                for (unsigned k = 0; k < ns && (long long)(slot + k) < l.heavy_cap; ++k)
+                    l.heavy[g * l.heavy_cap + slot + k] = make_uint4((unsigned)w, m, k, 0u);
             } else {
                 deg = (int)d;
             }
@@ -122,7 +159,7 @@ __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_kernel(const int64_t
             const uint32_t mo = __shfl_sync(kFull, m, ow);
             const long long ao = __shfl_sync(kFull, a0, ow);
             const int eo = __shfl_sync(kFull, excl, ow);
-            if (j < total) bwd_push_arc(v0 + ow, mo, col[ao + (j - eo)], gc, gcoef);
+            if (j < total) bwd_push_arc(v0 + ow, mo, col[ao + (j - eo)], gc, gs, gcoef, grecv);
         }
     }
 }
@@ -130,33 +167,32 @@ __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_kernel(const int64_t
 // The listed slices of heavy children of group blockIdx.y: one block per record, grid-stride.
 __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_heavy_kernel(const int64_t *__restrict__ off,
                                                                   const int32_t *__restrict__ col, int64_t n,
-                                                                  const uint32_t *__restrict__ cur, double *coef,
-                                                                  const uint4 *__restrict__ heavy_list,
-                                                                  const unsigned *__restrict__ heavy_count,
-                                                                  int64_t heavy_cap) {
+                                                                  const uint32_t *__restrict__ cur, double *sigma,
+                                                                  const double *coef, const BwdPushLists l) {
     const size_t g = blockIdx.y;
-    const unsigned cnt = (unsigned)min((long long)heavy_count[g], (long long)heavy_cap);
+    const unsigned cnt = (unsigned)min((long long)l.heavy_count[g], l.heavy_cap);
     const uint32_t *gc = cur + g * n;
-    double *gcoef = coef + g * n * 32;
+    double *gs = sigma + g * n * 32;
+    const double *gcoef = coef + g * n * 32;
+    uint32_t *grecv = l.recv + g * n;
     for (unsigned e = blockIdx.x; e < cnt; e += gridDim.x) {
-        const uint4 rec = heavy_list[g * heavy_cap + e];
+        const uint4 rec = l.heavy[g * l.heavy_cap + e];
         const int64_t w = rec.x;
         const long long a0 = off[w] + (long long)rec.z * kBwdPushSliceArcs;
         const long long a1 = min((long long)off[w + 1], a0 + kBwdPushSliceArcs);
         for (long long a = a0 + threadIdx.x; a < a1; a += kBwdPushThreads)
-            bwd_push_arc(w, rec.y, col[a], gc, gcoef);
+            bwd_push_arc(w, rec.y, col[a], gc, gs, gcoef, grecv);
     }
 }
 
-// accumulate: finalize_backward's bits (0: add delta into the BC partials, 1: clear sigma).
-__global__ void __launch_bounds__(kBwdPushThreads) bwd_push_finalize_kernel(const uint32_t *__restrict__ cur, int64_t n,
-                                                                     double *sigma, double *coef, double *bcg,
-                                                                     const uint32_t *__restrict__ live,
-                                                                     int accumulate) {
+// Sweeps recv[group][*]: for the served pairs S sits in the sigma slot, 1 / sigma in coef.
+__global__ void __launch_bounds__(kBwdPushThreads) bwd_child_apply_kernel(int64_t n, double *sigma, double *coef,
+                                                                   double *bcg, uint32_t *recv,
+                                                                   const uint32_t *__restrict__ live) {
     const size_t g = blockIdx.y;
     if (live[g] == 0) return;
     const int lane = threadIdx.x & 31;
-    const uint32_t *gc = cur + g * n;
+    uint32_t *gr = recv + g * n;
     double *gs = sigma + g * n * 32;
     double *gcoef = coef + g * n * 32;
     double *gb = bcg + g * n;
@@ -164,51 +200,24 @@ __global__ void __launch_bounds__(kBwdPushThreads) bwd_push_finalize_kernel(cons
     for (int64_t ch = (int64_t)blockIdx.x * kBwdPushWarps + (threadIdx.x >> 5); ch < chunks;
          ch += (int64_t)gridDim.x * kBwdPushWarps) {
         const int64_t v0 = ch * 32;
-        const uint32_t m = (v0 + lane < n) ? gc[v0 + lane] : 0u;
+        const uint32_t m = (v0 + lane < n) ? gr[v0 + lane] : 0u;
         unsigned any = __ballot_sync(kFull, m != 0);
+        if (m != 0) gr[v0 + lane] = 0u;
         while (any) {
-            // four vertices per round: all loads issued before the first dependent store
-            int idx[4];
-            bool on[4];
-            double sv[4], ac[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                idx[k] = any ? __ffs(any) - 1 : 0;
-                const bool have = any != 0;
-                any &= any - 1;
-                const uint32_t mk = __shfl_sync(kFull, m, idx[k]);
-                on[k] = have && ((mk >> lane) & 1u);
+            const int i = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t mi = __shfl_sync(kFull, m, i);
+            double contrib = 0.0;
+            if ((mi >> lane) & 1u) {
+                const size_t o = (size_t)(v0 + i) * 32 + lane;
+                const double S = gs[o];
+                const double c0 = gcoef[o];
+                gcoef[o] = c0 + S;
+                contrib = S / c0;   // delta = sigma * S
+                clear_after_use(gs + o, S);
             }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                sv[k] = 1.0;
-                ac[k] = 0.0;
-                if (on[k]) {
-                    const size_t o = (size_t)(v0 + idx[k]) * 32 + lane;
-                    sv[k] = gs[o];
-                    ac[k] = gcoef[o];
-                }
-            }
-            double contrib[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                contrib[k] = 0.0;
-                if (on[k]) {
-                    const size_t o = (size_t)(v0 + idx[k]) * 32 + lane;
-                    const double d = sv[k] * ac[k];
-                    gcoef[o] = (1.0 + d) / sv[k];
-                    contrib[k] = d;
-                    if (accumulate & 2) clear_after_use(gs + o, sv[k]);
-                }
-            }
-            if (accumulate & 1) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const double s = warp_sum(contrib[k]);
-                    // idx[k] repeats 0 only for exhausted slots, whose sum is zero
-                    if (lane == 0 && s != 0.0) gb[v0 + idx[k]] += s;
-                }
-            }
+            const double sum = warp_sum(contrib);
+            if (lane == 0) gb[v0 + i] += sum;
         }
     }
 }

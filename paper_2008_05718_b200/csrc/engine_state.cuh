@@ -268,7 +268,8 @@ struct bc_handle {
     // child-driven backward levels (bc_bwd_push.cuh): children above kBwdPushHeavyDegree arcs are
     // listed per group and walked by the whole grid
     uint4 *bp_list = nullptr;   // [alloc_groups][bp_cap] (vertex, lane mask, slice of its arcs)
-    unsigned *bp_count = nullptr;   // [alloc_groups]
+    unsigned *bp_count = nullptr;   // [alloc_groups] heavy records
+    uint32_t *bp_recv = nullptr;    // [alloc_groups][n] lanes of each parent that were handed a sum; zero between levels
     int64_t bp_cap = -1;        // slices of all vertices of the graph above that degree (-1: not counted yet)
     uint8_t *cand = nullptr;    // [alloc_groups][n] candidate flags of the dense forward sweeps (deep graphs)
     bool use_cand = false;      // set by forward_sweep for the launches of its levels
@@ -511,8 +512,8 @@ void free_state(bc_handle *h) {
     arena_free(h->heavy);
     arena_free(h->cand);
     h->cand = nullptr;
-    arena_free(h->bp_list), arena_free(h->bp_count);
-    h->bp_list = nullptr, h->bp_count = nullptr;
+    arena_free(h->bp_list), arena_free(h->bp_count), arena_free(h->bp_recv);
+    h->bp_list = nullptr, h->bp_count = nullptr, h->bp_recv = nullptr;
     h->heavy = nullptr;
     h->heavy_cap = 0;
     h->deep_log = nullptr;

@@ -861,8 +861,8 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
         };
         // direction switch of the dependency sweep (bc_bwd_push.cuh): past the peak the children
         // at L + 1 hold far fewer arcs than their parents at L, so they walk theirs
-        const bool child_driven = r.slot >= 0 && !deepest && !debug && h->bwd_push > 0 && c.wgt == nullptr &&
-                                  reps[L + 1].farcs * (unsigned long long)h->bwd_push <= r.farcs;
+        bool child_driven = r.slot >= 0 && !deepest && !debug && h->bwd_push > 0 && c.wgt == nullptr &&
+                            reps[L + 1].farcs * (unsigned long long)h->bwd_push <= r.farcs;
         if (child_driven) {
             const LevelRep &below = reps[L + 1];
             const uint32_t *live_cur = h->live + (size_t)L * G;
@@ -870,7 +870,7 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
             uint32_t *cur = h->lvl[r.slot];
             const dim3 sweep_grid(std::min<unsigned>(grid1d((size_t)(h->n + 31) / 32 * 32, kBwdPushThreads), 148 * 16), ng);
             const dim3 push_grid(std::min<unsigned>(grid1d((size_t)(h->n + 31) / 32 * 32, kBwdPushThreads), 148 * 64), ng);
-            if (h->bp_cap < 0) {   // vertices a warp does not deal out itself
+            if (h->bp_cap < 0) {   // slices of the vertices a warp does not deal out itself
                 int64_t heavy = 0;
                 for (int64_t v = 0; v < h->n; ++v) {
                     const int64_t d = h->h_off[v + 1] - h->h_off[v];
@@ -879,33 +879,42 @@ int backward_adaptive(bc_handle *h, const Csr &c, int depth, std::vector<LevelRe
                 h->bp_cap = heavy;
             }
             const bool any_heavy = h->bp_cap > 0 && below.maxdeg > (unsigned long long)kBwdPushHeavyDegree;
-            if (h->bp_cap > 0 && h->bp_list == nullptr) {
+            if (h->bp_cap > 0 && h->bp_list == nullptr)
                 CUDA_TRY(h, arena_malloc((void **)&h->bp_list, G * (size_t)h->bp_cap * sizeof(uint4)));
-                CUDA_TRY(h, arena_malloc((void **)&h->bp_count, G * sizeof(unsigned)));
+            if (h->bp_count == nullptr) CUDA_TRY(h, arena_malloc((void **)&h->bp_count, G * sizeof(unsigned)));
+            if (h->bp_recv == nullptr) {   // zero between levels: the apply pass clears what it reads
+                CUDA_TRY(h, arena_malloc((void **)&h->bp_recv, G * (size_t)h->n * sizeof(uint32_t)));
+                CUDA_TRY(h, cudaMemsetAsync(h->bp_recv, 0, G * (size_t)h->n * sizeof(uint32_t), st));
             }
-            if (h->bp_cap > 0) CUDA_TRY(h, cudaMemsetAsync(h->bp_count, 0, G * sizeof(unsigned), st));
+            BwdPushLists lists{};
+            lists.heavy = h->bp_list;
+            lists.heavy_count = h->bp_count;
+            lists.heavy_cap = h->bp_cap;
+            lists.recv = h->bp_recv;
+            CUDA_TRY(h, cudaMemsetAsync(h->bp_count, 0, G * sizeof(unsigned), st));
             LevelTimer timer(h, st);
-            bwd_push_zero_kernel<<<sweep_grid, kBwdPushThreads, 0, st>>>(cur, h->n, h->coef, live_cur);
-            bwd_push_kernel<<<push_grid, kBwdPushThreads, 0, st>>>(c.off, c.col, h->n, nbr, cur, h->coef, live_child,
-                                                                  h->bp_list, h->bp_count, h->bp_cap);
+            bwd_child_init_kernel<<<sweep_grid, kBwdPushThreads, 0, st>>>(cur, h->n, h->sigma, h->coef, live_cur);
+            bwd_push_kernel<<<push_grid, kBwdPushThreads, 0, st>>>(c.off, c.col, h->n, nbr, cur, h->sigma, h->coef,
+                                                                  live_child, lists);
             if (any_heavy) {
                 bwd_push_heavy_kernel<<<dim3((unsigned)std::min<int64_t>(h->bp_cap, 148 * 8), ng), kBwdPushThreads, 0, st>>>(
-                    c.off, c.col, h->n, cur, h->coef, h->bp_list, h->bp_count, h->bp_cap);
+                    c.off, c.col, h->n, cur, h->sigma, h->coef, lists);
                 ++h->launches;
             }
-            bwd_push_finalize_kernel<<<sweep_grid, kBwdPushThreads, 0, st>>>(
-                cur, h->n, h->sigma, h->coef, h->bcg, live_cur, 1 | (h->lazy_clear ? 2 : 0));
+            bwd_child_apply_kernel<<<sweep_grid, kBwdPushThreads, 0, st>>>(h->n, h->sigma, h->coef, h->bcg, h->bp_recv,
+                                                                          live_cur);
             timer.stop();
             h->launches += 3;
             ++h->level_launches;
             ++h->bwd_push_levels;
             CUDA_TRY(h, cudaGetLastError());
             // byte model: the children's arcs scanned, coef read + added per (DAG arc, lane), the
-            // parents' pairs zeroed, summed, finalised; three sweeps over the level masks
+            // parents' pairs initialised (sigma read + cleared, coef written) and the listed ones
+            // updated; two sweeps over the level masks plus the probes' share
             h->model_scan += (int64_t)below.farcs;
             if (below.pairs >= 0) h->model_pairs += 2 * below.pairs;
-            if (r.vlanes >= 0) h->model_vlanes += (h->lazy_clear ? 5 : 4) * r.vlanes;
-            h->model_dense_words += 4 * h->n * ng;
+            if (r.vlanes >= 0) h->model_vlanes += 3 * r.vlanes;
+            h->model_dense_words += 3 * h->n * ng;
             h->model_entries += (int64_t)r.nverts;
         } else if (r.slot >= 0) {
             model_backward();

@@ -68,12 +68,25 @@ if os.path.exists(rep) or os.path.exists(rawcsv):
     def to_bytes(val, unit):
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
         return float(val) * mult
-    lev = [r for r in rr[2:] if "level_kernel<" in r[idx[0]] and "advance" not in r[idx[0]]]
+    lev = [r for r in rr[2:] if ("level_kernel<" in r[idx[0]] and "advance" not in r[idx[0]]) or "bwd_push" in r[idx[0]] or "bwd_child" in r[idx[0]]]
+    # exactly one pass: cut where the forward kernel comes back after the backward sweep
+    one, seen_bwd = [], False
+    for r in lev:
+        fwd = "level_kernel<0" in r[idx[0]] or "level_kernel<(bool)0" in r[idx[0]]
+        if fwd and seen_bwd:
+            break
+        seen_bwd |= not fwd
+        one.append(r)
+    lev = one
     per = [to_bytes(r[idx[2]], units[idx[2]]) + to_bytes(r[idx[3]], units[idx[3]]) for r in lev]
-    rec = {"rmat20": sum(per) / len(per) if per else None,
-           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the %d level_kernel launches "
-                   "(forward and backward) = whole passes of 8 launches each (identical work), captured with ncu --set full from "
-                   "bench.py --steps 1 --warmup 0 --no-cpu --no-extra" % len(per),
+    # a child-driven backward level (bwd_child_init / bwd_push / bwd_child_apply) counts as ONE level launch, as in the
+    # engine's launches_level_timed
+    n_levels = sum(1 for r in lev if "level_kernel<" in r[idx[0]] or "bwd_child_apply" in r[idx[0]])
+    rec = {"rmat20": sum(per) / n_levels if n_levels else None,
+           "note": "dram__bytes_read.sum + dram__bytes_write.sum per level launch: sum over the %d captured kernels of one "
+                   "step (level_kernel forward and backward + the bwd_push kernels of the child-driven level) / %d level launches, "
+                   "captured with ncu --set full from bench.py --steps 1 --warmup 0 --no-cpu --no-extra --relabel 1"
+                   % (len(per), n_levels),
            "per_launch_bytes": per,
            "per_launch_ms": [float(r[idx[1]]) * {"ms": 1.0, "us": 1e-3, "s": 1e3, "ns": 1e-6}.get(units[idx[1]], 1.0)
                              for r in lev],
