@@ -658,7 +658,7 @@ def run_ours(args):
     achieved = model_per_launch / max(lvl_avg, 1e-9) / 1e6
     fwd_b, bwd_b, init_b = per_source_bytes(st, n)
     roofline = {
-        "bound": "hbm", "kernel": "level_kernel<forward | backward> + hub_kernel (dense pull levels)",
+        "bound": "hbm", "kernel": "level_kernel<forward | backward> + hub_kernel (dense pull levels; the child-driven tail levels of the backward sweep, bwd_child_init / bwd_push / bwd_child_apply, count as one level launch each)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
         "model": "batched byte model (DESIGN.md section 5): per launch, 8 B per arc scanned per group (col_idx word + "
