@@ -772,6 +772,11 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     if args.gpus > 1 and "RANK" not in os.environ:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:     # one rank per GPU: never several ranks on one device
+            print("bench.py: --gpus %d but %d CUDA device(s) visible" % (args.gpus, have), file=sys.stderr)
+            return 2
         return relaunch_under_torchrun(args)
     if args.gpu_mode == "graph-partitioned":
         return run_partitioned(args)
